@@ -1,0 +1,123 @@
+/*
+ * stanza_b200.h -- C ABI of the B200-native Stanza layer-separated step.
+ *
+ * The reference (stanza-sim 0.1.0, /root/reference/pkg/src/stanza) has no C
+ * ABI: its per-layer operator contract is the Python pair
+ *     forward(layer, params, x, labels=None) -> (y, cache)
+ *     backward(layer, params, cache, gy)    -> (gx, [gW, gb])   (sums)
+ * in tensor_core.py:153-301, plus sgd_step (tensor_core.py:366-388).  Each
+ * entry point below replaces one layer kind / phase of that contract and is
+ * what a reference-side FFI (ctypes) would bind.
+ *
+ * Conventions
+ *   - all tensors are fp32 (labels int32), row-major, device pointers owned
+ *     by the caller; layouts are the reference's: activations NCHW, conv W
+ *     [O,C,k,k], FC W [in,out] (tensor_core.py:81-88);
+ *   - ws / ws_bytes: optional caller workspace for split-K partials (pass
+ *     NULL, 0 to disable split-K);
+ *   - stream: a cudaStream_t passed as void*;
+ *   - returns 0 on success, 1 invalid argument (the reference raises
+ *     ShapeMismatch, tensor_core.py:25-26), 2 CUDA launch error,
+ *     3 workspace too small; stz_last_error() describes the failure.
+ *   - gradients are batch SUMS, as in the reference; the only division by
+ *     the global batch is the inv_n argument of stz_sgd_momentum.
+ */
+#ifndef STANZA_B200_H
+#define STANZA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ABI version (1) and the last error message of the calling thread. */
+int stz_abi_version(void);
+const char* stz_last_error(void);
+
+/* GEMM core: 0 = tcgen05 BF16x6 split (default, product), 1 = SIMT fp32
+ * (validation kernel the GPU tests cross-check against), 2 = tcgen05
+ * TF32x3 split (kept for the precision study; ~20-bit tf32 product sums). */
+int stz_set_gemm_impl(int impl);
+int stz_get_gemm_impl(void);
+
+/* Tuning/experiment knob: cap the K extent one CTA accumulates (0 = auto). */
+int stz_set_max_k_per_split(int k);
+
+/* Conv2d forward, replaces tensor_core.py:161-181 (+ReLU :213-214 when
+ * relu != 0).  x [N,C,H,W], w [O,C,k,k], b [O] -> y [N,O,OH,OW]. */
+int stz_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int N, int C, int H,
+                   int W, int O, int k, int s, int p, int relu, void* ws, size_t ws_bytes,
+                   void* stream);
+
+/* Conv2d input gradient, replaces tensor_core.py:257-258,:260.
+ * gy [N,O,OH,OW], w -> gx [N,C,H,W]; mask (nullable) = output of the ReLU
+ * feeding this conv: gx is zeroed where mask <= 0 (tensor_core.py:291-293). */
+int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int N,
+                        int C, int H, int W, int O, int k, int s, int p, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* Conv2d weight/bias gradient sums, replaces tensor_core.py:253-259.
+ * x [N,C,H,W], gy [N,O,OH,OW] -> gw [O,C,k,k], gb [O] (gb nullable). */
+int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb, int N, int C,
+                          int H, int W, int O, int k, int s, int p, void* ws, size_t ws_bytes,
+                          void* stream);
+
+/* FullyConnected forward y = x @ W + b (+ReLU), replaces tensor_core.py:205-211.
+ * x [M,in], W [in,out], b [out] -> y [M,out]. */
+int stz_fc_fwd(const float* x, const float* w, const float* b, float* y, int M, int in_dim,
+               int out_dim, int relu, void* ws, size_t ws_bytes, void* stream);
+
+/* FC input gradient gx = gy @ W^T, replaces tensor_core.py:286; optional
+ * ReLU mask as in stz_conv2d_bwd_data. */
+int stz_fc_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int M,
+                    int in_dim, int out_dim, void* ws, size_t ws_bytes, void* stream);
+
+/* FC weight/bias gradient sums gW = x^T @ gy, gb = colsum(gy), replaces
+ * tensor_core.py:287-288. */
+int stz_fc_bwd_weight(const float* x, const float* gy, float* gw, float* gb, int M, int in_dim,
+                      int out_dim, void* ws, size_t ws_bytes, void* stream);
+
+/* MaxPool2d forward with first-max argmax (uint8 index kh*k+kw), replaces
+ * tensor_core.py:183-198. */
+int stz_maxpool2d_fwd(const float* x, float* y, uint8_t* arg, int N, int C, int H, int W, int k,
+                      int s, void* stream);
+
+/* MaxPool2d backward (gather form, float64 sums), replaces
+ * tensor_core.py:263-276; optional ReLU mask on the pool input. */
+int stz_maxpool2d_bwd(const float* gy, const uint8_t* arg, float* gx, const float* mask, int N,
+                      int C, int H, int W, int k, int s, void* stream);
+
+/* Standalone ReLU, replaces tensor_core.py:213-214 / :291-293 (src is the
+ * ReLU input or output: both are > 0 at the same cells). */
+int stz_relu_fwd(const float* x, float* y, size_t n, void* stream);
+int stz_relu_bwd(const float* gy, const float* src, float* gx, size_t n, void* stream);
+
+/* SoftmaxCrossEntropy forward+backward in one pass (float64 inside),
+ * replaces tensor_core.py:216-228 and :295-299: per-sample losses [M] and
+ * the gradient of the loss SUM, p - onehot, [M,C]. */
+int stz_softmax_ce(const float* logits, const int* labels, float* losses, float* dlogits, int M,
+                   int C, void* stream);
+
+/* Deterministic float64 sum of n floats (the iteration loss sum,
+ * stanza_runtime.py:273); accumulate != 0 adds into *out instead of
+ * overwriting it (several FC workers' sums into one slot). */
+int stz_sum_f32(const float* x, size_t n, double* out, int accumulate, void* stream);
+
+/* Momentum SGD from gradient sums in the reference's exact fp32 op order,
+ * replaces tensor_core.py:366-388: v = v*mu + g*inv_n; w = w - lr*v.
+ * inv_n = float32(1)/float32(n_conv*K) computed by the caller. */
+int stz_sgd_momentum(float* w, float* v, const float* g, size_t n, float lr, float mu,
+                     float inv_n, void* stream);
+
+/* dst += src (fp32).  Sums FC-replica gradient vectors when several FC
+ * workers share one GPU -- the single-device stand-in for the FC-group
+ * allreduce (stanza_runtime.py:320-337); on >1 GPU NCCL does this. */
+int stz_vec_add(float* dst, const float* src, size_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STANZA_B200_H */

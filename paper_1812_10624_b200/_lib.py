@@ -1,0 +1,94 @@
+"""ctypes binding of the C ABI declared in include/stanza_b200.h.
+
+There is no CPU fallback: if the library is missing or a call fails, this
+module raises.  Device pointers come from torch tensors (PyTorch owns every
+buffer); the stream is torch's current CUDA stream unless given.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+from .build import LIB_PATH
+
+_HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "include", "stanza_b200.h")
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+Z = ctypes.c_size_t
+F = ctypes.c_float
+
+# name -> (restype, argtypes); must match include/stanza_b200.h
+SIGNATURES = {
+    "stz_abi_version": (I, []),
+    "stz_last_error": (ctypes.c_char_p, []),
+    "stz_set_gemm_impl": (I, [I]),
+    "stz_get_gemm_impl": (I, []),
+    "stz_set_max_k_per_split": (I, [I]),
+    "stz_conv2d_fwd": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stz_conv2d_bwd_data": (I, [P, P, P, P, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stz_conv2d_bwd_filter": (I, [P, P, P, P, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stz_fc_fwd": (I, [P, P, P, P, I, I, I, I, P, Z, P]),
+    "stz_fc_bwd_data": (I, [P, P, P, P, I, I, I, P, Z, P]),
+    "stz_fc_bwd_weight": (I, [P, P, P, P, I, I, I, P, Z, P]),
+    "stz_maxpool2d_fwd": (I, [P, P, P, I, I, I, I, I, I, P]),
+    "stz_maxpool2d_bwd": (I, [P, P, P, P, I, I, I, I, I, I, P]),
+    "stz_relu_fwd": (I, [P, P, Z, P]),
+    "stz_relu_bwd": (I, [P, P, P, Z, P]),
+    "stz_softmax_ce": (I, [P, P, P, P, I, I, P]),
+    "stz_sum_f32": (I, [P, Z, P, I, P]),
+    "stz_sgd_momentum": (I, [P, P, P, Z, F, F, F, P]),
+    "stz_vec_add": (I, [P, P, Z, P]),
+}
+
+
+class StanzaCudaError(RuntimeError):
+    """A C-ABI call returned a CUDA / launch failure."""
+
+
+class StanzaLibraryMissing(ImportError):
+    """libstz_b200.so is not built -- there is no fallback path."""
+
+
+def header_symbols(path: str = _HEADER) -> list[str]:
+    """Every function the public header declares."""
+    with open(path, "r", encoding="utf-8") as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(stz_[a-z0-9_]+)\s*\(", text)))
+
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load (once) and type the library.  Raises StanzaLibraryMissing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or os.environ.get("STZ_LIB", LIB_PATH)
+    if not os.path.exists(path):
+        raise StanzaLibraryMissing(
+            f"{path} not found; build it with `python -m paper_1812_10624_b200.build` "
+            "(the CUDA path is the only path)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an ABI function and raise on a non-zero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.stz_last_error().decode(errors="replace")
+        if rc == 1:
+            from .tensor_core import ShapeMismatch
+            raise ShapeMismatch(f"{name}: {msg}")
+        raise StanzaCudaError(f"{name} failed ({rc}): {msg}")

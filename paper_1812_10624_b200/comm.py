@@ -1,0 +1,98 @@
+"""Role communicator: one process per GPU, CONV and FC groups over NCCL.
+
+Replaces the reference's simulated network for the three per-iteration
+exchanges of the layer-separated step (stanza_runtime.py:228-338):
+
+* activations: many-to-one, CONV i -> FC conv_to_fc[i]; the FC worker
+  receives each member's [K, A] block straight into rows [pos*K, (pos+1)*K)
+  of its input buffer (zero-copy concat, :64-85, :266-267), labels likewise;
+* boundary gradients: one-to-many, the mirror image (:278-307, :274-275);
+* gradient exchange: allreduce(sum) of the flat block-gradient vector on the
+  CONV sub-group and, iff n_fc > 1, on the FC sub-group (:309-338).  The two
+  groups are disjoint process sets, so their allreduces overlap naturally.
+
+All of it is expressed with torch.distributed point-to-point ops and
+sub-group collectives, so the same code runs over NCCL on B200s and over
+gloo on CPU tensors (the multi-process CPU tests).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .roles import plan_groups
+
+
+class RoleComm:
+    """Rank r < n_conv is CONV worker r; rank n_conv + j is FC worker j."""
+
+    def __init__(self, n_conv: int, n_fc: int, group=None):
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialized (one process per GPU)")
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world != n_conv + n_fc:
+            raise ValueError(f"world size {self.world} != n_conv + n_fc = {n_conv + n_fc}")
+        self.n_conv, self.n_fc = n_conv, n_fc
+        self.conv_to_fc = plan_groups(n_conv, n_fc)
+        self.conv_ranks = list(range(n_conv))
+        self.fc_ranks = list(range(n_conv, n_conv + n_fc))
+        # every rank must create every group, members or not
+        self.conv_group = dist.new_group(self.conv_ranks) if n_conv > 1 else None
+        self.fc_group = dist.new_group(self.fc_ranks) if n_fc > 1 else None
+        self.is_conv = self.rank < n_conv
+        self.index = self.rank if self.is_conv else self.rank - n_conv
+
+    # -- topology -------------------------------------------------------------------
+
+    def members(self, fc_index: int) -> list[int]:
+        """CONV indices served by FC worker fc_index, ascending (concat order)."""
+        return [i for i, j in enumerate(self.conv_to_fc) if j == fc_index]
+
+    def fc_rank_of(self, conv_index: int) -> int:
+        return self.n_conv + self.conv_to_fc[conv_index]
+
+    # -- exchanges --------------------------------------------------------------------
+
+    def gather_activations(self, acts: torch.Tensor | None, labels: torch.Tensor | None,
+                           fc_in: torch.Tensor | None, fc_labels: torch.Tensor | None,
+                           k: int) -> None:
+        """CONV side passes (acts [K,A], labels [K]); FC side passes its input
+        buffers ([g*K, A], [g*K]) and receives every member's block in place."""
+        ops = []
+        if self.is_conv:
+            dst = self.fc_rank_of(self.index)
+            ops += [dist.P2POp(dist.isend, acts, dst), dist.P2POp(dist.isend, labels, dst)]
+        else:
+            for pos, i in enumerate(self.members(self.index)):
+                rows = slice(pos * k, (pos + 1) * k)
+                ops += [dist.P2POp(dist.irecv, fc_in[rows], i),
+                        dist.P2POp(dist.irecv, fc_labels[rows], i)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def scatter_boundary(self, gx: torch.Tensor | None, gy: torch.Tensor | None,
+                         k: int) -> None:
+        """FC side sends rows [pos*K, (pos+1)*K) of gx to member pos; the CONV
+        side receives its [K, A] boundary gradient into gy."""
+        ops = []
+        if self.is_conv:
+            ops.append(dist.P2POp(dist.irecv, gy, self.fc_rank_of(self.index)))
+        else:
+            for pos, i in enumerate(self.members(self.index)):
+                ops.append(dist.P2POp(dist.isend, gx[pos * k:(pos + 1) * k], i))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def allreduce_grads(self, flat: torch.Tensor) -> None:
+        """Sum the flat gradient vector over this rank's role group."""
+        group = self.conv_group if self.is_conv else self.fc_group
+        if group is not None:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+
+    def sum_scalar(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    def barrier(self) -> None:
+        dist.barrier()

@@ -1,0 +1,403 @@
+"""Layer-separated training on B200s -- drop-in for the reference runtime.
+
+``StanzaCluster(spec, *, n_conv, n_fc, batch_fn, lr, momentum=0.9, ...)``
+and ``.train(iterations) -> StanzaResult(losses, state, transport)`` keep the
+signature and semantics of /root/reference/pkg/src/stanza/stanza_runtime.py
+:96-375.  One BSP iteration (:352-375):
+
+  conv_compute  CONV trunk forward on each worker's batch (it, i)
+  activations   many-to-one gather of [K, A] activations + labels into the
+                FC worker's input rows, in ascending CONV index
+  fc_compute    FC head forward + SoftmaxCE + backward on the gathered batch
+  boundary      one-to-many scatter of each worker's [K, A] boundary grads
+  (conv bwd)    CONV trunk backward from the boundary gradient
+  exchange      allreduce(sum) of CONV grads over the CONV group and, iff
+                n_fc > 1, of FC grads over the FC group
+  update        momentum SGD with n = n_conv * K on every replica
+
+Two deployments:
+
+* single device (``comm=None``): every role on one GPU.  CONV replicas are
+  bit-identical by construction (reference test_stanza_runtime.py:70-83), so
+  the trunk runs once over the n_conv*K concatenated samples; each FC worker
+  runs its own head pass over its contiguous row slice (zero-copy gather and
+  scatter) and the FC replica gradients are summed on device.  With
+  n_conv = n_fc = 1 this is the co-located 1-GPU configuration.
+* one process per GPU (``comm=RoleComm``): rank i < n_conv is CONV worker
+  i, rank n_conv + j is FC worker j; the exchanges are NCCL point-to-point
+  ops and sub-group allreduces (comm.py).
+"""
+
+from __future__ import annotations
+
+import random
+from collections import Counter
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .checkpointing import TrainState, state_to_bytes
+from .engine import BlockEngine
+from .model_partition import ConfigError, ModelSpec, Partition, mlp_split, split
+from .roles import group_rows, plan_groups
+from .tensor_core import ShapeMismatch, seeded_init
+
+
+class MissingSource(TimeoutError):
+    """An expected upstream node never delivered its payload."""
+
+
+class Tag:
+    """Message classes of the per-iteration contract (reference transport.Tag)."""
+    ACTIVATIONS = "activations"
+    CONTROL = "control"
+    BOUNDARY_GRADS = "boundary_grads"
+    ALLREDUCE_CHUNK = "allreduce_chunk"
+    CHECKPOINT = "checkpoint"
+
+
+@dataclass
+class PhaseRecord:
+    label: str
+    payload_bytes: int = 0
+    elapsed_ms: float | None = None
+
+
+@dataclass
+class PhaseLedger:
+    """Device-side stand-in for the reference's TrafficLedger: the phase
+    sequence of every iteration, payload bytes per message class (what the
+    reference's ledger tests pin, test_stanza_runtime.py:158-179) and, when
+    phase timing is on, CUDA-event milliseconds per phase."""
+    phases: list = field(default_factory=list)
+    tag_payload_bytes: Counter = field(default_factory=Counter)
+    tag_messages: Counter = field(default_factory=Counter)
+
+    def record(self, label: str, nbytes: int = 0) -> PhaseRecord:
+        rec = PhaseRecord(label, nbytes)
+        self.phases.append(rec)
+        return rec
+
+
+@dataclass
+class StanzaResult:
+    losses: list
+    state: TrainState | None
+    transport: PhaseLedger
+
+
+PHASES = ("conv_compute", "activations", "fc_compute", "boundary", "exchange", "update")
+
+
+class StanzaCluster:
+    """A layer-separated deployment on B200 GPUs.
+
+    batch_fn(iteration, conv_index) -> (inputs [K, ...] float32, labels [K])
+    exactly as in the reference; iteration indices are absolute so resumed
+    runs replay the same data.  ``device`` selects the GPU (single-device
+    mode); ``comm`` switches to one-process-per-GPU mode.
+    """
+
+    def __init__(self, spec: ModelSpec, *, n_conv: int, n_fc: int, batch_fn, lr: float,
+                 momentum: float = 0.9, conv_time: float = 0.0, fc_unit_time: float = 0.0,
+                 net=None, seed: int = 0, boundary: int | None = None,
+                 state: TrainState | None = None, device=None, comm=None,
+                 time_phases: bool = False):
+        if lr <= 0.0:
+            raise ConfigError(f"learning rate must be positive, got {lr}")
+        if not 0.0 <= momentum < 1.0:
+            raise ValueError(f"momentum must be in [0, 1), got {momentum}")
+        self.spec = spec
+        self.layers = spec.require_layers()
+        self.partition: Partition = (mlp_split(spec, boundary) if boundary is not None
+                                     else split(spec))
+        self.batch_fn = batch_fn
+        self.lr, self.momentum = float(lr), float(momentum)
+        self.conv_time, self.fc_unit_time = float(conv_time), float(fc_unit_time)
+        self.seed = seed
+        self.n_conv, self.n_fc = n_conv, n_fc
+        self.conv_to_fc = plan_groups(n_conv, n_fc)
+        self.max_group = max(self.conv_to_fc.count(j) for j in range(n_fc))
+        self.comm = comm
+        self.time_phases = time_phases
+        self.k = spec.batch_k
+        cut = self.partition.split_index
+
+        ref = seeded_init(self.layers, seed)
+        if state is None:
+            full0 = ref
+            vel0 = [[np.zeros_like(t) for t in layer] for layer in ref]
+            self.iteration = 0
+        else:
+            for what, nested in (("snapshot parameters", state.params),
+                                 ("snapshot velocities", state.velocities)):
+                flat_r = [t for layer in ref for t in layer]
+                flat_c = [t for layer in nested for t in layer]
+                if len(flat_r) != len(flat_c) or any(
+                        tuple(a.shape) != tuple(np.shape(b)) for a, b in zip(flat_r, flat_c)):
+                    raise ShapeMismatch(f"{what}: structure does not match the model")
+            full0, vel0 = state.params, state.velocities
+            self.iteration = state.iteration
+
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self.conv_ids = [("conv", i) for i in range(n_conv)]
+        self.fc_ids = [("fc", j) for j in range(n_fc)]
+        self.transport = PhaseLedger()
+        self.replica_snapshots: dict = {}
+
+        conv_block, fc_block = self.partition.conv_block, self.partition.fc_block
+        in_shape = tuple(spec.input_shape)
+        self.boundary_shape = tuple(self._shape_at(cut))
+        a = int(np.prod(self.boundary_shape))
+        self.boundary_activations = a
+        dev = self.device
+        k = self.k
+        self.conv = None
+        self.fcs: list[BlockEngine] = []
+
+        if comm is None:
+            nk = n_conv * k
+            self.x = torch.zeros((nk, *in_shape), dtype=torch.float32, device=dev)
+            self.labels = torch.zeros(nk, dtype=torch.int32, device=dev)
+            self.gboundary = torch.zeros((nk, a), dtype=torch.float32, device=dev)
+            self.conv = BlockEngine(conv_block, in_shape, nk, dev, full0[:cut], vel0[:cut],
+                                    need_input_grad=False)
+            for j in range(n_fc):
+                lo, hi = group_rows(self.conv_to_fc, j)
+                eng = BlockEngine(fc_block, (a,), (hi - lo) * k, dev,
+                                  full0[cut:], vel0[cut:], need_input_grad=True,
+                                  shared=self.fcs[0] if self.fcs else None,
+                                  input_grad_buffer=self.gboundary[lo * k:hi * k])
+                eng.rows = (lo * k, hi * k)
+                self.fcs.append(eng)
+        else:
+            if comm.n_conv != n_conv or comm.n_fc != n_fc:
+                raise ConfigError("communicator roles do not match (n_conv, n_fc)")
+            if comm.is_conv:
+                self.x = torch.zeros((k, *in_shape), dtype=torch.float32, device=dev)
+                self.labels = torch.zeros(k, dtype=torch.int32, device=dev)
+                self.gboundary = torch.zeros((k, a), dtype=torch.float32, device=dev)
+                self.conv = BlockEngine(conv_block, in_shape, k, dev, full0[:cut], vel0[:cut],
+                                        need_input_grad=False)
+            else:
+                g = len(comm.members(comm.index))
+                self.fc_in = torch.zeros((g * k, a), dtype=torch.float32, device=dev)
+                self.labels = torch.zeros(g * k, dtype=torch.int32, device=dev)
+                eng = BlockEngine(fc_block, (a,), g * k, dev, full0[cut:], vel0[cut:],
+                                  need_input_grad=True)
+                eng.rows = (0, g * k)
+                self.fcs.append(eng)
+        self._loss_slots = None
+
+    # -- helpers -------------------------------------------------------------------------
+
+    def _shape_at(self, cut):
+        from .tensor_core import out_shape
+        shape = tuple(self.spec.input_shape)
+        for layer in self.layers[:cut]:
+            shape = out_shape(layer, shape)
+        return shape
+
+    def group_members(self, fc_index: int) -> list[int]:
+        return [i for i, j in enumerate(self.conv_to_fc) if j == fc_index]
+
+    @property
+    def conv_params(self):
+        """CONV replica parameters (device views, reference layout)."""
+        return self.conv.params if self.conv is not None else None
+
+    @property
+    def fc_params(self):
+        return self.fcs[0].params if self.fcs else None
+
+    def local_conv_indices(self) -> list[int]:
+        if self.comm is None:
+            return list(range(self.n_conv))
+        return [self.comm.index] if self.comm.is_conv else []
+
+    # -- one iteration on device-resident inputs ------------------------------------
+
+    def load_batch(self, it: int) -> None:
+        """Fetch this process's CONV batches from batch_fn and upload them."""
+        idx = self.local_conv_indices()
+        if not idx:
+            return
+        xs, ys = [], []
+        for i in idx:
+            x, y = self.batch_fn(it, i)
+            if x.shape[0] != self.k:
+                raise ShapeMismatch(f"CONV batch has {x.shape[0]} samples, "
+                                    f"expected batch_k={self.k}")
+            xs.append(np.asarray(x, dtype=np.float32))
+            ys.append(np.asarray(y))
+        x = torch.from_numpy(np.ascontiguousarray(np.concatenate(xs)))
+        y = torch.from_numpy(np.concatenate(ys).astype(np.int32))
+        self.x.copy_(x.pin_memory(), non_blocking=True)
+        self.labels.copy_(y.pin_memory(), non_blocking=True)
+
+    def step(self, loss_slot: torch.Tensor | None = None) -> None:
+        """One BSP layer-separated iteration on the batch already in
+        ``self.x`` / ``self.labels``.  Adds the iteration's summed per-sample
+        loss into loss_slot (float64, on this process's FC workers)."""
+        n = self.n_conv * self.k
+        led = self.transport
+        a_bytes = self.boundary_activations * self.k * 4
+        ev = self._events() if self.time_phases else None
+        mark = (lambda label: ev.append((label, self._event()))) if ev is not None else \
+            (lambda label: None)
+        comm = self.comm
+        k = self.k
+
+        mark("conv_compute")
+        led.record("conv_compute")
+        acts = self.conv.forward(self.x) if self.conv is not None else None
+
+        mark("activations")
+        led.record("activations", self.n_conv * (a_bytes + k * 4))
+        led.tag_payload_bytes[Tag.ACTIVATIONS] += self.n_conv * a_bytes
+        led.tag_payload_bytes[Tag.CONTROL] += self.n_conv * k * 4
+        led.tag_messages[Tag.ACTIVATIONS] += self.n_conv
+        led.tag_messages[Tag.CONTROL] += self.n_conv
+        if comm is not None:
+            if comm.is_conv:
+                comm.gather_activations(acts.reshape(k, -1), self.labels, None, None, k)
+            else:
+                comm.gather_activations(None, None, self.fc_in, self.labels, k)
+
+        mark("fc_compute")
+        led.record("fc_compute")
+        for j, eng in enumerate(self.fcs):
+            lo, hi = eng.rows
+            if comm is None:
+                xin = acts.reshape(self.n_conv * k, -1)[lo:hi]
+                lab = self.labels[lo:hi]
+            else:
+                xin, lab = self.fc_in, self.labels
+            eng.forward(xin, lab, loss_out=loss_slot)
+            eng.backward()
+
+        mark("boundary")
+        led.record("boundary", self.n_conv * a_bytes)
+        led.tag_payload_bytes[Tag.BOUNDARY_GRADS] += self.n_conv * a_bytes
+        led.tag_messages[Tag.BOUNDARY_GRADS] += self.n_conv
+        if comm is not None:
+            if comm.is_conv:
+                comm.scatter_boundary(None, self.gboundary, k)
+            else:
+                comm.scatter_boundary(self.fcs[0].gin[0], None, k)
+        if self.conv is not None:
+            self.conv.backward(self.gboundary.reshape((self.conv.batch,
+                                                       *self.conv.out_shape)))
+
+        mark("exchange")
+        ring = lambda p, m: 0 if m == 1 else int(2 * (m - 1) * p * 4)  # noqa: E731
+        ar_bytes = ring(self.partition.conv_params, self.n_conv) + \
+            (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
+        led.record("exchange", ar_bytes)
+        led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
+        if comm is not None:
+            if comm.is_conv:
+                comm.allreduce_grads(self.conv.grad_flat)
+            else:
+                comm.allreduce_grads(self.fcs[0].grad_flat)
+        else:
+            for eng in self.fcs[1:]:
+                self.fcs[0].add_grads_from(eng)
+
+        mark("update")
+        led.record("update")
+        if self.conv is not None:
+            self.conv.sgd(n, self.lr, self.momentum)
+        if self.fcs:
+            self.fcs[0].sgd(n, self.lr, self.momentum)
+        mark("end")
+        if ev is not None:
+            self._pending_events.append(ev)
+
+    # -- public API ------------------------------------------------------------------
+
+    def train(self, iterations: int) -> StanzaResult:
+        """Run `iterations` more iterations; may be called repeatedly."""
+        slots = torch.zeros(max(iterations, 1), dtype=torch.float64, device=self.device)
+        self._pending_events = []
+        for s in range(iterations):
+            self.load_batch(self.iteration)
+            self.step(slots[s:s + 1] if self.fcs else None)
+            self.iteration += 1
+        if self.comm is not None:
+            self.comm.sum_scalar(slots)     # FC ranks hold the loss sums
+        n = self.n_conv * self.k
+        losses = [float(v) / n for v in slots[:iterations].cpu().tolist()]
+        self._resolve_phase_times()
+        return StanzaResult(losses=losses, state=self.state(), transport=self.transport)
+
+    def state(self) -> TrainState | None:
+        """Full state stitched from the first CONV and the first FC replica.
+        Collective in one-process-per-GPU mode: FC worker 0 ships its block to
+        rank 0, which returns the TrainState (other ranks return None)."""
+        if self.comm is None:
+            cp, cv = self.conv.state_numpy()
+            fp, fv = self.fcs[0].state_numpy()
+            return TrainState(self.iteration, cp + fp, cv + fv)
+        import torch.distributed as dist
+        fc0 = self.comm.n_conv
+        rank = self.comm.rank
+        if rank == fc0:
+            dist.send(self.fcs[0].params_flat, 0)
+            dist.send(self.fcs[0].vel_flat, 0)
+        if rank != 0:
+            return None
+        cut = self.partition.split_index
+        proto = BlockEngine.__new__(BlockEngine)
+        proto.layers = self.partition.fc_block
+        proto._layout_params()
+        pf = torch.empty(proto.total, dtype=torch.float32, device=self.device)
+        vf = torch.empty_like(pf)
+        dist.recv(pf, fc0)
+        dist.recv(vf, fc0)
+        fp = [[t.cpu().numpy().copy() for t in row] for row in proto._views(pf)]
+        fv = [[t.cpu().numpy().copy() for t in row] for row in proto._views(vf)]
+        cp, cv = self.conv.state_numpy()
+        assert len(cp) == cut
+        return TrainState(self.iteration, cp + fp, cv + fv)
+
+    def checkpoint(self) -> TrainState:
+        """Snapshot; FC worker 0's block state is also copied (as an STZC
+        blob) to a seeded-random CONV worker (stanza_runtime.py:182-211)."""
+        st = self.state()
+        if st is None:
+            return st
+        cut = self.partition.split_index
+        fc_state = TrainState(self.iteration, st.params[cut:], st.velocities[cut:])
+        blob = state_to_bytes(fc_state)
+        holder = random.Random((self.seed << 32) ^ self.iteration).randrange(self.n_conv)
+        self.replica_snapshots[self.conv_ids[holder]] = blob
+        self.transport.record("checkpoint", len(blob))
+        self.transport.tag_payload_bytes[Tag.CHECKPOINT] += len(blob)
+        self.transport.tag_messages[Tag.CHECKPOINT] += 1
+        return st
+
+    # -- phase timing ----------------------------------------------------------------
+
+    def _events(self):
+        return []
+
+    def _event(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(self.device))
+        return e
+
+    def _resolve_phase_times(self):
+        if not self.time_phases or not getattr(self, "_pending_events", None):
+            return
+        torch.cuda.synchronize(self.device)
+        recs = [p for p in self.transport.phases if p.label in PHASES]
+        i = len(recs) - 6 * len(self._pending_events)
+        for ev in self._pending_events:
+            for (label, e0), (_, e1) in zip(ev[:-1], ev[1:]):
+                recs[i].elapsed_ms = e0.elapsed_time(e1)
+                i += 1
+        self._pending_events = []

@@ -1,0 +1,30 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in (ROOT, os.path.join(ROOT, "oracle")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path)")
+
+
+@pytest.fixture(scope="session")
+def lib():
+    """The in-tree C-ABI library (built on demand; nvcc cross-compiles)."""
+    from paper_1812_10624_b200.build import build_library
+    from paper_1812_10624_b200 import _lib
+    build_library()
+    return _lib.load()
+
+
+@pytest.fixture(params=[0, 1, 2], ids=["tcgen05-bf16x6", "simt", "tcgen05-tf32x3"])
+def gemm_impl(request, lib):
+    """Run a GPU test under both GEMM cores; restore the product core after."""
+    lib.stz_set_gemm_impl(request.param)
+    yield request.param
+    lib.stz_set_gemm_impl(0)

@@ -1,0 +1,142 @@
+"""Hot-path parity on the B200: StanzaCluster.train vs the reference.
+
+* golden fixtures = the reference's own StanzaCluster outputs (tiny_cnn at
+  (1,1), (2,1), (4,2), (3,2), (7,1); tiny_cnn32 (2,1); tiny_mlp cut at 4);
+* bar = the reference's own: max_param_dev <= 1e-5 after N iterations
+  (reference tests/test_stanza_runtime.py:53-60, test_acceptance.py:76-102);
+  losses within 1e-5 relative;
+* determinism: the same run twice is bit-identical; a resumed run replays
+  the uninterrupted one bit for bit (reference test_stanza_runtime.py:106-119);
+* block operator contract (block_forward / block_backward) vs the oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+import stanza_oracle as orc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def _spec(name):
+    from paper_1812_10624_b200 import model_partition as mp
+    return {"tiny": mp.tiny_cnn, "tiny32": mp.tiny_cnn32, "mlp": mp.tiny_mlp}[name]()
+
+
+def _cluster(spec, nc, nf, seed, dseed, boundary=None, **kw):
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+    mk = orc.batch_fn(spec.input_shape, spec.batch_k, dseed)
+    return StanzaCluster(spec, n_conv=nc, n_fc=nf, batch_fn=mk, lr=0.05, momentum=0.9,
+                         seed=seed, boundary=boundary, device="cuda:0", **kw)
+
+
+CASES = ["tiny_1x1", "tiny_2x1", "tiny_4x2", "tiny_3x2", "tiny_7x1", "tiny32_2x1", "mlp_2x1"]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_train_matches_reference_golden(lib, case):
+    g = golden_io.train()[f"train_{case}"]
+    spec = _spec(case.split("_")[0])
+    boundary = 4 if case.startswith("mlp") else None
+    cl = _cluster(spec, int(g["n_conv"]), int(g["n_fc"]), int(g["seed"]), int(g["data_seed"]),
+                  boundary)
+    res = cl.train(int(g["iters"]))
+    ref_p, ref_v = golden_io.nested_state(g)
+    assert orc.max_param_dev(res.state.params, ref_p) <= TOL
+    assert orc.max_param_dev(res.state.velocities, ref_v) <= 1e-4
+    np.testing.assert_allclose(res.losses, g["losses"], rtol=TOL)
+
+
+def test_fifty_iterations_acceptance(lib):
+    """Acceptance shape: tiny_cnn, 50 iterations, (4,1) and (8,1), <= 1e-5 of
+    one-node training (reference test_acceptance.py:76-102)."""
+    spec = _spec("tiny")
+    layers = [tuple_of(l) for l in spec.layers]
+    for nc, nf in [(4, 1), (8, 1)]:
+        mk = orc.batch_fn(spec.input_shape, spec.batch_k, 7)
+        ref_p, _, _ = orc.single_node_train(layers, spec.batch_k, nc, 50, 3, mk)
+        res = _cluster(spec, nc, nf, 3, 7).train(50)
+        assert orc.max_param_dev(res.state.params, ref_p) <= TOL
+
+
+def tuple_of(layer):
+    from paper_1812_10624_b200.tensor_core import as_tuple
+    return as_tuple(layer)
+
+
+def test_run_is_deterministic(lib):
+    spec = _spec("tiny")
+    a = _cluster(spec, 2, 1, 4, 21).train(5)
+    b = _cluster(spec, 2, 1, 4, 21).train(5)
+    for la, lb in zip(a.state.params, b.state.params):
+        for x, y in zip(la, lb):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_resume_replays_bit_exact(lib):
+    from paper_1812_10624_b200.checkpointing import param_digest
+    spec = _spec("tiny")
+    whole = _cluster(spec, 2, 1, 4, 21).train(10)
+    first = _cluster(spec, 2, 1, 4, 21)
+    first.train(5)
+    snap = first.checkpoint()
+    resumed = _cluster(spec, 2, 1, 4, 21, state=snap)
+    assert resumed.iteration == 5
+    res = resumed.train(5)
+    assert param_digest(res.state.params) == param_digest(whole.state.params)
+    (holder, blob), = first.replica_snapshots.items()
+    assert holder[0] == "conv"
+
+
+def test_phase_sequence_and_traffic(lib):
+    """Reference ledger pins (test_stanza_runtime.py:158-179)."""
+    spec = _spec("tiny")
+    n_conv, iters = 3, 2
+    res = _cluster(spec, n_conv, 1, 3, 7).train(iters)
+    labels = [p.label for p in res.transport.phases]
+    assert labels == ["conv_compute", "activations", "fc_compute", "boundary", "exchange",
+                      "update"] * iters
+    led = res.transport
+    assert led.tag_payload_bytes["activations"] == iters * n_conv * 256 * spec.batch_k * 4
+    assert led.tag_payload_bytes["boundary_grads"] == iters * n_conv * 256 * spec.batch_k * 4
+    assert led.tag_payload_bytes["control"] == iters * n_conv * spec.batch_k * 4
+
+
+def test_block_contract_vs_oracle(lib):
+    """block_forward / block_backward through the per-op C ABI == oracle."""
+    from paper_1812_10624_b200 import tensor_core as tc
+    spec = _spec("tiny")
+    layers = list(spec.layers)
+    params_np = tc.seeded_init(layers, 3)
+    mk = orc.batch_fn(spec.input_shape, 8, 9)
+    x, y = mk(0, 0)
+    out, caches = tc.block_forward(layers, tc.to_device(params_np, "cuda:0"),
+                                   torch.from_numpy(x).cuda(), labels=y)
+    gx, grads = tc.block_backward(layers, tc.to_device(params_np, "cuda:0"), caches, None)
+    rout, rc = orc.block_forward([tc.as_tuple(l) for l in layers], params_np, x, labels=y)
+    rgx, rgrads = orc.block_backward([tc.as_tuple(l) for l in layers], params_np, rc, None)
+    torch.cuda.synchronize()
+    assert orc.rel_err(out.cpu().numpy(), rout) <= 1e-6
+    assert orc.rel_err(gx.cpu().numpy(), rgx) <= 1e-5
+    for lg, lr in zip(grads, rgrads):
+        for a, b in zip(lg, lr):
+            assert orc.rel_err(a.cpu().numpy(), b) <= 1e-5
+
+
+def test_alexnet_reduced_batch_step(lib):
+    """AlexNet layer shapes at parity K=2, co-located (1,1), 1 iteration vs
+    the oracle (full-K oracle is ~35 min/iter)."""
+    from paper_1812_10624_b200 import model_partition as mp
+    spec = mp.alexnet(batch_k=2)
+    mk = orc.batch_fn(spec.input_shape, 2, 7, classes=1000)
+    layers = [tuple_of(l) for l in spec.layers]
+    ref_p, _, ref_l = orc.layer_separated_train(layers, 2, 1, 1, 1, 3, mk)
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+    cl = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=mk, lr=0.05, momentum=0.9, seed=3,
+                       device="cuda:0")
+    out = cl.train(1)
+    assert orc.max_param_dev(out.state.params, ref_p) <= TOL
+    np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)
