@@ -1,0 +1,456 @@
+"""Benchmark of the B200 layer-separated training step (Stanza, arXiv 1812.10624).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model alexnet_exec]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...      # the CPU reference arm
+
+One step = one BSP layer-separated iteration (reference
+stanza_runtime.py:352-375) over the configured workload: CONV trunk forward
+on every CONV worker's K images, activation gather, FC head forward /
+SoftmaxCE / backward, boundary-gradient scatter, CONV trunk backward,
+CONV-group (and FC-group) gradient allreduce, momentum SGD -- nothing
+skipped.  Roles per GPU count (roles.GPU_ROLES): 1 GPU co-locates CONV and
+FC (1:1 on one device), 2 -> 1:1, 4 -> 3:1, 8 -> 7:1; K images per CONV
+worker are fixed, so scaling is weak.  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from contextlib import contextmanager
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec at 1/2/4/8 B200 (CONV:FC split); FC tensor-pipe %; NVLink GB/s"
+UNIT = "images/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--model", default="alexnet_exec")
+    ap.add_argument("--batch-k", type=int, default=None)
+    ap.add_argument("--fc-workers", type=int, default=None)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pool", type=int, default=4, help="device-resident input batches")
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# CPU side: oracle port (the reference algorithm restated; test infra)
+# ---------------------------------------------------------------------------
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:  # pragma: no cover
+        return 1
+
+
+def oracle_sample(model: str, images: int = 1, classes: int = 1000):
+    """One co-located layer-separated iteration of the oracle on `images`
+    images per CONV worker (1 CONV : 1 FC); returns seconds."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import stanza_oracle as orc
+    layers, shape = {"alexnet_exec": orc.alexnet_layers, "vgg16_exec": orc.vgg16_layers}.get(
+        model, orc.alexnet_layers)()
+    mk = orc.batch_fn(shape, images, 7, classes=classes)
+    t0 = time.perf_counter()
+    orc.layer_separated_train(layers, images, 1, 1, 1, 3, mk)
+    return time.perf_counter() - t0
+
+
+def reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from paper_1812_10624_b200.roles import gpu_roles
+    n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
+    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64}.get(args.model, 128)
+    budget = 150.0
+    for _ in range(min(args.warmup, 1)):
+        oracle_sample(args.model)
+    times, t_start = [], time.perf_counter()
+    for _ in range(args.steps):
+        times.append(oracle_sample(args.model))
+        if time.perf_counter() - t_start > budget:
+            break
+    sec_per_img = statistics.mean(times)
+    value = 1.0 / sec_per_img
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
+        "ms_per_step": sec_per_img * 1e3 * n_conv * k, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate/f32-storage",
+        "data": "synthetic",
+        "config": workload_config(args, n_conv, n_fc, k),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle/stanza_oracle.py layer_separated_train, 1 image "
+                                   f"per step through the full {args.model} co-located "
+                                   f"iteration (trunk fwd+bwd, FC fwd+bwd, SGD); "
+                                   f"{len(times)} timed samples; ms_per_step extrapolates "
+                                   f"x{n_conv * k} images (CONV workers run sequentially "
+                                   f"in the reference, stanza_runtime.py:218,:366)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, n_conv, n_fc, k):
+    return {"workload": f"{args.model} 224x224 synthetic, K={k} images per CONV worker, "
+                        f"{n_conv} CONV : {n_fc} FC" + (" co-located on 1 GPU"
+                                                         if args.gpus == 1 else ""),
+            "model": args.model, "batch_per_conv_worker": k, "n_conv": n_conv, "n_fc": n_fc,
+            "global_batch": n_conv * k, "parallelism": f"layer-separated {n_conv}:{n_fc}",
+            "l2": "inputs larger than L2: pool of device-resident batches rotated"}
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (recipe clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gemm_flops(name, a):
+    """Algorithmic FLOPs of one GEMM-class ABI call from its size arguments."""
+    ints = [v for v in a if isinstance(v, int)]
+    if name.startswith("stz_conv2d"):
+        n, c, h, w, o, k, s, p = ints[:8]
+        oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        return 2.0 * n * oh * ow * o * c * k * k
+    if name.startswith("stz_fc"):
+        m, i, o = ints[:3]
+        return 2.0 * m * i * o
+    return 0.0
+
+
+class CallTimer:
+    """PROFILE_HOOK for paper_1812_10624_b200._lib: CUDA events around each
+    ABI call on the launching (current) stream."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.records = []
+
+    @contextmanager
+    def __call__(self, name, args):
+        t = self.torch
+        e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        e0.record()
+        yield
+        e1.record()
+        key = (name, tuple(v for v in args if isinstance(v, int))[:8])
+        self.records.append((key, e0, e1))
+
+    def table(self):
+        self.torch.cuda.synchronize()
+        agg = {}
+        for key, e0, e1 in self.records:
+            ms = e0.elapsed_time(e1)
+            tot, cnt = agg.get(key, (0.0, 0))
+            agg[key] = (tot + ms, cnt + 1)
+        return agg
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p["hbm_gbs"], "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(kernel_key: str):
+    path = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_10624_b200 import _lib
+    from paper_1812_10624_b200.model_partition import builtin_model
+    from paper_1812_10624_b200.roles import gpu_roles
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torch.distributed.run")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    lib.stz_set_gemm_impl(0)
+    n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
+    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64}.get(args.model, 4)
+    spec = builtin_model(args.model, k)
+
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_1812_10624_b200.comm import RoleComm
+        comm = RoleComm(n_conv, n_fc)
+
+    def batch_fn(it, i):  # only used for shapes; the timed loop feeds device pools
+        raise RuntimeError("bench feeds device-resident batches")
+
+    cl = StanzaCluster(spec, n_conv=n_conv, n_fc=n_fc, batch_fn=batch_fn, lr=0.01,
+                       momentum=0.9, seed=3, device=dev, comm=comm)
+    is_conv_rank = cl.conv is not None
+    classes = spec.layers[-2].out_dim
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    pool_x, pool_y = [], []
+    if is_conv_rank:
+        for _ in range(args.pool):
+            pool_x.append(torch.randn(cl.x.shape, generator=gen, device=dev))
+            pool_y.append(torch.randint(0, classes, cl.labels.shape, generator=gen,
+                                        device=dev, dtype=torch.int32))
+    slots = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.float64, device=dev)
+
+    def one(i, slot=None):
+        if is_conv_rank:
+            j = i % args.pool
+            cl.step(slot, x=pool_x[j], labels=pool_y[j])
+        else:
+            cl.step(slot)
+
+    def sync_all():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (W >= 3 enforced)
+    warm = max(args.warmup, 3)
+    for i in range(warm):
+        one(i, slots[i % slots.numel():i % slots.numel() + 1])
+    sync_all()
+
+    # ---- timed region: device-resident inputs ------------------------------------
+    launches0 = lib.stz_launch_count()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        sync_all()
+        e0.record(stream)
+        for i in range(args.steps):
+            one(i, slots[i:i + 1])
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = lib.stz_launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(t.item())
+    images = n_conv * k
+    value = images / (ms / 1e3)
+
+    # ---- e2e: host buffers through the public step API ---------------------------
+    h2d = 0
+    if is_conv_rank:
+        xh = pool_x[0].cpu().pin_memory()
+        yh = pool_y[0].cpu().pin_memory()
+        h2d = xh.numel() * 4 + yh.numel() * 4
+    loss_h = torch.zeros(args.steps, dtype=torch.float64).pin_memory()
+    sync_all()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for i in range(args.steps):
+        if is_conv_rank:
+            cl.x.copy_(xh, non_blocking=True)
+            cl.labels.copy_(yh, non_blocking=True)
+        cl.step(slots[i:i + 1])
+        loss_h[i:i + 1].copy_(slots[i:i + 1], non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = torch.tensor([e2.elapsed_time(e3) / args.steps], dtype=torch.float64, device=dev)
+    io = torch.tensor([float(h2d), float(8 if cl.fcs else 0)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(io, op=dist.ReduceOp.SUM)
+    e2e_ms = float(e2e_ms.item())
+
+    # ---- per-call kernel timing (separate, untimed pass) --------------------------
+    timer = CallTimer(torch)
+    _lib.PROFILE_HOOK = timer
+    cl.time_phases = True
+    cl._pending_events = []
+    one(0)
+    _lib.PROFILE_HOOK = None
+    cl._resolve_phase_times()
+    cl.time_phases = False
+    calls = timer.table()
+    phase_ms = {}
+    for rec in cl.transport.phases[-6:]:
+        phase_ms[rec.label] = rec.elapsed_ms
+
+    bf16_peak, hbm_peak, peak_src = peaks()
+    top_key, top = None, (0.0, 0)
+    for key, (tot, cnt) in calls.items():
+        if tot > top[0]:
+            top_key, top = key, (tot, cnt)
+    fl = gemm_flops(top_key[0], top_key[1]) if top_key else 0.0
+    avg_ms = top[0] / max(top[1], 1)
+    achieved = fl / (avg_ms / 1e3) / 1e12 if avg_ms > 0 and fl > 0 else 0.0
+    kernel_key = f"{top_key[0]}{list(top_key[1])}" if top_key else None
+    step_ms_sum = sum(tot for tot, _ in calls.values())
+    fc_fl = sum(gemm_flops(kk[0], kk[1]) * c for kk, (_, c) in calls.items()
+                if kk[0].startswith("stz_fc"))
+    fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("stz_fc"))
+    fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None
+    roofline = {
+        "bound": "tensor", "kernel": kernel_key, "achieved": achieved, "peak": bf16_peak,
+        "unit": "TFLOP/s", "frac": achieved / bf16_peak if bf16_peak else None,
+        "traffic": committed_traffic(kernel_key),
+        "peak_source": peak_src,
+        "note": ("achieved = algorithmic fp32 GEMM FLOPs (2*M*N*K of the conv/FC "
+                 "contraction) / mean CUDA-event duration of that ABI call; the BF16x6 "
+                 "split issues 6 bf16 MMAs per algorithmic MAC, so the tensor-pipe "
+                 "occupancy is 6*frac and the scheme's own ceiling is frac = 1/6"),
+        "tensor_pipe_frac": 6 * achieved / bf16_peak if bf16_peak else None,
+        "share_of_step": top[0] / step_ms_sum if step_ms_sum else None,
+    }
+
+    line = None
+    # gather per-rank extras to rank 0
+    extras = {"rank": rank, "role": "conv" if is_conv_rank else "fc", "phase_ms": phase_ms,
+              "roofline": roofline, "fc_tflops": fc_tflops, "launches": launches}
+    if world > 1:
+        objs = [None] * world
+        dist.all_gather_object(objs, extras)
+    else:
+        objs = [extras]
+    if rank == 0:
+        conv_ex = next(o for o in objs if o["role"] == "conv")
+        fc_ex = next((o for o in objs if o["fc_tflops"] is not None), conv_ex)
+        nvlink = None
+        if world > 1:
+            act_bytes = n_conv * k * cl.boundary_activations * 4
+            fcp = fc_ex["phase_ms"]
+            nvlink = {
+                "gather_GBps": act_bytes / (fcp["activations"] / 1e3) / 1e9
+                if fcp.get("activations") else None,
+                "scatter_GBps": act_bytes / (fcp["boundary"] / 1e3) / 1e9
+                if fcp.get("boundary") else None,
+                "peak_GBps": 770.0, "note": "payload bytes / FC-worker phase time"}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            secs = [oracle_sample(args.model) for _ in range(2)]
+            v = 1.0 / statistics.mean(secs)
+            cpu = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "port",
+                   "sample": f"oracle layer_separated_train, 1 image x {len(secs)} "
+                             f"co-located {args.model} iterations on this host"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": warm, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (N(0,1) images, uniform labels, "
+                                    "device-resident pool, random-init weights)",
+            "config": workload_config(args, n_conv, n_fc, k),
+            "roofline": conv_ex["roofline"],
+            "cpu_baseline": cpu,
+            "e2e": {"value": images / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(io[0].item()),
+                    "d2h_bytes_per_step": int(io[1].item()),
+                    "api": "StanzaCluster.step after pinned-host copies of the batch; "
+                           "loss copied back every step"},
+            "gpu_launches": int(sum(o["launches"] for o in objs)),
+            "clocks": clocks.summary(),
+            "fc_tensor_pipe_frac": (6 * fc_ex["fc_tflops"] / bf16_peak)
+            if fc_ex["fc_tflops"] else None,
+            "fc_tflops_algorithmic": fc_ex["fc_tflops"],
+            "nvlink": nvlink,
+            "phase_ms": {o["role"] + str(o["rank"]): o["phase_ms"] for o in objs},
+            "gemm": "tcgen05 BF16x6 (3-way bf16 split, 6 MMAs, split fp32 TMEM accumulators)",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

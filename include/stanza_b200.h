@@ -42,6 +42,9 @@ const char* stz_last_error(void);
 int stz_set_gemm_impl(int impl);
 int stz_get_gemm_impl(void);
 
+/* Number of kernels this library has launched (bench evidence). */
+unsigned long long stz_launch_count(void);
+
 /* Tuning/experiment knob: cap the K extent one CTA accumulates (0 = auto). */
 int stz_set_max_k_per_split(int k);
 

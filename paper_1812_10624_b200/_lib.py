@@ -28,6 +28,7 @@ SIGNATURES = {
     "stz_set_gemm_impl": (I, [I]),
     "stz_get_gemm_impl": (I, []),
     "stz_set_max_k_per_split": (I, [I]),
+    "stz_launch_count": (ctypes.c_ulonglong, []),
     "stz_conv2d_fwd": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stz_conv2d_bwd_data": (I, [P, P, P, P, I, I, I, I, I, I, I, I, P, Z, P]),
     "stz_conv2d_bwd_filter": (I, [P, P, P, P, I, I, I, I, I, I, I, I, P, Z, P]),
@@ -82,10 +83,19 @@ def load(path: str | None = None):
     return lib
 
 
+# Optional per-call hook (bench.py): callable(name, args) -> context manager
+# that brackets the call with CUDA events on the launching stream.
+PROFILE_HOOK = None
+
+
 def call(name: str, *args) -> None:
     """Invoke an ABI function and raise on a non-zero status."""
     lib = load()
-    rc = getattr(lib, name)(*args)
+    if PROFILE_HOOK is not None:
+        with PROFILE_HOOK(name, args):
+            rc = getattr(lib, name)(*args)
+    else:
+        rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.stz_last_error().decode(errors="replace")
         if rc == 1:

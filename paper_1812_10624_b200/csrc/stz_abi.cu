@@ -33,9 +33,12 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+unsigned long long g_launches = 0;  // kernels launched through this library
+
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(STZ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  ++g_launches;
   return STZ_OK;
 }
 
@@ -379,6 +382,8 @@ int stz_set_gemm_impl(int impl) {
 }
 
 int stz_get_gemm_impl(void) { return g_impl; }
+
+unsigned long long stz_launch_count(void) { return g_launches; }
 
 int stz_set_max_k_per_split(int k) {
   if (k < 0) return fail(STZ_EINVAL, "max_k_per_split must be >= 0");

@@ -238,10 +238,15 @@ class StanzaCluster:
         self.x.copy_(x.pin_memory(), non_blocking=True)
         self.labels.copy_(y.pin_memory(), non_blocking=True)
 
-    def step(self, loss_slot: torch.Tensor | None = None) -> None:
-        """One BSP layer-separated iteration on the batch already in
-        ``self.x`` / ``self.labels``.  Adds the iteration's summed per-sample
-        loss into loss_slot (float64, on this process's FC workers)."""
+    def step(self, loss_slot: torch.Tensor | None = None, x: torch.Tensor | None = None,
+             labels: torch.Tensor | None = None) -> None:
+        """One BSP layer-separated iteration on the batch in ``self.x`` /
+        ``self.labels`` (or on device-resident ``x`` / ``labels`` of the same
+        shapes, e.g. a pre-staged pool).  Adds the iteration's summed
+        per-sample loss into loss_slot (float64, on this process's FC
+        workers)."""
+        x_in = self.x if x is None else x
+        lab_all = self.labels if labels is None else labels
         n = self.n_conv * self.k
         led = self.transport
         a_bytes = self.boundary_activations * self.k * 4
@@ -253,7 +258,7 @@ class StanzaCluster:
 
         mark("conv_compute")
         led.record("conv_compute")
-        acts = self.conv.forward(self.x) if self.conv is not None else None
+        acts = self.conv.forward(x_in) if self.conv is not None else None
 
         mark("activations")
         led.record("activations", self.n_conv * (a_bytes + k * 4))
@@ -263,7 +268,7 @@ class StanzaCluster:
         led.tag_messages[Tag.CONTROL] += self.n_conv
         if comm is not None:
             if comm.is_conv:
-                comm.gather_activations(acts.reshape(k, -1), self.labels, None, None, k)
+                comm.gather_activations(acts.reshape(k, -1), lab_all, None, None, k)
             else:
                 comm.gather_activations(None, None, self.fc_in, self.labels, k)
 
@@ -273,7 +278,7 @@ class StanzaCluster:
             lo, hi = eng.rows
             if comm is None:
                 xin = acts.reshape(self.n_conv * k, -1)[lo:hi]
-                lab = self.labels[lo:hi]
+                lab = lab_all[lo:hi]
             else:
                 xin, lab = self.fc_in, self.labels
             eng.forward(xin, lab, loss_out=loss_slot)
