@@ -1,0 +1,84 @@
+"""The one-process-per-GPU exchange (comm.RoleComm) on CPU tensors over
+gloo: gather into FC input rows in ascending CONV order, scatter of boundary
+rows, role-group allreduce -- world sizes 2 (1:1), 3 (2:1) and 4 (2:2)."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, n_conv, n_fc, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1812_10624_b200.comm import RoleComm
+        comm = RoleComm(n_conv, n_fc)
+        k, a = 3, 5
+        out = {}
+        if comm.is_conv:
+            i = comm.index
+            acts = torch.full((k, a), float(i + 1)) + torch.arange(k * a).reshape(k, a) / 100
+            labels = torch.full((k,), i, dtype=torch.int32)
+            comm.gather_activations(acts, labels, None, None, k)
+            gy = torch.zeros(k, a)
+            comm.scatter_boundary(None, gy, k)
+            out["gy"] = gy
+            g = torch.full((7,), float(i + 1))
+            comm.allreduce_grads(g)
+            out["g"] = g
+        else:
+            members = comm.members(comm.index)
+            fc_in = torch.zeros(len(members) * k, a)
+            fc_lab = torch.zeros(len(members) * k, dtype=torch.int32)
+            comm.gather_activations(None, None, fc_in, fc_lab, k)
+            out["fc_in"], out["fc_lab"], out["members"] = fc_in, fc_lab, members
+            comm.scatter_boundary(-fc_in, None, k)
+            g = torch.full((4,), 10.0 * (comm.index + 1))
+            comm.allreduce_grads(g)
+            out["g"] = g
+        q.put((rank, {key: (v.tolist() if torch.is_tensor(v) else v) for key, v in out.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_conv,n_fc", [(1, 1), (2, 1), (2, 2), (3, 1)])
+def test_role_exchange(n_conv, n_fc):
+    world = n_conv + n_fc
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, n_conv, n_fc, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    k, a = 3, 5
+    base = torch.arange(k * a).reshape(k, a) / 100
+    from paper_1812_10624_b200.roles import plan_groups
+    conv_to_fc = plan_groups(n_conv, n_fc)
+    for r in range(n_conv, world):
+        j = r - n_conv
+        members = [i for i, f in enumerate(conv_to_fc) if f == j]
+        fc_in = torch.tensor(res[r]["fc_in"])
+        for pos, i in enumerate(members):
+            assert torch.allclose(fc_in[pos * k:(pos + 1) * k], base + (i + 1))
+            assert res[r]["fc_lab"][pos * k:(pos + 1) * k] == [i] * k
+        expect_fc = sum(10.0 * (jj + 1) for jj in range(n_fc))
+        assert res[r]["g"] == [expect_fc] * 4
+    for i in range(n_conv):
+        assert torch.allclose(torch.tensor(res[i]["gy"]), -(base + (i + 1)))
+        assert res[i]["g"] == [float(sum(range(1, n_conv + 1)))] * 7
+
