@@ -408,13 +408,19 @@ def main():
         nvlink = None
         if world > 1:
             act_bytes = n_conv * k * cl.boundary_activations * 4
-            fcp = fc_ex["phase_ms"]
+            # the FC side's gather phase includes waiting for the CONV forward and
+            # the CONV side's scatter phase includes the FC step, so each transfer
+            # is timed on the rank that is already ready when it starts
+            per_conv = k * cl.boundary_activations * 4
+            send_ms = max(o["phase_ms"]["activations"] for o in objs if o["role"] == "conv")
+            scat_ms = max(o["phase_ms"]["boundary"] for o in objs if o["role"] == "fc")
             nvlink = {
-                "gather_GBps": act_bytes / (fcp["activations"] / 1e3) / 1e9
-                if fcp.get("activations") else None,
-                "scatter_GBps": act_bytes / (fcp["boundary"] / 1e3) / 1e9
-                if fcp.get("boundary") else None,
-                "peak_GBps": 770.0, "note": "payload bytes / FC-worker phase time"}
+                "gather_GBps": per_conv / (send_ms / 1e3) / 1e9 if send_ms else None,
+                "scatter_GBps": act_bytes / n_fc / (scat_ms / 1e3) / 1e9 if scat_ms else None,
+                "peak_GBps": 770.0,
+                "bytes_per_conv_worker": per_conv,
+                "note": "gather: one CONV worker's [K,A] send / its phase time; scatter: an "
+                        "FC worker's outgoing boundary rows / its phase time (NCCL P2P)"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             secs = [oracle_sample(args.model) for _ in range(2)]

@@ -183,6 +183,8 @@ class StanzaCluster:
                 self.conv = BlockEngine(conv_block, in_shape, k, dev, full0[:cut], vel0[:cut],
                                         need_input_grad=False)
             else:
+                self.x = None
+                self.gboundary = None
                 g = len(comm.members(comm.index))
                 self.fc_in = torch.zeros((g * k, a), dtype=torch.float32, device=dev)
                 self.labels = torch.zeros(g * k, dtype=torch.int32, device=dev)
