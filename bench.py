@@ -259,7 +259,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _lib.load()
-    lib.stz_set_gemm_impl(0)
     n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
     k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64}.get(args.model, 4)
     spec = builtin_model(args.model, k)

@@ -32,15 +32,9 @@
 extern "C" {
 #endif
 
-/* ABI version (1) and the last error message of the calling thread. */
+/* ABI version (2) and the last error message of the calling thread. */
 int stz_abi_version(void);
 const char* stz_last_error(void);
-
-/* GEMM core: 0 = tcgen05 BF16x6 split (default, product), 1 = SIMT fp32
- * (validation kernel the GPU tests cross-check against), 2 = tcgen05
- * TF32x3 split (kept for the precision study; ~20-bit tf32 product sums). */
-int stz_set_gemm_impl(int impl);
-int stz_get_gemm_impl(void);
 
 /* Number of kernels this library has launched (bench evidence). */
 unsigned long long stz_launch_count(void);
@@ -118,6 +112,73 @@ int stz_sgd_momentum(float* w, float* v, const float* g, size_t n, float lr, flo
  * workers share one GPU -- the single-device stand-in for the FC-group
  * allreduce (stanza_runtime.py:320-337); on >1 GPU NCCL does this. */
 int stz_vec_add(float* dst, const float* src, size_t n, void* stream);
+
+/* ===========================================================================
+ * Hot path on split-plane tensors (engine.BlockEngine).
+ *
+ * A logical fp32 tensor is three bf16 planes P0,P1,P2 (uint16 storage, plane
+ * stride `ps` elements) with T = P0 + P1 + P2 exactly.  Conv activations are
+ * NHWC with channels padded to C8 = roundup(C, 8); flat activations and FC
+ * weights are row-major [rows][D8].  Conv weights are re-packed after every
+ * update as wf[O][kh][kw][C8] (forward) and wd[C][kh][kw][O8] (input
+ * gradient); FC W [in][out] as [in][out8] planes.  Every GEMM is the tcgen05
+ * BF16x6 kernel; fp32 master parameters stay in the reference layouts.
+ * ===========================================================================
+ */
+
+/* layout conversion (batch input, FC-block input, weights, debug read-back) */
+int stzx_pack_nchw(const float* x, void* xp, size_t ps, int N, int C, int H, int W, int C8,
+                   void* stream);
+int stzx_unpack_nhwc(const void* xp, size_t ps, float* x, int N, int C, int H, int W, int C8,
+                     void* stream);
+int stzx_pack_rows(const float* x, void* xp, size_t ps, int M, int D, int D8, void* stream);
+int stzx_unpack_rows(const void* xp, size_t ps, float* x, int M, int D, int D8, void* stream);
+int stzx_pack_conv_w(const float* w, void* wf, size_t psf, void* wd, size_t psd, int O, int C,
+                     int k, int C8, int O8, void* stream);
+int stzx_nhwc_to_flat(const void* x, size_t psx, void* y, size_t psy, int N, int C, int H, int W,
+                      int C8, int D8, void* stream);
+int stzx_flat_to_nhwc(const void* y, size_t psy, void* x, size_t psx, int N, int C, int H, int W,
+                      int C8, int D8, void* stream);
+
+/* Conv2d forward (tensor_core.py:161-181 + fused ReLU): y NHWC [N][OH][OW][O8]. */
+int stzx_conv_fwd(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
+                  void* y, size_t psy, int N, int C8, int H, int W, int O, int O8, int k, int s,
+                  int p, int relu, void* ws, size_t ws_bytes, void* stream);
+/* Conv2d input gradient (tensor_core.py:257-260), ReLU mask = plane 0 of the
+ * conv input when a ReLU produced it (nullable). */
+int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
+                    const void* mask, int N, int C, int C8, int H, int W, int O8, int k, int s,
+                    int p, void* ws, size_t ws_bytes, void* stream);
+/* Conv2d weight / bias gradient sums into fp32 [O,C,k,k] / [O] (tensor_core.py:253-259). */
+int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
+                    int N, int C, int C8, int H, int W, int O, int O8, int k, int s, int p,
+                    void* ws, size_t ws_bytes, void* stream);
+/* FC forward (tensor_core.py:205-211): split output (y) or fp32 logits (y_f32). */
+int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const float* bias, void* y,
+                size_t psy, float* y_f32, int M, int in_dim, int in8, int out_dim, int out8,
+                int relu, void* ws, size_t ws_bytes, void* stream);
+/* FC input gradient (tensor_core.py:286) with optional ReLU mask. */
+int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx, size_t psgx,
+                  const void* mask, int M, int in_dim, int in8, int out8, void* ws,
+                  size_t ws_bytes, void* stream);
+/* FC weight / bias gradient sums (tensor_core.py:287-288). */
+int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
+                  int M, int in_dim, int in8, int out_dim, int out8, void* ws, size_t ws_bytes,
+                  void* stream);
+/* MaxPool2d (tensor_core.py:183-198 / :263-276); flat_ld > 0 selects the
+ * CHW-flat [N][flat_ld] layout for y / gy (the FC-block boundary). */
+int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
+                     int C8, int H, int W, int k, int s, int flat_ld, void* stream);
+int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, size_t psx,
+                     const void* mask, int N, int C, int C8, int H, int W, int k, int s,
+                     int flat_ld, void* stream);
+/* standalone ReLU on split planes */
+int stzx_relu_fwd(const void* x, size_t psx, void* y, size_t psy, size_t n, void* stream);
+int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t psx, size_t n,
+                  void* stream);
+/* SoftmaxCE on fp32 logits -> losses + split dlogits [M][C8]. */
+int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
+                    int M, int C, int C8, void* stream);
 
 #ifdef __cplusplus
 }

@@ -25,8 +25,6 @@ F = ctypes.c_float
 SIGNATURES = {
     "stz_abi_version": (I, []),
     "stz_last_error": (ctypes.c_char_p, []),
-    "stz_set_gemm_impl": (I, [I]),
-    "stz_get_gemm_impl": (I, []),
     "stz_set_max_k_per_split": (I, [I]),
     "stz_launch_count": (ctypes.c_ulonglong, []),
     "stz_conv2d_fwd": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
@@ -43,6 +41,25 @@ SIGNATURES = {
     "stz_sum_f32": (I, [P, Z, P, I, P]),
     "stz_sgd_momentum": (I, [P, P, P, Z, F, F, F, P]),
     "stz_vec_add": (I, [P, P, Z, P]),
+    # split-plane hot path
+    "stzx_pack_nchw": (I, [P, P, Z, I, I, I, I, I, P]),
+    "stzx_unpack_nhwc": (I, [P, Z, P, I, I, I, I, I, P]),
+    "stzx_pack_rows": (I, [P, P, Z, I, I, I, P]),
+    "stzx_unpack_rows": (I, [P, Z, P, I, I, I, P]),
+    "stzx_pack_conv_w": (I, [P, P, Z, P, Z, I, I, I, I, I, P]),
+    "stzx_nhwc_to_flat": (I, [P, Z, P, Z, I, I, I, I, I, I, P]),
+    "stzx_flat_to_nhwc": (I, [P, Z, P, Z, I, I, I, I, I, I, P]),
+    "stzx_conv_fwd": (I, [P, Z, P, Z, P, P, Z, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_conv_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_conv_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_fc_fwd": (I, [P, Z, P, Z, P, P, Z, P, I, I, I, I, I, I, P, Z, P]),
+    "stzx_fc_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, P, Z, P]),
+    "stzx_fc_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, P, Z, P]),
+    "stzx_maxpool_fwd": (I, [P, Z, P, Z, P, I, I, I, I, I, I, I, I, P]),
+    "stzx_maxpool_bwd": (I, [P, Z, P, P, Z, P, I, I, I, I, I, I, I, I, P]),
+    "stzx_relu_fwd": (I, [P, Z, P, Z, Z, P]),
+    "stzx_relu_bwd": (I, [P, Z, P, P, Z, Z, P]),
+    "stzx_softmax_ce": (I, [P, P, P, P, Z, I, I, I, P]),
 }
 
 
@@ -58,7 +75,7 @@ def header_symbols(path: str = _HEADER) -> list[str]:
     """Every function the public header declares."""
     with open(path, "r", encoding="utf-8") as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"\b(stz_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(stzx?_[a-z0-9_]+)\s*\(", text)))
 
 
 _lib = None

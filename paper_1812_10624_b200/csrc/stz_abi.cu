@@ -1,15 +1,22 @@
 // C-ABI for the Stanza B200 hot path (declared in include/stanza_b200.h).
 //
-// Every entry takes device pointers owned by the caller (PyTorch), sizes,
-// an optional caller workspace and a cudaStream_t passed as void*.  Nothing
-// here allocates device memory.  Return value: 0 = ok, else an STZ_E* code;
-// stz_last_error() holds the message.
+// Two levels:
+//   stz_*   reference-layout operator contract (fp32 NCHW / row-major, the
+//           layouts of /root/reference/pkg/src/stanza/tensor_core.py); each
+//           GEMM op packs its inputs into split planes in the caller
+//           workspace and runs the same tcgen05 kernel as the hot path.
+//   stzx_*  the fused hot path on split-plane tensors (stz_split.cuh),
+//           driven by engine.BlockEngine.
+// Every entry takes device pointers owned by the caller (PyTorch), sizes, an
+// optional caller workspace and a cudaStream_t passed as void*.  Nothing here
+// allocates device memory.  0 = ok, else an STZ_E* code; stz_last_error()
+// holds the message.
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
 
-#include "stz_gemm.cuh"
+#include "stz_fmt.cuh"
 #include "../../include/stanza_b200.h"
 
 using namespace stz;
@@ -17,9 +24,9 @@ using namespace stz;
 namespace {
 
 thread_local std::string g_err;
-int g_impl = 0;  // 0 = tcgen05 BF16x6 (product), 1 = SIMT fp32, 2 = tcgen05 TF32x3
 int g_num_sms = 0;
-int g_max_kps = 0;  // >0: cap the K range one CTA accumulates (experiments/tests)
+int g_max_kps = 0;  // >0: cap the K range one CTA accumulates (tuning knob)
+unsigned long long g_launches = 0;
 
 enum { STZ_OK = 0, STZ_EINVAL = 1, STZ_ECUDA = 2, STZ_EWORKSPACE = 3 };
 
@@ -32,8 +39,6 @@ int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
-
-unsigned long long g_launches = 0;  // kernels launched through this library
 
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -54,108 +59,35 @@ int num_sms() {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline int rup8(int v) { return (v + 7) / 8 * 8; }
+inline const bf16_t* cb(const void* p) { return reinterpret_cast<const bf16_t*>(p); }
+inline bf16_t* mb(void* p) { return reinterpret_cast<bf16_t*>(p); }
 
-template <class S, int BN, int BK, class VA, class VB>
-void launch_tc(const VA& va, const VB& vb, const Epilogue& epi, float* partial, int M, int N,
-               int K, int kps, int splits, cudaStream_t st) {
-  using Cfg = TcCfg<S, BN, BK>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<S, BN, BK, VA, VB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr_set = true;
-  }
-  dim3 grid(cdiv(M, TC_BM), cdiv(N, BN), splits);
-  gemm_tc_kernel<S, BN, BK, VA, VB><<<grid, TC_THREADS, Cfg::SMEM, st>>>(va, vb, epi, partial, M,
-                                                                           N, K, kps);
+int grid_for(size_t n, int threads = 256) {
+  size_t b = (n + threads - 1) / threads;
+  const size_t cap = (size_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
 }
 
-template <class S, class VA, class VB>
-void launch_tc_bn(int BN, const VA& va, const VB& vb, const Epilogue& epi, float* partial, int M,
-                  int N, int K, int kps, int splits, cudaStream_t st) {
-  if (BN == 32) launch_tc<S, 32, 32>(va, vb, epi, partial, M, N, K, kps, splits, st);
-  else if (BN == 64) launch_tc<S, 64, 32>(va, vb, epi, partial, M, N, K, kps, splits, st);
-  else if (BN == 128) launch_tc<S, 128, 32>(va, vb, epi, partial, M, N, K, kps, splits, st);
-  else launch_tc<S, 256, 16>(va, vb, epi, partial, M, N, K, kps, splits, st);
-}
-
-// C[M,N] = A(M,K) . B(K,N) through the views, epilogue applied once.
-template <class VA, class VB>
-int run_gemm(const char* what, const VA& va, const VB& vb, const Epilogue& epi, int M, int N,
-             int K, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (M <= 0 || N <= 0) return STZ_OK;
-  if (K <= 0) return fail(STZ_EINVAL, "%s: empty contraction (K=%d)", what, K);
-  int BN, BK;
-  if (g_impl == 1) {
-    BN = 64;
-    BK = 16;
-  } else {
-    BN = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
-    BK = BN == 256 ? 16 : 32;
+// bump allocator over the caller workspace (256-byte aligned carving)
+struct Carve {
+  uint8_t* p;
+  size_t left;
+  Carve(void* ws, size_t bytes) : p(static_cast<uint8_t*>(ws)), left(ws ? bytes : 0) {}
+  template <class T>
+  T* take(size_t n) {
+    size_t bytes = (n * sizeof(T) + 255) / 256 * 256;
+    if (bytes > left) return nullptr;
+    T* r = reinterpret_cast<T*>(p);
+    p += bytes;
+    left -= bytes;
+    return r;
   }
-  const int tiles = cdiv(M, TC_BM) * cdiv(N, BN);
-  const int nkb = cdiv(K, BK);
-  const int target = 2 * num_sms();
-  int splits = 1;
-  if (tiles < target && nkb >= 8) {
-    splits = cdiv(target, tiles);
-    if (splits > nkb / 4) splits = nkb / 4;
-    const size_t per = (size_t)M * N * sizeof(float);
-    const size_t fit = ws ? ws_bytes / per : 0;
-    if ((size_t)splits > fit) splits = (int)fit;
-    if (splits < 2) splits = 1;
-  }
-  if (g_max_kps > 0 && K > g_max_kps) {
-    const size_t per = (size_t)M * N * sizeof(float);
-    const int want = cdiv(K, g_max_kps);
-    const int fit = ws ? (int)(ws_bytes / per) : 1;
-    splits = want < fit ? want : fit;
-    if (splits < 1) splits = 1;
-  }
-  const int kps = cdiv(nkb, splits) * BK;
-  splits = cdiv(K, kps);
-  float* partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
-
-  if (g_impl == 1) {
-    dim3 grid(cdiv(M, 128), cdiv(N, 64), splits);
-    gemm_simt_kernel<VA, VB><<<grid, 256, 0, st>>>(va, vb, epi, partial, M, N, K, kps);
-  } else if (g_impl == 2) {
-    launch_tc_bn<SchemeTF32x3>(BN, va, vb, epi, partial, M, N, K, kps, splits, st);
-  } else {
-    launch_tc_bn<SchemeBF16x6>(BN, va, vb, epi, partial, M, N, K, kps, splits, st);
-  }
-  int rc = check_launch(what);
-  if (rc) return rc;
-  if (splits > 1) {
-    const size_t total = (size_t)M * N;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(partial, splits, M, N, epi);
-    rc = check_launch("splitk_reduce");
-  }
-  return rc;
-}
-
-Epilogue make_epi(float* out, int M, int N, uint32_t mdiv, long long ld_hi, long long ld_lo,
-                  long long ld_n, const float* bias, const float* mask, int relu) {
-  Epilogue e;
-  e.out = out;
-  e.M = M;
-  e.N = N;
-  e.d_m = FastDiv(mdiv);
-  e.ld_hi = ld_hi;
-  e.ld_lo = ld_lo;
-  e.ld_n = ld_n;
-  e.bias = bias;
-  e.mask = mask;
-  e.relu = relu;
-  return e;
-}
-
-constexpr uint32_t kRowMajor = 1u << 30;  // m / kRowMajor == 0 for every row index
+};
 
 // ---------------------------------------------------------------------------
-// elementwise / reduction kernels
+// fp32 reference-layout elementwise kernels
 // ---------------------------------------------------------------------------
 
 // tensor_core.py:183-198 -- first maximum in kh-major, kw-minor order
@@ -357,11 +289,113 @@ __global__ void vec_add_kernel(float* __restrict__ dst, const float* __restrict_
     dst[i] = __fadd_rn(dst[i], src[i]);
 }
 
-int grid_for(size_t n, int threads = 256) {
-  size_t b = (n + threads - 1) / threads;
-  const size_t cap = (size_t)num_sms() * 16;
-  if (b > cap) b = cap;
-  return b < 1 ? 1 : (int)b;
+
+
+// ---------------------------------------------------------------------------
+// split-plane GEMM dispatch
+// ---------------------------------------------------------------------------
+
+template <int BN, int BK, class VA, class VB, class EP>
+void launch_sg(const VA& va, const VB& vb, const EP& ep, float* partial, int M, int N, int K,
+               int kps, int splits, cudaStream_t st) {
+  using Cfg = SgCfg<BN, BK>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(sgemm_kernel<BN, BK, VA, VB, EP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr_set = true;
+  }
+  dim3 grid(cdiv(M, SG_BM), cdiv(N, BN), splits);
+  sgemm_kernel<BN, BK, VA, VB, EP><<<grid, SG_THREADS, Cfg::SMEM, st>>>(va, vb, ep, partial, M, N,
+                                                                          K, kps);
+}
+
+// C[M,N] = A(M,K) . B(K,N) over split-plane views; ep applied once.
+template <class VA, class VB, class EP>
+int run_sgemm(const char* what, const VA& va, const VB& vb, const EP& ep, int M, int N, int K,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return STZ_OK;
+  if (K <= 0) return fail(STZ_EINVAL, "%s: empty contraction (K=%d)", what, K);
+  const int BN = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  const int BK = BN == 256 ? 16 : 32;
+  const int tiles = cdiv(M, SG_BM) * cdiv(N, BN);
+  const int nkb = cdiv(K, BK);
+  const int npad = rup8(N);
+  const size_t per = (size_t)M * npad * sizeof(float);
+  const int fit = ws ? (int)(ws_bytes / per) : 1;
+  int splits = 1;
+  if (tiles < 2 * num_sms() && nkb >= 8) {
+    splits = cdiv(2 * num_sms(), tiles);
+    if (splits > nkb / 4) splits = nkb / 4;
+  }
+  if (g_max_kps > 0 && K > g_max_kps) splits = cdiv(K, g_max_kps);
+  if (splits > fit) splits = fit;
+  if (splits < 1) splits = 1;
+  const int kps = cdiv(nkb, splits) * BK;
+  splits = cdiv(K, kps);
+  float* partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
+  if (BN == 32) launch_sg<32, 32>(va, vb, ep, partial, M, N, K, kps, splits, st);
+  else if (BN == 64) launch_sg<64, 32>(va, vb, ep, partial, M, N, K, kps, splits, st);
+  else if (BN == 128) launch_sg<128, 32>(va, vb, ep, partial, M, N, K, kps, splits, st);
+  else launch_sg<256, 16>(va, vb, ep, partial, M, N, K, kps, splits, st);
+  int rc = check_launch(what);
+  if (rc) return rc;
+  if (splits > 1) {
+    const size_t total = (size_t)M * (npad / 8);
+    sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(partial, splits, M, N, ep);
+    rc = check_launch("sgemm_reduce");
+  }
+  return rc;
+}
+
+EpF32 ep_f32(float* out, int M, int N, uint32_t mdiv, long long ld_hi, long long ld_lo,
+             long long ld_n, const float* bias, const float* mask, int relu) {
+  EpF32 e;
+  e.out = out;
+  e.M = M;
+  e.N = N;
+  e.d_m = FastDiv(mdiv);
+  e.ld_hi = ld_hi;
+  e.ld_lo = ld_lo;
+  e.ld_n = ld_n;
+  e.bias = bias;
+  e.mask = mask;
+  e.relu = relu;
+  return e;
+}
+
+constexpr uint32_t kRowMajor = 1u << 30;  // m / kRowMajor == 0 for every row index
+
+// ---- op bodies shared by both ABI levels --------------------------------------------
+
+SvConvFwdA conv_fwd_A(const bf16_t* x, size_t ps, int N, int C8, int H, int W, int k, int s,
+                      int p, int OH, int OW) {
+  return SvConvFwdA{x, ps, N * OH * OW, k * k * C8, H, W, C8, OW, s, p,
+                    FastDiv(OH * OW), FastDiv(OW), FastDiv(C8), FastDiv(k)};
+}
+SvConvDgradA conv_dgrad_A(const bf16_t* g, size_t ps, int N, int H, int W, int O8, int k, int s,
+                          int p, int OH, int OW) {
+  return SvConvDgradA{g, ps, N * H * W, k * k * O8, OH, OW, O8, s, p,
+                      FastDiv(H * W), FastDiv(W), FastDiv(O8), FastDiv(k)};
+}
+SvConvWgradA conv_wgrad_A(const bf16_t* x, size_t ps, int N, int C8, int H, int W, int k, int s,
+                          int p, int OH, int OW) {
+  return SvConvWgradA{x, ps, k * k * C8, N * OH * OW, H, W, C8, OW, s, p,
+                      FastDiv(C8), FastDiv(k), FastDiv(OH * OW), FastDiv(OW)};
+}
+
+int colsum_split(const bf16_t* g, size_t ps, int R, int N, int ld, float* out, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  const int blocks = cdiv(R, CS_ROWS);
+  Carve cv(ws, ws_bytes);
+  double* part = cv.take<double>((size_t)blocks * N);
+  if (!part) return fail(STZ_EWORKSPACE, "colsum: workspace too small");
+  dim3 grid(blocks, cdiv(N, 256) > 8 ? 8 : cdiv(N, 256));
+  colsum_partial_kernel<<<grid, 256, 0, st>>>(g, ps, R, N, ld, part);
+  int rc = check_launch("colsum_partial");
+  if (rc) return rc;
+  colsum_final_kernel<<<cdiv(N, 256), 256, 0, st>>>(part, blocks, N, out);
+  return check_launch("colsum_final");
 }
 
 }  // namespace
@@ -371,17 +405,9 @@ int grid_for(size_t n, int threads = 256) {
 // ===========================================================================
 extern "C" {
 
-int stz_abi_version(void) { return 1; }
+int stz_abi_version(void) { return 2; }
 
 const char* stz_last_error(void) { return g_err.c_str(); }
-
-int stz_set_gemm_impl(int impl) {
-  if (impl < 0 || impl > 2) return fail(STZ_EINVAL, "gemm impl must be 0, 1 or 2, got %d", impl);
-  g_impl = impl;
-  return STZ_OK;
-}
-
-int stz_get_gemm_impl(void) { return g_impl; }
 
 unsigned long long stz_launch_count(void) { return g_launches; }
 
@@ -391,6 +417,10 @@ int stz_set_max_k_per_split(int k) {
   return STZ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// reference-layout operator contract
+// ---------------------------------------------------------------------------
+
 int stz_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int N, int C, int H,
                    int W, int O, int k, int s, int p, int relu, void* ws, size_t ws_bytes,
                    void* stream) {
@@ -398,12 +428,25 @@ int stz_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int
   if (N < 0 || C <= 0 || O <= 0 || k <= 0 || s <= 0 || p < 0 || OH <= 0 || OW <= 0)
     return fail(STZ_EINVAL, "conv2d_fwd: bad shape N=%d C=%d H=%d W=%d O=%d k=%d s=%d p=%d", N, C,
                 H, W, O, k, s, p);
-  const int M = N * OH * OW, K = C * k * k;
-  ViewIm2col va{x, M, K, C, H, W, OW, s, p, k,
-                FastDiv(OH * OW), FastDiv(OW), FastDiv(k * k), FastDiv(k)};
-  ViewRowK vb{w, O, K, K, (K % 4 == 0 && aligned16(w)) ? 1 : 0};
-  Epilogue e = make_epi(y, M, O, OH * OW, (long long)O * OH * OW, 1, OH * OW, b, nullptr, relu);
-  return run_gemm("conv2d_fwd", va, vb, e, M, O, K, ws, ws_bytes, as_stream(stream));
+  if (N == 0) return STZ_OK;
+  cudaStream_t st = as_stream(stream);
+  const int C8 = rup8(C), kk = k * k;
+  Carve cv(ws, ws_bytes);
+  const size_t psx = (size_t)N * H * W * C8, psw = (size_t)O * kk * C8;
+  bf16_t* xp = cv.take<bf16_t>(3 * psx);
+  bf16_t* wf = cv.take<bf16_t>(3 * psw);
+  if (!xp || !wf) return fail(STZ_EWORKSPACE, "conv2d_fwd: workspace too small");
+  pack_nchw_kernel<<<grid_for((size_t)N * H * W * C8 / 8), 256, 0, st>>>(x, xp, psx, N, C, H, W,
+                                                                         C8);
+  int rc = check_launch("pack_nchw");
+  if (rc) return rc;
+  pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, wf, psw, nullptr, 0, O, C, kk, C8, 0);
+  if ((rc = check_launch("pack_conv_w"))) return rc;
+  SvConvFwdA va = conv_fwd_A(xp, psx, N, C8, H, W, k, s, p, OH, OW);
+  SvRowsK vb{wf, psw, O, kk * C8, kk * C8};
+  EpF32 e = ep_f32(y, N * OH * OW, O, OH * OW, (long long)O * OH * OW, 1, OH * OW, b, nullptr,
+                   relu);
+  return run_sgemm("conv2d_fwd", va, vb, e, N * OH * OW, O, kk * C8, cv.p, cv.left, st);
 }
 
 int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int N,
@@ -412,12 +455,23 @@ int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float*
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (N < 0 || C <= 0 || O <= 0 || k <= 0 || s <= 0 || p < 0 || OH <= 0 || OW <= 0)
     return fail(STZ_EINVAL, "conv2d_bwd_data: bad shape");
-  const int M = N * H * W, K = O * k * k;
-  ViewDgradG va{gy, M, K, O, OH, OW, s, p, k,
-                FastDiv(H * W), FastDiv(W), FastDiv(k * k), FastDiv(k)};
-  ViewDgradW vb{w, C, K, k * k, FastDiv(k * k)};
-  Epilogue e = make_epi(gx, M, C, H * W, (long long)C * H * W, 1, H * W, nullptr, mask, 0);
-  return run_gemm("conv2d_bwd_data", va, vb, e, M, C, K, ws, ws_bytes, as_stream(stream));
+  if (N == 0) return STZ_OK;
+  cudaStream_t st = as_stream(stream);
+  const int O8 = rup8(O), kk = k * k;
+  Carve cv(ws, ws_bytes);
+  const size_t psg = (size_t)N * OH * OW * O8, psw = (size_t)C * kk * O8;
+  bf16_t* gp = cv.take<bf16_t>(3 * psg);
+  bf16_t* wd = cv.take<bf16_t>(3 * psw);
+  if (!gp || !wd) return fail(STZ_EWORKSPACE, "conv2d_bwd_data: workspace too small");
+  pack_nchw_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, N, O, OH, OW, O8);
+  int rc = check_launch("pack_nchw");
+  if (rc) return rc;
+  pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, nullptr, 0, wd, psw, O, C, kk, 0, O8);
+  if ((rc = check_launch("pack_conv_w"))) return rc;
+  SvConvDgradA va = conv_dgrad_A(gp, psg, N, H, W, O8, k, s, p, OH, OW);
+  SvRowsK vb{wd, psw, C, kk * O8, kk * O8};
+  EpF32 e = ep_f32(gx, N * H * W, C, H * W, (long long)C * H * W, 1, H * W, nullptr, mask, 0);
+  return run_sgemm("conv2d_bwd_data", va, vb, e, N * H * W, C, kk * O8, cv.p, cv.left, st);
 }
 
 int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb, int N, int C,
@@ -426,55 +480,93 @@ int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb,
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (N <= 0 || C <= 0 || O <= 0 || k <= 0 || s <= 0 || p < 0 || OH <= 0 || OW <= 0)
     return fail(STZ_EINVAL, "conv2d_bwd_filter: bad shape");
-  const int CKK = C * k * k, K = N * OH * OW;
   cudaStream_t st = as_stream(stream);
-  ViewWgradX va{x, CKK, K, C, H, W, OW, s, p, k,
-                FastDiv(k * k), FastDiv(k), FastDiv(OH * OW), FastDiv(OW)};
-  ViewWgradG vb{gy, O, K, OH * OW, FastDiv(OH * OW)};
-  // C[ckk, o] stored transposed into gw[o, ckk]
-  Epilogue e = make_epi(gw, CKK, O, kRowMajor, 0, 1, CKK, nullptr, nullptr, 0);
-  int rc = run_gemm("conv2d_bwd_filter", va, vb, e, CKK, O, K, ws, ws_bytes, st);
+  const int C8 = rup8(C), O8 = rup8(O), kk = k * k;
+  Carve cv(ws, ws_bytes);
+  const size_t psx = (size_t)N * H * W * C8, psg = (size_t)N * OH * OW * O8;
+  bf16_t* xp = cv.take<bf16_t>(3 * psx);
+  bf16_t* gp = cv.take<bf16_t>(3 * psg);
+  if (!xp || !gp) return fail(STZ_EWORKSPACE, "conv2d_bwd_filter: workspace too small");
+  pack_nchw_kernel<<<grid_for(psx / 8), 256, 0, st>>>(x, xp, psx, N, C, H, W, C8);
+  int rc = check_launch("pack_nchw");
   if (rc) return rc;
-  if (gb) {
-    conv_bias_grad_kernel<<<O, 256, 0, st>>>(gy, gb, N, O, OH * OW);
-    rc = check_launch("conv_bias_grad");
-  }
-  return rc;
+  pack_nchw_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, N, O, OH, OW, O8);
+  if ((rc = check_launch("pack_nchw"))) return rc;
+  SvConvWgradA va = conv_wgrad_A(xp, psx, N, C8, H, W, k, s, p, OH, OW);
+  SvRowsMN vb{gp, psg, O, N * OH * OW, O8};
+  EpConvWgrad e{gw, kk * C8, O, C, kk, FastDiv(C8)};
+  rc = run_sgemm("conv2d_bwd_filter", va, vb, e, kk * C8, O, N * OH * OW, cv.p, cv.left, st);
+  if (rc || !gb) return rc;
+  conv_bias_grad_kernel<<<O, 256, 0, st>>>(gy, gb, N, O, OH * OW);
+  return check_launch("conv_bias_grad");
 }
 
 int stz_fc_fwd(const float* x, const float* w, const float* b, float* y, int M, int in_dim,
                int out_dim, int relu, void* ws, size_t ws_bytes, void* stream) {
   if (M < 0 || in_dim <= 0 || out_dim <= 0) return fail(STZ_EINVAL, "fc_fwd: bad shape");
-  ViewRowK va{x, M, in_dim, in_dim, (in_dim % 4 == 0 && aligned16(x)) ? 1 : 0};
-  ViewColK vb{w, out_dim, in_dim, out_dim};
-  Epilogue e = make_epi(y, M, out_dim, kRowMajor, 0, out_dim, 1, b, nullptr, relu);
-  return run_gemm("fc_fwd", va, vb, e, M, out_dim, in_dim, ws, ws_bytes, as_stream(stream));
+  if (M == 0) return STZ_OK;
+  cudaStream_t st = as_stream(stream);
+  const int I8 = rup8(in_dim), O8 = rup8(out_dim);
+  Carve cv(ws, ws_bytes);
+  const size_t psx = (size_t)M * I8, psw = (size_t)in_dim * O8;
+  bf16_t* xp = cv.take<bf16_t>(3 * psx);
+  bf16_t* wp = cv.take<bf16_t>(3 * psw);
+  if (!xp || !wp) return fail(STZ_EWORKSPACE, "fc_fwd: workspace too small");
+  pack_rows_kernel<<<grid_for(psx / 8), 256, 0, st>>>(x, xp, psx, M, in_dim, I8);
+  int rc = check_launch("pack_rows");
+  if (rc) return rc;
+  pack_rows_kernel<<<grid_for(psw / 8), 256, 0, st>>>(w, wp, psw, in_dim, out_dim, O8);
+  if ((rc = check_launch("pack_rows"))) return rc;
+  SvRowsK va{xp, psx, M, I8, I8};
+  SvRowsMN vb{wp, psw, out_dim, in_dim, O8};
+  EpF32 e = ep_f32(y, M, out_dim, kRowMajor, 0, out_dim, 1, b, nullptr, relu);
+  return run_sgemm("fc_fwd", va, vb, e, M, out_dim, I8, cv.p, cv.left, st);
 }
 
 int stz_fc_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int M,
                     int in_dim, int out_dim, void* ws, size_t ws_bytes, void* stream) {
   if (M < 0 || in_dim <= 0 || out_dim <= 0) return fail(STZ_EINVAL, "fc_bwd_data: bad shape");
-  ViewRowK va{gy, M, out_dim, out_dim, (out_dim % 4 == 0 && aligned16(gy)) ? 1 : 0};
-  ViewRowK vb{w, in_dim, out_dim, out_dim, (out_dim % 4 == 0 && aligned16(w)) ? 1 : 0};
-  Epilogue e = make_epi(gx, M, in_dim, kRowMajor, 0, in_dim, 1, nullptr, mask, 0);
-  return run_gemm("fc_bwd_data", va, vb, e, M, in_dim, out_dim, ws, ws_bytes,
-                  as_stream(stream));
+  if (M == 0) return STZ_OK;
+  cudaStream_t st = as_stream(stream);
+  const int O8 = rup8(out_dim);
+  Carve cv(ws, ws_bytes);
+  const size_t psg = (size_t)M * O8, psw = (size_t)in_dim * O8;
+  bf16_t* gp = cv.take<bf16_t>(3 * psg);
+  bf16_t* wp = cv.take<bf16_t>(3 * psw);
+  if (!gp || !wp) return fail(STZ_EWORKSPACE, "fc_bwd_data: workspace too small");
+  pack_rows_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, M, out_dim, O8);
+  int rc = check_launch("pack_rows");
+  if (rc) return rc;
+  pack_rows_kernel<<<grid_for(psw / 8), 256, 0, st>>>(w, wp, psw, in_dim, out_dim, O8);
+  if ((rc = check_launch("pack_rows"))) return rc;
+  SvRowsK va{gp, psg, M, O8, O8};
+  SvRowsK vb{wp, psw, in_dim, O8, O8};
+  EpF32 e = ep_f32(gx, M, in_dim, kRowMajor, 0, in_dim, 1, nullptr, mask, 0);
+  return run_sgemm("fc_bwd_data", va, vb, e, M, in_dim, O8, cv.p, cv.left, st);
 }
 
 int stz_fc_bwd_weight(const float* x, const float* gy, float* gw, float* gb, int M, int in_dim,
                       int out_dim, void* ws, size_t ws_bytes, void* stream) {
   if (M <= 0 || in_dim <= 0 || out_dim <= 0) return fail(STZ_EINVAL, "fc_bwd_weight: bad shape");
   cudaStream_t st = as_stream(stream);
-  ViewColK va{x, in_dim, M, in_dim};
-  ViewColK vb{gy, out_dim, M, out_dim};
-  Epilogue e = make_epi(gw, in_dim, out_dim, kRowMajor, 0, out_dim, 1, nullptr, nullptr, 0);
-  int rc = run_gemm("fc_bwd_weight", va, vb, e, in_dim, out_dim, M, ws, ws_bytes, st);
+  const int I8 = rup8(in_dim), O8 = rup8(out_dim);
+  Carve cv(ws, ws_bytes);
+  const size_t psx = (size_t)M * I8, psg = (size_t)M * O8;
+  bf16_t* xp = cv.take<bf16_t>(3 * psx);
+  bf16_t* gp = cv.take<bf16_t>(3 * psg);
+  if (!xp || !gp) return fail(STZ_EWORKSPACE, "fc_bwd_weight: workspace too small");
+  pack_rows_kernel<<<grid_for(psx / 8), 256, 0, st>>>(x, xp, psx, M, in_dim, I8);
+  int rc = check_launch("pack_rows");
   if (rc) return rc;
-  if (gb) {
-    fc_bias_grad_kernel<<<cdiv(out_dim, 256), 256, 0, st>>>(gy, gb, M, out_dim);
-    rc = check_launch("fc_bias_grad");
-  }
-  return rc;
+  pack_rows_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, M, out_dim, O8);
+  if ((rc = check_launch("pack_rows"))) return rc;
+  SvRowsMN va{xp, psx, in_dim, M, I8};
+  SvRowsMN vb{gp, psg, out_dim, M, O8};
+  EpF32 e = ep_f32(gw, in_dim, out_dim, kRowMajor, 0, out_dim, 1, nullptr, nullptr, 0);
+  rc = run_sgemm("fc_bwd_weight", va, vb, e, in_dim, out_dim, M, cv.p, cv.left, st);
+  if (rc || !gb) return rc;
+  fc_bias_grad_kernel<<<cdiv(out_dim, 256), 256, 0, st>>>(gy, gb, M, out_dim);
+  return check_launch("fc_bias_grad");
 }
 
 int stz_maxpool2d_fwd(const float* x, float* y, uint8_t* arg, int N, int C, int H, int W, int k,
@@ -538,6 +630,195 @@ int stz_vec_add(float* dst, const float* src, size_t n, void* stream) {
   if (n == 0) return STZ_OK;
   vec_add_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(dst, src, n);
   return check_launch("vec_add");
+}
+
+// ---------------------------------------------------------------------------
+// hot path on split-plane tensors (p = plane 0, ps = plane stride in elements)
+// ---------------------------------------------------------------------------
+
+int stzx_pack_nchw(const float* x, void* xp, size_t ps, int N, int C, int H, int W, int C8,
+                   void* stream) {
+  if (C8 % 8 || C8 < C) return fail(STZ_EINVAL, "pack_nchw: C8 must be a multiple of 8 >= C");
+  const size_t total = (size_t)N * H * W * C8 / 8;
+  if (total == 0) return STZ_OK;
+  pack_nchw_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(x, mb(xp), ps, N, C, H, W, C8);
+  return check_launch("pack_nchw");
+}
+
+int stzx_unpack_nhwc(const void* xp, size_t ps, float* x, int N, int C, int H, int W, int C8,
+                     void* stream) {
+  const size_t total = (size_t)N * C * H * W;
+  if (total == 0) return STZ_OK;
+  unpack_nhwc_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(cb(xp), ps, x, N, C, H, W,
+                                                                      C8);
+  return check_launch("unpack_nhwc");
+}
+
+int stzx_pack_rows(const float* x, void* xp, size_t ps, int M, int D, int D8, void* stream) {
+  if (D8 % 8 || D8 < D) return fail(STZ_EINVAL, "pack_rows: D8 must be a multiple of 8 >= D");
+  const size_t total = (size_t)M * D8 / 8;
+  if (total == 0) return STZ_OK;
+  pack_rows_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(x, mb(xp), ps, M, D, D8);
+  return check_launch("pack_rows");
+}
+
+int stzx_unpack_rows(const void* xp, size_t ps, float* x, int M, int D, int D8, void* stream) {
+  const size_t total = (size_t)M * D;
+  if (total == 0) return STZ_OK;
+  unpack_rows_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(cb(xp), ps, x, M, D, D8);
+  return check_launch("unpack_rows");
+}
+
+int stzx_pack_conv_w(const float* w, void* wf, size_t psf, void* wd, size_t psd, int O, int C,
+                     int k, int C8, int O8, void* stream) {
+  const size_t nf = wf ? (size_t)O * k * k * C8 : 0, nd = wd ? (size_t)C * k * k * O8 : 0;
+  if (nf + nd == 0) return STZ_OK;
+  // the kernel walks [nf | nd); a null target contributes an empty range
+  pack_conv_w_kernel<<<grid_for(nf + nd), 256, 0, as_stream(stream)>>>(
+      w, mb(wf), psf, mb(wd), psd, O, C, k * k, wf ? C8 : 0, wd ? O8 : 0);
+  return check_launch("pack_conv_w");
+}
+
+int stzx_conv_fwd(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
+                  void* y, size_t psy, int N, int C8, int H, int W, int O, int O8, int k, int s,
+                  int p, int relu, void* ws, size_t ws_bytes, void* stream) {
+  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8 || O8 < O) return fail(STZ_EINVAL, "conv_fwd: bad shape");
+  SvConvFwdA va = conv_fwd_A(cb(x), psx, N, C8, H, W, k, s, p, OH, OW);
+  SvRowsK vb{cb(wf), psw, O, k * k * C8, k * k * C8};
+  EpSplit e{mb(y), psy, N * OH * OW, O, O8, bias, nullptr, relu};
+  return run_sgemm("conv_fwd", va, vb, e, N * OH * OW, O, k * k * C8, ws, ws_bytes,
+                   as_stream(stream));
+}
+
+int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
+                    const void* mask, int N, int C, int C8, int H, int W, int O8, int k, int s,
+                    int p, void* ws, size_t ws_bytes, void* stream) {
+  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_dgrad: bad shape");
+  SvConvDgradA va = conv_dgrad_A(cb(g), psg, N, H, W, O8, k, s, p, OH, OW);
+  SvRowsK vb{cb(wd), psw, C, k * k * O8, k * k * O8};
+  EpSplit e{mb(gx), psgx, N * H * W, C, C8, nullptr, cb(mask), 0};
+  return run_sgemm("conv_dgrad", va, vb, e, N * H * W, C, k * k * O8, ws, ws_bytes,
+                   as_stream(stream));
+}
+
+int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
+                    int N, int C, int C8, int H, int W, int O, int O8, int k, int s, int p,
+                    void* ws, size_t ws_bytes, void* stream) {
+  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad: bad shape");
+  cudaStream_t st = as_stream(stream);
+  SvConvWgradA va = conv_wgrad_A(cb(x), psx, N, C8, H, W, k, s, p, OH, OW);
+  SvRowsMN vb{cb(g), psg, O, N * OH * OW, O8};
+  EpConvWgrad e{gw, k * k * C8, O, C, k * k, FastDiv(C8)};
+  int rc = run_sgemm("conv_wgrad", va, vb, e, k * k * C8, O, N * OH * OW, ws, ws_bytes, st);
+  if (rc || !gb) return rc;
+  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st);
+}
+
+int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const float* bias, void* y,
+                size_t psy, float* y_f32, int M, int in_dim, int in8, int out_dim, int out8,
+                int relu, void* ws, size_t ws_bytes, void* stream) {
+  if (in8 % 8 || out8 % 8 || in8 < in_dim || out8 < out_dim) return fail(STZ_EINVAL, "fc_fwd: bad shape");
+  SvRowsK va{cb(x), psx, M, in8, in8};
+  SvRowsMN vb{cb(w), psw, out_dim, in_dim, out8};
+  if (y) {
+    EpSplit e{mb(y), psy, M, out_dim, out8, bias, nullptr, relu};
+    return run_sgemm("fc_fwd", va, vb, e, M, out_dim, in8, ws, ws_bytes, as_stream(stream));
+  }
+  EpF32 e = ep_f32(y_f32, M, out_dim, kRowMajor, 0, out_dim, 1, bias, nullptr, relu);
+  return run_sgemm("fc_fwd", va, vb, e, M, out_dim, in8, ws, ws_bytes, as_stream(stream));
+}
+
+int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx, size_t psgx,
+                  const void* mask, int M, int in_dim, int in8, int out8, void* ws,
+                  size_t ws_bytes, void* stream) {
+  if (in8 % 8 || out8 % 8 || in8 < in_dim) return fail(STZ_EINVAL, "fc_dgrad: bad shape");
+  SvRowsK va{cb(g), psg, M, out8, out8};
+  SvRowsK vb{cb(w), psw, in_dim, out8, out8};
+  EpSplit e{mb(gx), psgx, M, in_dim, in8, nullptr, cb(mask), 0};
+  return run_sgemm("fc_dgrad", va, vb, e, M, in_dim, out8, ws, ws_bytes, as_stream(stream));
+}
+
+int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
+                  int M, int in_dim, int in8, int out_dim, int out8, void* ws, size_t ws_bytes,
+                  void* stream) {
+  if (in8 % 8 || out8 % 8) return fail(STZ_EINVAL, "fc_wgrad: bad shape");
+  cudaStream_t st = as_stream(stream);
+  SvRowsMN va{cb(x), psx, in_dim, M, in8};
+  SvRowsMN vb{cb(g), psg, out_dim, M, out8};
+  EpF32 e = ep_f32(gw, in_dim, out_dim, kRowMajor, 0, out_dim, 1, nullptr, nullptr, 0);
+  int rc = run_sgemm("fc_wgrad", va, vb, e, in_dim, out_dim, M, ws, ws_bytes, st);
+  if (rc || !gb) return rc;
+  return colsum_split(cb(g), psg, M, out_dim, out8, gb, ws, ws_bytes, st);
+}
+
+int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
+                     int C8, int H, int W, int k, int s, int flat_ld, void* stream) {
+  const int OH = (H - k) / s + 1, OW = (W - k) / s + 1;
+  if (k <= 0 || s <= 0 || OH <= 0 || OW <= 0 || k * k > 256)
+    return fail(STZ_EINVAL, "maxpool_fwd: bad shape");
+  cudaStream_t st = as_stream(stream);
+  const size_t total = (size_t)N * OH * OW * C8;
+  if (total == 0) return STZ_OK;
+  if (flat_ld > C * OH * OW) {
+    zero_flat_tail_kernel<<<grid_for((size_t)N * (flat_ld - C * OH * OW)), 256, 0, st>>>(
+        mb(y), psy, N, C * OH * OW, flat_ld);
+    int rc = check_launch("zero_flat_tail");
+    if (rc) return rc;
+  }
+  maxpool_fwd_split_kernel<<<grid_for(total), 256, 0, st>>>(cb(x), psx, mb(y), psy, arg, N, C, C8,
+                                                             H, W, k, s, OH, OW, flat_ld);
+  return check_launch("maxpool_fwd");
+}
+
+int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, size_t psx,
+                     const void* mask, int N, int C, int C8, int H, int W, int k, int s,
+                     int flat_ld, void* stream) {
+  const int OH = (H - k) / s + 1, OW = (W - k) / s + 1;
+  if (k <= 0 || s <= 0 || OH <= 0 || OW <= 0) return fail(STZ_EINVAL, "maxpool_bwd: bad shape");
+  const size_t total = (size_t)N * H * W * C8;
+  if (total == 0) return STZ_OK;
+  maxpool_bwd_split_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      cb(gy), psg, arg, mb(gx), psx, cb(mask), N, C, C8, H, W, k, s, OH, OW, flat_ld);
+  return check_launch("maxpool_bwd");
+}
+
+int stzx_relu_fwd(const void* x, size_t psx, void* y, size_t psy, size_t n, void* stream) {
+  if (n == 0) return STZ_OK;
+  relu_fwd_split_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(cb(x), psx, mb(y), psy, n);
+  return check_launch("relu_fwd_split");
+}
+
+int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t psx, size_t n,
+                  void* stream) {
+  if (n == 0) return STZ_OK;
+  relu_bwd_split_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(cb(gy), psg, cb(src), mb(gx),
+                                                                     psx, n);
+  return check_launch("relu_bwd_split");
+}
+
+int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
+                    int M, int C, int C8, void* stream) {
+  if (M <= 0 || C <= 0 || C8 < C) return fail(STZ_EINVAL, "softmax_ce: bad shape");
+  softmax_ce_split_kernel<<<M, 256, 0, as_stream(stream)>>>(logits, labels, losses, mb(dz), psd, C,
+                                                             C8);
+  return check_launch("softmax_ce_split");
+}
+
+int stzx_nhwc_to_flat(const void* x, size_t psx, void* y, size_t psy, int N, int C, int H, int W,
+                      int C8, int D8, void* stream) {
+  nhwc_to_flat_kernel<<<grid_for((size_t)N * D8), 256, 0, as_stream(stream)>>>(
+      cb(x), psx, mb(y), psy, N, C, H, W, C8, D8);
+  return check_launch("nhwc_to_flat");
+}
+
+int stzx_flat_to_nhwc(const void* y, size_t psy, void* x, size_t psx, int N, int C, int H, int W,
+                      int C8, int D8, void* stream) {
+  flat_to_nhwc_kernel<<<grid_for((size_t)N * H * W * C8), 256, 0, as_stream(stream)>>>(
+      cb(y), psy, mb(x), psx, N, C, H, W, C8, D8);
+  return check_launch("flat_to_nhwc");
 }
 
 }  // extern "C"

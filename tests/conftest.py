@@ -20,11 +20,3 @@ def lib():
     from paper_1812_10624_b200 import _lib
     build_library()
     return _lib.load()
-
-
-@pytest.fixture(params=[0, 1, 2], ids=["tcgen05-bf16x6", "simt", "tcgen05-tf32x3"])
-def gemm_impl(request, lib):
-    """Run a GPU test under both GEMM cores; restore the product core after."""
-    lib.stz_set_gemm_impl(request.param)
-    yield request.param
-    lib.stz_set_gemm_impl(0)

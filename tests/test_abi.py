@@ -20,10 +20,10 @@ def test_header_symbols_exported(lib):
 
 
 def test_version_and_control_calls(lib):
-    assert lib.stz_abi_version() == 1
-    assert lib.stz_set_gemm_impl(7) == 1               # invalid -> ShapeMismatch code
-    assert b"gemm impl" in lib.stz_last_error()
-    assert lib.stz_set_gemm_impl(0) == 0 and lib.stz_get_gemm_impl() == 0
+    assert lib.stz_abi_version() == 2
+    assert lib.stz_set_max_k_per_split(-1) == 1         # invalid -> ShapeMismatch code
+    assert b"max_k_per_split" in lib.stz_last_error()
+    assert lib.stz_set_max_k_per_split(0) == 0
 
 
 def test_sm100a_code_in_library(lib):
