@@ -178,19 +178,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def gemm_flops(name, a):
-    """Algorithmic FLOPs of one GEMM-class ABI call from its size arguments."""
-    ints = [v for v in a if isinstance(v, int)]
-    if name.startswith("stz_conv2d"):
-        n, c, h, w, o, k, s, p = ints[:8]
-        oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
-        return 2.0 * n * oh * ow * o * c * k * k
-    if name.startswith("stz_fc"):
-        m, i, o = ints[:3]
-        return 2.0 * m * i * o
-    return 0.0
-
-
 class CallTimer:
     """PROFILE_HOOK for paper_1812_10624_b200._lib: CUDA events around each
     ABI call on the launching (current) stream."""
@@ -200,14 +187,13 @@ class CallTimer:
         self.records = []
 
     @contextmanager
-    def __call__(self, name, args):
+    def __call__(self, name, args, flops=0.0, tag=None):
         t = self.torch
         e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
         e0.record()
         yield
         e1.record()
-        key = (name, tuple(v for v in args if isinstance(v, int))[:8])
-        self.records.append((key, e0, e1))
+        self.records.append(((tag or name, float(flops)), e0, e1))
 
     def table(self):
         self.torch.cuda.synchronize()
@@ -370,14 +356,16 @@ def main():
     for key, (tot, cnt) in calls.items():
         if tot > top[0]:
             top_key, top = key, (tot, cnt)
-    fl = gemm_flops(top_key[0], top_key[1]) if top_key else 0.0
+    fl = top_key[1] if top_key else 0.0
     avg_ms = top[0] / max(top[1], 1)
     achieved = fl / (avg_ms / 1e3) / 1e12 if avg_ms > 0 and fl > 0 else 0.0
-    kernel_key = f"{top_key[0]}{list(top_key[1])}" if top_key else None
+    kernel_key = f"{args.model}:{top_key[0]}" if top_key else None
     step_ms_sum = sum(tot for tot, _ in calls.values())
-    fc_fl = sum(gemm_flops(kk[0], kk[1]) * c for kk, (_, c) in calls.items()
-                if kk[0].startswith("stz_fc"))
-    fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("stz_fc"))
+    fc_fl = sum(kk[1] * c for kk, (_, c) in calls.items() if kk[0].startswith("fc"))
+    fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("fc"))
+    per_call = {f"{kk[0]}": {"ms": tot / max(c, 1), "tflops": (kk[1] / (tot / max(c, 1) / 1e3) / 1e12)
+                             if kk[1] and tot else None}
+                for kk, (tot, c) in sorted(calls.items(), key=lambda kv: -kv[1][0])}
     fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None
     roofline = {
         "bound": "tensor", "kernel": kernel_key, "achieved": achieved, "peak": bf16_peak,
@@ -390,6 +378,7 @@ def main():
                  "occupancy is 6*frac and the scheme's own ceiling is frac = 1/6"),
         "tensor_pipe_frac": 6 * achieved / bf16_peak if bf16_peak else None,
         "share_of_step": top[0] / step_ms_sum if step_ms_sum else None,
+        "calls": per_call,
     }
 
     line = None

@@ -39,6 +39,11 @@ const char* stz_last_error(void);
 /* Number of kernels this library has launched (bench evidence). */
 unsigned long long stz_launch_count(void);
 
+/* GEMM producer: 1 (default) = TMA (tiled / im2col tensor maps) where the
+ * shapes allow it, 0 = the cp.async gather kernel for every GEMM (the GPU
+ * tests run both and compare). */
+int stz_set_tma(int on);
+
 /* Tuning/experiment knob: cap the K extent one CTA accumulates (0 = auto). */
 int stz_set_max_k_per_split(int k);
 

@@ -26,6 +26,7 @@ SIGNATURES = {
     "stz_abi_version": (I, []),
     "stz_last_error": (ctypes.c_char_p, []),
     "stz_set_max_k_per_split": (I, [I]),
+    "stz_set_tma": (I, [I]),
     "stz_launch_count": (ctypes.c_ulonglong, []),
     "stz_conv2d_fwd": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stz_conv2d_bwd_data": (I, [P, P, P, P, I, I, I, I, I, I, I, I, P, Z, P]),
@@ -105,11 +106,12 @@ def load(path: str | None = None):
 PROFILE_HOOK = None
 
 
-def call(name: str, *args) -> None:
-    """Invoke an ABI function and raise on a non-zero status."""
+def call(name: str, *args, flops: float = 0.0, tag: str | None = None) -> None:
+    """Invoke an ABI function and raise on a non-zero status.  ``flops`` /
+    ``tag`` (algorithmic FLOPs, layer label) are only seen by PROFILE_HOOK."""
     lib = load()
     if PROFILE_HOOK is not None:
-        with PROFILE_HOOK(name, args):
+        with PROFILE_HOOK(name, args, flops, tag):
             rc = getattr(lib, name)(*args)
     else:
         rc = getattr(lib, name)(*args)

@@ -55,33 +55,31 @@ class RoleComm:
 
     # -- exchanges --------------------------------------------------------------------
 
-    def gather_activations(self, acts: torch.Tensor | None, labels: torch.Tensor | None,
-                           fc_in: torch.Tensor | None, fc_labels: torch.Tensor | None,
-                           k: int) -> None:
-        """CONV side passes (acts [K,A], labels [K]); FC side passes its input
-        buffers ([g*K, A], [g*K]) and receives every member's block in place."""
+    def gather_activations(self, send: list | None, recv: list | None, k: int = 0) -> None:
+        """CONV side: ``send`` = tensors of its [K, ...] block (the three
+        split planes and the labels).  FC side: ``recv[pos]`` = matching
+        tensors (row slices of its input buffers) for member ``pos``, which
+        are received in place -- ascending CONV order, zero-copy concat."""
         ops = []
         if self.is_conv:
             dst = self.fc_rank_of(self.index)
-            ops += [dist.P2POp(dist.isend, acts, dst), dist.P2POp(dist.isend, labels, dst)]
+            ops += [dist.P2POp(dist.isend, t, dst) for t in send]
         else:
             for pos, i in enumerate(self.members(self.index)):
-                rows = slice(pos * k, (pos + 1) * k)
-                ops += [dist.P2POp(dist.irecv, fc_in[rows], i),
-                        dist.P2POp(dist.irecv, fc_labels[rows], i)]
+                ops += [dist.P2POp(dist.irecv, t, i) for t in recv[pos]]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
 
-    def scatter_boundary(self, gx: torch.Tensor | None, gy: torch.Tensor | None,
-                         k: int) -> None:
-        """FC side sends rows [pos*K, (pos+1)*K) of gx to member pos; the CONV
-        side receives its [K, A] boundary gradient into gy."""
+    def scatter_boundary(self, send: list | None, recv: list | None, k: int = 0) -> None:
+        """FC side: ``send[pos]`` = row slices of its boundary gradient for
+        member ``pos``; CONV side: ``recv`` = its [K, ...] gradient tensors."""
         ops = []
         if self.is_conv:
-            ops.append(dist.P2POp(dist.irecv, gy, self.fc_rank_of(self.index)))
+            src = self.fc_rank_of(self.index)
+            ops += [dist.P2POp(dist.irecv, t, src) for t in recv]
         else:
             for pos, i in enumerate(self.members(self.index)):
-                ops.append(dist.P2POp(dist.isend, gx[pos * k:(pos + 1) * k], i))
+                ops += [dist.P2POp(dist.isend, t, i) for t in send[pos]]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
 

@@ -17,6 +17,11 @@
 #include <string>
 
 #include "stz_fmt.cuh"
+#include "stz_tma.cuh"
+
+#include <cuda.h>
+#include <mutex>
+#include <unordered_map>
 #include "../../include/stanza_b200.h"
 
 using namespace stz;
@@ -348,6 +353,199 @@ int run_sgemm(const char* what, const VA& va, const VB& vb, const EP& ep, int M,
   return rc;
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA operands (tensor maps via the driver entry points, cached)
+// ---------------------------------------------------------------------------
+
+typedef CUresult (*EncTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*EncIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+EncTiledFn g_enc_tiled = nullptr;
+EncIm2colFn g_enc_im2col = nullptr;
+int g_use_tma = 1;
+std::unordered_map<std::string, CUtensorMap> g_map_cache;
+
+bool tma_ready() {
+  if (g_enc_tiled && g_enc_im2col) return true;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_enc_tiled),
+                              cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    g_enc_tiled = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", reinterpret_cast<void**>(&g_enc_im2col),
+                              cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    g_enc_im2col = nullptr;
+  return g_enc_tiled && g_enc_im2col;
+}
+
+template <class... T>
+std::string cache_key(T... v) {
+  std::string k;
+  const long long vals[] = {static_cast<long long>(v)...};
+  k.assign(reinterpret_cast<const char*>(vals), sizeof(vals));
+  return k;
+}
+
+bool enc_tiled(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
+               uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+  const std::string key = cache_key(0, (uintptr_t)base, inner, outer, ld_elems, box_inner, box_outer);
+  auto it = g_map_cache.find(key);
+  if (it != g_map_cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  g_map_cache.emplace(key, *out);
+  return true;
+}
+
+bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8, int s, int lo,
+                int hi, int pixels) {
+  const std::string key = cache_key(1, (uintptr_t)base, N, H, W, C8, s, lo, hi, pixels);
+  auto it = g_map_cache.find(key);
+  if (it != g_map_cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)C8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C8 * 2, (cuuint64_t)W * C8 * 2, (cuuint64_t)H * W * C8 * 2};
+  int lower[2] = {lo, lo}, upper[2] = {hi, hi};
+  cuuint32_t es[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
+  CUresult r = g_enc_im2col(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                            strides, lower, upper, 32, (cuuint32_t)pixels, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  g_map_cache.emplace(key, *out);
+  return true;
+}
+
+// [rows][K] planes, K contiguous (row stride ld), tile of R rows
+bool op_tiled_k(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int ld, int R) {
+  op = TgOperand{};
+  op.mode = TG_TILED_K;
+  op.nbox = 1;
+  for (int pl = 0; pl < 3; ++pl)
+    if (!enc_tiled(&op.map[pl], p + pl * ps, (uint64_t)K, (uint64_t)rows, (uint64_t)ld, 32,
+                   (uint32_t)R))
+      return false;
+  return true;
+}
+
+// [K][rows] planes, rows contiguous (row stride ld), tile of R rows (R % 32 == 0)
+bool op_tiled_mn(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int ld, int R) {
+  op = TgOperand{};
+  op.mode = TG_TILED_MN;
+  op.nbox = R / 32;
+  for (int pl = 0; pl < 3; ++pl)
+    if (!enc_tiled(&op.map[pl], p + pl * ps, (uint64_t)rows, (uint64_t)K, (uint64_t)ld, 32, 32))
+      return false;
+  return true;
+}
+
+// NHWC [N][H][W][C8] planes read as im2col; output grid OHxOW enumerates the
+// window starts (oh*s + lo, ow*s + lo); taps (th, tw) are TMA offsets
+bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H, int W, int C8,
+               int ksz, int s, int lo, int hi, int OH, int OW, int R) {
+  op = TgOperand{};
+  op.mode = mn ? TG_IM2COL_MN : TG_IM2COL_K;
+  op.nbox = mn ? R / 32 : 1;
+  op.lo = lo;
+  op.s = s;
+  op.C8 = C8;
+  op.ksz = ksz;
+  op.d_ohw = FastDiv(OH * OW);
+  op.d_ow = FastDiv(OW);
+  op.d_c8 = FastDiv(C8);
+  op.d_k = FastDiv(ksz);
+  for (int pl = 0; pl < 3; ++pl)
+    if (!enc_im2col(&op.map[pl], p + pl * ps, N, H, W, C8, s, lo, hi, mn ? 32 : 128))
+      return false;
+  return true;
+}
+
+// tile width: 64 for thin outputs, 96 when N is a multiple of 96 but not of
+// 128 (192, 384 channels), else 128 (TMEM holds two sets of 2*BN columns)
+int tg_pick_bn(int N) {
+  if (N <= 64) return 64;
+  if (N % 96 == 0 && N % 128 != 0) return 96;
+  return 128;
+}
+
+template <int BN, class EP>
+void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
+  using Cfg = TgCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tgemm_kernel<BN, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM);
+    attr_set = true;
+  }
+  const int items = cdiv(prm.M, TG_BM) * cdiv(prm.N, BN) * splits;
+  const int grid = items < num_sms() ? items : num_sms();
+  tgemm_kernel<BN, EP><<<grid, TG_THREADS, Cfg::SMEM, st>>>(prm);
+}
+
+// C[M,N] = A . B with TMA operands built for tile width BN
+template <class EP>
+int run_tgemm(const char* what, int BN, const TgOperand& a, const TgOperand& b, const EP& ep,
+              int M, int N, int K, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return STZ_OK;
+  const int tiles = cdiv(M, TG_BM) * cdiv(N, BN);
+  const int nkb = cdiv(K, TG_BK);
+  const int npad = rup8(N);
+  const size_t per = (size_t)M * npad * sizeof(float);
+  const int fit = ws ? (int)(ws_bytes / per) : 1;
+  int splits = 1;
+  if (tiles < 2 * num_sms() && nkb >= 8) {
+    splits = cdiv(2 * num_sms(), tiles);
+    if (splits > nkb / 4) splits = nkb / 4;
+  }
+  if (g_max_kps > 0 && K > g_max_kps) splits = cdiv(K, g_max_kps);
+  if (splits > fit) splits = fit;
+  if (splits < 1) splits = 1;
+  const int kps = cdiv(nkb, splits) * TG_BK;
+  splits = cdiv(K, kps);
+  TgParams<EP> prm;
+  prm.a = a;
+  prm.b = b;
+  prm.ep = ep;
+  prm.partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
+  prm.M = M;
+  prm.N = N;
+  prm.K = K;
+  prm.k_per_split = kps;
+  if (BN == 64) launch_tg<64>(prm, splits, st);
+  else if (BN == 96) launch_tg<96>(prm, splits, st);
+  else launch_tg<128>(prm, splits, st);
+  int rc = check_launch(what);
+  if (rc) return rc;
+  if (splits > 1) {
+    const size_t total = (size_t)M * (npad / 8);
+    sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(prm.partial, splits, M, N, ep);
+    rc = check_launch("tgemm_reduce");
+  }
+  return rc;
+}
+
+bool tma_on() { return g_use_tma && tma_ready(); }
+
 EpF32 ep_f32(float* out, int M, int N, uint32_t mdiv, long long ld_hi, long long ld_lo,
              long long ld_n, const float* bias, const float* mask, int relu) {
   EpF32 e;
@@ -384,17 +582,120 @@ SvConvWgradA conv_wgrad_A(const bf16_t* x, size_t ps, int N, int C8, int H, int 
                       FastDiv(C8), FastDiv(k), FastDiv(OH * OW), FastDiv(OW)};
 }
 
+
+// ---- GEMM-class ops: TMA kernel when the shapes allow, cp.async kernel otherwise ----
+
+template <class EP>
+int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, const EP& ep, int N,
+                  int C8, int H, int W, int O, int k, int s, int p, int OH, int OW, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  const int M = N * OH * OW, K = k * k * C8;
+  if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
+    const int BN = tg_pick_bn(O);
+    TgOperand a, b;
+    if (op_im2col(a, false, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
+        op_tiled_k(b, wf, psw, O, K, K, BN))
+      return run_tgemm("conv_fwd[tma]", BN, a, b, ep, M, O, K, ws, ws_bytes, st);
+  }
+  SvConvFwdA va = conv_fwd_A(x, psx, N, C8, H, W, k, s, p, OH, OW);
+  SvRowsK vb{wf, psw, O, K, K};
+  return run_sgemm("conv_fwd", va, vb, ep, M, O, K, ws, ws_bytes, st);
+}
+
+template <class EP>
+int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, const EP& ep,
+                    int N, int C, int H, int W, int O8, int k, int s, int p, int OH, int OW,
+                    void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int M = N * H * W, K = k * k * O8;
+  if (tma_on() && O8 % 32 == 0 && s == 1 && p - (k - 1) >= -128 && p <= 127) {
+    const int BN = tg_pick_bn(C);
+    TgOperand a, b;
+    if (op_im2col(a, false, g, psg, N, OH, OW, O8, k, 1, p - (k - 1), -p, H, W, TG_BM) &&
+        op_tiled_k(b, wd, psw, C, K, K, BN))
+      return run_tgemm("conv_dgrad[tma]", BN, a, b, ep, M, C, K, ws, ws_bytes, st);
+  }
+  SvConvDgradA va = conv_dgrad_A(g, psg, N, H, W, O8, k, s, p, OH, OW);
+  SvRowsK vb{wd, psw, C, K, K};
+  return run_sgemm("conv_dgrad", va, vb, ep, M, C, K, ws, ws_bytes, st);
+}
+
+template <class EP>
+int gemm_conv_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, const EP& ep, int N,
+                    int C8, int H, int W, int O, int O8, int k, int s, int p, int OH, int OW,
+                    void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int M = k * k * C8, P = N * OH * OW;
+  if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128) {
+    const int BN = tg_pick_bn(O);
+    TgOperand a, b;
+    if (op_im2col(a, true, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
+        op_tiled_mn(b, g, psg, O, P, O8, BN))
+      return run_tgemm("conv_wgrad[tma]", BN, a, b, ep, M, O, P, ws, ws_bytes, st);
+  }
+  SvConvWgradA va = conv_wgrad_A(x, psx, N, C8, H, W, k, s, p, OH, OW);
+  SvRowsMN vb{g, psg, O, P, O8};
+  return run_sgemm("conv_wgrad", va, vb, ep, M, O, P, ws, ws_bytes, st);
+}
+
+template <class EP>
+int gemm_fc_fwd(const bf16_t* x, size_t psx, const bf16_t* w, size_t psw, const EP& ep, int M,
+                int in_dim, int I8, int out_dim, int O8, void* ws, size_t ws_bytes,
+                cudaStream_t st) {
+  if (tma_on()) {
+    const int BN = tg_pick_bn(out_dim);
+    TgOperand a, b;
+    if (op_tiled_k(a, x, psx, M, I8, I8, TG_BM) && op_tiled_mn(b, w, psw, out_dim, in_dim, O8, BN))
+      return run_tgemm("fc_fwd[tma]", BN, a, b, ep, M, out_dim, I8, ws, ws_bytes, st);
+  }
+  SvRowsK va{x, psx, M, I8, I8};
+  SvRowsMN vb{w, psw, out_dim, in_dim, O8};
+  return run_sgemm("fc_fwd", va, vb, ep, M, out_dim, I8, ws, ws_bytes, st);
+}
+
+template <class EP>
+int gemm_fc_dgrad(const bf16_t* g, size_t psg, const bf16_t* w, size_t psw, const EP& ep, int M,
+                  int in_dim, int O8, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (tma_on()) {
+    const int BN = tg_pick_bn(in_dim);
+    TgOperand a, b;
+    if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM) && op_tiled_k(b, w, psw, in_dim, O8, O8, BN))
+      return run_tgemm("fc_dgrad[tma]", BN, a, b, ep, M, in_dim, O8, ws, ws_bytes, st);
+  }
+  SvRowsK va{g, psg, M, O8, O8};
+  SvRowsK vb{w, psw, in_dim, O8, O8};
+  return run_sgemm("fc_dgrad", va, vb, ep, M, in_dim, O8, ws, ws_bytes, st);
+}
+
+template <class EP>
+int gemm_fc_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, const EP& ep, int M,
+                  int in_dim, int I8, int out_dim, int O8, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  if (tma_on()) {
+    const int BN = tg_pick_bn(out_dim);
+    TgOperand a, b;
+    if (op_tiled_mn(a, x, psx, in_dim, M, I8, TG_BM) &&
+        op_tiled_mn(b, g, psg, out_dim, M, O8, BN))
+      return run_tgemm("fc_wgrad[tma]", BN, a, b, ep, in_dim, out_dim, M, ws, ws_bytes, st);
+  }
+  SvRowsMN va{x, psx, in_dim, M, I8};
+  SvRowsMN vb{g, psg, out_dim, M, O8};
+  return run_sgemm("fc_wgrad", va, vb, ep, in_dim, out_dim, M, ws, ws_bytes, st);
+}
+
 int colsum_split(const bf16_t* g, size_t ps, int R, int N, int ld, float* out, void* ws,
                  size_t ws_bytes, cudaStream_t st) {
-  const int blocks = cdiv(R, CS_ROWS);
+  const int N8 = rup8(N);
+  const int chunks = N8 / 8;
+  const int lanes = chunks < 256 ? 256 / chunks : 1;
+  int rpb = cdiv(R, 4 * num_sms());
+  rpb = cdiv(rpb < 4 * lanes ? 4 * lanes : rpb, lanes) * lanes;
+  const int blocks = cdiv(R, rpb);
   Carve cv(ws, ws_bytes);
-  double* part = cv.take<double>((size_t)blocks * N);
+  double* part = cv.take<double>((size_t)blocks * N8);
   if (!part) return fail(STZ_EWORKSPACE, "colsum: workspace too small");
-  dim3 grid(blocks, cdiv(N, 256) > 8 ? 8 : cdiv(N, 256));
-  colsum_partial_kernel<<<grid, 256, 0, st>>>(g, ps, R, N, ld, part);
+  colsum_partial_kernel<<<blocks, 256, 0, st>>>(g, ps, R, N8, ld, rpb, part);
   int rc = check_launch("colsum_partial");
   if (rc) return rc;
-  colsum_final_kernel<<<cdiv(N, 256), 256, 0, st>>>(part, blocks, N, out);
+  colsum_final_kernel<<<cdiv(N, 256), 256, 0, st>>>(part, blocks, N, N8, out);
   return check_launch("colsum_final");
 }
 
@@ -410,6 +711,11 @@ int stz_abi_version(void) { return 2; }
 const char* stz_last_error(void) { return g_err.c_str(); }
 
 unsigned long long stz_launch_count(void) { return g_launches; }
+
+int stz_set_tma(int on) {
+  g_use_tma = on ? 1 : 0;
+  return STZ_OK;
+}
 
 int stz_set_max_k_per_split(int k) {
   if (k < 0) return fail(STZ_EINVAL, "max_k_per_split must be >= 0");
@@ -436,17 +742,15 @@ int stz_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int
   bf16_t* xp = cv.take<bf16_t>(3 * psx);
   bf16_t* wf = cv.take<bf16_t>(3 * psw);
   if (!xp || !wf) return fail(STZ_EWORKSPACE, "conv2d_fwd: workspace too small");
-  pack_nchw_kernel<<<grid_for((size_t)N * H * W * C8 / 8), 256, 0, st>>>(x, xp, psx, N, C, H, W,
-                                                                         C8);
+  pack_nchw_kernel<<<grid_for((size_t)N * H * W * C8 / 8), 256, 0, st>>>(
+      x, xp, psx, N, C, H, W, C8, FastDiv(C8 / 8), FastDiv(H * W));
   int rc = check_launch("pack_nchw");
   if (rc) return rc;
-  pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, wf, psw, nullptr, 0, O, C, kk, C8, 0);
+  pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, wf, psw, nullptr, 0, O, C, kk, C8, 0, k);
   if ((rc = check_launch("pack_conv_w"))) return rc;
-  SvConvFwdA va = conv_fwd_A(xp, psx, N, C8, H, W, k, s, p, OH, OW);
-  SvRowsK vb{wf, psw, O, kk * C8, kk * C8};
   EpF32 e = ep_f32(y, N * OH * OW, O, OH * OW, (long long)O * OH * OW, 1, OH * OW, b, nullptr,
                    relu);
-  return run_sgemm("conv2d_fwd", va, vb, e, N * OH * OW, O, kk * C8, cv.p, cv.left, st);
+  return gemm_conv_fwd(xp, psx, wf, psw, e, N, C8, H, W, O, k, s, p, OH, OW, cv.p, cv.left, st);
 }
 
 int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int N,
@@ -463,15 +767,14 @@ int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float*
   bf16_t* gp = cv.take<bf16_t>(3 * psg);
   bf16_t* wd = cv.take<bf16_t>(3 * psw);
   if (!gp || !wd) return fail(STZ_EWORKSPACE, "conv2d_bwd_data: workspace too small");
-  pack_nchw_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, N, O, OH, OW, O8);
+  pack_nchw_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, N, O, OH, OW, O8,
+                                                      FastDiv(O8 / 8), FastDiv(OH * OW));
   int rc = check_launch("pack_nchw");
   if (rc) return rc;
-  pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, nullptr, 0, wd, psw, O, C, kk, 0, O8);
+  pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, nullptr, 0, wd, psw, O, C, kk, 0, O8, k);
   if ((rc = check_launch("pack_conv_w"))) return rc;
-  SvConvDgradA va = conv_dgrad_A(gp, psg, N, H, W, O8, k, s, p, OH, OW);
-  SvRowsK vb{wd, psw, C, kk * O8, kk * O8};
   EpF32 e = ep_f32(gx, N * H * W, C, H * W, (long long)C * H * W, 1, H * W, nullptr, mask, 0);
-  return run_sgemm("conv2d_bwd_data", va, vb, e, N * H * W, C, kk * O8, cv.p, cv.left, st);
+  return gemm_conv_dgrad(gp, psg, wd, psw, e, N, C, H, W, O8, k, s, p, OH, OW, cv.p, cv.left, st);
 }
 
 int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb, int N, int C,
@@ -487,15 +790,15 @@ int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb,
   bf16_t* xp = cv.take<bf16_t>(3 * psx);
   bf16_t* gp = cv.take<bf16_t>(3 * psg);
   if (!xp || !gp) return fail(STZ_EWORKSPACE, "conv2d_bwd_filter: workspace too small");
-  pack_nchw_kernel<<<grid_for(psx / 8), 256, 0, st>>>(x, xp, psx, N, C, H, W, C8);
+  pack_nchw_kernel<<<grid_for(psx / 8), 256, 0, st>>>(x, xp, psx, N, C, H, W, C8,
+                                                      FastDiv(C8 / 8), FastDiv(H * W));
   int rc = check_launch("pack_nchw");
   if (rc) return rc;
-  pack_nchw_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, N, O, OH, OW, O8);
+  pack_nchw_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, N, O, OH, OW, O8,
+                                                      FastDiv(O8 / 8), FastDiv(OH * OW));
   if ((rc = check_launch("pack_nchw"))) return rc;
-  SvConvWgradA va = conv_wgrad_A(xp, psx, N, C8, H, W, k, s, p, OH, OW);
-  SvRowsMN vb{gp, psg, O, N * OH * OW, O8};
   EpConvWgrad e{gw, kk * C8, O, C, kk, FastDiv(C8)};
-  rc = run_sgemm("conv2d_bwd_filter", va, vb, e, kk * C8, O, N * OH * OW, cv.p, cv.left, st);
+  rc = gemm_conv_wgrad(xp, psx, gp, psg, e, N, C8, H, W, O, O8, k, s, p, OH, OW, cv.p, cv.left, st);
   if (rc || !gb) return rc;
   conv_bias_grad_kernel<<<O, 256, 0, st>>>(gy, gb, N, O, OH * OW);
   return check_launch("conv_bias_grad");
@@ -517,10 +820,8 @@ int stz_fc_fwd(const float* x, const float* w, const float* b, float* y, int M, 
   if (rc) return rc;
   pack_rows_kernel<<<grid_for(psw / 8), 256, 0, st>>>(w, wp, psw, in_dim, out_dim, O8);
   if ((rc = check_launch("pack_rows"))) return rc;
-  SvRowsK va{xp, psx, M, I8, I8};
-  SvRowsMN vb{wp, psw, out_dim, in_dim, O8};
   EpF32 e = ep_f32(y, M, out_dim, kRowMajor, 0, out_dim, 1, b, nullptr, relu);
-  return run_sgemm("fc_fwd", va, vb, e, M, out_dim, I8, cv.p, cv.left, st);
+  return gemm_fc_fwd(xp, psx, wp, psw, e, M, in_dim, I8, out_dim, O8, cv.p, cv.left, st);
 }
 
 int stz_fc_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int M,
@@ -539,10 +840,8 @@ int stz_fc_bwd_data(const float* gy, const float* w, float* gx, const float* mas
   if (rc) return rc;
   pack_rows_kernel<<<grid_for(psw / 8), 256, 0, st>>>(w, wp, psw, in_dim, out_dim, O8);
   if ((rc = check_launch("pack_rows"))) return rc;
-  SvRowsK va{gp, psg, M, O8, O8};
-  SvRowsK vb{wp, psw, in_dim, O8, O8};
   EpF32 e = ep_f32(gx, M, in_dim, kRowMajor, 0, in_dim, 1, nullptr, mask, 0);
-  return run_sgemm("fc_bwd_data", va, vb, e, M, in_dim, O8, cv.p, cv.left, st);
+  return gemm_fc_dgrad(gp, psg, wp, psw, e, M, in_dim, O8, cv.p, cv.left, st);
 }
 
 int stz_fc_bwd_weight(const float* x, const float* gy, float* gw, float* gb, int M, int in_dim,
@@ -560,10 +859,8 @@ int stz_fc_bwd_weight(const float* x, const float* gy, float* gw, float* gb, int
   if (rc) return rc;
   pack_rows_kernel<<<grid_for(psg / 8), 256, 0, st>>>(gy, gp, psg, M, out_dim, O8);
   if ((rc = check_launch("pack_rows"))) return rc;
-  SvRowsMN va{xp, psx, in_dim, M, I8};
-  SvRowsMN vb{gp, psg, out_dim, M, O8};
   EpF32 e = ep_f32(gw, in_dim, out_dim, kRowMajor, 0, out_dim, 1, nullptr, nullptr, 0);
-  rc = run_sgemm("fc_bwd_weight", va, vb, e, in_dim, out_dim, M, cv.p, cv.left, st);
+  rc = gemm_fc_wgrad(xp, psx, gp, psg, e, M, in_dim, I8, out_dim, O8, cv.p, cv.left, st);
   if (rc || !gb) return rc;
   fc_bias_grad_kernel<<<cdiv(out_dim, 256), 256, 0, st>>>(gy, gb, M, out_dim);
   return check_launch("fc_bias_grad");
@@ -641,7 +938,8 @@ int stzx_pack_nchw(const float* x, void* xp, size_t ps, int N, int C, int H, int
   if (C8 % 8 || C8 < C) return fail(STZ_EINVAL, "pack_nchw: C8 must be a multiple of 8 >= C");
   const size_t total = (size_t)N * H * W * C8 / 8;
   if (total == 0) return STZ_OK;
-  pack_nchw_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(x, mb(xp), ps, N, C, H, W, C8);
+  pack_nchw_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      x, mb(xp), ps, N, C, H, W, C8, FastDiv(C8 / 8), FastDiv(H * W));
   return check_launch("pack_nchw");
 }
 
@@ -675,7 +973,7 @@ int stzx_pack_conv_w(const float* w, void* wf, size_t psf, void* wd, size_t psd,
   if (nf + nd == 0) return STZ_OK;
   // the kernel walks [nf | nd); a null target contributes an empty range
   pack_conv_w_kernel<<<grid_for(nf + nd), 256, 0, as_stream(stream)>>>(
-      w, mb(wf), psf, mb(wd), psd, O, C, k * k, wf ? C8 : 0, wd ? O8 : 0);
+      w, mb(wf), psf, mb(wd), psd, O, C, k * k, wf ? C8 : 0, wd ? O8 : 0, k);
   return check_launch("pack_conv_w");
 }
 
@@ -684,11 +982,9 @@ int stzx_conv_fwd(const void* x, size_t psx, const void* wf, size_t psw, const f
                   int p, int relu, void* ws, size_t ws_bytes, void* stream) {
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8 || O8 < O) return fail(STZ_EINVAL, "conv_fwd: bad shape");
-  SvConvFwdA va = conv_fwd_A(cb(x), psx, N, C8, H, W, k, s, p, OH, OW);
-  SvRowsK vb{cb(wf), psw, O, k * k * C8, k * k * C8};
   EpSplit e{mb(y), psy, N * OH * OW, O, O8, bias, nullptr, relu};
-  return run_sgemm("conv_fwd", va, vb, e, N * OH * OW, O, k * k * C8, ws, ws_bytes,
-                   as_stream(stream));
+  return gemm_conv_fwd(cb(x), psx, cb(wf), psw, e, N, C8, H, W, O, k, s, p, OH, OW, ws, ws_bytes,
+                       as_stream(stream));
 }
 
 int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
@@ -696,11 +992,9 @@ int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void*
                     int p, void* ws, size_t ws_bytes, void* stream) {
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_dgrad: bad shape");
-  SvConvDgradA va = conv_dgrad_A(cb(g), psg, N, H, W, O8, k, s, p, OH, OW);
-  SvRowsK vb{cb(wd), psw, C, k * k * O8, k * k * O8};
   EpSplit e{mb(gx), psgx, N * H * W, C, C8, nullptr, cb(mask), 0};
-  return run_sgemm("conv_dgrad", va, vb, e, N * H * W, C, k * k * O8, ws, ws_bytes,
-                   as_stream(stream));
+  return gemm_conv_dgrad(cb(g), psg, cb(wd), psw, e, N, C, H, W, O8, k, s, p, OH, OW, ws,
+                         ws_bytes, as_stream(stream));
 }
 
 int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
@@ -709,10 +1003,9 @@ int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float*
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad: bad shape");
   cudaStream_t st = as_stream(stream);
-  SvConvWgradA va = conv_wgrad_A(cb(x), psx, N, C8, H, W, k, s, p, OH, OW);
-  SvRowsMN vb{cb(g), psg, O, N * OH * OW, O8};
   EpConvWgrad e{gw, k * k * C8, O, C, k * k, FastDiv(C8)};
-  int rc = run_sgemm("conv_wgrad", va, vb, e, k * k * C8, O, N * OH * OW, ws, ws_bytes, st);
+  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, C8, H, W, O, O8, k, s, p, OH, OW, ws,
+                           ws_bytes, st);
   if (rc || !gb) return rc;
   return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st);
 }
@@ -721,24 +1014,23 @@ int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const floa
                 size_t psy, float* y_f32, int M, int in_dim, int in8, int out_dim, int out8,
                 int relu, void* ws, size_t ws_bytes, void* stream) {
   if (in8 % 8 || out8 % 8 || in8 < in_dim || out8 < out_dim) return fail(STZ_EINVAL, "fc_fwd: bad shape");
-  SvRowsK va{cb(x), psx, M, in8, in8};
-  SvRowsMN vb{cb(w), psw, out_dim, in_dim, out8};
   if (y) {
     EpSplit e{mb(y), psy, M, out_dim, out8, bias, nullptr, relu};
-    return run_sgemm("fc_fwd", va, vb, e, M, out_dim, in8, ws, ws_bytes, as_stream(stream));
+    return gemm_fc_fwd(cb(x), psx, cb(w), psw, e, M, in_dim, in8, out_dim, out8, ws, ws_bytes,
+                       as_stream(stream));
   }
   EpF32 e = ep_f32(y_f32, M, out_dim, kRowMajor, 0, out_dim, 1, bias, nullptr, relu);
-  return run_sgemm("fc_fwd", va, vb, e, M, out_dim, in8, ws, ws_bytes, as_stream(stream));
+  return gemm_fc_fwd(cb(x), psx, cb(w), psw, e, M, in_dim, in8, out_dim, out8, ws, ws_bytes,
+                     as_stream(stream));
 }
 
 int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx, size_t psgx,
                   const void* mask, int M, int in_dim, int in8, int out8, void* ws,
                   size_t ws_bytes, void* stream) {
   if (in8 % 8 || out8 % 8 || in8 < in_dim) return fail(STZ_EINVAL, "fc_dgrad: bad shape");
-  SvRowsK va{cb(g), psg, M, out8, out8};
-  SvRowsK vb{cb(w), psw, in_dim, out8, out8};
   EpSplit e{mb(gx), psgx, M, in_dim, in8, nullptr, cb(mask), 0};
-  return run_sgemm("fc_dgrad", va, vb, e, M, in_dim, out8, ws, ws_bytes, as_stream(stream));
+  return gemm_fc_dgrad(cb(g), psg, cb(w), psw, e, M, in_dim, out8, ws, ws_bytes,
+                       as_stream(stream));
 }
 
 int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
@@ -746,10 +1038,9 @@ int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* g
                   void* stream) {
   if (in8 % 8 || out8 % 8) return fail(STZ_EINVAL, "fc_wgrad: bad shape");
   cudaStream_t st = as_stream(stream);
-  SvRowsMN va{cb(x), psx, in_dim, M, in8};
-  SvRowsMN vb{cb(g), psg, out_dim, M, out8};
   EpF32 e = ep_f32(gw, in_dim, out_dim, kRowMajor, 0, out_dim, 1, nullptr, nullptr, 0);
-  int rc = run_sgemm("fc_wgrad", va, vb, e, in_dim, out_dim, M, ws, ws_bytes, st);
+  int rc = gemm_fc_wgrad(cb(x), psx, cb(g), psg, e, M, in_dim, in8, out_dim, out8, ws, ws_bytes,
+                         st);
   if (rc || !gb) return rc;
   return colsum_split(cb(g), psg, M, out_dim, out8, gb, ws, ws_bytes, st);
 }
@@ -760,7 +1051,7 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
   if (k <= 0 || s <= 0 || OH <= 0 || OW <= 0 || k * k > 256)
     return fail(STZ_EINVAL, "maxpool_fwd: bad shape");
   cudaStream_t st = as_stream(stream);
-  const size_t total = (size_t)N * OH * OW * C8;
+  const size_t total = (size_t)N * OH * OW * C8 / 8;
   if (total == 0) return STZ_OK;
   if (flat_ld > C * OH * OW) {
     zero_flat_tail_kernel<<<grid_for((size_t)N * (flat_ld - C * OH * OW)), 256, 0, st>>>(
@@ -769,7 +1060,9 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
     if (rc) return rc;
   }
   maxpool_fwd_split_kernel<<<grid_for(total), 256, 0, st>>>(cb(x), psx, mb(y), psy, arg, N, C, C8,
-                                                             H, W, k, s, OH, OW, flat_ld);
+                                                             H, W, k, s, OH, OW, flat_ld,
+                                                             FastDiv(C8 / 8), FastDiv(OW),
+                                                             FastDiv(OH));
   return check_launch("maxpool_fwd");
 }
 
@@ -778,10 +1071,11 @@ int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, s
                      int flat_ld, void* stream) {
   const int OH = (H - k) / s + 1, OW = (W - k) / s + 1;
   if (k <= 0 || s <= 0 || OH <= 0 || OW <= 0) return fail(STZ_EINVAL, "maxpool_bwd: bad shape");
-  const size_t total = (size_t)N * H * W * C8;
+  const size_t total = (size_t)N * H * W * C8 / 8;
   if (total == 0) return STZ_OK;
   maxpool_bwd_split_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
-      cb(gy), psg, arg, mb(gx), psx, cb(mask), N, C, C8, H, W, k, s, OH, OW, flat_ld);
+      cb(gy), psg, arg, mb(gx), psx, cb(mask), N, C, C8, H, W, k, s, OH, OW, flat_ld,
+      FastDiv(C8 / 8), FastDiv(W), FastDiv(H));
   return check_launch("maxpool_bwd");
 }
 

@@ -19,21 +19,20 @@ namespace stz {
 
 // fp32 NCHW -> NHWC split planes (channels padded to C8 with zeros)
 __global__ void pack_nchw_kernel(const float* __restrict__ x, bf16_t* __restrict__ xp, size_t ps,
-                                 int N, int C, int H, int W, int C8) {
-  const int chunks = C8 / 8;
-  const size_t total = (size_t)N * H * W * chunks;
-  STZ_GRID_LOOP(i, total) {
-    const int cc = (int)(i % chunks);
-    const size_t pix = i / chunks;  // (n, h, w)
-    const int hw = (int)(pix % ((size_t)H * W));
-    const size_t n = pix / ((size_t)H * W);
+                                 int N, int C, int H, int W, int C8, FastDiv d_chunks,
+                                 FastDiv d_hw) {
+  const uint32_t total = (uint32_t)N * H * W * (C8 / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t pix, cc, n, hw;
+    d_chunks.divmod(i, pix, cc);  // pix = (n, h, w)
+    d_hw.divmod(pix, n, hw);
     float v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = cc * 8 + j;
-      v[j] = c < C ? x[(n * C + c) * H * W + hw] : 0.f;
+      const int c = (int)cc * 8 + j;
+      v[j] = c < C ? __ldg(x + ((size_t)n * C + c) * H * W + hw) : 0.f;
     }
-    store_split8(xp + pix * C8 + cc * 8, ps, v);
+    store_split8(xp + (size_t)pix * C8 + cc * 8, ps, v);
   }
 }
 
@@ -75,11 +74,13 @@ __global__ void unpack_rows_kernel(const bf16_t* __restrict__ xp, size_t ps, flo
   }
 }
 
-// conv W [O, C, k, k] -> forward B planes wf[O][tap][C8] and input-gradient
-// B planes wd[C][tap][O8]  (tap = kh*k + kw; zeros in the channel padding)
+// conv W [O, C, k, k] -> forward B planes wf[O][tap][C8] (tap = kh*k + kw)
+// and input-gradient B planes wd[C][t][O8] with FLIPPED taps
+// t = (k-1-kh)*k + (k-1-kw), the order in which the input gradient walks
+// the output-gradient window (zeros in the channel padding)
 __global__ void pack_conv_w_kernel(const float* __restrict__ w, bf16_t* __restrict__ wf,
                                    size_t psf, bf16_t* __restrict__ wd, size_t psd, int O, int C,
-                                   int kk, int C8, int O8) {
+                                   int kk, int C8, int O8, int ksz) {
   const size_t nf = (size_t)O * kk * C8, nd = (size_t)C * kk * O8;
   STZ_GRID_LOOP(i, nf + nd) {
     if (i < nf) {
@@ -90,8 +91,9 @@ __global__ void pack_conv_w_kernel(const float* __restrict__ w, bf16_t* __restri
     } else {
       const size_t j = i - nf;
       const int o = (int)(j % O8);
-      const int tap = (int)((j / O8) % kk);
+      const int t = (int)((j / O8) % kk);
       const int c = (int)(j / ((size_t)O8 * kk));
+      const int tap = kk - 1 - t;  // (k-1-th)*k + (k-1-tw)
       store_split(wd, psd, j, o < O ? w[((size_t)o * C + c) * kk + tap] : 0.f);
     }
   }
@@ -134,38 +136,72 @@ __global__ void flat_to_nhwc_kernel(const bf16_t* __restrict__ y, size_t psy, bf
   }
 }
 
-// max-pool forward on NHWC split planes.  Output NHWC [N][OH][OW][C8]
-// (flat_ld == 0) or CHW-flat [N][flat_ld] (the FC-block input, reference
-// flatten order).  arg (uint8, kh*k+kw of the first maximum) is indexed
-// NHWC [N][OH][OW][C8] in both modes.
+// 8-channel vector helpers on split planes (16-byte aligned chunks)
+__device__ __forceinline__ void load_split8(const bf16_t* p, size_t ps, float (&v)[8]) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p);
+  const uint4 b = *reinterpret_cast<const uint4*>(p + ps);
+  const uint4 c = *reinterpret_cast<const uint4*>(p + 2 * ps);
+  const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w},
+                 cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[2 * j] = join3((bf16_t)(aw[j] & 0xFFFF), (bf16_t)(bw[j] & 0xFFFF), (bf16_t)(cw[j] & 0xFFFF));
+    v[2 * j + 1] = join3((bf16_t)(aw[j] >> 16), (bf16_t)(bw[j] >> 16), (bf16_t)(cw[j] >> 16));
+  }
+}
+
+// max-pool forward on NHWC split planes, one thread per (output pixel, 8
+// channels).  Output NHWC [N][OH][OW][C8] (flat_ld == 0) or CHW-flat
+// [N][flat_ld] (the FC-block input, reference flatten order).  arg (uint8,
+// kh*k+kw of the FIRST maximum, scanning kh-major / kw-minor) is indexed NHWC
+// [N][OH][OW][C8] in both modes.
 __global__ void maxpool_fwd_split_kernel(const bf16_t* __restrict__ x, size_t psx,
                                          bf16_t* __restrict__ y, size_t psy,
                                          uint8_t* __restrict__ arg, int N, int C, int C8, int H,
-                                         int W, int k, int s, int OH, int OW, int flat_ld) {
-  STZ_GRID_LOOP(i, (size_t)N * OH * OW * C8) {
-    const int c = (int)(i % C8);
-    const size_t opix = i / C8;
-    const int ow = (int)(opix % OW), oh = (int)((opix / OW) % OH);
-    const size_t n = opix / ((size_t)OH * OW);
-    float best = 0.f;
-    int bi = 0;
-    if (c < C) {
-      const size_t base = ((n * H + (size_t)oh * s) * W + (size_t)ow * s) * C8 + c;
-      best = load_split(x, psx, base);
-      for (int kh = 0; kh < k; ++kh)
-        for (int kw = 0; kw < k; ++kw) {
-          const float v = load_split(x, psx, base + ((size_t)kh * W + kw) * C8);
-          if (v > best) {
-            best = v;
-            bi = kh * k + kw;
+                                         int W, int k, int s, int OH, int OW, int flat_ld,
+                                         FastDiv d_ch, FastDiv d_ow, FastDiv d_oh) {
+  const uint32_t total = (uint32_t)N * OH * OW * (C8 / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t opix, cc, t, ow, n, oh;
+    d_ch.divmod(i, opix, cc);
+    d_ow.divmod(opix, t, ow);
+    d_oh.divmod(t, n, oh);
+    const size_t base = (((size_t)n * H + (size_t)oh * s) * W + (size_t)ow * s) * C8 + cc * 8;
+    float best[8];
+    int bi[8];
+    load_split8(x + base, psx, best);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bi[j] = 0;
+    for (int kh = 0; kh < k; ++kh)
+      for (int kw = 0; kw < k; ++kw) {
+        if ((kh | kw) == 0) continue;
+        float v[8];
+        load_split8(x + base + ((size_t)kh * W + kw) * C8, psx, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v[j] > best[j]) {
+            best[j] = v[j];
+            bi[j] = kh * k + kw;
           }
-        }
-    }
-    arg[i] = (uint8_t)bi;
+      }
+    const size_t o = (size_t)opix * C8 + cc * 8;
+    uint2 packed;
+    packed.x = (uint32_t)bi[0] | ((uint32_t)bi[1] << 8) | ((uint32_t)bi[2] << 16) |
+               ((uint32_t)bi[3] << 24);
+    packed.y = (uint32_t)bi[4] | ((uint32_t)bi[5] << 8) | ((uint32_t)bi[6] << 16) |
+               ((uint32_t)bi[7] << 24);
+    *reinterpret_cast<uint2*>(arg + o) = packed;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if ((int)(cc * 8 + j) >= C) best[j] = 0.f;
     if (flat_ld == 0) {
-      store_split(y, psy, i, best);
-    } else if (c < C) {
-      store_split(y, psy, n * flat_ld + ((size_t)c * OH + oh) * OW + ow, best);
+      store_split8(y + o, psy, best);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = (int)cc * 8 + j;
+        if (c < C) store_split(y, psy, (size_t)n * flat_ld + ((size_t)c * OH + oh) * OW + ow, best[j]);
+      }
     }
   }
 }
@@ -178,38 +214,66 @@ __global__ void zero_flat_tail_kernel(bf16_t* __restrict__ y, size_t psy, int N,
   }
 }
 
-// max-pool backward, gather form: every input cell (NHWC) sums in float64,
-// in the reference's (kh, kw) order, the output gradients whose argmax it
-// was; gy is NHWC (flat_ld == 0) or CHW-flat.  mask = plane 0 of the pool
-// input when a ReLU fed the pool (its backward fused here).
+// max-pool backward, gather form, one thread per (input pixel, 8 channels):
+// every input cell sums in float64, in the reference's (kh, kw) order, the
+// output gradients whose argmax it was; gy is NHWC (flat_ld == 0) or
+// CHW-flat.  mask = plane 0 of the pool input when a ReLU fed the pool (its
+// backward fused here).
 __global__ void maxpool_bwd_split_kernel(const bf16_t* __restrict__ gy, size_t psg,
                                          const uint8_t* __restrict__ arg,
                                          bf16_t* __restrict__ gx, size_t psx,
                                          const bf16_t* __restrict__ mask, int N, int C, int C8,
                                          int H, int W, int k, int s, int OH, int OW,
-                                         int flat_ld) {
-  STZ_GRID_LOOP(i, (size_t)N * H * W * C8) {
-    const int c = (int)(i % C8);
-    const size_t pix = i / C8;
-    const int w = (int)(pix % W), h = (int)((pix / W) % H);
-    const size_t n = pix / ((size_t)H * W);
-    double acc = 0.0;
-    if (c < C) {
-      const int th = h - k + 1, tw = w - k + 1;
-      const int oh_lo = th <= 0 ? 0 : (th + s - 1) / s, ow_lo = tw <= 0 ? 0 : (tw + s - 1) / s;
-      const int oh_hi = min(OH - 1, h / s), ow_hi = min(OW - 1, w / s);
-      for (int oh = oh_hi; oh >= oh_lo; --oh)
-        for (int ow = ow_hi; ow >= ow_lo; --ow) {
-          const size_t o = ((n * OH + oh) * OW + ow) * C8 + c;
-          if (arg[o] == (uint8_t)((h - oh * s) * k + (w - ow * s))) {
-            const size_t gi = flat_ld == 0 ? o : n * flat_ld + ((size_t)c * OH + oh) * OW + ow;
-            acc += (double)load_split(gy, psg, gi);
+                                         int flat_ld, FastDiv d_ch, FastDiv d_w, FastDiv d_h) {
+  const uint32_t total = (uint32_t)N * H * W * (C8 / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t pix, cc, t, w, n, h;
+    d_ch.divmod(i, pix, cc);
+    d_w.divmod(pix, t, w);
+    d_h.divmod(t, n, h);
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    const int th = (int)h - k + 1, tw = (int)w - k + 1;
+    const int oh_lo = th <= 0 ? 0 : (th + s - 1) / s, ow_lo = tw <= 0 ? 0 : (tw + s - 1) / s;
+    const int oh_hi = min(OH - 1, (int)h / s), ow_hi = min(OW - 1, (int)w / s);
+    for (int oh = oh_hi; oh >= oh_lo; --oh)
+      for (int ow = ow_hi; ow >= ow_lo; --ow) {
+        const size_t o = (((size_t)n * OH + oh) * OW + ow) * C8 + cc * 8;
+        const uint2 a2 = *reinterpret_cast<const uint2*>(arg + o);
+        const uint32_t want = (uint32_t)(((int)h - oh * s) * k + ((int)w - ow * s));
+        float g[8];
+        if (flat_ld == 0) {
+          load_split8(gy + o, psg, g);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = (int)cc * 8 + j;
+            g[j] = c < C ? load_split(gy, psg,
+                                      (size_t)n * flat_ld + ((size_t)c * OH + oh) * OW + ow)
+                         : 0.f;
           }
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t aj = ((j < 4 ? a2.x : a2.y) >> (8 * (j & 3))) & 0xFFu;
+          if (aj == want) acc[j] += (double)g[j];
+        }
+      }
+    const size_t xi = (size_t)pix * C8 + cc * 8;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (int)(cc * 8 + j) < C ? (float)acc[j] : 0.f;
+    if (mask) {
+      const uint4 mk = *reinterpret_cast<const uint4*>(mask + xi);
+      const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bf16_t mb = (bf16_t)((mw[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
+        if (!(bf2f(mb) > 0.f)) v[j] = 0.f;
+      }
     }
-    float v = (float)acc;
-    if (mask && !(bf2f(mask[i]) > 0.f)) v = 0.f;
-    store_split(gx, psx, i, v);
+    store_split8(gx + xi, psx, v);
   }
 }
 
@@ -295,29 +359,54 @@ __global__ void __launch_bounds__(256) softmax_ce_split_kernel(
 }
 
 // column sums of split planes [R][ld] (first N columns) in float64, two
-// deterministic passes: per-block partials, then a fixed-order final sum.
-constexpr int CS_ROWS = 256;  // rows per partial block
-
+// deterministic passes.  Pass 1: block b covers rows [b*rpb, (b+1)*rpb); a
+// thread owns one 8-column chunk (16-byte loads per plane) and a row lane;
+// lanes are reduced through shared memory in fixed order -> part[b][N8].
+// Pass 2: fixed-order sum over blocks.
 __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16_t* __restrict__ g,
-                                                             size_t ps, int R, int N, int ld,
+                                                             size_t ps, int R, int N8, int ld,
+                                                             int rows_per_block,
                                                              double* __restrict__ part) {
-  const int r0 = blockIdx.x * CS_ROWS;
-  const int r1 = min(R, r0 + CS_ROWS);
-  for (int c0 = blockIdx.y * 256; c0 < N; c0 += 256 * gridDim.y) {
-    const int c = c0 + threadIdx.x;
-    double s = 0.0;
-    if (c < N)
-      for (int r = r0; r < r1; ++r) s += (double)load_split(g, ps, (size_t)r * ld + c);
-    if (c < N) part[(size_t)blockIdx.x * N + c] = s;
+  __shared__ double red[256 * 8];
+  const int chunks = N8 / 8;
+  const int per_pass = chunks < 256 ? chunks : 256;
+  const int lanes = 256 / per_pass;
+  const int tc = threadIdx.x % per_pass, tl = threadIdx.x / per_pass;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(R, r0 + rows_per_block);
+  for (int c0 = 0; c0 < chunks; c0 += per_pass) {
+    const int cc = c0 + tc;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    if (tl < lanes && cc < chunks)
+      for (int r = r0 + tl; r < r1; r += lanes) {
+        float v[8];
+        load_split8(g + (size_t)r * ld + cc * 8, ps, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += (double)v[j];
+      }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[threadIdx.x * 8 + j] = acc[j];
+    __syncthreads();
+    for (int e = threadIdx.x; e < per_pass * 8; e += 256) {
+      const int c = e / 8, j = e % 8;
+      if (c0 + c < chunks) {
+        double t = 0.0;
+        for (int l = 0; l < lanes; ++l) t += red[(l * per_pass + c) * 8 + j];
+        part[(size_t)blockIdx.x * N8 + (c0 + c) * 8 + j] = t;
+      }
+    }
+    __syncthreads();
   }
 }
 
-__global__ void colsum_final_kernel(const double* __restrict__ part, int blocks, int N,
+__global__ void colsum_final_kernel(const double* __restrict__ part, int blocks, int N, int N8,
                                     float* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
   double s = 0.0;
-  for (int b = 0; b < blocks; ++b) s += part[(size_t)b * N + c];
+  for (int b = 0; b < blocks; ++b) s += part[(size_t)b * N8 + c];
   out[c] = (float)s;
 }
 

@@ -135,7 +135,8 @@ struct SvConvFwdA {
 };
 
 // conv input-gradient A over NHWC gradient planes G[N, OH, OW, O8], K-major:
-// row m = (n, h, w), k = (kh, kw, o): G[n, (h+p-kh)/s, (w+p-kw)/s, o]
+// row m = (n, h, w), k = (th, tw, o) with flipped taps kh = k-1-th,
+// kw = k-1-tw (matches the wd packing): G[n, (h+p-kh)/s, (w+p-kw)/s, o]
 struct SvConvDgradA {
   static constexpr bool MN = false;
   const bf16_t* g;
@@ -150,6 +151,8 @@ struct SvConvDgradA {
     d_w.divmod(j, h, w);
     d_o8.divmod(k, tap, o0);
     d_k.divmod(tap, kh, kw);
+    kh = d_k.d - 1 - kh;  // flipped tap order
+    kw = d_k.d - 1 - kw;
     int ty = (int)(h + pad) - (int)kh, tx = (int)(w + pad) - (int)kw;
     if (ty < 0 || tx < 0) return nullptr;
     if (s != 1) {
@@ -233,6 +236,20 @@ struct EpF32 {
     uint32_t q, r;
     d_m.divmod((uint32_t)m, q, r);
     const long long row = (long long)q * ld_hi + (long long)r * ld_lo;
+    if (ld_n == 1 && n0 + 8 <= N && !mask && ((row + n0) & 3) == 0) {
+      float w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float x = v[j];
+        if (bias) x = __fadd_rn(x, __ldg(bias + n0 + j));
+        if (relu && x < 0.f) x = 0.f;
+        w[j] = x;
+      }
+      float4* dst = reinterpret_cast<float4*>(out + row + n0);
+      dst[0] = make_float4(w[0], w[1], w[2], w[3]);
+      dst[1] = make_float4(w[4], w[5], w[6], w[7]);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int n = n0 + j;

@@ -1,0 +1,313 @@
+// TMA-fed tcgen05 GEMM for split-plane operands (the main hot-path kernel).
+//
+// Round-1 profiling of the cp.async version (stz_split.cuh) showed the conv
+// GEMMs L1tex-bound (82-95% of L1tex throughput, tensor pipe 14-27%): every
+// 16-byte gather is an LSU request.  Here every operand tile moves L2 -> smem
+// through the Tensor Memory Accelerator, one elected thread issuing
+// cp.async.bulk.tensor per plane:
+//
+//   TILED_K   2D [rows][K] (K contiguous)       box {32 K, R rows}  -> K-major
+//   TILED_MN  2D [K][rows] (rows contiguous)    box {32 rows, 32 K} -> MN-major
+//   IM2COL_K  4D NHWC im2col, pixels = rows     32 channels x 128 pixels (conv fwd / dgrad A)
+//   IM2COL_MN 4D NHWC im2col, pixels = K        32 channels x 32 pixels  (conv wgrad A)
+//
+// All boxes land with the 64-byte swizzle (BK = 32 bf16 = one 64-byte row);
+// the UMMA shared-memory descriptors use the matching SWIZZLE_64B canonical
+// layouts:
+//   K-major : 8-row x 64 B atoms, SBO = 512 B, K step of 16 = +32 B
+//   MN-major: 32-element x 8-k-row atoms, LBO = 2048 B between 32-element
+//             MN groups, SBO = 512 B between 8-k-row groups, K step of 16 =
+//             +1024 B.
+// Out-of-range rows / pixels / channels are zero-filled by TMA.  The
+// BF16x6 MMA schedule, the two TMEM accumulators and the epilogues are the
+// ones of stz_split.cuh.
+#pragma once
+
+#include <cuda.h>
+
+#include "stz_split.cuh"
+
+namespace stz {
+
+enum TgMode : int { TG_TILED_K = 0, TG_TILED_MN = 1, TG_IM2COL_K = 2, TG_IM2COL_MN = 3 };
+
+struct alignas(64) TgOperand {
+  CUtensorMap map[3];  // one per plane
+  int mode;
+  int nbox;            // boxes per plane per k-block (TILED_MN / IM2COL_MN)
+  // im2col geometry: output pixel (n, oh, ow) -> window start (oh*s + lo, ow*s + lo)
+  int lo, s, C8, ksz, flip;
+  FastDiv d_ohw, d_ow, d_c8, d_k;
+};
+
+template <class EP>
+struct alignas(64) TgParams {
+  TgOperand a, b;
+  EP ep;
+  float* partial;
+  int M, N, K, k_per_split;
+};
+
+constexpr int TG_BM = 128, TG_BK = 32;
+constexpr int TG_THREADS = 256;  // w0 TMA (32 lanes), w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
+
+template <int BN>
+struct TgCfg {
+  static constexpr int A_BYTES = TG_BM * TG_BK * 2;  // one plane, 8 KB
+  static constexpr int B_BYTES = BN * TG_BK * 2;
+  static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;  // + alignment slack + barriers
+  // two accumulator SETS (double-buffered across tiles), each = big + small
+  static constexpr int ACC_COLS = 2 * BN;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 256 ? 256 : 512;
+  static_assert(2 * ACC_COLS <= 512, "BN too wide for double-buffered TMEM");
+  static_assert(STAGES >= 3, "tile too large");
+  static_assert(B_BYTES % 512 == 0, "B plane blocks must stay 512-byte aligned (SW64 atoms)");
+};
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint32_t dst, uint64_t* bar,
+                                       int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_im2col_4d(const CUtensorMap* map, uint32_t dst, uint64_t* bar,
+                                              int c, int w, int h, int n, uint16_t ow,
+                                              uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(ow), "h"(oh)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// SWIZZLE_64B UMMA descriptor (layout type 4)
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
+// issue box `bi` (0 <= bi < 3*nbox) of one operand tile: plane = bi / nbox,
+// box = bi % nbox (R rows starting at r0, K block starting at k0)
+__device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_t tile_base,
+                                            uint32_t plane_bytes, uint64_t* bar, int r0, int k0) {
+  const int plane = bi / op.nbox, box = bi - plane * op.nbox;
+  const CUtensorMap* map = &op.map[plane];
+  const uint32_t dst = tile_base + plane * plane_bytes + box * 2048;
+  switch (op.mode) {
+    case TG_TILED_K:
+      tma_2d(map, dst, bar, k0, r0);
+      break;
+    case TG_TILED_MN:
+      tma_2d(map, dst, bar, r0 + 32 * box, k0);
+      break;
+    case TG_IM2COL_K: {
+      uint32_t n, j, oh, ow, tap, c0, th, tw;
+      op.d_ohw.divmod((uint32_t)r0, n, j);
+      op.d_ow.divmod(j, oh, ow);
+      op.d_c8.divmod((uint32_t)k0, tap, c0);
+      op.d_k.divmod(tap, th, tw);
+      tma_im2col_4d(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo, (int)(oh * op.s) + op.lo,
+                    (int)n, (uint16_t)tw, (uint16_t)th);
+      break;
+    }
+    default: {  // TG_IM2COL_MN: k0 = first output pixel, rows = (tap, c)
+      uint32_t n, j, oh, ow, tap, c0, th, tw;
+      op.d_ohw.divmod((uint32_t)k0, n, j);
+      op.d_ow.divmod(j, oh, ow);
+      op.d_c8.divmod((uint32_t)(r0 + 32 * box), tap, c0);
+      op.d_k.divmod(tap, th, tw);
+      tma_im2col_4d(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo, (int)(oh * op.s) + op.lo,
+                    (int)n, (uint16_t)tw, (uint16_t)th);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t tg_desc(int mode, uint32_t plane_base, int kstep) {
+  const bool mn = mode == TG_TILED_MN || mode == TG_IM2COL_MN;
+  return mn ? umma_desc_sw64(plane_base + kstep * 1024, 2048, 512)
+            : umma_desc_sw64(plane_base + kstep * 32, 16, 512);
+}
+
+// Persistent: grid = min(#work items, #SMs); work item w -> (split z, m tile,
+// n tile), n fastest so consecutive items share the A tile in L2.  TMEM holds
+// two accumulator sets; the epilogue of item i overlaps the mainloop of i+1.
+template <int BN, class EP>
+__global__ void __launch_bounds__(TG_THREADS, 1)
+    tgemm_kernel(const __grid_constant__ TgParams<EP> p) {
+  using Cfg = TgCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t smem_base = (raw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (smem_base - raw);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;   // [2] accumulator set ready for the epilogue
+  uint64_t* tempty_bar = tfull_bar + 2;       // [2] accumulator set drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = cdiv(p.M, TG_BM), nt = cdiv(p.N, BN);
+  const int splits = cdiv(p.K, p.k_per_split);
+  const int items = mt * nt * splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 0 && lane < 3) {
+    prefetch_tmap(&p.a.map[lane]);
+    prefetch_tmap(&p.b.map[lane]);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: the warp's lanes issue boxes in parallel --
+    const int na = 3 * p.a.nbox, nbx = 3 * p.b.nbox;
+    int g = 0;  // global k-block counter (stage / phase)
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      const int z = w / (mt * nt), rem = w % (mt * nt);
+      const int m0 = (rem / nt) * TG_BM, n0 = (rem % nt) * BN;
+      const int kbeg = z * p.k_per_split, kend = min(p.K, kbeg + p.k_per_split);
+      const int nkb = cdiv(kend - kbeg, TG_BK);
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int stage = g % STAGES;
+        mbar_wait(&empty_bar[stage], ((g / STAGES) & 1) ^ 1);
+        if (lane == 0) mbar_arrive_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+        __syncwarp();
+        const int k0 = kbeg + kb * TG_BK;
+        const uint32_t st = smem_base + stage * Cfg::STAGE_BYTES;
+        for (int bi = lane; bi < na + nbx; bi += 32) {
+          if (bi < na)
+            tg_load_box(p.a, bi, st, Cfg::A_BYTES, &full_bar[stage], m0, k0);
+          else
+            tg_load_box(p.b, bi - na, st + 3 * Cfg::A_BYTES, Cfg::B_BYTES, &full_bar[stage], n0,
+                        k0);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer -----------------------------------------------
+    const bool amn = p.a.mode == TG_TILED_MN || p.a.mode == TG_IM2COL_MN;
+    const bool bmn = p.b.mode == TG_TILED_MN || p.b.mode == TG_IM2COL_MN;
+    const uint32_t idesc = sg_idesc(TG_BM, BN, amn, bmn);
+    constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
+    constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
+    int g = 0, it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int z = w / (mt * nt);
+      const int kbeg = z * p.k_per_split, kend = min(p.K, kbeg + p.k_per_split);
+      const int nkb = cdiv(kend - kbeg, TG_BK);
+      const int acc = it & 1;
+      mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tbig = tmem_base + acc * Cfg::ACC_COLS, tsmall = tbig + BN;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int stage = g % STAGES;
+        mbar_wait(&full_bar[stage], (g / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_base + stage * Cfg::STAGE_BYTES;
+        const uint32_t b0 = a0 + 3 * Cfg::A_BYTES;
+#pragma unroll
+        for (int j = 0; j < TG_BK / 16; ++j) {
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            const uint64_t da = tg_desc(p.a.mode, a0 + AP[i] * Cfg::A_BYTES, j);
+            const uint64_t db = tg_desc(p.b.mode, b0 + BP[i] * Cfg::B_BYTES, j);
+            const bool big = i == 5;
+            const bool first = (kb | j) == 0 && (big || i == 0);
+            umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
+          }
+        }
+        umma_commit(&empty_bar[stage]);
+      }
+      umma_commit(&tfull_bar[acc]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM (big + small) -> registers -> ep ---------
+    const int q = warp & 3;
+    const int npad = cdiv(p.N, 8) * 8;
+    int it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int z = w / (mt * nt), rem = w % (mt * nt);
+      const int m0 = (rem / nt) * TG_BM, n0 = (rem % nt) * BN;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        if (n0 + c >= npad) break;
+        uint32_t r[16], rs[16];
+        tmem_ld16(tbase + (uint32_t)c, r);
+        tmem_ld16(tbase + BN + (uint32_t)c, rs);
+        tmem_ld_wait();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int nb = n0 + c + 8 * h;
+          if (nb >= npad) break;
+          float v[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            v[jj] = __fadd_rn(__uint_as_float(r[8 * h + jj]), __uint_as_float(rs[8 * h + jj]));
+          if (p.partial) {
+            if (m < p.M) {
+              float4* dst =
+                  reinterpret_cast<float4*>(p.partial + ((size_t)z * p.M + m) * npad + nb);
+              dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+              dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
+          } else {
+            p.ep.store8(m, nb, v);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+}  // namespace stz

@@ -2,19 +2,24 @@
 
 A ``BlockEngine`` owns, for a fixed batch size:
 
-* flat parameter / velocity / gradient buffers for its block (one tensor
-  each; per-layer views in the reference layouts -- conv W [O,C,k,k], FC W
-  [in,out] -- each view 16-byte aligned), so the gradient allreduce and the
-  momentum step are single calls over one vector (no pack/unpack,
-  reference tensor_core.py:501-524);
-* preallocated activation, argmax and gradient buffers (no allocation per
-  step, so a whole step can be captured in a CUDA graph);
-* a fused plan over the C ABI: conv/FC + following ReLU fuse into the GEMM
-  epilogue; a ReLU's backward fuses into the input-gradient kernel of the
-  layer that consumed it (conv/FC dgrad or max-pool backward, skipping
-  Flatten, which is a view); SoftmaxCE emits loss and dlogits in one pass;
-  the first layer of the CONV block skips its input gradient, which the
-  reference computes and discards (stanza_runtime.py:366-369).
+* fp32 master parameter / velocity / gradient buffers for its block, one
+  flat tensor each with per-layer views in the reference layouts (conv W
+  [O,C,k,k], FC W [in,out]; every view 16-byte aligned), so the gradient
+  allreduce and the momentum step are single calls over one vector (no
+  pack/unpack, reference tensor_core.py:501-524);
+* split-plane copies of the weights in GEMM-ready layouts (conv forward
+  [O][kh][kw][C8], conv input-gradient [C][kh][kw][O8], FC [in][out8]),
+  refreshed after every update;
+* split-plane activation / gradient buffers (three bf16 planes whose sum is
+  the fp32 value exactly; conv tensors NHWC with channels padded to 8, flat
+  tensors [rows][D8]), preallocated for the batch so a step never allocates;
+* a fused plan over the C ABI (``stzx_*``): conv/FC + following ReLU in the
+  GEMM epilogue; a ReLU's backward folded into the input-gradient kernel of
+  the layer that consumed it (conv/FC dgrad, max-pool backward); a max-pool
+  followed by Flatten writes the CHW-flat (reference flatten order) tensor
+  directly; SoftmaxCE emits loss and dlogits in one pass; the first layer of
+  the CONV block skips its input gradient (stanza_runtime.py:366-369 discards
+  it).
 """
 
 from __future__ import annotations
@@ -29,31 +34,81 @@ from .tensor_core import (Conv2d, Flatten, FullyConnected, MaxPool2d, ReLU,
                           ShapeMismatch, SoftmaxCrossEntropy, inv_batch, out_shape,
                           param_shapes, ptr, stream_of, workspace)
 
-_ALIGN = 4  # floats: keeps every per-tensor view 16-byte aligned
+_ALIGN = 4  # floats: keeps every fp32 per-tensor view 16-byte aligned
 
 
 def _aligned(n: int) -> int:
     return (n + _ALIGN - 1) // _ALIGN * _ALIGN
 
 
+def rup8(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
+class Split:
+    """A split-plane tensor: storage [3, *dims] bf16, plane stride ``ps``.
+    layout "nhwc": dims (N, H, W, C8), logical channels C;
+    layout "rows": dims (N, D8), logical width D."""
+
+    def __init__(self, storage: torch.Tensor, layout: str, logical: int, row0: int = 0,
+                 rows: int | None = None):
+        self.storage = storage
+        self.layout = layout
+        self.logical = logical                       # C (nhwc) or D (rows)
+        self.ps = storage[0].numel()
+        self.row0 = row0                             # row offset of a slice view
+        self.rows = storage.shape[1] if rows is None else rows
+
+    @staticmethod
+    def alloc(layout, dims, logical, device):
+        return Split(torch.zeros((3, *dims), dtype=torch.bfloat16, device=device), layout,
+                     logical)
+
+    @property
+    def row_elems(self) -> int:
+        return int(np.prod(self.storage.shape[2:]))
+
+    @property
+    def width(self) -> int:
+        return self.storage.shape[-1]
+
+    def ptr(self) -> int:
+        return self.storage.data_ptr() + self.row0 * self.row_elems * 2
+
+    def rows_view(self, lo: int, hi: int) -> "Split":
+        s = Split(self.storage, self.layout, self.logical, self.row0 + lo, hi - lo)
+        return s
+
+    def plane_rows(self, p: int) -> torch.Tensor:
+        """Plane p restricted to this view's rows (a contiguous tensor view)."""
+        return self.storage[p, self.row0:self.row0 + self.rows]
+
+    def to_float(self) -> torch.Tensor:
+        """Debug read-back: exact fp32 values of this view."""
+        planes = [self.plane_rows(p).float() for p in range(3)]
+        return (planes[0] + planes[1]) + planes[2]
+
+
 @dataclass
 class _Op:
     kind: str                 # conv | fc | maxpool | relu | flatten | softmax_ce
     layer: object
-    index: int                # layer index within the block
-    in_shape: tuple           # per-sample
-    out_shape: tuple          # per-sample
+    index: int
+    in_shape: tuple           # per-sample logical shape
+    out_shape: tuple
     fused_relu: bool = False  # conv/fc: epilogue applies the following ReLU
-    mask_from: int = -1       # bwd: op index whose output masks this op's input grad
-    relu_bwd_fused: bool = False  # relu: its backward is done by its consumer
+    mask_from: int = -1       # bwd: op whose output (a ReLU output) masks the input grad
+    relu_bwd_fused: bool = False
     skip_dgrad: bool = False
+    flat_out: bool = False    # maxpool: writes the CHW-flat tensor for a following Flatten
 
 
 class BlockEngine:
-    """One block of layers bound to a device, a batch size and flat buffers."""
+    """One block of layers bound to a device, a batch size and its buffers."""
 
     def __init__(self, layers, in_shape, batch: int, device, params=None, velocities=None,
-                 need_input_grad: bool = True, shared=None, input_grad_buffer=None):
+                 need_input_grad: bool = True, shared=None, input_grad_buffer=None,
+                 allocate: bool = True):
         self.layers = tuple(layers)
         self.in_shape = tuple(in_shape)
         self.batch = int(batch)
@@ -61,14 +116,18 @@ class BlockEngine:
         self.need_input_grad = need_input_grad
         self._build_plan()
         self._layout_params()
+        if not allocate:
+            return
         dev, f32 = self.device, torch.float32
-        if shared is not None:                   # FC replicas on one GPU share (w, v)
+        if shared is not None:                   # FC replicas on one GPU share (w, v, planes)
             if shared.total != self.total:
                 raise ShapeMismatch("shared engine has a different parameter layout")
             self.params_flat, self.vel_flat = shared.params_flat, shared.vel_flat
+            self.wplanes = shared.wplanes
         else:
             self.params_flat = torch.zeros(self.total, dtype=f32, device=dev)
             self.vel_flat = torch.zeros(self.total, dtype=f32, device=dev)
+            self.wplanes = self._alloc_weight_planes()
         self.grad_flat = torch.zeros(self.total, dtype=f32, device=dev)
         self.params = self._views(self.params_flat)
         self.velocity = self._views(self.vel_flat)
@@ -77,7 +136,7 @@ class BlockEngine:
             self.load(params, velocities)
         self._alloc_activations(input_grad_buffer)
 
-    # -- plan ------------------------------------------------------------------
+    # -- plan ----------------------------------------------------------------------
 
     def _build_plan(self):
         ops, shape = [], self.in_shape
@@ -91,7 +150,8 @@ class BlockEngine:
         for i, op in enumerate(ops):
             if op.kind == "relu" and i > 0 and ops[i - 1].kind in ("conv", "fc"):
                 ops[i - 1].fused_relu = True
-        # ReLU backward goes into the input-gradient kernel of its consumer
+            if op.kind == "flatten" and i > 0 and ops[i - 1].kind == "maxpool":
+                ops[i - 1].flat_out = True
         for i, op in enumerate(ops):
             if op.kind != "relu":
                 continue
@@ -120,40 +180,85 @@ class BlockEngine:
     def _views(self, flat):
         return [[flat[o:o + n].view(shp) for (o, shp, n) in row] for row in self.slots]
 
+    def _alloc_weight_planes(self):
+        dev = self.device
+        planes = {}
+        for i, op in enumerate(self.ops):
+            l = op.layer
+            if op.kind == "conv":
+                kk, c8, o8 = l.kernel * l.kernel, rup8(l.in_ch), rup8(l.out_ch)
+                wf = torch.zeros((3, l.out_ch, kk * c8), dtype=torch.bfloat16, device=dev)
+                wd = None if op.skip_dgrad else torch.zeros((3, l.in_ch, kk * o8),
+                                                            dtype=torch.bfloat16, device=dev)
+                planes[i] = (wf, wd)
+            elif op.kind == "fc":
+                planes[i] = (torch.zeros((3, l.in_dim, rup8(l.out_dim)), dtype=torch.bfloat16,
+                                         device=dev), None)
+        return planes
+
+    # -- buffers -------------------------------------------------------------------
+
+    def _split_for(self, shape, rows: int, flat_from_nhwc: bool = False):
+        dev = self.device
+        if len(shape) == 3:
+            c, h, w = shape
+            return Split.alloc("nhwc", (rows, h, w, rup8(c)), c, dev)
+        d = shape[0]
+        return Split.alloc("rows", (rows, rup8(d)), d, dev)
+
     def _alloc_activations(self, input_grad_buffer):
-        dev, b, f32 = self.device, self.batch, torch.float32
-        self.acts: list = [None] * len(self.ops)
-        self.args: list = [None] * len(self.ops)
-        self.gin: list = [None] * len(self.ops)   # gradient wrt each op's input
+        b = self.batch
+        dev = self.device
+        n = len(self.ops)
+        self.acts: list = [None] * n      # Split output of op i (aliases resolved in _act)
+        self.args: list = [None] * n
+        self.gin: list = [None] * n       # Split gradient wrt op i's input
+        self.logits = None
         self.losses = None
         self.dlogits = None
+        self.xin = None   # packed block input, allocated on first pack_input()
         for i, op in enumerate(self.ops):
             if op.kind == "relu" and i > 0 and self.ops[i - 1].fused_relu:
-                continue                          # aliases its producer's output
-            if op.kind == "flatten":
-                continue                          # view of its input
-            if op.kind == "softmax_ce":
-                self.losses = torch.zeros(b, dtype=f32, device=dev)
-                self.dlogits = torch.zeros((b, *op.in_shape), dtype=f32, device=dev)
                 continue
-            self.acts[i] = torch.zeros((b, *op.out_shape), dtype=f32, device=dev)
+            if op.kind == "flatten":
+                src_flat = i > 0 and self.ops[i - 1].kind == "maxpool" and self.ops[i - 1].flat_out
+                if not src_flat and len(op.in_shape) == 3:
+                    self.acts[i] = self._split_for(op.out_shape, b)   # relayout target
+                continue
+            if op.kind == "softmax_ce":
+                c = op.in_shape[0]
+                self.losses = torch.zeros(b, dtype=torch.float32, device=dev)
+                self.dlogits = Split.alloc("rows", (b, rup8(c)), c, dev)
+                continue
+            if op.kind == "fc" and i + 1 < n and self.ops[i + 1].kind == "softmax_ce":
+                self.logits = torch.zeros((b, op.out_shape[0]), dtype=torch.float32, device=dev)
+                continue
+            shape = op.out_shape
+            if op.kind == "maxpool" and op.flat_out:
+                shape = (int(np.prod(op.out_shape)),)
+            self.acts[i] = self._split_for(shape, b)
             if op.kind == "maxpool":
-                self.args[i] = torch.zeros((b, *op.out_shape), dtype=torch.uint8, device=dev)
+                c, oh, ow = op.out_shape
+                self.args[i] = torch.zeros((b, oh, ow, rup8(c)), dtype=torch.uint8, device=dev)
         for i, op in enumerate(self.ops):
-            if op.kind in ("flatten", "softmax_ce"):
+            if op.kind in ("softmax_ce",):
                 continue
             if op.kind == "relu" and op.relu_bwd_fused:
                 continue
+            if op.kind == "flatten":
+                src_flat = i > 0 and self.ops[i - 1].kind == "maxpool" and self.ops[i - 1].flat_out
+                if src_flat or len(op.in_shape) != 3:
+                    continue
             if i == 0:
                 if not self.need_input_grad:
                     continue
                 if input_grad_buffer is not None:
                     self.gin[0] = input_grad_buffer
                     continue
-            self.gin[i] = torch.zeros((b, *op.in_shape), dtype=f32, device=dev)
+            self.gin[i] = self._split_for(op.in_shape, b)
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
 
-    # -- parameters --------------------------------------------------------------
+    # -- parameters ------------------------------------------------------------------
 
     def load(self, params, velocities=None):
         """Upload nested numpy (or tensor) params/velocities in reference layout."""
@@ -162,6 +267,22 @@ class BlockEngine:
                 self.params[li][ti].copy_(torch.as_tensor(np.asarray(params[li][ti])))
                 if velocities is not None:
                     self.velocity[li][ti].copy_(torch.as_tensor(np.asarray(velocities[li][ti])))
+        self.pack_weights()
+
+    def pack_weights(self):
+        """Refresh the split-plane weight copies from the fp32 masters."""
+        st = stream_of(self.device)
+        for i, (a, b) in self.wplanes.items():
+            op = self.ops[i]
+            l = op.layer
+            w = self.params[i][0]
+            if op.kind == "conv":
+                _lib.call("stzx_pack_conv_w", ptr(w), ptr(a), a[0].numel(), ptr(b),
+                          0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kernel,
+                          rup8(l.in_ch), rup8(l.out_ch), st)
+            else:
+                _lib.call("stzx_pack_rows", ptr(w), ptr(a), a[0].numel(), l.in_dim, l.out_dim,
+                          rup8(l.out_dim), st)
 
     def state_numpy(self):
         """(params, velocities) as nested fp32 numpy arrays, reference layout."""
@@ -169,82 +290,144 @@ class BlockEngine:
         v = [[t.detach().cpu().numpy().copy() for t in row] for row in self.velocity]
         return p, v
 
-    # -- execution ------------------------------------------------------------------
+    # -- execution -------------------------------------------------------------------
+
+    def op_flops(self, i: int) -> float:
+        """Algorithmic FLOPs of op i's forward contraction (2*M*N*K with the
+        logical channel counts); its dgrad and wgrad have the same count."""
+        op = self.ops[i]
+        l = op.layer
+        if op.kind == "conv":
+            _, oh, ow = op.out_shape
+            return 2.0 * self.batch * oh * ow * l.out_ch * l.in_ch * l.kernel * l.kernel
+        if op.kind == "fc":
+            return 2.0 * self.batch * l.in_dim * l.out_dim
+        return 0.0
 
     def _act(self, i):
-        """Output buffer of op i (resolving ReLU / Flatten aliases)."""
+        """Output Split of op i, resolving ReLU / Flatten aliases."""
+        if i < 0:
+            return self._x
         op = self.ops[i]
-        if op.kind == "flatten" or (op.kind == "relu" and self.acts[i] is None):
-            src = self._act(i - 1) if i > 0 else self._x
-            return src.reshape((self.batch, *op.out_shape))
-        return self.acts[i]
+        if self.acts[i] is not None:
+            return self.acts[i]
+        if op.kind in ("relu", "flatten"):
+            return self._act(i - 1)
+        return None
 
     def _input(self, i):
         return self._x if i == 0 else self._act(i - 1)
 
-    def forward(self, x: torch.Tensor, labels: torch.Tensor | None = None,
-                loss_out: torch.Tensor | None = None):
-        """Run the block on x [batch, *in_shape]; returns the block output
-        (per-sample losses for a loss block).  The float64 loss sum goes to
-        ``loss_sum``, or is ADDED into ``loss_out`` when given."""
+    def pack_input(self, x: torch.Tensor) -> Split:
+        """fp32 batch in the reference layout -> the packed block input."""
         if tuple(x.shape) != (self.batch, *self.in_shape):
             raise ShapeMismatch(f"block expects {(self.batch, *self.in_shape)}, "
                                 f"got {tuple(x.shape)}")
+        st = stream_of(self.device)
+        if self.xin is None:
+            self.xin = self._split_for(self.in_shape, self.batch)
+        s = self.xin
+        if s.layout == "nhwc":
+            c, h, w = self.in_shape
+            _lib.call("stzx_pack_nchw", ptr(x), s.ptr(), s.ps, self.batch, c, h, w, s.width, st)
+        else:
+            _lib.call("stzx_pack_rows", ptr(x), s.ptr(), s.ps, self.batch, self.in_shape[0],
+                      s.width, st)
+        return s
+
+    def forward(self, x, labels: torch.Tensor | None = None,
+                loss_out: torch.Tensor | None = None):
+        """Run the block.  ``x`` is a fp32 batch in the reference layout or an
+        already-packed Split (e.g. the CONV block's output rows).  Returns the
+        output Split (per-sample fp32 losses for a loss block).  The float64
+        loss sum goes to ``loss_sum`` or is ADDED into ``loss_out``."""
+        if isinstance(x, torch.Tensor):
+            x = self.pack_input(x)
         self._x = x
-        self._labels = labels
         st = stream_of(self.device)
         ws = workspace(self.device)
         b = self.batch
         for i, op in enumerate(self.ops):
             xin = self._input(i)
+            l = op.layer
             if op.kind == "conv":
-                l = op.layer
                 c, h, w = op.in_shape
-                _lib.call("stz_conv2d_fwd", ptr(xin), ptr(self.params[i][0]),
-                          ptr(self.params[i][1]), ptr(self.acts[i]), b, c, h, w, l.out_ch,
-                          l.kernel, l.stride, l.padding, int(op.fused_relu), ptr(ws),
-                          ws.numel(), st)
+                y = self.acts[i]
+                wf, _ = self.wplanes[i]
+                _lib.call("stzx_conv_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
+                          ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w, l.out_ch,
+                          y.width, l.kernel, l.stride, l.padding, int(op.fused_relu), ptr(ws),
+                          ws.numel(), st, flops=self.op_flops(i), tag=f"conv{i}_fwd")
             elif op.kind == "fc":
-                l = op.layer
-                _lib.call("stz_fc_fwd", ptr(xin), ptr(self.params[i][0]),
-                          ptr(self.params[i][1]), ptr(self.acts[i]), b, l.in_dim, l.out_dim,
-                          int(op.fused_relu), ptr(ws), ws.numel(), st)
+                wp, _ = self.wplanes[i]
+                if self.acts[i] is not None:
+                    y = self.acts[i]
+                    _lib.call("stzx_fc_fwd", xin.ptr(), xin.ps, ptr(wp), wp[0].numel(),
+                              ptr(self.params[i][1]), y.ptr(), y.ps, None, b, l.in_dim,
+                              xin.width, l.out_dim, y.width, int(op.fused_relu), ptr(ws),
+                              ws.numel(), st, flops=self.op_flops(i), tag=f"fc{i}_fwd")
+                else:
+                    _lib.call("stzx_fc_fwd", xin.ptr(), xin.ps, ptr(wp), wp[0].numel(),
+                              ptr(self.params[i][1]), None, 0, ptr(self.logits), b, l.in_dim,
+                              xin.width, l.out_dim, rup8(l.out_dim), int(op.fused_relu),
+                              ptr(ws), ws.numel(), st, flops=self.op_flops(i), tag=f"fc{i}_fwd")
             elif op.kind == "maxpool":
                 c, h, w = op.in_shape
-                _lib.call("stz_maxpool2d_fwd", ptr(xin), ptr(self.acts[i]), ptr(self.args[i]),
-                          b, c, h, w, op.layer.kernel, op.layer.stride, st)
+                y = self.acts[i]
+                _lib.call("stzx_maxpool_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, ptr(self.args[i]),
+                          b, c, xin.width, h, w, l.kernel, l.stride,
+                          y.width if op.flat_out else 0, st)
             elif op.kind == "relu":
                 if self.acts[i] is not None:
-                    _lib.call("stz_relu_fwd", ptr(xin), ptr(self.acts[i]), xin.numel(), st)
+                    y = self.acts[i]
+                    _lib.call("stzx_relu_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps,
+                              b * xin.row_elems, st)
+            elif op.kind == "flatten":
+                if self.acts[i] is not None:               # NHWC -> CHW-flat relayout
+                    c, h, w = op.in_shape
+                    y = self.acts[i]
+                    _lib.call("stzx_nhwc_to_flat", xin.ptr(), xin.ps, y.ptr(), y.ps, b, c, h, w,
+                              xin.width, y.width, st)
             elif op.kind == "softmax_ce":
                 if labels is None:
                     raise ValueError("SoftmaxCrossEntropy needs labels")
-                _lib.call("stz_softmax_ce", ptr(xin), ptr(labels), ptr(self.losses),
-                          ptr(self.dlogits), b, op.in_shape[0], st)
+                c = op.in_shape[0]
+                _lib.call("stzx_softmax_ce", ptr(self.logits), ptr(labels), ptr(self.losses),
+                          self.dlogits.ptr(), self.dlogits.ps, b, c, self.dlogits.width, st)
                 tgt, acc = (self.loss_sum, 0) if loss_out is None else (loss_out, 1)
                 _lib.call("stz_sum_f32", ptr(self.losses), b, ptr(tgt), acc, st)
         return self.losses if self.losses is not None else self._act(len(self.ops) - 1)
 
-    def backward(self, gy: torch.Tensor | None = None):
+    def backward(self, gy: Split | None = None):
         """Backward through the block; parameter-gradient sums land in
-        ``grad_flat``.  Returns the gradient wrt the block input (None when
-        the block was built with need_input_grad=False)."""
+        ``grad_flat``.  Returns the input-gradient Split (None when the block
+        was built with need_input_grad=False)."""
         st = stream_of(self.device)
         ws = workspace(self.device)
         b = self.batch
         g = gy
         for i in range(len(self.ops) - 1, -1, -1):
             op = self.ops[i]
+            l = op.layer
             xin = self._input(i)
-            mask = self._act(op.mask_from) if op.mask_from >= 0 else None
+            # the ReLU output feeding this op IS its input (possibly flattened):
+            # > 0 exactly where the ReLU passed its gradient
+            mptr = xin.ptr() if op.mask_from >= 0 else None
             if op.kind == "softmax_ce":
                 g = self.dlogits
             elif op.kind == "flatten":
-                g = g.reshape((b, *op.in_shape))
+                if self.acts[i] is not None:              # CHW-flat -> NHWC relayout back
+                    c, h, w = op.in_shape
+                    out = self.gin[i]
+                    _lib.call("stzx_flat_to_nhwc", g.ptr(), g.ps, out.ptr(), out.ps, b, c, h, w,
+                              out.width, g.width, st)
+                    g = out
             elif op.kind == "relu":
                 if not op.relu_bwd_fused:
                     out = self.gin[i]
-                    _lib.call("stz_relu_bwd", ptr(g), ptr(self._act(i)), ptr(out), g.numel(), st)
+                    src = self._act(i)
+                    _lib.call("stzx_relu_bwd", g.ptr(), g.ps, src.ptr(), out.ptr(), out.ps,
+                              b * g.row_elems, st)
                     g = out
             elif op.kind == "maxpool":
                 if op.skip_dgrad:
@@ -252,42 +435,49 @@ class BlockEngine:
                     continue
                 c, h, w = op.in_shape
                 out = self.gin[i]
-                _lib.call("stz_maxpool2d_bwd", ptr(g), ptr(self.args[i]), ptr(out), ptr(mask),
-                          b, c, h, w, op.layer.kernel, op.layer.stride, st)
+                _lib.call("stzx_maxpool_bwd", g.ptr(), g.ps, ptr(self.args[i]), out.ptr(), out.ps,
+                          mptr, b, c, out.width, h, w, l.kernel, l.stride,
+                          g.width if op.flat_out else 0, st)
                 g = out
             elif op.kind == "conv":
-                l = op.layer
                 c, h, w = op.in_shape
-                dims = (b, c, h, w, l.out_ch, l.kernel, l.stride, l.padding, ptr(ws),
-                        ws.numel(), st)
-                _lib.call("stz_conv2d_bwd_filter", ptr(xin), ptr(g), ptr(self.grads[i][0]),
-                          ptr(self.grads[i][1]), *dims)
+                _lib.call("stzx_conv_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), b, c, xin.width, h, w,
+                          l.out_ch, g.width, l.kernel, l.stride, l.padding, ptr(ws), ws.numel(),
+                          st, flops=self.op_flops(i), tag=f"conv{i}_wgrad")
                 if op.skip_dgrad:
                     g = None
                     continue
                 out = self.gin[i]
-                _lib.call("stz_conv2d_bwd_data", ptr(g), ptr(self.params[i][0]), ptr(out),
-                          ptr(mask), *dims)
+                _, wd = self.wplanes[i]
+                _lib.call("stzx_conv_dgrad", g.ptr(), g.ps, ptr(wd), wd[0].numel(), out.ptr(),
+                          out.ps, mptr, b, c, out.width, h, w, g.width, l.kernel, l.stride,
+                          l.padding, ptr(ws), ws.numel(), st, flops=self.op_flops(i),
+                          tag=f"conv{i}_dgrad")
                 g = out
             elif op.kind == "fc":
-                l = op.layer
-                _lib.call("stz_fc_bwd_weight", ptr(xin), ptr(g), ptr(self.grads[i][0]),
-                          ptr(self.grads[i][1]), b, l.in_dim, l.out_dim, ptr(ws), ws.numel(),
-                          st)
+                _lib.call("stzx_fc_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), b, l.in_dim, xin.width,
+                          l.out_dim, g.width, ptr(ws), ws.numel(), st, flops=self.op_flops(i),
+                          tag=f"fc{i}_wgrad")
                 if op.skip_dgrad:
                     g = None
                     continue
                 out = self.gin[i]
-                _lib.call("stz_fc_bwd_data", ptr(g), ptr(self.params[i][0]), ptr(out),
-                          ptr(mask), b, l.in_dim, l.out_dim, ptr(ws), ws.numel(), st)
+                wp, _ = self.wplanes[i]
+                _lib.call("stzx_fc_dgrad", g.ptr(), g.ps, ptr(wp), wp[0].numel(), out.ptr(),
+                          out.ps, mptr, b, l.in_dim, out.width, g.width, ptr(ws), ws.numel(), st,
+                          flops=self.op_flops(i), tag=f"fc{i}_dgrad")
                 g = out
         return g
 
     def sgd(self, n: int, lr: float, mu: float, grad: torch.Tensor | None = None):
-        """Momentum step over the whole flat block (tensor_core.py:366-388)."""
+        """Momentum step over the whole flat block (tensor_core.py:366-388),
+        then refresh the split-plane weight copies."""
         g = self.grad_flat if grad is None else grad
         _lib.call("stz_sgd_momentum", ptr(self.params_flat), ptr(self.vel_flat), ptr(g),
                   self.total, float(lr), float(mu), inv_batch(n), stream_of(self.device))
+        self.pack_weights()
 
     def add_grads_from(self, other: "BlockEngine"):
         """grad_flat += other.grad_flat (replica gradient sum on one device)."""

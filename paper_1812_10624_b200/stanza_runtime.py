@@ -158,11 +158,13 @@ class StanzaCluster:
         self.conv = None
         self.fcs: list[BlockEngine] = []
 
+        from .engine import Split, rup8
+        a8 = rup8(a)
         if comm is None:
             nk = n_conv * k
             self.x = torch.zeros((nk, *in_shape), dtype=torch.float32, device=dev)
             self.labels = torch.zeros(nk, dtype=torch.int32, device=dev)
-            self.gboundary = torch.zeros((nk, a), dtype=torch.float32, device=dev)
+            self.gboundary = Split.alloc("rows", (nk, a8), a, dev)
             self.conv = BlockEngine(conv_block, in_shape, nk, dev, full0[:cut], vel0[:cut],
                                     need_input_grad=False)
             for j in range(n_fc):
@@ -170,7 +172,7 @@ class StanzaCluster:
                 eng = BlockEngine(fc_block, (a,), (hi - lo) * k, dev,
                                   full0[cut:], vel0[cut:], need_input_grad=True,
                                   shared=self.fcs[0] if self.fcs else None,
-                                  input_grad_buffer=self.gboundary[lo * k:hi * k])
+                                  input_grad_buffer=self.gboundary.rows_view(lo * k, hi * k))
                 eng.rows = (lo * k, hi * k)
                 self.fcs.append(eng)
         else:
@@ -179,14 +181,14 @@ class StanzaCluster:
             if comm.is_conv:
                 self.x = torch.zeros((k, *in_shape), dtype=torch.float32, device=dev)
                 self.labels = torch.zeros(k, dtype=torch.int32, device=dev)
-                self.gboundary = torch.zeros((k, a), dtype=torch.float32, device=dev)
+                self.gboundary = Split.alloc("rows", (k, a8), a, dev)
                 self.conv = BlockEngine(conv_block, in_shape, k, dev, full0[:cut], vel0[:cut],
                                         need_input_grad=False)
             else:
                 self.x = None
                 self.gboundary = None
                 g = len(comm.members(comm.index))
-                self.fc_in = torch.zeros((g * k, a), dtype=torch.float32, device=dev)
+                self.fc_in = Split.alloc("rows", (g * k, a8), a, dev)
                 self.labels = torch.zeros(g * k, dtype=torch.int32, device=dev)
                 eng = BlockEngine(fc_block, (a,), g * k, dev, full0[cut:], vel0[cut:],
                                   need_input_grad=True)
@@ -270,16 +272,21 @@ class StanzaCluster:
         led.tag_messages[Tag.CONTROL] += self.n_conv
         if comm is not None:
             if comm.is_conv:
-                comm.gather_activations(acts.reshape(k, -1), lab_all, None, None, k)
+                comm.gather_activations([acts.plane_rows(p) for p in range(3)] + [lab_all], None)
             else:
-                comm.gather_activations(None, None, self.fc_in, self.labels, k)
+                recv = []
+                for pos in range(len(comm.members(comm.index))):
+                    rows = self.fc_in.rows_view(pos * k, (pos + 1) * k)
+                    recv.append([rows.plane_rows(p) for p in range(3)] +
+                                [self.labels[pos * k:(pos + 1) * k]])
+                comm.gather_activations(None, recv)
 
         mark("fc_compute")
         led.record("fc_compute")
         for j, eng in enumerate(self.fcs):
             lo, hi = eng.rows
             if comm is None:
-                xin = acts.reshape(self.n_conv * k, -1)[lo:hi]
+                xin = acts.rows_view(lo, hi)
                 lab = lab_all[lo:hi]
             else:
                 xin, lab = self.fc_in, self.labels
@@ -292,12 +299,16 @@ class StanzaCluster:
         led.tag_messages[Tag.BOUNDARY_GRADS] += self.n_conv
         if comm is not None:
             if comm.is_conv:
-                comm.scatter_boundary(None, self.gboundary, k)
+                comm.scatter_boundary(None, [self.gboundary.plane_rows(p) for p in range(3)])
             else:
-                comm.scatter_boundary(self.fcs[0].gin[0], None, k)
+                gx = self.fcs[0].gin[0]
+                send = []
+                for pos in range(len(comm.members(comm.index))):
+                    rows = gx.rows_view(pos * k, (pos + 1) * k)
+                    send.append([rows.plane_rows(p) for p in range(3)])
+                comm.scatter_boundary(send, None)
         if self.conv is not None:
-            self.conv.backward(self.gboundary.reshape((self.conv.batch,
-                                                       *self.conv.out_shape)))
+            self.conv.backward(self.gboundary)
 
         mark("exchange")
         ring = lambda p, m: 0 if m == 1 else int(2 * (m - 1) * p * 4)  # noqa: E731
@@ -358,9 +369,8 @@ class StanzaCluster:
         if rank != 0:
             return None
         cut = self.partition.split_index
-        proto = BlockEngine.__new__(BlockEngine)
-        proto.layers = self.partition.fc_block
-        proto._layout_params()
+        proto = BlockEngine(self.partition.fc_block, (self.boundary_activations,), 1,
+                            self.device, allocate=False)
         pf = torch.empty(proto.total, dtype=torch.float32, device=self.device)
         vf = torch.empty_like(pf)
         dist.recv(pf, fc0)

@@ -20,3 +20,12 @@ def lib():
     from paper_1812_10624_b200 import _lib
     build_library()
     return _lib.load()
+
+
+@pytest.fixture(params=[1, 0], ids=["tma", "cp.async"])
+def producer(request, lib):
+    """Run a GPU op test under both GEMM producers (TMA tensor maps and the
+    cp.async gather); restore TMA afterwards."""
+    lib.stz_set_tma(request.param)
+    yield request.param
+    lib.stz_set_tma(1)

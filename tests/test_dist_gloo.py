@@ -29,9 +29,9 @@ def _worker(rank, world, n_conv, n_fc, port, q):
             i = comm.index
             acts = torch.full((k, a), float(i + 1)) + torch.arange(k * a).reshape(k, a) / 100
             labels = torch.full((k,), i, dtype=torch.int32)
-            comm.gather_activations(acts, labels, None, None, k)
+            comm.gather_activations([acts, labels], None)
             gy = torch.zeros(k, a)
-            comm.scatter_boundary(None, gy, k)
+            comm.scatter_boundary(None, [gy])
             out["gy"] = gy
             g = torch.full((7,), float(i + 1))
             comm.allreduce_grads(g)
@@ -40,9 +40,11 @@ def _worker(rank, world, n_conv, n_fc, port, q):
             members = comm.members(comm.index)
             fc_in = torch.zeros(len(members) * k, a)
             fc_lab = torch.zeros(len(members) * k, dtype=torch.int32)
-            comm.gather_activations(None, None, fc_in, fc_lab, k)
+            comm.gather_activations(None, [[fc_in[p * k:(p + 1) * k], fc_lab[p * k:(p + 1) * k]]
+                                           for p in range(len(members))])
             out["fc_in"], out["fc_lab"], out["members"] = fc_in, fc_lab, members
-            comm.scatter_boundary(-fc_in, None, k)
+            neg = -fc_in
+            comm.scatter_boundary([[neg[p * k:(p + 1) * k]] for p in range(len(members))], None)
             g = torch.full((4,), 10.0 * (comm.index + 1))
             comm.allreduce_grads(g)
             out["g"] = g

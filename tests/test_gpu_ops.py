@@ -44,7 +44,7 @@ def tc():
 
 
 @pytest.mark.parametrize("case", ["c3s1p1", "c3s2p0", "c5s1p2", "c11s4p2", "c3s1p0_odd"])
-def test_conv_golden(ops, tc, case):
+def test_conv_golden(ops, tc, producer, case):
     g = ops[f"conv_{case}"]
     c, o, k, s, p = (int(v) for v in g["cfg"][:5])
     layer = tc.Conv2d(c, o, k, s, p)
@@ -70,7 +70,7 @@ def test_maxpool_golden_bit_exact(ops, tc, case):
 
 
 @pytest.mark.parametrize("case", ["fc_small", "fc_mid"])
-def test_fc_golden(ops, tc, case):
+def test_fc_golden(ops, tc, producer, case):
     g = ops[case]
     i, o = g["w"].shape
     layer = tc.FullyConnected(i, o)
@@ -134,11 +134,15 @@ CONV_SHAPES = [  # (N, C, H, W, O, k, s, p) incl. AlexNet-like layer shapes at s
     (1, 384, 13, 13, 256, 3, 1, 1),
     (3, 5, 9, 7, 33, 3, 2, 1),
     (1, 3, 224, 224, 64, 11, 4, 2),
+    (2, 64, 13, 13, 128, 3, 1, 1),
+    (2, 128, 9, 9, 192, 3, 1, 1),
+    (1, 256, 6, 6, 40, 3, 1, 1),
+    (2, 32, 12, 12, 64, 3, 2, 1),
 ]
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES, ids=lambda s: "x".join(map(str, s)))
-def test_conv_vs_oracle(tc, shape):
+def test_conv_vs_oracle(tc, producer, shape):
     n, c, h, w, o, k, s, p = shape
     rng = np.random.Generator(np.random.PCG64(hash(shape) & 0xFFFF))
     x = rng.standard_normal((n, c, h, w)).astype(np.float32)
@@ -157,12 +161,12 @@ def test_conv_vs_oracle(tc, shape):
     assert orc.rel_err(host(gb), rgb) <= 1e-7
 
 
-FC_SHAPES = [(8, 256, 128), (8, 128, 10), (128, 9216, 512), (896, 4096, 1000),
+FC_SHAPES = [(8, 256, 128), (8, 128, 10), (128, 9216, 512), (896, 4096, 1000), (100, 200, 300),
              (5, 11, 7), (33, 1024, 4096)]
 
 
 @pytest.mark.parametrize("shape", FC_SHAPES, ids=lambda s: "x".join(map(str, s)))
-def test_fc_vs_oracle(tc, shape):
+def test_fc_vs_oracle(tc, producer, shape):
     m, i, o = shape
     rng = np.random.Generator(np.random.PCG64(m * 7919 + i * 31 + o))
     x = rng.standard_normal((m, i)).astype(np.float32)
