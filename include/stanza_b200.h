@@ -181,6 +181,18 @@ int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, s
 int stzx_relu_fwd(const void* x, size_t psx, void* y, size_t psy, size_t n, void* stream);
 int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t psx, size_t n,
                   void* stream);
+/* Space-to-depth form of a strided first conv (AlexNet conv1, 11x11/4 on 3
+ * channels): the padded input is regrouped into s x s blocks, giving a
+ * stride-1 ceil(k/s) x ceil(k/s) conv over C*s*s (padded to Cs8) channels
+ * that runs on the TMA kernel; the forward uses stzx_conv_fwd on the packed
+ * tensors, the weight gradient maps back to [O,C,k,k]. */
+int stzx_pack_s2d(const float* x, void* xp, size_t ps, int N, int C, int H, int W, int s, int p,
+                  int Hs, int Ws, int Cs8, void* stream);
+int stzx_pack_conv_w_s2d(const float* w, void* wf, size_t ps, int O, int C, int k, int s,
+                         int Cs8, void* stream);
+int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, float* gw,
+                        float* gb, int N, int C, int Cs8, int Hs, int Ws, int O, int O8, int k,
+                        int s, void* ws, size_t ws_bytes, void* stream);
 /* SoftmaxCE on fp32 logits -> losses + split dlogits [M][C8]. */
 int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
                     int M, int C, int C8, void* stream);

@@ -61,6 +61,9 @@ SIGNATURES = {
     "stzx_relu_fwd": (I, [P, Z, P, Z, Z, P]),
     "stzx_relu_bwd": (I, [P, Z, P, P, Z, Z, P]),
     "stzx_softmax_ce": (I, [P, P, P, P, Z, I, I, I, P]),
+    "stzx_pack_s2d": (I, [P, P, Z, I, I, I, I, I, I, I, I, I, P]),
+    "stzx_pack_conv_w_s2d": (I, [P, P, Z, I, I, I, I, I, P]),
+    "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
 }
 
 

@@ -512,10 +512,23 @@ int run_tgemm(const char* what, int BN, const TgOperand& a, const TgOperand& b, 
   const int npad = rup8(N);
   const size_t per = (size_t)M * npad * sizeof(float);
   const int fit = ws ? (int)(ws_bytes / per) : 1;
+  // split-K: enough work items for the persistent grid, chosen to minimise the
+  // idle tail (items / (waves * SMs)), each split keeping >= 4 k-blocks
   int splits = 1;
-  if (tiles < 2 * num_sms() && nkb >= 8) {
-    splits = cdiv(2 * num_sms(), tiles);
-    if (splits > nkb / 4) splits = nkb / 4;
+  const int sms = num_sms();
+  if (tiles < 2 * sms && nkb >= 8) {
+    double best = 0.0;
+    const int smax = nkb / 4 < fit ? nkb / 4 : fit;
+    for (int sp = 1; sp <= smax && sp <= 64; ++sp) {
+      const int items = tiles * sp;
+      const int waves = cdiv(items, sms);
+      const double eff = (double)items / ((double)waves * sms);
+      // prefer more parallelism only while it pays: require a 3% gain
+      if (eff > best * 1.03 || (items < sms && eff >= best)) {
+        best = eff;
+        splits = sp;
+      }
+    }
   }
   if (g_max_kps > 0 && K > g_max_kps) splits = cdiv(K, g_max_kps);
   if (splits > fit) splits = fit;
@@ -1113,6 +1126,39 @@ int stzx_flat_to_nhwc(const void* y, size_t psy, void* x, size_t psx, int N, int
   flat_to_nhwc_kernel<<<grid_for((size_t)N * H * W * C8), 256, 0, as_stream(stream)>>>(
       cb(y), psy, mb(x), psx, N, C, H, W, C8, D8);
   return check_launch("flat_to_nhwc");
+}
+
+// space-to-depth form of a strided first conv (AlexNet conv1)
+int stzx_pack_s2d(const float* x, void* xp, size_t ps, int N, int C, int H, int W, int s, int p,
+                  int Hs, int Ws, int Cs8, void* stream) {
+  if (Cs8 % 8 || Cs8 < C * s * s) return fail(STZ_EINVAL, "pack_s2d: bad channel padding");
+  const size_t total = (size_t)N * Hs * Ws * Cs8 / 8;
+  if (total == 0) return STZ_OK;
+  pack_s2d_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      x, mb(xp), ps, N, C, H, W, s, p, Hs, Ws, Cs8, FastDiv(Cs8 / 8), FastDiv(Ws), FastDiv(Hs));
+  return check_launch("pack_s2d");
+}
+
+int stzx_pack_conv_w_s2d(const float* w, void* wf, size_t ps, int O, int C, int k, int s,
+                         int Cs8, void* stream) {
+  const int ks = (k + s - 1) / s;
+  pack_s2d_w_kernel<<<grid_for((size_t)O * ks * ks * Cs8), 256, 0, as_stream(stream)>>>(
+      w, mb(wf), ps, O, C, k, s, ks, Cs8);
+  return check_launch("pack_s2d_w");
+}
+
+int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, float* gw,
+                        float* gb, int N, int C, int Cs8, int Hs, int Ws, int O, int O8, int k,
+                        int s, void* ws, size_t ws_bytes, void* stream) {
+  const int ks = (k + s - 1) / s;
+  const int OH = Hs - ks + 1, OW = Ws - ks + 1;
+  if (OH <= 0 || OW <= 0 || Cs8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad_s2d: bad shape");
+  cudaStream_t st = as_stream(stream);
+  EpConvWgradS2D e{gw, ks * ks * Cs8, O, C, k, s, ks, C * s * s, FastDiv(Cs8)};
+  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, Cs8, Hs, Ws, O, O8, ks, 1, 0, OH, OW, ws,
+                           ws_bytes, st);
+  if (rc || !gb) return rc;
+  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st);
 }
 
 }  // extern "C"

@@ -74,6 +74,59 @@ __global__ void unpack_rows_kernel(const bf16_t* __restrict__ xp, size_t ps, flo
   }
 }
 
+// Space-to-depth for a strided first conv (AlexNet conv1: 11x11 stride 4 on
+// 3 channels).  With the input zero-padded by p, window row ih' = oh*s + kh;
+// s2d pixel (i, j) holds channels c' = (dy*s + dx)*C + c of padded input
+// (i*s + dy, j*s + dx).  The conv becomes a stride-1, unpadded k' x k'
+// (k' = ceil(k/s)) conv over C*s*s channels: tap (kh', kw'), channel c'
+// carries original tap (kh'*s + dy, kw'*s + dx) -- zero where that exceeds k.
+// fp32 NCHW -> s2d NHWC split planes [N][Hs][Ws][Cs8]
+__global__ void pack_s2d_kernel(const float* __restrict__ x, bf16_t* __restrict__ xp, size_t ps,
+                                int N, int C, int H, int W, int s, int pad, int Hs, int Ws,
+                                int Cs8, FastDiv d_chunks, FastDiv d_ws, FastDiv d_hs) {
+  const uint32_t total = (uint32_t)N * Hs * Ws * (Cs8 / 8);
+  const int Cs = C * s * s;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    uint32_t pix, cc, r, j, n, i;
+    d_chunks.divmod(t, pix, cc);
+    d_ws.divmod(pix, r, j);
+    d_hs.divmod(r, n, i);
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int cp = (int)cc * 8 + q;
+      float val = 0.f;
+      if (cp < Cs) {
+        const int c = cp % C, d = cp / C, dy = d / s, dx = d % s;
+        const int ih = (int)i * s + dy - pad, iw = (int)j * s + dx - pad;
+        if ((unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W)
+          val = __ldg(x + (((size_t)n * C + c) * H + ih) * W + iw);
+      }
+      v[q] = val;
+    }
+    store_split8(xp + (size_t)pix * Cs8 + cc * 8, ps, v);
+  }
+}
+
+// conv W [O, C, k, k] -> s2d forward B planes wf[O][kh'*ks + kw'][Cs8]
+__global__ void pack_s2d_w_kernel(const float* __restrict__ w, bf16_t* __restrict__ wf,
+                                  size_t ps, int O, int C, int k, int s, int ks, int Cs8) {
+  const size_t total = (size_t)O * ks * ks * Cs8;
+  const int Cs = C * s * s;
+  STZ_GRID_LOOP(i, total) {
+    const int cp = (int)(i % Cs8);
+    const int tap = (int)((i / Cs8) % (ks * ks));
+    const int o = (int)(i / ((size_t)Cs8 * ks * ks));
+    float val = 0.f;
+    if (cp < Cs) {
+      const int c = cp % C, d = cp / C, dy = d / s, dx = d % s;
+      const int kh = (tap / ks) * s + dy, kw = (tap % ks) * s + dx;
+      if (kh < k && kw < k) val = w[(((size_t)o * C + c) * k + kh) * k + kw];
+    }
+    store_split(wf, ps, i, val);
+  }
+}
+
 // conv W [O, C, k, k] -> forward B planes wf[O][tap][C8] (tap = kh*k + kw)
 // and input-gradient B planes wd[C][t][O8] with FLIPPED taps
 // t = (k-1-kh)*k + (k-1-kw), the order in which the input gradient walks

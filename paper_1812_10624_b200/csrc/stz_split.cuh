@@ -282,6 +282,28 @@ struct EpConvWgrad {
   }
 };
 
+// weight gradient of a space-to-depth conv (stz_fmt.cuh pack_s2d_kernel):
+// row m = (tap', c') over Cs8 channels -> gw[o, c, kh'*s+dy, kw'*s+dx],
+// dropping padded channels and taps beyond k
+struct EpConvWgradS2D {
+  float* gw;
+  int M, N, C, k, s, ks, Cs;
+  FastDiv d_cs8;
+  __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
+    if (m >= M) return;
+    uint32_t tap, cp;
+    d_cs8.divmod((uint32_t)m, tap, cp);
+    if ((int)cp >= Cs) return;
+    const int c = (int)cp % C, d = (int)cp / C, dy = d / s, dx = d % s;
+    const int kh = (int)(tap / ks) * s + dy, kw = (int)(tap % ks) * s + dx;
+    if (kh >= k || kw >= k) return;
+    const size_t base = ((size_t)c * k + kh) * k + kw;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (n0 + j < N) gw[(size_t)(n0 + j) * C * k * k + base] = v[j];
+  }
+};
+
 // ---------------------------------------------------------------------------
 // the tcgen05 split-plane GEMM
 // ---------------------------------------------------------------------------

@@ -101,6 +101,7 @@ class _Op:
     relu_bwd_fused: bool = False
     skip_dgrad: bool = False
     flat_out: bool = False    # maxpool: writes the CHW-flat tensor for a following Flatten
+    s2d: tuple | None = None  # first strided conv as space-to-depth: (ks, Cs8, Hs, Ws)
 
 
 class BlockEngine:
@@ -163,6 +164,15 @@ class BlockEngine:
                 op.relu_bwd_fused = True
         if ops and not self.need_input_grad:
             ops[0].skip_dgrad = True
+            # a strided first conv on few channels (AlexNet conv1) runs as a
+            # stride-1 conv over space-to-depth blocks: TMA-eligible channels
+            l0 = ops[0].layer
+            if ops[0].kind == "conv" and l0.stride > 1 and rup8(l0.in_ch) < 32 \
+                    and l0.in_ch * l0.stride ** 2 <= 256:
+                ks = -(-l0.kernel // l0.stride)
+                cs8 = -(-(l0.in_ch * l0.stride ** 2) // 32) * 32
+                _, oh, ow = ops[0].out_shape
+                ops[0].s2d = (ks, cs8, oh - 1 + ks, ow - 1 + ks)
         self.ops = ops
 
     def _layout_params(self):
@@ -187,6 +197,9 @@ class BlockEngine:
             l = op.layer
             if op.kind == "conv":
                 kk, c8, o8 = l.kernel * l.kernel, rup8(l.in_ch), rup8(l.out_ch)
+                if op.s2d is not None:
+                    ks, cs8, _, _ = op.s2d
+                    kk, c8 = ks * ks, cs8
                 wf = torch.zeros((3, l.out_ch, kk * c8), dtype=torch.bfloat16, device=dev)
                 wd = None if op.skip_dgrad else torch.zeros((3, l.in_ch, kk * o8),
                                                             dtype=torch.bfloat16, device=dev)
@@ -276,7 +289,10 @@ class BlockEngine:
             op = self.ops[i]
             l = op.layer
             w = self.params[i][0]
-            if op.kind == "conv":
+            if op.kind == "conv" and op.s2d is not None:
+                _lib.call("stzx_pack_conv_w_s2d", ptr(w), ptr(a), a[0].numel(), l.out_ch,
+                          l.in_ch, l.kernel, l.stride, op.s2d[1], st)
+            elif op.kind == "conv":
                 _lib.call("stzx_pack_conv_w", ptr(w), ptr(a), a[0].numel(), ptr(b),
                           0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kernel,
                           rup8(l.in_ch), rup8(l.out_ch), st)
@@ -324,10 +340,22 @@ class BlockEngine:
             raise ShapeMismatch(f"block expects {(self.batch, *self.in_shape)}, "
                                 f"got {tuple(x.shape)}")
         st = stream_of(self.device)
+        op0 = self.ops[0]
         if self.xin is None:
-            self.xin = self._split_for(self.in_shape, self.batch)
+            if op0.s2d is not None:
+                ks, cs8, hs, ws_ = op0.s2d
+                l0 = op0.layer
+                self.xin = Split.alloc("nhwc", (self.batch, hs, ws_, cs8),
+                                       l0.in_ch * l0.stride ** 2, self.device)
+            else:
+                self.xin = self._split_for(self.in_shape, self.batch)
         s = self.xin
-        if s.layout == "nhwc":
+        if op0.s2d is not None:
+            ks, cs8, hs, ws_ = op0.s2d
+            c, h, w = self.in_shape
+            _lib.call("stzx_pack_s2d", ptr(x), s.ptr(), s.ps, self.batch, c, h, w,
+                      op0.layer.stride, op0.layer.padding, hs, ws_, cs8, st)
+        elif s.layout == "nhwc":
             c, h, w = self.in_shape
             _lib.call("stzx_pack_nchw", ptr(x), s.ptr(), s.ps, self.batch, c, h, w, s.width, st)
         else:
@@ -354,9 +382,13 @@ class BlockEngine:
                 c, h, w = op.in_shape
                 y = self.acts[i]
                 wf, _ = self.wplanes[i]
+                k, cs, pd = l.kernel, l.stride, l.padding
+                if op.s2d is not None:             # stride-1 conv over s2d blocks
+                    k, _, h, w = op.s2d
+                    cs, pd = 1, 0
                 _lib.call("stzx_conv_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
                           ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w, l.out_ch,
-                          y.width, l.kernel, l.stride, l.padding, int(op.fused_relu), ptr(ws),
+                          y.width, k, cs, pd, int(op.fused_relu), ptr(ws),
                           ws.numel(), st, flops=self.op_flops(i), tag=f"conv{i}_fwd")
             elif op.kind == "fc":
                 wp, _ = self.wplanes[i]
@@ -439,6 +471,14 @@ class BlockEngine:
                           mptr, b, c, out.width, h, w, l.kernel, l.stride,
                           g.width if op.flat_out else 0, st)
                 g = out
+            elif op.kind == "conv" and op.s2d is not None:
+                ks, cs8, hs, ws_ = op.s2d
+                _lib.call("stzx_conv_wgrad_s2d", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), b, l.in_ch, cs8, hs, ws_,
+                          l.out_ch, g.width, l.kernel, l.stride, ptr(ws), ws.numel(), st,
+                          flops=self.op_flops(i), tag=f"conv{i}_wgrad")
+                g = None
+                continue
             elif op.kind == "conv":
                 c, h, w = op.in_shape
                 _lib.call("stzx_conv_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,

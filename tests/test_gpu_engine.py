@@ -1,0 +1,83 @@
+"""BlockEngine (the fused hot path on split-plane tensors) vs the oracle at
+the block level: forward output, parameter-gradient sums and the block input
+gradient, for the layer stacks the bench runs (AlexNet conv1 as
+space-to-depth, TMA im2col convs, pool -> flatten -> FC boundary)."""
+
+import numpy as np
+import pytest
+import torch
+
+import stanza_oracle as orc
+
+pytestmark = pytest.mark.gpu
+TOL = 3e-6
+
+
+def _run(layers, in_shape, batch, need_input_grad, seed):
+    from paper_1812_10624_b200.engine import BlockEngine
+    from paper_1812_10624_b200.tensor_core import as_tuple, seeded_init
+    params = seeded_init(layers, seed)
+    eng = BlockEngine(layers, in_shape, batch, "cuda:0", params,
+                      need_input_grad=need_input_grad)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = rng.standard_normal((batch, *in_shape)).astype(np.float32)
+    out = eng.forward(torch.from_numpy(x).cuda())
+    oshape = eng.out_shape
+    gy = rng.standard_normal((batch, *oshape)).astype(np.float32)
+    # feed gy in the engine's layout: rows for a flat output
+    from paper_1812_10624_b200 import _lib
+    from paper_1812_10624_b200.engine import Split, rup8
+    from paper_1812_10624_b200.tensor_core import ptr, stream_of
+    if out.layout == "rows":
+        g = Split.alloc("rows", (batch, rup8(oshape[0])), oshape[0], "cuda:0")
+        _lib.call("stzx_pack_rows", ptr(torch.from_numpy(gy).cuda()), g.ptr(), g.ps, batch,
+                  oshape[0], g.width, stream_of(torch.device("cuda:0")))
+        got = out.to_float()[:, :oshape[0]]
+    else:
+        c, h, w = oshape
+        g = Split.alloc("nhwc", (batch, h, w, rup8(c)), c, "cuda:0")
+        _lib.call("stzx_pack_nchw", ptr(torch.from_numpy(gy).cuda()), g.ptr(), g.ps, batch, c, h,
+                  w, g.width, stream_of(torch.device("cuda:0")))
+        got = out.to_float()[..., :c].permute(0, 3, 1, 2)
+    gin = eng.backward(g)
+    torch.cuda.synchronize()
+    tl = [as_tuple(l) for l in layers]
+    ry, caches = orc.block_forward(tl, params, x)
+    rgx, rgrads = orc.block_backward(tl, params, caches, gy)
+    assert orc.rel_err(got.cpu().numpy(), ry) <= TOL
+    for li, (gl, rl) in enumerate(zip(eng.grads, rgrads)):
+        for a, b in zip(gl, rl):
+            assert orc.rel_err(a.cpu().numpy(), b) <= TOL, f"layer {li}"
+    if need_input_grad:
+        c, h, w = in_shape
+        assert orc.rel_err(gin.to_float()[..., :c].permute(0, 3, 1, 2).cpu().numpy(), rgx) <= TOL
+    return eng
+
+
+def test_alexnet_conv1_space_to_depth():
+    from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
+    eng = _run([Conv2d(3, 64, 11, 4, 2), ReLU(), MaxPool2d(3, 2)], (3, 224, 224), 2, False, 1)
+    assert eng.ops[0].s2d == (3, 64, 57, 57)
+
+
+def test_alexnet_conv2_to_pool_tma():
+    from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
+    _run([Conv2d(64, 192, 5, 1, 2), ReLU(), MaxPool2d(3, 2)], (64, 27, 27), 2, True, 2)
+
+
+def test_alexnet_conv5_pool_flatten_boundary():
+    from paper_1812_10624_b200.tensor_core import Conv2d, Flatten, MaxPool2d, ReLU
+    _run([Conv2d(256, 256, 3, 1, 1), ReLU(), MaxPool2d(3, 2), Flatten()], (256, 13, 13), 3, True,
+         3)
+
+
+def test_vgg_stage_conv_conv_pool():
+    from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
+    _run([Conv2d(64, 128, 3, 1, 1), ReLU(), Conv2d(128, 128, 3, 1, 1), ReLU(), MaxPool2d(2, 2)],
+         (64, 28, 28), 2, True, 4)
+
+
+def test_flatten_without_pool_relayout():
+    from paper_1812_10624_b200.tensor_core import Conv2d, Flatten, FullyConnected, ReLU
+    _run([Conv2d(8, 16, 3, 1, 1), ReLU(), Flatten(), FullyConnected(16 * 6 * 6, 24), ReLU()],
+         (8, 6, 6), 4, True, 5)
