@@ -454,13 +454,16 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16_t* __res
   }
 }
 
-__global__ void colsum_final_kernel(const double* __restrict__ part, int blocks, int N, int N8,
-                                    float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+// one warp per column: lane-strided partial sums + a fixed shuffle tree
+__global__ void __launch_bounds__(256) colsum_final_kernel(const double* __restrict__ part,
+                                                           int blocks, int N, int N8,
+                                                           float* __restrict__ out) {
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= N) return;
   double s = 0.0;
-  for (int b = 0; b < blocks; ++b) s += part[(size_t)b * N8 + c];
-  out[c] = (float)s;
+  for (int b = lane; b < blocks; b += 32) s += part[(size_t)b * N8 + c];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[c] = (float)s;
 }
 
 }  // namespace stz

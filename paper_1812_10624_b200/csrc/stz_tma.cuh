@@ -51,17 +51,17 @@ struct alignas(64) TgParams {
 constexpr int TG_BM = 128, TG_BK = 32;
 constexpr int TG_THREADS = 256;  // w0 TMA (32 lanes), w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
 
-template <int BN>
+template <int BN, int NSETS = 2>
 struct TgCfg {
   static constexpr int A_BYTES = TG_BM * TG_BK * 2;  // one plane, 8 KB
   static constexpr int B_BYTES = BN * TG_BK * 2;
   static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;  // + alignment slack + barriers
-  // two accumulator SETS (double-buffered across tiles), each = big + small
+  // NSETS accumulator sets (2 = double-buffered across tiles), each = big + small
   static constexpr int ACC_COLS = 2 * BN;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 256 ? 256 : 512;
-  static_assert(2 * ACC_COLS <= 512, "BN too wide for double-buffered TMEM");
+  static constexpr int TMEM_COLS = NSETS * ACC_COLS <= 256 ? 256 : 512;
+  static_assert(NSETS * ACC_COLS <= 512, "BN too wide for the TMEM sets");
   static_assert(STAGES >= 3, "tile too large");
   static_assert(B_BYTES % 512 == 0, "B plane blocks must stay 512-byte aligned (SW64 atoms)");
 };
@@ -154,10 +154,10 @@ __device__ __forceinline__ uint64_t tg_desc(int mode, uint32_t plane_base, int k
 // Persistent: grid = min(#work items, #SMs); work item w -> (split z, m tile,
 // n tile), n fastest so consecutive items share the A tile in L2.  TMEM holds
 // two accumulator sets; the epilogue of item i overlaps the mainloop of i+1.
-template <int BN, class EP>
+template <int BN, int NSETS, class EP>
 __global__ void __launch_bounds__(TG_THREADS, 1)
     tgemm_kernel(const __grid_constant__ TgParams<EP> p) {
-  using Cfg = TgCfg<BN>;
+  using Cfg = TgCfg<BN, NSETS>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -232,8 +232,9 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
       const int z = w / (mt * nt);
       const int kbeg = z * p.k_per_split, kend = min(p.K, kbeg + p.k_per_split);
       const int nkb = cdiv(kend - kbeg, TG_BK);
-      const int acc = it & 1;
-      mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+      const int acc = NSETS == 2 ? (it & 1) : 0;
+      const int use = NSETS == 2 ? (it >> 1) : it;   // how often this set was used before
+      mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t tbig = tmem_base + acc * Cfg::ACC_COLS, tsmall = tbig + BN;
       for (int kb = 0; kb < nkb; ++kb, ++g) {
@@ -265,8 +266,9 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int z = w / (mt * nt), rem = w % (mt * nt);
       const int m0 = (rem / nt) * TG_BM, n0 = (rem % nt) * BN;
-      const int acc = it & 1;
-      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      const int acc = NSETS == 2 ? (it & 1) : 0;
+      const int use = NSETS == 2 ? (it >> 1) : it;
+      mbar_wait(&tfull_bar[acc], use & 1);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
