@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool", type=int, default=4, help="device-resident input batches")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph (N=1 uses graphs)")
     return ap.parse_args()
 
 
@@ -145,7 +146,7 @@ class ClockSampler:
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -290,7 +291,26 @@ def main():
         one(i, slots[i % slots.numel():i % slots.numel() + 1])
     sync_all()
 
+    # single device: one CUDA graph per pooled batch (the whole step, captured)
+    graphs = None
+    if world == 1 and not args.eager:
+        graph_slots = torch.zeros((args.pool, 1), dtype=torch.float64, device=dev)
+        graphs = [cl.capture(pool_x[j], pool_y[j], graph_slots[j]) for j in range(args.pool)]
+        for j in range(args.pool):
+            graphs[j].replay()
+        torch.cuda.synchronize(dev)
+
+        def one(i, slot=None):  # noqa: F811 -- the graph replay replaces the eager step
+            graphs[i % args.pool].replay()
+
     # ---- timed region: device-resident inputs ------------------------------------
+    n0 = lib.stz_launch_count()
+    if is_conv_rank:
+        cl.step(slots[0:1], x=pool_x[0], labels=pool_y[0])
+    else:
+        cl.step(slots[0:1])
+    torch.cuda.synchronize(dev)
+    per_step_launches = lib.stz_launch_count() - n0
     launches0 = lib.stz_launch_count()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -302,6 +322,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
     launches = lib.stz_launch_count() - launches0
+    if graphs is not None:   # replays launch the captured kernels without host calls
+        launches = per_step_launches * args.steps
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -318,6 +340,10 @@ def main():
         yh = pool_y[0].cpu().pin_memory()
         h2d = xh.numel() * 4 + yh.numel() * 4
     loss_h = torch.zeros(args.steps, dtype=torch.float64).pin_memory()
+    g_e2e = None
+    if graphs is not None:
+        e2e_slot = torch.zeros(1, dtype=torch.float64, device=dev)
+        g_e2e = cl.capture(cl.x, cl.labels, e2e_slot)
     sync_all()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
@@ -326,8 +352,12 @@ def main():
         if is_conv_rank:
             cl.x.copy_(xh, non_blocking=True)
             cl.labels.copy_(yh, non_blocking=True)
-        cl.step(slots[i:i + 1])
-        loss_h[i:i + 1].copy_(slots[i:i + 1], non_blocking=True)
+        if g_e2e is not None:
+            g_e2e.replay()
+            loss_h[i:i + 1].copy_(e2e_slot, non_blocking=True)
+        else:
+            cl.step(slots[i:i + 1])
+            loss_h[i:i + 1].copy_(slots[i:i + 1], non_blocking=True)
     e3.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = torch.tensor([e2.elapsed_time(e3) / args.steps], dtype=torch.float64, device=dev)
@@ -342,7 +372,10 @@ def main():
     _lib.PROFILE_HOOK = timer
     cl.time_phases = True
     cl._pending_events = []
-    one(0)
+    if is_conv_rank:
+        cl.step(None, x=pool_x[0], labels=pool_y[0])
+    else:
+        cl.step(None)
     _lib.PROFILE_HOOK = None
     cl._resolve_phase_times()
     cl.time_phases = False
@@ -431,6 +464,7 @@ def main():
                     "api": "StanzaCluster.step after pinned-host copies of the batch; "
                            "loss copied back every step"},
             "gpu_launches": int(sum(o["launches"] for o in objs)),
+            "cuda_graph": bool(graphs is not None),
             "clocks": clocks.summary(),
             "fc_tensor_pipe_frac": (6 * fc_ex["fc_tflops"] / bf16_peak)
             if fc_ex["fc_tflops"] else None,

@@ -335,6 +335,28 @@ class StanzaCluster:
         if ev is not None:
             self._pending_events.append(ev)
 
+    def capture(self, x: torch.Tensor | None = None, labels: torch.Tensor | None = None,
+                loss_slot: torch.Tensor | None = None) -> "torch.cuda.CUDAGraph":
+        """Capture one whole iteration (every kernel of conv fwd, FC step,
+        conv bwd, update) as a CUDA graph on device-resident inputs; replay()
+        runs it with no host launch overhead.  Single-device mode only (the
+        NCCL exchanges of the one-process-per-GPU mode stay eager).  Call
+        once eagerly first so every kernel attribute / tensor map is set."""
+        if self.comm is not None:
+            raise RuntimeError("graph capture covers the single-device deployment")
+        slot = loss_slot
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                if slot is not None:
+                    slot.zero_()
+                self.step(slot, x=x, labels=labels)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        # the ledger recorded the captured step once; it describes a replay
+        return g
+
     # -- public API ------------------------------------------------------------------
 
     def train(self, iterations: int) -> StanzaResult:
