@@ -44,6 +44,15 @@ unsigned long long stz_launch_count(void);
  * tests run both and compare). */
 int stz_set_tma(int on);
 
+/* 1 (default): GEMMs with >= 2 row tiles run on CTA pairs (cta_group::2
+ * UMMA, 256-row tiles, each CTA stages half of the B tile); 0: one CTA per
+ * 128-row tile.  The GPU tests run both. */
+int stz_set_cluster(int on);
+
+/* GEMM pipeline diagnostics (results are WRONG while set): 1 skips epilogue
+ * stores, 2 skips the MMAs, 4 skips the TMA loads.  0 = normal. */
+int stz_set_debug(int flags);
+
 /* Tuning/experiment knob: cap the K extent one CTA accumulates (0 = auto). */
 int stz_set_max_k_per_split(int k);
 

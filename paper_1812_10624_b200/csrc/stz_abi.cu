@@ -441,6 +441,8 @@ bool op_tiled_k(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int 
   op = TgOperand{};
   op.mode = TG_TILED_K;
   op.nbox = 1;
+  op.box_rows = R;
+  op.box_bytes = R * 64;
   for (int pl = 0; pl < 3; ++pl)
     if (!enc_tiled(&op.map[pl], p + pl * ps, (uint64_t)K, (uint64_t)rows, (uint64_t)ld, 32,
                    (uint32_t)R))
@@ -453,6 +455,7 @@ bool op_tiled_mn(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int
   op = TgOperand{};
   op.mode = TG_TILED_MN;
   op.nbox = R / 32;
+  op.box_bytes = 2048;
   for (int pl = 0; pl < 3; ++pl)
     if (!enc_tiled(&op.map[pl], p + pl * ps, (uint64_t)rows, (uint64_t)K, (uint64_t)ld, 32, 32))
       return false;
@@ -466,6 +469,7 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
   op = TgOperand{};
   op.mode = mn ? TG_IM2COL_MN : TG_IM2COL_K;
   op.nbox = mn ? R / 32 : 1;
+  op.box_bytes = 2048;
   op.lo = lo;
   op.s = s;
   op.C8 = C8;
@@ -480,37 +484,69 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
   return true;
 }
 
-// tile width: 64 for thin outputs; 192 with a single TMEM accumulator set
-// when N is a multiple of 192 (192 / 384 channels: 30% fewer operand bytes
-// per MMA cycle than two 96-wide tiles -- the split planes make these GEMMs
-// L2->SM bandwidth bound); else 128 with double-buffered TMEM
-int tg_pick_bn(int N) {
-  if (N <= 64) return 64;
-  if (N % 192 == 0) return 192;
-  if (N % 96 == 0 && N % 128 != 0) return 96;
-  return 128;
+// Tile shape.  The split-plane GEMMs are bound by the L2 -> SM operand feed
+// (measured with stz_set_debug: skipping the MMAs barely shortens them,
+// skipping the loads halves them), so the choice minimises operand bytes per
+// MMA cycle: CTA pairs (cta_group::2, 256-row tiles, each CTA stages half of
+// B) when there are >= 2 row tiles; width 256 / 192 with one TMEM set when N
+// allows, else 128 double-buffered, 64 for thin outputs.
+int g_use_cluster = 1;   // CTA pairs (stz_set_cluster)
+int g_debug = 0;         // GEMM pipeline diagnostics (stz_set_debug)
+
+struct TgShape {
+  int BN, CL;
+};
+
+TgShape tg_shape(int M, int N) {
+  TgShape t;
+  if (N <= 64) t.BN = 64;
+  else if (N % 256 == 0) t.BN = 256;
+  else if (N % 192 == 0) t.BN = 192;
+  else if (N % 96 == 0 && N % 128 != 0) t.BN = 96;
+  else t.BN = 128;
+  t.CL = (g_use_cluster && cdiv(M, TG_BM) >= 2 && (t.BN / 2) % 32 == 0) ? 2 : 1;
+  if (t.CL == 1 && t.BN == 256) t.BN = 128;   // unpaired: keep the double-buffered TMEM sets
+  return t;
 }
 
-template <int BN, int NSETS, class EP>
+template <int BN, int NSETS, int CL, class EP>
 void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
-  using Cfg = TgCfg<BN, NSETS>;
+  using Cfg = TgCfg<BN, NSETS, CL>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tgemm_kernel<BN, NSETS, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg::SMEM);
+    cudaFuncSetAttribute(tgemm_kernel<BN, NSETS, CL, EP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr_set = true;
   }
-  const int items = cdiv(prm.M, TG_BM) * cdiv(prm.N, BN) * splits;
-  const int grid = items < num_sms() ? items : num_sms();
-  tgemm_kernel<BN, NSETS, EP><<<grid, TG_THREADS, Cfg::SMEM, st>>>(prm);
+  const int items = cdiv(prm.M, TG_BM * CL) * cdiv(prm.N, BN) * splits;
+  const int max_ctas = num_sms() / CL * CL;
+  const int grid = items * CL < max_ctas ? items * CL : max_ctas;
+  if (CL == 1) {
+    tgemm_kernel<BN, NSETS, CL, EP><<<grid, TG_THREADS, Cfg::SMEM, st>>>(prm);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TG_THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, tgemm_kernel<BN, NSETS, CL, EP>, prm);
 }
 
 // C[M,N] = A . B with TMA operands built for tile width BN
 template <class EP>
-int run_tgemm(const char* what, int BN, const TgOperand& a, const TgOperand& b, const EP& ep,
+int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand& b, const EP& ep,
               int M, int N, int K, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (M <= 0 || N <= 0) return STZ_OK;
-  const int tiles = cdiv(M, TG_BM) * cdiv(N, BN);
+  const int BN = sh.BN, CL = sh.CL;
+  const int tiles = cdiv(M, TG_BM * CL) * cdiv(N, BN);
   const int nkb = cdiv(K, TG_BK);
   const int npad = rup8(N);
   const size_t per = (size_t)M * npad * sizeof(float);
@@ -518,7 +554,7 @@ int run_tgemm(const char* what, int BN, const TgOperand& a, const TgOperand& b, 
   // split-K: enough work items for the persistent grid, chosen to minimise the
   // idle tail (items / (waves * SMs)), each split keeping >= 4 k-blocks
   int splits = 1;
-  const int sms = num_sms();
+  const int sms = num_sms() / CL;   // work items run one per CTA pair
   if (tiles < 2 * sms && nkb >= 8) {
     double best = 0.0;
     const int smax = nkb / 4 < fit ? nkb / 4 : fit;
@@ -547,10 +583,18 @@ int run_tgemm(const char* what, int BN, const TgOperand& a, const TgOperand& b, 
   prm.N = N;
   prm.K = K;
   prm.k_per_split = kps;
-  if (BN == 64) launch_tg<64, 2>(prm, splits, st);
-  else if (BN == 96) launch_tg<96, 2>(prm, splits, st);
-  else if (BN == 192) launch_tg<192, 1>(prm, splits, st);
-  else launch_tg<128, 2>(prm, splits, st);
+  prm.debug = g_debug;
+  if (CL == 2) {
+    if (BN == 64) launch_tg<64, 2, 2>(prm, splits, st);
+    else if (BN == 256) launch_tg<256, 1, 2>(prm, splits, st);
+    else if (BN == 192) launch_tg<192, 1, 2>(prm, splits, st);
+    else launch_tg<128, 2, 2>(prm, splits, st);
+  } else {
+    if (BN == 64) launch_tg<64, 2, 1>(prm, splits, st);
+    else if (BN == 96) launch_tg<96, 2, 1>(prm, splits, st);
+    else if (BN == 192) launch_tg<192, 1, 1>(prm, splits, st);
+    else launch_tg<128, 2, 1>(prm, splits, st);
+  }
   int rc = check_launch(what);
   if (rc) return rc;
   if (splits > 1) {
@@ -608,11 +652,11 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
                   size_t ws_bytes, cudaStream_t st) {
   const int M = N * OH * OW, K = k * k * C8;
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
-    const int BN = tg_pick_bn(O);
+    const TgShape sh = tg_shape(M, O);
     TgOperand a, b;
     if (op_im2col(a, false, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
-        op_tiled_k(b, wf, psw, O, K, K, BN))
-      return run_tgemm("conv_fwd[tma]", BN, a, b, ep, M, O, K, ws, ws_bytes, st);
+        op_tiled_k(b, wf, psw, O, K, K, sh.BN / sh.CL))
+      return run_tgemm("conv_fwd[tma]", sh, a, b, ep, M, O, K, ws, ws_bytes, st);
   }
   SvConvFwdA va = conv_fwd_A(x, psx, N, C8, H, W, k, s, p, OH, OW);
   SvRowsK vb{wf, psw, O, K, K};
@@ -625,11 +669,11 @@ int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, c
                     void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = N * H * W, K = k * k * O8;
   if (tma_on() && O8 % 32 == 0 && s == 1 && p - (k - 1) >= -128 && p <= 127) {
-    const int BN = tg_pick_bn(C);
+    const TgShape sh = tg_shape(M, C);
     TgOperand a, b;
     if (op_im2col(a, false, g, psg, N, OH, OW, O8, k, 1, p - (k - 1), -p, H, W, TG_BM) &&
-        op_tiled_k(b, wd, psw, C, K, K, BN))
-      return run_tgemm("conv_dgrad[tma]", BN, a, b, ep, M, C, K, ws, ws_bytes, st);
+        op_tiled_k(b, wd, psw, C, K, K, sh.BN / sh.CL))
+      return run_tgemm("conv_dgrad[tma]", sh, a, b, ep, M, C, K, ws, ws_bytes, st);
   }
   SvConvDgradA va = conv_dgrad_A(g, psg, N, H, W, O8, k, s, p, OH, OW);
   SvRowsK vb{wd, psw, C, K, K};
@@ -642,11 +686,11 @@ int gemm_conv_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, co
                     void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = k * k * C8, P = N * OH * OW;
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128) {
-    const int BN = tg_pick_bn(O);
+    const TgShape sh = tg_shape(M, O);
     TgOperand a, b;
     if (op_im2col(a, true, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
-        op_tiled_mn(b, g, psg, O, P, O8, BN))
-      return run_tgemm("conv_wgrad[tma]", BN, a, b, ep, M, O, P, ws, ws_bytes, st);
+        op_tiled_mn(b, g, psg, O, P, O8, sh.BN / sh.CL))
+      return run_tgemm("conv_wgrad[tma]", sh, a, b, ep, M, O, P, ws, ws_bytes, st);
   }
   SvConvWgradA va = conv_wgrad_A(x, psx, N, C8, H, W, k, s, p, OH, OW);
   SvRowsMN vb{g, psg, O, P, O8};
@@ -658,10 +702,10 @@ int gemm_fc_fwd(const bf16_t* x, size_t psx, const bf16_t* w, size_t psw, const 
                 int in_dim, int I8, int out_dim, int O8, void* ws, size_t ws_bytes,
                 cudaStream_t st) {
   if (tma_on()) {
-    const int BN = tg_pick_bn(out_dim);
+    const TgShape sh = tg_shape(M, out_dim);
     TgOperand a, b;
-    if (op_tiled_k(a, x, psx, M, I8, I8, TG_BM) && op_tiled_mn(b, w, psw, out_dim, in_dim, O8, BN))
-      return run_tgemm("fc_fwd[tma]", BN, a, b, ep, M, out_dim, I8, ws, ws_bytes, st);
+    if (op_tiled_k(a, x, psx, M, I8, I8, TG_BM) && op_tiled_mn(b, w, psw, out_dim, in_dim, O8, sh.BN / sh.CL))
+      return run_tgemm("fc_fwd[tma]", sh, a, b, ep, M, out_dim, I8, ws, ws_bytes, st);
   }
   SvRowsK va{x, psx, M, I8, I8};
   SvRowsMN vb{w, psw, out_dim, in_dim, O8};
@@ -672,10 +716,10 @@ template <class EP>
 int gemm_fc_dgrad(const bf16_t* g, size_t psg, const bf16_t* w, size_t psw, const EP& ep, int M,
                   int in_dim, int O8, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (tma_on()) {
-    const int BN = tg_pick_bn(in_dim);
+    const TgShape sh = tg_shape(M, in_dim);
     TgOperand a, b;
-    if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM) && op_tiled_k(b, w, psw, in_dim, O8, O8, BN))
-      return run_tgemm("fc_dgrad[tma]", BN, a, b, ep, M, in_dim, O8, ws, ws_bytes, st);
+    if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM) && op_tiled_k(b, w, psw, in_dim, O8, O8, sh.BN / sh.CL))
+      return run_tgemm("fc_dgrad[tma]", sh, a, b, ep, M, in_dim, O8, ws, ws_bytes, st);
   }
   SvRowsK va{g, psg, M, O8, O8};
   SvRowsK vb{w, psw, in_dim, O8, O8};
@@ -687,11 +731,11 @@ int gemm_fc_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, cons
                   int in_dim, int I8, int out_dim, int O8, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
   if (tma_on()) {
-    const int BN = tg_pick_bn(out_dim);
+    const TgShape sh = tg_shape(in_dim, out_dim);
     TgOperand a, b;
     if (op_tiled_mn(a, x, psx, in_dim, M, I8, TG_BM) &&
-        op_tiled_mn(b, g, psg, out_dim, M, O8, BN))
-      return run_tgemm("fc_wgrad[tma]", BN, a, b, ep, in_dim, out_dim, M, ws, ws_bytes, st);
+        op_tiled_mn(b, g, psg, out_dim, M, O8, sh.BN / sh.CL))
+      return run_tgemm("fc_wgrad[tma]", sh, a, b, ep, in_dim, out_dim, M, ws, ws_bytes, st);
   }
   SvRowsMN va{x, psx, in_dim, M, I8};
   SvRowsMN vb{g, psg, out_dim, M, O8};
@@ -731,6 +775,16 @@ unsigned long long stz_launch_count(void) { return g_launches; }
 
 int stz_set_tma(int on) {
   g_use_tma = on ? 1 : 0;
+  return STZ_OK;
+}
+
+int stz_set_cluster(int on) {
+  g_use_cluster = on ? 1 : 0;
+  return STZ_OK;
+}
+
+int stz_set_debug(int flags) {
+  g_debug = flags;
   return STZ_OK;
 }
 

@@ -188,8 +188,24 @@ struct SvConvWgradA {
 };
 
 // ---------------------------------------------------------------------------
-// epilogues: store8(m, n0, v) for 8 consecutive columns n0..n0+7 of row m
+// epilogues: store8(m, n0, v) for 8 consecutive columns n0..n0+7 of row m.
+// HAS_BIAS epilogues split it as bias8(n0, b) (column bias, 0 past N) +
+// store8_nb(m, n0, v + b), so the TMA kernel can issue the bias loads before
+// its TMEM loads and keep them off the critical path.
 // ---------------------------------------------------------------------------
+
+// 8 consecutive fp32 values at p (n0 .. n0+7, zeros at n >= N)
+__device__ __forceinline__ void ldg8_f32(const float* p, int n0, int N, float (&b)[8]) {
+  if (n0 + 8 <= N && (reinterpret_cast<uintptr_t>(p + n0) & 15) == 0) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(p + n0));
+    const float4 y = __ldg(reinterpret_cast<const float4*>(p + n0) + 1);
+    b[0] = x.x; b[1] = x.y; b[2] = x.z; b[3] = x.w;
+    b[4] = y.x; b[5] = y.y; b[6] = y.z; b[7] = y.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = n0 + j < N ? __ldg(p + n0 + j) : 0.f;
+  }
+}
 
 // split planes, row-major [M][ld] (NHWC pixels or flat rows); columns in
 // [N, ld) are written as zeros (channel padding).  bias / ReLU / ReLU-mask
@@ -201,23 +217,45 @@ struct EpSplit {
   const float* bias;
   const bf16_t* mask;
   int relu;
-  __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
+  static constexpr bool HAS_BIAS = true;
+  __device__ __forceinline__ void bias8(int n0, float (&b)[8]) const {
+    if (bias) {
+      ldg8_f32(bias, n0, N, b);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = 0.f;
+    }
+  }
+  // v already includes the bias
+  __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const {
     if (m >= M || n0 >= ld) return;
     const size_t base = (size_t)m * ld + n0;
+    uint4 mk = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (mask) mk = __ldg(reinterpret_cast<const uint4*>(mask + base));   // 8 bf16, 16-B aligned
+    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int n = n0 + j;
       float x = v[j];
-      if (n < N) {
-        if (bias) x = __fadd_rn(x, __ldg(bias + n));
+      if (n0 + j < N) {
         if (relu && x < 0.f) x = 0.f;
-        if (mask && !(bf2f(mask[base + j]) > 0.f)) x = 0.f;
+        // bf16 > 0: sign bit clear and not +0 (mask = plane 0 of a ReLU output)
+        const uint32_t h = (mw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+        if (mask && !(h != 0u && h < 0x8000u)) x = 0.f;
       } else {
         x = 0.f;
       }
       v[j] = x;
     }
     store_split8(out + base, ps, v);
+  }
+  __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
+    if (bias && n0 < N) {
+      float b[8];
+      bias8(n0, b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __fadd_rn(v[j], b[j]);
+    }
+    store8_nb(m, n0, v);
   }
 };
 
@@ -231,7 +269,16 @@ struct EpF32 {
   const float* bias;
   const float* mask;  // fp32, same indexing as out
   int relu;
-  __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
+  static constexpr bool HAS_BIAS = true;
+  __device__ __forceinline__ void bias8(int n0, float (&b)[8]) const {
+    if (bias) {
+      ldg8_f32(bias, n0, N, b);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = 0.f;
+    }
+  }
+  __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const {
     if (m >= M) return;
     uint32_t q, r;
     d_m.divmod((uint32_t)m, q, r);
@@ -241,7 +288,6 @@ struct EpF32 {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float x = v[j];
-        if (bias) x = __fadd_rn(x, __ldg(bias + n0 + j));
         if (relu && x < 0.f) x = 0.f;
         w[j] = x;
       }
@@ -256,11 +302,19 @@ struct EpF32 {
       if (n >= N) break;
       const long long idx = row + (long long)n * ld_n;
       float x = v[j];
-      if (bias) x = __fadd_rn(x, __ldg(bias + n));
       if (relu && x < 0.f) x = 0.f;
       if (mask && !(__ldg(mask + idx) > 0.f)) x = 0.f;
       out[idx] = x;
     }
+  }
+  __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
+    if (bias && n0 < N) {
+      float b[8];
+      bias8(n0, b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __fadd_rn(v[j], b[j]);
+    }
+    store8_nb(m, n0, v);
   }
 };
 
@@ -270,6 +324,9 @@ struct EpConvWgrad {
   float* gw;
   int M, N, C, kk;
   FastDiv d_c8;
+  static constexpr bool HAS_BIAS = false;
+  __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
+  __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const { store8(m, n0, v); }
   __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
     if (m >= M) return;
     uint32_t tap, c;
@@ -289,6 +346,9 @@ struct EpConvWgradS2D {
   float* gw;
   int M, N, C, k, s, ks, Cs;
   FastDiv d_cs8;
+  static constexpr bool HAS_BIAS = false;
+  __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
+  __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const { store8(m, n0, v); }
   __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
     if (m >= M) return;
     uint32_t tap, cp;

@@ -34,7 +34,9 @@ enum TgMode : int { TG_TILED_K = 0, TG_TILED_MN = 1, TG_IM2COL_K = 2, TG_IM2COL_
 struct alignas(64) TgOperand {
   CUtensorMap map[3];  // one per plane
   int mode;
-  int nbox;            // boxes per plane per k-block (TILED_MN / IM2COL_MN)
+  int nbox;            // boxes per plane per k-block
+  int box_bytes;       // smem bytes per box (2048 for 32-wide MN boxes)
+  int box_rows;        // TILED_K: rows per box (a B tile split between 2 CTAs)
   // im2col geometry: output pixel (n, oh, ow) -> window start (oh*s + lo, ow*s + lo)
   int lo, s, C8, ksz, flip;
   FastDiv d_ohw, d_ow, d_c8, d_k;
@@ -46,15 +48,22 @@ struct alignas(64) TgParams {
   EP ep;
   float* partial;
   int M, N, K, k_per_split;
+  int debug;  // bench/diagnostics only: 1 skip epilogue stores, 2 skip MMAs, 4 skip TMA loads
 };
 
 constexpr int TG_BM = 128, TG_BK = 32;
 constexpr int TG_THREADS = 256;  // w0 TMA (32 lanes), w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
 
-template <int BN, int NSETS = 2>
+// CL = 1: one CTA per 128 x BN tile.  CL = 2: a CTA pair computes a 256 x BN
+// tile with cta_group::2 UMMA -- each CTA stages its own 128 A rows and HALF
+// of B (BN / 2 rows), so per-SM operand traffic per MMA cycle drops by
+// 1 - (128 + BN/2) / (128 + BN): the split-plane GEMMs are bound by the
+// L2 -> SM operand feed (3 planes per operand), not by the tensor pipe.
+template <int BN, int NSETS = 2, int CL = 1>
 struct TgCfg {
-  static constexpr int A_BYTES = TG_BM * TG_BK * 2;  // one plane, 8 KB
-  static constexpr int B_BYTES = BN * TG_BK * 2;
+  static constexpr int A_BYTES = TG_BM * TG_BK * 2;        // one plane, 8 KB
+  static constexpr int B_ROWS = BN / CL;                    // B rows staged by this CTA
+  static constexpr int B_BYTES = B_ROWS * TG_BK * 2;
   static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;  // + alignment slack + barriers
@@ -74,24 +83,99 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
       : "memory");
 }
 
+// the leader (even) CTA's copy of a barrier of this CTA (shared::cluster address)
+__device__ __forceinline__ uint32_t leader_bar(const uint64_t* bar) {
+  return smem_u32(bar) & 0xFEFFFFFFu;
+}
+
+// CL = 2 loads complete on the LEADER's full barrier (cta_group::2 form)
+template <int CL>
 __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint32_t dst, uint64_t* bar,
                                        int c0, int c1) {
+  if (CL == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+// ---- cta_group::2 (CTA pair) tcgen05 forms --------------------------------------
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
+// arrive on the barrier at this offset in both CTAs of the pair once the
+// pair's outstanding MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+
+// arrive on the leader CTA's copy of `bar`
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   leader_bar(bar))
+               : "memory");
+}
+
+template <int CL>
 __device__ __forceinline__ void tma_im2col_4d(const CUtensorMap* map, uint32_t dst, uint64_t* bar,
                                               int c, int w, int h, int n, uint16_t ow,
                                               uint16_t oh) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
-      "h"(ow), "h"(oh)
-      : "memory");
+  if (CL == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar(bar)), "r"(c), "r"(w), "r"(h),
+        "r"(n), "h"(ow), "h"(oh)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h),
+        "r"(n), "h"(ow), "h"(oh)
+        : "memory");
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -111,17 +195,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr, uint32_t lbo,
 
 // issue box `bi` (0 <= bi < 3*nbox) of one operand tile: plane = bi / nbox,
 // box = bi % nbox (R rows starting at r0, K block starting at k0)
+template <int CL>
 __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_t tile_base,
                                             uint32_t plane_bytes, uint64_t* bar, int r0, int k0) {
   const int plane = bi / op.nbox, box = bi - plane * op.nbox;
   const CUtensorMap* map = &op.map[plane];
-  const uint32_t dst = tile_base + plane * plane_bytes + box * 2048;
+  const uint32_t dst = tile_base + plane * plane_bytes + box * op.box_bytes;
   switch (op.mode) {
     case TG_TILED_K:
-      tma_2d(map, dst, bar, k0, r0);
+      tma_2d<CL>(map, dst, bar, k0, r0 + box * op.box_rows);
       break;
     case TG_TILED_MN:
-      tma_2d(map, dst, bar, r0 + 32 * box, k0);
+      tma_2d<CL>(map, dst, bar, r0 + 32 * box, k0);
       break;
     case TG_IM2COL_K: {
       uint32_t n, j, oh, ow, tap, c0, th, tw;
@@ -129,8 +214,8 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
       op.d_ow.divmod(j, oh, ow);
       op.d_c8.divmod((uint32_t)k0, tap, c0);
       op.d_k.divmod(tap, th, tw);
-      tma_im2col_4d(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo, (int)(oh * op.s) + op.lo,
-                    (int)n, (uint16_t)tw, (uint16_t)th);
+      tma_im2col_4d<CL>(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo,
+                        (int)(oh * op.s) + op.lo, (int)n, (uint16_t)tw, (uint16_t)th);
       break;
     }
     default: {  // TG_IM2COL_MN: k0 = first output pixel, rows = (tap, c)
@@ -139,8 +224,8 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
       op.d_ow.divmod(j, oh, ow);
       op.d_c8.divmod((uint32_t)(r0 + 32 * box), tap, c0);
       op.d_k.divmod(tap, th, tw);
-      tma_im2col_4d(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo, (int)(oh * op.s) + op.lo,
-                    (int)n, (uint16_t)tw, (uint16_t)th);
+      tma_im2col_4d<CL>(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo,
+                        (int)(oh * op.s) + op.lo, (int)n, (uint16_t)tw, (uint16_t)th);
     }
   }
 }
@@ -153,12 +238,21 @@ __device__ __forceinline__ uint64_t tg_desc(int mode, uint32_t plane_base, int k
 
 // Persistent: grid = min(#work items, #SMs); work item w -> (split z, m tile,
 // n tile), n fastest so consecutive items share the A tile in L2.  TMEM holds
-// two accumulator sets; the epilogue of item i overlaps the mainloop of i+1.
-template <int BN, int NSETS, class EP>
+// NSETS accumulator sets; with 2 the epilogue of item i overlaps the mainloop
+// of item i+1.
+// CL = 2 (cluster of 2 = one CTA pair per 256-row tile): rank r stages A rows
+// m0 + 128 r and B rows n0 + r BN/2; both CTAs' loads complete on the leader's
+// full barrier (expect_tx = both stages); the leader's single MMA thread
+// issues cta_group::2 MMAs that read both CTAs' smem and write both CTAs'
+// TMEM (each holds its 128 rows x BN); its commits arrive on the empty / tfull
+// barriers of both CTAs; both epilogues release the set on the leader's
+// tempty barrier (8 warp arrivals).
+template <int BN, int NSETS, int CL, class EP>
 __global__ void __launch_bounds__(TG_THREADS, 1)
     tgemm_kernel(const __grid_constant__ TgParams<EP> p) {
-  using Cfg = TgCfg<BN, NSETS>;
+  using Cfg = TgCfg<BN, NSETS, CL>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int PM = TG_BM * CL;   // rows per work item
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t smem_base = (raw + 1023u) & ~1023u;
@@ -170,9 +264,11 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = cdiv(p.M, TG_BM), nt = cdiv(p.N, BN);
+  const int mt = cdiv(p.M, PM), nt = cdiv(p.N, BN);
   const int splits = cdiv(p.K, p.k_per_split);
   const int items = mt * nt * splits;
+  const int rank = CL == 2 ? (int)cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -181,7 +277,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], 4 * CL);   // one arrival per epilogue warp of the pair
     }
     mbar_fence_init();
   }
@@ -189,9 +285,13 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     prefetch_tmap(&p.a.map[lane]);
     prefetch_tmap(&p.b.map[lane]);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if (CL == 2) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+    else tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CL == 2) cluster_sync_all();   // the peer's barriers / TMEM exist before any traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -199,36 +299,52 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     // ---------------- TMA producer: the warp's lanes issue boxes in parallel --
     const int na = 3 * p.a.nbox, nbx = 3 * p.b.nbox;
     int g = 0;  // global k-block counter (stage / phase)
-    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    for (int w = cid; w < items; w += ncl) {
       const int z = w / (mt * nt), rem = w % (mt * nt);
-      const int m0 = (rem / nt) * TG_BM, n0 = (rem % nt) * BN;
+      const int m0 = (rem / nt) * PM + rank * TG_BM;
+      const int n0 = (rem % nt) * BN + rank * Cfg::B_ROWS;
       const int kbeg = z * p.k_per_split, kend = min(p.K, kbeg + p.k_per_split);
       const int nkb = cdiv(kend - kbeg, TG_BK);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int stage = g % STAGES;
         mbar_wait(&empty_bar[stage], ((g / STAGES) & 1) ^ 1);
-        if (lane == 0) mbar_arrive_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+        if (p.debug & 4) {   // diagnostics: no data movement
+          if (lane == 0 && rank == 0) mbar_arrive(&full_bar[stage]);
+          __syncwarp();
+          continue;
+        }
+        if (lane == 0 && rank == 0) mbar_arrive_tx(&full_bar[stage], CL * Cfg::STAGE_BYTES);
         __syncwarp();
         const int k0 = kbeg + kb * TG_BK;
         const uint32_t st = smem_base + stage * Cfg::STAGE_BYTES;
         for (int bi = lane; bi < na + nbx; bi += 32) {
           if (bi < na)
-            tg_load_box(p.a, bi, st, Cfg::A_BYTES, &full_bar[stage], m0, k0);
+            tg_load_box<CL>(p.a, bi, st, Cfg::A_BYTES, &full_bar[stage], m0, k0);
           else
-            tg_load_box(p.b, bi - na, st + 3 * Cfg::A_BYTES, Cfg::B_BYTES, &full_bar[stage], n0,
-                        k0);
+            tg_load_box<CL>(p.b, bi - na, st + 3 * Cfg::A_BYTES, Cfg::B_BYTES, &full_bar[stage],
+                            n0, k0);
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer -----------------------------------------------
+    if (CL == 2 && lane == 0) {
+      // drain: every multicast release of our stages has landed before exit
+      for (int k = 0; k < STAGES; ++k, ++g) mbar_wait(&empty_bar[g % STAGES], ((g / STAGES) & 1) ^ 1);
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (the leader CTA for a pair) --------------------
     const bool amn = p.a.mode == TG_TILED_MN || p.a.mode == TG_IM2COL_MN;
     const bool bmn = p.b.mode == TG_TILED_MN || p.b.mode == TG_IM2COL_MN;
-    const uint32_t idesc = sg_idesc(TG_BM, BN, amn, bmn);
+    const uint32_t idesc = sg_idesc(PM, BN, amn, bmn);
     constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
     constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
+    // descriptors of stage 0 / plane 0 / k-step 0; every other (stage, plane,
+    // k-step) only moves the 14-bit start-address field (addresses < 256 KB,
+    // so the add never carries out of it): two integer adds per MMA
+    const uint64_t da0 = tg_desc(p.a.mode, smem_base, 0);
+    const uint64_t db0 = tg_desc(p.b.mode, smem_base + 3 * Cfg::A_BYTES, 0);
+    const uint32_t ak = (amn ? 1024u : 32u) >> 4, bk = (bmn ? 1024u : 32u) >> 4;
     int g = 0, it = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+    for (int w = cid; w < items; w += ncl, ++it) {
       const int z = w / (mt * nt);
       const int kbeg = z * p.k_per_split, kend = min(p.K, kbeg + p.k_per_split);
       const int nkb = cdiv(kend - kbeg, TG_BK);
@@ -241,31 +357,34 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
         const int stage = g % STAGES;
         mbar_wait(&full_bar[stage], (g / STAGES) & 1);
         tc_fence_after();
-        const uint32_t a0 = smem_base + stage * Cfg::STAGE_BYTES;
-        const uint32_t b0 = a0 + 3 * Cfg::A_BYTES;
+        const uint32_t so = (uint32_t)(stage * Cfg::STAGE_BYTES) >> 4;
 #pragma unroll
         for (int j = 0; j < TG_BK / 16; ++j) {
+          if (p.debug & 2) break;
 #pragma unroll
           for (int i = 0; i < 6; ++i) {
-            const uint64_t da = tg_desc(p.a.mode, a0 + AP[i] * Cfg::A_BYTES, j);
-            const uint64_t db = tg_desc(p.b.mode, b0 + BP[i] * Cfg::B_BYTES, j);
+            const uint64_t da = da0 + (so + AP[i] * (Cfg::A_BYTES >> 4) + j * ak);
+            const uint64_t db = db0 + (so + BP[i] * (Cfg::B_BYTES >> 4) + j * bk);
             const bool big = i == 5;
             const bool first = (kb | j) == 0 && (big || i == 0);
-            umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
+            if (CL == 2) umma_f16_pair(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
+            else umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
           }
         }
-        umma_commit(&empty_bar[stage]);
+        if (CL == 2) umma_commit_pair(&empty_bar[stage]);
+        else umma_commit(&empty_bar[stage]);
       }
-      umma_commit(&tfull_bar[acc]);
+      if (CL == 2) umma_commit_pair(&tfull_bar[acc]);
+      else umma_commit(&tfull_bar[acc]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM (big + small) -> registers -> ep ---------
     const int q = warp & 3;
     const int npad = cdiv(p.N, 8) * 8;
     int it = 0;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+    for (int w = cid; w < items; w += ncl, ++it) {
       const int z = w / (mt * nt), rem = w % (mt * nt);
-      const int m0 = (rem / nt) * TG_BM, n0 = (rem % nt) * BN;
+      const int m0 = (rem / nt) * PM + rank * TG_BM, n0 = (rem % nt) * BN;
       const int acc = NSETS == 2 ? (it & 1) : 0;
       const int use = NSETS == 2 ? (it >> 1) : it;
       mbar_wait(&tfull_bar[acc], use & 1);
@@ -273,21 +392,31 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
       const int m = m0 + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = 0; c < BN; c += 32) {
         if (n0 + c >= npad) break;
-        uint32_t r[16], rs[16];
-        tmem_ld16(tbase + (uint32_t)c, r);
-        tmem_ld16(tbase + BN + (uint32_t)c, rs);
+        // bias first (independent of TMEM), then 32 columns of big + small, one wait
+        float bb[4][8];
+        if (EP::HAS_BIAS && !p.partial) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) p.ep.bias8(n0 + c + 8 * q4, bb[q4]);
+        }
+        uint32_t r[32], rs[32];
+        tmem_ld16(tbase + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+        tmem_ld16(tbase + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+        tmem_ld16(tbase + BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&rs[0]));
+        tmem_ld16(tbase + BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs[16]));
         tmem_ld_wait();
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 4; ++h) {
           const int nb = n0 + c + 8 * h;
           if (nb >= npad) break;
           float v[8];
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
             v[jj] = __fadd_rn(__uint_as_float(r[8 * h + jj]), __uint_as_float(rs[8 * h + jj]));
-          if (p.partial) {
+          if (p.debug & 1) {
+            continue;
+          } else if (p.partial) {
             if (m < p.M) {
               float4* dst =
                   reinterpret_cast<float4*>(p.partial + ((size_t)z * p.M + m) * npad + nb);
@@ -295,20 +424,30 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
               dst[1] = make_float4(v[4], v[5], v[6], v[7]);
             }
           } else {
-            p.ep.store8(m, nb, v);
+            if (EP::HAS_BIAS) {
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) v[jj] = __fadd_rn(v[jj], bb[h][jj]);
+            }
+            p.ep.store8_nb(m, nb, v);
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (CL == 2) mbar_arrive_leader(&tempty_bar[acc]);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (CL == 2) cluster_sync_all();   // no pair traffic may target us after exit
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (CL == 2) tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 

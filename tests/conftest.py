@@ -29,3 +29,11 @@ def producer(request, lib):
     lib.stz_set_tma(request.param)
     yield request.param
     lib.stz_set_tma(1)
+
+
+@pytest.fixture(params=[1, 0], ids=["cluster2", "cta1"])
+def clusters(request, lib):
+    """Run with CTA-pair (cta_group::2) GEMMs and with single CTAs; restore after."""
+    lib.stz_set_cluster(request.param)
+    yield request.param
+    lib.stz_set_cluster(1)

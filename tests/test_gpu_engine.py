@@ -1,7 +1,11 @@
 """BlockEngine (the fused hot path on split-plane tensors) vs the oracle at
 the block level: forward output, parameter-gradient sums and the block input
 gradient, for the layer stacks the bench runs (AlexNet conv1 as
-space-to-depth, TMA im2col convs, pool -> flatten -> FC boundary)."""
+space-to-depth, TMA im2col convs, pool -> flatten -> FC boundary).
+
+Tolerance: 3e-6 (rel_err of the tensor max) per GEMM a value passed through;
+the input gradient of a block crosses every GEMM of the chain, so it gets
+3e-6 x (number of GEMM layers)."""
 
 import numpy as np
 import pytest
@@ -13,7 +17,39 @@ pytestmark = pytest.mark.gpu
 TOL = 3e-6
 
 
+TIE = 1e-5   # |pre-activation| <= TIE * max|.|: a ReLU decision fp32 rounding may flip
+
+
+def _device_act(eng, i):
+    """Op i's output on the device, in the oracle's layout (rows / NCHW)."""
+    a = eng._act(i)
+    f = a.to_float()
+    if a.layout == "rows":
+        return f[:, :a.logical].cpu().numpy()
+    return f[..., :a.logical].permute(0, 3, 1, 2).cpu().numpy()
+
+
+def _oracle_forward_tie_aware(tl, params, x, dev_pos):
+    """orc.block_forward, layer by layer, except that a ReLU whose
+    pre-activation is within TIE of zero takes the device's decision: both
+    sides are correct to fp32 rounding there, and one flipped unit would
+    otherwise perturb a whole weight-gradient row far beyond TOL."""
+    caches = []
+    for i, (layer, p) in enumerate(zip(tl, params)):
+        z = x
+        x, c = orc.block_forward([layer], [p], x)
+        c = c[0]
+        if layer[0] == "relu":
+            tie = np.abs(z) <= TIE * float(np.abs(z).max())
+            if tie.any():
+                c = np.where(tie, dev_pos[i], c)
+        caches.append(c)
+    return x, caches
+
+
 def _run(layers, in_shape, batch, need_input_grad, seed):
+    from paper_1812_10624_b200.tensor_core import Conv2d, FullyConnected
+    depth = sum(isinstance(l, (Conv2d, FullyConnected)) for l in layers)
     from paper_1812_10624_b200.engine import BlockEngine
     from paper_1812_10624_b200.tensor_core import as_tuple, seeded_init
     params = seeded_init(layers, seed)
@@ -22,6 +58,7 @@ def _run(layers, in_shape, batch, need_input_grad, seed):
     rng = np.random.Generator(np.random.PCG64(seed))
     x = rng.standard_normal((batch, *in_shape)).astype(np.float32)
     out = eng.forward(torch.from_numpy(x).cuda())
+    dev_pos = {i: _device_act(eng, i) > 0 for i, l in enumerate(layers) if type(l).__name__ == "ReLU"}
     oshape = eng.out_shape
     gy = rng.standard_normal((batch, *oshape)).astype(np.float32)
     # feed gy in the engine's layout: rows for a flat output
@@ -42,36 +79,40 @@ def _run(layers, in_shape, batch, need_input_grad, seed):
     gin = eng.backward(g)
     torch.cuda.synchronize()
     tl = [as_tuple(l) for l in layers]
-    ry, caches = orc.block_forward(tl, params, x)
+    ry, caches = _oracle_forward_tie_aware(tl, params, x, dev_pos)
     rgx, rgrads = orc.block_backward(tl, params, caches, gy)
     assert orc.rel_err(got.cpu().numpy(), ry) <= TOL
     for li, (gl, rl) in enumerate(zip(eng.grads, rgrads)):
         for a, b in zip(gl, rl):
             assert orc.rel_err(a.cpu().numpy(), b) <= TOL, f"layer {li}"
     if need_input_grad:
-        c, h, w = in_shape
-        assert orc.rel_err(gin.to_float()[..., :c].permute(0, 3, 1, 2).cpu().numpy(), rgx) <= TOL
+        if len(in_shape) == 1:
+            got_gx = gin.to_float()[:, :in_shape[0]]
+        else:
+            c, h, w = in_shape
+            got_gx = gin.to_float()[..., :c].permute(0, 3, 1, 2)
+        assert orc.rel_err(got_gx.cpu().numpy(), rgx) <= TOL * depth
     return eng
 
 
-def test_alexnet_conv1_space_to_depth():
+def test_alexnet_conv1_space_to_depth(clusters):
     from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
     eng = _run([Conv2d(3, 64, 11, 4, 2), ReLU(), MaxPool2d(3, 2)], (3, 224, 224), 2, False, 1)
     assert eng.ops[0].s2d == (3, 64, 57, 57)
 
 
-def test_alexnet_conv2_to_pool_tma():
+def test_alexnet_conv2_to_pool_tma(clusters):
     from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
     _run([Conv2d(64, 192, 5, 1, 2), ReLU(), MaxPool2d(3, 2)], (64, 27, 27), 2, True, 2)
 
 
-def test_alexnet_conv5_pool_flatten_boundary():
+def test_alexnet_conv5_pool_flatten_boundary(clusters):
     from paper_1812_10624_b200.tensor_core import Conv2d, Flatten, MaxPool2d, ReLU
     _run([Conv2d(256, 256, 3, 1, 1), ReLU(), MaxPool2d(3, 2), Flatten()], (256, 13, 13), 3, True,
          3)
 
 
-def test_vgg_stage_conv_conv_pool():
+def test_vgg_stage_conv_conv_pool(clusters):
     from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
     _run([Conv2d(64, 128, 3, 1, 1), ReLU(), Conv2d(128, 128, 3, 1, 1), ReLU(), MaxPool2d(2, 2)],
          (64, 28, 28), 2, True, 4)
@@ -81,3 +122,10 @@ def test_flatten_without_pool_relayout():
     from paper_1812_10624_b200.tensor_core import Conv2d, Flatten, FullyConnected, ReLU
     _run([Conv2d(8, 16, 3, 1, 1), ReLU(), Flatten(), FullyConnected(16 * 6 * 6, 24), ReLU()],
          (8, 6, 6), 4, True, 5)
+
+
+def test_fc_head_alexnet_shapes(clusters):
+    """FC head at the 7:1 FC worker's batch (M = 896): fc 9216->4096->4096->1000."""
+    from paper_1812_10624_b200.tensor_core import FullyConnected, ReLU
+    _run([FullyConnected(9216, 4096), ReLU(), FullyConnected(4096, 4096), ReLU(),
+          FullyConnected(4096, 1000)], (9216,), 896, True, 6)

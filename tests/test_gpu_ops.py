@@ -142,7 +142,7 @@ CONV_SHAPES = [  # (N, C, H, W, O, k, s, p) incl. AlexNet-like layer shapes at s
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES, ids=lambda s: "x".join(map(str, s)))
-def test_conv_vs_oracle(tc, producer, shape):
+def test_conv_vs_oracle(tc, producer, clusters, shape):
     n, c, h, w, o, k, s, p = shape
     rng = np.random.Generator(np.random.PCG64(hash(shape) & 0xFFFF))
     x = rng.standard_normal((n, c, h, w)).astype(np.float32)
@@ -166,7 +166,7 @@ FC_SHAPES = [(8, 256, 128), (8, 128, 10), (128, 9216, 512), (896, 4096, 1000), (
 
 
 @pytest.mark.parametrize("shape", FC_SHAPES, ids=lambda s: "x".join(map(str, s)))
-def test_fc_vs_oracle(tc, producer, shape):
+def test_fc_vs_oracle(tc, producer, clusters, shape):
     m, i, o = shape
     rng = np.random.Generator(np.random.PCG64(m * 7919 + i * 31 + o))
     x = rng.standard_normal((m, i)).astype(np.float32)

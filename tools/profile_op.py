@@ -49,6 +49,23 @@ for _ in range(20):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 20
+if os.environ.get("STZ_DIAG"):
+    lib = _lib.load()
+    for cl_on in (1, 0):
+        lib.stz_set_cluster(cl_on)
+        for flags in (0, 1, 2, 4, 1 | 2, 1 | 4):
+            lib.stz_set_debug(flags)
+            _lib.call(name, *args)
+            e0.record()
+            for _ in range(20):
+                _lib.call(name, *args)
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"  cluster={cl_on} debug={flags}: {e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
+    lib.stz_set_debug(0)
+    lib.stz_set_cluster(1)
+if os.environ.get("STZ_DEBUG"):   # capture a diagnostic variant (stz_set_debug flags)
+    _lib.load().stz_set_debug(int(os.environ["STZ_DEBUG"]))
 torch.cuda.nvtx.range_push("replay")
 _lib.call(name, *args)
 torch.cuda.nvtx.range_pop()
