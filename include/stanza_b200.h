@@ -49,6 +49,11 @@ int stz_set_tma(int on);
  * 128-row tile.  The GPU tests run both. */
 int stz_set_cluster(int on);
 
+/* Force the TMA GEMM tile (tests / tuning): width bn in {64, 96, 128, 192,
+ * 256}, cl = 2 for CTA pairs (required for 256; 64 / 96 run unpaired),
+ * splits = K splits (0 = 1).  bn = 0 restores the cost-model choice. */
+int stz_set_tile(int bn, int cl, int splits);
+
 /* GEMM pipeline diagnostics (results are WRONG while set): 1 skips epilogue
  * stores, 2 skips the MMAs, 4 skips the TMA loads.  0 = normal. */
 int stz_set_debug(int flags);

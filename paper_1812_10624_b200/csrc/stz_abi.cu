@@ -31,6 +31,11 @@ namespace {
 thread_local std::string g_err;
 int g_num_sms = 0;
 int g_max_kps = 0;  // >0: cap the K range one CTA accumulates (tuning knob)
+// STZ_TRACE=1: print every TMA GEMM's schedule (shape, tile, pairs, split-K, waves) to stderr
+const bool g_trace = [] {
+  const char* e = getenv("STZ_TRACE");
+  return e && *e == '1';
+}();
 unsigned long long g_launches = 0;
 
 enum { STZ_OK = 0, STZ_EINVAL = 1, STZ_ECUDA = 2, STZ_EWORKSPACE = 3 };
@@ -494,19 +499,72 @@ int g_use_cluster = 1;   // CTA pairs (stz_set_cluster)
 int g_debug = 0;         // GEMM pipeline diagnostics (stz_set_debug)
 
 struct TgShape {
-  int BN, CL;
+  int BN, CL, splits;
+  double cost;
 };
 
-TgShape tg_shape(int M, int N) {
-  TgShape t;
-  if (N <= 64) t.BN = 64;
-  else if (N % 256 == 0) t.BN = 256;
-  else if (N % 192 == 0) t.BN = 192;
-  else if (N % 96 == 0 && N % 128 != 0) t.BN = 96;
-  else t.BN = 128;
-  t.CL = (g_use_cluster && cdiv(M, TG_BM) >= 2 && (t.BN / 2) % 32 == 0) ? 2 : 1;
-  if (t.CL == 1 && t.BN == 256) t.BN = 128;   // unpaired: keep the double-buffered TMEM sets
-  return t;
+// Predicted seconds for a TMA GEMM with tile (BN, CL) and `sp` K-splits:
+//   waves * (k-blocks per item + per-item overhead) * t_kb + partial sums
+// t_kb = max(12 MMAs at max(48, BN/2) cycles, the stage's operand bytes at
+// ~27 B/cycle/SM of effective L2 -> SM feed), both measured (tools/mma_bench.cu and the
+// stz_set_debug runs); one TMEM set (BN >= 192) serialises the epilogue with
+// the next item's mainloop; partial sums are mostly L2-resident.
+double tg_cost(int M, int N, int K, int BN, int CL, int sp) {
+  const double clk = 1.9e9;
+  const int sms = num_sms() / CL;
+  const int tiles = cdiv(M, TG_BM * CL) * cdiv(N, BN);
+  const int nkb = cdiv(K, TG_BK);
+  const double mma_cyc = 12.0 * (BN / 2 > 48 ? BN / 2 : 48);
+  const double stage_bytes = 3.0 * (TG_BM * TG_BK * 2 + (double)(BN / CL) * TG_BK * 2);
+  const double feed_cyc = stage_bytes / 27.0;
+  const double t_kb = (mma_cyc > feed_cyc ? mma_cyc : feed_cyc) / clk;
+  const double t_epi = BN >= 192 ? 1.0 * t_kb : 0.0;
+  const double t_item0 = 4.0 * t_kb + t_epi + 2e-6;
+  const double waves = (double)cdiv(tiles * sp, sms);
+  double cost = waves * ((double)cdiv(nkb, sp) * t_kb + t_item0);
+  if (sp > 1) cost += (double)M * rup8(N) * 4.0 * (2.0 * sp + 1.0) / 10.0e12 + 4e-6;
+  return cost;
+}
+
+// tile shape + split-K with the lowest predicted time; pairs (cta_group::2)
+// only for tiles >= 128 wide (thin tiles are bound by the A-operand smem
+// reads, where pairs only add row padding)
+int g_force_bn = 0, g_force_cl = 0, g_force_splits = 0;   // stz_set_tile (tests)
+constexpr int TG_MAX_KB = 128;   // k-blocks (of 32) one work item may accumulate
+
+TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
+  const int nkb = cdiv(K, TG_BK);
+  // accuracy: tcgen05 truncates the bits it shifts out when adding into an
+  // accumulator, so the bias of the big b0*b0 accumulator
+  // grows with the MMAs one tile accumulates: cap them at 256 (K <= 4096 per
+  // split, worst case 2^-16 relative, typically a fifth of that)
+  const int sp_min = cdiv(nkb, TG_MAX_KB);
+  if (g_force_bn) {
+    const int cl = g_force_cl == 2 && cdiv(M, TG_BM) >= 2 ? 2 : 1;
+    const int sp = g_force_splits > sp_min ? g_force_splits : sp_min;
+    return TgShape{g_force_bn, cl, sp, 0.0};
+  }
+  TgShape best{64, 1, sp_min, 1e30};
+  const size_t per = (size_t)M * rup8(N) * sizeof(float);
+  const int fit = ws_bytes ? (int)(ws_bytes / per) : 1;
+  const int cand[][2] = {{64, 1}, {96, 1}, {128, 1}, {192, 1}, {128, 2}, {192, 2}, {256, 2}};
+  for (const auto& c : cand) {
+    const int BN = c[0], CL = c[1];
+    if (CL == 2 && (!g_use_cluster || cdiv(M, TG_BM) < 2)) continue;
+    if (BN > 64 && N <= BN / 2) continue;   // mostly padding
+    const int smax = nkb / 2 < fit ? nkb / 2 : fit;
+    int bsp = sp_min;
+    double bc = tg_cost(M, N, K, BN, CL, sp_min);
+    for (int sp = sp_min + 1; sp <= smax && sp <= 256; ++sp) {
+      const double cst = tg_cost(M, N, K, BN, CL, sp);
+      if (cst < bc * 0.98) {   // more splits only for a real (> 2%) gain
+        bc = cst;
+        bsp = sp;
+      }
+    }
+    if (bc < best.cost * 0.97) best = TgShape{BN, CL, bsp, bc};
+  }
+  return best;
 }
 
 template <int BN, int NSETS, int CL, class EP>
@@ -551,24 +609,8 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   const int npad = rup8(N);
   const size_t per = (size_t)M * npad * sizeof(float);
   const int fit = ws ? (int)(ws_bytes / per) : 1;
-  // split-K: enough work items for the persistent grid, chosen to minimise the
-  // idle tail (items / (waves * SMs)), each split keeping >= 4 k-blocks
-  int splits = 1;
+  int splits = sh.splits;
   const int sms = num_sms() / CL;   // work items run one per CTA pair
-  if (tiles < 2 * sms && nkb >= 8) {
-    double best = 0.0;
-    const int smax = nkb / 4 < fit ? nkb / 4 : fit;
-    for (int sp = 1; sp <= smax && sp <= 64; ++sp) {
-      const int items = tiles * sp;
-      const int waves = cdiv(items, sms);
-      const double eff = (double)items / ((double)waves * sms);
-      // prefer more parallelism only while it pays: require a 3% gain
-      if (eff > best * 1.03 || (items < sms && eff >= best)) {
-        best = eff;
-        splits = sp;
-      }
-    }
-  }
   if (g_max_kps > 0 && K > g_max_kps) splits = cdiv(K, g_max_kps);
   if (splits > fit) splits = fit;
   if (splits < 1) splits = 1;
@@ -584,6 +626,13 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   prm.K = K;
   prm.k_per_split = kps;
   prm.debug = g_debug;
+  if (g_trace) {
+    const int items = tiles * splits;
+    fprintf(stderr,
+            "[stz] %-16s M=%6d N=%5d K=%6d BN=%3d CL=%d tiles=%5d splits=%3d items=%5d "
+            "slots=%3d waves=%.2f est=%.1fus\n",
+            what, M, N, K, BN, CL, tiles, splits, items, sms, (double)items / sms, sh.cost * 1e6);
+  }
   if (CL == 2) {
     if (BN == 64) launch_tg<64, 2, 2>(prm, splits, st);
     else if (BN == 256) launch_tg<256, 1, 2>(prm, splits, st);
@@ -652,7 +701,7 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
                   size_t ws_bytes, cudaStream_t st) {
   const int M = N * OH * OW, K = k * k * C8;
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
-    const TgShape sh = tg_shape(M, O);
+    const TgShape sh = tg_shape(M, O, K, ws_bytes);
     TgOperand a, b;
     if (op_im2col(a, false, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
         op_tiled_k(b, wf, psw, O, K, K, sh.BN / sh.CL))
@@ -669,7 +718,7 @@ int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, c
                     void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = N * H * W, K = k * k * O8;
   if (tma_on() && O8 % 32 == 0 && s == 1 && p - (k - 1) >= -128 && p <= 127) {
-    const TgShape sh = tg_shape(M, C);
+    const TgShape sh = tg_shape(M, C, K, ws_bytes);
     TgOperand a, b;
     if (op_im2col(a, false, g, psg, N, OH, OW, O8, k, 1, p - (k - 1), -p, H, W, TG_BM) &&
         op_tiled_k(b, wd, psw, C, K, K, sh.BN / sh.CL))
@@ -686,7 +735,7 @@ int gemm_conv_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, co
                     void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = k * k * C8, P = N * OH * OW;
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128) {
-    const TgShape sh = tg_shape(M, O);
+    const TgShape sh = tg_shape(M, O, P, ws_bytes);
     TgOperand a, b;
     if (op_im2col(a, true, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
         op_tiled_mn(b, g, psg, O, P, O8, sh.BN / sh.CL))
@@ -702,7 +751,7 @@ int gemm_fc_fwd(const bf16_t* x, size_t psx, const bf16_t* w, size_t psw, const 
                 int in_dim, int I8, int out_dim, int O8, void* ws, size_t ws_bytes,
                 cudaStream_t st) {
   if (tma_on()) {
-    const TgShape sh = tg_shape(M, out_dim);
+    const TgShape sh = tg_shape(M, out_dim, I8, ws_bytes);
     TgOperand a, b;
     if (op_tiled_k(a, x, psx, M, I8, I8, TG_BM) && op_tiled_mn(b, w, psw, out_dim, in_dim, O8, sh.BN / sh.CL))
       return run_tgemm("fc_fwd[tma]", sh, a, b, ep, M, out_dim, I8, ws, ws_bytes, st);
@@ -716,7 +765,7 @@ template <class EP>
 int gemm_fc_dgrad(const bf16_t* g, size_t psg, const bf16_t* w, size_t psw, const EP& ep, int M,
                   int in_dim, int O8, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (tma_on()) {
-    const TgShape sh = tg_shape(M, in_dim);
+    const TgShape sh = tg_shape(M, in_dim, O8, ws_bytes);
     TgOperand a, b;
     if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM) && op_tiled_k(b, w, psw, in_dim, O8, O8, sh.BN / sh.CL))
       return run_tgemm("fc_dgrad[tma]", sh, a, b, ep, M, in_dim, O8, ws, ws_bytes, st);
@@ -731,7 +780,7 @@ int gemm_fc_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, cons
                   int in_dim, int I8, int out_dim, int O8, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
   if (tma_on()) {
-    const TgShape sh = tg_shape(in_dim, out_dim);
+    const TgShape sh = tg_shape(in_dim, out_dim, M, ws_bytes);
     TgOperand a, b;
     if (op_tiled_mn(a, x, psx, in_dim, M, I8, TG_BM) &&
         op_tiled_mn(b, g, psg, out_dim, M, O8, sh.BN / sh.CL))
@@ -780,6 +829,17 @@ int stz_set_tma(int on) {
 
 int stz_set_cluster(int on) {
   g_use_cluster = on ? 1 : 0;
+  return STZ_OK;
+}
+
+int stz_set_tile(int bn, int cl, int splits) {
+  if (bn != 0 && bn != 64 && bn != 96 && bn != 128 && bn != 192 && bn != 256)
+    return fail(STZ_EINVAL, "stz_set_tile: width must be 0 (auto), 64, 96, 128, 192 or 256");
+  if ((bn == 256 && cl != 2) || (bn == 96 && cl == 2) || (bn == 64 && cl == 2))
+    return fail(STZ_EINVAL, "stz_set_tile: widths 64 / 96 run unpaired, 256 only paired");
+  g_force_bn = bn;
+  g_force_cl = cl;
+  g_force_splits = splits;
   return STZ_OK;
 }
 

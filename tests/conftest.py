@@ -9,6 +9,18 @@ for p in (ROOT, os.path.join(ROOT, "oracle")):
         sys.path.insert(0, p)
 
 
+def gemm_tol(k: int) -> float:
+    """Tolerance (rel_err against the float64 oracle) of one BF16x6 GEMM with
+    contraction length k.  The product sums are exact; the error is the
+    tcgen05 accumulator's truncation when it adds each 16-deep MMA into the
+    big b0*b0 accumulator, up to 1 ulp per MMA.  The library
+    caps one work item at K = 4096 (split-K beyond), so the worst-case bias is
+    ceil(min(k, 4096) / 16) * 2^-23 of the output max; the tolerance is half
+    of that (measured errors sit at about a fifth), floored at 3e-6."""
+    import math
+    return max(3e-6, 0.5 * math.ceil(min(k, 4096) / 16) * 2.0 ** -23)
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path)")
 
