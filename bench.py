@@ -396,7 +396,8 @@ def main():
     step_ms_sum = sum(tot for tot, _ in calls.values())
     fc_fl = sum(kk[1] * c for kk, (_, c) in calls.items() if kk[0].startswith("fc"))
     fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("fc"))
-    per_call = {f"{kk[0]}": {"ms": tot / max(c, 1), "tflops": (kk[1] / (tot / max(c, 1) / 1e3) / 1e12)
+    per_call = {f"{kk[0]}": {"ms": tot / max(c, 1), "n": c, "total_ms": tot,
+                             "tflops": (kk[1] / (tot / max(c, 1) / 1e3) / 1e12)
                              if kk[1] and tot else None}
                 for kk, (tot, c) in sorted(calls.items(), key=lambda kv: -kv[1][0])}
     fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None

@@ -539,22 +539,13 @@ TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
   // grows with the MMAs one tile accumulates: cap them at 256 (K <= 4096 per
   // split, worst case 2^-16 relative, typically a fifth of that)
   const int sp_min = cdiv(nkb, TG_MAX_KB);
-  if (g_force_bn) {
-    const int cl = g_force_cl == 2 && cdiv(M, TG_BM) >= 2 ? 2 : 1;
-    const int sp = g_force_splits > sp_min ? g_force_splits : sp_min;
-    return TgShape{g_force_bn, cl, sp, 0.0};
-  }
-  TgShape best{64, 1, sp_min, 1e30};
   const size_t per = (size_t)M * rup8(N) * sizeof(float);
   const int fit = ws_bytes ? (int)(ws_bytes / per) : 1;
-  const int cand[][2] = {{64, 1}, {96, 1}, {128, 1}, {192, 1}, {128, 2}, {192, 2}, {256, 2}};
-  for (const auto& c : cand) {
-    const int BN = c[0], CL = c[1];
-    if (CL == 2 && (!g_use_cluster || cdiv(M, TG_BM) < 2)) continue;
-    if (BN > 64 && N <= BN / 2) continue;   // mostly padding
+  // best split count for one tile shape
+  auto best_split = [&](int BN, int CL, double& bc) {
     const int smax = nkb / 2 < fit ? nkb / 2 : fit;
     int bsp = sp_min;
-    double bc = tg_cost(M, N, K, BN, CL, sp_min);
+    bc = tg_cost(M, N, K, BN, CL, sp_min);
     for (int sp = sp_min + 1; sp <= smax && sp <= 256; ++sp) {
       const double cst = tg_cost(M, N, K, BN, CL, sp);
       if (cst < bc * 0.98) {   // more splits only for a real (> 2%) gain
@@ -562,6 +553,27 @@ TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
         bsp = sp;
       }
     }
+    return bsp;
+  };
+  if (g_force_bn) {
+    const int cl = g_force_cl == 2 && cdiv(M, TG_BM) >= 2 ? 2 : 1;
+    if (g_force_bn == 256 && cl == 1) {   // 256 wide needs a pair (TMEM)
+      double bc = 0.0;
+      return TgShape{128, 1, best_split(128, 1, bc), bc};
+    }
+    double bc = 0.0;
+    const int sp = g_force_splits > 0 ? (g_force_splits > sp_min ? g_force_splits : sp_min)
+                                      : best_split(g_force_bn, cl, bc);
+    return TgShape{g_force_bn, cl, sp, bc};
+  }
+  TgShape best{64, 1, sp_min, 1e30};
+  const int cand[][2] = {{64, 1}, {96, 1}, {128, 1}, {192, 1}, {128, 2}, {192, 2}, {256, 2}};
+  for (const auto& c : cand) {
+    const int BN = c[0], CL = c[1];
+    if (CL == 2 && (!g_use_cluster || cdiv(M, TG_BM) < 2)) continue;
+    if (BN > 64 && N <= BN / 2) continue;   // mostly padding
+    double bc;
+    const int bsp = best_split(BN, CL, bc);
     if (bc < best.cost * 0.97) best = TgShape{BN, CL, bsp, bc};
   }
   return best;
@@ -633,17 +645,15 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
             "slots=%3d waves=%.2f est=%.1fus\n",
             what, M, N, K, BN, CL, tiles, splits, items, sms, (double)items / sms, sh.cost * 1e6);
   }
-  if (CL == 2) {
-    if (BN == 64) launch_tg<64, 2, 2>(prm, splits, st);
-    else if (BN == 256) launch_tg<256, 1, 2>(prm, splits, st);
-    else if (BN == 192) launch_tg<192, 1, 2>(prm, splits, st);
-    else launch_tg<128, 2, 2>(prm, splits, st);
-  } else {
-    if (BN == 64) launch_tg<64, 2, 1>(prm, splits, st);
-    else if (BN == 96) launch_tg<96, 2, 1>(prm, splits, st);
-    else if (BN == 192) launch_tg<192, 1, 1>(prm, splits, st);
-    else launch_tg<128, 2, 1>(prm, splits, st);
-  }
+  if (CL == 2 && BN == 64) launch_tg<64, 2, 2>(prm, splits, st);
+  else if (CL == 2 && BN == 128) launch_tg<128, 2, 2>(prm, splits, st);
+  else if (CL == 2 && BN == 192) launch_tg<192, 1, 2>(prm, splits, st);
+  else if (CL == 2 && BN == 256) launch_tg<256, 1, 2>(prm, splits, st);
+  else if (CL == 1 && BN == 64) launch_tg<64, 2, 1>(prm, splits, st);
+  else if (CL == 1 && BN == 96) launch_tg<96, 2, 1>(prm, splits, st);
+  else if (CL == 1 && BN == 128) launch_tg<128, 2, 1>(prm, splits, st);
+  else if (CL == 1 && BN == 192) launch_tg<192, 1, 1>(prm, splits, st);
+  else return fail(STZ_EINVAL, "%s: no kernel for tile %d x %d", what, BN, CL);
   int rc = check_launch(what);
   if (rc) return rc;
   if (splits > 1) {
@@ -835,7 +845,7 @@ int stz_set_cluster(int on) {
 int stz_set_tile(int bn, int cl, int splits) {
   if (bn != 0 && bn != 64 && bn != 96 && bn != 128 && bn != 192 && bn != 256)
     return fail(STZ_EINVAL, "stz_set_tile: width must be 0 (auto), 64, 96, 128, 192 or 256");
-  if ((bn == 256 && cl != 2) || (bn == 96 && cl == 2) || (bn == 64 && cl == 2))
+  if ((bn == 256 && cl != 2) || (bn == 96 && cl == 2))
     return fail(STZ_EINVAL, "stz_set_tile: widths 64 / 96 run unpaired, 256 only paired");
   g_force_bn = bn;
   g_force_cl = cl;
@@ -1184,6 +1194,18 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
   cudaStream_t st = as_stream(stream);
   const size_t total = (size_t)N * OH * OW * C8 / 8;
   if (total == 0) return STZ_OK;
+  const size_t flat_smem = (size_t)C * OH * OW * sizeof(float);
+  if (flat_ld > 0 && flat_ld % 8 == 0 && flat_smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(maxpool_fwd_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    maxpool_fwd_flat_kernel<<<N, 512, flat_smem, st>>>(cb(x), psx, mb(y), psy, arg, C, C8, H, W,
+                                                        k, s, OH, OW, flat_ld);
+    return check_launch("maxpool_fwd_flat");
+  }
   if (flat_ld > C * OH * OW) {
     zero_flat_tail_kernel<<<grid_for((size_t)N * (flat_ld - C * OH * OW)), 256, 0, st>>>(
         mb(y), psy, N, C * OH * OW, flat_ld);
@@ -1204,7 +1226,32 @@ int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, s
   if (k <= 0 || s <= 0 || OH <= 0 || OW <= 0) return fail(STZ_EINVAL, "maxpool_bwd: bad shape");
   const size_t total = (size_t)N * H * W * C8 / 8;
   if (total == 0) return STZ_OK;
-  maxpool_bwd_split_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+  cudaStream_t st = as_stream(stream);
+  const size_t flat_smem = (size_t)C * OH * OW * sizeof(float);
+  if (flat_ld > 0 && flat_ld % 8 == 0 && flat_smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(maxpool_bwd_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    maxpool_bwd_flat_kernel<<<N, 512, flat_smem, st>>>(cb(gy), psg, arg, mb(gx), psx, cb(mask), C,
+                                                        C8, H, W, k, s, OH, OW, flat_ld);
+    return check_launch("maxpool_bwd_flat");
+  }
+  if (flat_ld == 0 && k == 3 && s == 2) {
+    maxpool_bwd_nhwc_kernel<3, 2><<<grid_for(total), 256, 0, st>>>(
+        cb(gy), psg, arg, mb(gx), psx, cb(mask), N, C, C8, H, W, OH, OW, FastDiv(C8 / 8),
+        FastDiv(W), FastDiv(H));
+    return check_launch("maxpool_bwd_nhwc");
+  }
+  if (flat_ld == 0 && k == 2 && s == 2) {
+    maxpool_bwd_nhwc_kernel<2, 2><<<grid_for(total), 256, 0, st>>>(
+        cb(gy), psg, arg, mb(gx), psx, cb(mask), N, C, C8, H, W, OH, OW, FastDiv(C8 / 8),
+        FastDiv(W), FastDiv(H));
+    return check_launch("maxpool_bwd_nhwc");
+  }
+  maxpool_bwd_split_kernel<<<grid_for(total), 256, 0, st>>>(
       cb(gy), psg, arg, mb(gx), psx, cb(mask), N, C, C8, H, W, k, s, OH, OW, flat_ld,
       FastDiv(C8 / 8), FastDiv(W), FastDiv(H));
   return check_launch("maxpool_bwd");
@@ -1252,6 +1299,12 @@ int stzx_pack_s2d(const float* x, void* xp, size_t ps, int N, int C, int H, int 
   if (Cs8 % 8 || Cs8 < C * s * s) return fail(STZ_EINVAL, "pack_s2d: bad channel padding");
   const size_t total = (size_t)N * Hs * Ws * Cs8 / 8;
   if (total == 0) return STZ_OK;
+  const size_t rows_smem = (size_t)C * s * s * Ws * sizeof(float);
+  if (C == 3 && s == 4 && rows_smem <= 48 * 1024 && Cs8 % 8 == 0) {
+    pack_s2d_rows_kernel<3, 4><<<N * Hs, 256, rows_smem, as_stream(stream)>>>(x, mb(xp), ps, H, W,
+                                                                              p, Hs, Ws, Cs8);
+    return check_launch("pack_s2d_rows");
+  }
   pack_s2d_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
       x, mb(xp), ps, N, C, H, W, s, p, Hs, Ws, Cs8, FastDiv(Cs8 / 8), FastDiv(Ws), FastDiv(Hs));
   return check_launch("pack_s2d");

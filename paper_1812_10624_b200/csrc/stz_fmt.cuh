@@ -330,6 +330,228 @@ __global__ void maxpool_bwd_split_kernel(const bf16_t* __restrict__ gy, size_t p
   }
 }
 
+// ---- max-pool, faster forms -------------------------------------------------
+
+// backward, NHWC gy, compile-time window (K, S): the <= ceil(K/S)^2 windows
+// covering a cell are known up front, so every load (argmax bytes, gradient
+// planes, ReLU mask) is issued before the float64 accumulation, which keeps
+// the reference's (kh, kw) order (oh, ow descending).
+template <int K, int S>
+__global__ void maxpool_bwd_nhwc_kernel(const bf16_t* __restrict__ gy, size_t psg,
+                                        const uint8_t* __restrict__ arg,
+                                        bf16_t* __restrict__ gx, size_t psx,
+                                        const bf16_t* __restrict__ mask, int N, int C, int C8,
+                                        int H, int W, int OH, int OW, FastDiv d_ch, FastDiv d_w,
+                                        FastDiv d_h) {
+  constexpr int R = (K + S - 1) / S;
+  const uint32_t total = (uint32_t)N * H * W * (C8 / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t pix, cc, t, w, n, h;
+    d_ch.divmod(i, pix, cc);
+    d_w.divmod(pix, t, w);
+    d_h.divmod(t, n, h);
+    const size_t xi = (size_t)pix * C8 + cc * 8;
+    uint4 mk = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (mask) mk = __ldg(reinterpret_cast<const uint4*>(mask + xi));
+    const int oh_hi = min(OH - 1, (int)h / S), ow_hi = min(OW - 1, (int)w / S);
+    bool ok[R][R];
+    uint2 ar[R][R];
+    float g[R][R][8];
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        const int oh = oh_hi - a, ow = ow_hi - b;
+        ok[a][b] = oh >= 0 && ow >= 0 && (int)h - oh * S < K && (int)w - ow * S < K;
+        if (ok[a][b]) {
+          const size_t o = (((size_t)n * OH + oh) * OW + ow) * C8 + cc * 8;
+          ar[a][b] = __ldg(reinterpret_cast<const uint2*>(arg + o));
+          load_split8(gy + o, psg, g[a][b]);
+        }
+      }
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        if (!ok[a][b]) continue;
+        const uint32_t want =
+            (uint32_t)(((int)h - (oh_hi - a) * S) * K + ((int)w - (ow_hi - b) * S));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t aj = ((j < 4 ? ar[a][b].x : ar[a][b].y) >> (8 * (j & 3))) & 0xFFu;
+          if (aj == want) acc[j] += (double)g[a][b][j];
+        }
+      }
+    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t hb = (mw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;   // bf16 > 0
+      const bool keep = !mask || (hb != 0u && hb < 0x8000u);
+      v[j] = ((int)(cc * 8 + j) < C && keep) ? (float)acc[j] : 0.f;
+    }
+    store_split8(gx + xi, psx, v);
+  }
+}
+
+// forward into the CHW-flat FC boundary, one block per image: windows are
+// scanned NHWC (coalesced, 8 channels per thread), the maxima land in shared
+// memory in flat (c, oh, ow) order and leave as coalesced 8-element rows; the
+// row's padding columns [C*OH*OW, flat_ld) are zeroed here too.
+__global__ void maxpool_fwd_flat_kernel(const bf16_t* __restrict__ x, size_t psx,
+                                        bf16_t* __restrict__ y, size_t psy,
+                                        uint8_t* __restrict__ arg, int C, int C8, int H, int W,
+                                        int k, int s, int OH, int OW, int flat_ld) {
+  extern __shared__ float sflat[];   // [C * OH * OW]
+  const int n = blockIdx.x;
+  const int chunks = C8 / 8, items = OH * OW * chunks, D = C * OH * OW;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int cc = it % chunks, opix = it / chunks, oh = opix / OW, ow = opix % OW;
+    const size_t base = (((size_t)n * H + (size_t)oh * s) * W + (size_t)ow * s) * C8 + cc * 8;
+    float best[8];
+    int bi[8];
+    load_split8(x + base, psx, best);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bi[j] = 0;
+    for (int kh = 0; kh < k; ++kh)
+      for (int kw = 0; kw < k; ++kw) {
+        if ((kh | kw) == 0) continue;
+        float v[8];
+        load_split8(x + base + ((size_t)kh * W + kw) * C8, psx, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v[j] > best[j]) {
+            best[j] = v[j];
+            bi[j] = kh * k + kw;
+          }
+      }
+    uint2 packed;
+    packed.x = (uint32_t)bi[0] | ((uint32_t)bi[1] << 8) | ((uint32_t)bi[2] << 16) |
+               ((uint32_t)bi[3] << 24);
+    packed.y = (uint32_t)bi[4] | ((uint32_t)bi[5] << 8) | ((uint32_t)bi[6] << 16) |
+               ((uint32_t)bi[7] << 24);
+    *reinterpret_cast<uint2*>(arg + ((size_t)n * OH * OW + opix) * C8 + cc * 8) = packed;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = cc * 8 + j;
+      if (c < C) sflat[(c * OH + oh) * OW + ow] = best[j];
+    }
+  }
+  __syncthreads();
+  bf16_t* row = y + (size_t)n * flat_ld;
+  for (int q = threadIdx.x; q < flat_ld / 8; q += blockDim.x) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = q * 8 + j < D ? sflat[q * 8 + j] : 0.f;
+    store_split8(row + q * 8, psy, v);
+  }
+}
+
+// backward from the CHW-flat FC boundary, one block per image: the image's
+// gradient row is staged in shared memory (coalesced), then every input cell
+// gathers in float64, (kh, kw) order, as maxpool_bwd_split_kernel does.
+__global__ void maxpool_bwd_flat_kernel(const bf16_t* __restrict__ gy, size_t psg,
+                                        const uint8_t* __restrict__ arg,
+                                        bf16_t* __restrict__ gx, size_t psx,
+                                        const bf16_t* __restrict__ mask, int C, int C8, int H,
+                                        int W, int k, int s, int OH, int OW, int flat_ld) {
+  extern __shared__ float sflat[];   // [C * OH * OW]
+  const int n = blockIdx.x;
+  const int D = C * OH * OW;
+  const bf16_t* row = gy + (size_t)n * flat_ld;
+  for (int q = threadIdx.x; q < (D + 7) / 8; q += blockDim.x) {
+    float v[8];
+    load_split8(row + q * 8, psg, v);   // flat_ld % 8 == 0: the padded tail is readable
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (q * 8 + j < D) sflat[q * 8 + j] = v[j];
+  }
+  __syncthreads();
+  const int chunks = C8 / 8, items = H * W * chunks;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int cc = it % chunks, pix = it / chunks, h = pix / W, w = pix % W;
+    const size_t xi = ((size_t)n * H * W + pix) * C8 + cc * 8;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    const int th = h - k + 1, tw = w - k + 1;
+    const int oh_lo = th <= 0 ? 0 : (th + s - 1) / s, ow_lo = tw <= 0 ? 0 : (tw + s - 1) / s;
+    const int oh_hi = min(OH - 1, h / s), ow_hi = min(OW - 1, w / s);
+    for (int oh = oh_hi; oh >= oh_lo; --oh)
+      for (int ow = ow_hi; ow >= ow_lo; --ow) {
+        const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(
+            arg + (((size_t)n * OH + oh) * OW + ow) * C8 + cc * 8));
+        const uint32_t want = (uint32_t)((h - oh * s) * k + (w - ow * s));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = cc * 8 + j;
+          const uint32_t aj = ((j < 4 ? a2.x : a2.y) >> (8 * (j & 3))) & 0xFFu;
+          if (aj == want && c < C) acc[j] += (double)sflat[(c * OH + oh) * OW + ow];
+        }
+      }
+    uint4 mk = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (mask) mk = __ldg(reinterpret_cast<const uint4*>(mask + xi));
+    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t hb = (mw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+      const bool keep = !mask || (hb != 0u && hb < 0x8000u);
+      v[j] = (cc * 8 + j < C && keep) ? (float)acc[j] : 0.f;
+    }
+    store_split8(gx + xi, psx, v);
+  }
+}
+
+// space-to-depth input pack, one block per (image, s2d row i): the C x S
+// input rows i*S - pad .. i*S - pad + S - 1 are read coalesced and staged in
+// shared memory as [c][dy][dx][j] (the s2d column j fastest, so the gather
+// below is conflict-free), then every s2d pixel of the row leaves as 16-byte
+// 8-channel chunks per plane.  C and S are compile-time (AlexNet conv1: 3, 4),
+// which turns every index division into a multiply / shift -- the generic
+// form of this kernel was bound by integer division.
+template <int C, int S>
+__global__ void pack_s2d_rows_kernel(const float* __restrict__ x, bf16_t* __restrict__ xp,
+                                     size_t ps, int H, int W, int pad, int Hs, int Ws, int Cs8) {
+  extern __shared__ float srows[];   // [C][S][S][Ws]
+  const int n = blockIdx.x / Hs, i = blockIdx.x % Hs;
+  const int WS = Ws * S;   // padded-input columns the row covers
+  // stage: row r = c*S + dy, columns col in [0, WS); one column per thread,
+  // all C*S rows' loads in flight before the shared stores
+  for (int col = threadIdx.x; col < WS; col += blockDim.x) {
+    const int iw = col - pad;
+    const bool col_ok = iw >= 0 && iw < W;
+    float v[C * S];
+#pragma unroll
+    for (int r = 0; r < C * S; ++r) {
+      const int c = r / S, dy = r % S;
+      const int ih = i * S + dy - pad;
+      v[r] = (col_ok && ih >= 0 && ih < H) ? __ldg(x + (((size_t)n * C + c) * H + ih) * W + iw)
+                                           : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < C * S; ++r) srows[(r * S + col % S) * Ws + col / S] = v[r];
+  }
+  __syncthreads();
+  constexpr int CS = C * S * S;
+  const int chunks = Cs8 / 8;
+  bf16_t* out = xp + ((size_t)n * Hs + i) * Ws * Cs8;
+  for (int q = threadIdx.x; q < Ws * chunks; q += blockDim.x) {
+    const int cc = q % chunks, j = q / chunks;
+    float v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int cp = cc * 8 + t;
+      // channel cp = (dy*S + dx)*C + c  ->  srows[c][dy][dx][j]
+      v[t] = cp < CS ? srows[((cp % C) * S * S + cp / C) * Ws + j] : 0.f;
+    }
+    store_split8(out + (size_t)j * Cs8 + cc * 8, ps, v);
+  }
+}
+
 // standalone ReLU on split planes (sign and zero-ness live in plane 0)
 __global__ void relu_fwd_split_kernel(const bf16_t* __restrict__ x, size_t psx,
                                       bf16_t* __restrict__ y, size_t psy, size_t n) {
