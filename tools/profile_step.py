@@ -1,5 +1,6 @@
 """One AlexNet (K=128) co-located layer-separated step for ncu: 2 warm-up
-steps, then exactly one more step (the one to profile)."""
+steps, then exactly one more step (the one to profile), inside the NVTX
+range "step"."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -17,6 +18,8 @@ for _ in range(2):
     cl.step(x=x, labels=y)
 torch.cuda.synchronize()
 n0 = _lib.load().stz_launch_count()
+torch.cuda.nvtx.range_push("step")   # ncu --nvtx --nvtx-include "step/" isolates it
 cl.step(x=x, labels=y)
+torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 print("launches per step:", _lib.load().stz_launch_count() - n0)
