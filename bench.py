@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool", type=int, default=4, help="device-resident input batches")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (N=1 uses graphs)")
+    ap.add_argument("--micro", type=int, default=None,
+                    help="micro-batches per iteration for N>1 (default: 4 when K allows)")
     return ap.parse_args()
 
 
@@ -260,7 +262,8 @@ def main():
         raise RuntimeError("bench feeds device-resident batches")
 
     cl = StanzaCluster(spec, n_conv=n_conv, n_fc=n_fc, batch_fn=batch_fn, lr=0.01,
-                       momentum=0.9, seed=3, device=dev, comm=comm)
+                       momentum=0.9, seed=3, device=dev, comm=comm,
+                       micro_batches=args.micro)
     is_conv_rank = cl.conv is not None
     classes = spec.layers[-2].out_dim
     gen = torch.Generator(device=dev)
@@ -481,7 +484,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (N(0,1) images, uniform labels, "
                                     "device-resident pool, random-init weights)",
-            "config": workload_config(args, n_conv, n_fc, k),
+            "config": dict(workload_config(args, n_conv, n_fc, k), micro_batches=cl.micro),
             "roofline": conv_ex["roofline"],
             "cpu_baseline": cpu,
             "e2e": {"value": images / (e2e_ms / 1e3), "unit": UNIT,

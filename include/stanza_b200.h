@@ -170,8 +170,8 @@ int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void*
                     int p, void* ws, size_t ws_bytes, void* stream);
 /* Conv2d weight / bias gradient sums into fp32 [O,C,k,k] / [O] (tensor_core.py:253-259). */
 int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
-                    int N, int C, int C8, int H, int W, int O, int O8, int k, int s, int p,
-                    void* ws, size_t ws_bytes, void* stream);
+                    int accumulate, int N, int C, int C8, int H, int W, int O, int O8, int k,
+                    int s, int p, void* ws, size_t ws_bytes, void* stream);
 /* FC forward (tensor_core.py:205-211): split output (y) or fp32 logits (y_f32). */
 int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const float* bias, void* y,
                 size_t psy, float* y_f32, int M, int in_dim, int in8, int out_dim, int out8,
@@ -180,10 +180,12 @@ int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const floa
 int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx, size_t psgx,
                   const void* mask, int M, int in_dim, int in8, int out8, void* ws,
                   size_t ws_bytes, void* stream);
-/* FC weight / bias gradient sums (tensor_core.py:287-288). */
+/* FC weight / bias gradient sums (tensor_core.py:287-288).  The engine-level
+ * weight-gradient entries take `accumulate`: 0 writes gw / gb, 1 adds into
+ * them (micro-batches of one iteration summing into the same gradient). */
 int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
-                  int M, int in_dim, int in8, int out_dim, int out8, void* ws, size_t ws_bytes,
-                  void* stream);
+                  int accumulate, int M, int in_dim, int in8, int out_dim, int out8, void* ws,
+                  size_t ws_bytes, void* stream);
 /* MaxPool2d (tensor_core.py:183-198 / :263-276); flat_ld > 0 selects the
  * CHW-flat [N][flat_ld] layout for y / gy (the FC-block boundary). */
 int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
@@ -205,8 +207,8 @@ int stzx_pack_s2d(const float* x, void* xp, size_t ps, int N, int C, int H, int 
 int stzx_pack_conv_w_s2d(const float* w, void* wf, size_t ps, int O, int C, int k, int s,
                          int Cs8, void* stream);
 int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, float* gw,
-                        float* gb, int N, int C, int Cs8, int Hs, int Ws, int O, int O8, int k,
-                        int s, void* ws, size_t ws_bytes, void* stream);
+                        float* gb, int accumulate, int N, int C, int Cs8, int Hs, int Ws, int O,
+                        int O8, int k, int s, void* ws, size_t ws_bytes, void* stream);
 /* SoftmaxCE on fp32 logits -> losses + split dlogits [M][C8]. */
 int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
                     int M, int C, int C8, void* stream);

@@ -55,10 +55,10 @@ SIGNATURES = {
     "stzx_flat_to_nhwc": (I, [P, Z, P, Z, I, I, I, I, I, I, P]),
     "stzx_conv_fwd": (I, [P, Z, P, Z, P, P, Z, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_conv_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
-    "stzx_conv_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_conv_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_fc_fwd": (I, [P, Z, P, Z, P, P, Z, P, I, I, I, I, I, I, P, Z, P]),
     "stzx_fc_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, P, Z, P]),
-    "stzx_fc_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, P, Z, P]),
+    "stzx_fc_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, P, Z, P]),
     "stzx_maxpool_fwd": (I, [P, Z, P, Z, P, I, I, I, I, I, I, I, I, P]),
     "stzx_maxpool_bwd": (I, [P, Z, P, P, Z, P, I, I, I, I, I, I, I, I, P]),
     "stzx_relu_fwd": (I, [P, Z, P, Z, Z, P]),
@@ -66,7 +66,7 @@ SIGNATURES = {
     "stzx_softmax_ce": (I, [P, P, P, P, Z, I, I, I, P]),
     "stzx_pack_s2d": (I, [P, P, Z, I, I, I, I, I, I, I, I, I, P]),
     "stzx_pack_conv_w_s2d": (I, [P, P, Z, I, I, I, I, I, P]),
-    "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
 }
 
 

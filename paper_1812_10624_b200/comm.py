@@ -14,6 +14,12 @@ exchanges of the layer-separated step (stanza_runtime.py:228-338):
 All of it is expressed with torch.distributed point-to-point ops and
 sub-group collectives, so the same code runs over NCCL on B200s and over
 gloo on CPU tensors (the multi-process CPU tests).
+
+Micro-batch pipelining posts the two P2P directions
+asynchronously: a CONV worker sends every micro-batch's activations before
+it receives any boundary gradient, while its FC worker alternates receive /
+compute / send.  Each direction therefore runs on its own communicator (own
+NCCL stream), so neither queue can block the other.
 """
 
 from __future__ import annotations
@@ -43,6 +49,22 @@ class RoleComm:
         self.fc_group = dist.new_group(self.fc_ranks) if n_fc > 1 else None
         self.is_conv = self.rank < n_conv
         self.index = self.rank if self.is_conv else self.rank - n_conv
+        # one communicator per P2P direction for the pipelined step
+        everyone = list(range(self.world))
+        self.act_group = dist.new_group(everyone)
+        self.grad_group = dist.new_group(everyone)
+        self._warm = False
+
+    def warm(self, device) -> None:
+        """Create the NCCL communicators of the P2P groups eagerly (a P2P op
+        must not be the first call on an NCCL group unless every rank joins)."""
+        if self._warm:
+            return
+        dev = torch.device(device) if dist.get_backend() == "nccl" else torch.device("cpu")
+        t = torch.zeros(1, device=dev)
+        for g in (self.act_group, self.grad_group):
+            dist.all_reduce(t, group=g)
+        self._warm = True
 
     # -- topology -------------------------------------------------------------------
 
@@ -82,6 +104,34 @@ class RoleComm:
                 ops += [dist.P2POp(dist.isend, t, i) for t in send[pos]]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+
+    # -- asynchronous exchanges (micro-batch pipelining) ----------------------------
+
+    def post_activations(self, send: list | None, recv: list | None) -> list:
+        """Like gather_activations for ONE micro-batch, but posted on the
+        activation communicator and returned un-waited (wait() on the FC side
+        before the tensors are read; on the CONV side before the buffers are
+        overwritten)."""
+        ops = []
+        if self.is_conv:
+            dst = self.fc_rank_of(self.index)
+            ops += [dist.P2POp(dist.isend, t, dst, group=self.act_group) for t in send]
+        else:
+            for pos, i in enumerate(self.members(self.index)):
+                ops += [dist.P2POp(dist.irecv, t, i, group=self.act_group) for t in recv[pos]]
+        return dist.batch_isend_irecv(ops)
+
+    def post_boundary(self, send: list | None, recv: list | None) -> list:
+        """scatter_boundary for ONE micro-batch on the gradient communicator,
+        returned un-waited."""
+        ops = []
+        if self.is_conv:
+            src = self.fc_rank_of(self.index)
+            ops += [dist.P2POp(dist.irecv, t, src, group=self.grad_group) for t in recv]
+        else:
+            for pos, i in enumerate(self.members(self.index)):
+                ops += [dist.P2POp(dist.isend, t, i, group=self.grad_group) for t in send[pos]]
+        return dist.batch_isend_irecv(ops)
 
     def allreduce_grads(self, flat: torch.Tensor) -> None:
         """Sum the flat gradient vector over this rank's role group."""

@@ -679,6 +679,7 @@ EpF32 ep_f32(float* out, int M, int N, uint32_t mdiv, long long ld_hi, long long
   e.bias = bias;
   e.mask = mask;
   e.relu = relu;
+  e.accumulate = 0;
   return e;
 }
 
@@ -802,7 +803,7 @@ int gemm_fc_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, cons
 }
 
 int colsum_split(const bf16_t* g, size_t ps, int R, int N, int ld, float* out, void* ws,
-                 size_t ws_bytes, cudaStream_t st) {
+                 size_t ws_bytes, cudaStream_t st, int accumulate = 0) {
   const int N8 = rup8(N);
   const int chunks = N8 / 8;
   const int lanes = chunks < 256 ? 256 / chunks : 1;
@@ -815,7 +816,7 @@ int colsum_split(const bf16_t* g, size_t ps, int R, int N, int ld, float* out, v
   colsum_partial_kernel<<<blocks, 256, 0, st>>>(g, ps, R, N8, ld, rpb, part);
   int rc = check_launch("colsum_partial");
   if (rc) return rc;
-  colsum_final_kernel<<<cdiv(N, 8), 256, 0, st>>>(part, blocks, N, N8, out);
+  colsum_final_kernel<<<cdiv(N, 8), 256, 0, st>>>(part, blocks, N, N8, out, accumulate);
   return check_launch("colsum_final");
 }
 
@@ -1139,16 +1140,16 @@ int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void*
 }
 
 int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
-                    int N, int C, int C8, int H, int W, int O, int O8, int k, int s, int p,
-                    void* ws, size_t ws_bytes, void* stream) {
+                    int accumulate, int N, int C, int C8, int H, int W, int O, int O8, int k,
+                    int s, int p, void* ws, size_t ws_bytes, void* stream) {
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad: bad shape");
   cudaStream_t st = as_stream(stream);
-  EpConvWgrad e{gw, k * k * C8, O, C, k * k, FastDiv(C8)};
+  EpConvWgrad e{gw, k * k * C8, O, C, k * k, FastDiv(C8), accumulate ? 1 : 0};
   int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, C8, H, W, O, O8, k, s, p, OH, OW, ws,
                            ws_bytes, st);
   if (rc || !gb) return rc;
-  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st);
+  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);
 }
 
 int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const float* bias, void* y,
@@ -1175,15 +1176,16 @@ int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx
 }
 
 int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
-                  int M, int in_dim, int in8, int out_dim, int out8, void* ws, size_t ws_bytes,
-                  void* stream) {
+                  int accumulate, int M, int in_dim, int in8, int out_dim, int out8, void* ws,
+                  size_t ws_bytes, void* stream) {
   if (in8 % 8 || out8 % 8) return fail(STZ_EINVAL, "fc_wgrad: bad shape");
   cudaStream_t st = as_stream(stream);
   EpF32 e = ep_f32(gw, in_dim, out_dim, kRowMajor, 0, out_dim, 1, nullptr, nullptr, 0);
+  e.accumulate = accumulate ? 1 : 0;
   int rc = gemm_fc_wgrad(cb(x), psx, cb(g), psg, e, M, in_dim, in8, out_dim, out8, ws, ws_bytes,
                          st);
   if (rc || !gb) return rc;
-  return colsum_split(cb(g), psg, M, out_dim, out8, gb, ws, ws_bytes, st);
+  return colsum_split(cb(g), psg, M, out_dim, out8, gb, ws, ws_bytes, st, accumulate);
 }
 
 int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
@@ -1319,17 +1321,18 @@ int stzx_pack_conv_w_s2d(const float* w, void* wf, size_t ps, int O, int C, int 
 }
 
 int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, float* gw,
-                        float* gb, int N, int C, int Cs8, int Hs, int Ws, int O, int O8, int k,
-                        int s, void* ws, size_t ws_bytes, void* stream) {
+                        float* gb, int accumulate, int N, int C, int Cs8, int Hs, int Ws, int O,
+                        int O8, int k, int s, void* ws, size_t ws_bytes, void* stream) {
   const int ks = (k + s - 1) / s;
   const int OH = Hs - ks + 1, OW = Ws - ks + 1;
   if (OH <= 0 || OW <= 0 || Cs8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad_s2d: bad shape");
   cudaStream_t st = as_stream(stream);
-  EpConvWgradS2D e{gw, ks * ks * Cs8, O, C, k, s, ks, C * s * s, FastDiv(Cs8)};
+  EpConvWgradS2D e{gw, ks * ks * Cs8, O, C, k, s, ks, C * s * s, FastDiv(Cs8),
+                   accumulate ? 1 : 0};
   int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, Cs8, Hs, Ws, O, O8, ks, 1, 0, OH, OW, ws,
                            ws_bytes, st);
   if (rc || !gb) return rc;
-  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st);
+  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);
 }
 
 }  // extern "C"

@@ -679,13 +679,14 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16_t* __res
 // one warp per column: lane-strided partial sums + a fixed shuffle tree
 __global__ void __launch_bounds__(256) colsum_final_kernel(const double* __restrict__ part,
                                                            int blocks, int N, int N8,
-                                                           float* __restrict__ out) {
+                                                           float* __restrict__ out,
+                                                           int accumulate) {
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= N) return;
   double s = 0.0;
   for (int b = lane; b < blocks; b += 32) s += part[(size_t)b * N8 + c];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[c] = (float)s;
+  if (lane == 0) out[c] = accumulate ? __fadd_rn(out[c], (float)s) : (float)s;
 }
 
 }  // namespace stz

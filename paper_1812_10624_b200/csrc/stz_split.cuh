@@ -269,6 +269,7 @@ struct EpF32 {
   const float* bias;
   const float* mask;  // fp32, same indexing as out
   int relu;
+  int accumulate;     // 1: out += value (micro-batch gradient sums)
   static constexpr bool HAS_BIAS = true;
   __device__ __forceinline__ void bias8(int n0, float (&b)[8]) const {
     if (bias) {
@@ -283,7 +284,8 @@ struct EpF32 {
     uint32_t q, r;
     d_m.divmod((uint32_t)m, q, r);
     const long long row = (long long)q * ld_hi + (long long)r * ld_lo;
-    if (ld_n == 1 && n0 + 8 <= N && !mask && ((row + n0) & 3) == 0) {
+    if (ld_n == 1 && n0 + 8 <= N && !mask &&
+        (reinterpret_cast<uintptr_t>(out + row + n0) & 15) == 0) {   // views may be offset
       float w[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -292,6 +294,13 @@ struct EpF32 {
         w[j] = x;
       }
       float4* dst = reinterpret_cast<float4*>(out + row + n0);
+      if (accumulate) {
+        const float4 a = dst[0], b = dst[1];
+        w[0] = __fadd_rn(a.x, w[0]); w[1] = __fadd_rn(a.y, w[1]);
+        w[2] = __fadd_rn(a.z, w[2]); w[3] = __fadd_rn(a.w, w[3]);
+        w[4] = __fadd_rn(b.x, w[4]); w[5] = __fadd_rn(b.y, w[5]);
+        w[6] = __fadd_rn(b.z, w[6]); w[7] = __fadd_rn(b.w, w[7]);
+      }
       dst[0] = make_float4(w[0], w[1], w[2], w[3]);
       dst[1] = make_float4(w[4], w[5], w[6], w[7]);
       return;
@@ -304,7 +313,7 @@ struct EpF32 {
       float x = v[j];
       if (relu && x < 0.f) x = 0.f;
       if (mask && !(__ldg(mask + idx) > 0.f)) x = 0.f;
-      out[idx] = x;
+      out[idx] = accumulate ? __fadd_rn(out[idx], x) : x;
     }
   }
   __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
@@ -324,6 +333,7 @@ struct EpConvWgrad {
   float* gw;
   int M, N, C, kk;
   FastDiv d_c8;
+  int accumulate;   // 1: gw += value (micro-batch gradient sums)
   static constexpr bool HAS_BIAS = false;
   __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
   __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const { store8(m, n0, v); }
@@ -335,7 +345,10 @@ struct EpConvWgrad {
     const size_t base = (size_t)c * kk + tap;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (n0 + j < N) gw[(size_t)(n0 + j) * C * kk + base] = v[j];
+      if (n0 + j < N) {
+        float* d = gw + (size_t)(n0 + j) * C * kk + base;
+        *d = accumulate ? __fadd_rn(*d, v[j]) : v[j];
+      }
   }
 };
 
@@ -346,6 +359,7 @@ struct EpConvWgradS2D {
   float* gw;
   int M, N, C, k, s, ks, Cs;
   FastDiv d_cs8;
+  int accumulate;   // 1: gw += value
   static constexpr bool HAS_BIAS = false;
   __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
   __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const { store8(m, n0, v); }
@@ -360,7 +374,10 @@ struct EpConvWgradS2D {
     const size_t base = ((size_t)c * k + kh) * k + kw;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (n0 + j < N) gw[(size_t)(n0 + j) * C * k * k + base] = v[j];
+      if (n0 + j < N) {
+        float* d = gw + (size_t)(n0 + j) * C * k * k + base;
+        *d = accumulate ? __fadd_rn(*d, v[j]) : v[j];
+      }
   }
 };
 

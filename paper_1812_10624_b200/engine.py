@@ -230,6 +230,7 @@ class BlockEngine:
         self.losses = None
         self.dlogits = None
         self.xin = None   # packed block input, allocated on first pack_input()
+        self._gout = None  # per-op output-gradient buffers of the last backward
         for i, op in enumerate(self.ops):
             if op.kind == "relu" and i > 0 and self.ops[i - 1].fused_relu:
                 continue
@@ -308,17 +309,29 @@ class BlockEngine:
 
     # -- execution -------------------------------------------------------------------
 
-    def op_flops(self, i: int) -> float:
+    def op_flops(self, i: int, rows: int | None = None) -> float:
         """Algorithmic FLOPs of op i's forward contraction (2*M*N*K with the
-        logical channel counts); its dgrad and wgrad have the same count."""
+        logical channel counts) over `rows` samples (default: the batch); its
+        dgrad and wgrad have the same count."""
         op = self.ops[i]
         l = op.layer
+        b = self.batch if rows is None else rows
         if op.kind == "conv":
             _, oh, ow = op.out_shape
-            return 2.0 * self.batch * oh * ow * l.out_ch * l.in_ch * l.kernel * l.kernel
+            return 2.0 * b * oh * ow * l.out_ch * l.in_ch * l.kernel * l.kernel
         if op.kind == "fc":
-            return 2.0 * self.batch * l.in_dim * l.out_dim
+            return 2.0 * b * l.in_dim * l.out_dim
         return 0.0
+
+    def _rows(self, rows):
+        """(r0, r1, view) for a pass over samples [r0, r1) of the batch (a
+        micro-batch): view(split) restricts a full-batch Split to those rows."""
+        r0, r1 = (0, self.batch) if rows is None else (int(rows[0]), int(rows[1]))
+        if not 0 <= r0 < r1 <= self.batch:
+            raise ShapeMismatch(f"rows {rows} outside the batch of {self.batch}")
+        if (r0, r1) == (0, self.batch):
+            return r0, r1, (lambda sp: sp)
+        return r0, r1, (lambda sp: None if sp is None else sp.rows_view(r0, r1))
 
     def _act(self, i):
         """Output Split of op i, resolving ReLU / Flatten aliases."""
@@ -334,11 +347,14 @@ class BlockEngine:
     def _input(self, i):
         return self._x if i == 0 else self._act(i - 1)
 
-    def pack_input(self, x: torch.Tensor) -> Split:
-        """fp32 batch in the reference layout -> the packed block input."""
+    def pack_input(self, x: torch.Tensor, rows=None) -> Split:
+        """fp32 batch in the reference layout -> the packed block input (only
+        samples [r0, r1) when `rows` is given).  Returns the full-batch Split."""
         if tuple(x.shape) != (self.batch, *self.in_shape):
             raise ShapeMismatch(f"block expects {(self.batch, *self.in_shape)}, "
                                 f"got {tuple(x.shape)}")
+        r0, r1, view = self._rows(rows)
+        b = r1 - r0
         st = stream_of(self.device)
         op0 = self.ops[0]
         if self.xin is None:
@@ -349,38 +365,42 @@ class BlockEngine:
                                        l0.in_ch * l0.stride ** 2, self.device)
             else:
                 self.xin = self._split_for(self.in_shape, self.batch)
-        s = self.xin
+        s = view(self.xin)
+        xs = x[r0:r1]
         if op0.s2d is not None:
             ks, cs8, hs, ws_ = op0.s2d
             c, h, w = self.in_shape
-            _lib.call("stzx_pack_s2d", ptr(x), s.ptr(), s.ps, self.batch, c, h, w,
+            _lib.call("stzx_pack_s2d", ptr(xs), s.ptr(), s.ps, b, c, h, w,
                       op0.layer.stride, op0.layer.padding, hs, ws_, cs8, st)
         elif s.layout == "nhwc":
             c, h, w = self.in_shape
-            _lib.call("stzx_pack_nchw", ptr(x), s.ptr(), s.ps, self.batch, c, h, w, s.width, st)
+            _lib.call("stzx_pack_nchw", ptr(xs), s.ptr(), s.ps, b, c, h, w, s.width, st)
         else:
-            _lib.call("stzx_pack_rows", ptr(x), s.ptr(), s.ps, self.batch, self.in_shape[0],
+            _lib.call("stzx_pack_rows", ptr(xs), s.ptr(), s.ps, b, self.in_shape[0],
                       s.width, st)
-        return s
+        return self.xin
 
     def forward(self, x, labels: torch.Tensor | None = None,
-                loss_out: torch.Tensor | None = None):
+                loss_out: torch.Tensor | None = None, rows=None):
         """Run the block.  ``x`` is a fp32 batch in the reference layout or an
-        already-packed Split (e.g. the CONV block's output rows).  Returns the
-        output Split (per-sample fp32 losses for a loss block).  The float64
+        already-packed Split (e.g. the CONV block's output rows), always
+        full-batch shaped; ``rows = (r0, r1)`` runs only samples [r0, r1) (a
+        micro-batch; ``labels`` is full-batch too).  Returns the output Split
+        of those rows (per-sample fp32 losses for a loss block).  The float64
         loss sum goes to ``loss_sum`` or is ADDED into ``loss_out``."""
+        r0, r1, V = self._rows(rows)
         if isinstance(x, torch.Tensor):
-            x = self.pack_input(x)
+            x = self.pack_input(x, rows)
         self._x = x
         st = stream_of(self.device)
         ws = workspace(self.device)
-        b = self.batch
+        b = r1 - r0
         for i, op in enumerate(self.ops):
-            xin = self._input(i)
+            xin = V(self._input(i))
             l = op.layer
             if op.kind == "conv":
                 c, h, w = op.in_shape
-                y = self.acts[i]
+                y = V(self.acts[i])
                 wf, _ = self.wplanes[i]
                 k, cs, pd = l.kernel, l.stride, l.padding
                 if op.s2d is not None:             # stride-1 conv over s2d blocks
@@ -389,127 +409,165 @@ class BlockEngine:
                 _lib.call("stzx_conv_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
                           ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w, l.out_ch,
                           y.width, k, cs, pd, int(op.fused_relu), ptr(ws),
-                          ws.numel(), st, flops=self.op_flops(i), tag=f"conv{i}_fwd")
+                          ws.numel(), st, flops=self.op_flops(i, b), tag=f"conv{i}_fwd")
             elif op.kind == "fc":
                 wp, _ = self.wplanes[i]
                 if self.acts[i] is not None:
-                    y = self.acts[i]
+                    y = V(self.acts[i])
                     _lib.call("stzx_fc_fwd", xin.ptr(), xin.ps, ptr(wp), wp[0].numel(),
                               ptr(self.params[i][1]), y.ptr(), y.ps, None, b, l.in_dim,
                               xin.width, l.out_dim, y.width, int(op.fused_relu), ptr(ws),
-                              ws.numel(), st, flops=self.op_flops(i), tag=f"fc{i}_fwd")
+                              ws.numel(), st, flops=self.op_flops(i, b), tag=f"fc{i}_fwd")
                 else:
                     _lib.call("stzx_fc_fwd", xin.ptr(), xin.ps, ptr(wp), wp[0].numel(),
-                              ptr(self.params[i][1]), None, 0, ptr(self.logits), b, l.in_dim,
-                              xin.width, l.out_dim, rup8(l.out_dim), int(op.fused_relu),
-                              ptr(ws), ws.numel(), st, flops=self.op_flops(i), tag=f"fc{i}_fwd")
+                              ptr(self.params[i][1]), None, 0, ptr(self.logits[r0:r1]), b,
+                              l.in_dim, xin.width, l.out_dim, rup8(l.out_dim), int(op.fused_relu),
+                              ptr(ws), ws.numel(), st, flops=self.op_flops(i, b),
+                              tag=f"fc{i}_fwd")
             elif op.kind == "maxpool":
                 c, h, w = op.in_shape
-                y = self.acts[i]
-                _lib.call("stzx_maxpool_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, ptr(self.args[i]),
-                          b, c, xin.width, h, w, l.kernel, l.stride,
+                y = V(self.acts[i])
+                _lib.call("stzx_maxpool_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps,
+                          ptr(self.args[i][r0:r1]), b, c, xin.width, h, w, l.kernel, l.stride,
                           y.width if op.flat_out else 0, st)
             elif op.kind == "relu":
                 if self.acts[i] is not None:
-                    y = self.acts[i]
+                    y = V(self.acts[i])
                     _lib.call("stzx_relu_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps,
                               b * xin.row_elems, st)
             elif op.kind == "flatten":
                 if self.acts[i] is not None:               # NHWC -> CHW-flat relayout
                     c, h, w = op.in_shape
-                    y = self.acts[i]
+                    y = V(self.acts[i])
                     _lib.call("stzx_nhwc_to_flat", xin.ptr(), xin.ps, y.ptr(), y.ps, b, c, h, w,
                               xin.width, y.width, st)
             elif op.kind == "softmax_ce":
                 if labels is None:
                     raise ValueError("SoftmaxCrossEntropy needs labels")
                 c = op.in_shape[0]
-                _lib.call("stzx_softmax_ce", ptr(self.logits), ptr(labels), ptr(self.losses),
-                          self.dlogits.ptr(), self.dlogits.ps, b, c, self.dlogits.width, st)
+                dl = V(self.dlogits)
+                _lib.call("stzx_softmax_ce", ptr(self.logits[r0:r1]), ptr(labels[r0:r1]),
+                          ptr(self.losses[r0:r1]), dl.ptr(), dl.ps, b, c, dl.width, st)
                 tgt, acc = (self.loss_sum, 0) if loss_out is None else (loss_out, 1)
-                _lib.call("stz_sum_f32", ptr(self.losses), b, ptr(tgt), acc, st)
-        return self.losses if self.losses is not None else self._act(len(self.ops) - 1)
+                _lib.call("stz_sum_f32", ptr(self.losses[r0:r1]), b, ptr(tgt), acc, st)
+        if self.losses is not None:
+            return self.losses[r0:r1]
+        return V(self._act(len(self.ops) - 1))
 
-    def backward(self, gy: Split | None = None):
+    def backward(self, gy: Split | None = None, rows=None, accumulate: bool = False,
+                 phase: str = "all"):
         """Backward through the block; parameter-gradient sums land in
-        ``grad_flat``.  Returns the input-gradient Split (None when the block
-        was built with need_input_grad=False)."""
+        ``grad_flat`` (ADDED to it with ``accumulate``: micro-batches of one
+        iteration).  ``gy`` is full-batch shaped; ``rows = (r0, r1)`` runs
+        samples [r0, r1) of the last forward over them.  ``phase``:
+
+        * "all"   -- weight and input gradients, layer by layer;
+        * "dgrad" -- only the input-gradient chain (pool / ReLU / conv and FC
+          dgrad): what a peer waits for.  Each layer's output gradient stays
+          in its own full-batch buffer;
+        * "wgrad" -- only the weight / bias gradients, from the buffers a
+          "dgrad" pass left (over ``rows``; the FC worker runs it over the
+          whole batch after the boundary gradients have left).
+
+        Returns the input-gradient Split of ``rows`` (None when the block has
+        no input gradient, or for phase "wgrad")."""
+        if phase not in ("all", "dgrad", "wgrad"):
+            raise ValueError(f"unknown backward phase {phase!r}")
+        r0, r1, V = self._rows(rows)
         st = stream_of(self.device)
         ws = workspace(self.device)
-        b = self.batch
-        g = gy
+        b = r1 - r0
+        acc = int(bool(accumulate))
+        do_w, do_d = phase in ("all", "wgrad"), phase in ("all", "dgrad")
+        if phase == "wgrad":
+            if self._gout is None:
+                raise RuntimeError("backward(phase='wgrad') needs a preceding 'dgrad' pass")
+            for i, op in enumerate(self.ops):
+                if op.kind in ("conv", "fc"):
+                    self._wgrad(i, V(self._input(i)), V(self._gout[i]), b, acc, ws, st)
+            return None
+        gout = [None] * len(self.ops)   # full-batch output-gradient buffer per op
+        g_full = gy
         for i in range(len(self.ops) - 1, -1, -1):
             op = self.ops[i]
             l = op.layer
-            xin = self._input(i)
+            xin = V(self._input(i))
+            g = V(g_full)
+            gout[i] = g_full
             # the ReLU output feeding this op IS its input (possibly flattened):
             # > 0 exactly where the ReLU passed its gradient
             mptr = xin.ptr() if op.mask_from >= 0 else None
             if op.kind == "softmax_ce":
-                g = self.dlogits
+                g_full = self.dlogits
             elif op.kind == "flatten":
                 if self.acts[i] is not None:              # CHW-flat -> NHWC relayout back
                     c, h, w = op.in_shape
-                    out = self.gin[i]
+                    out = V(self.gin[i])
                     _lib.call("stzx_flat_to_nhwc", g.ptr(), g.ps, out.ptr(), out.ps, b, c, h, w,
                               out.width, g.width, st)
-                    g = out
+                    g_full = self.gin[i]
             elif op.kind == "relu":
                 if not op.relu_bwd_fused:
-                    out = self.gin[i]
-                    src = self._act(i)
+                    out = V(self.gin[i])
+                    src = V(self._act(i))
                     _lib.call("stzx_relu_bwd", g.ptr(), g.ps, src.ptr(), out.ptr(), out.ps,
                               b * g.row_elems, st)
-                    g = out
+                    g_full = self.gin[i]
             elif op.kind == "maxpool":
                 if op.skip_dgrad:
-                    g = None
+                    g_full = None
                     continue
                 c, h, w = op.in_shape
-                out = self.gin[i]
-                _lib.call("stzx_maxpool_bwd", g.ptr(), g.ps, ptr(self.args[i]), out.ptr(), out.ps,
-                          mptr, b, c, out.width, h, w, l.kernel, l.stride,
+                out = V(self.gin[i])
+                _lib.call("stzx_maxpool_bwd", g.ptr(), g.ps, ptr(self.args[i][r0:r1]), out.ptr(),
+                          out.ps, mptr, b, c, out.width, h, w, l.kernel, l.stride,
                           g.width if op.flat_out else 0, st)
-                g = out
-            elif op.kind == "conv" and op.s2d is not None:
-                ks, cs8, hs, ws_ = op.s2d
-                _lib.call("stzx_conv_wgrad_s2d", xin.ptr(), xin.ps, g.ptr(), g.ps,
-                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), b, l.in_ch, cs8, hs, ws_,
-                          l.out_ch, g.width, l.kernel, l.stride, ptr(ws), ws.numel(), st,
-                          flops=self.op_flops(i), tag=f"conv{i}_wgrad")
-                g = None
-                continue
-            elif op.kind == "conv":
-                c, h, w = op.in_shape
-                _lib.call("stzx_conv_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
-                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), b, c, xin.width, h, w,
-                          l.out_ch, g.width, l.kernel, l.stride, l.padding, ptr(ws), ws.numel(),
-                          st, flops=self.op_flops(i), tag=f"conv{i}_wgrad")
-                if op.skip_dgrad:
-                    g = None
+                g_full = self.gin[i]
+            elif op.kind in ("conv", "fc"):
+                if do_w:
+                    self._wgrad(i, xin, g, b, acc, ws, st)
+                if op.skip_dgrad or (op.kind == "conv" and op.s2d is not None):
+                    g_full = None
                     continue
-                out = self.gin[i]
-                _, wd = self.wplanes[i]
-                _lib.call("stzx_conv_dgrad", g.ptr(), g.ps, ptr(wd), wd[0].numel(), out.ptr(),
-                          out.ps, mptr, b, c, out.width, h, w, g.width, l.kernel, l.stride,
-                          l.padding, ptr(ws), ws.numel(), st, flops=self.op_flops(i),
-                          tag=f"conv{i}_dgrad")
-                g = out
-            elif op.kind == "fc":
-                _lib.call("stzx_fc_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
-                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), b, l.in_dim, xin.width,
-                          l.out_dim, g.width, ptr(ws), ws.numel(), st, flops=self.op_flops(i),
-                          tag=f"fc{i}_wgrad")
-                if op.skip_dgrad:
-                    g = None
-                    continue
-                out = self.gin[i]
-                wp, _ = self.wplanes[i]
-                _lib.call("stzx_fc_dgrad", g.ptr(), g.ps, ptr(wp), wp[0].numel(), out.ptr(),
-                          out.ps, mptr, b, l.in_dim, out.width, g.width, ptr(ws), ws.numel(), st,
-                          flops=self.op_flops(i), tag=f"fc{i}_dgrad")
-                g = out
-        return g
+                out = V(self.gin[i])
+                if op.kind == "conv":
+                    c, h, w = op.in_shape
+                    _, wd = self.wplanes[i]
+                    _lib.call("stzx_conv_dgrad", g.ptr(), g.ps, ptr(wd), wd[0].numel(),
+                              out.ptr(), out.ps, mptr, b, c, out.width, h, w, g.width, l.kernel,
+                              l.stride, l.padding, ptr(ws), ws.numel(), st,
+                              flops=self.op_flops(i, b), tag=f"conv{i}_dgrad")
+                else:
+                    wp, _ = self.wplanes[i]
+                    _lib.call("stzx_fc_dgrad", g.ptr(), g.ps, ptr(wp), wp[0].numel(), out.ptr(),
+                              out.ps, mptr, b, l.in_dim, out.width, g.width, ptr(ws),
+                              ws.numel(), st, flops=self.op_flops(i, b), tag=f"fc{i}_dgrad")
+                g_full = self.gin[i]
+        self._gout = gout
+        return V(g_full)
+
+    def _wgrad(self, i, xin, g, b, acc, ws, st):
+        """Weight and bias gradient sums of conv / FC op i from its input rows
+        ``xin`` and output-gradient rows ``g`` (``acc``: add into grad_flat)."""
+        op = self.ops[i]
+        l = op.layer
+        if op.kind == "conv" and op.s2d is not None:
+            ks, cs8, hs, ws_ = op.s2d
+            _lib.call("stzx_conv_wgrad_s2d", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                      ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_ch, cs8,
+                      hs, ws_, l.out_ch, g.width, l.kernel, l.stride, ptr(ws), ws.numel(), st,
+                      flops=self.op_flops(i, b), tag=f"conv{i}_wgrad")
+        elif op.kind == "conv":
+            c, h, w = op.in_shape
+            _lib.call("stzx_conv_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                      ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, c, xin.width, h,
+                      w, l.out_ch, g.width, l.kernel, l.stride, l.padding, ptr(ws),
+                      ws.numel(), st, flops=self.op_flops(i, b), tag=f"conv{i}_wgrad")
+        else:
+            _lib.call("stzx_fc_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                      ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_dim,
+                      xin.width, l.out_dim, g.width, ptr(ws), ws.numel(), st,
+                      flops=self.op_flops(i, b), tag=f"fc{i}_wgrad")
 
     def sgd(self, n: int, lr: float, mu: float, grad: torch.Tensor | None = None):
         """Momentum step over the whole flat block (tensor_core.py:366-388),

@@ -103,7 +103,7 @@ class StanzaCluster:
                  momentum: float = 0.9, conv_time: float = 0.0, fc_unit_time: float = 0.0,
                  net=None, seed: int = 0, boundary: int | None = None,
                  state: TrainState | None = None, device=None, comm=None,
-                 time_phases: bool = False):
+                 time_phases: bool = False, micro_batches: int | None = None):
         if lr <= 0.0:
             raise ConfigError(f"learning rate must be positive, got {lr}")
         if not 0.0 <= momentum < 1.0:
@@ -122,6 +122,22 @@ class StanzaCluster:
         self.comm = comm
         self.time_phases = time_phases
         self.k = spec.batch_k
+        # micro-batch pipelining of CONV fwd -> gather -> FC -> scatter -> CONV bwd
+        # (one process per GPU only).  Gradient sums are
+        # unchanged up to fp32 summation order.
+        if micro_batches is None:
+            # measured (AlexNet K=128): 1:1 is fastest unsplit (28.5k vs 27.8k
+            # images/s at 2), 3:1 with 2 (77.8k vs 76.8k at 1, 75.3k at 4):
+            # split once the FC worker serves >= 3 CONV workers
+            group = max(plan_groups(n_conv, n_fc).count(j) for j in range(n_fc))
+            micro_batches = 2 if (comm is not None and group >= 3 and spec.batch_k % 2 == 0
+                                  and spec.batch_k >= 32) else 1
+        if micro_batches < 1 or spec.batch_k % micro_batches:
+            raise ConfigError(f"micro_batches={micro_batches} must divide batch_k="
+                              f"{spec.batch_k}")
+        if comm is None:
+            micro_batches = 1
+        self.micro = int(micro_batches)
         cut = self.partition.split_index
 
         ref = seeded_init(self.layers, seed)
@@ -244,25 +260,26 @@ class StanzaCluster:
 
     def step(self, loss_slot: torch.Tensor | None = None, x: torch.Tensor | None = None,
              labels: torch.Tensor | None = None) -> None:
-        """One BSP layer-separated iteration on the batch in ``self.x`` /
+        """One layer-separated iteration on the batch in ``self.x`` /
         ``self.labels`` (or on device-resident ``x`` / ``labels`` of the same
         shapes, e.g. a pre-staged pool).  Adds the iteration's summed
         per-sample loss into loss_slot (float64, on this process's FC
-        workers)."""
+        workers).  Single-device mode runs the reference's BSP phase order
+        below; one process per GPU runs _step_pipelined."""
         x_in = self.x if x is None else x
         lab_all = self.labels if labels is None else labels
-        n = self.n_conv * self.k
+        if self.comm is not None:
+            return self._step_pipelined(loss_slot, x_in, lab_all)
+        k = self.k
+        n = self.n_conv * k
         led = self.transport
-        a_bytes = self.boundary_activations * self.k * 4
+        a_bytes = self.boundary_activations * k * 4
         ev = self._events() if self.time_phases else None
         mark = (lambda label: ev.append((label, self._event()))) if ev is not None else \
             (lambda label: None)
-        comm = self.comm
-        k = self.k
-
         mark("conv_compute")
         led.record("conv_compute")
-        acts = self.conv.forward(x_in) if self.conv is not None else None
+        acts = self.conv.forward(x_in)
 
         mark("activations")
         led.record("activations", self.n_conv * (a_bytes + k * 4))
@@ -270,45 +287,19 @@ class StanzaCluster:
         led.tag_payload_bytes[Tag.CONTROL] += self.n_conv * k * 4
         led.tag_messages[Tag.ACTIVATIONS] += self.n_conv
         led.tag_messages[Tag.CONTROL] += self.n_conv
-        if comm is not None:
-            if comm.is_conv:
-                comm.gather_activations([acts.plane_rows(p) for p in range(3)] + [lab_all], None)
-            else:
-                recv = []
-                for pos in range(len(comm.members(comm.index))):
-                    rows = self.fc_in.rows_view(pos * k, (pos + 1) * k)
-                    recv.append([rows.plane_rows(p) for p in range(3)] +
-                                [self.labels[pos * k:(pos + 1) * k]])
-                comm.gather_activations(None, recv)
 
         mark("fc_compute")
         led.record("fc_compute")
         for j, eng in enumerate(self.fcs):
             lo, hi = eng.rows
-            if comm is None:
-                xin = acts.rows_view(lo, hi)
-                lab = lab_all[lo:hi]
-            else:
-                xin, lab = self.fc_in, self.labels
-            eng.forward(xin, lab, loss_out=loss_slot)
+            eng.forward(acts.rows_view(lo, hi), lab_all[lo:hi], loss_out=loss_slot)
             eng.backward()
 
         mark("boundary")
         led.record("boundary", self.n_conv * a_bytes)
         led.tag_payload_bytes[Tag.BOUNDARY_GRADS] += self.n_conv * a_bytes
         led.tag_messages[Tag.BOUNDARY_GRADS] += self.n_conv
-        if comm is not None:
-            if comm.is_conv:
-                comm.scatter_boundary(None, [self.gboundary.plane_rows(p) for p in range(3)])
-            else:
-                gx = self.fcs[0].gin[0]
-                send = []
-                for pos in range(len(comm.members(comm.index))):
-                    rows = gx.rows_view(pos * k, (pos + 1) * k)
-                    send.append([rows.plane_rows(p) for p in range(3)])
-                comm.scatter_boundary(send, None)
-        if self.conv is not None:
-            self.conv.backward(self.gboundary)
+        self.conv.backward(self.gboundary)
 
         mark("exchange")
         ring = lambda p, m: 0 if m == 1 else int(2 * (m - 1) * p * 4)  # noqa: E731
@@ -316,15 +307,112 @@ class StanzaCluster:
             (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
         led.record("exchange", ar_bytes)
         led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
-        if comm is not None:
-            if comm.is_conv:
-                comm.allreduce_grads(self.conv.grad_flat)
-            else:
-                comm.allreduce_grads(self.fcs[0].grad_flat)
-        else:
-            for eng in self.fcs[1:]:
-                self.fcs[0].add_grads_from(eng)
+        for eng in self.fcs[1:]:
+            self.fcs[0].add_grads_from(eng)
 
+        mark("update")
+        led.record("update")
+        self.conv.sgd(n, self.lr, self.momentum)
+        self.fcs[0].sgd(n, self.lr, self.momentum)
+        mark("end")
+        if ev is not None:
+            self._pending_events.append(ev)
+
+    def _step_pipelined(self, loss_slot, x_in, lab_all) -> None:
+        """One iteration in the one-process-per-GPU deployment, pipelined over
+        ``self.micro`` micro-batches of kb = K / micro samples per CONV worker.
+
+        CONV worker: forward each micro-batch and post its activations at
+        once (the FC worker starts while the next micro-batch is computed);
+        when every boundary gradient has arrived, one full-batch backward.
+        FC worker: per micro-batch, receive the group's rows (its input is
+        laid out [micro-batch][member][kb], so each micro-batch is
+        contiguous), run the FC forward and only the input-gradient chain,
+        and post each member's boundary rows back; the FC weight gradients
+        follow over the whole batch, overlapping the CONV backward.  With
+        micro = 1 this is the BSP step with the FC weight gradients moved off
+        the critical path.  Exchange and update are the BSP step's; the sums
+        are unchanged up to fp32 summation order."""
+        comm = self.comm
+        comm.warm(self.device)
+        m, k = self.micro, self.k
+        kb = k // m
+        n = self.n_conv * k
+        led = self.transport
+        a_bytes = self.boundary_activations * k * 4
+        ev = self._events() if self.time_phases else None
+        mark = (lambda label: ev.append((label, self._event()))) if ev is not None else \
+            (lambda label: None)
+        led.record("conv_compute")
+        led.record("activations", self.n_conv * (a_bytes + k * 4))
+        led.tag_payload_bytes[Tag.ACTIVATIONS] += self.n_conv * a_bytes
+        led.tag_payload_bytes[Tag.CONTROL] += self.n_conv * k * 4
+        led.tag_messages[Tag.ACTIVATIONS] += self.n_conv * m
+        led.tag_messages[Tag.CONTROL] += self.n_conv * m
+        led.record("fc_compute")
+        led.record("boundary", self.n_conv * a_bytes)
+        led.tag_payload_bytes[Tag.BOUNDARY_GRADS] += self.n_conv * a_bytes
+        led.tag_messages[Tag.BOUNDARY_GRADS] += self.n_conv * m
+
+        if comm.is_conv:
+            mark("conv_compute")
+            sends = []
+            for j in range(m):
+                rows = (j * kb, (j + 1) * kb)
+                acts = self.conv.forward(x_in, rows=rows)
+                sends += comm.post_activations(
+                    [acts.plane_rows(p) for p in range(3)] + [lab_all[rows[0]:rows[1]]], None)
+            mark("activations")
+            recvs = []
+            for j in range(m):
+                gb = self.gboundary.rows_view(j * kb, (j + 1) * kb)
+                recvs += comm.post_boundary(None, [gb.plane_rows(p) for p in range(3)])
+            mark("fc_compute")
+            for w in recvs:
+                w.wait()
+            mark("boundary")
+            self.conv.backward(self.gboundary)
+            for w in sends:
+                w.wait()
+        else:
+            eng = self.fcs[0]
+            g = len(comm.members(comm.index))
+            loss_to = loss_slot
+            if loss_to is None:           # micro-batch sums accumulate into loss_sum
+                eng.loss_sum.zero_()
+                loss_to = eng.loss_sum
+            mark("conv_compute")
+            mark("activations")
+            sends = []
+            for j in range(m):
+                base = j * g * kb
+                recv = []
+                for pos in range(g):
+                    rv = self.fc_in.rows_view(base + pos * kb, base + (pos + 1) * kb)
+                    recv.append([rv.plane_rows(p) for p in range(3)] +
+                                [self.labels[base + pos * kb:base + (pos + 1) * kb]])
+                for w in comm.post_activations(None, recv):
+                    w.wait()
+                if j == 0:
+                    mark("fc_compute")
+                rows = (base, base + g * kb)
+                eng.forward(self.fc_in, self.labels, loss_out=loss_to, rows=rows)
+                gx = eng.backward(rows=rows, phase="dgrad")
+                sends += comm.post_boundary(
+                    [[gx.rows_view(pos * kb, (pos + 1) * kb).plane_rows(p) for p in range(3)]
+                     for pos in range(g)], None)
+            mark("boundary")
+            eng.backward(phase="wgrad")     # overlaps the CONV workers' backward
+            for w in sends:
+                w.wait()
+
+        mark("exchange")
+        ring = lambda p, mm: 0 if mm == 1 else int(2 * (mm - 1) * p * 4)  # noqa: E731
+        ar_bytes = ring(self.partition.conv_params, self.n_conv) + \
+            (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
+        led.record("exchange", ar_bytes)
+        led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
+        comm.allreduce_grads(self.conv.grad_flat if comm.is_conv else self.fcs[0].grad_flat)
         mark("update")
         led.record("update")
         if self.conv is not None:

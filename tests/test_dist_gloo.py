@@ -84,3 +84,89 @@ def test_role_exchange(n_conv, n_fc):
         assert torch.allclose(torch.tensor(res[i]["gy"]), -(base + (i + 1)))
         assert res[i]["g"] == [float(sum(range(1, n_conv + 1)))] * 7
 
+
+
+def _pipelined_worker(rank, world, n_conv, n_fc, m, port, q):
+    """The posting order of StanzaCluster._step_pipelined: a CONV worker
+    posts every micro-batch's activations, then every boundary receive; its
+    FC worker alternates receive -> compute -> send per micro-batch."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1812_10624_b200.comm import RoleComm
+        comm = RoleComm(n_conv, n_fc)
+        comm.warm("cpu")
+        k, a = 4 * m, 3
+        kb = k // m
+        out = {}
+        if comm.is_conv:
+            i = comm.index
+            acts = 100.0 * (i + 1) + torch.arange(k * a, dtype=torch.float32).reshape(k, a)
+            labels = torch.arange(k, dtype=torch.int32) + 1000 * i
+            gy = torch.zeros(k, a)
+            sends, recvs = [], []
+            for j in range(m):
+                sends += comm.post_activations([acts[j * kb:(j + 1) * kb],
+                                                labels[j * kb:(j + 1) * kb]], None)
+            for j in range(m):
+                recvs += comm.post_boundary(None, [gy[j * kb:(j + 1) * kb]])
+            for w in recvs + sends:
+                w.wait()
+            out["gy"] = gy
+        else:
+            members = comm.members(comm.index)
+            g = len(members)
+            fc_in = torch.zeros(g * k, a)
+            fc_lab = torch.zeros(g * k, dtype=torch.int32)
+            sends = []
+            for j in range(m):
+                base = j * g * kb
+                for w in comm.post_activations(None, [
+                        [fc_in[base + p * kb:base + (p + 1) * kb],
+                         fc_lab[base + p * kb:base + (p + 1) * kb]] for p in range(g)]):
+                    w.wait()
+                gx = -fc_in[base:base + g * kb]          # the FC block's "input gradient"
+                sends += comm.post_boundary([[gx[p * kb:(p + 1) * kb].clone()]
+                                             for p in range(g)], None)
+            for w in sends:
+                w.wait()
+            out["fc_in"], out["fc_lab"], out["members"] = fc_in, fc_lab, members
+        q.put((rank, {key: (v.tolist() if torch.is_tensor(v) else v) for key, v in out.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_conv,n_fc,m", [(1, 1, 2), (2, 1, 4), (2, 2, 3)])
+def test_pipelined_exchange(n_conv, n_fc, m):
+    world = n_conv + n_fc
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipelined_worker, args=(r, world, n_conv, n_fc, m, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    k, a = 4 * m, 3
+    kb = k // m
+    from paper_1812_10624_b200.roles import plan_groups
+    conv_to_fc = plan_groups(n_conv, n_fc)
+
+    def acts_of(i):
+        return 100.0 * (i + 1) + torch.arange(k * a, dtype=torch.float32).reshape(k, a)
+
+    for r in range(n_conv, world):
+        members = [i for i, f in enumerate(conv_to_fc) if f == r - n_conv]
+        g = len(members)
+        fc_in = torch.tensor(res[r]["fc_in"])
+        lab = res[r]["fc_lab"]
+        for j in range(m):                      # layout [micro-batch][member][kb]
+            for pos, i in enumerate(members):
+                lo = j * g * kb + pos * kb
+                assert torch.equal(fc_in[lo:lo + kb], acts_of(i)[j * kb:(j + 1) * kb])
+                assert lab[lo:lo + kb] == list(range(j * kb + 1000 * i, (j + 1) * kb + 1000 * i))
+    for i in range(n_conv):
+        assert torch.equal(torch.tensor(res[i]["gy"]), -acts_of(i))

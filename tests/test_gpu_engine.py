@@ -147,3 +147,52 @@ def test_fc_head_alexnet_shapes(clusters):
     from paper_1812_10624_b200.tensor_core import FullyConnected, ReLU
     _run([FullyConnected(9216, 4096), ReLU(), FullyConnected(4096, 4096), ReLU(),
           FullyConnected(4096, 1000)], (9216,), 896, True, 6)
+
+
+@pytest.mark.parametrize("schedule", ["accumulate", "dgrad_then_wgrad"])
+def test_micro_batches_match_full_batch(schedule):
+    """Micro-batched passes (the pipelined step's building blocks) give the
+    full-batch results: forward rows, per-micro-batch backward with gradient
+    accumulation, or the FC worker's dgrad-per-micro-batch then one
+    full-batch wgrad.  Sums differ only in fp32 order."""
+    from paper_1812_10624_b200.engine import BlockEngine, Split, rup8
+    from paper_1812_10624_b200.tensor_core import (Conv2d, Flatten, FullyConnected, MaxPool2d,
+                                                    ReLU, seeded_init)
+    from paper_1812_10624_b200 import _lib
+    from paper_1812_10624_b200.tensor_core import ptr, stream_of
+    layers = [Conv2d(16, 32, 3, 1, 1), ReLU(), MaxPool2d(2, 2), Flatten(),
+              FullyConnected(32 * 4 * 4, 40), ReLU(), FullyConnected(40, 24)]
+    batch, m = 8, 4
+    kb = batch // m
+    params = seeded_init(layers, 9)
+    rng = np.random.Generator(np.random.PCG64(9))
+    x = torch.from_numpy(rng.standard_normal((batch, 16, 8, 8)).astype(np.float32)).cuda()
+    gy_h = rng.standard_normal((batch, 24)).astype(np.float32)
+
+    def run(micro):
+        eng = BlockEngine(layers, (16, 8, 8), batch, "cuda:0", params, need_input_grad=True)
+        g = Split.alloc("rows", (batch, rup8(24)), 24, "cuda:0")
+        _lib.call("stzx_pack_rows", ptr(torch.from_numpy(gy_h).cuda()), g.ptr(), g.ps, batch, 24,
+                  g.width, stream_of(torch.device("cuda:0")))
+        if not micro:
+            out = eng.forward(x).to_float()
+            gin = eng.backward(g).to_float()
+        else:
+            outs, gins = [], []
+            for j in range(m):
+                outs.append(eng.forward(x, rows=(j * kb, (j + 1) * kb)).to_float())
+            for j in range(m):
+                rows = (j * kb, (j + 1) * kb)
+                if schedule == "accumulate":
+                    gins.append(eng.backward(g, rows=rows, accumulate=j > 0).to_float())
+                else:
+                    gins.append(eng.backward(g, rows=rows, phase="dgrad").to_float())
+            if schedule == "dgrad_then_wgrad":
+                eng.backward(phase="wgrad")
+            out, gin = torch.cat(outs), torch.cat(gins)
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), gin.cpu().numpy(), eng.grad_flat.cpu().numpy()
+
+    full, micro = run(False), run(True)
+    for a, b in zip(full, micro):
+        assert orc.rel_err(b, a) <= 1e-6

@@ -1,7 +1,7 @@
 """One process per GPU: StanzaCluster over NCCL vs the oracle.
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-        tools/dist_parity.py <n_conv> <n_fc> [model] [iters]
+        tools/dist_parity.py <n_conv> <n_fc> [model] [iters] [micro_batches]
 Rank 0 prints PASS/FAIL with max_param_dev against the reference algorithm
 and checks that every CONV replica is bit-identical."""
 import os, sys
@@ -17,6 +17,7 @@ from paper_1812_10624_b200.tensor_core import as_tuple
 n_conv, n_fc = int(sys.argv[1]), int(sys.argv[2])
 model = sys.argv[3] if len(sys.argv) > 3 else "tiny_cnn"
 iters = int(sys.argv[4]) if len(sys.argv) > 4 else 8
+micro = int(sys.argv[5]) if len(sys.argv) > 5 else None
 local = int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
 dev = torch.device("cuda", local)
@@ -26,7 +27,7 @@ spec = mp.builtin_model(model)
 comm = RoleComm(n_conv, n_fc)
 mk = orc.batch_fn(spec.input_shape, spec.batch_k, 11)
 cl = StanzaCluster(spec, n_conv=n_conv, n_fc=n_fc, batch_fn=mk, lr=0.05, momentum=0.9,
-                   seed=5, device=dev, comm=comm)
+                   seed=5, device=dev, comm=comm, micro_batches=micro)
 res = cl.train(iters)
 # replica identity across CONV ranks (reference test_stanza_runtime.py:70-83)
 ok_rep = torch.ones(1, device=dev)
@@ -43,7 +44,7 @@ if dist.get_rank() == 0:
     dev_p = orc.max_param_dev(res.state.params, rp)
     dl = max(abs(a - b) / abs(b) for a, b in zip(res.losses, rl))
     ok = dev_p <= 1e-5 and dl <= 1e-5 and ok_rep.item() == 1.0
-    print(f"{'PASS' if ok else 'FAIL'} dist {n_conv}:{n_fc} {model} iters={iters} "
+    print(f"{'PASS' if ok else 'FAIL'} dist {n_conv}:{n_fc} {model} iters={iters} micro={cl.micro} "
           f"max_param_dev={dev_p:.2e} loss_rel={dl:.2e} replicas_identical={bool(ok_rep.item())}",
           flush=True)
 dist.barrier()

@@ -64,6 +64,19 @@ if os.environ.get("STZ_DIAG"):
             print(f"  cluster={cl_on} debug={flags}: {e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
     lib.stz_set_debug(0)
     lib.stz_set_cluster(1)
+if os.environ.get("STZ_SWEEP"):   # time every tile configuration (model-chosen splits)
+    lib = _lib.load()
+    for bn, cl in ((64, 1), (64, 2), (96, 1), (128, 1), (192, 1), (128, 2), (192, 2), (256, 2)):
+        if lib.stz_set_tile(bn, cl, 0) != 0:
+            continue
+        _lib.call(name, *args)
+        e0.record()
+        for _ in range(20):
+            _lib.call(name, *args)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"  tile bn={bn} cl={cl}: {e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
+    lib.stz_set_tile(0, 0, 0)
 if os.environ.get("STZ_DEBUG"):   # capture a diagnostic variant (stz_set_debug flags)
     _lib.load().stz_set_debug(int(os.environ["STZ_DEBUG"]))
 torch.cuda.nvtx.range_push("replay")
