@@ -654,13 +654,25 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16_t* __res
     double acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    if (tl < lanes && cc < chunks)
-      for (int r = r0 + tl; r < r1; r += lanes) {
+    if (tl < lanes && cc < chunks) {
+      // four rows' loads in flight per step; each thread's adds stay in row order
+      int r = r0 + tl;
+      for (; r + 3 * lanes < r1; r += 4 * lanes) {
+        float v[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load_split8(g + (size_t)(r + u * lanes) * ld + cc * 8, ps, v[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += (double)v[u][j];
+      }
+      for (; r < r1; r += lanes) {
         float v[8];
         load_split8(g + (size_t)r * ld + cc * 8, ps, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] += (double)v[j];
       }
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) red[threadIdx.x * 8 + j] = acc[j];
     __syncthreads();

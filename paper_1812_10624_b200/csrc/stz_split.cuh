@@ -603,13 +603,25 @@ __global__ void sgemm_reduce_kernel(const float* __restrict__ partial, int split
     float v[8];
     float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    for (int z = 1; z < splits; ++z) {
-      a = reinterpret_cast<const float4*>(src + z * zs)[0];
-      b = reinterpret_cast<const float4*>(src + z * zs)[1];
-      v[0] = __fadd_rn(v[0], a.x); v[1] = __fadd_rn(v[1], a.y);
-      v[2] = __fadd_rn(v[2], a.z); v[3] = __fadd_rn(v[3], a.w);
-      v[4] = __fadd_rn(v[4], b.x); v[5] = __fadd_rn(v[5], b.y);
-      v[6] = __fadd_rn(v[6], b.z); v[7] = __fadd_rn(v[7], b.w);
+    // four splits' loads in flight at a time; the adds keep the fixed split order
+    for (int z0 = 1; z0 < splits; z0 += 4) {
+      float4 pa[4], pb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (z0 + u < splits) {
+          pa[u] = __ldg(reinterpret_cast<const float4*>(src + (z0 + u) * zs));
+          pb[u] = __ldg(reinterpret_cast<const float4*>(src + (z0 + u) * zs) + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (z0 + u < splits) {
+          v[0] = __fadd_rn(v[0], pa[u].x); v[1] = __fadd_rn(v[1], pa[u].y);
+          v[2] = __fadd_rn(v[2], pa[u].z); v[3] = __fadd_rn(v[3], pa[u].w);
+          v[4] = __fadd_rn(v[4], pb[u].x); v[5] = __fadd_rn(v[5], pb[u].y);
+          v[6] = __fadd_rn(v[6], pb[u].z); v[7] = __fadd_rn(v[7], pb[u].w);
+        }
+      }
     }
     ep.store8(m, nb, v);
   }
