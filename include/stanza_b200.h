@@ -49,6 +49,11 @@ int stz_set_tma(int on);
  * 128-row tile.  The GPU tests run both. */
 int stz_set_cluster(int on);
 
+/* 1 (default): stride-1 unpadded convolutions run on the shifted-window
+ * ("band") implicit GEMM, one shared-memory band per channel block serving
+ * every tap; 0: the im2col TMA GEMM.  The GPU tests run both. */
+int stz_set_band(int on);
+
 /* Force the TMA GEMM tile (tests / tuning): width bn in {64, 96, 128, 192,
  * 256}, cl = 2 for CTA pairs (required for 256; 64 / 96 run unpaired),
  * splits = K splits (0 = 1).  bn = 0 restores the cost-model choice. */

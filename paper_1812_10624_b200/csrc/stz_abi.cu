@@ -18,6 +18,7 @@
 
 #include "stz_fmt.cuh"
 #include "stz_tma.cuh"
+#include "stz_band.cuh"
 
 #include <cuda.h>
 #include <mutex>
@@ -400,8 +401,9 @@ std::string cache_key(T... v) {
 }
 
 bool enc_tiled(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer,
-               uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
-  const std::string key = cache_key(0, (uintptr_t)base, inner, outer, ld_elems, box_inner, box_outer);
+               uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, bool swizzle = true) {
+  const std::string key = cache_key(0, (uintptr_t)base, inner, outer, ld_elems, box_inner,
+                                    box_outer, swizzle ? 1 : 0);
   auto it = g_map_cache.find(key);
   if (it != g_map_cache.end()) {
     *out = it->second;
@@ -413,8 +415,8 @@ bool enc_tiled(CUtensorMap* out, const void* base, uint64_t inner, uint64_t oute
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   g_map_cache.emplace(key, *out);
   return true;
@@ -610,6 +612,79 @@ void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
   cudaLaunchKernelEx(&cfg, tgemm_kernel<BN, NSETS, CL, EP>, prm);
 }
 
+// ---- shifted-window (band) conv: stride-1 "valid" conv over an NHWC input ----------
+int g_use_band = 1;   // stz_set_band
+
+template <int BN, int MT, class EP>
+int launch_band(BandParams<EP>& prm, int items, size_t smem, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(bandconv_kernel<BN, MT, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr_set = true;
+  }
+  const int grid = items < num_sms() ? items : num_sms();
+  bandconv_kernel<BN, MT, EP><<<grid, BD_THREADS, smem, st>>>(prm);
+  return STZ_OK;
+}
+
+// out[m = (n, y, x)][o] = sum_{th, tw, c} x[n][y+th][x+tw][c] * w[o][th*k+tw][c] for
+// y < Hi-k+1, x < Wi-k+1 (x: NHWC split planes [Nimg][Hi][Wi][C8], C8 % 32 == 0;
+// w: [O][k*k*C8] split planes).  Returns -1 when the band does not fit (caller
+// falls back to the im2col GEMM).
+template <class EP>
+int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w, size_t psw,
+                  const EP& ep, int Nimg, int C8, int Hi, int Wi, int O, int k,
+                  cudaStream_t st) {
+  if (!g_use_band || !g_use_tma || !tma_ready() || C8 % 32 != 0 || k < 1) return -1;
+  const int OH = Hi - k + 1, OW = Wi - k + 1;
+  if (OH <= 0 || OW <= 0) return -1;
+  int BN, MT;
+  if (O <= 64) { BN = 64; MT = 2; }
+  else if (O % 192 == 0) { BN = 192; MT = 1; }
+  else { BN = 128; MT = 1; }
+  const int band_rows = MT * TG_BM + (k - 1) * Wi + (k - 1);
+  const int nrb = cdiv(band_rows, 256);
+  const int box_rows = rup8(cdiv(band_rows, nrb));
+  const int rows_alloc = nrb * box_rows;
+  size_t smem = 0;
+  if (BN == 64) smem = band_smem<64, 2>(rows_alloc);
+  else if (BN == 192) smem = band_smem<192, 1>(rows_alloc);
+  else smem = band_smem<128, 1>(rows_alloc);
+  if (smem > 227 * 1024) return -1;
+  BandParams<EP> prm;
+  const long long rows = (long long)Nimg * Hi * Wi;
+  if (rows >= (1ll << 31)) return -1;
+  for (int pl = 0; pl < 3; ++pl)
+    if (!enc_tiled(&prm.band[pl], x + pl * psx, (uint64_t)C8, (uint64_t)rows, (uint64_t)C8, 8,
+                   (uint32_t)box_rows, false))
+      return -1;
+  if (!op_tiled_k(prm.b, w, psw, O, k * k * C8, k * k * C8, BN)) return -1;
+  prm.ep = ep;
+  prm.M_virt = (int)rows;
+  prm.N = O;
+  prm.C8 = C8;
+  prm.Wi = Wi;
+  prm.ksz = k;
+  prm.OH = OH;
+  prm.OW = OW;
+  prm.Nimg = Nimg;
+  prm.box_rows = box_rows;
+  prm.nrb = nrb;
+  prm.rows_alloc = rows_alloc;
+  prm.d_hw = FastDiv((uint32_t)(Hi * Wi));
+  prm.d_w = FastDiv((uint32_t)Wi);
+  prm.debug = g_debug;
+  const int items = cdiv((int)rows, MT * TG_BM) * cdiv(O, BN);
+  if (g_trace)
+    fprintf(stderr, "[stz] %-16s band rows=%d Wi=%d k=%d C8=%d N=%d BN=%d MT=%d items=%d "
+            "band_rows=%d smem=%zu\n", what, (int)rows, Wi, k, C8, O, BN, MT, items, band_rows, smem);
+  if (BN == 64) launch_band<64, 2>(prm, items, smem, st);
+  else if (BN == 192) launch_band<192, 1>(prm, items, smem, st);
+  else launch_band<128, 1>(prm, items, smem, st);
+  return check_launch(what);
+}
+
 // C[M,N] = A . B with TMA operands built for tile width BN
 template <class EP>
 int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand& b, const EP& ep,
@@ -711,6 +786,10 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
                   int C8, int H, int W, int O, int k, int s, int p, int OH, int OW, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const int M = N * OH * OW, K = k * k * C8;
+  if (s == 1 && p == 0 && k * k * C8 <= 4096) {   // K cap (accuracy) holds without splits
+    const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, k, st);
+    if (rc >= 0) return rc;
+  }
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
     const TgShape sh = tg_shape(M, O, K, ws_bytes);
     TgOperand a, b;
@@ -840,6 +919,11 @@ int stz_set_tma(int on) {
 
 int stz_set_cluster(int on) {
   g_use_cluster = on ? 1 : 0;
+  return STZ_OK;
+}
+
+int stz_set_band(int on) {
+  g_use_band = on ? 1 : 0;
   return STZ_OK;
 }
 

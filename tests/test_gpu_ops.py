@@ -230,3 +230,21 @@ def test_fc_every_tile_config(tc, tile, shape):
                          ids=lambda s: "x".join(map(str, s)))
 def test_conv_every_tile_config(tc, tile, shape):
     _conv_case(tc, shape)
+
+
+VALID_CONV_SHAPES = [  # stride 1, no padding: the shifted-window (band) path
+    (2, 64, 15, 15, 64, 3, 1, 0), (2, 32, 20, 17, 192, 5, 1, 0), (1, 64, 57, 57, 64, 3, 1, 0),
+    (3, 96, 9, 11, 128, 3, 1, 0), (2, 32, 8, 8, 40, 1, 1, 0), (1, 64, 31, 31, 64, 5, 1, 0)]
+
+
+@pytest.fixture(params=[1, 0], ids=["band", "im2col"])
+def band(request, lib):
+    """Run with the shifted-window conv and with the im2col GEMM; restore after."""
+    lib.stz_set_band(request.param)
+    yield request.param
+    lib.stz_set_band(1)
+
+
+@pytest.mark.parametrize("shape", VALID_CONV_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_valid_conv_band_vs_oracle(tc, band, shape):
+    _conv_case(tc, shape)
