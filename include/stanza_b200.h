@@ -51,7 +51,9 @@ int stz_set_cluster(int on);
 
 /* 1 (default): stride-1 unpadded convolutions run on the shifted-window
  * ("band") implicit GEMM, one shared-memory band per channel block serving
- * every tap; 0: the im2col TMA GEMM.  The GPU tests run both. */
+ * every tap; 2: padded stride-1 convolutions (and input gradients) too
+ * (measured slower, kept for coverage); 0: the im2col TMA GEMM.  The GPU
+ * tests run all three. */
 int stz_set_band(int on);
 
 /* Force the TMA GEMM tile (tests / tuning): width bn in {64, 96, 128, 192,

@@ -443,6 +443,28 @@ bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8,
   return true;
 }
 
+// NHWC [N][H][W][C8] planes as a 4D tiled map with box {8, bw, bh, 1}, no
+// swizzle: the shifted-window conv's band (out-of-range boxes zero-fill)
+bool enc_band4d(CUtensorMap* out, const void* base, int N, int H, int W, int C8, int bw, int bh) {
+  const std::string key = cache_key(2, (uintptr_t)base, N, H, W, C8, bw, bh);
+  auto it = g_map_cache.find(key);
+  if (it != g_map_cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)C8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C8 * 2, (cuuint64_t)W * C8 * 2, (cuuint64_t)H * W * C8 * 2};
+  cuuint32_t box[4] = {8, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  g_map_cache.emplace(key, *out);
+  return true;
+}
+
 // [rows][K] planes, K contiguous (row stride ld), tile of R rows
 bool op_tiled_k(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int ld, int R) {
   op = TgOperand{};
@@ -613,7 +635,8 @@ void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
 }
 
 // ---- shifted-window (band) conv: stride-1 "valid" conv over an NHWC input ----------
-int g_use_band = 1;   // stz_set_band
+int g_use_band = 1;     // stz_set_band
+int g_band_padded = 0;  // 1: also padded convs (measured slower; tests keep the path covered)
 
 template <int BN, int MT, class EP>
 int launch_band(BandParams<EP>& prm, int items, size_t smem, cudaStream_t st) {
@@ -628,61 +651,113 @@ int launch_band(BandParams<EP>& prm, int items, size_t smem, cudaStream_t st) {
   return STZ_OK;
 }
 
-// out[m = (n, y, x)][o] = sum_{th, tw, c} x[n][y+th][x+tw][c] * w[o][th*k+tw][c] for
-// y < Hi-k+1, x < Wi-k+1 (x: NHWC split planes [Nimg][Hi][Wi][C8], C8 % 32 == 0;
-// w: [O][k*k*C8] split planes).  Returns -1 when the band does not fit (caller
-// falls back to the im2col GEMM).
+struct BandShape {
+  int BN, MT, tiles, Hb;
+  double junk;   // computed rows / output rows
+};
+
+BandShape band_shape(int BN, int MT, int Nimg, int OH, int OW, int Wp, int k) {
+  BandShape b;
+  b.BN = BN;
+  b.MT = MT;
+  const int TM = MT * TG_BM;
+  b.tiles = cdiv(OH * Wp, TM);
+  b.Hb = cdiv(Wp - 1 + TM + (k - 1) * (Wp + 1), Wp);
+  b.junk = (double)b.tiles * TM / ((double)OH * OW);
+  (void)Nimg;
+  return b;
+}
+
+// Stride-1 conv of an NHWC split-plane input x [Nimg][H][W][C8] (C8 % 32 == 0),
+// zero padding `pad`, with weights w [O][k*k*C8] (K-major split planes):
+// out[(n, y, x)][o] for y < OH = H + 2 pad - k + 1, x < OW.  Returns -1 when
+// the band path does not apply or would not pay (the caller uses the im2col
+// GEMM): too much junk (computed rows outside the output), or too large.
 template <class EP>
 int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w, size_t psw,
-                  const EP& ep, int Nimg, int C8, int Hi, int Wi, int O, int k,
-                  cudaStream_t st) {
-  if (!g_use_band || !g_use_tma || !tma_ready() || C8 % 32 != 0 || k < 1) return -1;
-  const int OH = Hi - k + 1, OW = Wi - k + 1;
-  if (OH <= 0 || OW <= 0) return -1;
-  int BN, MT;
-  if (O <= 64) { BN = 64; MT = 2; }
-  else if (O % 192 == 0) { BN = 192; MT = 1; }
-  else { BN = 128; MT = 1; }
-  const int band_rows = MT * TG_BM + (k - 1) * Wi + (k - 1);
-  const int nrb = cdiv(band_rows, 256);
-  const int box_rows = rup8(cdiv(band_rows, nrb));
-  const int rows_alloc = nrb * box_rows;
+                  const EP& ep, int Nimg, int C8, int H, int W, int O, int k, int pad, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  if (!g_use_band || !g_use_tma || !tma_ready() || C8 % 32 != 0 || k < 1 || pad < 0) return -1;
+  // padded convs measured slower than the im2col GEMM (per-image tiling adds
+  // junk rows and unaligned tap shifts double the A reads): pad 0 only, with
+  // the images stacked into one raster
+  if (pad != 0 && !g_band_padded) return -1;
+  const int OH = H + 2 * pad - k + 1, OW = W + 2 * pad - k + 1, Wp = W + 2 * pad;
+  if (OH <= 0 || OW <= 0 || Wp > 256) return -1;
+  const bool stacked = pad == 0;
+  const int vimg = stacked ? 1 : Nimg;              // images the kernel tiles
+  const int vrows = stacked ? Nimg * H : OH;        // tiled rows per image
+  BandShape sh;
+  if (O <= 64) {
+    // thin outputs: two 128-row tiles share each weight tile unless that adds junk
+    BandShape s2 = band_shape(64, 2, Nimg, vrows, OW, Wp, k);
+    BandShape s1 = band_shape(64, 1, Nimg, vrows, OW, Wp, k);
+    if (stacked) {   // junk relative to the real output rows
+      s2.junk *= (double)vrows / (Nimg * OH);
+      s1.junk *= (double)vrows / (Nimg * OH);
+    }
+    sh = s2.junk <= s1.junk * 1.05 ? s2 : s1;
+    if (sh.junk > 1.35) return -1;
+  } else {
+    sh = band_shape(O % 192 == 0 ? 192 : 128, 1, Nimg, vrows, OW, Wp, k);
+    if (stacked) sh.junk *= (double)vrows / (Nimg * OH);
+    if (sh.junk > 1.12) return -1;   // wide tiles are near MMA-bound: junk costs directly
+  }
+  if (sh.Hb > 256) return -1;
+  const int rows_alloc = band_rows_alloc(sh.Hb, Wp);
   size_t smem = 0;
-  if (BN == 64) smem = band_smem<64, 2>(rows_alloc);
-  else if (BN == 192) smem = band_smem<192, 1>(rows_alloc);
+  if (sh.BN == 64) smem = sh.MT == 2 ? band_smem<64, 2>(rows_alloc) : band_smem<64, 1>(rows_alloc);
+  else if (sh.BN == 192) smem = band_smem<192, 1>(rows_alloc);
   else smem = band_smem<128, 1>(rows_alloc);
   if (smem > 227 * 1024) return -1;
+  // split-K over channel blocks to keep K per work item <= TG_MAX_KB k-blocks
+  const int cblocks = C8 / 32;
+  const int kb_per_cb = k * k;
+  int cb_per_split = TG_MAX_KB / kb_per_cb;
+  if (cb_per_split < 1) cb_per_split = 1;
+  if (cb_per_split > cblocks) cb_per_split = cblocks;
+  const int splits = cdiv(cblocks, cb_per_split);
+  const int M_out = Nimg * OH * OW, npad = rup8(O);
+  if (splits > 1 && (!ws || (size_t)splits * M_out * npad * sizeof(float) > ws_bytes)) return -1;
   BandParams<EP> prm;
-  const long long rows = (long long)Nimg * Hi * Wi;
-  if (rows >= (1ll << 31)) return -1;
   for (int pl = 0; pl < 3; ++pl)
-    if (!enc_tiled(&prm.band[pl], x + pl * psx, (uint64_t)C8, (uint64_t)rows, (uint64_t)C8, 8,
-                   (uint32_t)box_rows, false))
+    if (!enc_band4d(&prm.band[pl], x + pl * psx, vimg, stacked ? Nimg * H : H, W, C8, Wp, sh.Hb))
       return -1;
-  if (!op_tiled_k(prm.b, w, psw, O, k * k * C8, k * k * C8, BN)) return -1;
+  if (!op_tiled_k(prm.b, w, psw, O, k * k * C8, k * k * C8, sh.BN)) return -1;
   prm.ep = ep;
-  prm.M_virt = (int)rows;
+  prm.partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
   prm.N = O;
   prm.C8 = C8;
-  prm.Wi = Wi;
+  prm.Nimg = vimg;
+  prm.Nreal = Nimg;
+  prm.Hs = stacked ? H : (1 << 24);
+  prm.d_hs = FastDiv((uint32_t)prm.Hs);
+  prm.pad = pad;
+  prm.Wp = Wp;
   prm.ksz = k;
   prm.OH = OH;
   prm.OW = OW;
-  prm.Nimg = Nimg;
-  prm.box_rows = box_rows;
-  prm.nrb = nrb;
-  prm.rows_alloc = rows_alloc;
-  prm.d_hw = FastDiv((uint32_t)(Hi * Wi));
-  prm.d_w = FastDiv((uint32_t)Wi);
+  prm.tiles_per_img = sh.tiles;
+  prm.Hb = sh.Hb;
+  prm.cb_per_split = cb_per_split;
+  prm.splits = splits;
+  prm.d_wp = FastDiv((uint32_t)Wp);
   prm.debug = g_debug;
-  const int items = cdiv((int)rows, MT * TG_BM) * cdiv(O, BN);
+  const int items = vimg * sh.tiles * cdiv(O, sh.BN) * splits;
   if (g_trace)
-    fprintf(stderr, "[stz] %-16s band rows=%d Wi=%d k=%d C8=%d N=%d BN=%d MT=%d items=%d "
-            "band_rows=%d smem=%zu\n", what, (int)rows, Wi, k, C8, O, BN, MT, items, band_rows, smem);
-  if (BN == 64) launch_band<64, 2>(prm, items, smem, st);
-  else if (BN == 192) launch_band<192, 1>(prm, items, smem, st);
+    fprintf(stderr, "[stz] %-16s band N=%d OHxOW=%dx%d Wp=%d k=%d pad=%d C8=%d O=%d BN=%d MT=%d "
+            "tiles/img=%d Hb=%d junk=%.2f splits=%d items=%d smem=%zu\n",
+            what, Nimg, OH, OW, Wp, k, pad, C8, O, sh.BN, sh.MT, sh.tiles, sh.Hb, sh.junk, splits,
+            items, smem);
+  if (sh.BN == 64 && sh.MT == 2) launch_band<64, 2>(prm, items, smem, st);
+  else if (sh.BN == 64) launch_band<64, 1>(prm, items, smem, st);
+  else if (sh.BN == 192) launch_band<192, 1>(prm, items, smem, st);
   else launch_band<128, 1>(prm, items, smem, st);
-  return check_launch(what);
+  int rc = check_launch(what);
+  if (rc || splits == 1) return rc;
+  const size_t total = (size_t)M_out * (npad / 8);
+  sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(prm.partial, splits, M_out, O, ep);
+  return check_launch("band_reduce");
 }
 
 // C[M,N] = A . B with TMA operands built for tile width BN
@@ -786,8 +861,9 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
                   int C8, int H, int W, int O, int k, int s, int p, int OH, int OW, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const int M = N * OH * OW, K = k * k * C8;
-  if (s == 1 && p == 0 && k * k * C8 <= 4096) {   // K cap (accuracy) holds without splits
-    const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, k, st);
+  if (s == 1) {
+    const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, k, p, ws,
+                                 ws_bytes, st);
     if (rc >= 0) return rc;
   }
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
@@ -807,6 +883,11 @@ int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, c
                     int N, int C, int H, int W, int O8, int k, int s, int p, int OH, int OW,
                     void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = N * H * W, K = k * k * O8;
+  if (s == 1) {   // the same stride-1 conv over dY padded by k-1-p, flipped weights
+    const int rc = run_band_conv("conv_dgrad[band]", g, psg, wd, psw, ep, N, O8, OH, OW, C, k,
+                                 k - 1 - p, ws, ws_bytes, st);
+    if (rc >= 0) return rc;
+  }
   if (tma_on() && O8 % 32 == 0 && s == 1 && p - (k - 1) >= -128 && p <= 127) {
     const TgShape sh = tg_shape(M, C, K, ws_bytes);
     TgOperand a, b;
@@ -924,6 +1005,7 @@ int stz_set_cluster(int on) {
 
 int stz_set_band(int on) {
   g_use_band = on ? 1 : 0;
+  g_band_padded = on == 2 ? 1 : 0;
   return STZ_OK;
 }
 

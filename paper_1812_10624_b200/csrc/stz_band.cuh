@@ -17,10 +17,23 @@
 // reference at shifts 0..127).  TMA fills it with 16-byte-wide boxes of up to
 // 256 rows per (plane, chunk).
 //
-// The convolution is "valid" over a (pre-padded) input: output (y, x) for
-// y < Hi-k+1, x < Wi-k+1; the other virtual rows (the last k-1 columns and
-// rows of each image) are computed and dropped by the epilogue.  Weights are
-// the im2col GEMM's B operand ([N][k*k][C8] K-major, TILED_K boxes).
+// Padding needs no padded copy: the band is loaded with a 4D TMA tiled box
+// {8 channels, Wp = W + 2*pad columns, Hb rows, 1 image} at (-pad, y0 - pad);
+// out-of-range coordinates are zero-filled, so shared memory holds exactly
+// the padded image rows.  Work items tile each image's valid output rows
+// (virtual rows q = y * Wp + x, y < OH); the junk columns x >= OW are
+// computed and dropped by the epilogue.  Input gradients are the same conv
+// over the output gradient padded by k-1-p, with flipped weights.  Weights
+// are the im2col GEMM's B operand ([N][k*k][C8] K-major, TILED_K boxes).
+// Split-K runs over channel blocks (fp32 partials + the fixed-order reduce).
+//
+// Measured limit: a tap shift that is not a multiple of 8 rows makes every
+// core matrix straddle a 128-byte line, doubling the A read per MMA (~100
+// cycles per 128x64x16 MMA instead of ~66).  The band therefore pays only
+// where the im2col GEMM is badly feed-bound and the junk rows are few: the
+// unpadded space-to-depth conv1 (images stacked into one raster, ~7% junk).
+// Padded convs (per-image tiling, 23%+ junk) measured slower than im2col, so
+// the host enables the band for pad == 0 only.
 #pragma once
 
 #include "stz_tma.cuh"
@@ -29,15 +42,19 @@ namespace stz {
 
 template <class EP>
 struct alignas(64) BandParams {
-  CUtensorMap band[3];   // per plane: 2D [N*Hi*Wi rows][C8], box {8, box_rows}, no swizzle
+  CUtensorMap band[3];   // per plane: 4D [N][H][W][C8], box {8, Wp, Hb, 1}, no swizzle
   TgOperand b;           // weights, TILED_K
   EP ep;
-  int M_virt;            // N * Hi * Wi
+  float* partial;        // split-K partials [splits][M_out][npad] (nullptr: no split)
   int N;                 // GEMM N (output channels)
   int C8;                // input channels (multiple of 32)
-  int Wi, ksz, OH, OW, Nimg;
-  int box_rows, nrb, rows_alloc;   // band: nrb boxes of box_rows rows per (plane, chunk)
-  FastDiv d_hw, d_w;
+  int Nimg, pad, Wp, ksz, OH, OW;
+  int Nreal, Hs;         // stacked mode (pad 0): Nimg = 1 image of Nreal * Hs rows
+  FastDiv d_hs;
+  int tiles_per_img;     // ceil(OH * Wp / (MT * 128))
+  int Hb;                // padded rows per band
+  int cb_per_split, splits;
+  FastDiv d_wp;
   int debug;
 };
 
@@ -56,13 +73,19 @@ struct BandCfg {
   static_assert(B_PLANE % 512 == 0, "B planes must stay 512-byte aligned");
 };
 
-// bytes of one band buffer (3 planes x 4 chunks x rows_alloc x 16 B)
+// band geometry: each (plane, 8-channel chunk) holds Hb * Wp rows of 16 B,
+// padded to a multiple of 8 rows (TMA destinations stay 128-byte aligned);
+// the two bands are followed by the 1024-byte aligned weight stages
+__host__ __device__ inline int band_rows_alloc(int Hb, int Wp) { return (Hb * Wp + 7) / 8 * 8; }
 __host__ __device__ inline int band_bytes(int rows_alloc) { return 3 * 4 * rows_alloc * 16; }
+__host__ __device__ inline int band_region(int rows_alloc) {
+  return (2 * band_bytes(rows_alloc) + 1023) / 1024 * 1024;
+}
 
 template <int BN, int MT>
 __host__ inline int band_smem(int rows_alloc) {
   using Cfg = BandCfg<BN, MT>;
-  return 1024 + 2 * band_bytes(rows_alloc) + Cfg::STAGES * Cfg::B_STAGE + 512;
+  return 1024 + band_region(rows_alloc) + Cfg::STAGES * Cfg::B_STAGE + 512;
 }
 
 // non-swizzled K-major descriptor (layout type 0)
@@ -85,11 +108,13 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t smem_base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (smem_base - raw);
-  const int BAND = band_bytes(p.rows_alloc);
-  const int PLANE = 4 * p.rows_alloc * 16, CHUNK = p.rows_alloc * 16;
+  const int rows_alloc = band_rows_alloc(p.Hb, p.Wp);
+  const int BAND = band_bytes(rows_alloc);
+  const int PLANE = 4 * rows_alloc * 16, CHUNK = rows_alloc * 16;
+  const int REGION = band_region(rows_alloc);
   const uint32_t band0 = smem_base;                          // [2] bands
-  const uint32_t bst0 = band0 + 2 * BAND;                    // [STAGES] B tiles
-  uint64_t* band_full = reinterpret_cast<uint64_t*>(smem + 2 * BAND + STAGES * Cfg::B_STAGE);
+  const uint32_t bst0 = band0 + REGION;                      // [STAGES] B tiles
+  uint64_t* band_full = reinterpret_cast<uint64_t*>(smem + REGION + STAGES * Cfg::B_STAGE);
   uint64_t* band_empty = band_full + 2;
   uint64_t* b_full = band_empty + 2;
   uint64_t* b_empty = b_full + STAGES;
@@ -98,9 +123,19 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt_items = cdiv(p.M_virt, TM), nt = cdiv(p.N, BN);
-  const int items = mt_items * nt;
+  const int nt = cdiv(p.N, BN);
+  const int per_split = p.Nimg * p.tiles_per_img * nt;
+  const int items = per_split * p.splits;
   const int cblocks = p.C8 / 32, taps = p.ksz * p.ksz;
+  // item w -> (split z, image n, tile t, n tile); n fastest so tiles share the band in L2
+  auto decode = [&](int w, int& z, int& n, int& t, int& n0) {
+    z = w / per_split;
+    const int r = w - z * per_split;
+    n0 = (r % nt) * BN;
+    const int it = r / nt;
+    n = it / p.tiles_per_img;
+    t = it - n * p.tiles_per_img;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -127,29 +162,45 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer --------------------------------------------
-    const int nbox = 3 * 4 * p.nrb;
-    const uint32_t band_tx = (uint32_t)(nbox * p.box_rows * 16);
+    const uint32_t band_tx = (uint32_t)(12 * p.Hb * p.Wp * 16);   // bytes the 12 boxes land
     int gb = 0, gs = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
-      const int q0 = (w / nt) * TM, n0 = (w % nt) * BN;
-      for (int cb = 0; cb < cblocks; ++cb, ++gb) {
+      int z, n, t, n0;
+      decode(w, z, n, t, n0);
+      const int y0 = (t * TM) / p.Wp;
+      const int cb0 = z * p.cb_per_split, cb1 = min(cblocks, cb0 + p.cb_per_split);
+      for (int cb = cb0; cb < cb1; ++cb, ++gb) {
         const int bb = gb & 1;
         mbar_wait(&band_empty[bb], ((gb >> 1) & 1) ^ 1);
-        if (lane == 0) mbar_arrive_tx(&band_full[bb], band_tx);
-        __syncwarp();
-        for (int i = lane; i < nbox; i += 32) {
-          const int pl = i / (4 * p.nrb), c = (i / p.nrb) % 4, rb = i % p.nrb;
-          const uint32_t dst = band0 + bb * BAND + pl * PLANE + c * CHUNK + rb * p.box_rows * 16;
-          tma_2d<1>(&p.band[pl], dst, &band_full[bb], cb * 32 + c * 8, q0 + rb * p.box_rows);
+        if (p.debug & 4) {   // diagnostics: no data movement
+          if (lane == 0) mbar_arrive(&band_full[bb]);
+        } else if (lane == 0) {
+          mbar_arrive_tx(&band_full[bb], band_tx);
         }
-        for (int t = 0; t < taps; ++t, ++gs) {
+        __syncwarp();
+        if (lane < 12 && !(p.debug & 4)) {   // one 4D box per (plane, 8-channel chunk): padded rows y0 .. y0+Hb-1
+          const int pl = lane / 4, c = lane % 4;
+          const uint32_t dst = band0 + bb * BAND + pl * PLANE + c * CHUNK;
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+              "l"(reinterpret_cast<uint64_t>(&p.band[pl])), "r"(smem_u32(&band_full[bb])),
+              "r"(cb * 32 + c * 8), "r"(-p.pad), "r"(y0 - p.pad), "r"(n)
+              : "memory");
+        }
+        for (int tp = 0; tp < taps; ++tp, ++gs) {
           const int s = gs % STAGES;
           mbar_wait(&b_empty[s], ((gs / STAGES) & 1) ^ 1);
+          if (p.debug & 4) {
+            if (lane == 0) mbar_arrive(&b_full[s]);
+            __syncwarp();
+            continue;
+          }
           if (lane == 0) mbar_arrive_tx(&b_full[s], Cfg::B_STAGE);
           __syncwarp();
           const uint32_t st = bst0 + s * Cfg::B_STAGE;
           for (int bi = lane; bi < 3 * p.b.nbox; bi += 32)
-            tg_load_box<1>(p.b, bi, st, Cfg::B_PLANE, &b_full[s], n0, t * p.C8 + cb * 32);
+            tg_load_box<1>(p.b, bi, st, Cfg::B_PLANE, &b_full[s], n0, tp * p.C8 + cb * 32);
         }
       }
     }
@@ -162,21 +213,25 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
     const uint64_t db0 = tg_desc(TG_TILED_K, bst0, 0);
     int gb = 0, gs = 0, it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      int z, n, t, n0;
+      decode(w, z, n, t, n0);
+      const uint32_t x0 = (uint32_t)((t * TM) % p.Wp);   // band row of the tile's first output
+      const int cb0 = z * p.cb_per_split, cb1 = min(cblocks, cb0 + p.cb_per_split);
       const int set = NSETS == 2 ? (it & 1) : 0;
       const int use = NSETS == 2 ? (it >> 1) : it;
       mbar_wait(&tempty[set], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t tset = tmem_base + set * Cfg::SET_COLS;
-      for (int cb = 0; cb < cblocks; ++cb, ++gb) {
+      for (int cb = cb0; cb < cb1; ++cb, ++gb) {
         const int bb = gb & 1;
         mbar_wait(&band_full[bb], (gb >> 1) & 1);
         tc_fence_after();
-        for (int t = 0; t < taps; ++t, ++gs) {
+        for (int tp = 0; tp < taps; ++tp, ++gs) {
           const int s = gs % STAGES;
           mbar_wait(&b_full[s], (gs / STAGES) & 1);
           tc_fence_after();
-          const int th = t / p.ksz, tw = t - th * p.ksz;
-          const uint32_t shift = (uint32_t)(th * p.Wi + tw);
+          const int th = tp / p.ksz, tw = tp - th * p.ksz;
+          const uint32_t shift = x0 + (uint32_t)(th * p.Wp + tw);
           const uint32_t sb = (uint32_t)(s * Cfg::B_STAGE) >> 4;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
@@ -190,7 +245,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
                 const uint64_t da = da0 + (arow + (uint32_t)(AP[i] * PLANE) / 16);
                 const uint64_t db = db0 + (sb + BP[i] * (Cfg::B_PLANE >> 4) + j * 2);
                 const bool big = i == 5;
-                const bool first = (cb | t | j) == 0 && (big || i == 0);
+                const bool first = cb == cb0 && (tp | j) == 0 && (big || i == 0);
                 umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
               }
             }
@@ -205,27 +260,29 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
     // ---------------- epilogue: virtual rows -> output rows -----------------------
     const int q = warp & 3;
     const int npad = cdiv(p.N, 8) * 8;
-    const int M_out = p.Nimg * p.OH * p.OW;
+    const int M_out = p.Nreal * p.OH * p.OW;
     int it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-      const int q0 = (w / nt) * TM, n0 = (w % nt) * BN;
+      int z, n, t, n0;
+      decode(w, z, n, t, n0);
       const int set = NSETS == 2 ? (it & 1) : 0;
       const int use = NSETS == 2 ? (it >> 1) : it;
-      mbar_wait(&tfull[set], use & 1);
+      mbar_wait_backoff(&tfull[set], use & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int mt = 0; mt < MT; ++mt) {
-        const int vq = q0 + mt * TG_BM + q * 32 + lane;
-        uint32_t n, rem, y, x;
-        p.d_hw.divmod((uint32_t)vq, n, rem);
-        p.d_w.divmod(rem, y, x);
-        const bool valid = vq < p.M_virt && (int)y < p.OH && (int)x < p.OW;
-        const int m = valid ? ((int)n * p.OH + (int)y) * p.OW + (int)x : M_out;
+        const int vq = t * TM + mt * TG_BM + q * 32 + lane;   // virtual row within image n
+        uint32_t ya, x, ns, y;
+        p.d_wp.divmod((uint32_t)vq, ya, x);
+        p.d_hs.divmod(ya, ns, y);        // stacked images: (image, row); else ns = 0
+        const int nr = n + (int)ns;
+        const bool valid = nr < p.Nreal && (int)y < p.OH && (int)x < p.OW;
+        const int m = valid ? (nr * p.OH + (int)y) * p.OW + (int)x : M_out;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + set * Cfg::SET_COLS +
                                mt * Cfg::ACC_COLS;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
-          if (n0 + c >= npad) break;
+          if (n0 + c >= npad || (p.debug & 8)) break;
           float bb[4][8];
           if (EP::HAS_BIAS) {
 #pragma unroll
@@ -245,9 +302,19 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
               v[jj] = __fadd_rn(__uint_as_float(r[8 * h + jj]), __uint_as_float(rs[8 * h + jj]));
-              if (EP::HAS_BIAS) v[jj] = __fadd_rn(v[jj], bb[h][jj]);
+              if (EP::HAS_BIAS && !p.partial) v[jj] = __fadd_rn(v[jj], bb[h][jj]);
             }
-            if (!(p.debug & 1)) p.ep.store8_nb(m, nb, v);
+            if (p.debug & 1) continue;
+            if (p.partial) {
+              if (valid) {
+                float4* dst =
+                    reinterpret_cast<float4*>(p.partial + ((size_t)z * M_out + m) * npad + nb);
+                dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+              }
+            } else {
+              p.ep.store8_nb(m, nb, v);
+            }
           }
         }
       }

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
       const int m0 = (rem / nt) * PM + rank * TG_BM, n0 = (rem % nt) * BN;
       const int acc = NSETS == 2 ? (it & 1) : 0;
       const int use = NSETS == 2 ? (it >> 1) : it;
-      mbar_wait(&tfull_bar[acc], use & 1);
+      mbar_wait_backoff(&tfull_bar[acc], use & 1);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;

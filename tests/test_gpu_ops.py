@@ -232,14 +232,17 @@ def test_conv_every_tile_config(tc, tile, shape):
     _conv_case(tc, shape)
 
 
-VALID_CONV_SHAPES = [  # stride 1, no padding: the shifted-window (band) path
+VALID_CONV_SHAPES = [  # stride 1: the shifted-window (band) path, forward and input gradient
     (2, 64, 15, 15, 64, 3, 1, 0), (2, 32, 20, 17, 192, 5, 1, 0), (1, 64, 57, 57, 64, 3, 1, 0),
-    (3, 96, 9, 11, 128, 3, 1, 0), (2, 32, 8, 8, 40, 1, 1, 0), (1, 64, 31, 31, 64, 5, 1, 0)]
+    (3, 96, 9, 11, 128, 3, 1, 0), (2, 32, 8, 8, 40, 1, 1, 0), (1, 64, 31, 31, 64, 5, 1, 0),
+    (2, 64, 27, 27, 64, 5, 1, 2), (2, 192, 13, 13, 64, 3, 1, 1), (1, 32, 20, 21, 48, 3, 1, 1),
+    (2, 96, 15, 15, 32, 5, 1, 2), (1, 256, 9, 9, 64, 5, 1, 2)]
 
 
-@pytest.fixture(params=[1, 0], ids=["band", "im2col"])
+@pytest.fixture(params=[1, 2, 0], ids=["band", "band-padded", "im2col"])
 def band(request, lib):
-    """Run with the shifted-window conv and with the im2col GEMM; restore after."""
+    """Run with the shifted-window conv (unpadded only / padded too) and with
+    the im2col GEMM; restore the default after."""
     lib.stz_set_band(request.param)
     yield request.param
     lib.stz_set_band(1)

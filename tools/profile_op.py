@@ -53,7 +53,7 @@ if os.environ.get("STZ_DIAG"):
     lib = _lib.load()
     for cl_on in (1, 0):
         lib.stz_set_cluster(cl_on)
-        for flags in (0, 1, 2, 4, 1 | 2, 1 | 4):
+        for flags in (0, 1, 2, 4, 1 | 2, 1 | 4, 4 | 8):
             lib.stz_set_debug(flags)
             _lib.call(name, *args)
             e0.record()
