@@ -67,8 +67,12 @@ struct TgCfg {
   static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;  // + alignment slack + barriers
-  // NSETS accumulator sets (2 = double-buffered across tiles), each = big + small
-  static constexpr int ACC_COLS = 2 * BN;
+  // NSETS accumulator sets (2 = double-buffered across tiles), each = big + small.
+  // PAIRB (thin unpaired tiles): the B planes b0 | b1 are contiguous, so they
+  // act as one 128-wide operand -- 4 MMAs per 16-k (2 at N=128, 2 at N=64)
+  // instead of 6 at N=64; the products land in big + two small accumulators.
+  static constexpr bool PAIRB = BN == 64 && CL == 1;
+  static constexpr int ACC_COLS = PAIRB ? 3 * BN : 2 * BN;
   static constexpr int TMEM_COLS = NSETS * ACC_COLS <= 256 ? 256 : 512;
   static_assert(NSETS * ACC_COLS <= 512, "BN too wide for the TMEM sets");
   static_assert(STAGES >= 3, "tile too large");
@@ -358,6 +362,25 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
         mbar_wait(&full_bar[stage], (g / STAGES) & 1);
         tc_fence_after();
         const uint32_t so = (uint32_t)(stage * Cfg::STAGE_BYTES) >> 4;
+        if constexpr (Cfg::PAIRB) {
+          // big (cols 0..63) | S1 (64..127) | S2 (128..191):
+          //   a0*b2 -> S2;  a0*[b0|b1] -> big, S1;  a1*[b0|b1] -> S1, S2;  a2*b0 -> S1
+          // (ordered so that every accumulator's first write is an overwrite)
+          const uint32_t idesc2 = sg_idesc(PM, 2 * BN, amn, bmn);
+          const uint32_t tS1 = tbig + BN, tS2 = tbig + 2 * BN;
+#pragma unroll
+          for (int j = 0; j < TG_BK / 16; ++j) {
+            if (p.debug & 2) break;
+            const uint32_t acc_in = (kb | j) == 0 ? 0u : 1u;
+            const uint64_t a0d = da0 + (so + j * ak);
+            const uint64_t a1d = a0d + (Cfg::A_BYTES >> 4), a2d = a0d + 2 * (Cfg::A_BYTES >> 4);
+            const uint64_t b0d = db0 + (so + j * bk), b2d = b0d + 2 * (Cfg::B_BYTES >> 4);
+            umma_f16(tS2, a0d, b2d, idesc, acc_in);
+            umma_f16(tbig, a0d, b0d, idesc2, acc_in);
+            umma_f16(tS1, a1d, b0d, idesc2, 1u);
+            umma_f16(tS1, a2d, b0d, idesc, 1u);
+          }
+        } else {
 #pragma unroll
         for (int j = 0; j < TG_BK / 16; ++j) {
           if (p.debug & 2) break;
@@ -370,6 +393,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
             if (CL == 2) umma_f16_pair(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
             else umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
           }
+        }
         }
         if (CL == 2) umma_commit_pair(&empty_bar[stage]);
         else umma_commit(&empty_bar[stage]);
@@ -400,11 +424,15 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) p.ep.bias8(n0 + c + 8 * q4, bb[q4]);
         }
-        uint32_t r[32], rs[32];
+        uint32_t r[32], rs[32], rs2[Cfg::PAIRB ? 32 : 1];
         tmem_ld16(tbase + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
         tmem_ld16(tbase + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
         tmem_ld16(tbase + BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&rs[0]));
         tmem_ld16(tbase + BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs[16]));
+        if constexpr (Cfg::PAIRB) {
+          tmem_ld16(tbase + 2 * BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&rs2[0]));
+          tmem_ld16(tbase + 2 * BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs2[16]));
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -412,8 +440,11 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
           if (nb >= npad) break;
           float v[8];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            v[jj] = __fadd_rn(__uint_as_float(r[8 * h + jj]), __uint_as_float(rs[8 * h + jj]));
+          for (int jj = 0; jj < 8; ++jj) {
+            float sm = __uint_as_float(rs[8 * h + jj]);
+            if constexpr (Cfg::PAIRB) sm = __fadd_rn(sm, __uint_as_float(rs2[8 * h + jj]));
+            v[jj] = __fadd_rn(__uint_as_float(r[8 * h + jj]), sm);
+          }
           if (p.debug & 1) {
             continue;
           } else if (p.partial) {
