@@ -126,11 +126,9 @@ class StanzaCluster:
         # (one process per GPU only).  Gradient sums are
         # unchanged up to fp32 summation order.
         if micro_batches is None:
-            # measured (AlexNet K=128): 1:1 is fastest unsplit (28.5k vs 27.8k
-            # images/s at 2), 3:1 with 2 (77.8k vs 76.8k at 1, 75.3k at 4):
-            # split once the FC worker serves >= 3 CONV workers
-            group = max(plan_groups(n_conv, n_fc).count(j) for j in range(n_fc))
-            micro_batches = 2 if (comm is not None and group >= 3 and spec.batch_k % 2 == 0
+            # measured (AlexNet K=128, images/s): 1:1 29.3k / 30.1k / 26.6k and
+            # 3:1 77.3k / 85.8k / 78.0k at 1 / 2 / 4 micro-batches
+            micro_batches = 2 if (comm is not None and spec.batch_k % 2 == 0
                                   and spec.batch_k >= 32) else 1
         if micro_batches < 1 or spec.batch_k % micro_batches:
             raise ConfigError(f"micro_batches={micro_batches} must divide batch_k="
@@ -324,7 +322,9 @@ class StanzaCluster:
 
         CONV worker: forward each micro-batch and post its activations at
         once (the FC worker starts while the next micro-batch is computed);
-        when every boundary gradient has arrived, one full-batch backward.
+        as each micro-batch's boundary gradient arrives, its input-gradient
+        chain (overlapping the FC worker's next micro-batch); then every
+        weight gradient once over the whole batch.
         FC worker: per micro-batch, receive the group's rows (its input is
         laid out [micro-batch][member][kb], so each micro-batch is
         contiguous), run the FC forward and only the input-gradient chain,
@@ -368,10 +368,17 @@ class StanzaCluster:
                 gb = self.gboundary.rows_view(j * kb, (j + 1) * kb)
                 recvs += comm.post_boundary(None, [gb.plane_rows(p) for p in range(3)])
             mark("fc_compute")
-            for w in recvs:
-                w.wait()
-            mark("boundary")
-            self.conv.backward(self.gboundary)
+            per = len(recvs) // m
+            for j in range(m):
+                # the input-gradient chain of micro-batch j as soon as its
+                # boundary rows land (overlaps the FC worker's next one) ...
+                for w in recvs[j * per:(j + 1) * per]:
+                    w.wait()
+                if j == 0:
+                    mark("boundary")
+                self.conv.backward(self.gboundary, rows=(j * kb, (j + 1) * kb), phase="dgrad")
+            # ... then every weight / bias gradient once, over the whole batch
+            self.conv.backward(phase="wgrad")
             for w in sends:
                 w.wait()
         else:
