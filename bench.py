@@ -294,6 +294,14 @@ def main():
         one(i, slots[i % slots.numel():i % slots.numel() + 1])
     sync_all()
 
+    # one process per GPU: StanzaCluster captures each compute segment as a
+    # CUDA graph when it first sees it after its first step -- visit every
+    # pooled batch once more, untimed, so no capture lands in the timed region
+    if world > 1:
+        for i in range(args.pool):
+            one(warm + i, slots[0:1])
+        sync_all()
+
     # single device: one CUDA graph per pooled batch (the whole step, captured)
     graphs = None
     if world == 1 and not args.eager:
@@ -363,6 +371,12 @@ def main():
                 ybuf[buf].copy_(yh, non_blocking=True)
             copied[buf].record(copy_stream)
 
+    if world > 1 and is_conv_rank:   # capture the e2e buffers' segments untimed
+        for b in range(2):
+            cl.step(slots[0:1], x=xbuf[b], labels=ybuf[b])
+    elif world > 1:
+        for b in range(2):
+            cl.step(slots[0:1])
     sync_all()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)

@@ -381,7 +381,7 @@ class BlockEngine:
         return self.xin
 
     def forward(self, x, labels: torch.Tensor | None = None,
-                loss_out: torch.Tensor | None = None, rows=None):
+                loss_out: torch.Tensor | None = None, rows=None, sum_loss: bool = True):
         """Run the block.  ``x`` is a fp32 batch in the reference layout or an
         already-packed Split (e.g. the CONV block's output rows), always
         full-batch shaped; ``rows = (r0, r1)`` runs only samples [r0, r1) (a
@@ -448,8 +448,8 @@ class BlockEngine:
                 dl = V(self.dlogits)
                 _lib.call("stzx_softmax_ce", ptr(self.logits[r0:r1]), ptr(labels[r0:r1]),
                           ptr(self.losses[r0:r1]), dl.ptr(), dl.ps, b, c, dl.width, st)
-                tgt, acc = (self.loss_sum, 0) if loss_out is None else (loss_out, 1)
-                _lib.call("stz_sum_f32", ptr(self.losses[r0:r1]), b, ptr(tgt), acc, st)
+                if sum_loss:
+                    self.sum_loss(loss_out, rows)
         if self.losses is not None:
             return self.losses[r0:r1]
         return V(self._act(len(self.ops) - 1))
@@ -545,6 +545,14 @@ class BlockEngine:
                 g_full = self.gin[i]
         self._gout = gout
         return V(g_full)
+
+    def sum_loss(self, loss_out: torch.Tensor | None = None, rows=None):
+        """Float64 sum of the per-sample losses of ``rows`` (last forward) into
+        ``loss_sum``, or ADDED into ``loss_out``."""
+        r0, r1, _ = self._rows(rows)
+        tgt, acc = (self.loss_sum, 0) if loss_out is None else (loss_out, 1)
+        _lib.call("stz_sum_f32", ptr(self.losses[r0:r1]), r1 - r0, ptr(tgt), acc,
+                  stream_of(self.device))
 
     def _wgrad(self, i, xin, g, b, acc, ws, st):
         """Weight and bias gradient sums of conv / FC op i from its input rows

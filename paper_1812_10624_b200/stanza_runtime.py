@@ -103,7 +103,8 @@ class StanzaCluster:
                  momentum: float = 0.9, conv_time: float = 0.0, fc_unit_time: float = 0.0,
                  net=None, seed: int = 0, boundary: int | None = None,
                  state: TrainState | None = None, device=None, comm=None,
-                 time_phases: bool = False, micro_batches: int | None = None):
+                 time_phases: bool = False, micro_batches: int | None = None,
+                 segment_graphs: bool = True):
         if lr <= 0.0:
             raise ConfigError(f"learning rate must be positive, got {lr}")
         if not 0.0 <= momentum < 1.0:
@@ -136,6 +137,11 @@ class StanzaCluster:
         if comm is None:
             micro_batches = 1
         self.micro = int(micro_batches)
+        # one process per GPU: each compute segment of the pipelined step is
+        # captured as a CUDA graph the second time it runs (NCCL stays eager)
+        self.segment_graphs = bool(segment_graphs) and comm is not None
+        self._seg_graphs: dict = {}
+        self._steps_done = 0
         cut = self.partition.split_index
 
         ref = seeded_init(self.layers, seed)
@@ -316,6 +322,26 @@ class StanzaCluster:
         if ev is not None:
             self._pending_events.append(ev)
 
+    def _segment(self, key, fn) -> None:
+        """Run a compute segment of the pipelined step: eagerly during the
+        first step (kernel attributes, workspaces), then captured into a CUDA
+        graph the first time its ``key`` -- every pointer its kernels bake in
+        -- is seen, and replayed from then on."""
+        if not self.segment_graphs or self.time_phases or self._steps_done == 0:
+            fn()
+            return
+        g = self._seg_graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                    fn()
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            self._seg_graphs[key] = g
+        g.replay()
+
     def _step_pipelined(self, loss_slot, x_in, lab_all) -> None:
         """One iteration in the one-process-per-GPU deployment, pipelined over
         ``self.micro`` micro-batches of kb = K / micro samples per CONV worker.
@@ -359,7 +385,9 @@ class StanzaCluster:
             sends = []
             for j in range(m):
                 rows = (j * kb, (j + 1) * kb)
-                acts = self.conv.forward(x_in, rows=rows)
+                self._segment(("conv_fwd", j, x_in.data_ptr()),
+                              lambda rows=rows: self.conv.forward(x_in, rows=rows))
+                acts = self.conv._act(len(self.conv.ops) - 1).rows_view(*rows)
                 sends += comm.post_activations(
                     [acts.plane_rows(p) for p in range(3)] + [lab_all[rows[0]:rows[1]]], None)
             mark("activations")
@@ -376,9 +404,10 @@ class StanzaCluster:
                     w.wait()
                 if j == 0:
                     mark("boundary")
-                self.conv.backward(self.gboundary, rows=(j * kb, (j + 1) * kb), phase="dgrad")
+                self._segment(("conv_dgrad", j), lambda j=j: self.conv.backward(
+                    self.gboundary, rows=(j * kb, (j + 1) * kb), phase="dgrad"))
             # ... then every weight / bias gradient once, over the whole batch
-            self.conv.backward(phase="wgrad")
+            self._segment(("conv_wgrad",), lambda: self.conv.backward(phase="wgrad"))
             for w in sends:
                 w.wait()
         else:
@@ -403,13 +432,18 @@ class StanzaCluster:
                 if j == 0:
                     mark("fc_compute")
                 rows = (base, base + g * kb)
-                eng.forward(self.fc_in, self.labels, loss_out=loss_to, rows=rows)
-                gx = eng.backward(rows=rows, phase="dgrad")
+
+                def fc_mb(rows=rows):
+                    eng.forward(self.fc_in, self.labels, rows=rows, sum_loss=False)
+                    eng.backward(rows=rows, phase="dgrad")
+                self._segment(("fc_mb", j), fc_mb)
+                eng.sum_loss(loss_to, rows)
+                gx = eng.gin[0].rows_view(*rows)
                 sends += comm.post_boundary(
                     [[gx.rows_view(pos * kb, (pos + 1) * kb).plane_rows(p) for p in range(3)]
                      for pos in range(g)], None)
             mark("boundary")
-            eng.backward(phase="wgrad")     # overlaps the CONV workers' backward
+            self._segment(("fc_wgrad",), lambda: eng.backward(phase="wgrad"))  # overlaps CONV bwd
             for w in sends:
                 w.wait()
 
@@ -423,12 +457,13 @@ class StanzaCluster:
         mark("update")
         led.record("update")
         if self.conv is not None:
-            self.conv.sgd(n, self.lr, self.momentum)
+            self._segment(("conv_sgd",), lambda: self.conv.sgd(n, self.lr, self.momentum))
         if self.fcs:
-            self.fcs[0].sgd(n, self.lr, self.momentum)
+            self._segment(("fc_sgd",), lambda: self.fcs[0].sgd(n, self.lr, self.momentum))
         mark("end")
         if ev is not None:
             self._pending_events.append(ev)
+        self._steps_done += 1
 
     def capture(self, x: torch.Tensor | None = None, labels: torch.Tensor | None = None,
                 loss_slot: torch.Tensor | None = None) -> "torch.cuda.CUDAGraph":
