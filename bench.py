@@ -17,6 +17,7 @@ worker are fixed, so scaling is weak.  Rank 0 prints one JSON line.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -131,31 +132,45 @@ def workload_config(args, n_conv, n_fc, k):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (recipe clocks line)."""
+    """nvidia-smi sampling (recipe clocks line).  Started before the warm-up
+    so it is already emitting when the timed region begins; the summary keeps
+    the samples whose timestamps fall inside the timed window (mark_start /
+    mark_end), falling back to every sample taken under load (and saying so)
+    when the window is shorter than the sampling period."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{index}.csv")
 
-    def __enter__(self):
+    def start(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+        if self.proc is not None:
+            import atexit
+            atexit.register(self.stop)   # never leave nvidia-smi running
         return self
 
-    def __exit__(self, *exc):
-        if self.proc is not None:
+    def mark_start(self):
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        self.t1 = datetime.datetime.now()
+
+    def stop(self):
+        if self.proc is not None and self.proc.poll() is None:
             self.proc.terminate()
             self.proc.wait(timeout=5)
             self.fh.close()
@@ -163,22 +178,30 @@ class ClockSampler:
     def summary(self):
         if self.proc is None or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[5:9]))
             except ValueError:
                 continue
-            for name, flag in zip(names, parts[4:8]):
+        window = "timed"
+        sel = [r for r in rows if self.t0 and self.t1 and self.t0 <= r[0] <= self.t1]
+        if not sel:   # timed region shorter than the sampling period: all samples under load
+            sel, window = rows, "load"
+        reasons = set()
+        for r in sel:
+            for name, flag in zip(names, r[3]):
                 if flag.lower() == "active":
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [r[1] for r in sel]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": sel[-1][2] if sel else None, "reasons": sorted(reasons),
+                "samples": len(sm), "window": window}
 
 
 class CallTimer:
@@ -288,6 +311,8 @@ def main():
         if world > 1:
             dist.barrier()
 
+    clocks = ClockSampler(local).start()   # running before the timed region begins
+
     # warm-up (W >= 3 enforced)
     warm = max(args.warmup, 3)
     for i in range(warm):
@@ -325,13 +350,15 @@ def main():
     launches0 = lib.stz_launch_count()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        sync_all()
-        e0.record(stream)
-        for i in range(args.steps):
-            one(i, slots[i:i + 1])
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+    sync_all()
+    clocks.mark_start()
+    e0.record(stream)
+    for i in range(args.steps):
+        one(i, slots[i:i + 1])
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark_end()
+    clocks.stop()
     launches = lib.stz_launch_count() - launches0
     if graphs is not None:   # replays launch the captured kernels without host calls
         launches = per_step_launches * args.steps
