@@ -220,6 +220,67 @@ int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, fl
 int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
                     int M, int C, int C8, void* stream);
 
+/* ===========================================================================
+ * Gradient exchange + update over NVLink peer memory (replaces the
+ * reference's _exchange_phase, stanza_runtime.py:309-338 -> allreduce_sum,
+ * collectives.py:117-157, and _update_phase, stanza_runtime.py:340-350 ->
+ * unpack_vector tensor_core.py:510-524 + sgd_step tensor_core.py:366-388).
+ *
+ * One role group (the CONV workers, or the FC workers when n_fc > 1) of
+ * nranks processes, one per GPU.  Each member owns three device buffers that
+ * every other member maps through CUDA IPC: its flat gradient vector, a
+ * reduced-gradient vector of the same length and a block of
+ * STZ_PEER_FLAG_WORDS uint32 flag words (zeroed once).  Pointer arrays are
+ * HOST arrays of nranks device pointers indexed by group rank (the local
+ * member's own entries are its local pointers).
+ * ===========================================================================
+ */
+#define STZ_IPC_HANDLE_BYTES 64
+#define STZ_PEER_FLAG_WORDS 32
+
+/* CUDA IPC: handle (STZ_IPC_HANDLE_BYTES) of the allocation holding dptr and
+ * dptr's byte offset in it; open maps a peer's allocation (returns its base),
+ * close unmaps it. */
+int stz_ipc_handle(const void* dptr, void* handle, size_t* offset);
+int stz_ipc_open(const void* handle, void** base);
+int stz_ipc_close(void* base);
+
+/* Timeout after which a peer barrier that is still waiting traps (loud
+ * failure instead of a hung GPU); 0 restores the default 60 s. */
+int stz_set_peer_timeout_ms(unsigned long long ms);
+
+/* Stream-ordered barrier of the group: returns (on the stream) once every
+ * member's stream reached its matching barrier call. */
+int stz_peer_barrier(unsigned* const* flags, int nranks, int me, void* stream);
+
+/* Member `me` sums chunk `me` (256-byte aligned, ceil(n/nranks) rounded up)
+ * of every member's gradient in group-rank order and stores the sum into the
+ * same chunk of every member's reduced buffer. */
+int stz_peer_reduce_push(const float* const* grads, float* const* red, int nranks, int me,
+                         size_t n, void* stream);
+
+/* A slice [off, off+len) of the flat parameter vector whose split-plane GEMM
+ * copy is a row-major [len/D][D8] matrix (FC W [in][out8], planes ps
+ * elements apart); off % 4 == 0. */
+typedef struct {
+  size_t off, len;
+  void* planes;
+  size_t ps;
+  int D, D8;
+} stz_plane_range;
+
+/* stz_sgd_momentum fused with the split-plane weight repack of the given
+ * ranges (sorted, disjoint, <= 16 including the gaps between them). */
+int stz_sgd_momentum_pack(float* w, float* v, const float* g, size_t n, float lr, float mu,
+                          float inv_n, const stz_plane_range* ranges, int nranges, void* stream);
+
+/* The whole exchange + update of one member: barrier, reduce-push, barrier,
+ * then SGD + repack of its replica from its reduced buffer (nranks == 1: SGD
+ * + repack from grads[0]).  Every member ends with bit-identical w, v. */
+int stz_allreduce_sgd(const float* const* grads, float* const* red, unsigned* const* flags,
+                      int nranks, int me, float* w, float* v, size_t n, float lr, float mu,
+                      float inv_n, const stz_plane_range* ranges, int nranges, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

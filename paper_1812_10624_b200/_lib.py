@@ -68,7 +68,35 @@ SIGNATURES = {
     "stzx_pack_s2d": (I, [P, P, Z, I, I, I, I, I, I, I, I, I, P]),
     "stzx_pack_conv_w_s2d": (I, [P, P, Z, I, I, I, I, I, P]),
     "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    # exchange + update over NVLink peer memory
+    "stz_ipc_handle": (I, [P, P, P]),
+    "stz_ipc_open": (I, [P, P]),
+    "stz_ipc_close": (I, [P]),
+    "stz_set_peer_timeout_ms": (I, [ctypes.c_ulonglong]),
+    "stz_peer_barrier": (I, [P, I, I, P]),
+    "stz_peer_reduce_push": (I, [P, P, I, I, Z, P]),
+    "stz_sgd_momentum_pack": (I, [P, P, P, Z, F, F, F, P, I, P]),
+    "stz_allreduce_sgd": (I, [P, P, P, I, I, P, P, Z, F, F, F, P, I, P]),
 }
+
+
+class PlaneRange(ctypes.Structure):
+    """stz_plane_range (include/stanza_b200.h)."""
+    _fields_ = [("off", Z), ("len", Z), ("planes", P), ("ps", Z), ("D", I), ("D8", I)]
+
+
+IPC_HANDLE_BYTES = 64
+PEER_FLAG_WORDS = 32
+
+
+def ptr_array(ptrs) -> ctypes.Array:
+    """Host array of device pointers (keep the returned object alive for the call)."""
+    return (P * len(ptrs))(*[int(p) for p in ptrs])
+
+
+def range_array(ranges) -> ctypes.Array:
+    """Host array of stz_plane_range from (off, len, planes_ptr, ps, D, D8) tuples."""
+    return (PlaneRange * max(len(ranges), 1))(*[PlaneRange(*r) for r in ranges])
 
 
 class StanzaCudaError(RuntimeError):
@@ -112,6 +140,21 @@ def load(path: str | None = None):
 # that brackets the call with CUDA events on the launching stream.
 PROFILE_HOOK = None
 
+# STZ_SYNC_CHECK=1 (debugging): synchronize after every call made outside a
+# CUDA-graph capture and raise on the first asynchronous fault, naming the call
+_SYNC_CHECK = os.environ.get("STZ_SYNC_CHECK") == "1"
+
+
+def _sync_check(name: str) -> int:
+    import torch
+    if torch.cuda.is_current_stream_capturing():
+        return 0
+    try:
+        torch.cuda.current_stream().synchronize()
+    except Exception as e:  # noqa: BLE001
+        raise StanzaCudaError(f"{name}: asynchronous fault: {e}") from e
+    return 0
+
 
 def call(name: str, *args, flops: float = 0.0, tag: str | None = None) -> None:
     """Invoke an ABI function and raise on a non-zero status.  ``flops`` /
@@ -122,6 +165,8 @@ def call(name: str, *args, flops: float = 0.0, tag: str | None = None) -> None:
             rc = getattr(lib, name)(*args)
     else:
         rc = getattr(lib, name)(*args)
+    if rc == 0 and _SYNC_CHECK:
+        rc = _sync_check(name)
     if rc != 0:
         msg = lib.stz_last_error().decode(errors="replace")
         if rc == 1:

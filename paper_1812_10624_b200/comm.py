@@ -24,6 +24,8 @@ NCCL stream), so neither queue can block the other.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -144,3 +146,96 @@ class RoleComm:
 
     def barrier(self) -> None:
         dist.barrier()
+
+    def group_of_role(self):
+        """(process group, member ranks) of this rank's role group; group is
+        None when the role group has one member."""
+        if self.is_conv:
+            return self.conv_group, self.conv_ranks
+        return self.fc_group, self.fc_ranks
+
+    def peer_exchange(self, engine) -> "PeerExchange":
+        """Map this role group's gradient / reduced-gradient / flag buffers
+        into every member (CUDA IPC over NVLink) for the fused exchange +
+        update (stz_allreduce_sgd)."""
+        group, ranks = self.group_of_role()
+        return PeerExchange(engine, group, ranks.index(self.rank), len(ranks))
+
+
+class PeerExchange:
+    """Gradient exchange + momentum SGD of one role group over NVLink peer
+    memory, without NCCL on the data path (stanza_runtime.py:309-350;
+    kernels in csrc/stz_peer.cuh).
+
+    Each member owns its engine's flat gradient vector, a reduced-gradient
+    vector of the same length and a flag block.  Their CUDA-IPC handles are
+    exchanged once over the role group (host plumbing); every member then
+    holds device pointers to every other member's buffers, and one call to
+    stz_allreduce_sgd per iteration does barrier -> reduce-push (member r sums
+    chunk r of all gradients in group-rank order and stores it into every
+    member's reduced vector) -> barrier -> SGD + split-plane repack from the
+    local reduced vector.  Every replica ends bit-identical."""
+
+    def __init__(self, engine, group, me: int, nranks: int):
+        from . import _lib
+        self.engine = engine
+        self.me, self.nranks = me, nranks
+        dev = engine.device
+        self.flags = torch.zeros(_lib.PEER_FLAG_WORDS, dtype=torch.int32, device=dev)
+        self.red = torch.zeros(engine.total, dtype=torch.float32, device=dev) if nranks > 1 \
+            else engine.grad_flat
+        self._opened: dict[bytes, int] = {}
+        grads, reds, flags = [0] * nranks, [0] * nranks, [0] * nranks
+        grads[me], reds[me], flags[me] = (engine.grad_flat.data_ptr(), self.red.data_ptr(),
+                                          self.flags.data_ptr())
+        if nranks > 1:
+            torch.cuda.synchronize(dev)       # flags are zero before any peer can write them
+            mine = [self._handle(t) for t in (engine.grad_flat, self.red, self.flags)]
+            objs = [None] * nranks
+            dist.all_gather_object(objs, mine, group=group)
+            for j, theirs in enumerate(objs):
+                if j == me:
+                    continue
+                grads[j], reds[j], flags[j] = (self._open(h, off) for h, off in theirs)
+            dist.barrier(group=group)
+        self._grads = _lib.ptr_array(grads)
+        self._reds = _lib.ptr_array(reds)
+        self._flags = _lib.ptr_array(flags)
+
+    @staticmethod
+    def _handle(t: torch.Tensor):
+        from . import _lib
+        h = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+        off = ctypes.c_size_t(0)
+        _lib.call("stz_ipc_handle", ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off))
+        return bytes(h.raw), int(off.value)
+
+    def _open(self, handle: bytes, off: int) -> int:
+        """Peer allocation base (opened once per allocation) + offset."""
+        from . import _lib
+        base = self._opened.get(handle)
+        if base is None:
+            out = ctypes.c_void_p(0)
+            _lib.call("stz_ipc_open", ctypes.create_string_buffer(handle, len(handle)),
+                      ctypes.byref(out))
+            base = self._opened[handle] = int(out.value)
+        return base + off
+
+    def run(self, n: int, lr: float, mu: float) -> None:
+        """This member's exchange + update of one iteration (collective: every
+        member of the group calls it once per iteration, in the same order)."""
+        from . import _lib
+        from .tensor_core import inv_batch, ptr, stream_of
+        eng = self.engine
+        ranges, nr, fused = eng.fused_pack_ranges()
+        _lib.call("stz_allreduce_sgd", self._grads, self._reds, self._flags, self.nranks,
+                  self.me, ptr(eng.params_flat), ptr(eng.vel_flat), eng.total, float(lr),
+                  float(mu), inv_batch(n), ranges, nr, stream_of(eng.device))
+        eng.pack_weights(skip=fused)
+
+    def close(self) -> None:
+        from . import _lib
+        for base in self._opened.values():
+            _lib.call("stz_ipc_close", ctypes.c_void_p(base))
+        self._opened.clear()
+

@@ -11,6 +11,7 @@
 // optional caller workspace and a cudaStream_t passed as void*.  Nothing here
 // allocates device memory.  0 = ok, else an STZ_E* code; stz_last_error()
 // holds the message.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include "stz_fmt.cuh"
 #include "stz_tma.cuh"
 #include "stz_band.cuh"
+#include "stz_peer.cuh"
 
 #include <cuda.h>
 #include <mutex>
@@ -225,7 +227,10 @@ __global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict
     if (j == lab) p -= 1.0;
     dr[j] = (float)p;
   }
-  if (threadIdx.x == 0) loss[row] = (float)(-log(exp((double)zr[lab] - mx) / se));
+  // a label outside [0, C) (the reference raises IndexError on it) never
+  // indexes memory: the loss is NaN, which the harness reports as NonFinite
+  if (threadIdx.x == 0)
+    loss[row] = (lab >= 0 && lab < C) ? (float)(-log(exp((double)zr[lab] - mx) / se)) : __int_as_float(0x7fc00000);
 }
 
 // deterministic float64 sum of an fp32 vector (one block)
@@ -1499,6 +1504,176 @@ int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, fl
                            ws_bytes, st);
   if (rc || !gb) return rc;
   return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// exchange + update over NVLink peer memory (stz_peer.cuh)
+// ---------------------------------------------------------------------------
+
+namespace {
+using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn g_addr_range = nullptr;
+unsigned long long g_peer_timeout_ns = 60ull * 1000000000ull;
+
+int fill_peers(PeerTable& t, const float* const* grads, float* const* red,
+               unsigned* const* flags, int nranks, int me) {
+  if (nranks < 1 || nranks > kMaxPeers || me < 0 || me >= nranks)
+    return fail(STZ_EINVAL, "peer group: %d members, me=%d (1..%d members)", nranks, me,
+                kMaxPeers);
+  memset(&t, 0, sizeof(t));
+  t.R = nranks;
+  t.me = me;
+  for (int j = 0; j < nranks; ++j) {
+    if (grads) t.g[j] = grads[j];
+    if (red) t.red[j] = red[j];
+    if (flags) t.flags[j] = flags[j];
+    if ((grads && !aligned16(t.g[j])) || (red && !aligned16(t.red[j])))
+      return fail(STZ_EINVAL, "peer group: member %d buffers must be 16-byte aligned", j);
+  }
+  return STZ_OK;
+}
+
+int fill_ranges(PackTable& tab, size_t n, const stz_plane_range* ranges, int nranges) {
+  memset(&tab, 0, sizeof(tab));
+  size_t at = 0;
+  auto add_plain = [&](size_t upto) {
+    if (upto > at) {
+      if (tab.n == kMaxPackRanges) return false;
+      tab.r[tab.n++] = PackRange{at, upto - at, nullptr, 0, 1, 1};
+      at = upto;
+    }
+    return true;
+  };
+  for (int i = 0; i < nranges; ++i) {
+    const stz_plane_range& r = ranges[i];
+    if (r.off < at || r.off + r.len > n || r.off % 4 || !r.planes || r.D < 1 || r.D8 < r.D ||
+        r.len % (size_t)r.D || r.ps % 4 || !aligned16(r.planes))
+      return fail(STZ_EINVAL, "sgd pack range %d: off %zu len %zu D %d D8 %d (sorted, "
+                  "disjoint, 16-byte aligned, whole rows)", i, r.off, r.len, r.D, r.D8);
+    if (!add_plain(r.off) || tab.n == kMaxPackRanges)
+      return fail(STZ_EINVAL, "sgd pack: more than %d ranges", kMaxPackRanges);
+    tab.r[tab.n++] = PackRange{r.off, r.len, mb(r.planes), r.ps, r.D, r.D8};
+    at = r.off + r.len;
+  }
+  if (!add_plain(n)) return fail(STZ_EINVAL, "sgd pack: more than %d ranges", kMaxPackRanges);
+  return STZ_OK;
+}
+
+int launch_reduce_push(const PeerTable& t, size_t n, cudaStream_t st) {
+  // chunk r of member r: 256-byte aligned, the last one ragged
+  const size_t per = ((n + t.R - 1) / t.R + 63) / 64 * 64;
+  const size_t c0 = std::min(n, per * t.me), c1 = std::min(n, c0 + per);
+  const int grid = grid_for((c1 - c0) / 8 + 1);
+  switch (t.R) {
+#define STZ_RP(R) \
+  case R: peer_reduce_push_kernel<R><<<grid, 256, 0, st>>>(t, c0, c1); break;
+    STZ_RP(1) STZ_RP(2) STZ_RP(3) STZ_RP(4) STZ_RP(5) STZ_RP(6) STZ_RP(7) STZ_RP(8)
+#undef STZ_RP
+    default: return fail(STZ_EINVAL, "reduce_push: %d members", t.R);
+  }
+  return check_launch("peer_reduce_push");
+}
+}  // namespace
+
+extern "C" {
+
+int stz_ipc_handle(const void* dptr, void* handle, size_t* offset) {
+  if (!dptr || !handle || !offset) return fail(STZ_EINVAL, "ipc_handle: null argument");
+  if (!g_addr_range) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&g_addr_range),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      g_addr_range = nullptr;
+      return fail(STZ_ECUDA, "ipc_handle: cuMemGetAddressRange unavailable");
+    }
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (g_addr_range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS)
+    return fail(STZ_ECUDA, "ipc_handle: %p is not device memory", dptr);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(STZ_ECUDA, "ipc_handle: %s", cudaGetErrorString(e));
+  static_assert(sizeof(h) == STZ_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *offset = reinterpret_cast<uintptr_t>(dptr) - (uintptr_t)base;
+  return STZ_OK;
+}
+
+int stz_ipc_open(const void* handle, void** base) {
+  if (!handle || !base) return fail(STZ_EINVAL, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(STZ_ECUDA, "ipc_open: %s", cudaGetErrorString(e));
+  return STZ_OK;
+}
+
+int stz_ipc_close(void* base) {
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) return fail(STZ_ECUDA, "ipc_close: %s", cudaGetErrorString(e));
+  return STZ_OK;
+}
+
+int stz_set_peer_timeout_ms(unsigned long long ms) {
+  g_peer_timeout_ns = (ms ? ms : 60000ull) * 1000000ull;
+  return STZ_OK;
+}
+
+int stz_peer_barrier(unsigned* const* flags, int nranks, int me, void* stream) {
+  PeerTable t;
+  if (int rc = fill_peers(t, nullptr, nullptr, flags, nranks, me)) return rc;
+  for (int j = 0; j < nranks; ++j)
+    if (!t.flags[j]) return fail(STZ_EINVAL, "peer_barrier: member %d flags null", j);
+  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, g_peer_timeout_ns);
+  return check_launch("peer_barrier");
+}
+
+int stz_peer_reduce_push(const float* const* grads, float* const* red, int nranks, int me,
+                         size_t n, void* stream) {
+  PeerTable t;
+  if (int rc = fill_peers(t, grads, red, nullptr, nranks, me)) return rc;
+  if (n == 0) return STZ_OK;
+  return launch_reduce_push(t, n, as_stream(stream));
+}
+
+int stz_sgd_momentum_pack(float* w, float* v, const float* g, size_t n, float lr, float mu,
+                          float inv_n, const stz_plane_range* ranges, int nranges, void* stream) {
+  if (n == 0) return STZ_OK;
+  if (!aligned16(w) || !aligned16(v) || !aligned16(g))
+    return fail(STZ_EINVAL, "sgd_momentum_pack: buffers must be 16-byte aligned");
+  PackTable tab;
+  if (int rc = fill_ranges(tab, n, ranges, nranges)) return rc;
+  sgd_pack_kernel<<<grid_for(n / 4 + 1), 256, 0, as_stream(stream)>>>(w, v, g, tab, lr, mu,
+                                                                        inv_n);
+  return check_launch("sgd_momentum_pack");
+}
+
+int stz_allreduce_sgd(const float* const* grads, float* const* red, unsigned* const* flags,
+                      int nranks, int me, float* w, float* v, size_t n, float lr, float mu,
+                      float inv_n, const stz_plane_range* ranges, int nranges, void* stream) {
+  PeerTable t;
+  if (int rc = fill_peers(t, grads, red, flags, nranks, me)) return rc;
+  PackTable tab;
+  if (int rc = fill_ranges(tab, n, ranges, nranges)) return rc;
+  if (!aligned16(w) || !aligned16(v)) return fail(STZ_EINVAL, "allreduce_sgd: w, v alignment");
+  cudaStream_t st = as_stream(stream);
+  if (nranks > 1) {
+    peer_barrier_kernel<<<1, 32, 0, st>>>(t, g_peer_timeout_ns);
+    if (int rc = check_launch("allreduce_sgd barrier")) return rc;
+    if (n) {
+      if (int rc = launch_reduce_push(t, n, st)) return rc;
+    }
+    peer_barrier_kernel<<<1, 32, 0, st>>>(t, g_peer_timeout_ns);
+    if (int rc = check_launch("allreduce_sgd barrier")) return rc;
+  }
+  if (n == 0) return STZ_OK;
+  const float* g = nranks > 1 ? red[me] : grads[me];
+  sgd_pack_kernel<<<grid_for(n / 4 + 1), 256, 0, st>>>(w, v, g, tab, lr, mu, inv_n);
+  return check_launch("allreduce_sgd update");
 }
 
 }  // extern "C"

@@ -630,7 +630,10 @@ __global__ void __launch_bounds__(256) softmax_ce_split_kernel(
     }
     store_split(dz, psd, (size_t)row * C8 + j, g);
   }
-  if (threadIdx.x == 0) loss[row] = (float)(-log(exp((double)zr[lab] - mx) / se));
+  // a label outside [0, C) (the reference raises IndexError on it) never
+  // indexes memory: the loss is NaN, which the harness reports as NonFinite
+  if (threadIdx.x == 0)
+    loss[row] = (lab >= 0 && lab < C) ? (float)(-log(exp((double)zr[lab] - mx) / se)) : __int_as_float(0x7fc00000);
 }
 
 // column sums of split planes [R][ld] (first N columns) in float64, two

@@ -283,10 +283,13 @@ class BlockEngine:
                     self.velocity[li][ti].copy_(torch.as_tensor(np.asarray(velocities[li][ti])))
         self.pack_weights()
 
-    def pack_weights(self):
-        """Refresh the split-plane weight copies from the fp32 masters."""
+    def pack_weights(self, skip=frozenset()):
+        """Refresh the split-plane weight copies from the fp32 masters (except
+        the layers in ``skip``, already repacked by the fused SGD)."""
         st = stream_of(self.device)
         for i, (a, b) in self.wplanes.items():
+            if i in skip:
+                continue
             op = self.ops[i]
             l = op.layer
             w = self.params[i][0]
@@ -577,13 +580,34 @@ class BlockEngine:
                       xin.width, l.out_dim, g.width, ptr(ws), ws.numel(), st,
                       flops=self.op_flops(i, b), tag=f"fc{i}_wgrad")
 
+    def fused_pack_ranges(self):
+        """(ctypes stz_plane_range array, count, layer indices): the FC weights,
+        whose split-plane copy [in][out8] is row-major, are repacked inside
+        the SGD kernel (stz_sgd_momentum_pack / stz_allreduce_sgd); the conv
+        weight copies are permuted and keep their own pack kernels."""
+        if getattr(self, "_pack_ranges", None) is None:
+            rs, idx = [], []
+            for i, (a, _) in sorted(self.wplanes.items()):
+                op = self.ops[i]
+                if op.kind != "fc" or 2 * len(rs) + 3 > 16:   # ranges + gaps <= 16
+                    continue
+                off, _, cnt = self.slots[i][0]
+                l = op.layer
+                rs.append((off, cnt, a.data_ptr(), a[0].numel(), l.out_dim, rup8(l.out_dim)))
+                idx.append(i)
+            self._pack_ranges = (_lib.range_array(rs), len(rs), frozenset(idx))
+        return self._pack_ranges
+
     def sgd(self, n: int, lr: float, mu: float, grad: torch.Tensor | None = None):
-        """Momentum step over the whole flat block (tensor_core.py:366-388),
-        then refresh the split-plane weight copies."""
+        """Momentum step over the whole flat block (tensor_core.py:366-388)
+        fused with the refresh of the FC split-plane weight copies; the conv
+        copies are repacked after it."""
         g = self.grad_flat if grad is None else grad
-        _lib.call("stz_sgd_momentum", ptr(self.params_flat), ptr(self.vel_flat), ptr(g),
-                  self.total, float(lr), float(mu), inv_batch(n), stream_of(self.device))
-        self.pack_weights()
+        ranges, nr, fused = self.fused_pack_ranges()
+        _lib.call("stz_sgd_momentum_pack", ptr(self.params_flat), ptr(self.vel_flat), ptr(g),
+                  self.total, float(lr), float(mu), inv_batch(n), ranges, nr,
+                  stream_of(self.device))
+        self.pack_weights(skip=fused)
 
     def add_grads_from(self, other: "BlockEngine"):
         """grad_flat += other.grad_flat (replica gradient sum on one device)."""

@@ -44,6 +44,11 @@ from .roles import group_rows, plan_groups
 from .tensor_core import ShapeMismatch, seeded_init
 
 
+def dist_backend() -> str | None:
+    import torch.distributed as dist
+    return dist.get_backend() if dist.is_available() and dist.is_initialized() else None
+
+
 class MissingSource(TimeoutError):
     """An expected upstream node never delivered its payload."""
 
@@ -104,7 +109,7 @@ class StanzaCluster:
                  net=None, seed: int = 0, boundary: int | None = None,
                  state: TrainState | None = None, device=None, comm=None,
                  time_phases: bool = False, micro_batches: int | None = None,
-                 segment_graphs: bool = True):
+                 segment_graphs: bool = True, exchange: str | None = None):
         if lr <= 0.0:
             raise ConfigError(f"learning rate must be positive, got {lr}")
         if not 0.0 <= momentum < 1.0:
@@ -140,6 +145,15 @@ class StanzaCluster:
         # one process per GPU: each compute segment of the pipelined step is
         # captured as a CUDA graph the second time it runs (NCCL stays eager)
         self.segment_graphs = bool(segment_graphs) and comm is not None
+        # gradient exchange + update of one process per GPU: "peer" = the fused
+        # NVLink peer-memory kernels (stz_allreduce_sgd), "nccl" = NCCL
+        # all_reduce followed by the SGD kernel (and the only choice on gloo)
+        if exchange is None:
+            exchange = "peer" if comm is not None and dist_backend() == "nccl" else "nccl"
+        if exchange not in ("peer", "nccl"):
+            raise ConfigError(f"exchange must be 'peer' or 'nccl', got {exchange!r}")
+        self.exchange = exchange if comm is not None else "local"
+        self._peer = None
         self._seg_graphs: dict = {}
         self._steps_done = 0
         cut = self.partition.split_index
@@ -214,6 +228,8 @@ class StanzaCluster:
                                   need_input_grad=True)
                 eng.rows = (0, g * k)
                 self.fcs.append(eng)
+            if self.exchange == "peer":   # collective: every rank maps its role group
+                self._peer = comm.peer_exchange(self.conv if comm.is_conv else self.fcs[0])
         self._loss_slots = None
 
     # -- helpers -------------------------------------------------------------------------
@@ -453,13 +469,20 @@ class StanzaCluster:
             (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
         led.record("exchange", ar_bytes)
         led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
-        comm.allreduce_grads(self.conv.grad_flat if comm.is_conv else self.fcs[0].grad_flat)
-        mark("update")
-        led.record("update")
-        if self.conv is not None:
-            self._segment(("conv_sgd",), lambda: self.conv.sgd(n, self.lr, self.momentum))
-        if self.fcs:
-            self._segment(("fc_sgd",), lambda: self.fcs[0].sgd(n, self.lr, self.momentum))
+        if self._peer is not None:
+            # exchange + update fused over NVLink peer memory (one segment)
+            self._segment(("peer_exchange_sgd",),
+                          lambda: self._peer.run(n, self.lr, self.momentum))
+            mark("update")
+            led.record("update")
+        else:
+            comm.allreduce_grads(self.conv.grad_flat if comm.is_conv else self.fcs[0].grad_flat)
+            mark("update")
+            led.record("update")
+            if self.conv is not None:
+                self._segment(("conv_sgd",), lambda: self.conv.sgd(n, self.lr, self.momentum))
+            if self.fcs:
+                self._segment(("fc_sgd",), lambda: self.fcs[0].sgd(n, self.lr, self.momentum))
         mark("end")
         if ev is not None:
             self._pending_events.append(ev)
