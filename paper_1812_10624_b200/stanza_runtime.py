@@ -181,6 +181,9 @@ class StanzaCluster:
         self.fc_ids = [("fc", j) for j in range(n_fc)]
         self.transport = PhaseLedger()
         self.replica_snapshots: dict = {}
+        self._fc_replica = None          # (params_flat, vel_flat) on the holder's GPU
+        self._replica_holder = None
+        self._replica_iteration = None
 
         conv_block, fc_block = self.partition.conv_block, self.partition.fc_block
         in_shape = tuple(spec.input_shape)
@@ -557,20 +560,99 @@ class StanzaCluster:
         return TrainState(self.iteration, cp + fp, cv + fv)
 
     def checkpoint(self) -> TrainState:
-        """Snapshot; FC worker 0's block state is also copied (as an STZC
-        blob) to a seeded-random CONV worker (stanza_runtime.py:182-211)."""
-        st = self.state()
-        if st is None:
-            return st
-        cut = self.partition.split_index
-        fc_state = TrainState(self.iteration, st.params[cut:], st.velocities[cut:])
-        blob = state_to_bytes(fc_state)
+        """Snapshot the run (stanza_runtime.py:182-211).  FC worker 0's block
+        state (w, v) is also replicated to a seeded-random CONV worker so the
+        heavyweight FC parameters exist on two GPUs: a device-to-device copy
+        over NVLink into a buffer on the holder's GPU (one process per GPU)
+        or a device copy (single device).  The holder keeps the replica
+        resident in HBM for restore_fc_replica() and its STZC blob in
+        replica_snapshots, byte-identical to the reference's
+        (checkpointing.py:44-50).  Collective in one-process-per-GPU mode;
+        returns the TrainState on rank 0 (None elsewhere), like state()."""
         holder = random.Random((self.seed << 32) ^ self.iteration).randrange(self.n_conv)
-        self.replica_snapshots[self.conv_ids[holder]] = blob
-        self.transport.record("checkpoint", len(blob))
-        self.transport.tag_payload_bytes[Tag.CHECKPOINT] += len(blob)
+        self._replicate_fc(holder)
+        st = self.state()
+        blob = self._replica_blob()
+        if blob is not None:
+            self.replica_snapshots[self.conv_ids[holder]] = blob
+        nbytes = 2 * 4 * self.partition.fc_params + 16 * len(self.layers)
+        self.transport.record("checkpoint", nbytes)
+        self.transport.tag_payload_bytes[Tag.CHECKPOINT] += nbytes
         self.transport.tag_messages[Tag.CHECKPOINT] += 1
         return st
+
+    def _fc_proto(self) -> BlockEngine:
+        return BlockEngine(self.partition.fc_block, (self.boundary_activations,), 1,
+                           self.device, allocate=False)
+
+    def _replicate_fc(self, holder: int) -> None:
+        self._replica_holder, self._replica_iteration = holder, self.iteration
+        if self.comm is None:
+            eng = self.fcs[0]
+            self._fc_replica = (eng.params_flat.clone(), eng.vel_flat.clone())
+            return
+        import torch.distributed as dist
+        comm = self.comm
+        fc0 = comm.n_conv
+        ops = []
+        if comm.rank == fc0:
+            ops = [dist.P2POp(dist.isend, t, holder, group=comm.act_group)
+                   for t in (self.fcs[0].params_flat, self.fcs[0].vel_flat)]
+        elif comm.rank == holder:
+            total = self._fc_proto().total
+            if self._fc_replica is None or self._fc_replica[0].numel() != total:
+                self._fc_replica = (torch.empty(total, dtype=torch.float32, device=self.device),
+                                    torch.empty(total, dtype=torch.float32, device=self.device))
+            ops = [dist.P2POp(dist.irecv, t, fc0, group=comm.act_group)
+                   for t in self._fc_replica]
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+
+    def _holds_replica(self) -> bool:
+        if self._fc_replica is None:
+            return False
+        return self.comm is None or self.comm.rank == self._replica_holder
+
+    def _replica_blob(self) -> bytes | None:
+        """STZC blob of the resident replica (on its holder), else None."""
+        if not self._holds_replica():
+            return None
+        proto = self._fc_proto()
+        pf, vf = self._fc_replica
+        fp = [[t.cpu().numpy().copy() for t in row] for row in proto._views(pf)]
+        fv = [[t.cpu().numpy().copy() for t in row] for row in proto._views(vf)]
+        return state_to_bytes(TrainState(self._replica_iteration, fp, fv))
+
+    def restore_fc_replica(self) -> int:
+        """Reload every FC replica's (w, v) from the checkpoint replica held on
+        the CONV worker's GPU (the paper's FC-worker recovery):
+        the holder sends it over NVLink to each FC worker, which repacks its
+        split-plane weight copies.  Collective in one-process-per-GPU mode.
+        Returns the iteration the replica was taken at."""
+        if self._replica_holder is None:
+            raise RuntimeError("no FC replica: call checkpoint() first")
+        if self.comm is None:
+            pf, vf = self._fc_replica
+            self.fcs[0].params_flat.copy_(pf)
+            self.fcs[0].vel_flat.copy_(vf)
+            self.fcs[0].pack_weights()
+            return self._replica_iteration
+        import torch.distributed as dist
+        comm = self.comm
+        ops = []
+        if comm.rank == self._replica_holder:
+            for r in comm.fc_ranks:
+                ops += [dist.P2POp(dist.isend, t, r, group=comm.act_group)
+                        for t in self._fc_replica]
+        elif not comm.is_conv:
+            eng = self.fcs[0]
+            ops = [dist.P2POp(dist.irecv, t, self._replica_holder, group=comm.act_group)
+                   for t in (eng.params_flat, eng.vel_flat)]
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+        if not comm.is_conv:
+            self.fcs[0].pack_weights()
+        return self._replica_iteration
 
     # -- phase timing ----------------------------------------------------------------
 

@@ -140,3 +140,29 @@ def test_alexnet_reduced_batch_step(lib):
     out = cl.train(1)
     assert orc.max_param_dev(out.state.params, ref_p) <= TOL
     np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)
+
+
+def test_fc_replica_digest_and_recovery(lib):
+    """checkpoint() leaves FC worker 0's (w, v) resident on a CONV worker's
+    device; its STZC blob decodes to the snapshot's FC block (same
+    param_digest, checkpointing.py:39-50); after the FC state is lost,
+    restore_fc_replica() brings it back and the run continues bit-exactly
+    as if nothing happened."""
+    from paper_1812_10624_b200.checkpointing import param_digest, state_from_bytes
+    spec = _spec("tiny")
+    whole = _cluster(spec, 3, 1, 4, 21).train(6)
+    cl = _cluster(spec, 3, 1, 4, 21)
+    cl.train(3)
+    snap = cl.checkpoint()
+    cut = cl.partition.split_index
+    (holder, blob), = cl.replica_snapshots.items()
+    rep = state_from_bytes(blob)
+    assert rep.iteration == 3
+    assert param_digest(rep.params) == param_digest(snap.params[cut:])
+    assert param_digest(rep.velocities) == param_digest(snap.velocities[cut:])
+    cl.fcs[0].params_flat.zero_()          # the FC worker's state is lost
+    cl.fcs[0].vel_flat.fill_(1.0)
+    cl.fcs[0].pack_weights()
+    assert cl.restore_fc_replica() == 3
+    res = cl.train(3)
+    assert param_digest(res.state.params) == param_digest(whole.state.params)
