@@ -40,9 +40,15 @@ const char* stz_last_error(void);
 unsigned long long stz_launch_count(void);
 
 /* GEMM producer: 1 (default) = TMA (tiled / im2col tensor maps) where the
- * shapes allow it, 0 = the cp.async gather kernel for every GEMM (the GPU
- * tests run both and compare). */
+ * shapes allow it, with each MN-major tile fetched as one 3D box; 2 = TMA
+ * with one 2D box per 32 MN-major rows; 0 = the cp.async gather kernel for
+ * every GEMM (the GPU tests run all and compare). */
 int stz_set_tma(int on);
+
+/* Thin (64-wide, unpaired) GEMM tiles as two 128-row halves per CTA sharing
+ * one B stage and one 256-row A box: 0 (default) when the GEMM has enough row
+ * tiles to fill the GPU, 1 never, 2 always (tests). */
+int stz_set_mh(int mode);
 
 /* 1 (default): GEMMs with >= 2 row tiles run on CTA pairs (cta_group::2
  * UMMA, 256-row tiles, each CTA stages half of the B tile); 0: one CTA per

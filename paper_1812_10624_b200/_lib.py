@@ -31,6 +31,7 @@ SIGNATURES = {
     "stz_set_debug": (I, [I]),
     "stz_set_tile": (I, [I, I, I]),
     "stz_set_band": (I, [I]),
+    "stz_set_mh": (I, [I]),
     "stz_launch_count": (ctypes.c_ulonglong, []),
     "stz_conv2d_fwd": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stz_conv2d_bwd_data": (I, [P, P, P, P, I, I, I, I, I, I, I, I, P, Z, P]),

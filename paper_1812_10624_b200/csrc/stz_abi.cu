@@ -484,15 +484,46 @@ bool op_tiled_k(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int 
   return true;
 }
 
-// [K][rows] planes, rows contiguous (row stride ld), tile of R rows (R % 32 == 0)
+// [K][rows] viewed as 3D {rows % 32, K, rows / 32} (strides ld, 32 elements):
+// box {32, 32, groups} = an MN-major tile of 32*groups rows, SW64 atoms
+bool enc_mn3d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t K, uint64_t ld,
+              uint32_t groups) {
+  const std::string key = cache_key(3, (uintptr_t)base, rows, K, ld, groups);
+  auto it = g_map_cache.find(key);
+  if (it != g_map_cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  cuuint64_t dims[3] = {32, K, rows / 32};
+  cuuint64_t strides[2] = {ld * 2, 64};
+  cuuint32_t box[3] = {32, 32, groups};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  g_map_cache.emplace(key, *out);
+  return true;
+}
+
+int g_mn3d = 1;   // stz_set_tma(2) disables the 3D MN-major boxes (tests compare)
+
+// [K][rows] planes, rows contiguous (row stride ld), tile of R rows (R % 32 == 0).
+// rows % 32 == 0: one 3D box per plane per k-block; else R/32 2D boxes
 bool op_tiled_mn(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int ld, int R) {
   op = TgOperand{};
   op.mode = TG_TILED_MN;
-  op.nbox = R / 32;
-  op.box_bytes = 2048;
-  for (int pl = 0; pl < 3; ++pl)
-    if (!enc_tiled(&op.map[pl], p + pl * ps, (uint64_t)rows, (uint64_t)K, (uint64_t)ld, 32, 32))
-      return false;
+  op.mn3d = g_mn3d && rows % 32 == 0 && R % 32 == 0;
+  op.nbox = op.mn3d ? 1 : R / 32;
+  op.box_bytes = op.mn3d ? R * 64 : 2048;
+  for (int pl = 0; pl < 3; ++pl) {
+    const bool ok = op.mn3d ? enc_mn3d(&op.map[pl], p + pl * ps, (uint64_t)rows, (uint64_t)K,
+                                       (uint64_t)ld, (uint32_t)(R / 32))
+                            : enc_tiled(&op.map[pl], p + pl * ps, (uint64_t)rows, (uint64_t)K,
+                                        (uint64_t)ld, 32, 32);
+    if (!ok) return false;
+  }
   return true;
 }
 
@@ -513,7 +544,7 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
   op.d_c8 = FastDiv(C8);
   op.d_k = FastDiv(ksz);
   for (int pl = 0; pl < 3; ++pl)
-    if (!enc_im2col(&op.map[pl], p + pl * ps, N, H, W, C8, s, lo, hi, mn ? 32 : 128))
+    if (!enc_im2col(&op.map[pl], p + pl * ps, N, H, W, C8, s, lo, hi, mn ? 32 : R))
       return false;
   return true;
 }
@@ -530,7 +561,9 @@ int g_debug = 0;         // GEMM pipeline diagnostics (stz_set_debug)
 struct TgShape {
   int BN, CL, splits;
   double cost;
+  int MH = 1;   // 2: two 128-row halves per CTA (thin unpaired tiles)
 };
+int g_mh_mode = 0;   // stz_set_mh: 0 auto, 1 never, 2 whenever the tile is thin
 
 // Predicted seconds for a TMA GEMM with tile (BN, CL) and `sp` K-splits:
 //   waves * (k-blocks per item + per-item overhead) * t_kb + partial sums
@@ -538,14 +571,16 @@ struct TgShape {
 // ~27 B/cycle/SM of effective L2 -> SM feed), both measured (tools/mma_bench.cu and the
 // stz_set_debug runs); one TMEM set (BN >= 192) serialises the epilogue with
 // the next item's mainloop; partial sums are mostly L2-resident.
-double tg_cost(int M, int N, int K, int BN, int CL, int sp) {
+// MH = 2 halves the A boxes per row (one 256-row box) and fetches B once for
+// both halves; TMA cost is per box (tools/tma_bench.cu), credited as 0.8x feed.
+double tg_cost(int M, int N, int K, int BN, int CL, int sp, int MH = 1) {
   const double clk = 1.9e9;
   const int sms = num_sms() / CL;
-  const int tiles = cdiv(M, TG_BM * CL) * cdiv(N, BN);
+  const int tiles = cdiv(M, TG_BM * CL * MH) * cdiv(N, BN);
   const int nkb = cdiv(K, TG_BK);
-  const double mma_cyc = 12.0 * (BN / 2 > 48 ? BN / 2 : 48);
-  const double stage_bytes = 3.0 * (TG_BM * TG_BK * 2 + (double)(BN / CL) * TG_BK * 2);
-  const double feed_cyc = stage_bytes / 27.0;
+  const double mma_cyc = 12.0 * MH * (BN / 2 > 48 ? BN / 2 : 48);
+  const double stage_bytes = 3.0 * (TG_BM * MH * TG_BK * 2 + (double)(BN / CL) * TG_BK * 2);
+  const double feed_cyc = stage_bytes / 27.0 * (MH == 2 ? 0.8 : 1.0);
   const double t_kb = (mma_cyc > feed_cyc ? mma_cyc : feed_cyc) / clk;
   const double t_epi = BN >= 192 ? 1.0 * t_kb : 0.0;
   const double t_item0 = 4.0 * t_kb + t_epi + 2e-6;
@@ -561,6 +596,19 @@ double tg_cost(int M, int N, int K, int BN, int CL, int sp) {
 int g_force_bn = 0, g_force_cl = 0, g_force_splits = 0;   // stz_set_tile (tests)
 constexpr int TG_MAX_KB = 128;   // k-blocks (of 32) one work item may accumulate
 
+// thin unpaired tile -> two 128-row halves per CTA when there are enough
+// row tiles to fill the GPU (auto) or always (stz_set_mh(2)); splits re-chosen
+template <class BS>
+TgShape with_halves(TgShape sh, int M, BS& best_split) {
+  if (sh.BN != 64 || sh.CL != 1 || g_mh_mode == 1) return sh;
+  if (g_mh_mode == 0 && cdiv(M, 2 * TG_BM) < num_sms() / 2) return sh;
+  double bc = 0.0;
+  const int sp = best_split(64, 1, bc, 2);
+  TgShape h{64, 1, sp, bc};
+  h.MH = 2;
+  return h;
+}
+
 TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
   const int nkb = cdiv(K, TG_BK);
   // accuracy: tcgen05 truncates the bits it shifts out when adding into an
@@ -571,12 +619,12 @@ TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
   const size_t per = (size_t)M * rup8(N) * sizeof(float);
   const int fit = ws_bytes ? (int)(ws_bytes / per) : 1;
   // best split count for one tile shape
-  auto best_split = [&](int BN, int CL, double& bc) {
+  auto best_split = [&](int BN, int CL, double& bc, int MH = 1) {
     const int smax = nkb / 2 < fit ? nkb / 2 : fit;
     int bsp = sp_min;
-    bc = tg_cost(M, N, K, BN, CL, sp_min);
+    bc = tg_cost(M, N, K, BN, CL, sp_min, MH);
     for (int sp = sp_min + 1; sp <= smax && sp <= 256; ++sp) {
-      const double cst = tg_cost(M, N, K, BN, CL, sp);
+      const double cst = tg_cost(M, N, K, BN, CL, sp, MH);
       if (cst < bc * 0.98) {   // more splits only for a real (> 2%) gain
         bc = cst;
         bsp = sp;
@@ -593,7 +641,9 @@ TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
     double bc = 0.0;
     const int sp = g_force_splits > 0 ? (g_force_splits > sp_min ? g_force_splits : sp_min)
                                       : best_split(g_force_bn, cl, bc);
-    return TgShape{g_force_bn, cl, sp, bc};
+    TgShape sh{g_force_bn, cl, sp, bc};
+    if (g_mh_mode == 2 && sh.BN == 64 && sh.CL == 1) sh.MH = 2;
+    return sh;
   }
   TgShape best{64, 1, sp_min, 1e30};
   const int cand[][2] = {{64, 1}, {96, 1}, {128, 1}, {192, 1}, {128, 2}, {192, 2}, {256, 2}};
@@ -605,23 +655,23 @@ TgShape tg_shape(int M, int N, int K, size_t ws_bytes) {
     const int bsp = best_split(BN, CL, bc);
     if (bc < best.cost * 0.97) best = TgShape{BN, CL, bsp, bc};
   }
-  return best;
+  return with_halves(best, M, best_split);
 }
 
-template <int BN, int NSETS, int CL, class EP>
+template <int BN, int NSETS, int CL, class EP, int MH = 1>
 void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
-  using Cfg = TgCfg<BN, NSETS, CL>;
+  using Cfg = TgCfg<BN, NSETS, CL, MH>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tgemm_kernel<BN, NSETS, CL, EP>,
+    cudaFuncSetAttribute(tgemm_kernel<BN, NSETS, CL, EP, MH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr_set = true;
   }
-  const int items = cdiv(prm.M, TG_BM * CL) * cdiv(prm.N, BN) * splits;
+  const int items = cdiv(prm.M, TG_BM * CL * MH) * cdiv(prm.N, BN) * splits;
   const int max_ctas = num_sms() / CL * CL;
   const int grid = items * CL < max_ctas ? items * CL : max_ctas;
   if (CL == 1) {
-    tgemm_kernel<BN, NSETS, CL, EP><<<grid, TG_THREADS, Cfg::SMEM, st>>>(prm);
+    tgemm_kernel<BN, NSETS, CL, EP, MH><<<grid, TG_THREADS, Cfg::SMEM, st>>>(prm);
     return;
   }
   cudaLaunchConfig_t cfg{};
@@ -771,7 +821,7 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
               int M, int N, int K, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (M <= 0 || N <= 0) return STZ_OK;
   const int BN = sh.BN, CL = sh.CL;
-  const int tiles = cdiv(M, TG_BM * CL) * cdiv(N, BN);
+  const int tiles = cdiv(M, TG_BM * CL * sh.MH) * cdiv(N, BN);
   const int nkb = cdiv(K, TG_BK);
   const int npad = rup8(N);
   const size_t per = (size_t)M * npad * sizeof(float);
@@ -796,11 +846,14 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   if (g_trace) {
     const int items = tiles * splits;
     fprintf(stderr,
-            "[stz] %-16s M=%6d N=%5d K=%6d BN=%3d CL=%d tiles=%5d splits=%3d items=%5d "
+            "[stz] %-16s M=%6d N=%5d K=%6d BN=%3d CL=%d MH=%d tiles=%5d splits=%3d items=%5d "
             "slots=%3d waves=%.2f est=%.1fus\n",
-            what, M, N, K, BN, CL, tiles, splits, items, sms, (double)items / sms, sh.cost * 1e6);
+            what, M, N, K, BN, CL, sh.MH, tiles, splits, items, sms, (double)items / sms,
+            sh.cost * 1e6);
   }
-  if (CL == 2 && BN == 64) launch_tg<64, 2, 2>(prm, splits, st);
+  if (sh.MH == 2 && CL == 1 && BN == 64) launch_tg<64, 1, 1, EP, 2>(prm, splits, st);
+  else if (sh.MH != 1) return fail(STZ_EINVAL, "%s: no two-half kernel for tile %d x %d", what, BN, CL);
+  else if (CL == 2 && BN == 64) launch_tg<64, 2, 2>(prm, splits, st);
   else if (CL == 2 && BN == 128) launch_tg<128, 2, 2>(prm, splits, st);
   else if (CL == 2 && BN == 192) launch_tg<192, 1, 2>(prm, splits, st);
   else if (CL == 2 && BN == 256) launch_tg<256, 1, 2>(prm, splits, st);
@@ -874,7 +927,7 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
     const TgShape sh = tg_shape(M, O, K, ws_bytes);
     TgOperand a, b;
-    if (op_im2col(a, false, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
+    if (op_im2col(a, false, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM * sh.MH) &&
         op_tiled_k(b, wf, psw, O, K, K, sh.BN / sh.CL))
       return run_tgemm("conv_fwd[tma]", sh, a, b, ep, M, O, K, ws, ws_bytes, st);
   }
@@ -896,7 +949,7 @@ int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, c
   if (tma_on() && O8 % 32 == 0 && s == 1 && p - (k - 1) >= -128 && p <= 127) {
     const TgShape sh = tg_shape(M, C, K, ws_bytes);
     TgOperand a, b;
-    if (op_im2col(a, false, g, psg, N, OH, OW, O8, k, 1, p - (k - 1), -p, H, W, TG_BM) &&
+    if (op_im2col(a, false, g, psg, N, OH, OW, O8, k, 1, p - (k - 1), -p, H, W, TG_BM * sh.MH) &&
         op_tiled_k(b, wd, psw, C, K, K, sh.BN / sh.CL))
       return run_tgemm("conv_dgrad[tma]", sh, a, b, ep, M, C, K, ws, ws_bytes, st);
   }
@@ -913,7 +966,7 @@ int gemm_conv_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, co
   if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128) {
     const TgShape sh = tg_shape(M, O, P, ws_bytes);
     TgOperand a, b;
-    if (op_im2col(a, true, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM) &&
+    if (op_im2col(a, true, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM * sh.MH) &&
         op_tiled_mn(b, g, psg, O, P, O8, sh.BN / sh.CL))
       return run_tgemm("conv_wgrad[tma]", sh, a, b, ep, M, O, P, ws, ws_bytes, st);
   }
@@ -929,7 +982,7 @@ int gemm_fc_fwd(const bf16_t* x, size_t psx, const bf16_t* w, size_t psw, const 
   if (tma_on()) {
     const TgShape sh = tg_shape(M, out_dim, I8, ws_bytes);
     TgOperand a, b;
-    if (op_tiled_k(a, x, psx, M, I8, I8, TG_BM) && op_tiled_mn(b, w, psw, out_dim, in_dim, O8, sh.BN / sh.CL))
+    if (op_tiled_k(a, x, psx, M, I8, I8, TG_BM * sh.MH) && op_tiled_mn(b, w, psw, out_dim, in_dim, O8, sh.BN / sh.CL))
       return run_tgemm("fc_fwd[tma]", sh, a, b, ep, M, out_dim, I8, ws, ws_bytes, st);
   }
   SvRowsK va{x, psx, M, I8, I8};
@@ -943,7 +996,7 @@ int gemm_fc_dgrad(const bf16_t* g, size_t psg, const bf16_t* w, size_t psw, cons
   if (tma_on()) {
     const TgShape sh = tg_shape(M, in_dim, O8, ws_bytes);
     TgOperand a, b;
-    if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM) && op_tiled_k(b, w, psw, in_dim, O8, O8, sh.BN / sh.CL))
+    if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM * sh.MH) && op_tiled_k(b, w, psw, in_dim, O8, O8, sh.BN / sh.CL))
       return run_tgemm("fc_dgrad[tma]", sh, a, b, ep, M, in_dim, O8, ws, ws_bytes, st);
   }
   SvRowsK va{g, psg, M, O8, O8};
@@ -958,7 +1011,7 @@ int gemm_fc_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, cons
   if (tma_on()) {
     const TgShape sh = tg_shape(in_dim, out_dim, M, ws_bytes);
     TgOperand a, b;
-    if (op_tiled_mn(a, x, psx, in_dim, M, I8, TG_BM) &&
+    if (op_tiled_mn(a, x, psx, in_dim, M, I8, TG_BM * sh.MH) &&
         op_tiled_mn(b, g, psg, out_dim, M, O8, sh.BN / sh.CL))
       return run_tgemm("fc_wgrad[tma]", sh, a, b, ep, in_dim, out_dim, M, ws, ws_bytes, st);
   }
@@ -1000,6 +1053,13 @@ unsigned long long stz_launch_count(void) { return g_launches; }
 
 int stz_set_tma(int on) {
   g_use_tma = on ? 1 : 0;
+  g_mn3d = on == 1 ? 1 : 0;
+  return STZ_OK;
+}
+
+int stz_set_mh(int mode) {
+  if (mode < 0 || mode > 2) return fail(STZ_EINVAL, "set_mh: mode %d (0 auto, 1 never, 2 always)", mode);
+  g_mh_mode = mode;
   return STZ_OK;
 }
 

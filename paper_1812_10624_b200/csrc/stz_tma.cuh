@@ -37,6 +37,7 @@ struct alignas(64) TgOperand {
   int nbox;            // boxes per plane per k-block
   int box_bytes;       // smem bytes per box (2048 for 32-wide MN boxes)
   int box_rows;        // TILED_K: rows per box (a B tile split between 2 CTAs)
+  int mn3d;            // TILED_MN: the tile is one 3D box (rows % 32 == 0)
   // im2col geometry: output pixel (n, oh, ow) -> window start (oh*s + lo, ow*s + lo)
   int lo, s, C8, ksz, flip;
   FastDiv d_ohw, d_ow, d_c8, d_k;
@@ -59,9 +60,14 @@ constexpr int TG_THREADS = 256;  // w0 TMA (32 lanes), w1 MMA, w2 TMEM alloc, w3
 // of B (BN / 2 rows), so per-SM operand traffic per MMA cycle drops by
 // 1 - (128 + BN/2) / (128 + BN): the split-plane GEMMs are bound by the
 // L2 -> SM operand feed (3 planes per operand), not by the tensor pipe.
-template <int BN, int NSETS = 2, int CL = 1>
+// MH = 2 (unpaired only): one CTA computes TWO 128-row halves of a 256 x BN
+// tile against the same B stage -- one 256-row A box per plane (TMA cost is
+// per box: tools/tma_bench.cu) and B fetched once for both halves; each half
+// has its own TMEM accumulators (MH * NSETS * ACC_COLS <= 512).
+template <int BN, int NSETS = 2, int CL = 1, int MH = 1>
 struct TgCfg {
-  static constexpr int A_BYTES = TG_BM * TG_BK * 2;        // one plane, 8 KB
+  static_assert(MH == 1 || (CL == 1 && BN == 64), "two M halves: thin unpaired tiles only");
+  static constexpr int A_BYTES = TG_BM * MH * TG_BK * 2;   // one plane, 8 KB per half
   static constexpr int B_ROWS = BN / CL;                    // B rows staged by this CTA
   static constexpr int B_BYTES = B_ROWS * TG_BK * 2;
   static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
@@ -73,8 +79,8 @@ struct TgCfg {
   // instead of 6 at N=64; the products land in big + two small accumulators.
   static constexpr bool PAIRB = BN == 64 && CL == 1;
   static constexpr int ACC_COLS = PAIRB ? 3 * BN : 2 * BN;
-  static constexpr int TMEM_COLS = NSETS * ACC_COLS <= 256 ? 256 : 512;
-  static_assert(NSETS * ACC_COLS <= 512, "BN too wide for the TMEM sets");
+  static constexpr int TMEM_COLS = MH * NSETS * ACC_COLS <= 256 ? 256 : 512;
+  static_assert(MH * NSETS * ACC_COLS <= 512, "BN too wide for the TMEM sets");
   static_assert(STAGES >= 3, "tile too large");
   static_assert(B_BYTES % 512 == 0, "B plane blocks must stay 512-byte aligned (SW64 atoms)");
 };
@@ -107,6 +113,28 @@ __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint32_t dst, uin
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// 3D tiled box {32 elements, 32 K rows, g 32-element groups}: an MN-major tile
+// of 32 g rows in ONE TMA instruction (the box lands as g consecutive 2 KB
+// SW64 atoms -- the layout of g separate 2D boxes).  TMA cost is per box, so
+// fewer, larger boxes feed faster (tools/tma_bench.cu: 2 KB boxes ~21
+// B/cycle/SM, 8 KB ~41, 16 KB ~60 from L2).
+template <int CL>
+__device__ __forceinline__ void tma_3d(const CUtensorMap* map, uint32_t dst, uint64_t* bar,
+                                       int c0, int c1, int c2) {
+  if (CL == 2)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
 
@@ -210,7 +238,10 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
       tma_2d<CL>(map, dst, bar, k0, r0 + box * op.box_rows);
       break;
     case TG_TILED_MN:
-      tma_2d<CL>(map, dst, bar, r0 + 32 * box, k0);
+      if (op.mn3d)   // one box for the whole tile: {32, 32 K, R/32 groups}
+        tma_3d<CL>(map, dst, bar, 0, k0, r0 >> 5);
+      else
+        tma_2d<CL>(map, dst, bar, r0 + 32 * box, k0);
       break;
     case TG_IM2COL_K: {
       uint32_t n, j, oh, ow, tap, c0, th, tw;
@@ -251,12 +282,12 @@ __device__ __forceinline__ uint64_t tg_desc(int mode, uint32_t plane_base, int k
 // TMEM (each holds its 128 rows x BN); its commits arrive on the empty / tfull
 // barriers of both CTAs; both epilogues release the set on the leader's
 // tempty barrier (8 warp arrivals).
-template <int BN, int NSETS, int CL, class EP>
+template <int BN, int NSETS, int CL, class EP, int MH = 1>
 __global__ void __launch_bounds__(TG_THREADS, 1)
     tgemm_kernel(const __grid_constant__ TgParams<EP> p) {
-  using Cfg = TgCfg<BN, NSETS, CL>;
+  using Cfg = TgCfg<BN, NSETS, CL, MH>;
   constexpr int STAGES = Cfg::STAGES;
-  constexpr int PM = TG_BM * CL;   // rows per work item
+  constexpr int PM = TG_BM * CL * MH;   // rows per work item
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t smem_base = (raw + 1023u) & ~1023u;
@@ -338,7 +369,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     // ---------------- MMA issuer (the leader CTA for a pair) --------------------
     const bool amn = p.a.mode == TG_TILED_MN || p.a.mode == TG_IM2COL_MN;
     const bool bmn = p.b.mode == TG_TILED_MN || p.b.mode == TG_IM2COL_MN;
-    const uint32_t idesc = sg_idesc(PM, BN, amn, bmn);
+    const uint32_t idesc = sg_idesc(TG_BM * CL, BN, amn, bmn);
     constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
     constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
     // descriptors of stage 0 / plane 0 / k-step 0; every other (stage, plane,
@@ -366,19 +397,23 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
           // big (cols 0..63) | S1 (64..127) | S2 (128..191):
           //   a0*b2 -> S2;  a0*[b0|b1] -> big, S1;  a1*[b0|b1] -> S1, S2;  a2*b0 -> S1
           // (ordered so that every accumulator's first write is an overwrite)
-          const uint32_t idesc2 = sg_idesc(PM, 2 * BN, amn, bmn);
-          const uint32_t tS1 = tbig + BN, tS2 = tbig + 2 * BN;
+          const uint32_t idesc2 = sg_idesc(TG_BM, 2 * BN, amn, bmn);
 #pragma unroll
           for (int j = 0; j < TG_BK / 16; ++j) {
             if (p.debug & 2) break;
             const uint32_t acc_in = (kb | j) == 0 ? 0u : 1u;
-            const uint64_t a0d = da0 + (so + j * ak);
-            const uint64_t a1d = a0d + (Cfg::A_BYTES >> 4), a2d = a0d + 2 * (Cfg::A_BYTES >> 4);
             const uint64_t b0d = db0 + (so + j * bk), b2d = b0d + 2 * (Cfg::B_BYTES >> 4);
-            umma_f16(tS2, a0d, b2d, idesc, acc_in);
-            umma_f16(tbig, a0d, b0d, idesc2, acc_in);
-            umma_f16(tS1, a1d, b0d, idesc2, 1u);
-            umma_f16(tS1, a2d, b0d, idesc, 1u);
+#pragma unroll
+            for (int h = 0; h < MH; ++h) {   // half h: A rows 128 h.., TMEM set h
+              const uint32_t th = tbig + h * Cfg::ACC_COLS;
+              const uint32_t tS1 = th + BN, tS2 = th + 2 * BN;
+              const uint64_t a0d = da0 + (so + j * ak + h * ((TG_BM * TG_BK * 2) >> 4));
+              const uint64_t a1d = a0d + (Cfg::A_BYTES >> 4), a2d = a0d + 2 * (Cfg::A_BYTES >> 4);
+              umma_f16(tS2, a0d, b2d, idesc, acc_in);
+              umma_f16(th, a0d, b0d, idesc2, acc_in);
+              umma_f16(tS1, a1d, b0d, idesc2, 1u);
+              umma_f16(tS1, a2d, b0d, idesc, 1u);
+            }
           }
         } else {
 #pragma unroll
@@ -413,8 +448,10 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
       const int use = NSETS == 2 ? (it >> 1) : it;
       mbar_wait_backoff(&tfull_bar[acc], use & 1);
       tc_fence_after();
-      const int m = m0 + q * 32 + lane;
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
+#pragma unroll 1
+      for (int h = 0; h < MH; ++h) {
+      const int m = m0 + h * TG_BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (acc + h) * Cfg::ACC_COLS;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         if (n0 + c >= npad) break;
@@ -463,6 +500,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
           }
         }
       }
+      }   // halves
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

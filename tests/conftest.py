@@ -34,10 +34,11 @@ def lib():
     return _lib.load()
 
 
-@pytest.fixture(params=[1, 0], ids=["tma", "cp.async"])
+@pytest.fixture(params=[1, 2, 0], ids=["tma", "tma2d", "cp.async"])
 def producer(request, lib):
-    """Run a GPU op test under both GEMM producers (TMA tensor maps and the
-    cp.async gather); restore TMA afterwards."""
+    """Run a GPU op test under every GEMM producer (TMA tensor maps with 3D
+    MN-major boxes, TMA with 2D boxes only, and the cp.async gather);
+    restore the default afterwards."""
     lib.stz_set_tma(request.param)
     yield request.param
     lib.stz_set_tma(1)

@@ -251,3 +251,27 @@ def band(request, lib):
 @pytest.mark.parametrize("shape", VALID_CONV_SHAPES, ids=lambda s: "x".join(map(str, s)))
 def test_valid_conv_band_vs_oracle(tc, band, shape):
     _conv_case(tc, shape)
+
+
+@pytest.fixture(params=[(64, 1, 1), (64, 1, 3)], ids=["bn64-sp1", "bn64-sp3"])
+def halves(request, lib):
+    """Thin tiles as two 128-row halves per CTA (stz_set_mh(2)): one 256-row A
+    box, one B stage shared by both halves' TMEM accumulators."""
+    assert lib.stz_set_tile(*request.param) == 0
+    assert lib.stz_set_mh(2) == 0
+    yield request.param
+    lib.stz_set_mh(0)
+    lib.stz_set_tile(0, 0, 0)
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 27, 27, 192, 5, 1, 2), (2, 64, 13, 13, 64, 3, 1, 1),
+                                   (3, 96, 9, 9, 40, 3, 1, 1), (1, 3, 224, 224, 64, 11, 4, 2)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_conv_two_halves(tc, producer, halves, shape):
+    _conv_case(tc, shape)
+
+
+@pytest.mark.parametrize("shape", [(300, 640, 64), (896, 1024, 40), (257, 200, 96)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_fc_two_halves(tc, producer, halves, shape):
+    _fc_case(tc, shape)
