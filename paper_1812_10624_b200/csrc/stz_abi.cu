@@ -428,8 +428,8 @@ bool enc_tiled(CUtensorMap* out, const void* base, uint64_t inner, uint64_t oute
 }
 
 bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8, int s, int lo,
-                int hi, int pixels) {
-  const std::string key = cache_key(1, (uintptr_t)base, N, H, W, C8, s, lo, hi, pixels);
+                int hi, int pixels, int chans = 32) {
+  const std::string key = cache_key(1, (uintptr_t)base, N, H, W, C8, s, lo, hi, pixels, chans);
   auto it = g_map_cache.find(key);
   if (it != g_map_cache.end()) {
     *out = it->second;
@@ -440,8 +440,9 @@ bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8,
   int lower[2] = {lo, lo}, upper[2] = {hi, hi};
   cuuint32_t es[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
   CUresult r = g_enc_im2col(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
-                            strides, lower, upper, 32, (cuuint32_t)pixels, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                            strides, lower, upper, (cuuint32_t)chans, (cuuint32_t)pixels, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            chans == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   g_map_cache.emplace(key, *out);
@@ -507,7 +508,7 @@ bool enc_mn3d(CUtensorMap* out, const void* base, uint64_t rows, uint64_t K, uin
   return true;
 }
 
-int g_mn3d = 1;   // stz_set_tma(2) disables the 3D MN-major boxes (tests compare)
+int g_mn3d = 1;   // stz_set_tma(2): no 3D MN-major boxes, no SW128 im2col boxes (tests compare)
 
 // [K][rows] planes, rows contiguous (row stride ld), tile of R rows (R % 32 == 0).
 // rows % 32 == 0: one 3D box per plane per k-block; else R/32 2D boxes
@@ -533,8 +534,10 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
                int ksz, int s, int lo, int hi, int OH, int OW, int R) {
   op = TgOperand{};
   op.mode = mn ? TG_IM2COL_MN : TG_IM2COL_K;
-  op.nbox = mn ? R / 32 : 1;
-  op.box_bytes = 2048;
+  // MN-major (weight-gradient A): 64-channel SW128 boxes when the channels allow
+  op.sw128 = mn && g_mn3d && C8 % 64 == 0 && R % 64 == 0;
+  op.nbox = mn ? R / (op.sw128 ? 64 : 32) : 1;
+  op.box_bytes = op.sw128 ? 4096 : 2048;
   op.lo = lo;
   op.s = s;
   op.C8 = C8;
@@ -544,7 +547,8 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
   op.d_c8 = FastDiv(C8);
   op.d_k = FastDiv(ksz);
   for (int pl = 0; pl < 3; ++pl)
-    if (!enc_im2col(&op.map[pl], p + pl * ps, N, H, W, C8, s, lo, hi, mn ? 32 : R))
+    if (!enc_im2col(&op.map[pl], p + pl * ps, N, H, W, C8, s, lo, hi, mn ? 32 : R,
+                    op.sw128 ? 64 : 32))
       return false;
   return true;
 }

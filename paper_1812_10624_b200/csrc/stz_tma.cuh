@@ -38,6 +38,7 @@ struct alignas(64) TgOperand {
   int box_bytes;       // smem bytes per box (2048 for 32-wide MN boxes)
   int box_rows;        // TILED_K: rows per box (a B tile split between 2 CTAs)
   int mn3d;            // TILED_MN: the tile is one 3D box (rows % 32 == 0)
+  int sw128;           // IM2COL_MN: 64-channel boxes with the 128-byte swizzle (C8 % 64 == 0)
   // im2col geometry: output pixel (n, oh, ow) -> window start (oh*s + lo, ow*s + lo)
   int lo, s, C8, ksz, flip;
   FastDiv d_ohw, d_ow, d_c8, d_k;
@@ -257,7 +258,7 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
       uint32_t n, j, oh, ow, tap, c0, th, tw;
       op.d_ohw.divmod((uint32_t)k0, n, j);
       op.d_ow.divmod(j, oh, ow);
-      op.d_c8.divmod((uint32_t)(r0 + 32 * box), tap, c0);
+      op.d_c8.divmod((uint32_t)(r0 + (op.sw128 ? 64 : 32) * box), tap, c0);
       op.d_k.divmod(tap, th, tw);
       tma_im2col_4d<CL>(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo,
                         (int)(oh * op.s) + op.lo, (int)n, (uint16_t)tw, (uint16_t)th);
@@ -265,8 +266,16 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
   }
 }
 
-__device__ __forceinline__ uint64_t tg_desc(int mode, uint32_t plane_base, int kstep) {
+// SWIZZLE_128B UMMA descriptor (layout type 2): MN-major 64-element x 8-k-row
+// atoms of 1 KB; LBO = bytes between 64-element MN groups, SBO = 1 KB
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (umma_desc_sw64(saddr, lbo, sbo) & ~((uint64_t)7 << 61)) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ uint64_t tg_desc(int mode, uint32_t plane_base, int kstep,
+                                            int sw128 = 0) {
   const bool mn = mode == TG_TILED_MN || mode == TG_IM2COL_MN;
+  if (mn && sw128) return umma_desc_sw128(plane_base + kstep * 2048, 4096, 1024);
   return mn ? umma_desc_sw64(plane_base + kstep * 1024, 2048, 512)
             : umma_desc_sw64(plane_base + kstep * 32, 16, 512);
 }
@@ -375,9 +384,10 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     // descriptors of stage 0 / plane 0 / k-step 0; every other (stage, plane,
     // k-step) only moves the 14-bit start-address field (addresses < 256 KB,
     // so the add never carries out of it): two integer adds per MMA
-    const uint64_t da0 = tg_desc(p.a.mode, smem_base, 0);
+    const uint64_t da0 = tg_desc(p.a.mode, smem_base, 0, p.a.sw128);
     const uint64_t db0 = tg_desc(p.b.mode, smem_base + 3 * Cfg::A_BYTES, 0);
-    const uint32_t ak = (amn ? 1024u : 32u) >> 4, bk = (bmn ? 1024u : 32u) >> 4;
+    const uint32_t ak = (amn ? (p.a.sw128 ? 2048u : 1024u) : 32u) >> 4,
+                   bk = (bmn ? 1024u : 32u) >> 4;
     int g = 0, it = 0;
     for (int w = cid; w < items; w += ncl, ++it) {
       const int z = w / (mt * nt);
