@@ -15,5 +15,6 @@ for tag in "$@"; do
       -k regex:tgemm -c 1 -o "$OUT/$tag" python tools/profile_op.py "$tag" > "$OUT/${tag}_ncu.log" 2>&1
   ncu -i "$OUT/$tag.ncu-rep" --page raw --csv > "$OUT/${tag}_raw.csv" 2>/dev/null
   ncu -i "$OUT/$tag.ncu-rep" --page details --csv > "$OUT/${tag}_details.csv" 2>/dev/null
+  ncu -i "$OUT/$tag.ncu-rep" --page source --csv --print-source sass > "$OUT/${tag}_source.csv" 2>/dev/null
   rm -f "$OUT/$tag.ncu-rep"
 done
