@@ -318,6 +318,20 @@ class StanzaCluster:
             eng.forward(acts.rows_view(lo, hi), lab_all[lo:hi], loss_out=loss_slot)
             eng.backward()
 
+        # the FC block's exchange + update depend only on the FC gradients: they
+        # run on a side stream, concurrently with the CONV backward (the
+        # momentum kernel is HBM-bound and co-resides with the GEMMs, which
+        # are bound by the L2 -> SM feed); joined before the step ends
+        overlap = ev is None
+        main = torch.cuda.current_stream(self.device)
+        if overlap:
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                for eng in self.fcs[1:]:
+                    self.fcs[0].add_grads_from(eng)
+                self.fcs[0].sgd(n, self.lr, self.momentum)
+
         mark("boundary")
         led.record("boundary", self.n_conv * a_bytes)
         led.tag_payload_bytes[Tag.BOUNDARY_GRADS] += self.n_conv * a_bytes
@@ -330,16 +344,25 @@ class StanzaCluster:
             (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
         led.record("exchange", ar_bytes)
         led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
-        for eng in self.fcs[1:]:
-            self.fcs[0].add_grads_from(eng)
+        if not overlap:
+            for eng in self.fcs[1:]:
+                self.fcs[0].add_grads_from(eng)
 
         mark("update")
         led.record("update")
         self.conv.sgd(n, self.lr, self.momentum)
-        self.fcs[0].sgd(n, self.lr, self.momentum)
+        if overlap:
+            main.wait_stream(side)
+        else:
+            self.fcs[0].sgd(n, self.lr, self.momentum)
         mark("end")
         if ev is not None:
             self._pending_events.append(ev)
+
+    def _side_stream(self) -> "torch.cuda.Stream":
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side
 
     def _segment(self, key, fn) -> None:
         """Run a compute segment of the pipelined step: eagerly during the
