@@ -276,6 +276,57 @@ def measure_constants(spec, device=None, reps: int = 7, bandwidth: float | None 
                "reps": reps, "device": str(dev)}
 
 
+def measure_fc_group_time(spec, groups=(1, 3, 7), device=None, reps: int = 7,
+                          seed: int = 0) -> dict:
+    """Seconds for one FC worker's share of an iteration when it serves g
+    CONV batches: FC block forward + backward on g*K boundary rows plus its
+    momentum update (the FC worker's critical work in the pipelined step).
+    The reference model charges g * T_f; on B200 the FC GEMMs run at larger M
+    more efficiently, so this is what decides 7:1 vs 6:2."""
+    import numpy as np
+    import torch
+
+    from .engine import BlockEngine
+    from .tensor_core import seeded_init
+
+    dev = torch.device(device if device is not None else "cuda")
+    part = split(spec)
+    layers = spec.require_layers()
+    cut = part.split_index
+    params = seeded_init(layers, seed)
+    vel = [[np.zeros_like(t) for t in row] for row in params]
+    a = part.boundary_activations
+    classes = layers[-2].out_dim
+    out = {}
+    for g in groups:
+        rows = g * spec.batch_k
+        fc = BlockEngine(layers[cut:], (a,), rows, dev, params[cut:], vel[cut:],
+                         need_input_grad=True)
+        gen = torch.Generator(device=dev).manual_seed(seed)
+        x = torch.randn((rows, a), generator=gen, device=dev)
+        y = torch.randint(0, classes, (rows,), generator=gen, device=dev, dtype=torch.int32)
+
+        def step():
+            fc.forward(x, y)
+            fc.backward()
+            fc.sgd(rows, 1e-6, 0.9)
+
+        step()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        out[g] = statistics.median(ts)
+        del fc
+    return out
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("--model", default="alexnet_exec")
@@ -305,6 +356,19 @@ def main(argv=None) -> int:
         bsp = stanza_throughput(part, n_conv, n_fc, c)
         pip = n_conv * spec.batch_k / pipelined_iter_time(part, n_conv, n_fc, c, args.micro)
         print(f"{n_conv:>4}:{n_fc:<2} {bsp:12.0f} {pip:16.0f}")
+    if args.measure:
+        gt = measure_fc_group_time(spec, groups=sorted({1, 2, 3, 7}))
+        print("# FC worker time per iteration serving g CONV batches (fwd + bwd + update): " +
+              ", ".join(f"g={g}: {t * 1e3:.3f} ms" for g, t in gt.items()))
+        for n_fc in range(1, args.nodes):
+            n_conv = args.nodes - n_fc
+            if n_fc > n_conv:
+                break
+            g = -(-n_conv // n_fc)
+            if g in gt:
+                t = max(c.conv_time, gt[g])
+                print(f"# measured-FC pipelined {n_conv}:{n_fc}: max(T_c, T_fc(g={g})) = "
+                      f"{t * 1e3:.3f} ms -> {n_conv * spec.batch_k / t:.0f} img/s")
     a = assign_nodes(part, args.nodes, c, fc_memory_bytes=mem)
     p = assign_nodes(part, args.nodes, c, fc_memory_bytes=mem,
                      model=lambda *a_: pipelined_iter_time(*a_, micro=args.micro))
