@@ -326,6 +326,21 @@ void launch_sg(const VA& va, const VB& vb, const EP& ep, float* partial, int M, 
                                                                           K, kps);
 }
 
+// split-K reduction launcher: the lane-parallel kernel when there are many
+// splits, else the one-thread-per-chunk serial walk
+template <class EP>
+void launch_reduce(const float* partial, int splits, int M, int N, const EP& ep, cudaStream_t st) {
+  const size_t total = (size_t)M * (rup8(N) / 8);
+  if (splits >= 16) {
+    const size_t blocks = (total + 31) / 32;
+    const size_t cap = (size_t)num_sms() * 8;
+    sgemm_reduce_wide_kernel<EP><<<(int)(blocks < cap ? blocks : cap), 256, 0, st>>>(
+        partial, splits, M, N, ep);
+  } else {
+    sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(partial, splits, M, N, ep);
+  }
+}
+
 // C[M,N] = A(M,K) . B(K,N) over split-plane views; ep applied once.
 template <class VA, class VB, class EP>
 int run_sgemm(const char* what, const VA& va, const VB& vb, const EP& ep, int M, int N, int K,
@@ -357,8 +372,7 @@ int run_sgemm(const char* what, const VA& va, const VB& vb, const EP& ep, int M,
   int rc = check_launch(what);
   if (rc) return rc;
   if (splits > 1) {
-    const size_t total = (size_t)M * (npad / 8);
-    sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(partial, splits, M, N, ep);
+    launch_reduce(partial, splits, M, N, ep, st);
     rc = check_launch("sgemm_reduce");
   }
   return rc;
@@ -814,8 +828,7 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   else launch_band<128, 1>(prm, items, smem, st);
   int rc = check_launch(what);
   if (rc || splits == 1) return rc;
-  const size_t total = (size_t)M_out * (npad / 8);
-  sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(prm.partial, splits, M_out, O, ep);
+  launch_reduce(prm.partial, splits, M_out, O, ep, st);
   return check_launch("band_reduce");
 }
 
@@ -869,8 +882,7 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   int rc = check_launch(what);
   if (rc) return rc;
   if (splits > 1) {
-    const size_t total = (size_t)M * (npad / 8);
-    sgemm_reduce_kernel<EP><<<grid_for(total), 256, 0, st>>>(prm.partial, splits, M, N, ep);
+    launch_reduce(prm.partial, splits, M, N, ep, st);
     rc = check_launch("tgemm_reduce");
   }
   return rc;

@@ -627,4 +627,64 @@ __global__ void sgemm_reduce_kernel(const float* __restrict__ partial, int split
   }
 }
 
+// Split-K reduction for many splits (S >= 16): the plain kernel above gives
+// one thread per 8-column chunk a serial walk over all S partials, which is
+// latency-bound when M*N is small (conv1's weight gradient: 4,608 threads x
+// 118 splits).  Here a block of 256 threads covers 32 chunks x 8 z-lanes;
+// lane l sums splits l, l+8, l+16, ... in order, and the 8 lane sums are then
+// added in lane order through shared memory -- a fixed order, so the result
+// is deterministic (it differs from the serial order only by fp32 rounding).
+template <class EP>
+__global__ void __launch_bounds__(256) sgemm_reduce_wide_kernel(const float* __restrict__ partial,
+                                                                 int splits, int M, int N, EP ep) {
+  __shared__ float red[8][32][9];
+  const int npad = cdiv(N, 8) * 8;
+  const int chunks = npad / 8;
+  const size_t total = (size_t)M * chunks;
+  const size_t zs = (size_t)M * npad;
+  const int cl = threadIdx.x & 31, zl = threadIdx.x >> 5;
+  for (size_t base = (size_t)blockIdx.x * 32; base < total; base += (size_t)gridDim.x * 32) {
+    const size_t i = base + cl;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+    if (i < total) {
+      const int m = (int)(i / chunks), nb = (int)(i % chunks) * 8;
+      const float* src = partial + (size_t)m * npad + nb;
+      for (int z = zl; z < splits; z += 16) {
+        const bool two = z + 8 < splits;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(src + z * zs));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(src + z * zs) + 1);
+        float4 c = make_float4(0.f, 0.f, 0.f, 0.f), d = c;
+        if (two) {
+          c = __ldg(reinterpret_cast<const float4*>(src + (z + 8) * zs));
+          d = __ldg(reinterpret_cast<const float4*>(src + (z + 8) * zs) + 1);
+        }
+        v[0] = __fadd_rn(v[0], a.x); v[1] = __fadd_rn(v[1], a.y);
+        v[2] = __fadd_rn(v[2], a.z); v[3] = __fadd_rn(v[3], a.w);
+        v[4] = __fadd_rn(v[4], b.x); v[5] = __fadd_rn(v[5], b.y);
+        v[6] = __fadd_rn(v[6], b.z); v[7] = __fadd_rn(v[7], b.w);
+        if (two) {
+          v[0] = __fadd_rn(v[0], c.x); v[1] = __fadd_rn(v[1], c.y);
+          v[2] = __fadd_rn(v[2], c.z); v[3] = __fadd_rn(v[3], c.w);
+          v[4] = __fadd_rn(v[4], d.x); v[5] = __fadd_rn(v[5], d.y);
+          v[6] = __fadd_rn(v[6], d.z); v[7] = __fadd_rn(v[7], d.w);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[zl][cl][j] = v[j];
+    __syncthreads();
+    if (zl == 0 && i < total) {
+#pragma unroll
+      for (int l = 1; l < 8; ++l)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __fadd_rn(v[j], red[l][cl][j]);
+      const int m = (int)(i / chunks), nb = (int)(i % chunks) * 8;
+      ep.store8(m, nb, v);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace stz
