@@ -77,8 +77,8 @@ def oracle_sample(model: str, images: int = 1, classes: int = 1000):
     images per CONV worker (1 CONV : 1 FC); returns seconds."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import stanza_oracle as orc
-    layers, shape = {"alexnet_exec": orc.alexnet_layers, "vgg16_exec": orc.vgg16_layers}.get(
-        model, orc.alexnet_layers)()
+    layers, shape = {"alexnet_exec": orc.alexnet_layers, "vgg16_exec": orc.vgg16_layers,
+                     "resnet50_exec": orc.resnet_layers}.get(model, orc.alexnet_layers)()
     mk = orc.batch_fn(shape, images, 7, classes=classes)
     t0 = time.perf_counter()
     orc.layer_separated_train(layers, images, 1, 1, 1, 3, mk)
@@ -91,7 +91,8 @@ def reference_arm(args):
         return 0
     from paper_1812_10624_b200.roles import gpu_roles
     n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
-    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64}.get(args.model, 128)
+    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32}.get(
+        args.model, 128)
     budget = 150.0
     for _ in range(min(args.warmup, 1)):
         oracle_sample(args.model)

@@ -222,6 +222,31 @@ int stzx_pack_conv_w_s2d(const float* w, void* wf, size_t ps, int O, int C, int 
 int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, float* gw,
                         float* gb, int accumulate, int N, int C, int Cs8, int Hs, int Ws, int O,
                         int O8, int k, int s, void* ws, size_t ws_bytes, void* stream);
+/* ResNet-trunk kinds.  The reference has no such layers
+ * (tensor_core.py:37-74 stops at SoftmaxCrossEntropy), so there is no
+ * reference entry point to replace; semantics are the oracle's
+ * (oracle/stanza_oracle.py: bn_forward, bn_backward, gap_forward, gap_backward,
+ * residual), parity
+ * unpinned.  BatchNorm runs in training mode with float64 statistics per
+ * group of `group` samples (one CONV worker's batch); `stats` is caller-owned
+ * double [N/group][C8][2] = (mean, rstd), written by the forward and read by
+ * the backward.  y = ((x-mean)*rstd)*gamma + beta (+ res, fp32 add) (ReLU). */
+int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta, const void* res,
+                size_t psr, void* y, size_t psy, double* stats, int N, int HW, int C, int C8,
+                int group, float eps, int relu, void* ws, size_t ws_bytes, void* stream);
+/* dgamma / dbeta batch sums (added with `accumulate`), gx nullable. */
+int stzx_bn_bwd(const void* g, size_t psg, const void* x, size_t psx, const double* stats,
+                const float* gamma, float* ggamma, float* gbeta, int accumulate, void* gx,
+                size_t psgx, int N, int HW, int C, int C8, int group, void* ws, size_t ws_bytes,
+                void* stream);
+/* global average pool NHWC [N][HW][C8] <-> rows [N][C8] (float64 sums / HW) */
+int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, int C8,
+                 void* stream);
+int stzx_gap_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int HW, int C8,
+                 void* stream);
+/* y = a + b elementwise (fp32 RN), n a multiple of 8: residual input gradients */
+int stzx_add(const void* a, size_t psa, const void* b, size_t psb, void* y, size_t psy, size_t n,
+             void* stream);
 /* SoftmaxCE on fp32 logits -> losses + split dlogits [M][C8]. */
 int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
                     int M, int C, int C8, void* stream);

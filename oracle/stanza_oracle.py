@@ -25,6 +25,18 @@ Layers are plain tuples so this module depends on nothing but numpy:
     ("fc", in_dim, out_dim)
     ("relu",)
     ("softmax_ce",)
+
+SURVEY.md §8f row 4 adds the layer kinds of the ResNet trunk.  The
+reference has no such kinds (``tensor_core.py:37-74``), so their semantics
+are defined HERE (training-mode BatchNorm over each call's batch, global
+average pooling, post-activation residual blocks); parity for them is
+UNPINNED -- no reference output exists to check this restatement against:
+
+    ("bn", channels, eps)             gamma, beta [C]; init 1 / 0 (no RNG draw)
+    ("gap",)                          (C, H, W) -> (C, 1, 1)
+    ("residual", body, shortcut)      relu(body(x) + shortcut(x)); shortcut
+                                      () is the identity; params = body's
+                                      then shortcut's, one flat row
 """
 
 from __future__ import annotations
@@ -169,6 +181,60 @@ def softmax_ce_backward(p, labels):
     return g.astype(F32)
 
 
+def bn_forward(x, gamma, beta, eps):
+    """BatchNorm2d forward, training mode (not in the reference; §8f row 4).
+
+    Batch statistics over (N, H, W) in float64 (two-pass, biased variance),
+    xhat = (x - mean) * rstd, y = xhat * gamma + beta rounded once to fp32.
+    eps is taken at float32 precision (the value the C ABI receives).
+    Returns (y, cache) with cache = (xhat64, rstd64, m).
+    """
+    xd = x.astype(F64)
+    m = x.shape[0] * x.shape[2] * x.shape[3]
+    mean = xd.mean(axis=(0, 2, 3))
+    var = ((xd - mean[None, :, None, None]) ** 2).mean(axis=(0, 2, 3))
+    rstd = 1.0 / np.sqrt(var + float(F32(eps)))
+    xhat = (xd - mean[None, :, None, None]) * rstd[None, :, None, None]
+    y = xhat * gamma.astype(F64)[None, :, None, None] + beta.astype(F64)[None, :, None, None]
+    return y.astype(F32), (xhat, rstd, m)
+
+
+def bn_backward(cache, gamma, gy):
+    """BatchNorm2d backward of the loss SUM -> (gx, dgamma, dbeta):
+    gx = (gamma * rstd / m) * ((m * g - sum g) - xhat * sum(g * xhat)),
+    everything float64, rounded once."""
+    xhat, rstd, m = cache
+    gd = gy.astype(F64)
+    sg = gd.sum(axis=(0, 2, 3))
+    sgx = (gd * xhat).sum(axis=(0, 2, 3))
+    coef = (gamma.astype(F64) * rstd) / m
+    inner = (m * gd - sg[None, :, None, None]) - xhat * sgx[None, :, None, None]
+    gx = coef[None, :, None, None] * inner
+    return gx.astype(F32), sgx.astype(F32), sg.astype(F32)
+
+
+def gap_forward(x):
+    """Global average pool (C, H, W) -> (C, 1, 1): float64 sum / (H*W)."""
+    hw = x.shape[2] * x.shape[3]
+    return (x.astype(F64).sum(axis=(2, 3), keepdims=True) / hw).astype(F32)
+
+
+def gap_backward(x_shape, gy):
+    """Each input cell receives g / (H*W) (float64 quotient, rounded once)."""
+    hw = x_shape[2] * x_shape[3]
+    return np.broadcast_to((gy.astype(F64) / hw).astype(F32), x_shape).copy()
+
+
+def _split_rows(layers, flat):
+    """Cut one residual row's flat tensor list into per-sub-layer lists."""
+    out, off = [], 0
+    for l in layers:
+        n = len(param_shapes(l))
+        out.append(list(flat[off:off + n]))
+        off += n
+    return out
+
+
 # ---------------------------------------------------------------------------
 # shapes, init, blocks
 # ---------------------------------------------------------------------------
@@ -180,6 +246,10 @@ def param_shapes(layer):
         return [(cout, cin, k, k), (cout,)]
     if layer[0] == "fc":
         return [(layer[1], layer[2]), (layer[2],)]
+    if layer[0] == "bn":
+        return [(layer[1],), (layer[1],)]
+    if layer[0] == "residual":
+        return [s for l in layer[1] + layer[2] for s in param_shapes(l)]
     return []
 
 
@@ -203,23 +273,36 @@ def out_shape(layer, shape):
         return (int(np.prod(shape)),)
     if kind == "fc":
         return (layer[2],)
-    if kind == "relu":
+    if kind in ("relu", "bn"):
+        return shape
+    if kind == "gap":
+        return (shape[0], 1, 1)
+    if kind == "residual":
+        for l in layer[1]:
+            shape = out_shape(l, shape)
         return shape
     return ()
 
 
+def _init_layer(gen, layer):
+    if layer[0] == "bn":
+        return [np.ones(layer[1], F32), np.zeros(layer[1], F32)]
+    if layer[0] == "residual":
+        return [t for l in layer[1] + layer[2] for t in _init_layer(gen, l)]
+    ts = []
+    for shp in param_shapes(layer):
+        bound = float(np.sqrt(1.0 / fan_in(layer)))
+        ts.append(gen.uniform(-bound, bound, size=shp).astype(F32))
+    return ts
+
+
 def seeded_init(layers, seed):
     """tensor_core.py:332-346: one PCG64(seed) stream, U(-s, s) drawn in float64
-    then rounded, s = sqrt(1/fan_in), weight before bias, layer order."""
+    then rounded, s = sqrt(1/fan_in), weight before bias, layer order.  (§8f
+    kinds: BatchNorm gamma 1 / beta 0 without a draw; a residual block draws
+    for its body then its shortcut.)"""
     gen = np.random.Generator(np.random.PCG64(seed))
-    out = []
-    for layer in layers:
-        ts = []
-        for shp in param_shapes(layer):
-            bound = float(np.sqrt(1.0 / fan_in(layer)))
-            ts.append(gen.uniform(-bound, bound, size=shp).astype(F32))
-        out.append(ts)
-    return out
+    return [_init_layer(gen, layer) for layer in layers]
 
 
 def block_forward(layers, params, x, labels=None):
@@ -245,6 +328,18 @@ def block_forward(layers, params, x, labels=None):
         elif kind == "softmax_ce":
             x, probs = softmax_ce_forward(x, labels)
             cache = (probs, labels)
+        elif kind == "bn":
+            x, cache = bn_forward(x, p[0], p[1], layer[2])
+        elif kind == "gap":
+            cache = x.shape
+            x = gap_forward(x)
+        elif kind == "residual":
+            body, short = layer[1], layer[2]
+            pb, ps = _split_rows(body, p), _split_rows(short, p[len(param_shapes(("residual", body, ()))):])
+            yb, cb = block_forward(body, pb, x)
+            ys, cs = block_forward(short, ps, x) if short else (x, None)
+            x, mask = relu_forward(yb + ys)
+            cache = (cb, cs, mask, pb, ps)
         else:
             raise TypeError(kind)
         caches.append(cache)
@@ -275,6 +370,22 @@ def block_backward(layers, params, caches, gy, need_input_grad=True):
             gy = relu_backward(cache, gy)
         elif kind == "softmax_ce":
             gy = softmax_ce_backward(*cache)
+        elif kind == "bn":
+            gy, dg, db = bn_backward(cache, params[i][0], gy)
+            grads[i] = [dg, db]
+        elif kind == "gap":
+            gy = gap_backward(cache, gy)
+        elif kind == "residual":
+            body, short = layer[1], layer[2]
+            cb, cs, mask, pb, ps = cache
+            g = relu_backward(mask, gy)
+            gxb, gb = block_backward(body, pb, cb, g)
+            if short:
+                gxs, gs = block_backward(short, ps, cs, g)
+            else:
+                gxs, gs = g, []
+            gy = gxb + gxs
+            grads[i] = [t for row in gb + gs for t in row]
     return gy, grads
 
 
@@ -517,6 +628,39 @@ def alexnet_layers():
             ("flatten",), ("fc", 9216, 4096), ("relu",),
             ("fc", 4096, 4096), ("relu",), ("fc", 4096, 1000),
             ("softmax_ce",)], (3, 224, 224)
+
+
+def resnet_layers(blocks=(3, 4, 6, 3), widths=(64, 128, 256, 512), side=224, stem=64,
+                  expansion=4, classes=1000, stem_kernel=7, eps=1e-5):
+    """Post-activation bottleneck ResNet (ResNet-50 with the defaults) in the
+    tuple grammar (§8f row 4).  The reference's MaxPool2d has no padding, so
+    the stem pool is an unpadded 3x3/2 (112 -> 55; the stages then give 28,
+    14, 7).  Conv layers keep their bias (the reference's Conv2d always has
+    one)."""
+    layers = [("conv", 3, stem, stem_kernel, 2, stem_kernel // 2), ("bn", stem, eps), ("relu",),
+              ("maxpool", 3, 2)]
+    cin = stem
+    for si, (n, w) in enumerate(zip(blocks, widths)):
+        for b in range(n):
+            s = 2 if (b == 0 and si > 0) else 1
+            cout = w * expansion
+            body = (("conv", cin, w, 1, 1, 0), ("bn", w, eps), ("relu",),
+                    ("conv", w, w, 3, s, 1), ("bn", w, eps), ("relu",),
+                    ("conv", w, cout, 1, 1, 0), ("bn", cout, eps))
+            short = ((("conv", cin, cout, 1, s, 0), ("bn", cout, eps))
+                     if (s != 1 or cin != cout) else ())
+            layers.append(("residual", body, short))
+            cin = cout
+    layers += [("gap",), ("flatten",), ("fc", cin, classes), ("softmax_ce",)]
+    return layers, (3, side, side)
+
+
+def tiny_resnet_layers():
+    """Two bottleneck stages on 16x16 inputs (parity-sized, §8f row 4):
+    strided stem (space-to-depth on the GPU), a projection shortcut in each
+    stage (stride 1, then stride 2), and an identity block."""
+    return resnet_layers(blocks=(2, 1), widths=(8, 16), side=16, stem=8, expansion=2,
+                         classes=10, stem_kernel=3)
 
 
 def vgg16_layers():

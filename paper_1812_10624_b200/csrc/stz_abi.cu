@@ -18,6 +18,7 @@
 #include <string>
 
 #include "stz_fmt.cuh"
+#include "stz_norm.cuh"
 #include "stz_tma.cuh"
 #include "stz_band.cuh"
 #include "stz_peer.cuh"
@@ -1518,6 +1519,91 @@ int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t 
   relu_bwd_split_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(cb(gy), psg, cb(src), mb(gx),
                                                                      psx, n);
   return check_launch("relu_bwd_split");
+}
+
+/* ---- ResNet-trunk kinds (semantics: oracle bn_* / gap_* / residual) ---- */
+
+namespace {
+// slices per group for the BatchNorm reductions: ~4 blocks per SM in total,
+// at least 256 rows per slice
+int bn_slices(size_t grows, int G, int tiles) {
+  const long want = std::max(1L, (long)(4 * num_sms()) / std::max(1, G * tiles));
+  const long cap = std::max(1L, (long)((grows + 255) / 256));
+  return (int)std::min(want, cap);
+}
+}  // namespace
+
+int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta, const void* res,
+                size_t psr, void* y, size_t psy, double* stats, int N, int HW, int C, int C8,
+                int group, float eps, int relu, void* ws, size_t ws_bytes, void* stream) {
+  if (N <= 0 || HW <= 0 || C <= 0 || C8 < C || C8 % 8 || group <= 0 || N % group)
+    return fail(STZ_EINVAL, "bn_fwd: bad shape N=%d HW=%d C=%d C8=%d group=%d", N, HW, C, C8, group);
+  cudaStream_t st = as_stream(stream);
+  const int G = N / group, tiles = cdiv(C8 / 8, 32);
+  const size_t grows = (size_t)group * HW;
+  const int slices = bn_slices(grows, G, tiles);
+  const int rps = (int)((grows + slices - 1) / slices);
+  Carve cv(ws, ws_bytes);
+  double* part = cv.take<double>((size_t)G * slices * C8 * 2);
+  if (!part) return fail(STZ_EWORKSPACE, "bn_fwd: workspace too small");
+  bn_reduce_kernel<false><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, nullptr, 0, nullptr,
+                                                                 part, HW, C8, group, rps);
+  bn_stats_final_kernel<<<cdiv(G * C8, 128), 128, 0, st>>>(part, stats, G, slices, C8,
+                                                          (double)grows, (double)eps);
+  bn_apply_kernel<<<grid_for((size_t)N * HW * (C8 / 8)), 256, 0, st>>>(
+      cb(x), psx, gamma, beta, stats, cb(res), psr, mb(y), psy, (size_t)N * HW, HW, C, C8, group,
+      relu);
+  return check_launch("bn_fwd");
+}
+
+int stzx_bn_bwd(const void* g, size_t psg, const void* x, size_t psx, const double* stats,
+                const float* gamma, float* ggamma, float* gbeta, int accumulate, void* gx,
+                size_t psgx, int N, int HW, int C, int C8, int group, void* ws, size_t ws_bytes,
+                void* stream) {
+  if (N <= 0 || HW <= 0 || C <= 0 || C8 < C || C8 % 8 || group <= 0 || N % group)
+    return fail(STZ_EINVAL, "bn_bwd: bad shape N=%d HW=%d C=%d C8=%d group=%d", N, HW, C, C8, group);
+  cudaStream_t st = as_stream(stream);
+  const int G = N / group, tiles = cdiv(C8 / 8, 32);
+  const size_t grows = (size_t)group * HW;
+  const int slices = bn_slices(grows, G, tiles);
+  const int rps = (int)((grows + slices - 1) / slices);
+  Carve cv(ws, ws_bytes);
+  double* part = cv.take<double>((size_t)G * slices * C8 * 2);
+  double* sums = cv.take<double>((size_t)G * C8 * 2);
+  if (!part || !sums) return fail(STZ_EWORKSPACE, "bn_bwd: workspace too small");
+  bn_reduce_kernel<true><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, cb(g), psg, stats,
+                                                                part, HW, C8, group, rps);
+  bn_bwd_final_kernel<<<cdiv(C8, 128), 128, 0, st>>>(part, sums, ggamma, gbeta, G, slices, C, C8,
+                                                    accumulate);
+  if (gx)
+    bn_bwd_apply_kernel<<<grid_for((size_t)N * HW * (C8 / 8)), 256, 0, st>>>(
+        cb(g), psg, cb(x), psx, gamma, stats, sums, mb(gx), psgx, (size_t)N * HW, HW, C, C8, group);
+  return check_launch("bn_bwd");
+}
+
+int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, int C8,
+                 void* stream) {
+  if (N <= 0 || HW <= 0 || C8 <= 0 || C8 % 8) return fail(STZ_EINVAL, "gap_fwd: bad shape");
+  gap_fwd_kernel<<<grid_for((size_t)N * (C8 / 8)), 256, 0, as_stream(stream)>>>(cb(x), psx, mb(y),
+                                                                               psy, N, HW, C8);
+  return check_launch("gap_fwd");
+}
+
+int stzx_gap_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int HW, int C8,
+                 void* stream) {
+  if (N <= 0 || HW <= 0 || C8 <= 0 || C8 % 8) return fail(STZ_EINVAL, "gap_bwd: bad shape");
+  gap_bwd_kernel<<<grid_for((size_t)N * HW * (C8 / 8)), 256, 0, as_stream(stream)>>>(
+      cb(gy), psg, mb(gx), psx, N, HW, C8);
+  return check_launch("gap_bwd");
+}
+
+int stzx_add(const void* a, size_t psa, const void* b, size_t psb, void* y, size_t psy, size_t n,
+             void* stream) {
+  if (n % 8) return fail(STZ_EINVAL, "add: %zu elements is not a multiple of 8", n);
+  if (n == 0) return STZ_OK;
+  add_split_kernel<<<grid_for(n / 8), 256, 0, as_stream(stream)>>>(cb(a), psa, cb(b), psb, mb(y),
+                                                                   psy, n / 8);
+  return check_launch("add_split");
 }
 
 int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,

@@ -1,0 +1,253 @@
+// ResNet-trunk kernels on the split-plane formats:
+// training-mode BatchNorm, global average pooling and the residual add.
+//
+// The reference has none of these layer kinds (tensor_core.py:37-74); their
+// semantics are the oracle's (oracle/stanza_oracle.py bn_forward /
+// bn_backward / gap_forward / gap_backward / "residual"), all statistics and
+// per-element arithmetic in float64 with one fp32 rounding, reductions in a
+// fixed order (deterministic).  Every kernel is HBM-bound: 8 channels per
+// thread as 16-byte loads of each plane.
+//
+// BatchNorm statistics are per GROUP of `group` samples (one CONV worker's
+// batch) so that the co-located single-GPU trunk, which runs n_c workers'
+// batches as one N = n_c*K pass, normalises exactly as each worker would.
+#pragma once
+
+#include "stz_fmt.cuh"
+
+namespace stz {
+
+// Per (group, row slice, channel) float64 partial sums.
+//   forward : (sum x, sum x^2)
+//   backward: (sum g, sum g * xhat), xhat = (x - mean) * rstd
+// Block = 256 threads as L channel-chunk lanes x R row lanes (L = min(chunks
+// left in this 32-chunk tile, 32), R = 256 / L); grid (slices, groups, tiles).
+template <bool BWD>
+__global__ void __launch_bounds__(256) bn_reduce_kernel(
+    const bf16_t* __restrict__ x, size_t psx, const bf16_t* __restrict__ g, size_t psg,
+    const double* __restrict__ stats, double* __restrict__ partial, int HW, int C8, int group,
+    int rows_per_slice) {
+  __shared__ double red[256][16];
+  const int nch = C8 / 8, ct = blockIdx.z;
+  const int L = min(nch - ct * 32, 32), R = 256 / L;
+  const int t = threadIdx.x, cl = t % L, rl = t / L;
+  const int gi = blockIdx.y, slice = blockIdx.x, nslices = gridDim.x;
+  const size_t grows = (size_t)group * HW, grow0 = (size_t)gi * grows;
+  const size_t r0 = (size_t)slice * rows_per_slice;
+  const size_t r1 = min(grows, r0 + (size_t)rows_per_slice);
+  const int cc = ct * 32 + cl;
+  double s[8], q[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.0;
+  if (rl < R) {
+    double mean[8], rstd[8];
+    if (BWD) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        mean[j] = stats[((size_t)gi * C8 + cc * 8 + j) * 2];
+        rstd[j] = stats[((size_t)gi * C8 + cc * 8 + j) * 2 + 1];
+      }
+    }
+    for (size_t r = r0 + rl; r < r1; r += R) {
+      const size_t off = (grow0 + r) * C8 + (size_t)cc * 8;
+      float v[8];
+      load_split8(x + off, psx, v);
+      if (!BWD) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s[j] += (double)v[j];
+          q[j] = fma((double)v[j], (double)v[j], q[j]);
+        }
+      } else {
+        float gv[8];
+        load_split8(g + off, psg, gv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double xh = __dmul_rn(__dsub_rn((double)v[j], mean[j]), rstd[j]);
+          s[j] += (double)gv[j];
+          q[j] = fma((double)gv[j], xh, q[j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    red[t][j] = s[j];
+    red[t][8 + j] = q[j];
+  }
+  __syncthreads();
+  if (t < L * 16) {                   // (lane, quantity): fixed-order sum over row lanes
+    const int lane = t % L, jj = t / L;
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += red[r * L + lane][jj];
+    const int c = (ct * 32 + lane) * 8 + (jj & 7);
+    partial[(((size_t)gi * nslices + slice) * C8 + c) * 2 + (jj >> 3)] = acc;
+  }
+}
+
+// forward finalize: per (group, channel) mean and rstd = 1/sqrt(var + eps),
+// var = E[x^2] - mean^2 (float64; clamped at 0)
+__global__ void bn_stats_final_kernel(const double* __restrict__ partial, double* __restrict__ stats,
+                                      int G, int nslices, int C8, double m, double eps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G * C8) return;
+  const int gi = i / C8, c = i % C8;
+  double s = 0.0, q = 0.0;
+  for (int k = 0; k < nslices; ++k) {
+    s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
+    q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
+  }
+  const double mean = s / m;
+  const double var = fmax(q / m - mean * mean, 0.0);
+  stats[(size_t)i * 2] = mean;
+  stats[(size_t)i * 2 + 1] = 1.0 / sqrt(var + eps);
+}
+
+// backward finalize: per-group (sum g, sum g*xhat) for the apply pass, and the
+// parameter-gradient batch sums dgamma = sum g*xhat, dbeta = sum g over all
+// groups (written, or added in fp32 with `accumulate`)
+__global__ void bn_bwd_final_kernel(const double* __restrict__ partial, double* __restrict__ sums,
+                                    float* __restrict__ ggamma, float* __restrict__ gbeta, int G,
+                                    int nslices, int C, int C8, int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C8) return;
+  double tg = 0.0, tgx = 0.0;
+  for (int gi = 0; gi < G; ++gi) {
+    double s = 0.0, q = 0.0;
+    for (int k = 0; k < nslices; ++k) {
+      s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
+      q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
+    }
+    sums[((size_t)gi * C8 + c) * 2] = s;
+    sums[((size_t)gi * C8 + c) * 2 + 1] = q;
+    tg += s;
+    tgx += q;
+  }
+  if (c < C) {
+    ggamma[c] = accumulate ? __fadd_rn(ggamma[c], (float)tgx) : (float)tgx;
+    gbeta[c] = accumulate ? __fadd_rn(gbeta[c], (float)tg) : (float)tg;
+  }
+}
+
+// y = ((x - mean) * rstd) * gamma + beta (float64, one rounding), then
+// optionally + residual (fp32 add) and ReLU; padded channels stay 0
+__global__ void bn_apply_kernel(const bf16_t* __restrict__ x, size_t psx,
+                                const float* __restrict__ gamma, const float* __restrict__ beta,
+                                const double* __restrict__ stats, const bf16_t* __restrict__ res,
+                                size_t psr, bf16_t* __restrict__ y, size_t psy, size_t rows,
+                                int HW, int C, int C8, int group, int relu) {
+  const int nch = C8 / 8;
+  const size_t total = rows * nch, grows = (size_t)group * HW;
+  STZ_GRID_LOOP(i, total) {
+    const size_t row = i / nch;
+    const int cc = (int)(i % nch);
+    const size_t gi = row / grows;
+    const size_t off = row * C8 + (size_t)cc * 8;
+    float v[8], r[8];
+    load_split8(x + off, psx, v);
+    if (res) load_split8(res + off, psr, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = cc * 8 + j;
+      float o = 0.f;
+      if (c < C) {
+        const double mean = stats[(gi * C8 + c) * 2], rstd = stats[(gi * C8 + c) * 2 + 1];
+        const double xh = __dmul_rn(__dsub_rn((double)v[j], mean), rstd);
+        o = (float)__dadd_rn(__dmul_rn(xh, (double)gamma[c]), (double)beta[c]);
+        if (res) o = __fadd_rn(o, r[j]);
+        if (relu) o = o > 0.f ? o : 0.f;
+      }
+      v[j] = o;
+    }
+    store_split8(y + off, psy, v);
+  }
+}
+
+// gx = ((gamma * rstd) / m) * ((m * g - sum g) - xhat * sum(g * xhat))
+__global__ void bn_bwd_apply_kernel(const bf16_t* __restrict__ g, size_t psg,
+                                    const bf16_t* __restrict__ x, size_t psx,
+                                    const float* __restrict__ gamma,
+                                    const double* __restrict__ stats,
+                                    const double* __restrict__ sums, bf16_t* __restrict__ gx,
+                                    size_t psgx, size_t rows, int HW, int C, int C8, int group) {
+  const int nch = C8 / 8;
+  const size_t total = rows * nch, grows = (size_t)group * HW;
+  const double m = (double)grows;
+  STZ_GRID_LOOP(i, total) {
+    const size_t row = i / nch;
+    const int cc = (int)(i % nch);
+    const size_t gi = row / grows;
+    const size_t off = row * C8 + (size_t)cc * 8;
+    float v[8], gv[8];
+    load_split8(x + off, psx, v);
+    load_split8(g + off, psg, gv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = cc * 8 + j;
+      float o = 0.f;
+      if (c < C) {
+        const size_t k = (gi * C8 + c) * 2;
+        const double mean = stats[k], rstd = stats[k + 1], sg = sums[k], sgx = sums[k + 1];
+        const double xh = __dmul_rn(__dsub_rn((double)v[j], mean), rstd);
+        const double coef = __ddiv_rn(__dmul_rn((double)gamma[c], rstd), m);
+        const double inner = __dsub_rn(__dsub_rn(__dmul_rn(m, (double)gv[j]), sg), __dmul_rn(xh, sgx));
+        o = (float)__dmul_rn(coef, inner);
+      }
+      v[j] = o;
+    }
+    store_split8(gx + off, psgx, v);
+  }
+}
+
+// global average pool: NHWC [N][HW][C8] -> rows [N][C8] (= NHWC [N][1][1][C8])
+__global__ void gap_fwd_kernel(const bf16_t* __restrict__ x, size_t psx, bf16_t* __restrict__ y,
+                               size_t psy, int N, int HW, int C8) {
+  const int nch = C8 / 8;
+  STZ_GRID_LOOP(i, (size_t)N * nch) {
+    const size_t n = i / nch;
+    const int cc = (int)(i % nch);
+    double s[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = 0.0;
+    for (int p = 0; p < HW; ++p) {
+      float v[8];
+      load_split8(x + (n * HW + p) * C8 + (size_t)cc * 8, psx, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] += (double)v[j];
+    }
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (float)__ddiv_rn(s[j], (double)HW);
+    store_split8(y + n * C8 + (size_t)cc * 8, psy, o);
+  }
+}
+
+__global__ void gap_bwd_kernel(const bf16_t* __restrict__ gy, size_t psg, bf16_t* __restrict__ gx,
+                               size_t psx, int N, int HW, int C8) {
+  const int nch = C8 / 8;
+  STZ_GRID_LOOP(i, (size_t)N * HW * nch) {
+    const size_t pix = i / nch, n = pix / HW;
+    const int cc = (int)(i % nch);
+    float v[8];
+    load_split8(gy + n * C8 + (size_t)cc * 8, psg, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (float)__ddiv_rn((double)v[j], (double)HW);
+    store_split8(gx + pix * C8 + (size_t)cc * 8, psx, v);
+  }
+}
+
+// y = a + b (fp32 RN), n elements (multiple of 8)
+__global__ void add_split_kernel(const bf16_t* __restrict__ a, size_t psa,
+                                 const bf16_t* __restrict__ b, size_t psb, bf16_t* __restrict__ y,
+                                 size_t psy, size_t n8) {
+  STZ_GRID_LOOP(i, n8) {
+    float va[8], vb[8];
+    load_split8(a + i * 8, psa, va);
+    load_split8(b + i * 8, psb, vb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) va[j] = __fadd_rn(va[j], vb[j]);
+    store_split8(y + i * 8, psy, va);
+  }
+}
+
+}  // namespace stz

@@ -20,6 +20,13 @@ A ``BlockEngine`` owns, for a fixed batch size:
   directly; SoftmaxCE emits loss and dlogits in one pass; the first layer of
   the CONV block skips its input gradient (stanza_runtime.py:366-369 discards
   it).
+
+The ResNet-trunk kinds of SURVEY.md §8f row 4 (not in the reference):
+BatchNorm2d (statistics per ``group`` of samples = one CONV worker's batch,
+following ReLU fused into its apply pass), GlobalAvgPool2d (a following
+Flatten is a view), and Residual, run by two child engines (body, shortcut)
+whose parameter / velocity / gradient views live inside this engine's flat
+vectors; the residual add + ReLU is fused into the body's last BatchNorm.
 """
 
 from __future__ import annotations
@@ -30,9 +37,9 @@ import numpy as np
 import torch
 
 from . import _lib
-from .tensor_core import (Conv2d, Flatten, FullyConnected, MaxPool2d, ReLU,
-                          ShapeMismatch, SoftmaxCrossEntropy, inv_batch, out_shape,
-                          param_shapes, ptr, stream_of, workspace)
+from .tensor_core import (BatchNorm2d, Conv2d, Flatten, FullyConnected, GlobalAvgPool2d,
+                          MaxPool2d, ReLU, Residual, ShapeMismatch, SoftmaxCrossEntropy,
+                          inv_batch, out_shape, param_shapes, ptr, stream_of, workspace)
 
 _ALIGN = 4  # floats: keeps every fp32 per-tensor view 16-byte aligned
 
@@ -91,7 +98,7 @@ class Split:
 
 @dataclass
 class _Op:
-    kind: str                 # conv | fc | maxpool | relu | flatten | softmax_ce
+    kind: str                 # conv | fc | maxpool | relu | flatten | softmax_ce | bn | gap | residual
     layer: object
     index: int
     in_shape: tuple           # per-sample logical shape
@@ -109,18 +116,29 @@ class BlockEngine:
 
     def __init__(self, layers, in_shape, batch: int, device, params=None, velocities=None,
                  need_input_grad: bool = True, shared=None, input_grad_buffer=None,
-                 allocate: bool = True):
+                 allocate: bool = True, group: int | None = None, flats=None, tag: str = ""):
         self.layers = tuple(layers)
         self.in_shape = tuple(in_shape)
         self.batch = int(batch)
         self.device = torch.device(device)
         self.need_input_grad = need_input_grad
+        # BatchNorm statistics group (samples): one CONV worker's batch
+        self.group = self.batch if group is None else int(group)
+        if self.batch % self.group:
+            raise ShapeMismatch(f"batch {self.batch} is not a multiple of the group {self.group}")
+        self.tag = tag
         self._build_plan()
         self._layout_params()
+        self.children: dict = {}
         if not allocate:
             return
         dev, f32 = self.device, torch.float32
-        if shared is not None:                   # FC replicas on one GPU share (w, v, planes)
+        if flats is not None:                    # a residual block's child: views of the parent
+            base, (pf, vf, gf) = flats
+            self.params_flat, self.vel_flat = pf[base:base + self.total], vf[base:base + self.total]
+            self.grad_flat = gf[base:base + self.total]
+            self.wplanes = self._alloc_weight_planes()
+        elif shared is not None:                   # FC replicas on one GPU share (w, v, planes)
             if shared.total != self.total:
                 raise ShapeMismatch("shared engine has a different parameter layout")
             self.params_flat, self.vel_flat = shared.params_flat, shared.vel_flat
@@ -129,10 +147,12 @@ class BlockEngine:
             self.params_flat = torch.zeros(self.total, dtype=f32, device=dev)
             self.vel_flat = torch.zeros(self.total, dtype=f32, device=dev)
             self.wplanes = self._alloc_weight_planes()
-        self.grad_flat = torch.zeros(self.total, dtype=f32, device=dev)
+        if flats is None:
+            self.grad_flat = torch.zeros(self.total, dtype=f32, device=dev)
         self.params = self._views(self.params_flat)
         self.velocity = self._views(self.vel_flat)
         self.grads = self._views(self.grad_flat)
+        self._make_children()
         if shared is None and params is not None:
             self.load(params, velocities)
         self._alloc_activations(input_grad_buffer)
@@ -143,16 +163,17 @@ class BlockEngine:
         ops, shape = [], self.in_shape
         for i, layer in enumerate(self.layers):
             kind = {Conv2d: "conv", FullyConnected: "fc", MaxPool2d: "maxpool", ReLU: "relu",
-                    Flatten: "flatten", SoftmaxCrossEntropy: "softmax_ce"}[type(layer)]
+                    Flatten: "flatten", SoftmaxCrossEntropy: "softmax_ce", BatchNorm2d: "bn",
+                    GlobalAvgPool2d: "gap", Residual: "residual"}[type(layer)]
             nxt = out_shape(layer, shape)
             ops.append(_Op(kind, layer, i, shape, nxt))
             shape = nxt
         self.out_shape = shape
         for i, op in enumerate(ops):
-            if op.kind == "relu" and i > 0 and ops[i - 1].kind in ("conv", "fc"):
+            if op.kind == "relu" and i > 0 and ops[i - 1].kind in ("conv", "fc", "bn"):
                 ops[i - 1].fused_relu = True
-            if op.kind == "flatten" and i > 0 and ops[i - 1].kind == "maxpool":
-                ops[i - 1].flat_out = True
+            if op.kind == "flatten" and i > 0 and ops[i - 1].kind in ("maxpool", "gap"):
+                ops[i - 1].flat_out = True      # gap: (C,1,1) NHWC is the flat row already
         for i, op in enumerate(ops):
             if op.kind != "relu":
                 continue
@@ -189,6 +210,38 @@ class BlockEngine:
 
     def _views(self, flat):
         return [[flat[o:o + n].view(shp) for (o, shp, n) in row] for row in self.slots]
+
+    def _make_children(self):
+        """Body / shortcut engines of each Residual op, their parameters views
+        of this engine's flat vectors at the residual row's offset."""
+        flats = (self.params_flat, self.vel_flat, self.grad_flat)
+        for i, op in enumerate(self.ops):
+            if op.kind != "residual":
+                continue
+            base = self.slots[i][0][0] if self.slots[i] else 0
+            kids = []
+            for part, name in ((op.layer.body, "b"), (op.layer.shortcut, "s")):
+                if not part:
+                    kids.append(None)
+                    continue
+                eng = BlockEngine(part, op.in_shape, self.batch, self.device,
+                                  need_input_grad=True, group=self.group, flats=(base, flats),
+                                  tag=f"{self.tag}r{i}{name}.")
+                base += eng.total if eng.param_count else 0
+                kids.append(eng)
+            self.children[i] = tuple(kids)
+
+    def has_bn(self) -> bool:
+        """Whether the block normalises over its batch (BatchNorm, directly or
+        inside a residual block): passes must cover whole sample groups."""
+        def walk(layers):
+            for l in layers:
+                if isinstance(l, BatchNorm2d):
+                    return True
+                if isinstance(l, Residual) and walk(l.body + l.shortcut):
+                    return True
+            return False
+        return walk(self.layers)
 
     def _alloc_weight_planes(self):
         dev = self.device
@@ -231,11 +284,22 @@ class BlockEngine:
         self.dlogits = None
         self.xin = None   # packed block input, allocated on first pack_input()
         self._gout = None  # per-op output-gradient buffers of the last backward
+        self.bnstats: dict = {}   # bn op -> float64 [groups][C8][2] (mean, rstd)
+        self.rgp: dict = {}       # residual op -> ReLU-masked output gradient
         for i, op in enumerate(self.ops):
             if op.kind == "relu" and i > 0 and self.ops[i - 1].fused_relu:
                 continue
+            if op.kind == "residual":             # the body's last BatchNorm writes it
+                body, _ = self.children[i]
+                self.acts[i] = body._act(len(body.ops) - 1)
+                self.rgp[i] = self._split_for(op.out_shape, b)
+                continue
+            if op.kind == "bn":
+                c = op.in_shape[0]
+                self.bnstats[i] = torch.zeros((b // self.group, rup8(c), 2), dtype=torch.float64,
+                                              device=dev)
             if op.kind == "flatten":
-                src_flat = i > 0 and self.ops[i - 1].kind == "maxpool" and self.ops[i - 1].flat_out
+                src_flat = i > 0 and self.ops[i - 1].flat_out
                 if not src_flat and len(op.in_shape) == 3:
                     self.acts[i] = self._split_for(op.out_shape, b)   # relayout target
                 continue
@@ -260,7 +324,7 @@ class BlockEngine:
             if op.kind == "relu" and op.relu_bwd_fused:
                 continue
             if op.kind == "flatten":
-                src_flat = i > 0 and self.ops[i - 1].kind == "maxpool" and self.ops[i - 1].flat_out
+                src_flat = i > 0 and self.ops[i - 1].flat_out
                 if src_flat or len(op.in_shape) != 3:
                     continue
             if i == 0:
@@ -303,6 +367,10 @@ class BlockEngine:
             else:
                 _lib.call("stzx_pack_rows", ptr(w), ptr(a), a[0].numel(), l.in_dim, l.out_dim,
                           rup8(l.out_dim), st)
+        for kids in self.children.values():
+            for k in kids:
+                if k is not None:
+                    k.pack_weights()
 
     def state_numpy(self):
         """(params, velocities) as nested fp32 numpy arrays, reference layout."""
@@ -347,6 +415,11 @@ class BlockEngine:
             return self._act(i - 1)
         return None
 
+    def _check_groups(self, r0, r1):
+        if r0 % self.group or (r1 - r0) % self.group:
+            raise ShapeMismatch(f"BatchNorm needs whole sample groups of {self.group}; "
+                                f"got rows [{r0}, {r1})")
+
     def _input(self, i):
         return self._x if i == 0 else self._act(i - 1)
 
@@ -384,13 +457,16 @@ class BlockEngine:
         return self.xin
 
     def forward(self, x, labels: torch.Tensor | None = None,
-                loss_out: torch.Tensor | None = None, rows=None, sum_loss: bool = True):
+                loss_out: torch.Tensor | None = None, rows=None, sum_loss: bool = True,
+                residual: "Split | None" = None):
         """Run the block.  ``x`` is a fp32 batch in the reference layout or an
         already-packed Split (e.g. the CONV block's output rows), always
         full-batch shaped; ``rows = (r0, r1)`` runs only samples [r0, r1) (a
         micro-batch; ``labels`` is full-batch too).  Returns the output Split
         of those rows (per-sample fp32 losses for a loss block).  The float64
-        loss sum goes to ``loss_sum`` or is ADDED into ``loss_out``."""
+        loss sum goes to ``loss_sum`` or is ADDED into ``loss_out``.
+        ``residual`` (a residual block's body): full-batch Split added to the
+        last op's (a BatchNorm's) output before a ReLU."""
         r0, r1, V = self._rows(rows)
         if isinstance(x, torch.Tensor):
             x = self.pack_input(x, rows)
@@ -412,7 +488,7 @@ class BlockEngine:
                 _lib.call("stzx_conv_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
                           ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w, l.out_ch,
                           y.width, k, cs, pd, int(op.fused_relu), ptr(ws),
-                          ws.numel(), st, flops=self.op_flops(i, b), tag=f"conv{i}_fwd")
+                          ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_fwd")
             elif op.kind == "fc":
                 wp, _ = self.wplanes[i]
                 if self.acts[i] is not None:
@@ -420,13 +496,13 @@ class BlockEngine:
                     _lib.call("stzx_fc_fwd", xin.ptr(), xin.ps, ptr(wp), wp[0].numel(),
                               ptr(self.params[i][1]), y.ptr(), y.ps, None, b, l.in_dim,
                               xin.width, l.out_dim, y.width, int(op.fused_relu), ptr(ws),
-                              ws.numel(), st, flops=self.op_flops(i, b), tag=f"fc{i}_fwd")
+                              ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}fc{i}_fwd")
                 else:
                     _lib.call("stzx_fc_fwd", xin.ptr(), xin.ps, ptr(wp), wp[0].numel(),
                               ptr(self.params[i][1]), None, 0, ptr(self.logits[r0:r1]), b,
                               l.in_dim, xin.width, l.out_dim, rup8(l.out_dim), int(op.fused_relu),
                               ptr(ws), ws.numel(), st, flops=self.op_flops(i, b),
-                              tag=f"fc{i}_fwd")
+                              tag=f"{self.tag}fc{i}_fwd")
             elif op.kind == "maxpool":
                 c, h, w = op.in_shape
                 y = V(self.acts[i])
@@ -444,6 +520,30 @@ class BlockEngine:
                     y = V(self.acts[i])
                     _lib.call("stzx_nhwc_to_flat", xin.ptr(), xin.ps, y.ptr(), y.ps, b, c, h, w,
                               xin.width, y.width, st)
+            elif op.kind == "bn":
+                self._check_groups(r0, r1)
+                c, h, w = op.in_shape
+                y = V(self.acts[i])
+                last = i == len(self.ops) - 1 and residual is not None
+                res = V(residual) if last else None
+                _lib.call("stzx_bn_fwd", xin.ptr(), xin.ps, ptr(self.params[i][0]),
+                          ptr(self.params[i][1]), None if res is None else res.ptr(),
+                          0 if res is None else res.ps, y.ptr(), y.ps,
+                          ptr(self.bnstats[i][r0 // self.group:]), b, h * w, c, y.width,
+                          self.group, float(l.eps), int(op.fused_relu or last), ptr(ws),
+                          ws.numel(), st)
+            elif op.kind == "gap":
+                c, h, w = op.in_shape
+                y = V(self.acts[i])
+                _lib.call("stzx_gap_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, b, h * w, xin.width, st)
+            elif op.kind == "residual":
+                body, short = self.children[i]
+                x_full = self._input(i)
+                s_full = x_full
+                if short is not None:
+                    short.forward(x_full, rows=rows)
+                    s_full = short._act(len(short.ops) - 1)
+                body.forward(x_full, rows=rows, residual=s_full)
             elif op.kind == "softmax_ce":
                 if labels is None:
                     raise ValueError("SoftmaxCrossEntropy needs labels")
@@ -488,6 +588,10 @@ class BlockEngine:
             for i, op in enumerate(self.ops):
                 if op.kind in ("conv", "fc"):
                     self._wgrad(i, V(self._input(i)), V(self._gout[i]), b, acc, ws, st)
+                elif op.kind == "residual":
+                    for k in self.children[i]:
+                        if k is not None:
+                            k.backward(rows=rows, accumulate=accumulate, phase="wgrad")
             return None
         gout = [None] * len(self.ops)   # full-batch output-gradient buffer per op
         g_full = gy
@@ -516,6 +620,37 @@ class BlockEngine:
                     _lib.call("stzx_relu_bwd", g.ptr(), g.ps, src.ptr(), out.ptr(), out.ps,
                               b * g.row_elems, st)
                     g_full = self.gin[i]
+            elif op.kind == "bn":
+                # dgamma / dbeta come out of the same reduction as the input
+                # gradient, so they are produced in the "dgrad" pass
+                self._check_groups(r0, r1)
+                c, h, w = op.in_shape
+                out = None if op.skip_dgrad else V(self.gin[i])
+                _lib.call("stzx_bn_bwd", g.ptr(), g.ps, xin.ptr(), xin.ps,
+                          ptr(self.bnstats[i][r0 // self.group:]), ptr(self.params[i][0]),
+                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc,
+                          None if out is None else out.ptr(), 0 if out is None else out.ps,
+                          b, h * w, c, xin.width, self.group, ptr(ws), ws.numel(), st)
+                g_full = None if out is None else self.gin[i]
+            elif op.kind == "gap":
+                c, h, w = op.in_shape
+                out = V(self.gin[i])
+                _lib.call("stzx_gap_bwd", g.ptr(), g.ps, out.ptr(), out.ps, b, h * w, out.width,
+                          st)
+                g_full = self.gin[i]
+            elif op.kind == "residual":
+                body, short = self.children[i]
+                gp = V(self.rgp[i])
+                z = V(self.acts[i])
+                _lib.call("stzx_relu_bwd", g.ptr(), g.ps, z.ptr(), gp.ptr(), gp.ps,
+                          b * g.row_elems, st)
+                gb = body.backward(self.rgp[i], rows=rows, accumulate=accumulate, phase=phase)
+                gs = short.backward(self.rgp[i], rows=rows, accumulate=accumulate, phase=phase) \
+                    if short is not None else gp
+                out = V(self.gin[i])
+                _lib.call("stzx_add", gb.ptr(), gb.ps, gs.ptr(), gs.ps, out.ptr(), out.ps,
+                          b * out.row_elems, st)
+                g_full = self.gin[i]
             elif op.kind == "maxpool":
                 if op.skip_dgrad:
                     g_full = None
@@ -539,12 +674,12 @@ class BlockEngine:
                     _lib.call("stzx_conv_dgrad", g.ptr(), g.ps, ptr(wd), wd[0].numel(),
                               out.ptr(), out.ps, mptr, b, c, out.width, h, w, g.width, l.kernel,
                               l.stride, l.padding, ptr(ws), ws.numel(), st,
-                              flops=self.op_flops(i, b), tag=f"conv{i}_dgrad")
+                              flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_dgrad")
                 else:
                     wp, _ = self.wplanes[i]
                     _lib.call("stzx_fc_dgrad", g.ptr(), g.ps, ptr(wp), wp[0].numel(), out.ptr(),
                               out.ps, mptr, b, l.in_dim, out.width, g.width, ptr(ws),
-                              ws.numel(), st, flops=self.op_flops(i, b), tag=f"fc{i}_dgrad")
+                              ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}fc{i}_dgrad")
                 g_full = self.gin[i]
         self._gout = gout
         return V(g_full)
@@ -567,18 +702,18 @@ class BlockEngine:
             _lib.call("stzx_conv_wgrad_s2d", xin.ptr(), xin.ps, g.ptr(), g.ps,
                       ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_ch, cs8,
                       hs, ws_, l.out_ch, g.width, l.kernel, l.stride, ptr(ws), ws.numel(), st,
-                      flops=self.op_flops(i, b), tag=f"conv{i}_wgrad")
+                      flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         elif op.kind == "conv":
             c, h, w = op.in_shape
             _lib.call("stzx_conv_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
                       ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, c, xin.width, h,
                       w, l.out_ch, g.width, l.kernel, l.stride, l.padding, ptr(ws),
-                      ws.numel(), st, flops=self.op_flops(i, b), tag=f"conv{i}_wgrad")
+                      ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         else:
             _lib.call("stzx_fc_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
                       ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_dim,
                       xin.width, l.out_dim, g.width, ptr(ws), ws.numel(), st,
-                      flops=self.op_flops(i, b), tag=f"fc{i}_wgrad")
+                      flops=self.op_flops(i, b), tag=f"{self.tag}fc{i}_wgrad")
 
     def fused_pack_ranges(self):
         """(ctypes stz_plane_range array, count, layer indices): the FC weights,

@@ -131,6 +131,14 @@ class StanzaCluster:
         # micro-batch pipelining of CONV fwd -> gather -> FC -> scatter -> CONV bwd
         # (one process per GPU only).  Gradient sums are
         # unchanged up to fp32 summation order.
+        from .engine import BlockEngine as _BE
+        has_bn = (not spec.is_profile) and _BE(self.partition.conv_block, spec.input_shape, 1,
+                                                "cpu", allocate=False).has_bn()
+        if has_bn and micro_batches is not None and micro_batches > 1:
+            raise ConfigError("BatchNorm normalises over each CONV worker's whole batch: "
+                              "micro_batches must be 1")
+        if micro_batches is None and has_bn:
+            micro_batches = 1
         if micro_batches is None:
             # measured (AlexNet K=128, images/s): 1:1 29.3k / 30.1k / 26.6k and
             # 3:1 77.3k / 85.8k / 78.0k at 1 / 2 / 4 micro-batches
@@ -203,7 +211,7 @@ class StanzaCluster:
             self.labels = torch.zeros(nk, dtype=torch.int32, device=dev)
             self.gboundary = Split.alloc("rows", (nk, a8), a, dev)
             self.conv = BlockEngine(conv_block, in_shape, nk, dev, full0[:cut], vel0[:cut],
-                                    need_input_grad=False)
+                                    need_input_grad=False, group=k)
             for j in range(n_fc):
                 lo, hi = group_rows(self.conv_to_fc, j)
                 eng = BlockEngine(fc_block, (a,), (hi - lo) * k, dev,
@@ -220,7 +228,7 @@ class StanzaCluster:
                 self.labels = torch.zeros(k, dtype=torch.int32, device=dev)
                 self.gboundary = Split.alloc("rows", (k, a8), a, dev)
                 self.conv = BlockEngine(conv_block, in_shape, k, dev, full0[:cut], vel0[:cut],
-                                        need_input_grad=False)
+                                        need_input_grad=False, group=k)
             else:
                 self.x = None
                 self.gboundary = None

@@ -71,19 +71,53 @@ class SoftmaxCrossEntropy:
     pass
 
 
-LayerKind = Union[Conv2d, MaxPool2d, Flatten, FullyConnected, ReLU, SoftmaxCrossEntropy]
+# -- ResNet-trunk kinds.  The reference has none of these
+# (tensor_core.py:37-74 stops at SoftmaxCrossEntropy); their semantics are
+# defined by oracle/stanza_oracle.py (bn_forward / gap_forward / residual) and
+# their parity is unpinned.  They run only through the block engine.
+
+@dataclass(frozen=True)
+class BatchNorm2d:
+    """Training-mode batch normalisation over (N, H, W) of each CONV worker's
+    batch; gamma / beta [C] initialised to 1 / 0 without an RNG draw."""
+    channels: int
+    eps: float = 1e-5
+
+
+@dataclass(frozen=True)
+class GlobalAvgPool2d:
+    """(C, H, W) -> (C, 1, 1)."""
+
+
+@dataclass(frozen=True)
+class Residual:
+    """relu(body(x) + shortcut(x)); an empty shortcut is the identity.  Its
+    parameter row is the body's tensors then the shortcut's."""
+    body: tuple
+    shortcut: tuple = ()
+
+
+LayerKind = Union[Conv2d, MaxPool2d, Flatten, FullyConnected, ReLU, SoftmaxCrossEntropy,
+                  BatchNorm2d, GlobalAvgPool2d, Residual]
 
 
 def has_params(layer) -> bool:
-    return isinstance(layer, (Conv2d, FullyConnected))
+    if isinstance(layer, Residual):
+        return bool(param_shapes(layer))
+    return isinstance(layer, (Conv2d, FullyConnected, BatchNorm2d))
 
 
 def param_shapes(layer) -> list[tuple[int, ...]]:
-    """Weight then bias: conv [O,C,k,k]+[O], FC [in,out]+[out] (tensor_core.py:81-88)."""
+    """Weight then bias: conv [O,C,k,k]+[O], FC [in,out]+[out] (tensor_core.py:81-88);
+    BatchNorm gamma+beta [C]; a residual block its sub-layers' in order."""
     if isinstance(layer, Conv2d):
         return [(layer.out_ch, layer.in_ch, layer.kernel, layer.kernel), (layer.out_ch,)]
     if isinstance(layer, FullyConnected):
         return [(layer.in_dim, layer.out_dim), (layer.out_dim,)]
+    if isinstance(layer, BatchNorm2d):
+        return [(layer.channels,), (layer.channels,)]
+    if isinstance(layer, Residual):
+        return [s for l in layer.body + layer.shortcut for s in param_shapes(l)]
     return []
 
 
@@ -131,6 +165,26 @@ def out_shape(layer, in_shape: tuple[int, ...]) -> tuple[int, ...]:
         if len(in_shape) != 1:
             raise ShapeMismatch(f"SoftmaxCrossEntropy expects logits (C,), got {in_shape}")
         return ()
+    if isinstance(layer, BatchNorm2d):
+        if len(in_shape) != 3 or in_shape[0] != layer.channels:
+            raise ShapeMismatch(f"BatchNorm2d expects ({layer.channels}, H, W), got {in_shape}")
+        return in_shape
+    if isinstance(layer, GlobalAvgPool2d):
+        if len(in_shape) != 3:
+            raise ShapeMismatch(f"GlobalAvgPool2d expects (C, H, W), got {in_shape}")
+        return (in_shape[0], 1, 1)
+    if isinstance(layer, Residual):
+        if not layer.body:
+            raise ShapeMismatch("Residual needs a non-empty body")
+        shape = in_shape
+        for l in layer.body:
+            shape = out_shape(l, shape)
+        short = in_shape
+        for l in layer.shortcut:
+            short = out_shape(l, short)
+        if shape != short:
+            raise ShapeMismatch(f"Residual body gives {shape}, shortcut gives {short}")
+        return shape
     raise TypeError(f"unknown layer kind {layer!r}")
 
 
@@ -148,6 +202,13 @@ def as_tuple(layer) -> tuple:
         return ("relu",)
     if isinstance(layer, SoftmaxCrossEntropy):
         return ("softmax_ce",)
+    if isinstance(layer, BatchNorm2d):
+        return ("bn", layer.channels, layer.eps)
+    if isinstance(layer, GlobalAvgPool2d):
+        return ("gap",)
+    if isinstance(layer, Residual):
+        return ("residual", tuple(as_tuple(l) for l in layer.body),
+                tuple(as_tuple(l) for l in layer.shortcut))
     raise TypeError(f"unknown layer kind {layer!r}")
 
 
@@ -329,12 +390,16 @@ def seeded_init(layers, seed: int) -> list[list[np.ndarray]]:
     PCG64(seed) stream, U[-s, s] with s = sqrt(1/fan_in), weight then bias,
     layer order (tensor_core.py:332-346).  Upload with ``to_device``."""
     gen = np.random.Generator(np.random.PCG64(seed))
-    out = []
-    for layer in layers:
-        bound = float(np.sqrt(1.0 / fan_in(layer))) if has_params(layer) else 0.0
-        out.append([gen.uniform(-bound, bound, size=s).astype(FLOAT)
-                    for s in param_shapes(layer)])
-    return out
+    return [_init_layer(gen, layer) for layer in layers]
+
+
+def _init_layer(gen, layer) -> list[np.ndarray]:
+    if isinstance(layer, BatchNorm2d):      # §8f kinds: no draw for gamma / beta
+        return [np.ones(layer.channels, FLOAT), np.zeros(layer.channels, FLOAT)]
+    if isinstance(layer, Residual):
+        return [t for l in layer.body + layer.shortcut for t in _init_layer(gen, l)]
+    bound = float(np.sqrt(1.0 / fan_in(layer))) if has_params(layer) else 0.0
+    return [gen.uniform(-bound, bound, size=s).astype(FLOAT) for s in param_shapes(layer)]
 
 
 def to_device(nested, device) -> list[list[torch.Tensor]]:
