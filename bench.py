@@ -219,13 +219,13 @@ class CallTimer:
         self.records = []
 
     @contextmanager
-    def __call__(self, name, args, flops=0.0, tag=None):
+    def __call__(self, name, args, flops=0.0, tag=None, nbytes=0.0):
         t = self.torch
         e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
         e0.record()
         yield
         e1.record()
-        self.records.append(((tag or name, float(flops)), e0, e1))
+        self.records.append(((tag or name, float(flops), float(nbytes)), e0, e1))
 
     def table(self):
         self.torch.cuda.synchronize()
@@ -278,7 +278,8 @@ def main():
     dev = torch.device("cuda", local)
     lib = _lib.load()
     n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
-    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64}.get(args.model, 4)
+    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32}.get(
+        args.model, 4)
     spec = builtin_model(args.model, k)
 
     comm = None
@@ -470,18 +471,31 @@ def main():
         if tot > top[0]:
             top_key, top = key, (tot, cnt)
     fl = top_key[1] if top_key else 0.0
+    nb = top_key[2] if top_key else 0.0
     avg_ms = top[0] / max(top[1], 1)
     achieved = fl / (avg_ms / 1e3) / 1e12 if avg_ms > 0 and fl > 0 else 0.0
+    hbm_bound = fl == 0.0 and nb > 0.0      # a memory-bound kernel (BatchNorm, pool, ...)
+    achieved_gbs = nb / (avg_ms / 1e3) / 1e9 if avg_ms > 0 and nb > 0 else 0.0
     kernel_key = f"{args.model}:{top_key[0]}" if top_key else None
     step_ms_sum = sum(tot for tot, _ in calls.values())
     fc_fl = sum(kk[1] * c for kk, (_, c) in calls.items() if kk[0].startswith("fc"))
     fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("fc"))
     per_call = {f"{kk[0]}": {"ms": tot / max(c, 1), "n": c, "total_ms": tot,
                              "tflops": (kk[1] / (tot / max(c, 1) / 1e3) / 1e12)
-                             if kk[1] and tot else None}
+                             if kk[1] and tot else None,
+                             "GBps": (kk[2] / (tot / max(c, 1) / 1e3) / 1e9)
+                             if kk[2] and tot else None}
                 for kk, (tot, c) in sorted(calls.items(), key=lambda kv: -kv[1][0])}
     fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None
     roofline = {
+        "bound": "hbm", "kernel": kernel_key, "achieved": achieved_gbs, "peak": hbm_peak,
+        "unit": "GB/s", "frac": achieved_gbs / hbm_peak if hbm_peak else None,
+        "traffic": committed_traffic(kernel_key), "peak_source": peak_src,
+        "note": ("achieved = algorithmic HBM bytes of that ABI call (split planes, 6 B per "
+                 "element per pass) / its mean CUDA-event duration"),
+        "share_of_step": top[0] / step_ms_sum if step_ms_sum else None,
+        "calls": per_call,
+    } if hbm_bound else {
         "bound": "tensor", "kernel": kernel_key, "achieved": achieved, "peak": bf16_peak,
         "unit": "TFLOP/s", "frac": achieved / bf16_peak if bf16_peak else None,
         "traffic": committed_traffic(kernel_key),

@@ -162,12 +162,14 @@ def _sync_check(name: str) -> int:
     return 0
 
 
-def call(name: str, *args, flops: float = 0.0, tag: str | None = None) -> None:
+def call(name: str, *args, flops: float = 0.0, tag: str | None = None,
+         nbytes: float = 0.0) -> None:
     """Invoke an ABI function and raise on a non-zero status.  ``flops`` /
-    ``tag`` (algorithmic FLOPs, layer label) are only seen by PROFILE_HOOK."""
+    ``nbytes`` / ``tag`` (algorithmic FLOPs or HBM bytes, layer label) are
+    only seen by PROFILE_HOOK."""
     lib = load()
     if PROFILE_HOOK is not None:
-        with PROFILE_HOOK(name, args, flops, tag):
+        with PROFILE_HOOK(name, args, flops, tag, nbytes=nbytes):
             rc = getattr(lib, name)(*args)
     else:
         rc = getattr(lib, name)(*args)

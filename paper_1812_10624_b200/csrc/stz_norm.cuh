@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(256) bn_reduce_kernel(
     red[t][8 + j] = q[j];
   }
   __syncthreads();
-  if (t < L * 16) {                   // (lane, quantity): fixed-order sum over row lanes
-    const int lane = t % L, jj = t / L;
+  for (int idx = t; idx < L * 16; idx += 256) {   // (lane, quantity): fixed-order sum over row lanes
+    const int lane = idx % L, jj = idx / L;
     double acc = 0.0;
     for (int r = 0; r < R; ++r) acc += red[r * L + lane][jj];
     const int c = (ct * 32 + lane) * 8 + (jj & 7);

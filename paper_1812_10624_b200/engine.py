@@ -312,7 +312,7 @@ class BlockEngine:
                 self.logits = torch.zeros((b, op.out_shape[0]), dtype=torch.float32, device=dev)
                 continue
             shape = op.out_shape
-            if op.kind == "maxpool" and op.flat_out:
+            if op.kind in ("maxpool", "gap") and op.flat_out:
                 shape = (int(np.prod(op.out_shape)),)
             self.acts[i] = self._split_for(shape, b)
             if op.kind == "maxpool":
@@ -531,11 +531,13 @@ class BlockEngine:
                           0 if res is None else res.ps, y.ptr(), y.ps,
                           ptr(self.bnstats[i][r0 // self.group:]), b, h * w, c, y.width,
                           self.group, float(l.eps), int(op.fused_relu or last), ptr(ws),
-                          ws.numel(), st)
+                          ws.numel(), st, tag=f"{self.tag}bn{i}_fwd",
+                          nbytes=6.0 * (3 + (res is not None)) * b * xin.row_elems)
             elif op.kind == "gap":
                 c, h, w = op.in_shape
                 y = V(self.acts[i])
-                _lib.call("stzx_gap_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, b, h * w, xin.width, st)
+                _lib.call("stzx_gap_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, b, h * w, xin.width, st,
+                          tag=f"{self.tag}gap{i}_fwd", nbytes=6.0 * b * (xin.row_elems + y.width))
             elif op.kind == "residual":
                 body, short = self.children[i]
                 x_full = self._input(i)
@@ -630,26 +632,30 @@ class BlockEngine:
                           ptr(self.bnstats[i][r0 // self.group:]), ptr(self.params[i][0]),
                           ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc,
                           None if out is None else out.ptr(), 0 if out is None else out.ps,
-                          b, h * w, c, xin.width, self.group, ptr(ws), ws.numel(), st)
+                          b, h * w, c, xin.width, self.group, ptr(ws), ws.numel(), st,
+                          tag=f"{self.tag}bn{i}_bwd",
+                          nbytes=6.0 * (4 + 3 * (out is not None)) * b * xin.row_elems)
                 g_full = None if out is None else self.gin[i]
             elif op.kind == "gap":
                 c, h, w = op.in_shape
                 out = V(self.gin[i])
                 _lib.call("stzx_gap_bwd", g.ptr(), g.ps, out.ptr(), out.ps, b, h * w, out.width,
-                          st)
+                          st, tag=f"{self.tag}gap{i}_bwd", nbytes=6.0 * b * (out.row_elems + g.width))
                 g_full = self.gin[i]
             elif op.kind == "residual":
                 body, short = self.children[i]
                 gp = V(self.rgp[i])
                 z = V(self.acts[i])
                 _lib.call("stzx_relu_bwd", g.ptr(), g.ps, z.ptr(), gp.ptr(), gp.ps,
-                          b * g.row_elems, st)
+                          b * g.row_elems, st, tag=f"{self.tag}res{i}_mask",
+                          nbytes=6.0 * 3 * b * g.row_elems)
                 gb = body.backward(self.rgp[i], rows=rows, accumulate=accumulate, phase=phase)
                 gs = short.backward(self.rgp[i], rows=rows, accumulate=accumulate, phase=phase) \
                     if short is not None else gp
                 out = V(self.gin[i])
                 _lib.call("stzx_add", gb.ptr(), gb.ps, gs.ptr(), gs.ps, out.ptr(), out.ps,
-                          b * out.row_elems, st)
+                          b * out.row_elems, st, tag=f"{self.tag}res{i}_add",
+                          nbytes=6.0 * 3 * b * out.row_elems)
                 g_full = self.gin[i]
             elif op.kind == "maxpool":
                 if op.skip_dgrad:

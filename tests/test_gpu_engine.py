@@ -21,11 +21,14 @@ TOL = 3e-6
 def _longest_contraction(layers, in_shape, batch):
     """Largest K over the stack's forward, input-gradient and weight-gradient
     GEMMs."""
-    from paper_1812_10624_b200.tensor_core import Conv2d, FullyConnected, out_shape
+    from paper_1812_10624_b200.tensor_core import Conv2d, FullyConnected, Residual, out_shape
     shape, kmax = tuple(in_shape), 1
     for l in layers:
         nxt = out_shape(l, shape)
-        if isinstance(l, FullyConnected):
+        if isinstance(l, Residual):
+            kmax = max(kmax, _longest_contraction(l.body, shape, batch),
+                       _longest_contraction(l.shortcut, shape, batch))
+        elif isinstance(l, FullyConnected):
             kmax = max(kmax, l.in_dim, l.out_dim, batch)
         elif isinstance(l, Conv2d):
             kk = l.kernel * l.kernel
@@ -64,9 +67,36 @@ def _oracle_forward_tie_aware(tl, params, x, dev_pos):
     return x, caches
 
 
+def _bn_fed_biases(layers):
+    """(layer, tensor) positions of conv biases that feed a BatchNorm, inside
+    residual rows too (tensor index within the row)."""
+    from paper_1812_10624_b200.tensor_core import BatchNorm2d, Conv2d, Residual, param_shapes
+    out = set()
+
+    def scan(seq, li, t0):
+        t = t0
+        for j, l in enumerate(seq):
+            if isinstance(l, Conv2d) and j + 1 < len(seq) and isinstance(seq[j + 1], BatchNorm2d):
+                out.add((li, t + 1))
+            t += len(param_shapes(l))
+        return t
+    for li, l in enumerate(layers):
+        if isinstance(l, Residual):
+            scan(l.shortcut, li, scan(l.body, li, 0))
+        elif isinstance(l, Conv2d) and li + 1 < len(layers) and \
+                isinstance(layers[li + 1], BatchNorm2d):
+            out.add((li, 1))
+    return out
+
+
 def _run(layers, in_shape, batch, need_input_grad, seed):
     from paper_1812_10624_b200.tensor_core import Conv2d, FullyConnected
-    depth = sum(isinstance(l, (Conv2d, FullyConnected)) for l in layers)
+    from paper_1812_10624_b200.tensor_core import Residual
+
+    def _depth(seq):
+        return sum(_depth(l.body) + _depth(l.shortcut) if isinstance(l, Residual)
+                   else isinstance(l, (Conv2d, FullyConnected)) for l in seq)
+    depth = max(1, _depth(layers))
     tol = gemm_tol(_longest_contraction(layers, in_shape, batch))
     from paper_1812_10624_b200.engine import BlockEngine
     from paper_1812_10624_b200.tensor_core import as_tuple, seeded_init
@@ -100,9 +130,16 @@ def _run(layers, in_shape, batch, need_input_grad, seed):
     ry, caches = _oracle_forward_tie_aware(tl, params, x, dev_pos)
     rgx, rgrads = orc.block_backward(tl, params, caches, gy)
     assert orc.rel_err(got.cpu().numpy(), ry) <= tol
+    noise = _bn_fed_biases(layers)
     for li, (gl, rl) in enumerate(zip(eng.grads, rgrads)):
-        for a, b in zip(gl, rl):
-            assert orc.rel_err(a.cpu().numpy(), b) <= tol, f"layer {li}"
+        for ti, (a, b) in enumerate(zip(gl, rl)):
+            if (li, ti) in noise:
+                # a conv bias feeding a BatchNorm: its true gradient is 0 (BN
+                # removes any per-channel shift), both sides hold rounding noise
+                scale = max(float(np.abs(r).max()) for r in rl)
+                assert float(np.abs(a.cpu().numpy()).max()) <= 1e-4 * scale, f"layer {li}.{ti}"
+                continue
+            assert orc.rel_err(a.cpu().numpy(), b) <= tol, f"layer {li}.{ti}"
     if need_input_grad:
         if len(in_shape) == 1:
             got_gx = gin.to_float()[:, :in_shape[0]]
@@ -196,3 +233,29 @@ def test_micro_batches_match_full_batch(schedule):
     full, micro = run(False), run(True)
     for a, b in zip(full, micro):
         assert orc.rel_err(b, a) <= 1e-6
+
+
+# -- ResNet-trunk kinds (oracle-defined, parity unpinned) --------
+
+RESNET_STRIDED = [  # (layers factory, in_shape, batch): ResNet-50 stage-4 shapes at 64x64
+    ("proj1x1s2", lambda m: [m.Conv2d(1024, 2048, 1, 2)], (1024, 4, 4), 2),
+    ("c3x3s2", lambda m: [m.Conv2d(512, 512, 3, 2, 1)], (512, 4, 4), 2),
+    ("c3x3s2_c64", lambda m: [m.Conv2d(64, 64, 3, 2, 1)], (64, 16, 16), 2),
+    ("bn_relu", lambda m: [m.BatchNorm2d(256), m.ReLU()], (256, 7, 7), 4),
+    ("gap_flatten", lambda m: [m.GlobalAvgPool2d(), m.Flatten()], (2048, 2, 2), 3),
+]
+
+
+@pytest.mark.parametrize("case", RESNET_STRIDED, ids=lambda c: c[0])
+def test_resnet_pieces(case):
+    from paper_1812_10624_b200 import tensor_core as m
+    _, make, shape, batch = case
+    _run(make(m), shape, batch, True, 7)
+
+
+def test_resnet_stage4_first_block():
+    from paper_1812_10624_b200 import tensor_core as m
+    body = (m.Conv2d(1024, 512, 1), m.BatchNorm2d(512), m.ReLU(), m.Conv2d(512, 512, 3, 2, 1),
+            m.BatchNorm2d(512), m.ReLU(), m.Conv2d(512, 2048, 1), m.BatchNorm2d(2048))
+    short = (m.Conv2d(1024, 2048, 1, 2), m.BatchNorm2d(2048))
+    _run([m.Residual(body, short)], (1024, 4, 4), 2, True, 8)

@@ -26,7 +26,7 @@ captured = []
 
 
 @contextmanager
-def hook(name, args, flops=0.0, t=None):
+def hook(name, args, flops=0.0, t=None, nbytes=0.0):
     if t == tag and not captured:
         captured.append((name, args, flops))
     yield
