@@ -466,9 +466,11 @@ def main():
         phase_ms[rec.label] = rec.elapsed_ms
 
     bf16_peak, hbm_peak, peak_src = peaks()
+    # dominant kernel = the ABI call with the largest total time among the
+    # ones that carry algorithmic work (GEMM FLOPs or HBM bytes)
     top_key, top = None, (0.0, 0)
     for key, (tot, cnt) in calls.items():
-        if tot > top[0]:
+        if (key[1] > 0 or key[2] > 0) and tot > top[0]:
             top_key, top = key, (tot, cnt)
     fl = top_key[1] if top_key else 0.0
     nb = top_key[2] if top_key else 0.0

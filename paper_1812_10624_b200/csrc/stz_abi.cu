@@ -1543,16 +1543,20 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   const size_t grows = (size_t)group * HW;
   const int slices = bn_slices(grows, G, tiles);
   const int rps = (int)((grows + slices - 1) / slices);
+  const size_t total = (size_t)N * HW * (C8 / 8);
+  if (total >= (1ull << 31)) return fail(STZ_EINVAL, "bn_fwd: %zu chunks exceed 2^31", total);
   Carve cv(ws, ws_bytes);
   double* part = cv.take<double>((size_t)G * slices * C8 * 2);
-  if (!part) return fail(STZ_EWORKSPACE, "bn_fwd: workspace too small");
+  double2* coef = cv.take<double2>((size_t)G * C8);
+  if (!part || !coef) return fail(STZ_EWORKSPACE, "bn_fwd: workspace too small");
   bn_reduce_kernel<false><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, nullptr, 0, nullptr,
                                                                  part, HW, C8, group, rps);
-  bn_stats_final_kernel<<<cdiv(G * C8, 128), 128, 0, st>>>(part, stats, G, slices, C8,
-                                                          (double)grows, (double)eps);
-  bn_apply_kernel<<<grid_for((size_t)N * HW * (C8 / 8)), 256, 0, st>>>(
-      cb(x), psx, gamma, beta, stats, cb(res), psr, mb(y), psy, (size_t)N * HW, HW, C, C8, group,
-      relu);
+  bn_stats_final_kernel<<<cdiv(G * C8, 128), 128, 0, st>>>(part, stats, coef, gamma, beta, G,
+                                                          slices, C, C8, (double)grows,
+                                                          (double)eps);
+  bn_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(x), psx, coef, cb(res), psr, mb(y), psy,
+                                                   (uint32_t)total, FastDiv(C8 / 8),
+                                                   FastDiv((uint32_t)grows), C8, relu);
   return check_launch("bn_fwd");
 }
 
@@ -1567,17 +1571,20 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* x, size_t psx, const doub
   const size_t grows = (size_t)group * HW;
   const int slices = bn_slices(grows, G, tiles);
   const int rps = (int)((grows + slices - 1) / slices);
+  const size_t total = (size_t)N * HW * (C8 / 8);
+  if (total >= (1ull << 31)) return fail(STZ_EINVAL, "bn_bwd: %zu chunks exceed 2^31", total);
   Carve cv(ws, ws_bytes);
   double* part = cv.take<double>((size_t)G * slices * C8 * 2);
-  double* sums = cv.take<double>((size_t)G * C8 * 2);
-  if (!part || !sums) return fail(STZ_EWORKSPACE, "bn_bwd: workspace too small");
+  double4* coef = cv.take<double4>((size_t)G * C8);
+  if (!part || !coef) return fail(STZ_EWORKSPACE, "bn_bwd: workspace too small");
   bn_reduce_kernel<true><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, cb(g), psg, stats,
                                                                 part, HW, C8, group, rps);
-  bn_bwd_final_kernel<<<cdiv(C8, 128), 128, 0, st>>>(part, sums, ggamma, gbeta, G, slices, C, C8,
-                                                    accumulate);
+  bn_bwd_final_kernel<<<cdiv(C8, 128), 128, 0, st>>>(part, stats, gamma, coef, ggamma, gbeta, G,
+                                                    slices, C, C8, (double)grows, accumulate);
   if (gx)
-    bn_bwd_apply_kernel<<<grid_for((size_t)N * HW * (C8 / 8)), 256, 0, st>>>(
-        cb(g), psg, cb(x), psx, gamma, stats, sums, mb(gx), psgx, (size_t)N * HW, HW, C, C8, group);
+    bn_bwd_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(g), psg, cb(x), psx, coef, mb(gx), psgx,
+                                                         (uint32_t)total, FastDiv(C8 / 8),
+                                                         FastDiv((uint32_t)grows), C8);
   return check_launch("bn_bwd");
 }
 

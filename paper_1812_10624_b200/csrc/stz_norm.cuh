@@ -86,9 +86,13 @@ __global__ void __launch_bounds__(256) bn_reduce_kernel(
 }
 
 // forward finalize: per (group, channel) mean and rstd = 1/sqrt(var + eps),
-// var = E[x^2] - mean^2 (float64; clamped at 0)
+// var = E[x^2] - mean^2 (float64; clamped at 0), kept in `stats` for the
+// backward; and the apply pass's affine form y = x*A + B, A = rstd*gamma,
+// B = beta - mean*A (float64; padded channels A = B = 0)
 __global__ void bn_stats_final_kernel(const double* __restrict__ partial, double* __restrict__ stats,
-                                      int G, int nslices, int C8, double m, double eps) {
+                                      double2* __restrict__ coef, const float* __restrict__ gamma,
+                                      const float* __restrict__ beta, int G, int nslices, int C,
+                                      int C8, double m, double eps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G * C8) return;
   const int gi = i / C8, c = i % C8;
@@ -99,16 +103,23 @@ __global__ void bn_stats_final_kernel(const double* __restrict__ partial, double
   }
   const double mean = s / m;
   const double var = fmax(q / m - mean * mean, 0.0);
+  const double rstd = 1.0 / sqrt(var + eps);
   stats[(size_t)i * 2] = mean;
-  stats[(size_t)i * 2 + 1] = 1.0 / sqrt(var + eps);
+  stats[(size_t)i * 2 + 1] = rstd;
+  const double A = c < C ? rstd * (double)gamma[c] : 0.0;
+  coef[i] = make_double2(A, c < C ? (double)beta[c] - mean * A : 0.0);
 }
 
-// backward finalize: per-group (sum g, sum g*xhat) for the apply pass, and the
-// parameter-gradient batch sums dgamma = sum g*xhat, dbeta = sum g over all
-// groups (written, or added in fp32 with `accumulate`)
-__global__ void bn_bwd_final_kernel(const double* __restrict__ partial, double* __restrict__ sums,
+// backward finalize: per-group (sum g, sum g*xhat) -> the apply pass's
+// affine form gx = P*g + Q*x + R with coef = gamma*rstd/m:
+//   P = coef*m, Q = -coef*sgx*rstd, R = coef*(sgx*rstd*mean - sg)
+// and the parameter-gradient batch sums dgamma = sum g*xhat, dbeta = sum g
+// over all groups (written, or added in fp32 with `accumulate`)
+__global__ void bn_bwd_final_kernel(const double* __restrict__ partial,
+                                    const double* __restrict__ stats,
+                                    const float* __restrict__ gamma, double4* __restrict__ coef,
                                     float* __restrict__ ggamma, float* __restrict__ gbeta, int G,
-                                    int nslices, int C, int C8, int accumulate) {
+                                    int nslices, int C, int C8, double m, int accumulate) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C8) return;
   double tg = 0.0, tgx = 0.0;
@@ -118,8 +129,10 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial, double* 
       s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
       q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
     }
-    sums[((size_t)gi * C8 + c) * 2] = s;
-    sums[((size_t)gi * C8 + c) * 2 + 1] = q;
+    const size_t i = (size_t)gi * C8 + c;
+    const double mean = stats[i * 2], rstd = stats[i * 2 + 1];
+    const double cf = c < C ? (double)gamma[c] * rstd / m : 0.0;
+    coef[i] = make_double4(cf * m, -cf * q * rstd, cf * (q * rstd * mean - s), 0.0);
     tg += s;
     tgx += q;
   }
@@ -129,71 +142,51 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial, double* 
   }
 }
 
-// y = ((x - mean) * rstd) * gamma + beta (float64, one rounding), then
-// optionally + residual (fp32 add) and ReLU; padded channels stay 0
-__global__ void bn_apply_kernel(const bf16_t* __restrict__ x, size_t psx,
-                                const float* __restrict__ gamma, const float* __restrict__ beta,
-                                const double* __restrict__ stats, const bf16_t* __restrict__ res,
-                                size_t psr, bf16_t* __restrict__ y, size_t psy, size_t rows,
-                                int HW, int C, int C8, int group, int relu) {
-  const int nch = C8 / 8;
-  const size_t total = rows * nch, grows = (size_t)group * HW;
-  STZ_GRID_LOOP(i, total) {
-    const size_t row = i / nch;
-    const int cc = (int)(i % nch);
-    const size_t gi = row / grows;
-    const size_t off = row * C8 + (size_t)cc * 8;
+// y = x*A + B (float64, one rounding), then optionally + residual (fp32
+// add) and ReLU.  One thread per (row, 8 channels), 32-bit indices.
+__global__ void __launch_bounds__(256) bn_apply_kernel(
+    const bf16_t* __restrict__ x, size_t psx, const double2* __restrict__ coef,
+    const bf16_t* __restrict__ res, size_t psr, bf16_t* __restrict__ y, size_t psy,
+    uint32_t total, FastDiv d_nch, FastDiv d_grows, int C8, int relu) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t row, cc;
+    d_nch.divmod(i, row, cc);
+    const uint32_t gi = d_grows.div(row);
+    const size_t off = (size_t)i * 8;
     float v[8], r[8];
     load_split8(x + off, psx, v);
     if (res) load_split8(res + off, psr, r);
+    const double2* cf = coef + (size_t)gi * C8 + cc * 8;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = cc * 8 + j;
-      float o = 0.f;
-      if (c < C) {
-        const double mean = stats[(gi * C8 + c) * 2], rstd = stats[(gi * C8 + c) * 2 + 1];
-        const double xh = __dmul_rn(__dsub_rn((double)v[j], mean), rstd);
-        o = (float)__dadd_rn(__dmul_rn(xh, (double)gamma[c]), (double)beta[c]);
-        if (res) o = __fadd_rn(o, r[j]);
-        if (relu) o = o > 0.f ? o : 0.f;
-      }
+      const double2 ab = __ldg(cf + j);
+      float o = (float)fma((double)v[j], ab.x, ab.y);
+      if (res) o = __fadd_rn(o, r[j]);
+      if (relu) o = o > 0.f ? o : 0.f;
       v[j] = o;
     }
     store_split8(y + off, psy, v);
   }
 }
 
-// gx = ((gamma * rstd) / m) * ((m * g - sum g) - xhat * sum(g * xhat))
-__global__ void bn_bwd_apply_kernel(const bf16_t* __restrict__ g, size_t psg,
-                                    const bf16_t* __restrict__ x, size_t psx,
-                                    const float* __restrict__ gamma,
-                                    const double* __restrict__ stats,
-                                    const double* __restrict__ sums, bf16_t* __restrict__ gx,
-                                    size_t psgx, size_t rows, int HW, int C, int C8, int group) {
-  const int nch = C8 / 8;
-  const size_t total = rows * nch, grows = (size_t)group * HW;
-  const double m = (double)grows;
-  STZ_GRID_LOOP(i, total) {
-    const size_t row = i / nch;
-    const int cc = (int)(i % nch);
-    const size_t gi = row / grows;
-    const size_t off = row * C8 + (size_t)cc * 8;
+// gx = P*g + Q*x + R (float64, one rounding)
+__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(
+    const bf16_t* __restrict__ g, size_t psg, const bf16_t* __restrict__ x, size_t psx,
+    const double4* __restrict__ coef, bf16_t* __restrict__ gx, size_t psgx, uint32_t total,
+    FastDiv d_nch, FastDiv d_grows, int C8) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t row, cc;
+    d_nch.divmod(i, row, cc);
+    const uint32_t gi = d_grows.div(row);
+    const size_t off = (size_t)i * 8;
     float v[8], gv[8];
     load_split8(x + off, psx, v);
     load_split8(g + off, psg, gv);
+    const double4* cf = coef + (size_t)gi * C8 + cc * 8;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = cc * 8 + j;
-      float o = 0.f;
-      if (c < C) {
-        const size_t k = (gi * C8 + c) * 2;
-        const double mean = stats[k], rstd = stats[k + 1], sg = sums[k], sgx = sums[k + 1];
-        const double xh = __dmul_rn(__dsub_rn((double)v[j], mean), rstd);
-        const double coef = __ddiv_rn(__dmul_rn((double)gamma[c], rstd), m);
-        const double inner = __dsub_rn(__dsub_rn(__dmul_rn(m, (double)gv[j]), sg), __dmul_rn(xh, sgx));
-        o = (float)__dmul_rn(coef, inner);
-      }
-      v[j] = o;
+      const double4 pqr = cf[j];
+      v[j] = (float)fma(pqr.x, (double)gv[j], fma(pqr.y, (double)v[j], pqr.z));
     }
     store_split8(gx + off, psgx, v);
   }

@@ -70,7 +70,9 @@ def test_resnet50_structure_matches_oracle(lib):
     exactly, since the following BatchNorm's backward removes the mean; a
     channel that is constant over K*H*W = 8 values turns rounding into O(1)
     normalised values).  So the bar here is the loss (rtol 1e-5) and the
-    update direction (cosine >= 0.9999 over the whole gradient vector);
+    update direction: cosine over the whole gradient vector >= 0.999 (the
+    oracle against itself under 1e-7 parameter perturbations: 0.99981 and
+    0.99994 for two perturbation seeds; the GPU measured 0.99973);
     exact per-block parity at these shapes is test_gpu_engine.py's
     test_resnet_stage4_first_block / test_resnet_pieces."""
     from paper_1812_10624_b200.model_partition import resnet
@@ -81,7 +83,7 @@ def test_resnet50_structure_matches_oracle(lib):
     b = np.concatenate([np.ravel(t) for row in ref_v for t in row]).astype(np.float64)
     assert np.isfinite(a).all()
     cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
-    assert cos >= 0.9999, cos
+    assert cos >= 0.999, cos
 
 
 def test_tiny_resnet_deterministic_and_graph(lib):
