@@ -234,8 +234,11 @@ int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, fl
 int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta, const void* res,
                 size_t psr, void* y, size_t psy, double* stats, int N, int HW, int C, int C8,
                 int group, float eps, int relu, void* ws, size_t ws_bytes, void* stream);
-/* dgamma / dbeta batch sums (added with `accumulate`), gx nullable. */
-int stzx_bn_bwd(const void* g, size_t psg, const void* x, size_t psx, const double* stats,
+/* dgamma / dbeta batch sums (added with `accumulate`), gx nullable; `mask`
+ * (nullable): g is the gradient of a ReLU output, masked where plane 0 of
+ * `mask` (that output) is not > 0 (a residual block's final ReLU). */
+int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size_t psx,
+                const double* stats,
                 const float* gamma, float* ggamma, float* gbeta, int accumulate, void* gx,
                 size_t psgx, int N, int HW, int C, int C8, int group, void* ws, size_t ws_bytes,
                 void* stream);
@@ -244,9 +247,10 @@ int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, 
                  void* stream);
 int stzx_gap_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int HW, int C8,
                  void* stream);
-/* y = a + b elementwise (fp32 RN), n a multiple of 8: residual input gradients */
-int stzx_add(const void* a, size_t psa, const void* b, size_t psb, void* y, size_t psy, size_t n,
-             void* stream);
+/* y = a + b elementwise (fp32 RN), n a multiple of 8: residual input
+ * gradients; b masked by a ReLU output (plane 0 > 0) when mask_b != NULL */
+int stzx_add(const void* a, size_t psa, const void* b, size_t psb, const void* mask_b, void* y,
+             size_t psy, size_t n, void* stream);
 /* SoftmaxCE on fp32 logits -> losses + split dlogits [M][C8]. */
 int stzx_softmax_ce(const float* logits, const int* labels, float* losses, void* dz, size_t psd,
                     int M, int C, int C8, void* stream);

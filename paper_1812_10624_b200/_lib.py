@@ -70,10 +70,10 @@ SIGNATURES = {
     "stzx_pack_conv_w_s2d": (I, [P, P, Z, I, I, I, I, I, P]),
     "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_bn_fwd": (I, [P, Z, P, P, P, Z, P, Z, P, I, I, I, I, I, F, I, P, Z, P]),
-    "stzx_bn_bwd": (I, [P, Z, P, Z, P, P, P, P, I, P, Z, I, I, I, I, I, P, Z, P]),
+    "stzx_bn_bwd": (I, [P, Z, P, P, Z, P, P, P, P, I, P, Z, I, I, I, I, I, P, Z, P]),
     "stzx_gap_fwd": (I, [P, Z, P, Z, I, I, I, P]),
     "stzx_gap_bwd": (I, [P, Z, P, Z, I, I, I, P]),
-    "stzx_add": (I, [P, Z, P, Z, P, Z, Z, P]),
+    "stzx_add": (I, [P, Z, P, Z, P, P, Z, Z, P]),
     # exchange + update over NVLink peer memory
     "stz_ipc_handle": (I, [P, P, P]),
     "stz_ipc_open": (I, [P, P]),

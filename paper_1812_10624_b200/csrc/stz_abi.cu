@@ -936,6 +936,15 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
                   int C8, int H, int W, int O, int k, int s, int p, int OH, int OW, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const int M = N * OH * OW, K = k * k * C8;
+  if (k == 1 && s == 1 && p == 0 && tma_on() && C8 % 32 == 0) {
+    // 1x1 conv = a plain GEMM over the NHWC pixel rows (ResNet bottlenecks):
+    // tiled boxes for both operands, no im2col / band addressing
+    const TgShape sh = tg_shape(M, O, K, ws_bytes);
+    TgOperand a, b;
+    if (op_tiled_k(a, x, psx, M, C8, C8, TG_BM * sh.MH) &&
+        op_tiled_k(b, wf, psw, O, K, K, sh.BN / sh.CL))
+      return run_tgemm("conv_fwd[1x1]", sh, a, b, ep, M, O, K, ws, ws_bytes, st);
+  }
   if (s == 1) {
     const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, k, p, ws,
                                  ws_bytes, st);
@@ -958,6 +967,13 @@ int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, c
                     int N, int C, int H, int W, int O8, int k, int s, int p, int OH, int OW,
                     void* ws, size_t ws_bytes, cudaStream_t st) {
   const int M = N * H * W, K = k * k * O8;
+  if (k == 1 && s == 1 && p == 0 && tma_on() && O8 % 32 == 0) {   // 1x1: plain GEMM
+    const TgShape sh = tg_shape(M, C, K, ws_bytes);
+    TgOperand a, b;
+    if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM * sh.MH) &&
+        op_tiled_k(b, wd, psw, C, K, K, sh.BN / sh.CL))
+      return run_tgemm("conv_dgrad[1x1]", sh, a, b, ep, M, C, K, ws, ws_bytes, st);
+  }
   if (s == 1) {   // the same stride-1 conv over dY padded by k-1-p, flipped weights
     const int rc = run_band_conv("conv_dgrad[band]", g, psg, wd, psw, ep, N, O8, OH, OW, C, k,
                                  k - 1 - p, ws, ws_bytes, st);
@@ -1550,8 +1566,8 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   double2* coef = cv.take<double2>((size_t)G * C8);
   if (!part || !coef) return fail(STZ_EWORKSPACE, "bn_fwd: workspace too small");
   bn_reduce_kernel<false><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, nullptr, 0, nullptr,
-                                                                 part, HW, C8, group, rps);
-  bn_stats_final_kernel<<<cdiv(G * C8, 128), 128, 0, st>>>(part, stats, coef, gamma, beta, G,
+                                                                 nullptr, part, HW, C8, group, rps);
+  bn_stats_final_kernel<<<cdiv(G * C8 * 32, 256), 256, 0, st>>>(part, stats, coef, gamma, beta, G,
                                                           slices, C, C8, (double)grows,
                                                           (double)eps);
   bn_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(x), psx, coef, cb(res), psr, mb(y), psy,
@@ -1560,7 +1576,8 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   return check_launch("bn_fwd");
 }
 
-int stzx_bn_bwd(const void* g, size_t psg, const void* x, size_t psx, const double* stats,
+int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size_t psx,
+                const double* stats,
                 const float* gamma, float* ggamma, float* gbeta, int accumulate, void* gx,
                 size_t psgx, int N, int HW, int C, int C8, int group, void* ws, size_t ws_bytes,
                 void* stream) {
@@ -1577,12 +1594,13 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* x, size_t psx, const doub
   double* part = cv.take<double>((size_t)G * slices * C8 * 2);
   double4* coef = cv.take<double4>((size_t)G * C8);
   if (!part || !coef) return fail(STZ_EWORKSPACE, "bn_bwd: workspace too small");
-  bn_reduce_kernel<true><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, cb(g), psg, stats,
-                                                                part, HW, C8, group, rps);
-  bn_bwd_final_kernel<<<cdiv(C8, 128), 128, 0, st>>>(part, stats, gamma, coef, ggamma, gbeta, G,
+  bn_reduce_kernel<true><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, cb(g), psg, cb(mask),
+                                                                stats, part, HW, C8, group, rps);
+  bn_bwd_final_kernel<<<cdiv(C8 * 32, 256), 256, 0, st>>>(part, stats, gamma, coef, ggamma, gbeta, G,
                                                     slices, C, C8, (double)grows, accumulate);
   if (gx)
-    bn_bwd_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(g), psg, cb(x), psx, coef, mb(gx), psgx,
+    bn_bwd_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(g), psg, cb(mask), cb(x), psx, coef,
+                                                         mb(gx), psgx,
                                                          (uint32_t)total, FastDiv(C8 / 8),
                                                          FastDiv((uint32_t)grows), C8);
   return check_launch("bn_bwd");
@@ -1604,12 +1622,12 @@ int stzx_gap_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int HW
   return check_launch("gap_bwd");
 }
 
-int stzx_add(const void* a, size_t psa, const void* b, size_t psb, void* y, size_t psy, size_t n,
-             void* stream) {
+int stzx_add(const void* a, size_t psa, const void* b, size_t psb, const void* mask_b, void* y,
+             size_t psy, size_t n, void* stream) {
   if (n % 8) return fail(STZ_EINVAL, "add: %zu elements is not a multiple of 8", n);
   if (n == 0) return STZ_OK;
-  add_split_kernel<<<grid_for(n / 8), 256, 0, as_stream(stream)>>>(cb(a), psa, cb(b), psb, mb(y),
-                                                                   psy, n / 8);
+  add_split_kernel<<<grid_for(n / 8), 256, 0, as_stream(stream)>>>(cb(a), psa, cb(b), psb,
+                                                                   cb(mask_b), mb(y), psy, n / 8);
   return check_launch("add_split");
 }
 

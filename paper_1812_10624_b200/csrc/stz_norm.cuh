@@ -17,6 +17,18 @@
 
 namespace stz {
 
+// gradient of a ReLU output -> gradient of its input: zero where the output
+// (plane 0, whose sign is the value's) is not > 0
+__device__ __forceinline__ void apply_mask8(const bf16_t* m, float (&v)[8]) {
+  const uint4 w = *reinterpret_cast<const uint4*>(m);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (!(bf2f((bf16_t)(ws[j] & 0xFFFF)) > 0.f)) v[2 * j] = 0.f;
+    if (!(bf2f((bf16_t)(ws[j] >> 16)) > 0.f)) v[2 * j + 1] = 0.f;
+  }
+}
+
 // Per (group, row slice, channel) float64 partial sums.
 //   forward : (sum x, sum x^2)
 //   backward: (sum g, sum g * xhat), xhat = (x - mean) * rstd
@@ -25,8 +37,8 @@ namespace stz {
 template <bool BWD>
 __global__ void __launch_bounds__(256) bn_reduce_kernel(
     const bf16_t* __restrict__ x, size_t psx, const bf16_t* __restrict__ g, size_t psg,
-    const double* __restrict__ stats, double* __restrict__ partial, int HW, int C8, int group,
-    int rows_per_slice) {
+    const bf16_t* __restrict__ mask, const double* __restrict__ stats,
+    double* __restrict__ partial, int HW, int C8, int group, int rows_per_slice) {
   __shared__ double red[256][16];
   const int nch = C8 / 8, ct = blockIdx.z;
   const int L = min(nch - ct * 32, 32), R = 256 / L;
@@ -61,6 +73,7 @@ __global__ void __launch_bounds__(256) bn_reduce_kernel(
       } else {
         float gv[8];
         load_split8(g + off, psg, gv);
+        if (mask) apply_mask8(mask + off, gv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const double xh = __dmul_rn(__dsub_rn((double)v[j], mean[j]), rstd[j]);
@@ -93,14 +106,21 @@ __global__ void bn_stats_final_kernel(const double* __restrict__ partial, double
                                       double2* __restrict__ coef, const float* __restrict__ gamma,
                                       const float* __restrict__ beta, int G, int nslices, int C,
                                       int C8, double m, double eps) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per (group, channel): lanes take slices l, l+32, ... and a fixed
+  // xor-shuffle tree combines them (deterministic)
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= G * C8) return;
   const int gi = i / C8, c = i % C8;
   double s = 0.0, q = 0.0;
-  for (int k = 0; k < nslices; ++k) {
+  for (int k = lane; k < nslices; k += 32) {
     s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
     q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  if (lane) return;
   const double mean = s / m;
   const double var = fmax(q / m - mean * mean, 0.0);
   const double rstd = 1.0 / sqrt(var + eps);
@@ -120,23 +140,29 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial,
                                     const float* __restrict__ gamma, double4* __restrict__ coef,
                                     float* __restrict__ ggamma, float* __restrict__ gbeta, int G,
                                     int nslices, int C, int C8, double m, int accumulate) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per channel (groups in order; slices over the lanes, fixed tree)
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= C8) return;
   double tg = 0.0, tgx = 0.0;
   for (int gi = 0; gi < G; ++gi) {
     double s = 0.0, q = 0.0;
-    for (int k = 0; k < nslices; ++k) {
+    for (int k = lane; k < nslices; k += 32) {
       s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
       q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      q += __shfl_xor_sync(0xffffffffu, q, o);
     }
     const size_t i = (size_t)gi * C8 + c;
     const double mean = stats[i * 2], rstd = stats[i * 2 + 1];
     const double cf = c < C ? (double)gamma[c] * rstd / m : 0.0;
-    coef[i] = make_double4(cf * m, -cf * q * rstd, cf * (q * rstd * mean - s), 0.0);
+    if (lane == 0)
+      coef[i] = make_double4(cf * m, -cf * q * rstd, cf * (q * rstd * mean - s), 0.0);
     tg += s;
     tgx += q;
   }
-  if (c < C) {
+  if (c < C && lane == 0) {
     ggamma[c] = accumulate ? __fadd_rn(ggamma[c], (float)tgx) : (float)tgx;
     gbeta[c] = accumulate ? __fadd_rn(gbeta[c], (float)tg) : (float)tg;
   }
@@ -171,7 +197,8 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(
 
 // gx = P*g + Q*x + R (float64, one rounding)
 __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(
-    const bf16_t* __restrict__ g, size_t psg, const bf16_t* __restrict__ x, size_t psx,
+    const bf16_t* __restrict__ g, size_t psg, const bf16_t* __restrict__ mask,
+    const bf16_t* __restrict__ x, size_t psx,
     const double4* __restrict__ coef, bf16_t* __restrict__ gx, size_t psgx, uint32_t total,
     FastDiv d_nch, FastDiv d_grows, int C8) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -182,6 +209,7 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(
     float v[8], gv[8];
     load_split8(x + off, psx, v);
     load_split8(g + off, psg, gv);
+    if (mask) apply_mask8(mask + off, gv);
     const double4* cf = coef + (size_t)gi * C8 + cc * 8;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -229,14 +257,17 @@ __global__ void gap_bwd_kernel(const bf16_t* __restrict__ gy, size_t psg, bf16_t
   }
 }
 
-// y = a + b (fp32 RN), n elements (multiple of 8)
+// y = a + b (fp32 RN), n elements (multiple of 8); b masked by a ReLU output
+// (plane 0 > 0) when `mask_b` is given
 __global__ void add_split_kernel(const bf16_t* __restrict__ a, size_t psa,
-                                 const bf16_t* __restrict__ b, size_t psb, bf16_t* __restrict__ y,
+                                 const bf16_t* __restrict__ b, size_t psb,
+                                 const bf16_t* __restrict__ mask_b, bf16_t* __restrict__ y,
                                  size_t psy, size_t n8) {
   STZ_GRID_LOOP(i, n8) {
     float va[8], vb[8];
     load_split8(a + i * 8, psa, va);
     load_split8(b + i * 8, psb, vb);
+    if (mask_b) apply_mask8(mask_b + i * 8, vb);
 #pragma unroll
     for (int j = 0; j < 8; ++j) va[j] = __fadd_rn(va[j], vb[j]);
     store_split8(y + i * 8, psy, va);

@@ -285,14 +285,12 @@ class BlockEngine:
         self.xin = None   # packed block input, allocated on first pack_input()
         self._gout = None  # per-op output-gradient buffers of the last backward
         self.bnstats: dict = {}   # bn op -> float64 [groups][C8][2] (mean, rstd)
-        self.rgp: dict = {}       # residual op -> ReLU-masked output gradient
         for i, op in enumerate(self.ops):
             if op.kind == "relu" and i > 0 and self.ops[i - 1].fused_relu:
                 continue
             if op.kind == "residual":             # the body's last BatchNorm writes it
                 body, _ = self.children[i]
                 self.acts[i] = body._act(len(body.ops) - 1)
-                self.rgp[i] = self._split_for(op.out_shape, b)
                 continue
             if op.kind == "bn":
                 c = op.in_shape[0]
@@ -560,7 +558,7 @@ class BlockEngine:
         return V(self._act(len(self.ops) - 1))
 
     def backward(self, gy: Split | None = None, rows=None, accumulate: bool = False,
-                 phase: str = "all"):
+                 phase: str = "all", gy_mask: Split | None = None):
         """Backward through the block; parameter-gradient sums land in
         ``grad_flat`` (ADDED to it with ``accumulate``: micro-batches of one
         iteration).  ``gy`` is full-batch shaped; ``rows = (r0, r1)`` runs
@@ -573,6 +571,10 @@ class BlockEngine:
         * "wgrad" -- only the weight / bias gradients, from the buffers a
           "dgrad" pass left (over ``rows``; the FC worker runs it over the
           whole batch after the boundary gradients have left).
+
+        ``gy_mask`` (a residual block's body / shortcut): ``gy`` is the
+        gradient of relu(last output + other branch); the last op (a
+        BatchNorm) applies that ReLU's mask (plane 0 of ``gy_mask`` > 0).
 
         Returns the input-gradient Split of ``rows`` (None when the block has
         no input gradient, or for phase "wgrad")."""
@@ -628,13 +630,16 @@ class BlockEngine:
                 self._check_groups(r0, r1)
                 c, h, w = op.in_shape
                 out = None if op.skip_dgrad else V(self.gin[i])
-                _lib.call("stzx_bn_bwd", g.ptr(), g.ps, xin.ptr(), xin.ps,
+                m = V(gy_mask) if (gy_mask is not None and i == len(self.ops) - 1) else None
+                _lib.call("stzx_bn_bwd", g.ptr(), g.ps, None if m is None else m.ptr(),
+                          xin.ptr(), xin.ps,
                           ptr(self.bnstats[i][r0 // self.group:]), ptr(self.params[i][0]),
                           ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc,
                           None if out is None else out.ptr(), 0 if out is None else out.ps,
                           b, h * w, c, xin.width, self.group, ptr(ws), ws.numel(), st,
                           tag=f"{self.tag}bn{i}_bwd",
-                          nbytes=6.0 * (4 + 3 * (out is not None)) * b * xin.row_elems)
+                          nbytes=(12.0 + 18.0 * (out is not None) + 4.0 * (m is not None))
+                          * b * xin.row_elems)
                 g_full = None if out is None else self.gin[i]
             elif op.kind == "gap":
                 c, h, w = op.in_shape
@@ -643,19 +648,25 @@ class BlockEngine:
                           st, tag=f"{self.tag}gap{i}_bwd", nbytes=6.0 * b * (out.row_elems + g.width))
                 g_full = self.gin[i]
             elif op.kind == "residual":
+                # the block's final ReLU mask (its output z > 0) is applied by
+                # the consumers of the incoming gradient: the body's and the
+                # projection shortcut's last BatchNorm, or the add itself for
+                # an identity shortcut
                 body, short = self.children[i]
-                gp = V(self.rgp[i])
-                z = V(self.acts[i])
-                _lib.call("stzx_relu_bwd", g.ptr(), g.ps, z.ptr(), gp.ptr(), gp.ps,
-                          b * g.row_elems, st, tag=f"{self.tag}res{i}_mask",
-                          nbytes=6.0 * 3 * b * g.row_elems)
-                gb = body.backward(self.rgp[i], rows=rows, accumulate=accumulate, phase=phase)
-                gs = short.backward(self.rgp[i], rows=rows, accumulate=accumulate, phase=phase) \
-                    if short is not None else gp
+                z_full = self.acts[i]
+                gb = body.backward(g_full, rows=rows, accumulate=accumulate, phase=phase,
+                                   gy_mask=z_full)
+                mask_b = None
+                if short is not None:
+                    gs = short.backward(g_full, rows=rows, accumulate=accumulate, phase=phase,
+                                        gy_mask=z_full)
+                else:
+                    gs, mask_b = g, V(z_full)
                 out = V(self.gin[i])
-                _lib.call("stzx_add", gb.ptr(), gb.ps, gs.ptr(), gs.ps, out.ptr(), out.ps,
+                _lib.call("stzx_add", gb.ptr(), gb.ps, gs.ptr(), gs.ps,
+                          None if mask_b is None else mask_b.ptr(), out.ptr(), out.ps,
                           b * out.row_elems, st, tag=f"{self.tag}res{i}_add",
-                          nbytes=6.0 * 3 * b * out.row_elems)
+                          nbytes=(18.0 + 2.0 * (mask_b is not None)) * b * out.row_elems)
                 g_full = self.gin[i]
             elif op.kind == "maxpool":
                 if op.skip_dgrad:

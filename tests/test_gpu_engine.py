@@ -241,7 +241,11 @@ RESNET_STRIDED = [  # (layers factory, in_shape, batch): ResNet-50 stage-4 shape
     ("proj1x1s2", lambda m: [m.Conv2d(1024, 2048, 1, 2)], (1024, 4, 4), 2),
     ("c3x3s2", lambda m: [m.Conv2d(512, 512, 3, 2, 1)], (512, 4, 4), 2),
     ("c3x3s2_c64", lambda m: [m.Conv2d(64, 64, 3, 2, 1)], (64, 16, 16), 2),
+    ("c1x1_reduce", lambda m: [m.Conv2d(256, 64, 1)], (256, 14, 14), 2),
+    ("c1x1_expand_relu", lambda m: [m.Conv2d(64, 256, 1), m.ReLU(), m.Conv2d(256, 64, 1)],
+     (64, 28, 28), 2),
     ("bn_relu", lambda m: [m.BatchNorm2d(256), m.ReLU()], (256, 7, 7), 4),
+    ("bn_large", lambda m: [m.BatchNorm2d(64)], (64, 56, 56), 2),
     ("gap_flatten", lambda m: [m.GlobalAvgPool2d(), m.Flatten()], (2048, 2, 2), 3),
 ]
 
