@@ -1570,9 +1570,12 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   bn_stats_final_kernel<<<cdiv(G * C8 * 32, 256), 256, 0, st>>>(part, stats, coef, gamma, beta, G,
                                                           slices, C, C8, (double)grows,
                                                           (double)eps);
-  bn_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(x), psx, coef, cb(res), psr, mb(y), psy,
-                                                   (uint32_t)total, FastDiv(C8 / 8),
-                                                   FastDiv((uint32_t)grows), C8, relu);
+  const uint32_t rows = (uint32_t)N * HW;
+  const int aslices = bn_slices(rows, 1, tiles);
+  const uint32_t arps = (rows + aslices - 1) / aslices;
+  bn_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(cb(x), psx, coef, cb(res), psr, mb(y), psy,
+                                                        rows, arps, FastDiv((uint32_t)grows), C8,
+                                                        relu);
   return check_launch("bn_fwd");
 }
 
@@ -1598,11 +1601,14 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
                                                                 stats, part, HW, C8, group, rps);
   bn_bwd_final_kernel<<<cdiv(C8 * 32, 256), 256, 0, st>>>(part, stats, gamma, coef, ggamma, gbeta, G,
                                                     slices, C, C8, (double)grows, accumulate);
-  if (gx)
-    bn_bwd_apply_kernel<<<grid_for(total), 256, 0, st>>>(cb(g), psg, cb(mask), cb(x), psx, coef,
-                                                         mb(gx), psgx,
-                                                         (uint32_t)total, FastDiv(C8 / 8),
-                                                         FastDiv((uint32_t)grows), C8);
+  if (gx) {
+    const uint32_t rows = (uint32_t)N * HW;
+    const int aslices = bn_slices(rows, 1, tiles);
+    const uint32_t arps = (rows + aslices - 1) / aslices;
+    bn_bwd_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(
+        cb(g), psg, cb(mask), cb(x), psx, coef, mb(gx), psgx, rows, arps,
+        FastDiv((uint32_t)grows), C8);
+  }
   return check_launch("bn_bwd");
 }
 

@@ -168,26 +168,44 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial,
   }
 }
 
+// The apply passes use the reduce kernels' block shape: L channel-chunk lanes
+// x R row lanes over a slice of rows, so each thread keeps its 8 channels'
+// coefficients in registers (reloaded only when its rows cross into the next
+// sample group) instead of re-reading them per element.
+
 // y = x*A + B (float64, one rounding), then optionally + residual (fp32
-// add) and ReLU.  One thread per (row, 8 channels), 32-bit indices.
+// add) and ReLU.  grid (slices, channel tiles).
 __global__ void __launch_bounds__(256) bn_apply_kernel(
     const bf16_t* __restrict__ x, size_t psx, const double2* __restrict__ coef,
     const bf16_t* __restrict__ res, size_t psr, bf16_t* __restrict__ y, size_t psy,
-    uint32_t total, FastDiv d_nch, FastDiv d_grows, int C8, int relu) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t row, cc;
-    d_nch.divmod(i, row, cc);
-    const uint32_t gi = d_grows.div(row);
-    const size_t off = (size_t)i * 8;
-    float v[8], r[8];
+    uint32_t rows, uint32_t rows_per_slice, FastDiv d_grows, int C8, int relu) {
+  const int nch = C8 / 8, ct = blockIdx.y;
+  const int L = min(nch - ct * 32, 32), R = 256 / L;
+  const int t = threadIdx.x, cl = t % L, rl = t / L;
+  if (rl >= R) return;
+  const int cc = ct * 32 + cl;
+  const uint32_t r0 = blockIdx.x * rows_per_slice, r1 = min(rows, r0 + rows_per_slice);
+  double A[8], B[8];
+  uint32_t cur = 0xFFFFFFFFu;
+  for (uint32_t r = r0 + rl; r < r1; r += R) {
+    const uint32_t gi = d_grows.div(r);
+    if (gi != cur) {
+      cur = gi;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double2 ab = coef[(size_t)gi * C8 + cc * 8 + j];
+        A[j] = ab.x;
+        B[j] = ab.y;
+      }
+    }
+    const size_t off = (size_t)r * C8 + cc * 8;
+    float v[8], rr[8];
     load_split8(x + off, psx, v);
-    if (res) load_split8(res + off, psr, r);
-    const double2* cf = coef + (size_t)gi * C8 + cc * 8;
+    if (res) load_split8(res + off, psr, rr);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double2 ab = __ldg(cf + j);
-      float o = (float)fma((double)v[j], ab.x, ab.y);
-      if (res) o = __fadd_rn(o, r[j]);
+      float o = (float)fma((double)v[j], A[j], B[j]);
+      if (res) o = __fadd_rn(o, rr[j]);
       if (relu) o = o > 0.f ? o : 0.f;
       v[j] = o;
     }
@@ -195,27 +213,40 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(
   }
 }
 
-// gx = P*g + Q*x + R (float64, one rounding)
+// gx = P*g + Q*x + R (float64, one rounding); g masked by a ReLU output
+// when `mask` is given
 __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(
     const bf16_t* __restrict__ g, size_t psg, const bf16_t* __restrict__ mask,
-    const bf16_t* __restrict__ x, size_t psx,
-    const double4* __restrict__ coef, bf16_t* __restrict__ gx, size_t psgx, uint32_t total,
-    FastDiv d_nch, FastDiv d_grows, int C8) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t row, cc;
-    d_nch.divmod(i, row, cc);
-    const uint32_t gi = d_grows.div(row);
-    const size_t off = (size_t)i * 8;
+    const bf16_t* __restrict__ x, size_t psx, const double4* __restrict__ coef,
+    bf16_t* __restrict__ gx, size_t psgx, uint32_t rows, uint32_t rows_per_slice,
+    FastDiv d_grows, int C8) {
+  const int nch = C8 / 8, ct = blockIdx.y;
+  const int L = min(nch - ct * 32, 32), R = 256 / L;
+  const int t = threadIdx.x, cl = t % L, rl = t / L;
+  if (rl >= R) return;
+  const int cc = ct * 32 + cl;
+  const uint32_t r0 = blockIdx.x * rows_per_slice, r1 = min(rows, r0 + rows_per_slice);
+  double P[8], Q[8], Rc[8];
+  uint32_t cur = 0xFFFFFFFFu;
+  for (uint32_t r = r0 + rl; r < r1; r += R) {
+    const uint32_t gi = d_grows.div(r);
+    if (gi != cur) {
+      cur = gi;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double4 pqr = coef[(size_t)gi * C8 + cc * 8 + j];
+        P[j] = pqr.x;
+        Q[j] = pqr.y;
+        Rc[j] = pqr.z;
+      }
+    }
+    const size_t off = (size_t)r * C8 + cc * 8;
     float v[8], gv[8];
     load_split8(x + off, psx, v);
     load_split8(g + off, psg, gv);
     if (mask) apply_mask8(mask + off, gv);
-    const double4* cf = coef + (size_t)gi * C8 + cc * 8;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double4 pqr = cf[j];
-      v[j] = (float)fma(pqr.x, (double)gv[j], fma(pqr.y, (double)v[j], pqr.z));
-    }
+    for (int j = 0; j < 8; ++j) v[j] = (float)fma(P[j], (double)gv[j], fma(Q[j], (double)v[j], Rc[j]));
     store_split8(gx + off, psgx, v);
   }
 }
