@@ -1540,11 +1540,11 @@ int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t 
 /* ---- ResNet-trunk kinds (semantics: oracle bn_* / gap_* / residual) ---- */
 
 namespace {
-// slices per group for the BatchNorm reductions: ~4 blocks per SM in total,
-// at least 256 rows per slice
-int bn_slices(size_t grows, int G, int tiles) {
+// slices per group for the BatchNorm passes: ~4 blocks per SM in total, at
+// least `min_rows` rows per slice (small late-stage layers still fill the GPU)
+int bn_slices(size_t grows, int G, int tiles, int min_rows = 64) {
   const long want = std::max(1L, (long)(4 * num_sms()) / std::max(1, G * tiles));
-  const long cap = std::max(1L, (long)((grows + 255) / 256));
+  const long cap = std::max(1L, (long)((grows + min_rows - 1) / min_rows));
   return (int)std::min(want, cap);
 }
 }  // namespace
@@ -1571,7 +1571,7 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
                                                           slices, C, C8, (double)grows,
                                                           (double)eps);
   const uint32_t rows = (uint32_t)N * HW;
-  const int aslices = bn_slices(rows, 1, tiles);
+  const int aslices = bn_slices(rows, 1, tiles, 16);
   const uint32_t arps = (rows + aslices - 1) / aslices;
   bn_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(cb(x), psx, coef, cb(res), psr, mb(y), psy,
                                                         rows, arps, FastDiv((uint32_t)grows), C8,
@@ -1603,7 +1603,7 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
                                                     slices, C, C8, (double)grows, accumulate);
   if (gx) {
     const uint32_t rows = (uint32_t)N * HW;
-    const int aslices = bn_slices(rows, 1, tiles);
+    const int aslices = bn_slices(rows, 1, tiles, 16);
     const uint32_t arps = (rows + aslices - 1) / aslices;
     bn_bwd_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(
         cb(g), psg, cb(mask), cb(x), psx, coef, mb(gx), psgx, rows, arps,
