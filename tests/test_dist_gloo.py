@@ -17,7 +17,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, n_conv, n_fc, port, q):
+def _worker(rank, world, n_conv, n_fc, port, q, gap_view=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -29,6 +29,8 @@ def _worker(rank, world, n_conv, n_fc, port, q):
             i = comm.index
             acts = torch.full((k, a), float(i + 1)) + torch.arange(k * a).reshape(k, a) / 100
             labels = torch.full((k,), i, dtype=torch.int32)
+            if gap_view:   # a global-pool boundary: NHWC [K,1,1,C8] rows, same bytes as [K,C8]
+                acts = acts.reshape(k, 1, 1, a)
             comm.gather_activations([acts, labels], None)
             gy = torch.zeros(k, a)
             comm.scatter_boundary(None, [gy])
@@ -53,13 +55,16 @@ def _worker(rank, world, n_conv, n_fc, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_conv,n_fc", [(1, 1), (2, 1), (2, 2), (3, 1)])
-def test_role_exchange(n_conv, n_fc):
+@pytest.mark.parametrize("n_conv,n_fc,gap_view", [(1, 1, False), (2, 1, False), (2, 2, False),
+                                                 (3, 1, False), (2, 1, True)])
+def test_role_exchange(n_conv, n_fc, gap_view):
+    """gap_view: the CONV side sends its boundary as the [K,1,1,C] tensor a
+    ResNet trunk's global pool leaves into [K,C] rows."""
     world = n_conv + n_fc
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, n_conv, n_fc, port, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, n_conv, n_fc, port, q, gap_view))
              for r in range(world)]
     for p in procs:
         p.start()
