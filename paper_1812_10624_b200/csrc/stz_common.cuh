@@ -43,6 +43,15 @@ struct FastDiv {
 
 __host__ __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 
+// one 256-bit global store (STG.E.256 on sm_100): a warp storing 32 rows x
+// 8 floats writes 32 whole 32-byte sectors in one instruction instead of
+// 64 half sectors in two.  p must be 32-byte aligned.
+__device__ __forceinline__ void stg256(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // shared-memory / barrier wrappers
 // ---------------------------------------------------------------------------

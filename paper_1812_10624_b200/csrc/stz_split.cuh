@@ -301,8 +301,12 @@ struct EpF32 {
         w[4] = __fadd_rn(b.x, w[4]); w[5] = __fadd_rn(b.y, w[5]);
         w[6] = __fadd_rn(b.z, w[6]); w[7] = __fadd_rn(b.w, w[7]);
       }
-      dst[0] = make_float4(w[0], w[1], w[2], w[3]);
-      dst[1] = make_float4(w[4], w[5], w[6], w[7]);
+      if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+        stg256(out + row + n0, w);
+      } else {
+        dst[0] = make_float4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_float4(w[4], w[5], w[6], w[7]);
+      }
       return;
     }
 #pragma unroll

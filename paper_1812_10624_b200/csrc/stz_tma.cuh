@@ -496,10 +496,13 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
             continue;
           } else if (p.partial) {
             if (m < p.M) {
-              float4* dst =
-                  reinterpret_cast<float4*>(p.partial + ((size_t)z * p.M + m) * npad + nb);
-              dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-              dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+              float* dst = p.partial + ((size_t)z * p.M + m) * npad + nb;
+              if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+                stg256(dst, v);
+              } else {
+                reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+              }
             }
           } else {
             if (EP::HAS_BIAS) {
