@@ -1398,6 +1398,29 @@ int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void*
                     int p, void* ws, size_t ws_bytes, void* stream) {
   const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
   if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_dgrad: bad shape");
+  if (k == 1 && s > 1 && p == 0 && tma_on() && O8 % 32 == 0 && (size_t)N * H * W < (1u << 31)) {
+    // 1x1 stride-s (ResNet projection shortcut): input pixel (s*oh, s*ow)
+    // receives g[oh, ow] . W and every other pixel 0 -- a plain GEMM over the
+    // output rows whose epilogue scatters each row to its input pixel, after
+    // zeroing gx
+    cudaStream_t st = as_stream(stream);
+    const size_t plane = (size_t)N * H * W * C8 * sizeof(bf16_t);
+    for (int q = 0; q < 3; ++q)
+      if (cudaMemsetAsync(mb(gx) + q * psgx, 0, plane, st) != cudaSuccess)
+        return fail(STZ_ECUDA, "conv_dgrad: memset");
+    EpSplit e{mb(gx), psgx, N * OH * OW, C, C8, nullptr, cb(mask), 0};
+    e.rs = s;
+    e.rH = H;
+    e.rW = W;
+    e.rd_ow = FastDiv(OW);
+    e.rd_oh = FastDiv(OH);
+    const int M = N * OH * OW;
+    const TgShape sh = tg_shape(M, C, O8, ws_bytes);
+    TgOperand a, b;
+    if (op_tiled_k(a, cb(g), psg, M, O8, O8, TG_BM * sh.MH) &&
+        op_tiled_k(b, cb(wd), psw, C, O8, O8, sh.BN / sh.CL))
+      return run_tgemm("conv_dgrad[1x1s]", sh, a, b, e, M, C, O8, ws, ws_bytes, st);
+  }
   EpSplit e{mb(gx), psgx, N * H * W, C, C8, nullptr, cb(mask), 0};
   return gemm_conv_dgrad(cb(g), psg, cb(wd), psw, e, N, C, H, W, O8, k, s, p, OH, OW, ws,
                          ws_bytes, as_stream(stream));

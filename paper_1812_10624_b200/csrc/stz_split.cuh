@@ -217,6 +217,11 @@ struct EpSplit {
   const float* bias;
   const bf16_t* mask;
   int relu;
+  // strided row scatter (a 1x1 stride-rs conv's input gradient): GEMM row
+  // m = (n, oh, ow) of the output grid lands on input pixel (n, rs*oh, rs*ow)
+  // of the rH x rW input; rs = 0 keeps rows in place
+  int rs = 0, rH = 0, rW = 0;
+  FastDiv rd_ow, rd_oh;
   static constexpr bool HAS_BIAS = true;
   __device__ __forceinline__ void bias8(int n0, float (&b)[8]) const {
     if (bias) {
@@ -229,7 +234,14 @@ struct EpSplit {
   // v already includes the bias
   __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const {
     if (m >= M || n0 >= ld) return;
-    const size_t base = (size_t)m * ld + n0;
+    size_t row = (size_t)m;
+    if (rs) {
+      uint32_t q, ow, n, oh;
+      rd_ow.divmod((uint32_t)m, q, ow);
+      rd_oh.divmod(q, n, oh);
+      row = ((size_t)n * rH + (size_t)rs * oh) * rW + (size_t)rs * ow;
+    }
+    const size_t base = row * ld + n0;
     uint4 mk = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     if (mask) mk = __ldg(reinterpret_cast<const uint4*>(mask + base));   // 8 bf16, 16-B aligned
     const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};

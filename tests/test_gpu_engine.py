@@ -239,6 +239,8 @@ def test_micro_batches_match_full_batch(schedule):
 
 RESNET_STRIDED = [  # (layers factory, in_shape, batch): ResNet-50 stage-4 shapes at 64x64
     ("proj1x1s2", lambda m: [m.Conv2d(1024, 2048, 1, 2)], (1024, 4, 4), 2),
+    ("proj1x1s2_relu_in", lambda m: [m.Conv2d(64, 256, 3, 1, 1), m.ReLU(), m.Conv2d(256, 512, 1, 2)],
+     (64, 15, 15), 2),
     ("c3x3s2", lambda m: [m.Conv2d(512, 512, 3, 2, 1)], (512, 4, 4), 2),
     ("c3x3s2_c64", lambda m: [m.Conv2d(64, 64, 3, 2, 1)], (64, 16, 16), 2),
     ("c1x1_reduce", lambda m: [m.Conv2d(256, 64, 1)], (256, 14, 14), 2),
