@@ -52,6 +52,8 @@ def parse():
                          "(default) or NCCL all_reduce + SGD")
     ap.add_argument("--micro", type=int, default=None,
                     help="micro-batches per iteration for N>1 (default: 4 when K allows)")
+    ap.add_argument("--no-nvlink-probe", action="store_true",
+                    help="N>1: skip the untimed CONV<->FC transfer probe after the step")
     return ap.parse_args()
 
 
@@ -254,6 +256,85 @@ def committed_traffic(kernel_key: str):
             return json.load(fh).get(kernel_key)
     except (OSError, ValueError):
         return None
+
+
+def nvlink_probe(torch, dist, comm, dev, per_conv: int, reps: int = 10):
+    """CONV<->FC transfer rates over NVLink, timed OUTSIDE the step.
+
+    Inside the step the gather/scatter overlap compute and the phase clocks
+    include waiting, so neither gives a transfer rate.  Here every rank posts
+    exactly one micro-batch's exchange through the step's own RoleComm calls
+    (post_activations = the many-to-one gather, post_boundary = the
+    one-to-many scatter, stanza_runtime.py:228-307 in the reference), timed
+    between two barriers with CUDA events after wait(), max over ranks,
+    median of `reps`.  `link_GBps` is one 256 MiB NCCL send CONV 0 -> its FC
+    worker, the measured single-peer ceiling the fractions are taken against."""
+    fan = max(len(comm.members(i)) for i in range(comm.n_fc))
+    n_el = per_conv // 4
+
+    def timed(post_fn, make):
+        out = []
+        for r in range(reps + 3):
+            send, recv = make()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            for req in post_fn(send, recv):
+                req.wait()
+            b.record()
+            torch.cuda.synchronize(dev)
+            t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if r >= 3:
+                out.append(float(t.item()))
+        return statistics.median(out)
+
+    buf_c = torch.empty(n_el, dtype=torch.float32, device=dev)
+    bufs_f = [torch.empty(n_el, dtype=torch.float32, device=dev)
+              for _ in range(len(comm.members(comm.index)))] if not comm.is_conv else []
+
+    def make_gather():
+        return ([buf_c], None) if comm.is_conv else (None, [[t] for t in bufs_f])
+
+    def make_scatter():
+        return (None, [buf_c]) if comm.is_conv else ([[t] for t in bufs_f], None)
+
+    g_ms = timed(comm.post_activations, make_gather)
+    s_ms = timed(comm.post_boundary, make_scatter)
+    # single-peer ceiling: CONV 0 -> its FC worker
+    big = 256 << 20
+    src, dst = 0, comm.fc_rank_of(0)
+    link = torch.empty(big // 4, dtype=torch.float32, device=dev) \
+        if comm.rank in (src, dst) else None
+
+    def post_link(send, recv):
+        if comm.rank == src:
+            return dist.batch_isend_irecv([dist.P2POp(dist.isend, link, dst,
+                                                      group=comm.act_group)])
+        if comm.rank == dst:
+            return dist.batch_isend_irecv([dist.P2POp(dist.irecv, link, src,
+                                                      group=comm.act_group)])
+        return []
+
+    l_ms = timed(post_link, lambda: (None, None))
+    link_gbs = big / (l_ms / 1e3) / 1e9
+    gather_gbs = fan * per_conv / (g_ms / 1e3) / 1e9
+    scatter_gbs = fan * per_conv / (s_ms / 1e3) / 1e9
+    return {
+        "gather_GBps": gather_gbs, "scatter_GBps": scatter_gbs,
+        "gather_ms": g_ms, "scatter_ms": s_ms,
+        "link_GBps": link_gbs, "gather_frac": gather_gbs / link_gbs,
+        "scatter_frac": scatter_gbs / link_gbs,
+        "bytes_per_conv_worker": per_conv, "fan_in": fan,
+        "note": ("one step's [K,A] CONV->FC gather and FC->CONV scatter through "
+                 "RoleComm.post_activations / post_boundary (NCCL P2P over NVLink), "
+                 "timed alone between barriers (CUDA events, max over ranks, median of "
+                 f"{reps}); GBps = bytes into / out of the busiest FC worker "
+                 "(fan_in x bytes_per_conv_worker) / time; frac against link_GBps = one "
+                 "256 MiB NCCL send between two GPUs measured in the same run"),
+    }
 
 
 def main():
@@ -511,6 +592,10 @@ def main():
         "calls": per_call,
     }
 
+    probe = None
+    if world > 1 and not args.no_nvlink_probe:
+        probe = nvlink_probe(torch, dist, comm, dev, k * cl.boundary_activations * 4)
+
     line = None
     # gather per-rank extras to rank 0
     extras = {"rank": rank, "role": "conv" if is_conv_rank else "fc", "phase_ms": phase_ms,
@@ -523,22 +608,7 @@ def main():
     if rank == 0:
         conv_ex = next(o for o in objs if o["role"] == "conv")
         fc_ex = next((o for o in objs if o["fc_tflops"] is not None), conv_ex)
-        nvlink = None
-        if world > 1:
-            act_bytes = n_conv * k * cl.boundary_activations * 4
-            # the FC side's gather phase includes waiting for the CONV forward and
-            # the CONV side's scatter phase includes the FC step, so each transfer
-            # is timed on the rank that is already ready when it starts
-            per_conv = k * cl.boundary_activations * 4
-            send_ms = max(o["phase_ms"]["activations"] for o in objs if o["role"] == "conv")
-            scat_ms = max(o["phase_ms"]["boundary"] for o in objs if o["role"] == "fc")
-            nvlink = {
-                "gather_GBps": per_conv / (send_ms / 1e3) / 1e9 if send_ms else None,
-                "scatter_GBps": act_bytes / n_fc / (scat_ms / 1e3) / 1e9 if scat_ms else None,
-                "peak_GBps": 770.0,
-                "bytes_per_conv_worker": per_conv,
-                "note": "gather: one CONV worker's [K,A] send / its phase time; scatter: an "
-                        "FC worker's outgoing boundary rows / its phase time (NCCL P2P)"}
+        nvlink = probe
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             secs = [oracle_sample(args.model) for _ in range(2)]
