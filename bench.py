@@ -52,6 +52,8 @@ def parse():
                          "(default) or NCCL all_reduce + SGD")
     ap.add_argument("--micro", type=int, default=None,
                     help="micro-batches per iteration for N>1 (default: 4 when K allows)")
+    ap.add_argument("--no-autotune", action="store_true",
+                    help="keep the cost model's GEMM tile shapes (no measured override)")
     ap.add_argument("--no-nvlink-probe", action="store_true",
                     help="N>1: skip the untimed CONV<->FC transfer probe after the step")
     return ap.parse_args()
@@ -404,8 +406,15 @@ def main():
 
     # warm-up (W >= 3 enforced)
     warm = max(args.warmup, 3)
+    tiles = {}
     for i in range(warm):
-        one(i, slots[i % slots.numel():i % slots.numel() + 1])
+        sl = slots[i % slots.numel():i % slots.numel() + 1]
+        if i == 0 and not args.no_autotune:
+            # measured GEMM tile shapes (_lib.autotune_tiles), chosen on the
+            # first (eager) warm-up step, before any CUDA graph is captured
+            tiles = _lib.autotune_tiles(lambda: one(0, sl))
+        else:
+            one(i, sl)
     sync_all()
 
     # one process per GPU: StanzaCluster captures each compute segment as a
@@ -634,6 +643,7 @@ def main():
                             "(overlapping the previous step) and its loss copied back")},
             "gpu_launches": int(sum(o["launches"] for o in objs)),
             "cuda_graph": bool(graphs is not None),
+            "tile_overrides": {f"{kk[1]}": list(v) for kk, v in tiles.items()},
             "clocks": clocks.summary(),
             "fc_tensor_pipe_frac": (6 * fc_ex["fc_tflops"] / bf16_peak)
             if fc_ex["fc_tflops"] else None,

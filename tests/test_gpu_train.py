@@ -166,3 +166,59 @@ def test_fc_replica_digest_and_recovery(lib):
     assert cl.restore_fc_replica() == 3
     res = cl.train(3)
     assert param_digest(res.state.params) == param_digest(whole.state.params)
+
+
+@pytest.mark.parametrize("tile", [(192, 1), (128, 2), (64, 1)])
+def test_tile_overrides_match_oracle(lib, tile):
+    """GEMM calls listed in _lib.TILE_TABLE (measured tile overrides, as
+    autotune_tiles installs them) keep parity: AlexNet shapes at K=2, every
+    GEMM forced to one tile shape, 1 iteration vs the oracle."""
+    from contextlib import contextmanager
+    from paper_1812_10624_b200 import _lib, model_partition as mp
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+    spec = mp.alexnet(batch_k=2)
+    mk = orc.batch_fn(spec.input_shape, 2, 7, classes=1000)
+    layers = [tuple_of(l) for l in spec.layers]
+    ref_p, _, ref_l = orc.layer_separated_train(layers, 2, 1, 1, 1, 3, mk)
+    keys = set()
+
+    @contextmanager
+    def record(name, args, flops=0.0, tag=None, nbytes=0.0):
+        if flops > 0:
+            keys.add((name, tag, flops))
+        yield
+
+    probe = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=mk, lr=0.05, momentum=0.9,
+                          seed=3, device="cuda:0")
+    _lib.PROFILE_HOOK = record
+    try:
+        probe.train(1)
+    finally:
+        _lib.PROFILE_HOOK = None
+    assert keys
+    _lib.TILE_TABLE.update({k: tile for k in keys})
+    try:
+        cl = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=mk, lr=0.05, momentum=0.9,
+                           seed=3, device="cuda:0")
+        out = cl.train(1)
+    finally:
+        _lib.TILE_TABLE.clear()
+    assert orc.max_param_dev(out.state.params, ref_p) <= TOL
+    np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)
+
+
+def test_autotune_tiles_installs_valid_table(lib):
+    from paper_1812_10624_b200 import _lib, model_partition as mp
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+    spec = mp.alexnet(batch_k=2)
+    mk = orc.batch_fn(spec.input_shape, 2, 7, classes=1000)
+    cl = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=mk, lr=0.05, momentum=0.9, seed=3,
+                       device="cuda:0")
+    try:
+        table = _lib.autotune_tiles(lambda: cl.train(1), reps=2)
+        assert table is not _lib.TILE_TABLE and table == _lib.TILE_TABLE
+        for (name, tag, flops), (bn, c) in table.items():
+            assert flops > 0 and (bn, c) in _lib._TILE_CANDIDATES
+        cl.train(1)   # runs under the installed overrides
+    finally:
+        _lib.TILE_TABLE.clear()

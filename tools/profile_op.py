@@ -77,6 +77,25 @@ if os.environ.get("STZ_SWEEP"):   # time every tile configuration (model-chosen 
         torch.cuda.synchronize()
         print(f"  tile bn={bn} cl={cl}: {e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
     lib.stz_set_tile(0, 0, 0)
+    if os.environ.get("STZ_SWEEP") == "2":   # split counts per tile as well
+        for bn, cl in ((64, 1), (96, 1), (128, 1), (192, 1), (128, 2), (192, 2), (256, 2)):
+            row = []
+            for sp in (4, 8, 16, 24, 32, 48, 64, 96, 128, 148, 192, 256):
+                if lib.stz_set_tile(bn, cl, sp) != 0:
+                    continue
+                try:
+                    _lib.call(name, *args)
+                except Exception as exc:  # workspace too small for this split count
+                    row.append(f"{sp}:-")
+                    continue
+                e0.record()
+                for _ in range(20):
+                    _lib.call(name, *args)
+                e1.record()
+                torch.cuda.synchronize()
+                row.append(f"{sp}:{e0.elapsed_time(e1) / 20:.4f}")
+            print(f"  tile bn={bn} cl={cl} splits->ms " + " ".join(row), flush=True)
+        lib.stz_set_tile(0, 0, 0)
 if os.environ.get("STZ_DEBUG"):   # capture a diagnostic variant (stz_set_debug flags)
     _lib.load().stz_set_debug(int(os.environ["STZ_DEBUG"]))
 torch.cuda.nvtx.range_push("replay")
