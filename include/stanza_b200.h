@@ -64,7 +64,10 @@ int stz_set_band(int on);
 
 /* Force the TMA GEMM tile (tests / tuning): width bn in {64, 96, 128, 192,
  * 256}, cl = 2 for CTA pairs (required for 256; 64 / 96 run unpaired),
- * splits = K splits (0 = 1).  bn = 0 restores the cost-model choice. */
+ * splits = K splits (0 = the cost model's count for that tile, never below the
+ * per-tile accumulation cap).  bn = 0 restores the cost-model choice.  The
+ * setting is process-global host state read at launch, so a caller brackets
+ * one call with it (paper_1812_10624_b200/_lib.py: call, autotune_tiles). */
 int stz_set_tile(int bn, int cl, int splits);
 
 /* GEMM pipeline diagnostics (results are WRONG while set): 1 skips epilogue
