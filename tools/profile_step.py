@@ -14,6 +14,9 @@ spec = builtin_model(model, k)
 cl = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=None, lr=0.01, seed=3, device="cuda:0")
 x = torch.randn(cl.x.shape, device="cuda:0")
 y = torch.randint(0, 1000, cl.labels.shape, device="cuda:0", dtype=torch.int32)
+# the bench's measured tile overrides (off with STZ_AUTOTUNE=0)
+if os.environ.get("STZ_AUTOTUNE", "1") != "0":
+    print("tile overrides:", _lib.autotune_tiles(lambda: cl.step(x=x, labels=y)))
 for _ in range(2):
     cl.step(x=x, labels=y)
 torch.cuda.synchronize()
