@@ -546,6 +546,26 @@ class StanzaCluster:
 
     # -- public API ------------------------------------------------------------------
 
+    def autotune_tiles(self, x: torch.Tensor | None = None,
+                       labels: torch.Tensor | None = None) -> dict:
+        """Measure the GEMM tile shapes of this cluster's step on this GPU
+        (`_lib.autotune_tiles`) and install the winners for every later step
+        and capture.  Runs one full iteration (like step(); its loss is not
+        recorded), on every rank when the cluster spans processes.  The
+        parameters and velocities this process holds are restored afterwards
+        (and their split-plane weight copies repacked), so training continues
+        from the same state as without it."""
+        from . import _lib
+        engines = [e for e in [self.conv, *self.fcs] if e is not None]
+        saved = [(e.params_flat.clone(), e.vel_flat.clone()) for e in engines]
+        table = _lib.autotune_tiles(lambda: self.step(None, x=x, labels=labels))
+        for e, (pf, vf) in zip(engines, saved):
+            e.params_flat.copy_(pf)
+            e.vel_flat.copy_(vf)
+            e.pack_weights()
+        torch.cuda.synchronize(self.device)
+        return table
+
     def train(self, iterations: int) -> StanzaResult:
         """Run `iterations` more iterations; may be called repeatedly."""
         slots = torch.zeros(max(iterations, 1), dtype=torch.float64, device=self.device)

@@ -222,3 +222,23 @@ def test_autotune_tiles_installs_valid_table(lib):
         cl.train(1)   # runs under the installed overrides
     finally:
         _lib.TILE_TABLE.clear()
+
+
+@pytest.mark.parametrize("case", ["tiny_1x1", "tiny_3x2"])
+def test_cluster_autotune_keeps_parity(lib, case):
+    """StanzaCluster.autotune_tiles runs a step, restores the state, installs
+    the measured tiles; the following training matches the reference golden."""
+    from paper_1812_10624_b200 import _lib
+    g = golden_io.train()[f"train_{case}"]
+    spec = _spec(case.split("_")[0])
+    cl = _cluster(spec, int(g["n_conv"]), int(g["n_fc"]), int(g["seed"]), int(g["data_seed"]))
+    try:
+        cl.load_batch(0)
+        cl.autotune_tiles()
+        res = cl.train(int(g["iters"]))
+    finally:
+        _lib.TILE_TABLE.clear()
+    ref_p, ref_v = golden_io.nested_state(g)
+    assert orc.max_param_dev(res.state.params, ref_p) <= TOL
+    assert orc.max_param_dev(res.state.velocities, ref_v) <= 1e-4
+    np.testing.assert_allclose(res.losses, g["losses"], rtol=TOL)
