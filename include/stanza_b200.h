@@ -283,8 +283,11 @@ int stz_ipc_handle(const void* dptr, void* handle, size_t* offset);
 int stz_ipc_open(const void* handle, void** base);
 int stz_ipc_close(void* base);
 
-/* Timeout after which a peer barrier that is still waiting traps (loud
- * failure instead of a hung GPU); 0 restores the default 60 s. */
+/* Timeout after which a peer wait (exchange barrier, link get) gives up: it
+ * writes a status word (flags[17] of the exchange block, word
+ * STZ_LINK_STATUS of the link block), later kernels of that member skip
+ * their work, and the host raises MissingSource (the reference's
+ * stanza_runtime.py:37-38, :77-82, :295-299); 0 restores the default 60 s. */
 int stz_set_peer_timeout_ms(unsigned long long ms);
 
 /* Stream-ordered barrier of the group: returns (on the stream) once every
@@ -318,6 +321,45 @@ int stz_sgd_momentum_pack(float* w, float* v, const float* g, size_t n, float lr
 int stz_allreduce_sgd(const float* const* grads, float* const* red, unsigned* const* flags,
                       int nranks, int me, float* w, float* v, size_t n, float lr, float mu,
                       float inv_n, const stz_plane_range* ranges, int nranges, void* stream);
+
+/* ===========================================================================
+ * CONV <-> FC link over peer memory: the many-to-one activation gather
+ * (_activations_phase + collect_group_activations, stanza_runtime.py:64-85,
+ * :228-253) and the one-to-many boundary-gradient scatter (_boundary_phase,
+ * :278-307) of the layer-separated step, one message per (CONV worker,
+ * micro-batch), 4 bytes per element on the link.
+ *
+ * Every rank owns a link flag block of STZ_LINK_FLAG_WORDS uint32 (zeroed
+ * once; IPC-mapped by its link peers) and an fp32 staging buffer for what it
+ * receives.  Per step: stz_link_begin on every rank; the sender's
+ * stz_link_put stores its split-plane rows as fp32 into the receiver's
+ * staging rows (and labels into the receiver's label rows) and then publishes
+ * its epoch in the receiver's message slot; the receiver's stz_link_get waits
+ * for the slots of one micro-batch and splits the staged rows into its local
+ * split-plane buffer.  All stream-ordered device work (no host sync).
+ * ===========================================================================
+ */
+#define STZ_LINK_FLAG_WORDS 256
+#define STZ_LINK_SLOTS 192
+#define STZ_LINK_EPOCH 240
+#define STZ_LINK_STATUS 241
+
+/* epoch += 1 on the rank's link block (once per step, before its puts/gets) */
+int stz_link_begin(unsigned* flags, void* stream);
+
+/* src: split planes [rows][D8] (plane stride ps, 16-byte aligned); dst: the
+ * receiver's fp32 staging rows [rows][D] (peer pointer); labels (optional):
+ * rows int32 copied to labels_dst (peer pointer); then
+ * *remote_slot = this rank's epoch (release, system scope). */
+int stz_link_put(const void* src, size_t ps, int rows, int D, int D8, float* dst,
+                 const int* labels, int* labels_dst, unsigned* my_flags, unsigned* remote_slot,
+                 void* stream);
+
+/* Wait until my_flags[slot0 + i*slot_stride] >= this rank's epoch for every
+ * i < nslots (timeout: status word, see stz_set_peer_timeout_ms), then
+ * src fp32 [rows][D] -> split planes dst [rows][D8] (plane stride ps). */
+int stz_link_get(const float* src, int rows, int D, void* dst, size_t ps, int D8,
+                 unsigned* my_flags, int slot0, int nslots, int slot_stride, void* stream);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,10 @@ SIGNATURES = {
     "stz_peer_reduce_push": (I, [P, P, I, I, Z, P]),
     "stz_sgd_momentum_pack": (I, [P, P, P, Z, F, F, F, P, I, P]),
     "stz_allreduce_sgd": (I, [P, P, P, I, I, P, P, Z, F, F, F, P, I, P]),
+    # CONV <-> FC link over peer memory
+    "stz_link_begin": (I, [P, P]),
+    "stz_link_put": (I, [P, Z, I, I, I, P, P, P, P, P, P]),
+    "stz_link_get": (I, [P, I, I, P, Z, I, P, I, I, I, P]),
 }
 
 
@@ -93,6 +97,11 @@ class PlaneRange(ctypes.Structure):
 
 IPC_HANDLE_BYTES = 64
 PEER_FLAG_WORDS = 32
+PEER_FLAG_STATUS = 17          # exchange block: != 0 after a barrier timed out
+LINK_FLAG_WORDS = 256
+LINK_SLOTS = 192
+LINK_EPOCH = 240
+LINK_STATUS = 241              # link block: kStatusLink | slot after a get timed out
 
 
 def ptr_array(ptrs) -> ctypes.Array:
@@ -173,13 +182,16 @@ def autotune_tiles(run_step, reps: int = 5, gain: float = 0.97) -> dict:
     """Time every GEMM call of one step under each tile shape and keep the
     measured winner where it beats the cost model's pick by > 3%.
 
-    ``run_step()`` runs one eager step; its GEMM calls (every call carrying
-    algorithmic FLOPs) are recorded with their arguments and replayed on the
-    current stream with CUDA events -- like a convolution autotuner, the
-    replays overwrite that step's outputs, so run it before real training
-    steps (or before the warm-up).  Split counts stay the model's, so the
-    accumulation cap per tile is unchanged.  Returns and
-    installs the table."""
+    ``run_step()`` runs one EAGER step (no graph replay: replays bypass this
+    module and record nothing); its GEMM calls (every call carrying
+    algorithmic FLOPs) are recorded with their arguments and replayed with
+    CUDA events on the stream each call was launched on -- like a
+    convolution autotuner, the replays overwrite that step's outputs, so run
+    it before real training steps (or before the warm-up).  A forced tile
+    keeps the accumulation cap per work item but the library
+    re-derives the split count for the new width.  Returns and installs the
+    table; when the step recorded no GEMM the installed table is left
+    unchanged."""
     global PROFILE_HOOK
     import torch
     from contextlib import contextmanager
@@ -196,19 +208,25 @@ def autotune_tiles(run_step, reps: int = 5, gain: float = 0.97) -> dict:
         run_step()
     finally:
         PROFILE_HOOK = prev
+    if not seen:
+        return {}
     lib = load()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def timed(name, args):
         fn = getattr(lib, name)
+        st = args[-1]                          # every GEMM entry ends with its stream
+        stream = torch.cuda.ExternalStream(int(st.value or 0)) if isinstance(
+            st, ctypes.c_void_p) and st.value else torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         if fn(*args) != 0:
             return None
-        e0.record()
+        e0.record(stream)
         for _ in range(reps):
             fn(*args)
-        e1.record()
-        torch.cuda.synchronize()
+        e1.record(stream)
+        e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
     table = {}

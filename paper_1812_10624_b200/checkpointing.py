@@ -95,6 +95,14 @@ def state_to_bytes(state: TrainState) -> bytes:
     return _STZC + struct.pack(_STZC_HEAD, _STZC_VERSION, state.iteration, len(p), len(v)) + p + v
 
 
+def stzc_blob_len(shapes) -> int:
+    """Byte length of state_to_bytes for a block whose tensors have the
+    nested ``shapes`` [layer][tensor] -- without building the blob."""
+    stzt = 16 + 4 * len(shapes) + sum(4 + 4 * len(s) + 4 * int(np.prod(s, dtype=np.int64))
+                                      for row in shapes for s in row)
+    return 4 + struct.calcsize(_STZC_HEAD) + 2 * stzt
+
+
 def state_from_bytes(blob: bytes) -> TrainState:
     head = 4 + struct.calcsize(_STZC_HEAD)
     if len(blob) < head or blob[:4] != _STZC:

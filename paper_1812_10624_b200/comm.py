@@ -15,11 +15,22 @@ All of it is expressed with torch.distributed point-to-point ops and
 sub-group collectives, so the same code runs over NCCL on B200s and over
 gloo on CPU tensors (the multi-process CPU tests).
 
-Micro-batch pipelining posts the two P2P directions
-asynchronously: a CONV worker sends every micro-batch's activations before
-it receives any boundary gradient, while its FC worker alternates receive /
-compute / send.  Each direction therefore runs on its own communicator (own
-NCCL stream), so neither queue can block the other.
+Two data paths:
+
+* ``PeerLink`` + ``PeerExchange`` (exchange="peer", the default between
+  GPUs of one node): the gather / scatter and the gradient exchange are
+  kernels that load and store peer memory mapped through CUDA IPC, ordered
+  by device-side flags (csrc/stz_peer.cuh).  torch.distributed only carries
+  the one-time handle exchange, so the process group can be NCCL or gloo --
+  gloo lets several ranks share one GPU (the multi-process parity tests on
+  a 1-GPU box).
+* NCCL point-to-point ops and sub-group allreduces (exchange="nccl"), which
+  also run over gloo on CPU tensors (the multi-process CPU tests).  Micro-
+  batch pipelining posts the two P2P directions
+  asynchronously: a CONV worker sends every micro-batch's activations before
+  it receives any boundary gradient, while its FC worker alternates receive
+  / compute / send.  Each direction therefore runs on its own communicator
+  (own NCCL stream), so neither queue can block the other.
 """
 
 from __future__ import annotations
@@ -76,6 +87,9 @@ class RoleComm:
 
     def fc_rank_of(self, conv_index: int) -> int:
         return self.n_conv + self.conv_to_fc[conv_index]
+
+    def fc_index_of(self, conv_index: int) -> int:
+        return self.conv_to_fc[conv_index]
 
     # -- exchanges --------------------------------------------------------------------
 
@@ -142,7 +156,32 @@ class RoleComm:
             dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
 
     def sum_scalar(self, t: torch.Tensor) -> None:
+        if t.is_cuda and dist.get_backend() != "nccl":
+            c = t.cpu()
+            dist.all_reduce(c, op=dist.ReduceOp.SUM)
+            t.copy_(c)
+            return
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    def p2p(self, sends=(), recvs=()) -> None:
+        """Blocking point-to-point transfers of whole tensors on the
+        activation communicator: ``sends`` = [(tensor, dst_rank)], ``recvs``
+        = [(tensor, src_rank)].  Device tensors are staged through host
+        memory when the process group is not NCCL (gloo)."""
+        staged = dist.get_backend() != "nccl"
+        ops, back = [], []
+        for t, r in sends:
+            ops.append(dist.P2POp(dist.isend, t.cpu() if staged and t.is_cuda else t, r,
+                                  group=self.act_group))
+        for t, r in recvs:
+            buf = torch.empty(t.shape, dtype=t.dtype) if staged and t.is_cuda else t
+            if buf is not t:
+                back.append((t, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, r, group=self.act_group))
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+        for t, buf in back:
+            t.copy_(buf)
 
     def barrier(self) -> None:
         dist.barrier()
@@ -160,6 +199,176 @@ class RoleComm:
         update (stz_allreduce_sgd)."""
         group, ranks = self.group_of_role()
         return PeerExchange(engine, group, ranks.index(self.rank), len(ranks))
+
+
+class _IpcMap:
+    """CUDA-IPC handles of local tensors and the mapping of peers' handles
+    (each peer allocation opened once)."""
+
+    def __init__(self):
+        self._opened: dict[bytes, int] = {}
+
+    @staticmethod
+    def handle(t: torch.Tensor):
+        from . import _lib
+        h = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+        off = ctypes.c_size_t(0)
+        _lib.call("stz_ipc_handle", ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off))
+        return bytes(h.raw), int(off.value)
+
+    def open(self, handle: bytes, off: int) -> int:
+        from . import _lib
+        base = self._opened.get(handle)
+        if base is None:
+            out = ctypes.c_void_p(0)
+            _lib.call("stz_ipc_open", ctypes.create_string_buffer(handle, len(handle)),
+                      ctypes.byref(out))
+            base = self._opened[handle] = int(out.value)
+        return base + off
+
+    def failure(self) -> str | None:
+        """Description of a timed-out barrier (reads the status word: syncs)."""
+        from . import _lib
+        st = int(self.flags[_lib.PEER_FLAG_STATUS].item())
+        if st == 0:
+            return None
+        return f"group member {st & 0xFFFF} never reached the gradient exchange"
+
+    def close(self) -> None:
+        self._ipc.close()
+
+
+class PeerLink:
+    """The CONV <-> FC link of the layer-separated step over peer memory
+    (reference _activations_phase / collect_group_activations /
+    _boundary_phase, stanza_runtime.py:64-85, :228-307; kernels
+    stz_link_* in csrc/stz_peer.cuh).
+
+    Per micro-batch j (kb = K / m rows per CONV worker):
+
+    * CONV worker i -> its FC worker: ``put_acts`` stores its kb boundary
+      rows as fp32 into the FC worker's staging rows [(j*g + pos)*kb, ...)
+      and its labels into the FC worker's label rows, then sets slot
+      pos*m + j; the FC worker's ``get_acts(j)`` waits for the g slots of
+      micro-batch j and splits the g*kb staged rows into its input rows --
+      the FC input is laid out [micro][member][kb], members ascending (the
+      reference's concat order, :266-267);
+    * FC worker -> each member: ``put_grads(j)`` stores member pos's kb
+      boundary-gradient rows into that member's staging rows [j*kb, ...)
+      and sets its slot j; the CONV worker's ``get_grads(j)`` waits and
+      splits them into its boundary-gradient rows.
+
+    Collective constructor (every rank of the world, handle exchange over
+    torch.distributed, any backend)."""
+
+    def __init__(self, comm: "RoleComm", device, k: int, micro: int, a: int,
+                 dst=None, labels=None):
+        from . import _lib
+        self.comm, self.k, self.m, self.a = comm, k, micro, a
+        self.kb = k // micro
+        dev = torch.device(device)
+        self.device = dev
+        self.flags = torch.zeros(_lib.LINK_FLAG_WORDS, dtype=torch.int32, device=dev)
+        self.dst = dst                 # Split receiving the split rows (FC input / CONV gboundary)
+        self.labels = labels           # FC: int32 [g*K] label rows
+        if comm.is_conv:
+            self.g = len(comm.members(comm.fc_index_of(comm.index)))
+            self.pos = comm.members(comm.fc_index_of(comm.index)).index(comm.index)
+            self.stage = torch.zeros(k * a, dtype=torch.float32, device=dev)
+        else:
+            self.g = len(comm.members(comm.index))
+            self.stage = torch.zeros(self.g * k * a, dtype=torch.float32, device=dev)
+        if self.g * micro > _lib.LINK_SLOTS:
+            raise ValueError(f"{self.g} members x {micro} micro-batches exceed "
+                             f"{_lib.LINK_SLOTS} link slots")
+        torch.cuda.synchronize(dev)       # flags are zero before any peer can write them
+        self._ipc = _IpcMap()
+        mine = [self._ipc.handle(self.flags), self._ipc.handle(self.stage),
+                self._ipc.handle(labels) if labels is not None else None]
+        objs = [None] * comm.world
+        dist.all_gather_object(objs, mine)
+        self.fail_word = None
+        if comm.is_conv:
+            fc = comm.fc_rank_of(comm.index)
+            fl, st, lb = objs[fc]
+            self._peer_flags = self._ipc.open(*fl)
+            self._peer_stage = self._ipc.open(*st)
+            self._peer_labels = self._ipc.open(*lb)
+        else:
+            self._members = []
+            for i in comm.members(comm.index):
+                fl, st, _ = objs[i]
+                self._members.append((self._ipc.open(*fl), self._ipc.open(*st)))
+        dist.barrier()
+
+    def _stream(self):
+        from .tensor_core import stream_of
+        return stream_of(self.device)
+
+    def begin(self) -> None:
+        from . import _lib
+        _lib.call("stz_link_begin", self.flags.data_ptr(), self._stream())
+
+    def put_acts(self, j: int, rows, labels: torch.Tensor) -> None:
+        """CONV side: ``rows`` = the Split view of micro-batch j's boundary
+        activations (kb rows), ``labels`` its kb int32 labels."""
+        from . import _lib
+        kb, a = self.kb, self.a
+        row0 = (j * self.g + self.pos) * kb
+        _lib.call("stz_link_put", rows.ptr(), rows.ps, kb, a, rows.width,
+                  self._peer_stage + row0 * a * 4, labels.data_ptr(),
+                  self._peer_labels + row0 * 4, self.flags.data_ptr(),
+                  self._peer_flags + 4 * (self.pos * self.m + j), self._stream(),
+                  nbytes=kb * a * 10.0 + kb * 8.0, tag="link_put_acts")
+
+    def get_acts(self, j: int) -> None:
+        """FC side: wait for every member's micro-batch j, then split its
+        g*kb staged rows into the input rows [j*g*kb, (j+1)*g*kb)."""
+        from . import _lib
+        gk = self.g * self.kb
+        out = self.dst.rows_view(j * gk, (j + 1) * gk)
+        _lib.call("stz_link_get", self.stage.data_ptr() + j * gk * self.a * 4, gk, self.a,
+                  out.ptr(), out.ps, out.width, self.flags.data_ptr(), j, self.g, self.m,
+                  self._stream(), nbytes=gk * self.a * 10.0, tag="link_get_acts")
+
+    def put_grads(self, j: int, rows) -> None:
+        """FC side: ``rows`` = the Split view of micro-batch j's g*kb boundary
+        gradient rows ([member][kb]); member pos gets its kb rows."""
+        from . import _lib
+        kb, a = self.kb, self.a
+        for pos, (fl, st) in enumerate(self._members):
+            v = rows.rows_view(pos * kb, (pos + 1) * kb)
+            _lib.call("stz_link_put", v.ptr(), v.ps, kb, a, v.width, st + j * kb * a * 4,
+                      None, None, self.flags.data_ptr(), fl + 4 * j, self._stream(),
+                      nbytes=kb * a * 10.0, tag="link_put_grads")
+
+    def get_grads(self, j: int) -> None:
+        """CONV side: wait for micro-batch j's boundary gradient, then split
+        it into rows [j*kb, (j+1)*kb) of the boundary-gradient buffer."""
+        from . import _lib
+        kb = self.kb
+        out = self.dst.rows_view(j * kb, (j + 1) * kb)
+        _lib.call("stz_link_get", self.stage.data_ptr() + j * kb * self.a * 4, kb, self.a,
+                  out.ptr(), out.ps, out.width, self.flags.data_ptr(), j, 1, 1,
+                  self._stream(), nbytes=kb * self.a * 10.0, tag="link_get_grads")
+
+    def failure(self) -> str | None:
+        """Description of a timed-out wait (reads the status word: syncs)."""
+        from . import _lib
+        st = int(self.flags[_lib.LINK_STATUS].item())
+        if st == 0:
+            return None
+        slot = st & 0xFFFF
+        epoch = int(self.flags[_lib.LINK_EPOCH].item())
+        if self.comm.is_conv:
+            src = f"fc{self.comm.fc_index_of(self.comm.index)}"
+            return f"no boundary gradients from {src} (micro-batch {slot}, step {epoch})"
+        pos, j = divmod(slot, self.m)
+        i = self.comm.members(self.comm.index)[pos]
+        return f"no activations from conv{i} (micro-batch {j}, step {epoch})"
+
+    def close(self) -> None:
+        self._ipc.close()
 
 
 class PeerExchange:
@@ -184,42 +393,23 @@ class PeerExchange:
         self.flags = torch.zeros(_lib.PEER_FLAG_WORDS, dtype=torch.int32, device=dev)
         self.red = torch.zeros(engine.total, dtype=torch.float32, device=dev) if nranks > 1 \
             else engine.grad_flat
-        self._opened: dict[bytes, int] = {}
+        self._ipc = _IpcMap()
         grads, reds, flags = [0] * nranks, [0] * nranks, [0] * nranks
         grads[me], reds[me], flags[me] = (engine.grad_flat.data_ptr(), self.red.data_ptr(),
                                           self.flags.data_ptr())
         if nranks > 1:
             torch.cuda.synchronize(dev)       # flags are zero before any peer can write them
-            mine = [self._handle(t) for t in (engine.grad_flat, self.red, self.flags)]
+            mine = [self._ipc.handle(t) for t in (engine.grad_flat, self.red, self.flags)]
             objs = [None] * nranks
             dist.all_gather_object(objs, mine, group=group)
             for j, theirs in enumerate(objs):
                 if j == me:
                     continue
-                grads[j], reds[j], flags[j] = (self._open(h, off) for h, off in theirs)
+                grads[j], reds[j], flags[j] = (self._ipc.open(h, off) for h, off in theirs)
             dist.barrier(group=group)
         self._grads = _lib.ptr_array(grads)
         self._reds = _lib.ptr_array(reds)
         self._flags = _lib.ptr_array(flags)
-
-    @staticmethod
-    def _handle(t: torch.Tensor):
-        from . import _lib
-        h = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
-        off = ctypes.c_size_t(0)
-        _lib.call("stz_ipc_handle", ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off))
-        return bytes(h.raw), int(off.value)
-
-    def _open(self, handle: bytes, off: int) -> int:
-        """Peer allocation base (opened once per allocation) + offset."""
-        from . import _lib
-        base = self._opened.get(handle)
-        if base is None:
-            out = ctypes.c_void_p(0)
-            _lib.call("stz_ipc_open", ctypes.create_string_buffer(handle, len(handle)),
-                      ctypes.byref(out))
-            base = self._opened[handle] = int(out.value)
-        return base + off
 
     def run(self, n: int, lr: float, mu: float) -> None:
         """This member's exchange + update of one iteration (collective: every
@@ -233,9 +423,14 @@ class PeerExchange:
                   float(mu), inv_batch(n), ranges, nr, stream_of(eng.device))
         eng.pack_weights(skip=fused)
 
-    def close(self) -> None:
+    def failure(self) -> str | None:
+        """Description of a timed-out barrier (reads the status word: syncs)."""
         from . import _lib
-        for base in self._opened.values():
-            _lib.call("stz_ipc_close", ctypes.c_void_p(base))
-        self._opened.clear()
+        st = int(self.flags[_lib.PEER_FLAG_STATUS].item())
+        if st == 0:
+            return None
+        return f"group member {st & 0xFFFF} never reached the gradient exchange"
+
+    def close(self) -> None:
+        self._ipc.close()
 

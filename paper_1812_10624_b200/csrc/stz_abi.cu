@@ -1888,8 +1888,48 @@ int stz_allreduce_sgd(const float* const* grads, float* const* red, unsigned* co
   }
   if (n == 0) return STZ_OK;
   const float* g = nranks > 1 ? red[me] : grads[me];
-  sgd_pack_kernel<<<grid_for(n / 4 + 1), 256, 0, st>>>(w, v, g, tab, lr, mu, inv_n);
+  sgd_pack_kernel<<<grid_for(n / 4 + 1), 256, 0, st>>>(
+      w, v, g, tab, lr, mu, inv_n, nranks > 1 ? t.flags[me] + kFlagStatus : nullptr);
   return check_launch("allreduce_sgd update");
+}
+
+static_assert(STZ_LINK_FLAG_WORDS == kLinkWords && STZ_LINK_SLOTS == kLinkSlots &&
+                  STZ_LINK_EPOCH == kLinkEpoch && STZ_LINK_STATUS == kLinkStatus,
+              "link flag layout");
+static_assert(STZ_PEER_FLAG_WORDS == kFlagWords, "peer flag layout");
+
+int stz_link_begin(unsigned* flags, void* stream) {
+  if (!flags) return fail(STZ_EINVAL, "link_begin: null flags");
+  link_begin_kernel<<<1, 32, 0, as_stream(stream)>>>(flags);
+  return check_launch("link_begin");
+}
+
+int stz_link_put(const void* src, size_t ps, int rows, int D, int D8, float* dst,
+                 const int* labels, int* labels_dst, unsigned* my_flags, unsigned* remote_slot,
+                 void* stream) {
+  if (!src || !dst || !my_flags || !remote_slot || rows < 0 || D < 1 || D8 < D || D8 % 8 ||
+      ps % 8 || !aligned16(src) || (D % 4 == 0 && !aligned16(dst)) ||
+      (labels != nullptr) != (labels_dst != nullptr))
+    return fail(STZ_EINVAL, "link_put: rows %d D %d D8 %d (D8 %% 8 == 0, 16-byte aligned "
+                "planes, labels and their destination together)", rows, D, D8);
+  const int grid = grid_for((size_t)rows * (D8 / 8) + 1);
+  link_put_kernel<<<grid, 256, 0, as_stream(stream)>>>(cb(src), ps, rows, D, D8, dst, labels,
+                                                       labels_dst, my_flags, remote_slot);
+  return check_launch("link_put");
+}
+
+int stz_link_get(const float* src, int rows, int D, void* dst, size_t ps, int D8,
+                 unsigned* my_flags, int slot0, int nslots, int slot_stride, void* stream) {
+  if (!src || !dst || !my_flags || rows < 0 || D < 1 || D8 < D || D8 % 8 || ps % 8 ||
+      !aligned16(dst) || (D % 4 == 0 && !aligned16(src)) || nslots < 0 || nslots > 32 ||
+      slot0 < 0 || slot0 + (nslots > 0 ? (nslots - 1) * slot_stride : 0) >= kLinkSlots)
+    return fail(STZ_EINVAL, "link_get: rows %d D %d D8 %d slots %d+%d*%d (< %d)", rows, D, D8,
+                slot0, nslots, slot_stride, kLinkSlots);
+  const int grid = grid_for((size_t)rows * (D8 / 8) + 1);
+  link_get_kernel<<<grid, 256, 0, as_stream(stream)>>>(src, rows, D, D8, mb(dst), ps, my_flags,
+                                                       slot0, nslots, slot_stride,
+                                                       g_peer_timeout_ns);
+  return check_launch("link_get");
 }
 
 }  // extern "C"

@@ -39,8 +39,10 @@
 // Barrier: flags[t][me] = epoch (release, system scope) for every member t,
 // then wait (acquire) until flags[me][t] >= epoch for every t.  The epoch is a
 // device-resident counter so CUDA-graph replays advance it.  A member that
-// never arrives does not hang the GPU: after the timeout the kernel prints
-// and traps, and the context error surfaces at the caller's next sync.
+// never arrives does not hang the GPU: after the timeout the waiting kernel
+// writes a status word (kFlagStatus) and returns; every later exchange kernel
+// of that member sees the status and does nothing, and the host raises
+// MissingSource when it reads the word (stanza_runtime.StanzaCluster.train).
 #pragma once
 
 #include "stz_split.cuh"
@@ -51,6 +53,7 @@ constexpr int kMaxPeers = 8;
 constexpr int kMaxPackRanges = 16;
 // flag-word layout of one member's IPC-visible int32 block
 constexpr int kFlagCounter = 16;   // local epoch counter
+constexpr int kFlagStatus = 17;    // != 0: a wait timed out (code, see peer_barrier_kernel)
 constexpr int kFlagWords = 32;
 
 struct PeerTable {
@@ -87,9 +90,17 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+__device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+
+// status code of a barrier that timed out waiting for member j
+constexpr unsigned kStatusBarrier = 0x10000u;
+
 __global__ void peer_barrier_kernel(PeerTable t, unsigned long long timeout_ns) {
   __shared__ unsigned epoch;
   unsigned* mine = t.flags[t.me];
+  if (ld_volatile(mine + kFlagStatus)) return;   // an earlier wait already failed
   if (threadIdx.x == 0) {
     epoch = mine[kFlagCounter] + 1;
     mine[kFlagCounter] = epoch;
@@ -103,9 +114,10 @@ __global__ void peer_barrier_kernel(PeerTable t, unsigned long long timeout_ns) 
     while ((int)(ld_acquire_sys(mine + j) - epoch) < 0) {
       __nanosleep(64);
       if (globaltimer_ns() - t0 > timeout_ns) {
-        printf("stz_peer_barrier: member %d waited %.1f s for member %d (epoch %u); trapping\n",
-               t.me, timeout_ns * 1e-9, j, epoch);
-        __trap();
+        printf("stz_peer_barrier: member %d waited %.1f s for member %d (epoch %u)\n", t.me,
+               timeout_ns * 1e-9, j, epoch);
+        atomicCAS(mine + kFlagStatus, 0u, kStatusBarrier | (unsigned)j);
+        break;
       }
     }
   }
@@ -122,6 +134,7 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
 // keep 2R remote loads in flight.
 template <int R>
 __global__ void __launch_bounds__(256) peer_reduce_push_kernel(PeerTable t, size_t c0, size_t c1) {
+  if (ld_volatile(t.flags[t.me] + kFlagStatus)) return;   // a peer is missing: touch nothing
   const size_t q0 = c0 / 4, q1 = c1 / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t q = q0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < q1; q += 2 * stride) {
@@ -171,7 +184,9 @@ __device__ __forceinline__ uint2 pack4(bf16_t a, bf16_t b, bf16_t c, bf16_t d) {
 // offsets are multiples of 4 (16-byte aligned tensor views).
 __global__ void __launch_bounds__(256) sgd_pack_kernel(float* __restrict__ w, float* __restrict__ v,
                                                        const float* __restrict__ g, PackTable tab,
-                                                       float lr, float mu, float inv_n) {
+                                                       float lr, float mu, float inv_n,
+                                                       const unsigned* status = nullptr) {
+  if (status && ld_volatile(status)) return;   // the exchange before it failed
   const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (int r = 0; r < tab.n; ++r) {
@@ -216,6 +231,147 @@ __global__ void __launch_bounds__(256) sgd_pack_kernel(float* __restrict__ w, fl
       v[rg.off + j] = b;
       if (rg.planes != nullptr) store_split(rg.planes, rg.ps, (j / rg.D) * rg.D8 + j % rg.D, a);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CONV <-> FC link over peer memory (the activation gather and the
+// boundary-gradient scatter, stanza_runtime.py:228-307 in the reference)
+//
+// Each rank owns a link flag block (kLinkWords uint32, zeroed once, mapped
+// by its link peers) and an fp32 staging buffer for what it receives (FC
+// worker: [micro][member][kb][A] activations; CONV worker: [K][A] boundary
+// gradients).  One iteration:
+//
+//   link_begin  epoch += 1 (every rank, once per step, first on its stream);
+//   link_put    the sender reads its split-plane rows, joins them to fp32
+//               (exact) and stores them straight into the receiver's staging
+//               rows over NVLink -- 4 B per element on the link, one kernel
+//               per (member, micro-batch) message -- plus the labels (int32)
+//               into the receiver's label rows; the last CTA to finish
+//               publishes the sender's epoch in the receiver's slot
+//               (fence.sys + st.release.sys);
+//   link_get    the receiver's CTAs each wait (ld.acquire.sys) until every
+//               slot of the micro-batch carries the epoch, then split the
+//               staged fp32 rows into its local split-plane buffer.
+//
+// No host synchronisation and no NCCL on the data path: the whole step is
+// stream-ordered device work (a CUDA graph per rank).  Staging reuse is safe
+// without credits: a sender's put of iteration t+1 follows (on its stream) its
+// receipt of iteration t's answer, which the receiver sends only after its
+// get of iteration t consumed the staging rows.
+// ---------------------------------------------------------------------------
+constexpr int kLinkWords = 256;
+constexpr int kLinkSlots = 192;     // message slots [0, 192)
+constexpr int kLinkEpoch = 240;     // local step epoch
+constexpr int kLinkStatus = 241;    // != 0: a get timed out (kStatusLink | slot)
+constexpr int kLinkDone = 242;      // CTA-completion counter of the running put
+constexpr unsigned kStatusLink = 0x20000u;
+
+__global__ void link_begin_kernel(unsigned* flags) {
+  if (threadIdx.x == 0) flags[kLinkEpoch] += 1;
+}
+
+// src: split planes [rows][D8] (plane stride ps); dst: fp32 [rows][D] (remote)
+__global__ void __launch_bounds__(256) link_put_kernel(const bf16_t* __restrict__ src, size_t ps,
+                                                       int rows, int D, int D8, float* dst,
+                                                       const int* __restrict__ lab_src,
+                                                       int* lab_dst, unsigned* my_flags,
+                                                       unsigned* remote_slot) {
+  const unsigned epoch = ld_volatile(my_flags + kLinkEpoch);
+  const int per_row = D8 / 8;
+  const size_t n8 = (size_t)rows * per_row;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const bool vec = (D % 8) == 0;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n8; q += stride) {
+    const size_t r = q / per_row;
+    const int c = (int)(q - r * per_row) * 8;
+    const size_t s = r * D8 + c;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(src + s));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + s + ps));
+    const uint4 d = __ldg(reinterpret_cast<const uint4*>(src + s + 2 * ps));
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w},
+                   dw[4] = {d.x, d.y, d.z, d.w};
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int sh = (e & 1) * 16;
+      v[e] = join3((bf16_t)(aw[e / 2] >> sh), (bf16_t)(bw[e / 2] >> sh), (bf16_t)(dw[e / 2] >> sh));
+    }
+    float* out = dst + r * D + c;
+    if (vec) {
+      reinterpret_cast<float4*>(out)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(out)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (c + e < D) out[e] = v[e];
+    }
+  }
+  if (lab_src)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)rows; i += stride)
+      lab_dst[i] = lab_src[i];
+  // publish: every thread's remote stores before the CTA's arrival, the last
+  // CTA releases the receiver's slot
+  __shared__ bool last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(my_flags + kLinkDone, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    my_flags[kLinkDone] = 0;
+    __threadfence_system();
+    st_release_sys(remote_slot, epoch);
+  }
+}
+
+// wait for slots slot0 + i*slot_stride (i < nslots), then src fp32 [rows][D]
+// (local staging, written by peers) -> split planes dst [rows][D8]
+__global__ void __launch_bounds__(256) link_get_kernel(const float* src, int rows, int D, int D8,
+                                                       bf16_t* __restrict__ dst, size_t ps,
+                                                       unsigned* my_flags, int slot0, int nslots,
+                                                       int slot_stride,
+                                                       unsigned long long timeout_ns) {
+  __shared__ int failed;
+  const unsigned epoch = ld_volatile(my_flags + kLinkEpoch);
+  if (threadIdx.x == 0) failed = ld_volatile(my_flags + kLinkStatus) != 0;
+  __syncthreads();
+  if (failed) return;
+  if (threadIdx.x < nslots) {
+    const int slot = slot0 + threadIdx.x * slot_stride;
+    const unsigned long long t0 = globaltimer_ns();
+    while ((int)(ld_acquire_sys(my_flags + slot) - epoch) < 0) {
+      __nanosleep(128);
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        if (atomicCAS(my_flags + kLinkStatus, 0u, kStatusLink | (unsigned)slot) == 0u)
+          printf("stz_link_get: slot %d waited %.1f s (epoch %u)\n", slot, timeout_ns * 1e-9,
+                 epoch);
+        failed = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (failed) return;
+  const int per_row = D8 / 8;
+  const size_t n8 = (size_t)rows * per_row;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const bool vec = (D % 8) == 0;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n8; q += stride) {
+    const size_t r = q / per_row;
+    const int c = (int)(q - r * per_row) * 8;
+    const float* in = src + r * D + c;
+    float v[8];
+    if (vec) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(in));
+      const float4 y = __ldcg(reinterpret_cast<const float4*>(in) + 1);
+      v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w, v[4] = y.x, v[5] = y.y, v[6] = y.z,
+      v[7] = y.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = c + e < D ? __ldcg(in + e) : 0.f;
+    }
+    store_split8(dst + r * D8 + c, ps, v);
   }
 }
 

@@ -3,7 +3,10 @@
 ``StanzaCluster(spec, *, n_conv, n_fc, batch_fn, lr, momentum=0.9, ...)``
 and ``.train(iterations) -> StanzaResult(losses, state, transport)`` keep the
 signature and semantics of /root/reference/pkg/src/stanza/stanza_runtime.py
-:96-375.  One BSP iteration (:352-375):
+:96-375 (``conv_ids`` / ``fc_ids`` are ``NodeId``s, ``conv_params`` /
+``fc_params`` map them to reference-layout numpy parameters,
+``transport.ledger`` is the reference's ledger surface).  One BSP iteration
+(:352-375):
 
   conv_compute  CONV trunk forward on each worker's batch (it, i)
   activations   many-to-one gather of [K, A] activations + labels into the
@@ -24,24 +27,35 @@ Two deployments:
   scatter) and the FC replica gradients are summed on device.  With
   n_conv = n_fc = 1 this is the co-located 1-GPU configuration.
 * one process per GPU (``comm=RoleComm``): rank i < n_conv is CONV worker
-  i, rank n_conv + j is FC worker j; the exchanges are NCCL point-to-point
-  ops and sub-group allreduces (comm.py).
+  i, rank n_conv + j is FC worker j.  With ``exchange="peer"`` (default on
+  one node) the gather / scatter and the gradient exchange are peer-memory
+  kernels ordered by device flags (comm.PeerLink / PeerExchange), so a step
+  is pure stream-ordered device work and runs as one CUDA graph per rank;
+  ``exchange="nccl"`` keeps NCCL P2P + allreduce (comm.RoleComm).
+
+``train()`` is the fast path: the next iteration's batch is fetched from
+``batch_fn`` and copied host -> device on a side stream into the other of
+two persistent input buffers while the current step's graph replays.
 """
 
 from __future__ import annotations
 
 import random
-from collections import Counter
-from dataclasses import dataclass, field
+from collections.abc import Mapping
 
 import numpy as np
 import torch
 
-from .checkpointing import TrainState, state_to_bytes
+from .checkpointing import TrainState, state_to_bytes, stzc_blob_len
 from .engine import BlockEngine
 from .model_partition import ConfigError, ModelSpec, Partition, mlp_split, split
 from .roles import group_rows, plan_groups
 from .tensor_core import ShapeMismatch, seeded_init
+from .transport import (DeviceTransport, NetConfig, NodeId, PhaseRecord, Role, Tag, Timeout,
+                        TrafficLedger, record_iteration)
+
+__all__ = ["MissingSource", "StanzaCluster", "StanzaResult", "plan_groups", "NodeId", "Role",
+           "Tag", "NetConfig", "PhaseRecord", "TrafficLedger"]
 
 
 def dist_backend() -> str | None:
@@ -49,67 +63,135 @@ def dist_backend() -> str | None:
     return dist.get_backend() if dist.is_available() and dist.is_initialized() else None
 
 
-class MissingSource(TimeoutError):
-    """An expected upstream node never delivered its payload."""
+class MissingSource(Timeout):
+    """An expected upstream node never delivered its payload (reference
+    stanza_runtime.py:37-38): raised by ``train()`` when a device-side wait
+    for a peer's activations, boundary gradients or exchange contribution
+    exceeded ``net.default_timeout``."""
 
 
-class Tag:
-    """Message classes of the per-iteration contract (reference transport.Tag)."""
-    ACTIVATIONS = "activations"
-    CONTROL = "control"
-    BOUNDARY_GRADS = "boundary_grads"
-    ALLREDUCE_CHUNK = "allreduce_chunk"
-    CHECKPOINT = "checkpoint"
-
-
-@dataclass
-class PhaseRecord:
-    label: str
-    payload_bytes: int = 0
-    elapsed_ms: float | None = None
-
-
-@dataclass
-class PhaseLedger:
-    """Device-side stand-in for the reference's TrafficLedger: the phase
-    sequence of every iteration, payload bytes per message class (what the
-    reference's ledger tests pin, test_stanza_runtime.py:158-179) and, when
-    phase timing is on, CUDA-event milliseconds per phase."""
-    phases: list = field(default_factory=list)
-    tag_payload_bytes: Counter = field(default_factory=Counter)
-    tag_messages: Counter = field(default_factory=Counter)
-
-    def record(self, label: str, nbytes: int = 0) -> PhaseRecord:
-        rec = PhaseRecord(label, nbytes)
-        self.phases.append(rec)
-        return rec
-
-
-@dataclass
 class StanzaResult:
-    losses: list
-    state: TrainState | None
-    transport: PhaseLedger
+    """Outcome of a training call (reference stanza_runtime.py:88-93)."""
+
+    def __init__(self, losses: list, state: TrainState | None, transport: DeviceTransport):
+        self.losses, self.state, self.transport = losses, state, transport
+
+    def __repr__(self):
+        return f"StanzaResult(losses={self.losses!r}, state=..., transport=...)"
 
 
 PHASES = ("conv_compute", "activations", "fc_compute", "boundary", "exchange", "update")
+# device-timing marks (time_phases=True): the reference phases plus the CONV
+# trunk backward, which the reference runs between the boundary and exchange
+# phases without a phase of its own (stanza_runtime.py:365-369)
+MARKS = ("conv_compute", "activations", "fc_compute", "boundary", "conv_backward", "exchange",
+         "update")
+
+
+class _Replicas(Mapping):
+    """``conv_params`` / ``fc_params``: NodeId -> nested fp32 numpy arrays in
+    the reference layouts, read from the replica that node's engine holds
+    (each access is a fresh device -> host copy)."""
+
+    def __init__(self, ids: list, engine_of, which: str):
+        self._ids, self._engine_of, self._which = ids, engine_of, which
+
+    def __getitem__(self, node):
+        if node not in self._ids:
+            raise KeyError(node)
+        eng = self._engine_of(node)
+        if eng is None:
+            raise KeyError(f"{node} is not hosted by this process")
+        views = eng.params if self._which == "params" else eng.velocity
+        return [[t.detach().cpu().numpy().copy() for t in row] for row in views]
+
+    def __iter__(self):
+        return iter([n for n in self._ids if self._engine_of(n) is not None])
+
+    def __len__(self):
+        return sum(1 for _ in self)
+
+
+class _Feed:
+    """Persistent double-buffered input pipeline of ``train()``: batch
+    ``it`` is fetched from batch_fn on the host and copied into buffer b on
+    a copy stream (from pinned staging, or straight from a pinned / CUDA
+    tensor batch_fn returns) while the previous step computes."""
+
+    def __init__(self, cluster: "StanzaCluster"):
+        dev = cluster.device
+        self.cl = cluster
+        self.x = [cluster.x, torch.empty_like(cluster.x)]
+        self.y = [cluster.labels, torch.empty_like(cluster.labels)]
+        self.hx = [torch.empty(cluster.x.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.hy = [torch.empty(cluster.labels.shape, dtype=torch.int32).pin_memory()
+                   for _ in range(2)]
+        self.stream = torch.cuda.Stream(dev)
+        self.copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        self.used = [False, False]
+        self.h2d_bytes = 0
+
+    def stage(self, it: int, b: int) -> None:
+        cl, k = self.cl, self.cl.k
+        idx = cl.local_conv_indices()
+        batches = [cl.batch_fn(it, i) for i in idx]
+        for x, _ in batches:
+            if x.shape[0] != k:
+                raise ShapeMismatch(f"CONV batch has {x.shape[0]} samples, "
+                                    f"expected batch_k={k}")
+        if self.used[b]:
+            self.copied[b].synchronize()      # host staging b is free again
+            self.stream.wait_event(self.consumed[b])
+        self.used[b] = True
+        with torch.cuda.stream(self.stream):
+            for pos, (x, y) in enumerate(batches):
+                rows = slice(pos * k, (pos + 1) * k)
+                self._put(self.x[b][rows], self.hx[b][rows], x, torch.float32)
+                self._put(self.y[b][rows], self.hy[b][rows], y, torch.int32)
+            self.copied[b].record(self.stream)
+        self.h2d_bytes = self.x[b].numel() * 4 + self.y[b].numel() * 4
+
+    @staticmethod
+    def _put(dst, host, src, dtype):
+        if isinstance(src, torch.Tensor):
+            if src.is_cuda:
+                dst.copy_(src.to(dtype))
+                return
+            if src.is_pinned() and src.dtype == dtype and src.is_contiguous():
+                dst.copy_(src, non_blocking=True)
+                return
+            src = src.numpy()
+        host.numpy()[...] = np.asarray(src).reshape(host.shape)
+        dst.copy_(host, non_blocking=True)
+
+    def ready(self, b: int, stream) -> None:
+        stream.wait_event(self.copied[b])
+
+    def done(self, b: int, stream) -> None:
+        self.consumed[b].record(stream)
 
 
 class StanzaCluster:
     """A layer-separated deployment on B200 GPUs.
 
     batch_fn(iteration, conv_index) -> (inputs [K, ...] float32, labels [K])
-    exactly as in the reference; iteration indices are absolute so resumed
-    runs replay the same data.  ``device`` selects the GPU (single-device
-    mode); ``comm`` switches to one-process-per-GPU mode.
+    exactly as in the reference (numpy arrays; pinned-host or CUDA torch
+    tensors are taken without a host copy); iteration indices are absolute
+    so resumed runs replay the same data.  ``net`` is the reference's
+    NetConfig: it drives the ledger's logical clock, and its
+    ``default_timeout`` bounds every device-side wait for a peer
+    (MissingSource).  ``device`` selects the GPU (single-device mode);
+    ``comm`` switches to one-process-per-GPU mode.
     """
 
     def __init__(self, spec: ModelSpec, *, n_conv: int, n_fc: int, batch_fn, lr: float,
                  momentum: float = 0.9, conv_time: float = 0.0, fc_unit_time: float = 0.0,
-                 net=None, seed: int = 0, boundary: int | None = None,
+                 net: NetConfig | None = None, seed: int = 0, boundary: int | None = None,
                  state: TrainState | None = None, device=None, comm=None,
                  time_phases: bool = False, micro_batches: int | None = None,
-                 segment_graphs: bool = True, exchange: str | None = None):
+                 segment_graphs: bool = True, exchange: str | None = None,
+                 graphs: bool = True):
         if lr <= 0.0:
             raise ConfigError(f"learning rate must be positive, got {lr}")
         if not 0.0 <= momentum < 1.0:
@@ -127,21 +209,21 @@ class StanzaCluster:
         self.max_group = max(self.conv_to_fc.count(j) for j in range(n_fc))
         self.comm = comm
         self.time_phases = time_phases
+        self.graphs = bool(graphs)
         self.k = spec.batch_k
+        self.net = net or NetConfig()
         # micro-batch pipelining of CONV fwd -> gather -> FC -> scatter -> CONV bwd
         # (one process per GPU only).  Gradient sums are
         # unchanged up to fp32 summation order.
-        from .engine import BlockEngine as _BE
-        has_bn = (not spec.is_profile) and _BE(self.partition.conv_block, spec.input_shape, 1,
-                                                "cpu", allocate=False).has_bn()
+        has_bn = (not spec.is_profile) and BlockEngine(self.partition.conv_block,
+                                                       spec.input_shape, 1, "cpu",
+                                                       allocate=False).has_bn()
         if has_bn and micro_batches is not None and micro_batches > 1:
             raise ConfigError("BatchNorm normalises over each CONV worker's whole batch: "
                               "micro_batches must be 1")
         if micro_batches is None and has_bn:
             micro_batches = 1
         if micro_batches is None:
-            # measured (AlexNet K=128, images/s): 1:1 29.3k / 30.1k / 26.6k and
-            # 3:1 77.3k / 85.8k / 78.0k at 1 / 2 / 4 micro-batches
             micro_batches = 2 if (comm is not None and spec.batch_k % 2 == 0
                                   and spec.batch_k >= 32) else 1
         if micro_batches < 1 or spec.batch_k % micro_batches:
@@ -150,20 +232,24 @@ class StanzaCluster:
         if comm is None:
             micro_batches = 1
         self.micro = int(micro_batches)
-        # one process per GPU: each compute segment of the pipelined step is
-        # captured as a CUDA graph the second time it runs (NCCL stays eager)
-        self.segment_graphs = bool(segment_graphs) and comm is not None
-        # gradient exchange + update of one process per GPU: "peer" = the fused
-        # NVLink peer-memory kernels (stz_allreduce_sgd), "nccl" = NCCL
-        # all_reduce followed by the SGD kernel (and the only choice on gloo)
+        # exchange path of one process per GPU: "peer" = the CONV<->FC link
+        # and the gradient exchange + update as peer-memory kernels (any
+        # process-group backend: the group only carries the handle exchange);
+        # "nccl" = NCCL P2P + all_reduce + the SGD kernel
         if exchange is None:
-            exchange = "peer" if comm is not None and dist_backend() == "nccl" else "nccl"
+            exchange = "peer" if comm is not None and torch.cuda.is_available() else "nccl"
         if exchange not in ("peer", "nccl"):
             raise ConfigError(f"exchange must be 'peer' or 'nccl', got {exchange!r}")
         self.exchange = exchange if comm is not None else "local"
+        self.segment_graphs = bool(segment_graphs) and comm is not None
         self._peer = None
+        self._link = None
         self._seg_graphs: dict = {}
+        self._step_graphs: dict = {}
         self._steps_done = 0
+        self._feed = None
+        self._pending_events: list = []
+        self.device_phase_ms: list = []
         cut = self.partition.split_index
 
         ref = seeded_init(self.layers, seed)
@@ -185,9 +271,9 @@ class StanzaCluster:
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
-        self.conv_ids = [("conv", i) for i in range(n_conv)]
-        self.fc_ids = [("fc", j) for j in range(n_fc)]
-        self.transport = PhaseLedger()
+        self.conv_ids = [NodeId(Role.CONV_WORKER, i) for i in range(n_conv)]
+        self.fc_ids = [NodeId(Role.FC_WORKER, j) for j in range(n_fc)]
+        self.transport = DeviceTransport(self.net)
         self.replica_snapshots: dict = {}
         self._fc_replica = None          # (params_flat, vel_flat) on the holder's GPU
         self._replica_holder = None
@@ -239,9 +325,20 @@ class StanzaCluster:
                                   need_input_grad=True)
                 eng.rows = (0, g * k)
                 self.fcs.append(eng)
-            if self.exchange == "peer":   # collective: every rank maps its role group
+            if self.exchange == "peer":
+                # collective: every rank maps its link peers, then its role group
+                from . import _lib
+                from .comm import PeerLink
+                _lib.call("stz_set_peer_timeout_ms", max(1, int(self.net.default_timeout * 1e3)))
+                self._link = PeerLink(comm, dev, k, self.micro, a,
+                                      dst=self.gboundary if comm.is_conv else self.fc_in,
+                                      labels=None if comm.is_conv else self.labels)
                 self._peer = comm.peer_exchange(self.conv if comm.is_conv else self.fcs[0])
-        self._loss_slots = None
+        self.conv_params = _Replicas(self.conv_ids, self._conv_engine_of, "params")
+        self.fc_params = _Replicas(self.fc_ids, self._fc_engine_of, "params")
+        self.conv_velocities = _Replicas(self.conv_ids, self._conv_engine_of, "velocity")
+        self.fc_velocities = _Replicas(self.fc_ids, self._fc_engine_of, "velocity")
+        self._loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
 
     # -- helpers -------------------------------------------------------------------------
 
@@ -252,17 +349,18 @@ class StanzaCluster:
             shape = out_shape(layer, shape)
         return shape
 
+    def _conv_engine_of(self, node):
+        if self.conv is None:
+            return None
+        return self.conv if self.comm is None or node.index == self.comm.index else None
+
+    def _fc_engine_of(self, node):
+        if not self.fcs:
+            return None
+        return self.fcs[0] if self.comm is None or node.index == self.comm.index else None
+
     def group_members(self, fc_index: int) -> list[int]:
         return [i for i, j in enumerate(self.conv_to_fc) if j == fc_index]
-
-    @property
-    def conv_params(self):
-        """CONV replica parameters (device views, reference layout)."""
-        return self.conv.params if self.conv is not None else None
-
-    @property
-    def fc_params(self):
-        return self.fcs[0].params if self.fcs else None
 
     def local_conv_indices(self) -> list[int]:
         if self.comm is None:
@@ -272,60 +370,73 @@ class StanzaCluster:
     # -- one iteration on device-resident inputs ------------------------------------
 
     def load_batch(self, it: int) -> None:
-        """Fetch this process's CONV batches from batch_fn and upload them."""
-        idx = self.local_conv_indices()
-        if not idx:
+        """Fetch this process's CONV batches from batch_fn and upload them
+        into ``self.x`` / ``self.labels`` (synchronously ordered on the
+        current stream; ``train()`` uses the double-buffered feed instead)."""
+        if not self.local_conv_indices():
             return
-        xs, ys = [], []
-        for i in idx:
+        k = self.k
+        for pos, i in enumerate(self.local_conv_indices()):
             x, y = self.batch_fn(it, i)
-            if x.shape[0] != self.k:
+            if x.shape[0] != k:
                 raise ShapeMismatch(f"CONV batch has {x.shape[0]} samples, "
-                                    f"expected batch_k={self.k}")
-            xs.append(np.asarray(x, dtype=np.float32))
-            ys.append(np.asarray(y))
-        x = torch.from_numpy(np.ascontiguousarray(np.concatenate(xs)))
-        y = torch.from_numpy(np.concatenate(ys).astype(np.int32))
-        self.x.copy_(x.pin_memory(), non_blocking=True)
-        self.labels.copy_(y.pin_memory(), non_blocking=True)
+                                    f"expected batch_k={k}")
+            rows = slice(pos * k, (pos + 1) * k)
+            _Feed._put(self.x[rows], torch.empty(self.x[rows].shape).pin_memory(), x,
+                       torch.float32)
+            _Feed._put(self.labels[rows], torch.empty(k, dtype=torch.int32).pin_memory(), y,
+                       torch.int32)
+
+    def _record(self, iterations: int = 1) -> list:
+        """Log ``iterations`` iterations of the reference protocol's messages
+        on the ledger (transport.record_iteration); returns the last
+        iteration's six PhaseRecords."""
+        recs = []
+        for d in range(iterations):
+            recs = record_iteration(
+                self.transport, conv_ids=self.conv_ids, fc_ids=self.fc_ids,
+                conv_to_fc=self.conv_to_fc, k=self.k, a=self.boundary_activations,
+                conv_params=self.partition.conv_params, fc_params=self.partition.fc_params,
+                seed=self.seed, iteration=self.iteration + d, conv_time=self.conv_time,
+                fc_unit_time=self.fc_unit_time, max_group=self.max_group)
+        return recs
 
     def step(self, loss_slot: torch.Tensor | None = None, x: torch.Tensor | None = None,
              labels: torch.Tensor | None = None) -> None:
         """One layer-separated iteration on the batch in ``self.x`` /
         ``self.labels`` (or on device-resident ``x`` / ``labels`` of the same
-        shapes, e.g. a pre-staged pool).  Adds the iteration's summed
-        per-sample loss into loss_slot (float64, on this process's FC
-        workers).  Single-device mode runs the reference's BSP phase order
-        below; one process per GPU runs _step_pipelined."""
+        shapes, e.g. a pre-staged pool), eagerly (time_phases=True records
+        CUDA-event times per phase).  Adds the iteration's summed per-sample
+        loss into loss_slot (float64, on this process's FC workers) and logs
+        the iteration on the ledger.  Does not advance ``self.iteration``."""
+        recs = self._record()
+        ev = [] if self.time_phases else None
+        self._device_step(loss_slot, x, labels, ev)
+        if ev is not None:
+            self._pending_events.append((ev, recs))
+
+    def _device_step(self, loss_slot, x, labels, ev=None) -> None:
         x_in = self.x if x is None else x
         lab_all = self.labels if labels is None else labels
+        if lab_all is not None and lab_all.dtype != torch.int32:
+            raise TypeError("labels must be an int32 device tensor")
         if self.comm is not None:
-            return self._step_pipelined(loss_slot, x_in, lab_all)
-        k = self.k
-        n = self.n_conv * k
-        led = self.transport
-        a_bytes = self.boundary_activations * k * 4
-        ev = self._events() if self.time_phases else None
-        mark = (lambda label: ev.append((label, self._event()))) if ev is not None else \
-            (lambda label: None)
+            if self._link is not None:
+                self._step_peer(loss_slot, x_in, lab_all, ev)
+            else:
+                self._step_pipelined(loss_slot, x_in, lab_all, ev)
+            self._steps_done += 1
+            return
+        n = self.n_conv * self.k
+        mark = self._marker(ev)
         mark("conv_compute")
-        led.record("conv_compute")
         acts = self.conv.forward(x_in)
-
-        mark("activations")
-        led.record("activations", self.n_conv * (a_bytes + k * 4))
-        led.tag_payload_bytes[Tag.ACTIVATIONS] += self.n_conv * a_bytes
-        led.tag_payload_bytes[Tag.CONTROL] += self.n_conv * k * 4
-        led.tag_messages[Tag.ACTIVATIONS] += self.n_conv
-        led.tag_messages[Tag.CONTROL] += self.n_conv
-
+        mark("activations")               # zero-copy: FC workers read row slices
         mark("fc_compute")
-        led.record("fc_compute")
-        for j, eng in enumerate(self.fcs):
+        for eng in self.fcs:
             lo, hi = eng.rows
             eng.forward(acts.rows_view(lo, hi), lab_all[lo:hi], loss_out=loss_slot)
             eng.backward()
-
         # the FC block's exchange + update depend only on the FC gradients: they
         # run on a side stream, concurrently with the CONV backward (the
         # momentum kernel is HBM-bound and co-resides with the GEMMs, which
@@ -339,44 +450,107 @@ class StanzaCluster:
                 for eng in self.fcs[1:]:
                     self.fcs[0].add_grads_from(eng)
                 self.fcs[0].sgd(n, self.lr, self.momentum)
-
-        mark("boundary")
-        led.record("boundary", self.n_conv * a_bytes)
-        led.tag_payload_bytes[Tag.BOUNDARY_GRADS] += self.n_conv * a_bytes
-        led.tag_messages[Tag.BOUNDARY_GRADS] += self.n_conv
+        mark("boundary")                  # zero-copy: FC dgrad wrote the trunk's rows
+        mark("conv_backward")
         self.conv.backward(self.gboundary)
-
         mark("exchange")
-        ring = lambda p, m: 0 if m == 1 else int(2 * (m - 1) * p * 4)  # noqa: E731
-        ar_bytes = ring(self.partition.conv_params, self.n_conv) + \
-            (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
-        led.record("exchange", ar_bytes)
-        led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
         if not overlap:
             for eng in self.fcs[1:]:
                 self.fcs[0].add_grads_from(eng)
-
         mark("update")
-        led.record("update")
         self.conv.sgd(n, self.lr, self.momentum)
         if overlap:
             main.wait_stream(side)
         else:
             self.fcs[0].sgd(n, self.lr, self.momentum)
         mark("end")
-        if ev is not None:
-            self._pending_events.append(ev)
+        self._steps_done += 1
+
+    def _marker(self, ev):
+        """mark(label): an NVTX range per phase label (reference phase names,
+        tests/test_stanza_runtime.py:159-165) and, when timing, a CUDA event."""
+        state = {"open": False}
+
+        def mark(label):
+            if state["open"]:
+                torch.cuda.nvtx.range_pop()
+                state["open"] = False
+            if label != "end":
+                torch.cuda.nvtx.range_push(f"stanza:{label}")
+                state["open"] = True
+            if ev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(torch.cuda.current_stream(self.device))
+                ev.append((label, e))
+        return mark
 
     def _side_stream(self) -> "torch.cuda.Stream":
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream(self.device)
         return self._side
 
+    def _step_peer(self, loss_slot, x_in, lab_all, ev) -> None:
+        """One iteration of one process per GPU over the peer-memory link,
+        pipelined over ``self.micro`` micro-batches of kb = K / micro samples
+        per CONV worker -- all of it stream-ordered device work.
+
+        CONV worker: forward each micro-batch and put its activations to the
+        FC worker at once (the FC worker starts while the next micro-batch
+        is computed); as each micro-batch's boundary gradient lands, its
+        input-gradient chain (overlapping the FC worker's next micro-batch);
+        then every weight gradient once over the whole batch; exchange +
+        update with the other CONV workers.
+        FC worker: per micro-batch, wait for the group's rows (its input is
+        laid out [micro-batch][member][kb]), FC forward + SoftmaxCE + the
+        input-gradient chain only, and put each member's boundary rows back;
+        then the FC weight gradients over the whole batch (overlapping the
+        CONV backward), exchange (n_fc > 1) + update.  Sums are the BSP
+        step's up to fp32 summation order."""
+        link, m, kb = self._link, self.micro, self.k // self.micro
+        n = self.n_conv * self.k
+        mark = self._marker(ev)
+        link.begin()
+        if self.conv is not None:
+            mark("conv_compute")
+            last = len(self.conv.ops) - 1
+            for j in range(m):
+                rows = (j * kb, (j + 1) * kb)
+                self.conv.forward(x_in, rows=rows)
+                link.put_acts(j, self.conv._act(last).rows_view(*rows), lab_all[rows[0]:rows[1]])
+            mark("boundary")
+            for j in range(m):
+                link.get_grads(j)
+                self.conv.backward(self.gboundary, rows=(j * kb, (j + 1) * kb), phase="dgrad")
+            mark("conv_backward")
+            self.conv.backward(phase="wgrad")
+        else:
+            eng = self.fcs[0]
+            g = link.g
+            loss_to = self._loss_dev if loss_slot is None else loss_slot
+            if loss_slot is None:
+                self._loss_dev.zero_()
+            for j in range(m):
+                mark("activations" if j == 0 else "fc_compute")
+                link.get_acts(j)
+                if j == 0:
+                    mark("fc_compute")
+                rows = (j * g * kb, (j + 1) * g * kb)
+                eng.forward(self.fc_in, self.labels, rows=rows, sum_loss=False)
+                eng.backward(rows=rows, phase="dgrad")
+                eng.sum_loss(loss_to, rows)
+                link.put_grads(j, eng.gin[0].rows_view(*rows))
+            mark("boundary")
+            eng.backward(phase="wgrad")
+        mark("exchange")
+        self._peer.run(n, self.lr, self.momentum)
+        mark("update")
+        mark("end")
+
     def _segment(self, key, fn) -> None:
-        """Run a compute segment of the pipelined step: eagerly during the
-        first step (kernel attributes, workspaces), then captured into a CUDA
-        graph the first time its ``key`` -- every pointer its kernels bake in
-        -- is seen, and replayed from then on."""
+        """exchange="nccl": run a compute segment eagerly during the first
+        step (kernel attributes, workspaces), then captured into a CUDA graph
+        the first time its ``key`` -- every pointer its kernels bake in -- is
+        seen, and replayed from then on (NCCL calls stay eager between)."""
         if not self.segment_graphs or self.time_phases or self._steps_done == 0:
             fn()
             return
@@ -392,44 +566,17 @@ class StanzaCluster:
             self._seg_graphs[key] = g
         g.replay()
 
-    def _step_pipelined(self, loss_slot, x_in, lab_all) -> None:
-        """One iteration in the one-process-per-GPU deployment, pipelined over
-        ``self.micro`` micro-batches of kb = K / micro samples per CONV worker.
-
-        CONV worker: forward each micro-batch and post its activations at
-        once (the FC worker starts while the next micro-batch is computed);
-        as each micro-batch's boundary gradient arrives, its input-gradient
-        chain (overlapping the FC worker's next micro-batch); then every
-        weight gradient once over the whole batch.
-        FC worker: per micro-batch, receive the group's rows (its input is
-        laid out [micro-batch][member][kb], so each micro-batch is
-        contiguous), run the FC forward and only the input-gradient chain,
-        and post each member's boundary rows back; the FC weight gradients
-        follow over the whole batch, overlapping the CONV backward.  With
-        micro = 1 this is the BSP step with the FC weight gradients moved off
-        the critical path.  Exchange and update are the BSP step's; the sums
-        are unchanged up to fp32 summation order."""
+    def _step_pipelined(self, loss_slot, x_in, lab_all, ev) -> None:
+        """exchange="nccl": the pipelined iteration of _step_peer with NCCL
+        point-to-point ops for the gather / scatter (one communicator per
+        direction) and NCCL all_reduce + the SGD kernel for the exchange;
+        compute segments are CUDA graphs."""
         comm = self.comm
         comm.warm(self.device)
         m, k = self.micro, self.k
         kb = k // m
         n = self.n_conv * k
-        led = self.transport
-        a_bytes = self.boundary_activations * k * 4
-        ev = self._events() if self.time_phases else None
-        mark = (lambda label: ev.append((label, self._event()))) if ev is not None else \
-            (lambda label: None)
-        led.record("conv_compute")
-        led.record("activations", self.n_conv * (a_bytes + k * 4))
-        led.tag_payload_bytes[Tag.ACTIVATIONS] += self.n_conv * a_bytes
-        led.tag_payload_bytes[Tag.CONTROL] += self.n_conv * k * 4
-        led.tag_messages[Tag.ACTIVATIONS] += self.n_conv * m
-        led.tag_messages[Tag.CONTROL] += self.n_conv * m
-        led.record("fc_compute")
-        led.record("boundary", self.n_conv * a_bytes)
-        led.tag_payload_bytes[Tag.BOUNDARY_GRADS] += self.n_conv * a_bytes
-        led.tag_messages[Tag.BOUNDARY_GRADS] += self.n_conv * m
-
+        mark = self._marker(ev)
         if comm.is_conv:
             mark("conv_compute")
             sends = []
@@ -440,23 +587,18 @@ class StanzaCluster:
                 acts = self.conv._act(len(self.conv.ops) - 1).rows_view(*rows)
                 sends += comm.post_activations(
                     [acts.plane_rows(p) for p in range(3)] + [lab_all[rows[0]:rows[1]]], None)
-            mark("activations")
             recvs = []
             for j in range(m):
                 gb = self.gboundary.rows_view(j * kb, (j + 1) * kb)
                 recvs += comm.post_boundary(None, [gb.plane_rows(p) for p in range(3)])
-            mark("fc_compute")
+            mark("boundary")
             per = len(recvs) // m
             for j in range(m):
-                # the input-gradient chain of micro-batch j as soon as its
-                # boundary rows land (overlaps the FC worker's next one) ...
                 for w in recvs[j * per:(j + 1) * per]:
                     w.wait()
-                if j == 0:
-                    mark("boundary")
                 self._segment(("conv_dgrad", j), lambda j=j: self.conv.backward(
                     self.gboundary, rows=(j * kb, (j + 1) * kb), phase="dgrad"))
-            # ... then every weight / bias gradient once, over the whole batch
+            mark("conv_backward")
             self._segment(("conv_wgrad",), lambda: self.conv.backward(phase="wgrad"))
             for w in sends:
                 w.wait()
@@ -467,7 +609,6 @@ class StanzaCluster:
             if loss_to is None:           # micro-batch sums accumulate into loss_sum
                 eng.loss_sum.zero_()
                 loss_to = eng.loss_sum
-            mark("conv_compute")
             mark("activations")
             sends = []
             for j in range(m):
@@ -496,41 +637,34 @@ class StanzaCluster:
             self._segment(("fc_wgrad",), lambda: eng.backward(phase="wgrad"))  # overlaps CONV bwd
             for w in sends:
                 w.wait()
-
         mark("exchange")
-        ring = lambda p, mm: 0 if mm == 1 else int(2 * (mm - 1) * p * 4)  # noqa: E731
-        ar_bytes = ring(self.partition.conv_params, self.n_conv) + \
-            (ring(self.partition.fc_params, self.n_fc) if self.n_fc > 1 else 0)
-        led.record("exchange", ar_bytes)
-        led.tag_payload_bytes[Tag.ALLREDUCE_CHUNK] += ar_bytes
-        if self._peer is not None:
-            # exchange + update fused over NVLink peer memory (one segment)
-            self._segment(("peer_exchange_sgd",),
-                          lambda: self._peer.run(n, self.lr, self.momentum))
-            mark("update")
-            led.record("update")
-        else:
-            comm.allreduce_grads(self.conv.grad_flat if comm.is_conv else self.fcs[0].grad_flat)
-            mark("update")
-            led.record("update")
-            if self.conv is not None:
-                self._segment(("conv_sgd",), lambda: self.conv.sgd(n, self.lr, self.momentum))
-            if self.fcs:
-                self._segment(("fc_sgd",), lambda: self.fcs[0].sgd(n, self.lr, self.momentum))
+        comm.allreduce_grads(self.conv.grad_flat if comm.is_conv else self.fcs[0].grad_flat)
+        mark("update")
+        if self.conv is not None:
+            self._segment(("conv_sgd",), lambda: self.conv.sgd(n, self.lr, self.momentum))
+        if self.fcs:
+            self._segment(("fc_sgd",), lambda: self.fcs[0].sgd(n, self.lr, self.momentum))
         mark("end")
-        if ev is not None:
-            self._pending_events.append(ev)
-        self._steps_done += 1
+
+    # -- CUDA graphs -------------------------------------------------------------------
+
+    def graph_capable(self) -> bool:
+        """Whether one whole iteration is pure device work (capturable)."""
+        return self.comm is None or self._link is not None
 
     def capture(self, x: torch.Tensor | None = None, labels: torch.Tensor | None = None,
                 loss_slot: torch.Tensor | None = None) -> "torch.cuda.CUDAGraph":
-        """Capture one whole iteration (every kernel of conv fwd, FC step,
-        conv bwd, update) as a CUDA graph on device-resident inputs; replay()
-        runs it with no host launch overhead.  Single-device mode only (the
-        NCCL exchanges of the one-process-per-GPU mode stay eager).  Call
-        once eagerly first so every kernel attribute / tensor map is set."""
-        if self.comm is not None:
-            raise RuntimeError("graph capture covers the single-device deployment")
+        """Capture one whole iteration (conv fwd, gather, FC step, scatter,
+        conv bwd, exchange, update) as a CUDA graph on device-resident
+        inputs; replay() runs it with no host launch overhead.  Every rank
+        of a one-process-per-GPU cluster captures its own part (exchange=
+        "peer": the link and exchange kernels synchronise through device
+        flags, so ranks replay independently).  Call once eagerly first so
+        every kernel attribute / tensor map is set.  Replays are not logged
+        on the ledger (train() logs each iteration it runs)."""
+        if not self.graph_capable():
+            raise RuntimeError("exchange='nccl' keeps NCCL calls on the host: "
+                               "whole-step capture needs exchange='peer'")
         slot = loss_slot
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
@@ -539,10 +673,18 @@ class StanzaCluster:
             with torch.cuda.graph(g, stream=s):
                 if slot is not None:
                     slot.zero_()
-                self.step(slot, x=x, labels=labels)
+                self._device_step(slot, x, labels)
         torch.cuda.current_stream(self.device).wait_stream(s)
-        # the ledger recorded the captured step once; it describes a replay
         return g
+
+    def _graph_for(self, b: int, x, labels):
+        """The whole-step graph of input buffer b (captured on first use)
+        and its loss slot."""
+        ent = self._step_graphs.get(b)
+        if ent is None:
+            slot = torch.zeros(1, dtype=torch.float64, device=self.device)
+            ent = self._step_graphs[b] = (self.capture(x, labels, slot), slot)
+        return ent
 
     # -- public API ------------------------------------------------------------------
 
@@ -550,36 +692,94 @@ class StanzaCluster:
                        labels: torch.Tensor | None = None) -> dict:
         """Measure the GEMM tile shapes of this cluster's step on this GPU
         (`_lib.autotune_tiles`) and install the winners for every later step
-        and capture.  Runs one full iteration (like step(); its loss is not
-        recorded), on every rank when the cluster spans processes.  The
-        parameters and velocities this process holds are restored afterwards
-        (and their split-plane weight copies repacked), so training continues
-        from the same state as without it."""
+        and capture.  Must run before the first step: later steps replay
+        CUDA graphs, which keep the tiles they were captured with.  Runs one
+        full iteration eagerly (its loss and ledger entries are discarded),
+        on every rank when the cluster spans processes.  The parameters and
+        velocities this process holds are restored afterwards (and their
+        split-plane weight copies repacked), so training continues from the
+        same state as without it."""
         from . import _lib
+        if self._steps_done or self._step_graphs or self._seg_graphs:
+            raise RuntimeError("autotune_tiles() must run before the first step (captured "
+                               "graphs keep the tiles they were captured with)")
         engines = [e for e in [self.conv, *self.fcs] if e is not None]
         saved = [(e.params_flat.clone(), e.vel_flat.clone()) for e in engines]
-        table = _lib.autotune_tiles(lambda: self.step(None, x=x, labels=labels))
+        ledger, self.transport = self.transport, DeviceTransport(self.net)
+        timing, self.time_phases = self.time_phases, False
+        try:
+            with torch.cuda.device(self.device):
+                table = _lib.autotune_tiles(lambda: self._device_step(None, x, labels))
+        finally:
+            self.transport, self.time_phases = ledger, timing
         for e, (pf, vf) in zip(engines, saved):
             e.params_flat.copy_(pf)
             e.vel_flat.copy_(vf)
             e.pack_weights()
         torch.cuda.synchronize(self.device)
+        self._steps_done = 0          # the graphs of later steps are captured fresh
         return table
 
     def train(self, iterations: int) -> StanzaResult:
-        """Run `iterations` more iterations; may be called repeatedly."""
-        slots = torch.zeros(max(iterations, 1), dtype=torch.float64, device=self.device)
-        self._pending_events = []
-        for s in range(iterations):
-            self.load_batch(self.iteration)
-            self.step(slots[s:s + 1] if self.fcs else None)
+        """Run `iterations` more iterations; may be called repeatedly.
+
+        The fast path: batch it+1 is fetched and copied host -> device on a
+        side stream while step it runs (two persistent device buffers with
+        pinned host staging), and every step after the first is one CUDA
+        graph replay per rank (time_phases=True or exchange="nccl": eager).
+        Losses are copied back per step into pinned host memory."""
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        n_it = max(int(iterations), 0)
+        host_losses = torch.zeros(max(n_it, 1), dtype=torch.float64).pin_memory()
+        slots = torch.zeros(max(n_it, 1), dtype=torch.float64, device=dev)
+        feed = None
+        if self.local_conv_indices():
+            if self._feed is None:
+                self._feed = _Feed(self)
+            feed = self._feed
+            if n_it:
+                feed.stage(self.iteration, 0)
+        use_graphs = self.graphs and not self.time_phases and self.graph_capable()
+        for s in range(n_it):
+            b = s & 1
+            recs = self._record()
+            if feed is not None:
+                feed.ready(b, main)
+                if s + 1 < n_it:
+                    feed.stage(self.iteration + 1, b ^ 1)
+            x = feed.x[b] if feed is not None else None
+            y = feed.y[b] if feed is not None else None
+            if use_graphs and self._steps_done > 0:
+                g, gslot = self._graph_for(b, x, y)
+                g.replay()
+                slots[s:s + 1].copy_(gslot)
+            else:
+                ev = [] if self.time_phases else None
+                self._device_step(slots[s:s + 1], x, y, ev)
+                if ev is not None:
+                    self._pending_events.append((ev, recs))
+            if feed is not None:
+                feed.done(b, main)
+            host_losses[s:s + 1].copy_(slots[s:s + 1], non_blocking=True)
             self.iteration += 1
+        torch.cuda.synchronize(dev)
+        self.check_peers()
         if self.comm is not None:
             self.comm.sum_scalar(slots)     # FC ranks hold the loss sums
+            host_losses.copy_(slots.cpu())
         n = self.n_conv * self.k
-        losses = [float(v) / n for v in slots[:iterations].cpu().tolist()]
+        losses = [float(v) / n for v in host_losses[:n_it].tolist()]
         self._resolve_phase_times()
         return StanzaResult(losses=losses, state=self.state(), transport=self.transport)
+
+    def check_peers(self) -> None:
+        """Raise MissingSource if a device-side wait for a peer timed out
+        (reads the link / exchange status words; synchronises)."""
+        for part in (self._link, self._peer):
+            msg = part.failure() if part is not None else None
+            if msg is not None:
+                raise MissingSource(f"{msg} (iteration <= {self.iteration - 1})")
 
     def state(self) -> TrainState | None:
         """Full state stitched from the first CONV and the first FC replica.
@@ -589,21 +789,17 @@ class StanzaCluster:
             cp, cv = self.conv.state_numpy()
             fp, fv = self.fcs[0].state_numpy()
             return TrainState(self.iteration, cp + fp, cv + fv)
-        import torch.distributed as dist
-        fc0 = self.comm.n_conv
-        rank = self.comm.rank
-        if rank == fc0:
-            dist.send(self.fcs[0].params_flat, 0)
-            dist.send(self.fcs[0].vel_flat, 0)
-        if rank != 0:
+        comm = self.comm
+        fc0 = comm.n_conv
+        if comm.rank == fc0:
+            comm.p2p(sends=[(self.fcs[0].params_flat, 0), (self.fcs[0].vel_flat, 0)])
+        if comm.rank != 0:
             return None
         cut = self.partition.split_index
-        proto = BlockEngine(self.partition.fc_block, (self.boundary_activations,), 1,
-                            self.device, allocate=False)
+        proto = self._fc_proto()
         pf = torch.empty(proto.total, dtype=torch.float32, device=self.device)
         vf = torch.empty_like(pf)
-        dist.recv(pf, fc0)
-        dist.recv(vf, fc0)
+        comm.p2p(recvs=[(pf, fc0), (vf, fc0)])
         fp = [[t.cpu().numpy().copy() for t in row] for row in proto._views(pf)]
         fv = [[t.cpu().numpy().copy() for t in row] for row in proto._views(vf)]
         cp, cv = self.conv.state_numpy()
@@ -626,11 +822,17 @@ class StanzaCluster:
         blob = self._replica_blob()
         if blob is not None:
             self.replica_snapshots[self.conv_ids[holder]] = blob
-        nbytes = 2 * 4 * self.partition.fc_params + 16 * len(self.layers)
-        self.transport.record("checkpoint", nbytes)
-        self.transport.tag_payload_bytes[Tag.CHECKPOINT] += nbytes
-        self.transport.tag_messages[Tag.CHECKPOINT] += 1
+        tr = self.transport
+        tr.begin_phase("checkpoint")
+        tr.send(self.fc_ids[0], self.conv_ids[holder], Tag.CHECKPOINT, self._blob_len(),
+                op="checkpoint")
+        tr.end_phase()
         return st
+
+    def _blob_len(self) -> int:
+        """Length of the STZC blob of the FC block (checkpointing.py:44-50):
+        header + two STZT blobs (params, velocities)."""
+        return stzc_blob_len([[shp for (_, shp, _) in row] for row in self._fc_proto().slots])
 
     def _fc_proto(self) -> BlockEngine:
         return BlockEngine(self.partition.fc_block, (self.boundary_activations,), 1,
@@ -642,22 +844,16 @@ class StanzaCluster:
             eng = self.fcs[0]
             self._fc_replica = (eng.params_flat.clone(), eng.vel_flat.clone())
             return
-        import torch.distributed as dist
         comm = self.comm
         fc0 = comm.n_conv
-        ops = []
         if comm.rank == fc0:
-            ops = [dist.P2POp(dist.isend, t, holder, group=comm.act_group)
-                   for t in (self.fcs[0].params_flat, self.fcs[0].vel_flat)]
+            comm.p2p(sends=[(self.fcs[0].params_flat, holder), (self.fcs[0].vel_flat, holder)])
         elif comm.rank == holder:
             total = self._fc_proto().total
             if self._fc_replica is None or self._fc_replica[0].numel() != total:
                 self._fc_replica = (torch.empty(total, dtype=torch.float32, device=self.device),
                                     torch.empty(total, dtype=torch.float32, device=self.device))
-            ops = [dist.P2POp(dist.irecv, t, fc0, group=comm.act_group)
-                   for t in self._fc_replica]
-        for w in (dist.batch_isend_irecv(ops) if ops else []):
-            w.wait()
+            comm.p2p(recvs=[(t, fc0) for t in self._fc_replica])
 
     def _holds_replica(self) -> bool:
         if self._fc_replica is None:
@@ -688,41 +884,37 @@ class StanzaCluster:
             self.fcs[0].vel_flat.copy_(vf)
             self.fcs[0].pack_weights()
             return self._replica_iteration
-        import torch.distributed as dist
         comm = self.comm
-        ops = []
         if comm.rank == self._replica_holder:
-            for r in comm.fc_ranks:
-                ops += [dist.P2POp(dist.isend, t, r, group=comm.act_group)
-                        for t in self._fc_replica]
+            comm.p2p(sends=[(t, r) for r in comm.fc_ranks for t in self._fc_replica])
         elif not comm.is_conv:
             eng = self.fcs[0]
-            ops = [dist.P2POp(dist.irecv, t, self._replica_holder, group=comm.act_group)
-                   for t in (eng.params_flat, eng.vel_flat)]
-        for w in (dist.batch_isend_irecv(ops) if ops else []):
-            w.wait()
-        if not comm.is_conv:
-            self.fcs[0].pack_weights()
+            comm.p2p(recvs=[(t, self._replica_holder) for t in (eng.params_flat, eng.vel_flat)])
+            eng.pack_weights()
         return self._replica_iteration
+
+    def close(self) -> None:
+        """Unmap peer buffers (one process per GPU)."""
+        for part in (self._link, self._peer):
+            if part is not None:
+                part.close()
+        self._link = self._peer = None
 
     # -- phase timing ----------------------------------------------------------------
 
-    def _events(self):
-        return []
-
-    def _event(self):
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(torch.cuda.current_stream(self.device))
-        return e
-
     def _resolve_phase_times(self):
-        if not self.time_phases or not getattr(self, "_pending_events", None):
+        """CUDA-event phase times of the eager steps since the last call:
+        each ledger PhaseRecord gets ``device_ms`` of its label and
+        ``device_phase_ms`` gets one {mark: ms} dict per step (including
+        conv_backward, which is not a reference phase)."""
+        if not self._pending_events:
             return
         torch.cuda.synchronize(self.device)
-        recs = [p for p in self.transport.phases if p.label in PHASES]
-        i = len(recs) - 6 * len(self._pending_events)
-        for ev in self._pending_events:
+        for ev, recs in self._pending_events:
+            ms: dict = {}
             for (label, e0), (_, e1) in zip(ev[:-1], ev[1:]):
-                recs[i].elapsed_ms = e0.elapsed_time(e1)
-                i += 1
+                ms[label] = ms.get(label, 0.0) + e0.elapsed_time(e1)
+            self.device_phase_ms.append(ms)
+            for rec in recs:
+                rec.device_ms = ms.get(rec.label)
         self._pending_events = []
