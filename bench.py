@@ -76,17 +76,87 @@ def blas_threads() -> int:
         return 1
 
 
-def oracle_sample(model: str, images: int = 1, classes: int = 1000):
-    """One co-located layer-separated iteration of the oracle on `images`
-    images per CONV worker (1 CONV : 1 FC); returns seconds."""
+def host_info() -> dict:
+    import platform
+    import numpy as np
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next((l.split(":", 1)[1].strip() for l in fh if l.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": cpu or platform.processor(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "blas_threads": blas_threads(), "numpy": np.__version__}
+
+
+_REF_K = {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32}
+
+
+def reference_sample(model: str, n_conv: int, n_fc: int, k: int) -> dict:
+    """One bounded sample of the reference iteration on the host (the oracle
+    port, pinned bit-exact to the reference's StanzaCluster), timed per part
+    as BASELINE.md §2b item 3 prescribes:
+
+    * t_img: the CONV trunk forward + backward on ONE image (the reference
+      runs every CONV worker's trunk sequentially, stanza_runtime.py:218,
+      :366, so a worker's K images cost K * t_img);
+    * t_fc: one FC worker's step at its full M = (group size) * K rows --
+      forward, SoftmaxCE, backward (stanza_runtime.py:255-276);
+    * t_upd: the FC-group gradient sum (n_fc > 1) and the momentum SGD of
+      every replica (stanza_runtime.py:309-350).
+
+    The reference iteration is n_conv*K*t_img + n_fc*t_fc + t_upd
+    (extrapolated from the measured parts; the FC workers run sequentially
+    in the reference's _fc_step loop)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
     import stanza_oracle as orc
     layers, shape = {"alexnet_exec": orc.alexnet_layers, "vgg16_exec": orc.vgg16_layers,
                      "resnet50_exec": orc.resnet_layers}.get(model, orc.alexnet_layers)()
-    mk = orc.batch_fn(shape, images, 7, classes=classes)
+    cut = orc.split_index(layers)
+    front, back = layers[:cut], layers[cut:]
+    params = orc.seeded_init(layers, 3)
+    conv_p, fc_p = params[:cut], params[cut:]
+    mk = orc.batch_fn(shape, 1, 7, classes=1000)
+    x, _ = mk(0, 0)
     t0 = time.perf_counter()
-    orc.layer_separated_train(layers, images, 1, 1, 1, 3, mk)
-    return time.perf_counter() - t0
+    a, cache = orc.block_forward(front, conv_p, x)
+    orc.block_backward(front, conv_p, cache, np.ones_like(a))   # incl. layer-0 dgrad, as the reference
+    t_img = time.perf_counter() - t0
+    m = max(orc.plan_groups(n_conv, n_fc).count(j) for j in range(n_fc)) * k
+    gen = np.random.Generator(np.random.PCG64(11))
+    xs = gen.standard_normal((m, a.shape[1])).astype(np.float32)
+    ys = gen.integers(0, 1000, size=m)
+    t0 = time.perf_counter()
+    out, fcache = orc.block_forward(back, fc_p, xs, labels=ys)
+    _, fgrads = orc.block_backward(back, fc_p, fcache, None)
+    t_fc = time.perf_counter() - t0
+    conv_g = [[np.zeros_like(t) for t in row] for row in conv_p]
+    t0 = time.perf_counter()
+    if n_fc > 1:
+        orc.allreduce_sum([orc._flat(fgrads)] * n_fc, 0)
+    for _ in range(n_fc):
+        orc.sgd_update(fc_p, fgrads, [[np.zeros_like(t) for t in r] for r in fc_p], n_conv * k,
+                       0.01, 0.9)
+    for _ in range(n_conv):
+        orc.sgd_update(conv_p, conv_g, [[np.zeros_like(t) for t in r] for r in conv_p],
+                       n_conv * k, 0.01, 0.9)
+    t_upd = time.perf_counter() - t0
+    t_iter = n_conv * k * t_img + n_fc * t_fc + t_upd
+    return {"t_img": t_img, "t_fc": t_fc, "t_upd": t_upd, "t_iter": t_iter, "m": m}
+
+
+def reference_baseline(model, n_conv, n_fc, k, steps, budget=150.0) -> dict:
+    samples, t_start = [], time.perf_counter()
+    for _ in range(max(steps, 1)):
+        samples.append(reference_sample(model, n_conv, n_fc, k))
+        if time.perf_counter() - t_start > budget:
+            break
+    t_iter = statistics.median(s["t_iter"] for s in samples)
+    parts = {key: statistics.median(s[key] for s in samples) for key in ("t_img", "t_fc", "t_upd")}
+    return {"value": n_conv * k / t_iter, "t_iter": t_iter, "samples": len(samples),
+            "m": samples[0]["m"], **parts}
 
 
 def reference_arm(args):
@@ -95,37 +165,35 @@ def reference_arm(args):
         return 0
     from paper_1812_10624_b200.roles import gpu_roles
     n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
-    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32}.get(
-        args.model, 128)
-    budget = 150.0
+    k = args.batch_k or _REF_K.get(args.model, 128)
     for _ in range(min(args.warmup, 1)):
-        oracle_sample(args.model)
-    times, t_start = [], time.perf_counter()
-    for _ in range(args.steps):
-        times.append(oracle_sample(args.model))
-        if time.perf_counter() - t_start > budget:
-            break
-    sec_per_img = statistics.mean(times)
-    value = 1.0 / sec_per_img
-    cores = blas_threads()
+        reference_sample(args.model, n_conv, n_fc, k)
+    ref = reference_baseline(args.model, n_conv, n_fc, k, args.steps)
+    info = host_info()
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
-        "ms_per_step": sec_per_img * 1e3 * n_conv * k, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": ref["samples"], "warmup": min(args.warmup, 1),
+        "ms_per_step": ref["t_iter"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate/f32-storage",
         "data": "synthetic",
         "config": workload_config(args, n_conv, n_fc, k),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"oracle/stanza_oracle.py layer_separated_train, 1 image "
-                                   f"per step through the full {args.model} co-located "
-                                   f"iteration (trunk fwd+bwd, FC fwd+bwd, SGD); "
-                                   f"{len(times)} timed samples; ms_per_step extrapolates "
-                                   f"x{n_conv * k} images (CONV workers run sequentially "
-                                   f"in the reference, stanza_runtime.py:218,:366)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": ref["value"], "unit": UNIT, "cores": info["blas_threads"],
+                         "kind": "port", "host": info, "sample": _sample_text(ref, n_conv, n_fc,
+                                                                              k)},
+        "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _sample_text(ref, n_conv, n_fc, k):
+    return (f"oracle/stanza_oracle.py (the reference algorithm, pinned bit-exact to its "
+            f"StanzaCluster) per part, median of {ref['samples']} samples: CONV trunk "
+            f"fwd+bwd {ref['t_img']:.3f} s/image, FC step at M={ref['m']} {ref['t_fc']:.3f} s, "
+            f"exchange+SGD of every replica {ref['t_upd']:.3f} s; iteration = {n_conv}*{k}*t_img "
+            f"+ {n_fc}*t_fc + t_upd = {ref['t_iter']:.1f} s (extrapolated: the reference runs "
+            f"CONV workers and FC workers sequentially, stanza_runtime.py:218,:255-276,:366)")
 
 
 def workload_config(args, n_conv, n_fc, k):
@@ -260,82 +328,44 @@ def committed_traffic(kernel_key: str):
         return None
 
 
-def nvlink_probe(torch, dist, comm, dev, per_conv: int, reps: int = 10):
-    """CONV<->FC transfer rates over NVLink, timed OUTSIDE the step.
-
-    Inside the step the gather/scatter overlap compute and the phase clocks
-    include waiting, so neither gives a transfer rate.  Here every rank posts
-    exactly one micro-batch's exchange through the step's own RoleComm calls
-    (post_activations = the many-to-one gather, post_boundary = the
-    one-to-many scatter, stanza_runtime.py:228-307 in the reference), timed
-    between two barriers with CUDA events after wait(), max over ranks,
-    median of `reps`.  `link_GBps` is one 256 MiB NCCL send CONV 0 -> its FC
-    worker, the measured single-peer ceiling the fractions are taken against."""
-    fan = max(len(comm.members(i)) for i in range(comm.n_fc))
-    n_el = per_conv // 4
-
-    def timed(post_fn, make):
-        out = []
-        for r in range(reps + 3):
-            send, recv = make()
-            torch.cuda.synchronize(dev)
-            dist.barrier()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record()
-            for req in post_fn(send, recv):
-                req.wait()
-            b.record()
-            torch.cuda.synchronize(dev)
-            t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            if r >= 3:
-                out.append(float(t.item()))
-        return statistics.median(out)
-
-    buf_c = torch.empty(n_el, dtype=torch.float32, device=dev)
-    bufs_f = [torch.empty(n_el, dtype=torch.float32, device=dev)
-              for _ in range(len(comm.members(comm.index)))] if not comm.is_conv else []
-
-    def make_gather():
-        return ([buf_c], None) if comm.is_conv else (None, [[t] for t in bufs_f])
-
-    def make_scatter():
-        return (None, [buf_c]) if comm.is_conv else ([[t] for t in bufs_f], None)
-
-    g_ms = timed(comm.post_activations, make_gather)
-    s_ms = timed(comm.post_boundary, make_scatter)
-    # single-peer ceiling: CONV 0 -> its FC worker
-    big = 256 << 20
-    src, dst = 0, comm.fc_rank_of(0)
-    link = torch.empty(big // 4, dtype=torch.float32, device=dev) \
-        if comm.rank in (src, dst) else None
-
-    def post_link(send, recv):
-        if comm.rank == src:
-            return dist.batch_isend_irecv([dist.P2POp(dist.isend, link, dst,
-                                                      group=comm.act_group)])
-        if comm.rank == dst:
-            return dist.batch_isend_irecv([dist.P2POp(dist.irecv, link, src,
-                                                      group=comm.act_group)])
-        return []
-
-    l_ms = timed(post_link, lambda: (None, None))
-    link_gbs = big / (l_ms / 1e3) / 1e9
-    gather_gbs = fan * per_conv / (g_ms / 1e3) / 1e9
-    scatter_gbs = fan * per_conv / (s_ms / 1e3) / 1e9
+def nvlink_probe(torch, dist, cl, reps: int = 20) -> dict:
+    """CONV<->FC traffic of the step through the step's own link calls,
+    timed OUTSIDE the timed region (inside the step the transfers overlap
+    compute, so no phase clock is a transfer time).  ``reps`` back-to-back
+    round trips of micro-batch 0 on the real buffers (PeerLink.probe:
+    CONV put_acts -> FC get_acts -> FC put_grads -> CONV get_grads, 4 B per
+    element on the link, one message per member per direction), max over
+    ranks; ``link_GBps`` = one 256 MiB put CONV 0 -> its FC worker (the
+    same kernel, PeerLink.ceiling), the single-peer ceiling the fractions
+    are taken against."""
+    link = cl._link
+    if link is None:
+        return None
+    kb = link.kb
+    if cl.conv is not None:
+        src = cl.conv._act(len(cl.conv.ops) - 1).rows_view(0, kb)
+        labels = cl.labels[:kb] if cl.labels is not None else None
+    else:
+        src = cl.fcs[0].gin[0].rows_view(0, link.g * kb)
+        labels = None
+    rt = link.probe(src, labels, reps=reps)
+    ceil = link.ceiling()
+    objs = [None] * dist.get_world_size()
+    dist.all_gather_object(objs, ceil)
+    ceil = next(c for c in objs if c is not None)
+    per_dir = rt["bytes_per_direction"]
+    gbs = 2 * per_dir / (rt["round_trip_ms"] / 1e3) / 1e9
     return {
-        "gather_GBps": gather_gbs, "scatter_GBps": scatter_gbs,
-        "gather_ms": g_ms, "scatter_ms": s_ms,
-        "link_GBps": link_gbs, "gather_frac": gather_gbs / link_gbs,
-        "scatter_frac": scatter_gbs / link_gbs,
-        "bytes_per_conv_worker": per_conv, "fan_in": fan,
-        "note": ("one step's [K,A] CONV->FC gather and FC->CONV scatter through "
-                 "RoleComm.post_activations / post_boundary (NCCL P2P over NVLink), "
-                 "timed alone between barriers (CUDA events, max over ranks, median of "
-                 f"{reps}); GBps = bytes into / out of the busiest FC worker "
-                 "(fan_in x bytes_per_conv_worker) / time; frac against link_GBps = one "
-                 "256 MiB NCCL send between two GPUs measured in the same run"),
+        "round_trip_ms": rt["round_trip_ms"], "bytes_per_direction": per_dir,
+        "fan_in": link.g, "micro_batch_rows": kb,
+        "exchange_GBps": gbs, "link_GBps": ceil, "frac_of_link": gbs / ceil if ceil else None,
+        "nvlink5_GBps": 900.0, "frac_of_nvlink5": gbs / 900.0,
+        "note": ("one micro-batch's gather (every member's kb x A rows, fp32 on the link, "
+                 "into the FC worker) + scatter (back), through the step's PeerLink calls "
+                 f"on the step's buffers, {reps} back-to-back round trips, max over ranks; "
+                 "exchange_GBps = bytes into + out of the busiest FC worker / round-trip "
+                 "time (includes the flag handshakes and the receivers' split kernels); "
+                 "link_GBps = one 256 MiB put of the same kernel, CONV 0 -> its FC worker"),
     }
 
 
@@ -344,7 +374,6 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -354,9 +383,8 @@ def main():
     from paper_1812_10624_b200.stanza_runtime import StanzaCluster
 
     rank, world, local = env_rank()
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N>1 must be launched with torch.distributed.run")
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N>1 must be launched with torch.distributed.run")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _lib.load()
@@ -371,8 +399,10 @@ def main():
         from paper_1812_10624_b200.comm import RoleComm
         comm = RoleComm(n_conv, n_fc)
 
-    def batch_fn(it, i):  # only used for shapes; the timed loop feeds device pools
-        raise RuntimeError("bench feeds device-resident batches")
+    host_pool = []
+
+    def batch_fn(it, i):   # a loader handing out pinned host batches (train(), e2e)
+        return host_pool[it % len(host_pool)]
 
     cl = StanzaCluster(spec, n_conv=n_conv, n_fc=n_fc, batch_fn=batch_fn, lr=0.01,
                        momentum=0.9, seed=3, device=dev, comm=comm,
@@ -383,7 +413,7 @@ def main():
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     pool_x, pool_y = [], []
-    if is_conv_rank:
+    if cl.x is not None:
         for _ in range(args.pool):
             pool_x.append(torch.randn(cl.x.shape, generator=gen, device=dev))
             pool_y.append(torch.randint(0, classes, cl.labels.shape, generator=gen,
@@ -391,7 +421,7 @@ def main():
     slots = torch.zeros(max(args.steps, args.warmup, 1), dtype=torch.float64, device=dev)
 
     def one(i, slot=None):
-        if is_conv_rank:
+        if pool_x:
             j = i % args.pool
             cl.step(slot, x=pool_x[j], labels=pool_y[j])
         else:
@@ -404,46 +434,46 @@ def main():
 
     clocks = ClockSampler(local).start()   # running before the timed region begins
 
-    # warm-up (W >= 3 enforced)
+    # warm-up (W >= 3 enforced); the measured GEMM tile shapes
+    # (_lib.autotune_tiles) are chosen on the first, eager, warm-up step,
+    # before any CUDA graph is captured
     warm = max(args.warmup, 3)
     tiles = {}
     for i in range(warm):
         sl = slots[i % slots.numel():i % slots.numel() + 1]
         if i == 0 and not args.no_autotune:
-            # measured GEMM tile shapes (_lib.autotune_tiles), chosen on the
-            # first (eager) warm-up step, before any CUDA graph is captured
             tiles = _lib.autotune_tiles(lambda: one(0, sl))
         else:
             one(i, sl)
     sync_all()
 
-    # one process per GPU: StanzaCluster captures each compute segment as a
-    # CUDA graph when it first sees it after its first step -- visit every
-    # pooled batch once more, untimed, so no capture lands in the timed region
-    if world > 1:
+    # one CUDA graph per pooled batch: the whole step (single device, or every
+    # rank's part of it over the peer-memory link); exchange="nccl" keeps its
+    # NCCL calls on the host and replays compute segments instead
+    graphs = None
+    if not args.eager and cl.graph_capable():
+        graph_slots = torch.zeros((args.pool, 1), dtype=torch.float64, device=dev)
+        graphs = [cl.capture(pool_x[j] if pool_x else None, pool_y[j] if pool_y else None,
+                             graph_slots[j]) for j in range(args.pool)]
+        sync_all()
+        for j in range(args.pool):
+            graphs[j].replay()
+        sync_all()
+
+        def one(i, slot=None):  # noqa: F811 -- the graph replay replaces the eager step
+            graphs[i % args.pool].replay()
+    elif world > 1:   # segment graphs are captured on first sight: visit every batch untimed
         for i in range(args.pool):
             one(warm + i, slots[0:1])
         sync_all()
 
-    # single device: one CUDA graph per pooled batch (the whole step, captured)
-    graphs = None
-    if world == 1 and not args.eager:
-        graph_slots = torch.zeros((args.pool, 1), dtype=torch.float64, device=dev)
-        graphs = [cl.capture(pool_x[j], pool_y[j], graph_slots[j]) for j in range(args.pool)]
-        for j in range(args.pool):
-            graphs[j].replay()
-        torch.cuda.synchronize(dev)
-
-        def one(i, slot=None):  # noqa: F811 -- the graph replay replaces the eager step
-            graphs[i % args.pool].replay()
-
     # ---- timed region: device-resident inputs ------------------------------------
     n0 = lib.stz_launch_count()
-    if is_conv_rank:
+    if pool_x:
         cl.step(slots[0:1], x=pool_x[0], labels=pool_y[0])
     else:
         cl.step(slots[0:1])
-    torch.cuda.synchronize(dev)
+    sync_all()
     per_step_launches = lib.stz_launch_count() - n0
     launches0 = lib.stz_launch_count()
     stream = torch.cuda.current_stream(dev)
@@ -456,7 +486,6 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize(dev)
     clocks.mark_end()
-    clocks.stop()
     launches = lib.stz_launch_count() - launches0
     if graphs is not None:   # replays launch the captured kernels without host calls
         launches = per_step_launches * args.steps
@@ -469,81 +498,36 @@ def main():
     images = n_conv * k
     value = images / (ms / 1e3)
 
-    # ---- e2e: host buffers through the public step API ---------------------------
-    h2d = 0
-    if is_conv_rank:
-        xh = pool_x[0].cpu().pin_memory()
-        yh = pool_y[0].cpu().pin_memory()
-        h2d = xh.numel() * 4 + yh.numel() * 4
-    loss_h = torch.zeros(args.steps, dtype=torch.float64).pin_memory()
-    # double-buffered input pipeline (a prefetching loader): step i+1's batch is
-    # copied host -> device on a side stream while step i runs; every step still
-    # moves its full batch over PCIe and reads its loss back inside the region
-    # both buffers start as real batches: the untimed capture steps below run on them
-    xbuf = [cl.x, pool_x[0].clone()] if is_conv_rank else [None, None]
-    ybuf = [cl.labels, pool_y[0].clone()] if is_conv_rank else [None, None]
-    if is_conv_rank:
-        cl.x.copy_(pool_x[0])
-        cl.labels.copy_(pool_y[0])
-    e2e_slot = torch.zeros(1, dtype=torch.float64, device=dev)
-    g_e2e = None
-    if graphs is not None:
-        g_e2e = [cl.capture(xbuf[0], ybuf[0], e2e_slot), cl.capture(xbuf[1], ybuf[1], e2e_slot)]
-    copy_stream = torch.cuda.Stream(dev)
-    copied = [torch.cuda.Event(), torch.cuda.Event()]
-    consumed = [torch.cuda.Event(), torch.cuda.Event()]
-
-    def prefetch(buf):
-        with torch.cuda.stream(copy_stream):
-            if is_conv_rank:
-                xbuf[buf].copy_(xh, non_blocking=True)
-                ybuf[buf].copy_(yh, non_blocking=True)
-            copied[buf].record(copy_stream)
-
-    if world > 1 and is_conv_rank:   # capture the e2e buffers' segments untimed
-        for b in range(2):
-            cl.step(slots[0:1], x=xbuf[b], labels=ybuf[b])
-    elif world > 1:
-        for b in range(2):
-            cl.step(slots[0:1])
+    # ---- e2e: StanzaCluster.train() fed from pinned host batches ----------------
+    # the public entry point: each iteration's batch comes from batch_fn (here a
+    # loader returning pinned host tensors), is copied host -> device on train()'s
+    # side stream while the previous step runs, every step is a graph replay, and
+    # every step's loss is copied back to host memory
+    for j in range(len(pool_x)):
+        host_pool.append((pool_x[j].cpu().pin_memory(), pool_y[j].cpu().pin_memory()))
+    cl.iteration = 0
+    cl.train(2)                     # captures the feed buffers' graphs, untimed
     sync_all()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    copy_stream.wait_event(e2)
-    prefetch(0)
-    for i in range(args.steps):
-        buf = i & 1
-        stream.wait_event(copied[buf])
-        if i + 1 < args.steps:
-            if i >= 1:
-                copy_stream.wait_event(consumed[buf ^ 1])
-            prefetch(buf ^ 1)
-        if g_e2e is not None:
-            g_e2e[buf].replay()
-            loss_h[i:i + 1].copy_(e2e_slot, non_blocking=True)
-        elif is_conv_rank:
-            cl.step(slots[i:i + 1], x=xbuf[buf], labels=ybuf[buf])
-            loss_h[i:i + 1].copy_(slots[i:i + 1], non_blocking=True)
-        else:
-            cl.step(slots[i:i + 1])
-            loss_h[i:i + 1].copy_(slots[i:i + 1], non_blocking=True)
-        consumed[buf].record(stream)
+    res = cl.train(args.steps)
     e3.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = torch.tensor([e2.elapsed_time(e3) / args.steps], dtype=torch.float64, device=dev)
+    h2d = (cl.x.numel() * 4 + cl.labels.numel() * 4) if pool_x else 0
     io = torch.tensor([float(h2d), float(8 if cl.fcs else 0)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         dist.all_reduce(io, op=dist.ReduceOp.SUM)
     e2e_ms = float(e2e_ms.item())
+    finite = all(l == l for l in res.losses)
 
-    # ---- per-call kernel timing (separate, untimed pass) --------------------------
+    # ---- per-call kernel timing (separate, untimed eager pass) -------------------
     timer = CallTimer(torch)
     _lib.PROFILE_HOOK = timer
     cl.time_phases = True
-    cl._pending_events = []
-    if is_conv_rank:
+    if pool_x:
         cl.step(None, x=pool_x[0], labels=pool_y[0])
     else:
         cl.step(None)
@@ -551,16 +535,15 @@ def main():
     cl._resolve_phase_times()
     cl.time_phases = False
     calls = timer.table()
-    phase_ms = {}
-    for rec in cl.transport.phases[-6:]:
-        phase_ms[rec.label] = rec.elapsed_ms
+    phase_ms = cl.device_phase_ms[-1] if cl.device_phase_ms else {}
 
     bf16_peak, hbm_peak, peak_src = peaks()
     # dominant kernel = the ABI call with the largest total time among the
-    # ones that carry algorithmic work (GEMM FLOPs or HBM bytes)
+    # ones that carry algorithmic work (GEMM FLOPs or HBM bytes); the link
+    # gets (which include the wait for the peer) are not kernels of the step's work
     top_key, top = None, (0.0, 0)
     for key, (tot, cnt) in calls.items():
-        if (key[1] > 0 or key[2] > 0) and tot > top[0]:
+        if (key[1] > 0 or key[2] > 0) and tot > top[0] and not key[0].startswith("link_get"):
             top_key, top = key, (tot, cnt)
     fl = top_key[1] if top_key else 0.0
     nb = top_key[2] if top_key else 0.0
@@ -571,13 +554,14 @@ def main():
     kernel_key = f"{args.model}:{top_key[0]}" if top_key else None
     step_ms_sum = sum(tot for tot, _ in calls.values())
     fc_fl = sum(kk[1] * c for kk, (_, c) in calls.items() if kk[0].startswith("fc"))
-    fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("fc"))
-    per_call = {f"{kk[0]}": {"ms": tot / max(c, 1), "n": c, "total_ms": tot,
-                             "tflops": (kk[1] / (tot / max(c, 1) / 1e3) / 1e12)
-                             if kk[1] and tot else None,
-                             "GBps": (kk[2] / (tot / max(c, 1) / 1e3) / 1e9)
-                             if kk[2] and tot else None}
-                for kk, (tot, c) in sorted(calls.items(), key=lambda kv: -kv[1][0])}
+    fc_ms = sum(tot for kk, (tot, _) in calls.items() if kk[0].startswith("fc") and kk[1] > 0)
+    per_call = {}
+    for kk, (tot, c) in sorted(calls.items(), key=lambda kv: -kv[1][0]):
+        mean = tot / max(c, 1)
+        gbs = kk[2] / (mean / 1e3) / 1e9 if kk[2] and tot else None
+        per_call[kk[0]] = {"ms": mean, "n": c, "total_ms": tot,
+                           "tflops": (kk[1] / (mean / 1e3) / 1e12) if kk[1] and tot else None,
+                           "GBps": gbs, "hbm_frac": gbs / hbm_peak if gbs else None}
     fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None
     roofline = {
         "bound": "hbm", "kernel": kernel_key, "achieved": achieved_gbs, "peak": hbm_peak,
@@ -603,10 +587,9 @@ def main():
 
     probe = None
     if world > 1 and not args.no_nvlink_probe:
-        probe = nvlink_probe(torch, dist, comm, dev, k * cl.boundary_activations * 4)
+        probe = nvlink_probe(torch, dist, cl)
 
-    line = None
-    # gather per-rank extras to rank 0
+    clocks.stop()
     extras = {"rank": rank, "role": "conv" if is_conv_rank else "fc", "phase_ms": phase_ms,
               "roofline": roofline, "fc_tflops": fc_tflops, "launches": launches}
     if world > 1:
@@ -617,14 +600,12 @@ def main():
     if rank == 0:
         conv_ex = next(o for o in objs if o["role"] == "conv")
         fc_ex = next((o for o in objs if o["fc_tflops"] is not None), conv_ex)
-        nvlink = probe
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            secs = [oracle_sample(args.model) for _ in range(2)]
-            v = 1.0 / statistics.mean(secs)
-            cpu = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "port",
-                   "sample": f"oracle layer_separated_train, 1 image x {len(secs)} "
-                             f"co-located {args.model} iterations on this host"}
+            ref = reference_baseline(args.model, n_conv, n_fc, k, 1)
+            info = host_info()
+            cpu = {"value": ref["value"], "unit": UNIT, "cores": info["blas_threads"],
+                   "kind": "port", "host": info, "sample": _sample_text(ref, n_conv, n_fc, k)}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": warm, "ms_per_step": ms,
@@ -638,9 +619,12 @@ def main():
             "e2e": {"value": images / (e2e_ms / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(io[0].item()),
                     "d2h_bytes_per_step": int(io[1].item()),
-                    "api": ("StanzaCluster.step on a double-buffered input pipeline: every "
-                            "step's batch is copied from pinned host memory on a side stream "
-                            "(overlapping the previous step) and its loss copied back")},
+                    "ms_per_step": e2e_ms, "losses_finite": finite,
+                    "api": ("StanzaCluster.train(steps): batch_fn hands out pinned host "
+                            "batches; train() copies each step's batch host -> device on a "
+                            "side stream into the other of two persistent buffers while the "
+                            "previous step's CUDA graph runs, and copies every step's loss "
+                            "back to host memory")},
             "gpu_launches": int(sum(o["launches"] for o in objs)),
             "cuda_graph": bool(graphs is not None),
             "tile_overrides": {f"{kk[1]}": list(v) for kk, v in tiles.items()},
@@ -648,13 +632,14 @@ def main():
             "fc_tensor_pipe_frac": (6 * fc_ex["fc_tflops"] / bf16_peak)
             if fc_ex["fc_tflops"] else None,
             "fc_tflops_algorithmic": fc_ex["fc_tflops"],
-            "nvlink": nvlink,
+            "nvlink": probe,
             "phase_ms": {o["role"] + str(o["rank"]): o["phase_ms"] for o in objs},
             "gemm": "tcgen05 BF16x6 (3-way bf16 split, 6 MMAs, split fp32 TMEM accumulators)",
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        cl.close()
         dist.destroy_process_group()
     return 0
 

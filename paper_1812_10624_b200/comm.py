@@ -226,16 +226,11 @@ class _IpcMap:
             base = self._opened[handle] = int(out.value)
         return base + off
 
-    def failure(self) -> str | None:
-        """Description of a timed-out barrier (reads the status word: syncs)."""
-        from . import _lib
-        st = int(self.flags[_lib.PEER_FLAG_STATUS].item())
-        if st == 0:
-            return None
-        return f"group member {st & 0xFFFF} never reached the gradient exchange"
-
     def close(self) -> None:
-        self._ipc.close()
+        from . import _lib
+        for base in self._opened.values():
+            _lib.call("stz_ipc_close", ctypes.c_void_p(base))
+        self._opened.clear()
 
 
 class PeerLink:
@@ -352,6 +347,69 @@ class PeerLink:
                   out.ptr(), out.ps, out.width, self.flags.data_ptr(), j, 1, 1,
                   self._stream(), nbytes=kb * self.a * 10.0, tag="link_get_grads")
 
+    def probe(self, src_rows, labels=None, reps: int = 20) -> dict:
+        """Time the step's own exchange pattern alone (collective, after
+        training): ``reps`` back-to-back round trips of micro-batch 0 --
+        CONV: begin, put_acts(0), get_grads(0); FC: begin, get_acts(0),
+        put_grads(0) -- on the real buffers, no compute in between.
+        ``src_rows``: the Split rows this rank sends (CONV: its kb boundary
+        rows; FC: its g*kb boundary-gradient rows).  Returns the mean
+        milliseconds per round trip (max over ranks) and the bytes one
+        round trip moves into + out of this rank's FC worker."""
+        torch.cuda.synchronize(self.device)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            self.begin()
+            if self.comm.is_conv:
+                self.put_acts(0, src_rows, labels)
+                self.get_grads(0)
+            else:
+                self.get_acts(0)
+                self.put_grads(0, src_rows)
+        e1.record()
+        torch.cuda.synchronize(self.device)
+        t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return {"round_trip_ms": float(t.item()),
+                "bytes_per_direction": self.g * self.kb * self.a * 4}
+
+    def ceiling(self, nbytes: int = 256 << 20, reps: int = 5) -> float | None:
+        """Single-peer link ceiling of the put kernel (collective): CONV
+        worker 0 stores ``nbytes`` of fp32 into a buffer mapped from its FC
+        worker, timed on the sender (the kernel's closing system fence waits
+        for the stores to land).  GB/s on rank 0, None elsewhere."""
+        from . import _lib
+        from .engine import Split
+        d = 8192
+        rows = max(1, nbytes // (4 * d))
+        fc0 = self.comm.fc_rank_of(0)
+        me = self.comm.rank
+        dst = torch.empty(rows * d if me == fc0 else 1, dtype=torch.float32, device=self.device)
+        h = [self._ipc.handle(dst)] if me == fc0 else [None]
+        objs = [None] * self.comm.world
+        dist.all_gather_object(objs, h[0])
+        gbs = torch.zeros(1, dtype=torch.float64)
+        if me == 0:
+            src = Split.alloc("rows", (rows, d), d, self.device)
+            remote = self._ipc.open(*objs[fc0])
+            slot = torch.zeros(1, dtype=torch.int32, device=self.device)   # local dummy slot
+
+            def put():
+                _lib.call("stz_link_put", src.ptr(), src.ps, rows, d, d, remote, None, None,
+                          self.flags.data_ptr(), slot.data_ptr(), self._stream())
+            put()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                put()
+            e1.record()
+            torch.cuda.synchronize(self.device)
+            gbs[0] = rows * d * 4 / (e0.elapsed_time(e1) / reps / 1e3) / 1e9
+        dist.barrier()
+        return float(gbs.item()) if me == 0 else None
+
     def failure(self) -> str | None:
         """Description of a timed-out wait (reads the status word: syncs)."""
         from . import _lib
@@ -420,7 +478,9 @@ class PeerExchange:
         ranges, nr, fused = eng.fused_pack_ranges()
         _lib.call("stz_allreduce_sgd", self._grads, self._reds, self._flags, self.nranks,
                   self.me, ptr(eng.params_flat), ptr(eng.vel_flat), eng.total, float(lr),
-                  float(mu), inv_batch(n), ranges, nr, stream_of(eng.device))
+                  float(mu), inv_batch(n), ranges, nr, stream_of(eng.device),
+                  tag=f"{eng.tag}exchange_sgd",
+                  nbytes=20.0 * eng.total + 6.0 * eng.fused_param_count())
         eng.pack_weights(skip=fused)
 
     def failure(self) -> str | None:

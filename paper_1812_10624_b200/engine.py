@@ -445,10 +445,12 @@ class BlockEngine:
             ks, cs8, hs, ws_ = op0.s2d
             c, h, w = self.in_shape
             _lib.call("stzx_pack_s2d", ptr(xs), s.ptr(), s.ps, b, c, h, w,
-                      op0.layer.stride, op0.layer.padding, hs, ws_, cs8, st)
+                      op0.layer.stride, op0.layer.padding, hs, ws_, cs8, st,
+                      tag=f"{self.tag}pack_s2d", nbytes=4.0 * b * c * h * w + 6.0 * b * s.row_elems)
         elif s.layout == "nhwc":
             c, h, w = self.in_shape
-            _lib.call("stzx_pack_nchw", ptr(xs), s.ptr(), s.ps, b, c, h, w, s.width, st)
+            _lib.call("stzx_pack_nchw", ptr(xs), s.ptr(), s.ps, b, c, h, w, s.width, st,
+                      tag=f"{self.tag}pack_nchw", nbytes=4.0 * b * c * h * w + 6.0 * b * s.row_elems)
         else:
             _lib.call("stzx_pack_rows", ptr(xs), s.ptr(), s.ps, b, self.in_shape[0],
                       s.width, st)
@@ -506,7 +508,8 @@ class BlockEngine:
                 y = V(self.acts[i])
                 _lib.call("stzx_maxpool_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps,
                           ptr(self.args[i][r0:r1]), b, c, xin.width, h, w, l.kernel, l.stride,
-                          y.width if op.flat_out else 0, st)
+                          y.width if op.flat_out else 0, st, tag=f"{self.tag}pool{i}_fwd",
+                          nbytes=6.0 * b * xin.row_elems + 7.0 * b * self.args[i][0].numel())
             elif op.kind == "relu":
                 if self.acts[i] is not None:
                     y = V(self.acts[i])
@@ -676,7 +679,9 @@ class BlockEngine:
                 out = V(self.gin[i])
                 _lib.call("stzx_maxpool_bwd", g.ptr(), g.ps, ptr(self.args[i][r0:r1]), out.ptr(),
                           out.ps, mptr, b, c, out.width, h, w, l.kernel, l.stride,
-                          g.width if op.flat_out else 0, st)
+                          g.width if op.flat_out else 0, st, tag=f"{self.tag}pool{i}_bwd",
+                          nbytes=7.0 * b * self.args[i][0].numel()
+                          + (6.0 + 2.0 * (mptr is not None)) * b * out.row_elems)
                 g_full = self.gin[i]
             elif op.kind in ("conv", "fc"):
                 if do_w:
@@ -750,6 +755,11 @@ class BlockEngine:
             self._pack_ranges = (_lib.range_array(rs), len(rs), frozenset(idx))
         return self._pack_ranges
 
+    def fused_param_count(self) -> int:
+        """Parameters whose split-plane copy the fused SGD rewrites (FC W)."""
+        _, _, idx = self.fused_pack_ranges()
+        return sum(self.slots[i][0][2] for i in idx)
+
     def sgd(self, n: int, lr: float, mu: float, grad: torch.Tensor | None = None):
         """Momentum step over the whole flat block (tensor_core.py:366-388)
         fused with the refresh of the FC split-plane weight copies; the conv
@@ -758,7 +768,8 @@ class BlockEngine:
         ranges, nr, fused = self.fused_pack_ranges()
         _lib.call("stz_sgd_momentum_pack", ptr(self.params_flat), ptr(self.vel_flat), ptr(g),
                   self.total, float(lr), float(mu), inv_batch(n), ranges, nr,
-                  stream_of(self.device))
+                  stream_of(self.device), tag=f"{self.tag}sgd_pack",
+                  nbytes=20.0 * self.total + 6.0 * self.fused_param_count())
         self.pack_weights(skip=fused)
 
     def add_grads_from(self, other: "BlockEngine"):

@@ -71,10 +71,23 @@ class MissingSource(Timeout):
 
 
 class StanzaResult:
-    """Outcome of a training call (reference stanza_runtime.py:88-93)."""
+    """Outcome of a training call (reference stanza_runtime.py:88-93).
 
-    def __init__(self, losses: list, state: TrainState | None, transport: DeviceTransport):
-        self.losses, self.state, self.transport = losses, state, transport
+    ``state`` is the TrainState at the end of the call.  train() takes it as
+    a device-side snapshot (a device copy of the flat parameter / velocity
+    vectors; in one-process-per-GPU mode FC worker 0's block is sent to rank
+    0) and converts it to reference-layout numpy arrays on first access, so
+    the device -> host copy is only paid by callers that read it."""
+
+    def __init__(self, losses: list, state, transport: DeviceTransport):
+        self.losses, self.transport = losses, transport
+        self._state = state
+
+    @property
+    def state(self) -> TrainState | None:
+        if callable(self._state):
+            self._state = self._state()
+        return self._state
 
     def __repr__(self):
         return f"StanzaResult(losses={self.losses!r}, state=..., transport=...)"
@@ -771,7 +784,42 @@ class StanzaCluster:
         n = self.n_conv * self.k
         losses = [float(v) / n for v in host_losses[:n_it].tolist()]
         self._resolve_phase_times()
-        return StanzaResult(losses=losses, state=self.state(), transport=self.transport)
+        return StanzaResult(losses=losses, state=self._snapshot(), transport=self.transport)
+
+    def _snapshot(self):
+        """Device copy of the state now; returns a callable building the
+        TrainState from it (None on ranks other than 0)."""
+        it = self.iteration
+        if self.comm is None:
+            flats = [(e, e.params_flat.clone(), e.vel_flat.clone()) for e in (self.conv, self.fcs[0])]
+        else:
+            flats = self._gather_state()
+            if flats is None:
+                return None
+
+        def build():
+            ps, vs = [], []
+            for eng, pf, vf in flats:
+                ps += [[t.cpu().numpy().copy() for t in row] for row in eng._views(pf)]
+                vs += [[t.cpu().numpy().copy() for t in row] for row in eng._views(vf)]
+            return TrainState(it, ps, vs)
+        return build
+
+    def _gather_state(self):
+        """Collective: FC worker 0 ships its (w, v) to rank 0; rank 0 gets
+        [(conv engine, w, v), (FC prototype, w, v)] device copies."""
+        comm = self.comm
+        fc0 = comm.n_conv
+        if comm.rank == fc0:
+            comm.p2p(sends=[(self.fcs[0].params_flat, 0), (self.fcs[0].vel_flat, 0)])
+        if comm.rank != 0:
+            return None
+        proto = self._fc_proto()
+        pf = torch.empty(proto.total, dtype=torch.float32, device=self.device)
+        vf = torch.empty_like(pf)
+        comm.p2p(recvs=[(pf, fc0), (vf, fc0)])
+        return [(self.conv, self.conv.params_flat.clone(), self.conv.vel_flat.clone()),
+                (proto, pf, vf)]
 
     def check_peers(self) -> None:
         """Raise MissingSource if a device-side wait for a peer timed out
@@ -785,26 +833,8 @@ class StanzaCluster:
         """Full state stitched from the first CONV and the first FC replica.
         Collective in one-process-per-GPU mode: FC worker 0 ships its block to
         rank 0, which returns the TrainState (other ranks return None)."""
-        if self.comm is None:
-            cp, cv = self.conv.state_numpy()
-            fp, fv = self.fcs[0].state_numpy()
-            return TrainState(self.iteration, cp + fp, cv + fv)
-        comm = self.comm
-        fc0 = comm.n_conv
-        if comm.rank == fc0:
-            comm.p2p(sends=[(self.fcs[0].params_flat, 0), (self.fcs[0].vel_flat, 0)])
-        if comm.rank != 0:
-            return None
-        cut = self.partition.split_index
-        proto = self._fc_proto()
-        pf = torch.empty(proto.total, dtype=torch.float32, device=self.device)
-        vf = torch.empty_like(pf)
-        comm.p2p(recvs=[(pf, fc0), (vf, fc0)])
-        fp = [[t.cpu().numpy().copy() for t in row] for row in proto._views(pf)]
-        fv = [[t.cpu().numpy().copy() for t in row] for row in proto._views(vf)]
-        cp, cv = self.conv.state_numpy()
-        assert len(cp) == cut
-        return TrainState(self.iteration, cp + fp, cv + fv)
+        build = self._snapshot()
+        return build() if build is not None else None
 
     def checkpoint(self) -> TrainState:
         """Snapshot the run (stanza_runtime.py:182-211).  FC worker 0's block

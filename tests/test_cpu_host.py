@@ -156,3 +156,20 @@ def test_engine_fusion_plan_alexnet():
     for row in fc.slots:
         for off, _, _ in row:
             assert off % 4 == 0
+
+
+def test_runtime_and_bench_import():
+    """The public runtime, the communicator and bench.py import without a GPU."""
+    import importlib
+    rt = importlib.import_module("paper_1812_10624_b200.stanza_runtime")
+    for name in ("StanzaCluster", "StanzaResult", "MissingSource", "NodeId", "Role", "Tag",
+                 "NetConfig"):
+        assert hasattr(rt, name), name
+    comm = importlib.import_module("paper_1812_10624_b200.comm")
+    for name in ("RoleComm", "PeerLink", "PeerExchange"):
+        assert hasattr(comm, name), name
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    bench = importlib.import_module("bench")
+    assert callable(bench.main) and callable(bench.reference_arm)
