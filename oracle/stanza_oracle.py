@@ -37,6 +37,20 @@ UNPINNED -- no reference output exists to check this restatement against:
     ("residual", body, shortcut)      relu(body(x) + shortcut(x)); shortcut
                                       () is the identity; params = body's
                                       then shortcut's, one flat row
+
+and those of the Inception-V3 trunk (same status: defined here, unpinned):
+
+    ("conv", C, O, (kh, kw), s, (ph, pw))   asymmetric kernel / padding
+                                      (1xn, nx1); W [O, C, kh, kw]
+    ("avgpool", kernel, stride, pad)  zero-padded average pool, every window
+                                      divided by kernel^2 (padding counted)
+    ("concat", branches)              branches: tuple of layer tuples, each
+                                      applied to the same input; outputs
+                                      concatenated along channels in branch
+                                      order; params = every branch's in order,
+                                      one flat row; the input gradient is the
+                                      fp32 left fold of the branches' input
+                                      gradients in branch order
 """
 
 from __future__ import annotations
@@ -54,7 +68,13 @@ F64 = np.float64
 # ---------------------------------------------------------------------------
 
 def _conv_out_hw(h, w, k, s, p):
-    return (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    kh, kw = _pair(k)
+    ph, pw = _pair(p)
+    return (h + 2 * ph - kh) // s + 1, (w + 2 * pw - kw) // s + 1
+
+
+def _pair(v):
+    return (int(v[0]), int(v[1])) if isinstance(v, (tuple, list)) else (int(v), int(v))
 
 
 def conv_forward(x, w, b, stride, pad):
@@ -63,17 +83,19 @@ def conv_forward(x, w, b, stride, pad):
     Zero-padded input, one float64 contraction per kernel tap (kh, kw)
     accumulated in tap order, bias added in float64, one fp32 rounding.
     Returns (y, padded input) -- the padded input is the backward cache.
+    ``pad`` may be (ph, pw) and W [O, C, kh, kw] rectangular (Inception kinds).
     """
-    o, c, k, _ = w.shape
-    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad))) if pad else x
+    o, c, kh_, kw_ = w.shape
+    ph, pw = _pair(pad)
+    xp = np.pad(x, ((0, 0), (0, 0), (ph, ph), (pw, pw))) if (ph or pw) else x
     n, _, hp, wp = xp.shape
-    oh = (hp - k) // stride + 1
-    ow = (wp - k) // stride + 1
+    oh = (hp - kh_) // stride + 1
+    ow = (wp - kw_) // stride + 1
     xd = xp.astype(F64)
     wd = w.astype(F64)
     acc = np.zeros((n, o, oh, ow), F64)
-    for kh in range(k):
-        for kw in range(k):
+    for kh in range(kh_):
+        for kw in range(kw_):
             tap = xd[:, :, kh:kh + stride * oh:stride, kw:kw + stride * ow:stride]
             # sum over input channels for this tap: [n,c,h,w] x [o,c] -> [n,o,h,w]
             acc += np.einsum("nchw,oc->nohw", tap, wd[:, :, kh, kw])
@@ -87,7 +109,8 @@ def conv_backward(xp, w, gy, stride, pad):
     Returns (gx, gw, gb): input gradient (padding cropped), weight-gradient
     sum, bias-gradient sum, each computed in float64 and rounded once.
     """
-    o, c, k, _ = w.shape
+    o, c, kh_, kw_ = w.shape
+    ph, pw = _pair(pad)
     _, _, hp, wp = xp.shape
     oh, ow = gy.shape[2], gy.shape[3]
     gd = gy.astype(F64)
@@ -95,14 +118,14 @@ def conv_backward(xp, w, gy, stride, pad):
     wd = w.astype(F64)
     gw = np.zeros(wd.shape, F64)
     gxp = np.zeros(xd.shape, F64)
-    for kh in range(k):
-        for kw in range(k):
+    for kh in range(kh_):
+        for kw in range(kw_):
             tap = xd[:, :, kh:kh + stride * oh:stride, kw:kw + stride * ow:stride]
             gw[:, :, kh, kw] = np.einsum("nohw,nchw->oc", gd, tap)
             gxp[:, :, kh:kh + stride * oh:stride, kw:kw + stride * ow:stride] += \
                 np.einsum("nohw,oc->nchw", gd, wd[:, :, kh, kw])
     gb = gd.sum(axis=(0, 2, 3))
-    gx = gxp[:, :, pad:hp - pad, pad:wp - pad] if pad else gxp
+    gx = gxp[:, :, ph:hp - ph, pw:wp - pw]
     return gx.astype(F32), gw.astype(F32), gb.astype(F32)
 
 
@@ -133,6 +156,32 @@ def maxpool_backward(arg, x_shape, gy, k, s):
             hit = arg == kh * k + kw
             gx[:, :, kh:kh + s * oh:s, kw:kw + s * ow:s] += np.where(hit, gd, 0.0)
     return gx.astype(F32)
+
+
+def avgpool_forward(x, k, s, p):
+    """AvgPool2d (Inception kinds): zero padding p, window sum in float64
+    (kh-major), divided by k*k (padding counted), one fp32 rounding."""
+    xp = np.pad(x, ((0, 0), (0, 0), (p, p), (p, p))).astype(F64) if p else x.astype(F64)
+    n, c, hp, wp = xp.shape
+    oh, ow = (hp - k) // s + 1, (wp - k) // s + 1
+    acc = np.zeros((n, c, oh, ow), F64)
+    for kh in range(k):
+        for kw in range(k):
+            acc += xp[:, :, kh:kh + s * oh:s, kw:kw + s * ow:s]
+    return (acc / (k * k)).astype(F32)
+
+
+def avgpool_backward(x_shape, gy, k, s, p):
+    """Each input cell receives the sum over the windows covering it of
+    g / (k*k), in float64, rounded once."""
+    n, c, h, w = x_shape
+    oh, ow = gy.shape[2], gy.shape[3]
+    gxp = np.zeros((n, c, h + 2 * p, w + 2 * p), F64)
+    gd = gy.astype(F64) / (k * k)
+    for kh in range(k):
+        for kw in range(k):
+            gxp[:, :, kh:kh + s * oh:s, kw:kw + s * ow:s] += gd
+    return gxp[:, :, p:p + h, p:p + w].astype(F32)
 
 
 def fc_forward(x, w, b):
@@ -243,19 +292,23 @@ def param_shapes(layer):
     """tensor_core.py:81-88: conv W [O,C,k,k] + b [O]; FC W [in,out] + b [out]."""
     if layer[0] == "conv":
         _, cin, cout, k, _, _ = layer
-        return [(cout, cin, k, k), (cout,)]
+        kh, kw = _pair(k)
+        return [(cout, cin, kh, kw), (cout,)]
     if layer[0] == "fc":
         return [(layer[1], layer[2]), (layer[2],)]
     if layer[0] == "bn":
         return [(layer[1],), (layer[1],)]
     if layer[0] == "residual":
         return [s for l in layer[1] + layer[2] for s in param_shapes(l)]
+    if layer[0] == "concat":
+        return [s for br in layer[1] for l in br for s in param_shapes(l)]
     return []
 
 
 def fan_in(layer):
     if layer[0] == "conv":
-        return layer[1] * layer[3] * layer[3]
+        kh, kw = _pair(layer[3])
+        return layer[1] * kh * kw
     return layer[1]
 
 
@@ -269,6 +322,17 @@ def out_shape(layer, shape):
     if kind == "maxpool":
         _, k, s = layer
         return (shape[0], (shape[1] - k) // s + 1, (shape[2] - k) // s + 1)
+    if kind == "avgpool":
+        _, k, s, p = layer
+        return (shape[0], (shape[1] + 2 * p - k) // s + 1, (shape[2] + 2 * p - k) // s + 1)
+    if kind == "concat":
+        outs = []
+        for br in layer[1]:
+            sh = shape
+            for l in br:
+                sh = out_shape(l, sh)
+            outs.append(sh)
+        return (sum(o[0] for o in outs), outs[0][1], outs[0][2])
     if kind == "flatten":
         return (int(np.prod(shape)),)
     if kind == "fc":
@@ -289,6 +353,8 @@ def _init_layer(gen, layer):
         return [np.ones(layer[1], F32), np.zeros(layer[1], F32)]
     if layer[0] == "residual":
         return [t for l in layer[1] + layer[2] for t in _init_layer(gen, l)]
+    if layer[0] == "concat":
+        return [t for br in layer[1] for l in br for t in _init_layer(gen, l)]
     ts = []
     for shp in param_shapes(layer):
         bound = float(np.sqrt(1.0 / fan_in(layer)))
@@ -333,6 +399,21 @@ def block_forward(layers, params, x, labels=None):
         elif kind == "gap":
             cache = x.shape
             x = gap_forward(x)
+        elif kind == "avgpool":
+            cache = x.shape
+            x = avgpool_forward(x, layer[1], layer[2], layer[3])
+        elif kind == "concat":
+            outs, bcaches, off, bparams = [], [], 0, []
+            for br in layer[1]:
+                nb = len(param_shapes(("concat", (br,))))
+                pb = _split_rows(br, p[off:off + nb])
+                off += nb
+                yb, cb = block_forward(br, pb, x)
+                outs.append(yb)
+                bcaches.append(cb)
+                bparams.append(pb)
+            cache = (bcaches, bparams, [o.shape[1] for o in outs])
+            x = np.concatenate(outs, axis=1)
         elif kind == "residual":
             body, short = layer[1], layer[2]
             pb, ps = _split_rows(body, p), _split_rows(short, p[len(param_shapes(("residual", body, ()))):])
@@ -375,6 +456,18 @@ def block_backward(layers, params, caches, gy, need_input_grad=True):
             grads[i] = [dg, db]
         elif kind == "gap":
             gy = gap_backward(cache, gy)
+        elif kind == "avgpool":
+            gy = avgpool_backward(cache, gy, layer[1], layer[2], layer[3])
+        elif kind == "concat":
+            bcaches, bparams, widths = cache
+            c0, gx, flat = 0, None, []
+            for br, cb, pb, cw in zip(layer[1], bcaches, bparams, widths):
+                gxb, gb = block_backward(br, pb, cb, np.ascontiguousarray(gy[:, c0:c0 + cw]))
+                c0 += cw
+                gx = gxb if gx is None else (gx + gxb).astype(F32)
+                flat += [t for row in gb for t in row]
+            gy = gx
+            grads[i] = flat
         elif kind == "residual":
             body, short = layer[1], layer[2]
             cb, cs, mask, pb, ps = cache

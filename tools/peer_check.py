@@ -61,8 +61,13 @@ class FlatBlock:
         self._r = _lib.range_array([(OFF, rows * D, self.planes.data_ptr(),
                                      self.planes[0].numel(), D, D)])
 
+    tag = ""
+
     def fused_pack_ranges(self):
         return self._r, 1, frozenset()
+
+    def fused_param_count(self):
+        return rows * D
 
     def pack_weights(self, skip=frozenset()):
         pass
