@@ -250,6 +250,35 @@ int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, 
                  void* stream);
 int stzx_gap_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int HW, int C8,
                  void* stream);
+/* ---- Inception-V3 kinds (not in the reference: semantics
+ * restated in oracle/stanza_oracle.py, parity unpinned) ---- */
+/* Rectangular conv (kh x kw kernel, padding (ph, pw): 1xn / nx1) on the TMA
+ * im2col path (C8 % 32 == 0 for fwd / wgrad, O8 % 32 and stride 1 for
+ * dgrad); the square entries above are these with kh = kw, ph = pw. */
+int stzx_pack_conv2_w(const float* w, void* wf, size_t psf, void* wd, size_t psd, int O, int C,
+                      int kh, int kw, int C8, int O8, void* stream);
+int stzx_conv2_fwd(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
+                   void* y, size_t psy, int N, int C8, int H, int W, int O, int O8, int kh, int kw,
+                   int s, int ph, int pw, int relu, void* ws, size_t ws_bytes, void* stream);
+int stzx_conv2_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
+                     const void* mask, int N, int C, int C8, int H, int W, int O8, int kh, int kw,
+                     int s, int ph, int pw, void* ws, size_t ws_bytes, void* stream);
+int stzx_conv2_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
+                     int accumulate, int N, int C, int C8, int H, int W, int O, int O8, int kh,
+                     int kw, int s, int ph, int pw, void* ws, size_t ws_bytes, void* stream);
+/* AvgPool2d, zero padding p (2p <= k), every window divided by k*k: float64
+ * window sums (forward) / float64 sums of g/(k*k) over covering windows
+ * (backward, gather form), NHWC split planes [N][H][W][C8]. */
+int stzx_avgpool_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int C8, int H,
+                     int W, int k, int s, int p, void* stream);
+int stzx_avgpool_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int C8, int H, int W,
+                     int k, int s, int p, void* stream);
+/* Channel-slice copy of split-plane rows (the Inception concat and its
+ * backward): dst[r][d0 + c] = src[r][s0 + c], c < C; row pitches src8 / dst8;
+ * C, s0, d0, pitches multiples of 8. */
+int stzx_copy_channels(const void* src, size_t pss, int src8, int s0, void* dst, size_t psd,
+                       int dst8, int d0, size_t rows, int C, void* stream);
+
 /* y = a + b elementwise (fp32 RN), n a multiple of 8: residual input
  * gradients; b masked by a ReLU output (plane 0 > 0) when mask_b != NULL */
 int stzx_add(const void* a, size_t psa, const void* b, size_t psb, const void* mask_b, void* y,

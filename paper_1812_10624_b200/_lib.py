@@ -74,6 +74,14 @@ SIGNATURES = {
     "stzx_gap_fwd": (I, [P, Z, P, Z, I, I, I, P]),
     "stzx_gap_bwd": (I, [P, Z, P, Z, I, I, I, P]),
     "stzx_add": (I, [P, Z, P, Z, P, P, Z, Z, P]),
+    # Inception-V3 kinds
+    "stzx_pack_conv2_w": (I, [P, P, Z, P, Z, I, I, I, I, I, I, P]),
+    "stzx_conv2_fwd": (I, [P, Z, P, Z, P, P, Z, I, I, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_conv2_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_conv2_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
+    "stzx_avgpool_fwd": (I, [P, Z, P, Z, I, I, I, I, I, I, I, P]),
+    "stzx_avgpool_bwd": (I, [P, Z, P, Z, I, I, I, I, I, I, I, P]),
+    "stzx_copy_channels": (I, [P, Z, I, I, P, Z, I, I, Z, I, P]),
     # exchange + update over NVLink peer memory
     "stz_ipc_handle": (I, [P, P, P]),
     "stz_ipc_open": (I, [P, P]),

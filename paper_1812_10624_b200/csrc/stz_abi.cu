@@ -12,6 +12,7 @@
 // allocates device memory.  0 = ok, else an STZ_E* code; stz_last_error()
 // holds the message.
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -443,8 +444,11 @@ bool enc_tiled(CUtensorMap* out, const void* base, uint64_t inner, uint64_t oute
 }
 
 bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8, int s, int lo,
-                int hi, int pixels, int chans = 32) {
-  const std::string key = cache_key(1, (uintptr_t)base, N, H, W, C8, s, lo, hi, pixels, chans);
+                int hi, int pixels, int chans = 32, int lo_h = INT_MIN, int hi_h = INT_MIN) {
+  if (lo_h == INT_MIN) lo_h = lo;
+  if (hi_h == INT_MIN) hi_h = hi;
+  const std::string key = cache_key(1, (uintptr_t)base, N, H, W, C8, s, lo, hi, pixels, chans,
+                                    lo_h, hi_h);
   auto it = g_map_cache.find(key);
   if (it != g_map_cache.end()) {
     *out = it->second;
@@ -452,7 +456,7 @@ bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8,
   }
   cuuint64_t dims[4] = {(cuuint64_t)C8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
   cuuint64_t strides[3] = {(cuuint64_t)C8 * 2, (cuuint64_t)W * C8 * 2, (cuuint64_t)H * W * C8 * 2};
-  int lower[2] = {lo, lo}, upper[2] = {hi, hi};
+  int lower[2] = {lo, lo_h}, upper[2] = {hi, hi_h};   // {W, H}
   cuuint32_t es[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
   CUresult r = g_enc_im2col(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                             strides, lower, upper, (cuuint32_t)chans, (cuuint32_t)pixels, es,
@@ -546,7 +550,10 @@ bool op_tiled_mn(TgOperand& op, const bf16_t* p, size_t ps, int rows, int K, int
 // NHWC [N][H][W][C8] planes read as im2col; output grid OHxOW enumerates the
 // window starts (oh*s + lo, ow*s + lo); taps (th, tw) are TMA offsets
 bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H, int W, int C8,
-               int ksz, int s, int lo, int hi, int OH, int OW, int R) {
+               int ksz, int s, int lo, int hi, int OH, int OW, int R, int lo_h = INT_MIN,
+               int hi_h = INT_MIN) {
+  if (lo_h == INT_MIN) lo_h = lo;
+  if (hi_h == INT_MIN) hi_h = hi;
   op = TgOperand{};
   op.mode = mn ? TG_IM2COL_MN : TG_IM2COL_K;
   // MN-major (weight-gradient A): 64-channel SW128 boxes when the channels allow
@@ -554,6 +561,7 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
   op.nbox = mn ? R / (op.sw128 ? 64 : 32) : 1;
   op.box_bytes = op.sw128 ? 4096 : 2048;
   op.lo = lo;
+  op.lo_h = lo_h;
   op.s = s;
   op.C8 = C8;
   op.ksz = ksz;
@@ -563,7 +571,7 @@ bool op_im2col(TgOperand& op, bool mn, const bf16_t* p, size_t ps, int N, int H,
   op.d_k = FastDiv(ksz);
   for (int pl = 0; pl < 3; ++pl)
     if (!enc_im2col(&op.map[pl], p + pl * ps, N, H, W, C8, s, lo, hi, mn ? 32 : R,
-                    op.sw128 ? 64 : 32))
+                    op.sw128 ? 64 : 32, lo_h, hi_h))
       return false;
   return true;
 }
@@ -931,12 +939,18 @@ SvConvWgradA conv_wgrad_A(const bf16_t* x, size_t ps, int N, int C8, int H, int 
 
 // ---- GEMM-class ops: TMA kernel when the shapes allow, cp.async kernel otherwise ----
 
+// Rectangular kernels (kh x kw, padding (ph, pw): Inception's 1xn / nx1)
+// run only on the TMA im2col path -- per-dimension window corners, taps
+// (th, tw) = divmod(tap, kw); the band and cp.async producers are square-only.
+inline bool square_kp(int kh, int kw, int ph, int pw) { return kh == kw && ph == pw; }
+
 template <class EP>
 int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, const EP& ep, int N,
-                  int C8, int H, int W, int O, int k, int s, int p, int OH, int OW, void* ws,
-                  size_t ws_bytes, cudaStream_t st) {
-  const int M = N * OH * OW, K = k * k * C8;
-  if (k == 1 && s == 1 && p == 0 && tma_on() && C8 % 32 == 0) {
+                  int C8, int H, int W, int O, int kh, int kw, int s, int ph, int pw, int OH,
+                  int OW, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int M = N * OH * OW, K = kh * kw * C8;
+  const bool sq = square_kp(kh, kw, ph, pw);
+  if (kh == 1 && kw == 1 && s == 1 && ph == 0 && pw == 0 && tma_on() && C8 % 32 == 0) {
     // 1x1 conv = a plain GEMM over the NHWC pixel rows (ResNet bottlenecks):
     // tiled boxes for both operands, no im2col / band addressing
     const TgShape sh = tg_shape(M, O, K, ws_bytes);
@@ -945,65 +959,78 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
         op_tiled_k(b, wf, psw, O, K, K, sh.BN / sh.CL))
       return run_tgemm("conv_fwd[1x1]", sh, a, b, ep, M, O, K, ws, ws_bytes, st);
   }
-  if (s == 1) {
-    const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, k, p, ws,
+  if (s == 1 && sq) {
+    const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, kh, ph, ws,
                                  ws_bytes, st);
     if (rc >= 0) return rc;
   }
-  if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128 && -p >= -128) {
+  if (tma_on() && C8 % 32 == 0 && ph - (kh - 1) >= -128 && pw - (kw - 1) >= -128 && ph <= 128 &&
+      pw <= 128) {
     const TgShape sh = tg_shape(M, O, K, ws_bytes);
     TgOperand a, b;
-    if (op_im2col(a, false, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM * sh.MH) &&
+    if (op_im2col(a, false, x, psx, N, H, W, C8, kw, s, -pw, pw - (kw - 1), OH, OW,
+                  TG_BM * sh.MH, -ph, ph - (kh - 1)) &&
         op_tiled_k(b, wf, psw, O, K, K, sh.BN / sh.CL))
       return run_tgemm("conv_fwd[tma]", sh, a, b, ep, M, O, K, ws, ws_bytes, st);
   }
-  SvConvFwdA va = conv_fwd_A(x, psx, N, C8, H, W, k, s, p, OH, OW);
+  if (!sq) return fail(STZ_EINVAL, "conv_fwd: a %dx%d kernel needs the TMA path (C8 %% 32 == 0)",
+                       kh, kw);
+  SvConvFwdA va = conv_fwd_A(x, psx, N, C8, H, W, kh, s, ph, OH, OW);
   SvRowsK vb{wf, psw, O, K, K};
   return run_sgemm("conv_fwd", va, vb, ep, M, O, K, ws, ws_bytes, st);
 }
 
 template <class EP>
 int gemm_conv_dgrad(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, const EP& ep,
-                    int N, int C, int H, int W, int O8, int k, int s, int p, int OH, int OW,
-                    void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int M = N * H * W, K = k * k * O8;
-  if (k == 1 && s == 1 && p == 0 && tma_on() && O8 % 32 == 0) {   // 1x1: plain GEMM
-    const TgShape sh = tg_shape(M, C, K, ws_bytes);
+                    int N, int C, int H, int W, int O8, int kh, int kw, int s, int ph, int pw,
+                    int OH, int OW, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int M = N * H * W, K = kh * kw * O8;
+  const bool sq = square_kp(kh, kw, ph, pw);
+  if (kh == 1 && kw == 1 && s == 1 && ph == 0 && pw == 0 && tma_on() && O8 % 32 == 0) {
+    const TgShape sh = tg_shape(M, C, K, ws_bytes);   // 1x1: plain GEMM
     TgOperand a, b;
     if (op_tiled_k(a, g, psg, M, O8, O8, TG_BM * sh.MH) &&
         op_tiled_k(b, wd, psw, C, K, K, sh.BN / sh.CL))
       return run_tgemm("conv_dgrad[1x1]", sh, a, b, ep, M, C, K, ws, ws_bytes, st);
   }
-  if (s == 1) {   // the same stride-1 conv over dY padded by k-1-p, flipped weights
-    const int rc = run_band_conv("conv_dgrad[band]", g, psg, wd, psw, ep, N, O8, OH, OW, C, k,
-                                 k - 1 - p, ws, ws_bytes, st);
+  if (s == 1 && sq) {   // the same stride-1 conv over dY padded by k-1-p, flipped weights
+    const int rc = run_band_conv("conv_dgrad[band]", g, psg, wd, psw, ep, N, O8, OH, OW, C, kh,
+                                 kh - 1 - ph, ws, ws_bytes, st);
     if (rc >= 0) return rc;
   }
-  if (tma_on() && O8 % 32 == 0 && s == 1 && p - (k - 1) >= -128 && p <= 127) {
+  if (tma_on() && O8 % 32 == 0 && s == 1 && ph - (kh - 1) >= -128 && pw - (kw - 1) >= -128 &&
+      ph <= 127 && pw <= 127) {
     const TgShape sh = tg_shape(M, C, K, ws_bytes);
     TgOperand a, b;
-    if (op_im2col(a, false, g, psg, N, OH, OW, O8, k, 1, p - (k - 1), -p, H, W, TG_BM * sh.MH) &&
+    if (op_im2col(a, false, g, psg, N, OH, OW, O8, kw, 1, pw - (kw - 1), -pw, H, W,
+                  TG_BM * sh.MH, ph - (kh - 1), -ph) &&
         op_tiled_k(b, wd, psw, C, K, K, sh.BN / sh.CL))
       return run_tgemm("conv_dgrad[tma]", sh, a, b, ep, M, C, K, ws, ws_bytes, st);
   }
-  SvConvDgradA va = conv_dgrad_A(g, psg, N, H, W, O8, k, s, p, OH, OW);
+  if (!sq) return fail(STZ_EINVAL, "conv_dgrad: a %dx%d kernel needs the TMA path (stride 1, "
+                       "O8 %% 32 == 0)", kh, kw);
+  SvConvDgradA va = conv_dgrad_A(g, psg, N, H, W, O8, kh, s, ph, OH, OW);
   SvRowsK vb{wd, psw, C, K, K};
   return run_sgemm("conv_dgrad", va, vb, ep, M, C, K, ws, ws_bytes, st);
 }
 
 template <class EP>
 int gemm_conv_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg, const EP& ep, int N,
-                    int C8, int H, int W, int O, int O8, int k, int s, int p, int OH, int OW,
-                    void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int M = k * k * C8, P = N * OH * OW;
-  if (tma_on() && C8 % 32 == 0 && p - (k - 1) >= -128) {
+                    int C8, int H, int W, int O, int O8, int kh, int kw, int s, int ph, int pw,
+                    int OH, int OW, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int M = kh * kw * C8, P = N * OH * OW;
+  if (tma_on() && C8 % 32 == 0 && ph - (kh - 1) >= -128 && pw - (kw - 1) >= -128) {
     const TgShape sh = tg_shape(M, O, P, ws_bytes);
     TgOperand a, b;
-    if (op_im2col(a, true, x, psx, N, H, W, C8, k, s, -p, p - (k - 1), OH, OW, TG_BM * sh.MH) &&
+    if (op_im2col(a, true, x, psx, N, H, W, C8, kw, s, -pw, pw - (kw - 1), OH, OW,
+                  TG_BM * sh.MH, -ph, ph - (kh - 1)) &&
         op_tiled_mn(b, g, psg, O, P, O8, sh.BN / sh.CL))
       return run_tgemm("conv_wgrad[tma]", sh, a, b, ep, M, O, P, ws, ws_bytes, st);
   }
-  SvConvWgradA va = conv_wgrad_A(x, psx, N, C8, H, W, k, s, p, OH, OW);
+  if (!square_kp(kh, kw, ph, pw))
+    return fail(STZ_EINVAL, "conv_wgrad: a %dx%d kernel needs the TMA path (C8 %% 32 == 0)", kh,
+                kw);
+  SvConvWgradA va = conv_wgrad_A(x, psx, N, C8, H, W, kh, s, ph, OH, OW);
   SvRowsMN vb{g, psg, O, P, O8};
   return run_sgemm("conv_wgrad", va, vb, ep, M, O, P, ws, ws_bytes, st);
 }
@@ -1156,7 +1183,8 @@ int stz_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int
   if ((rc = check_launch("pack_conv_w"))) return rc;
   EpF32 e = ep_f32(y, N * OH * OW, O, OH * OW, (long long)O * OH * OW, 1, OH * OW, b, nullptr,
                    relu);
-  return gemm_conv_fwd(xp, psx, wf, psw, e, N, C8, H, W, O, k, s, p, OH, OW, cv.p, cv.left, st);
+  return gemm_conv_fwd(xp, psx, wf, psw, e, N, C8, H, W, O, k, k, s, p, p, OH, OW, cv.p, cv.left,
+                       st);
 }
 
 int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float* mask, int N,
@@ -1180,7 +1208,8 @@ int stz_conv2d_bwd_data(const float* gy, const float* w, float* gx, const float*
   pack_conv_w_kernel<<<grid_for(psw), 256, 0, st>>>(w, nullptr, 0, wd, psw, O, C, kk, 0, O8, k);
   if ((rc = check_launch("pack_conv_w"))) return rc;
   EpF32 e = ep_f32(gx, N * H * W, C, H * W, (long long)C * H * W, 1, H * W, nullptr, mask, 0);
-  return gemm_conv_dgrad(gp, psg, wd, psw, e, N, C, H, W, O8, k, s, p, OH, OW, cv.p, cv.left, st);
+  return gemm_conv_dgrad(gp, psg, wd, psw, e, N, C, H, W, O8, k, k, s, p, p, OH, OW, cv.p, cv.left,
+                         st);
 }
 
 int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb, int N, int C,
@@ -1204,7 +1233,8 @@ int stz_conv2d_bwd_filter(const float* x, const float* gy, float* gw, float* gb,
                                                       FastDiv(O8 / 8), FastDiv(OH * OW));
   if ((rc = check_launch("pack_nchw"))) return rc;
   EpConvWgrad e{gw, kk * C8, O, C, kk, FastDiv(C8)};
-  rc = gemm_conv_wgrad(xp, psx, gp, psg, e, N, C8, H, W, O, O8, k, s, p, OH, OW, cv.p, cv.left, st);
+  rc = gemm_conv_wgrad(xp, psx, gp, psg, e, N, C8, H, W, O, O8, k, k, s, p, p, OH, OW, cv.p,
+                       cv.left, st);
   if (rc || !gb) return rc;
   conv_bias_grad_kernel<<<O, 256, 0, st>>>(gy, gb, N, O, OH * OW);
   return check_launch("conv_bias_grad");
@@ -1373,32 +1403,47 @@ int stzx_unpack_rows(const void* xp, size_t ps, float* x, int M, int D, int D8, 
   return check_launch("unpack_rows");
 }
 
+int stzx_pack_conv2_w(const float* w, void* wf, size_t psf, void* wd, size_t psd, int O, int C,
+                      int kh, int kw, int C8, int O8, void* stream) {
+  const size_t kk = (size_t)kh * kw;
+  const size_t nf = wf ? (size_t)O * kk * C8 : 0, nd = wd ? (size_t)C * kk * O8 : 0;
+  if (nf + nd == 0) return STZ_OK;
+  // the kernel walks [nf | nd); a null target contributes an empty range.
+  // Flipping both tap axes of [kh][kw] is tap -> kk - 1 - tap.
+  pack_conv_w_kernel<<<grid_for(nf + nd), 256, 0, as_stream(stream)>>>(
+      w, mb(wf), psf, mb(wd), psd, O, C, (int)kk, wf ? C8 : 0, wd ? O8 : 0, kw);
+  return check_launch("pack_conv_w");
+}
+
 int stzx_pack_conv_w(const float* w, void* wf, size_t psf, void* wd, size_t psd, int O, int C,
                      int k, int C8, int O8, void* stream) {
-  const size_t nf = wf ? (size_t)O * k * k * C8 : 0, nd = wd ? (size_t)C * k * k * O8 : 0;
-  if (nf + nd == 0) return STZ_OK;
-  // the kernel walks [nf | nd); a null target contributes an empty range
-  pack_conv_w_kernel<<<grid_for(nf + nd), 256, 0, as_stream(stream)>>>(
-      w, mb(wf), psf, mb(wd), psd, O, C, k * k, wf ? C8 : 0, wd ? O8 : 0, k);
-  return check_launch("pack_conv_w");
+  return stzx_pack_conv2_w(w, wf, psf, wd, psd, O, C, k, k, C8, O8, stream);
+}
+
+int stzx_conv2_fwd(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
+                   void* y, size_t psy, int N, int C8, int H, int W, int O, int O8, int kh, int kw,
+                   int s, int ph, int pw, int relu, void* ws, size_t ws_bytes, void* stream) {
+  const int OH = (H + 2 * ph - kh) / s + 1, OW = (W + 2 * pw - kw) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8 || O8 < O) return fail(STZ_EINVAL, "conv_fwd: bad shape");
+  EpSplit e{mb(y), psy, N * OH * OW, O, O8, bias, nullptr, relu};
+  return gemm_conv_fwd(cb(x), psx, cb(wf), psw, e, N, C8, H, W, O, kh, kw, s, ph, pw, OH, OW, ws,
+                       ws_bytes, as_stream(stream));
 }
 
 int stzx_conv_fwd(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
                   void* y, size_t psy, int N, int C8, int H, int W, int O, int O8, int k, int s,
                   int p, int relu, void* ws, size_t ws_bytes, void* stream) {
-  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
-  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8 || O8 < O) return fail(STZ_EINVAL, "conv_fwd: bad shape");
-  EpSplit e{mb(y), psy, N * OH * OW, O, O8, bias, nullptr, relu};
-  return gemm_conv_fwd(cb(x), psx, cb(wf), psw, e, N, C8, H, W, O, k, s, p, OH, OW, ws, ws_bytes,
-                       as_stream(stream));
+  return stzx_conv2_fwd(x, psx, wf, psw, bias, y, psy, N, C8, H, W, O, O8, k, k, s, p, p, relu, ws,
+                        ws_bytes, stream);
 }
 
-int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
-                    const void* mask, int N, int C, int C8, int H, int W, int O8, int k, int s,
-                    int p, void* ws, size_t ws_bytes, void* stream) {
-  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
+int stzx_conv2_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
+                     const void* mask, int N, int C, int C8, int H, int W, int O8, int kh, int kw,
+                     int s, int ph, int pw, void* ws, size_t ws_bytes, void* stream) {
+  const int OH = (H + 2 * ph - kh) / s + 1, OW = (W + 2 * pw - kw) / s + 1;
   if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_dgrad: bad shape");
-  if (k == 1 && s > 1 && p == 0 && tma_on() && O8 % 32 == 0 && (size_t)N * H * W < (1u << 31)) {
+  if (kh == 1 && kw == 1 && s > 1 && ph == 0 && pw == 0 && tma_on() && O8 % 32 == 0 &&
+      (size_t)N * H * W < (1u << 31)) {
     // 1x1 stride-s (ResNet projection shortcut): input pixel (s*oh, s*ow)
     // receives g[oh, ow] . W and every other pixel 0 -- a plain GEMM over the
     // output rows whose epilogue scatters each row to its input pixel, after
@@ -1422,21 +1467,35 @@ int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void*
       return run_tgemm("conv_dgrad[1x1s]", sh, a, b, e, M, C, O8, ws, ws_bytes, st);
   }
   EpSplit e{mb(gx), psgx, N * H * W, C, C8, nullptr, cb(mask), 0};
-  return gemm_conv_dgrad(cb(g), psg, cb(wd), psw, e, N, C, H, W, O8, k, s, p, OH, OW, ws,
-                         ws_bytes, as_stream(stream));
+  return gemm_conv_dgrad(cb(g), psg, cb(wd), psw, e, N, C, H, W, O8, kh, kw, s, ph, pw, OH, OW,
+                         ws, ws_bytes, as_stream(stream));
+}
+
+int stzx_conv_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
+                    const void* mask, int N, int C, int C8, int H, int W, int O8, int k, int s,
+                    int p, void* ws, size_t ws_bytes, void* stream) {
+  return stzx_conv2_dgrad(g, psg, wd, psw, gx, psgx, mask, N, C, C8, H, W, O8, k, k, s, p, p, ws,
+                          ws_bytes, stream);
+}
+
+int stzx_conv2_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
+                     int accumulate, int N, int C, int C8, int H, int W, int O, int O8, int kh,
+                     int kw, int s, int ph, int pw, void* ws, size_t ws_bytes, void* stream) {
+  const int OH = (H + 2 * ph - kh) / s + 1, OW = (W + 2 * pw - kw) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad: bad shape");
+  cudaStream_t st = as_stream(stream);
+  EpConvWgrad e{gw, kh * kw * C8, O, C, kh * kw, FastDiv(C8), accumulate ? 1 : 0};
+  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, C8, H, W, O, O8, kh, kw, s, ph, pw, OH,
+                           OW, ws, ws_bytes, st);
+  if (rc || !gb) return rc;
+  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);
 }
 
 int stzx_conv_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
                     int accumulate, int N, int C, int C8, int H, int W, int O, int O8, int k,
                     int s, int p, void* ws, size_t ws_bytes, void* stream) {
-  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
-  if (OH <= 0 || OW <= 0 || C8 % 8 || O8 % 8) return fail(STZ_EINVAL, "conv_wgrad: bad shape");
-  cudaStream_t st = as_stream(stream);
-  EpConvWgrad e{gw, k * k * C8, O, C, k * k, FastDiv(C8), accumulate ? 1 : 0};
-  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, C8, H, W, O, O8, k, s, p, OH, OW, ws,
-                           ws_bytes, st);
-  if (rc || !gb) return rc;
-  return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);
+  return stzx_conv2_wgrad(x, psx, g, psg, gw, gb, accumulate, N, C, C8, H, W, O, O8, k, k, s, p,
+                          p, ws, ws_bytes, stream);
 }
 
 int stzx_fc_fwd(const void* x, size_t psx, const void* w, size_t psw, const float* bias, void* y,
@@ -1635,6 +1694,38 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
   return check_launch("bn_bwd");
 }
 
+int stzx_avgpool_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int C8, int H,
+                     int W, int k, int s, int p, void* stream) {
+  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || k < 1 || s < 1 || p < 0 || 2 * p > k)
+    return fail(STZ_EINVAL, "avgpool_fwd: k %d s %d p %d on %dx%d", k, s, p, H, W);
+  avgpool_fwd_kernel<<<grid_for((size_t)N * OH * OW * (C8 / 8)), 256, 0, as_stream(stream)>>>(
+      cb(x), psx, mb(y), psy, N, H, W, C8, OH, OW, k, s, p);
+  return check_launch("avgpool_fwd");
+}
+
+int stzx_avgpool_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int C8, int H, int W,
+                     int k, int s, int p, void* stream) {
+  const int OH = (H + 2 * p - k) / s + 1, OW = (W + 2 * p - k) / s + 1;
+  if (OH <= 0 || OW <= 0 || C8 % 8 || k < 1 || s < 1 || p < 0 || 2 * p > k)
+    return fail(STZ_EINVAL, "avgpool_bwd: k %d s %d p %d on %dx%d", k, s, p, H, W);
+  avgpool_bwd_kernel<<<grid_for((size_t)N * H * W * (C8 / 8)), 256, 0, as_stream(stream)>>>(
+      cb(gy), psg, mb(gx), psx, N, H, W, C8, OH, OW, k, s, p);
+  return check_launch("avgpool_bwd");
+}
+
+int stzx_copy_channels(const void* src, size_t pss, int src8, int s0, void* dst, size_t psd,
+                       int dst8, int d0, size_t rows, int C, void* stream) {
+  if (C % 8 || s0 % 8 || d0 % 8 || src8 % 8 || dst8 % 8 || s0 + C > src8 || d0 + C > dst8 ||
+      !aligned16(src) || !aligned16(dst) || pss % 8 || psd % 8)
+    return fail(STZ_EINVAL, "copy_channels: C %d from %d/%d to %d/%d (multiples of 8)", C, s0,
+                src8, d0, dst8);
+  if (rows == 0 || C == 0) return STZ_OK;
+  copy_channels_kernel<<<grid_for(rows * (C / 8)), 256, 0, as_stream(stream)>>>(
+      cb(src), pss, src8, s0, mb(dst), psd, dst8, d0, rows, C);
+  return check_launch("copy_channels");
+}
+
 int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, int C8,
                  void* stream) {
   if (N <= 0 || HW <= 0 || C8 <= 0 || C8 % 8) return fail(STZ_EINVAL, "gap_fwd: bad shape");
@@ -1716,7 +1807,7 @@ int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, fl
   cudaStream_t st = as_stream(stream);
   EpConvWgradS2D e{gw, ks * ks * Cs8, O, C, k, s, ks, C * s * s, FastDiv(Cs8),
                    accumulate ? 1 : 0};
-  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, Cs8, Hs, Ws, O, O8, ks, 1, 0, OH, OW, ws,
+  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, Cs8, Hs, Ws, O, O8, ks, ks, 1, 0, 0, OH, OW, ws,
                            ws_bytes, st);
   if (rc || !gb) return rc;
   return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);

@@ -305,4 +305,104 @@ __global__ void add_split_kernel(const bf16_t* __restrict__ a, size_t psa,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Inception-V3 kinds (§8f row 4; semantics oracle/stanza_oracle.py
+// avgpool_forward / avgpool_backward / "concat")
+// ---------------------------------------------------------------------------
+
+// AvgPool2d forward, NHWC split planes, 8 channels per thread: float64 sum of
+// the window taps in (kh, kw) order (padding contributes nothing), divided by
+// k*k, one fp32 rounding
+__global__ void __launch_bounds__(256) avgpool_fwd_kernel(const bf16_t* __restrict__ x, size_t psx,
+                                                          bf16_t* __restrict__ y, size_t psy,
+                                                          int N, int H, int W, int C8, int OH,
+                                                          int OW, int k, int s, int p) {
+  const int nch = C8 / 8;
+  const double kk = (double)(k * k);
+  STZ_GRID_LOOP(i, (size_t)N * OH * OW * nch) {
+    const int cc = (int)(i % nch);
+    const size_t pix = i / nch;
+    const int ow = (int)(pix % OW), oh = (int)((pix / OW) % OH);
+    const size_t n = pix / ((size_t)OW * OH);
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (int kh = 0; kh < k; ++kh) {
+      const int h = oh * s + kh - p;
+      if (h < 0 || h >= H) continue;
+      for (int kw = 0; kw < k; ++kw) {
+        const int w = ow * s + kw - p;
+        if (w < 0 || w >= W) continue;
+        float v[8];
+        load_split8(x + ((n * H + h) * W + w) * C8 + (size_t)cc * 8, psx, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += (double)v[j];
+      }
+    }
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (float)__ddiv_rn(acc[j], kk);
+    store_split8(y + pix * C8 + (size_t)cc * 8, psy, o);
+  }
+}
+
+// AvgPool2d backward (gather form): input cell (h, w) sums g[oh, ow] / (k*k)
+// (float64 quotient per term) over the windows covering it, in (kh, kw) order
+__global__ void __launch_bounds__(256) avgpool_bwd_kernel(const bf16_t* __restrict__ gy, size_t psg,
+                                                          bf16_t* __restrict__ gx, size_t psx,
+                                                          int N, int H, int W, int C8, int OH,
+                                                          int OW, int k, int s, int p) {
+  const int nch = C8 / 8;
+  const double kk = (double)(k * k);
+  STZ_GRID_LOOP(i, (size_t)N * H * W * nch) {
+    const int cc = (int)(i % nch);
+    const size_t pix = i / nch;
+    const int w = (int)(pix % W), h = (int)((pix / W) % H);
+    const size_t n = pix / ((size_t)W * H);
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (int kh = 0; kh < k; ++kh) {
+      const int th = h + p - kh;
+      if (th < 0 || th % s) continue;
+      const int oh = th / s;
+      if (oh >= OH) continue;
+      for (int kw = 0; kw < k; ++kw) {
+        const int tw = w + p - kw;
+        if (tw < 0 || tw % s) continue;
+        const int ow = tw / s;
+        if (ow >= OW) continue;
+        float v[8];
+        load_split8(gy + ((n * OH + oh) * OW + ow) * C8 + (size_t)cc * 8, psg, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __ddiv_rn((double)v[j], kk);
+      }
+    }
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (float)acc[j];
+    store_split8(gx + pix * C8 + (size_t)cc * 8, psx, o);
+  }
+}
+
+// channel-slice copy of split-plane rows: dst[r][d0 + c] = src[r][s0 + c] for
+// c < C (C, s0, d0, both row pitches multiples of 8): the Inception concat
+// (branch output -> its channel slice) and its backward (slice -> branch)
+__global__ void __launch_bounds__(256) copy_channels_kernel(const bf16_t* __restrict__ src,
+                                                            size_t pss, int src8, int s0,
+                                                            bf16_t* __restrict__ dst, size_t psd,
+                                                            int dst8, int d0, size_t R, int C) {
+  const int nch = C / 8;
+  STZ_GRID_LOOP(i, R * nch) {
+    const size_t r = i / nch;
+    const int cc = (int)(i % nch) * 8;
+    const bf16_t* a = src + r * src8 + s0 + cc;
+    bf16_t* b = dst + r * dst8 + d0 + cc;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      *reinterpret_cast<uint4*>(b + q * psd) = __ldg(reinterpret_cast<const uint4*>(a + q * pss));
+  }
+}
+
 }  // namespace stz

@@ -39,8 +39,9 @@ struct alignas(64) TgOperand {
   int box_rows;        // TILED_K: rows per box (a B tile split between 2 CTAs)
   int mn3d;            // TILED_MN: the tile is one 3D box (rows % 32 == 0)
   int sw128;           // IM2COL_MN: 64-channel boxes with the 128-byte swizzle (C8 % 64 == 0)
-  // im2col geometry: output pixel (n, oh, ow) -> window start (oh*s + lo, ow*s + lo)
-  int lo, s, C8, ksz, flip;
+  // im2col geometry: output pixel (n, oh, ow) -> window start (oh*s + lo_h, ow*s + lo);
+  // taps (th, tw) = divmod(tap, ksz) with ksz = the kernel width
+  int lo, s, C8, ksz, flip, lo_h;
   FastDiv d_ohw, d_ow, d_c8, d_k;
 };
 
@@ -251,7 +252,7 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
       op.d_c8.divmod((uint32_t)k0, tap, c0);
       op.d_k.divmod(tap, th, tw);
       tma_im2col_4d<CL>(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo,
-                        (int)(oh * op.s) + op.lo, (int)n, (uint16_t)tw, (uint16_t)th);
+                        (int)(oh * op.s) + op.lo_h, (int)n, (uint16_t)tw, (uint16_t)th);
       break;
     }
     default: {  // TG_IM2COL_MN: k0 = first output pixel, rows = (tap, c)
@@ -261,7 +262,7 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
       op.d_c8.divmod((uint32_t)(r0 + (op.sw128 ? 64 : 32) * box), tap, c0);
       op.d_k.divmod(tap, th, tw);
       tma_im2col_4d<CL>(map, dst, bar, (int)c0, (int)(ow * op.s) + op.lo,
-                        (int)(oh * op.s) + op.lo, (int)n, (uint16_t)tw, (uint16_t)th);
+                        (int)(oh * op.s) + op.lo_h, (int)n, (uint16_t)tw, (uint16_t)th);
     }
   }
 }

@@ -37,9 +37,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .tensor_core import (BatchNorm2d, Conv2d, Flatten, FullyConnected, GlobalAvgPool2d,
-                          MaxPool2d, ReLU, Residual, ShapeMismatch, SoftmaxCrossEntropy,
-                          inv_batch, out_shape, param_shapes, ptr, stream_of, workspace)
+from .tensor_core import (AvgPool2d, BatchNorm2d, Concat, Conv2d, Flatten, FullyConnected,
+                          GlobalAvgPool2d, MaxPool2d, ReLU, Residual, ShapeMismatch,
+                          SoftmaxCrossEntropy, inv_batch, out_shape, param_shapes, ptr, stream_of,
+                          workspace)
 
 _ALIGN = 4  # floats: keeps every fp32 per-tensor view 16-byte aligned
 
@@ -98,7 +99,8 @@ class Split:
 
 @dataclass
 class _Op:
-    kind: str                 # conv | fc | maxpool | relu | flatten | softmax_ce | bn | gap | residual
+    kind: str                 # conv | fc | maxpool | relu | flatten | softmax_ce | bn | gap |
+    #                           residual | avgpool | concat
     layer: object
     index: int
     in_shape: tuple           # per-sample logical shape
@@ -164,7 +166,8 @@ class BlockEngine:
         for i, layer in enumerate(self.layers):
             kind = {Conv2d: "conv", FullyConnected: "fc", MaxPool2d: "maxpool", ReLU: "relu",
                     Flatten: "flatten", SoftmaxCrossEntropy: "softmax_ce", BatchNorm2d: "bn",
-                    GlobalAvgPool2d: "gap", Residual: "residual"}[type(layer)]
+                    GlobalAvgPool2d: "gap", Residual: "residual", AvgPool2d: "avgpool",
+                    Concat: "concat"}[type(layer)]
             nxt = out_shape(layer, shape)
             ops.append(_Op(kind, layer, i, shape, nxt))
             shape = nxt
@@ -189,7 +192,7 @@ class BlockEngine:
             # stride-1 conv over space-to-depth blocks: TMA-eligible channels
             l0 = ops[0].layer
             if ops[0].kind == "conv" and l0.stride > 1 and rup8(l0.in_ch) < 32 \
-                    and l0.in_ch * l0.stride ** 2 <= 256:
+                    and l0.in_ch * l0.stride ** 2 <= 256 and l0.square:
                 ks = -(-l0.kernel // l0.stride)
                 cs8 = -(-(l0.in_ch * l0.stride ** 2) // 32) * 32
                 _, oh, ow = ops[0].out_shape
@@ -212,10 +215,28 @@ class BlockEngine:
         return [[flat[o:o + n].view(shp) for (o, shp, n) in row] for row in self.slots]
 
     def _make_children(self):
-        """Body / shortcut engines of each Residual op, their parameters views
-        of this engine's flat vectors at the residual row's offset."""
+        """Body / shortcut engines of each Residual op and branch engines of
+        each Concat op, their parameters views of this engine's flat vectors
+        at the op's row offset."""
         flats = (self.params_flat, self.vel_flat, self.grad_flat)
         for i, op in enumerate(self.ops):
+            if op.kind == "concat":
+                base = self.slots[i][0][0] if self.slots[i] else 0
+                kids = []
+                for bi, br in enumerate(op.layer.branches):
+                    shp = op.in_shape
+                    for l in br:
+                        shp = out_shape(l, shp)
+                    if shp[0] % 8:
+                        raise ShapeMismatch(f"Concat branch {bi} gives {shp[0]} channels: "
+                                            "branch widths must be multiples of 8")
+                    eng = BlockEngine(br, op.in_shape, self.batch, self.device,
+                                      need_input_grad=True, group=self.group, flats=(base, flats),
+                                      tag=f"{self.tag}c{i}b{bi}.")
+                    base += eng.total if eng.param_count else 0
+                    kids.append(eng)
+                self.children[i] = tuple(kids)
+                continue
             if op.kind != "residual":
                 continue
             base = self.slots[i][0][0] if self.slots[i] else 0
@@ -240,6 +261,8 @@ class BlockEngine:
                     return True
                 if isinstance(l, Residual) and walk(l.body + l.shortcut):
                     return True
+                if isinstance(l, Concat) and any(walk(br) for br in l.branches):
+                    return True
             return False
         return walk(self.layers)
 
@@ -249,7 +272,7 @@ class BlockEngine:
         for i, op in enumerate(self.ops):
             l = op.layer
             if op.kind == "conv":
-                kk, c8, o8 = l.kernel * l.kernel, rup8(l.in_ch), rup8(l.out_ch)
+                kk, c8, o8 = l.kh * l.kw, rup8(l.in_ch), rup8(l.out_ch)
                 if op.s2d is not None:
                     ks, cs8, _, _ = op.s2d
                     kk, c8 = ks * ks, cs8
@@ -332,6 +355,11 @@ class BlockEngine:
                     self.gin[0] = input_grad_buffer
                     continue
             self.gin[i] = self._split_for(op.in_shape, b)
+        self._concat_gy: dict = {}        # concat op -> per-branch output-gradient buffers
+        for i, op in enumerate(self.ops):
+            if op.kind == "concat":
+                self._concat_gy[i] = [self._split_for(kid.out_shape, b)
+                                      for kid in self.children[i]]
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
 
     # -- parameters ------------------------------------------------------------------
@@ -359,9 +387,11 @@ class BlockEngine:
                 _lib.call("stzx_pack_conv_w_s2d", ptr(w), ptr(a), a[0].numel(), l.out_ch,
                           l.in_ch, l.kernel, l.stride, op.s2d[1], st)
             elif op.kind == "conv":
-                _lib.call("stzx_pack_conv_w", ptr(w), ptr(a), a[0].numel(), ptr(b),
-                          0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kernel,
-                          rup8(l.in_ch), rup8(l.out_ch), st)
+                _lib.call("stzx_pack_conv2_w", ptr(w), ptr(a), a[0].numel(), ptr(b),
+                          0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kh, l.kw,
+                          rup8(l.in_ch), rup8(l.out_ch), st, tag=f"{self.tag}pack_conv_w",
+                          nbytes=4.0 * w.numel() + 6.0 * (a[0].numel() + (0 if b is None
+                                                                           else b[0].numel())))
             else:
                 _lib.call("stzx_pack_rows", ptr(w), ptr(a), a[0].numel(), l.in_dim, l.out_dim,
                           rup8(l.out_dim), st)
@@ -387,7 +417,7 @@ class BlockEngine:
         b = self.batch if rows is None else rows
         if op.kind == "conv":
             _, oh, ow = op.out_shape
-            return 2.0 * b * oh * ow * l.out_ch * l.in_ch * l.kernel * l.kernel
+            return 2.0 * b * oh * ow * l.out_ch * l.in_ch * l.kh * l.kw
         if op.kind == "fc":
             return 2.0 * b * l.in_dim * l.out_dim
         return 0.0
@@ -481,13 +511,13 @@ class BlockEngine:
                 c, h, w = op.in_shape
                 y = V(self.acts[i])
                 wf, _ = self.wplanes[i]
-                k, cs, pd = l.kernel, l.stride, l.padding
+                kh, kw, cs, ph, pw = l.kh, l.kw, l.stride, l.ph, l.pw
                 if op.s2d is not None:             # stride-1 conv over s2d blocks
-                    k, _, h, w = op.s2d
-                    cs, pd = 1, 0
-                _lib.call("stzx_conv_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
+                    kh, _, h, w = op.s2d
+                    kw, cs, ph, pw = kh, 1, 0, 0
+                _lib.call("stzx_conv2_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
                           ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w, l.out_ch,
-                          y.width, k, cs, pd, int(op.fused_relu), ptr(ws),
+                          y.width, kh, kw, cs, ph, pw, int(op.fused_relu), ptr(ws),
                           ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_fwd")
             elif op.kind == "fc":
                 wp, _ = self.wplanes[i]
@@ -539,6 +569,27 @@ class BlockEngine:
                 y = V(self.acts[i])
                 _lib.call("stzx_gap_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, b, h * w, xin.width, st,
                           tag=f"{self.tag}gap{i}_fwd", nbytes=6.0 * b * (xin.row_elems + y.width))
+            elif op.kind == "avgpool":
+                c, h, w = op.in_shape
+                y = V(self.acts[i])
+                _lib.call("stzx_avgpool_fwd", xin.ptr(), xin.ps, y.ptr(), y.ps, b, xin.width, h, w,
+                          l.kernel, l.stride, l.padding, st, tag=f"{self.tag}avgpool{i}_fwd",
+                          nbytes=6.0 * b * (xin.row_elems + y.row_elems))
+            elif op.kind == "concat":
+                # every branch on the same input; each branch's output is copied
+                # into its channel slice of the concatenated tensor
+                x_full = self._input(i)
+                y = V(self.acts[i])
+                _, oh, ow = op.out_shape
+                c0 = 0
+                for kid in self.children[i]:
+                    kid.forward(x_full, rows=rows)
+                    out = V(kid._act(len(kid.ops) - 1))
+                    cb = kid.out_shape[0]
+                    _lib.call("stzx_copy_channels", out.ptr(), out.ps, out.width, 0, y.ptr(), y.ps,
+                              y.width, c0, b * oh * ow, cb, st, tag=f"{self.tag}concat{i}_fwd",
+                              nbytes=12.0 * b * oh * ow * cb)
+                    c0 += cb
             elif op.kind == "residual":
                 body, short = self.children[i]
                 x_full = self._input(i)
@@ -595,7 +646,7 @@ class BlockEngine:
             for i, op in enumerate(self.ops):
                 if op.kind in ("conv", "fc"):
                     self._wgrad(i, V(self._input(i)), V(self._gout[i]), b, acc, ws, st)
-                elif op.kind == "residual":
+                elif op.kind in ("residual", "concat"):
                     for k in self.children[i]:
                         if k is not None:
                             k.backward(rows=rows, accumulate=accumulate, phase="wgrad")
@@ -650,6 +701,35 @@ class BlockEngine:
                 _lib.call("stzx_gap_bwd", g.ptr(), g.ps, out.ptr(), out.ps, b, h * w, out.width,
                           st, tag=f"{self.tag}gap{i}_bwd", nbytes=6.0 * b * (out.row_elems + g.width))
                 g_full = self.gin[i]
+            elif op.kind == "avgpool":
+                c, h, w = op.in_shape
+                out = V(self.gin[i])
+                _lib.call("stzx_avgpool_bwd", g.ptr(), g.ps, out.ptr(), out.ps, b, out.width, h, w,
+                          l.kernel, l.stride, l.padding, st, tag=f"{self.tag}avgpool{i}_bwd",
+                          nbytes=6.0 * b * (out.row_elems + g.row_elems))
+                g_full = self.gin[i]
+            elif op.kind == "concat":
+                # each branch's channel slice of the gradient into its own
+                # buffer, the branch backward, then the fp32 left fold of the
+                # branches' input gradients in branch order
+                _, oh, ow = op.out_shape
+                c0, gxs = 0, []
+                for kid, gyb in zip(self.children[i], self._concat_gy[i]):
+                    cb = kid.out_shape[0]
+                    gv = V(gyb)
+                    _lib.call("stzx_copy_channels", g.ptr(), g.ps, g.width, c0, gv.ptr(), gv.ps,
+                              gv.width, 0, b * oh * ow, cb, st, tag=f"{self.tag}concat{i}_bwd",
+                              nbytes=12.0 * b * oh * ow * cb)
+                    gxs.append(kid.backward(gyb, rows=rows, accumulate=accumulate, phase=phase))
+                    c0 += cb
+                out = V(self.gin[i])
+                acc = gxs[0]
+                for gx in gxs[1:]:
+                    _lib.call("stzx_add", acc.ptr(), acc.ps, gx.ptr(), gx.ps, None, out.ptr(),
+                              out.ps, b * out.row_elems, st, tag=f"{self.tag}concat{i}_add",
+                              nbytes=18.0 * b * out.row_elems)
+                    acc = out
+                g_full = self.gin[i]
             elif op.kind == "residual":
                 # the block's final ReLU mask (its output z > 0) is applied by
                 # the consumers of the incoming gradient: the body's and the
@@ -693,9 +773,9 @@ class BlockEngine:
                 if op.kind == "conv":
                     c, h, w = op.in_shape
                     _, wd = self.wplanes[i]
-                    _lib.call("stzx_conv_dgrad", g.ptr(), g.ps, ptr(wd), wd[0].numel(),
-                              out.ptr(), out.ps, mptr, b, c, out.width, h, w, g.width, l.kernel,
-                              l.stride, l.padding, ptr(ws), ws.numel(), st,
+                    _lib.call("stzx_conv2_dgrad", g.ptr(), g.ps, ptr(wd), wd[0].numel(),
+                              out.ptr(), out.ps, mptr, b, c, out.width, h, w, g.width, l.kh, l.kw,
+                              l.stride, l.ph, l.pw, ptr(ws), ws.numel(), st,
                               flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_dgrad")
                 else:
                     wp, _ = self.wplanes[i]
@@ -727,9 +807,9 @@ class BlockEngine:
                       flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         elif op.kind == "conv":
             c, h, w = op.in_shape
-            _lib.call("stzx_conv_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
+            _lib.call("stzx_conv2_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
                       ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, c, xin.width, h,
-                      w, l.out_ch, g.width, l.kernel, l.stride, l.padding, ptr(ws),
+                      w, l.out_ch, g.width, l.kh, l.kw, l.stride, l.ph, l.pw, ptr(ws),
                       ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         else:
             _lib.call("stzx_fc_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,

@@ -42,6 +42,30 @@ class Conv2d:
     kernel: int
     stride: int = 1
     padding: int = 0
+    # Inception-V3 kinds (§8f row 4, not in the reference): an asymmetric
+    # kernel kernel x kernel_w with padding (padding, padding_w); None = square
+    kernel_w: int | None = None
+    padding_w: int | None = None
+
+    @property
+    def kh(self) -> int:
+        return self.kernel
+
+    @property
+    def kw(self) -> int:
+        return self.kernel if self.kernel_w is None else self.kernel_w
+
+    @property
+    def ph(self) -> int:
+        return self.padding
+
+    @property
+    def pw(self) -> int:
+        return self.padding if self.padding_w is None else self.padding_w
+
+    @property
+    def square(self) -> bool:
+        return self.kh == self.kw and self.ph == self.pw
 
 
 @dataclass(frozen=True)
@@ -97,12 +121,31 @@ class Residual:
     shortcut: tuple = ()
 
 
+# -- Inception-V3 kinds (§8f row 4; semantics in oracle/stanza_oracle.py
+# avgpool_* / "concat", parity unpinned like the ResNet kinds)
+
+@dataclass(frozen=True)
+class AvgPool2d:
+    """Zero-padded average pool; every window is divided by kernel^2."""
+    kernel: int
+    stride: int
+    padding: int = 0
+
+
+@dataclass(frozen=True)
+class Concat:
+    """Branches applied to the same input, outputs concatenated along
+    channels in branch order (an Inception module).  Its parameter row is
+    every branch's tensors in order."""
+    branches: tuple
+
+
 LayerKind = Union[Conv2d, MaxPool2d, Flatten, FullyConnected, ReLU, SoftmaxCrossEntropy,
-                  BatchNorm2d, GlobalAvgPool2d, Residual]
+                  BatchNorm2d, GlobalAvgPool2d, Residual, AvgPool2d, Concat]
 
 
 def has_params(layer) -> bool:
-    if isinstance(layer, Residual):
+    if isinstance(layer, (Residual, Concat)):
         return bool(param_shapes(layer))
     return isinstance(layer, (Conv2d, FullyConnected, BatchNorm2d))
 
@@ -111,13 +154,15 @@ def param_shapes(layer) -> list[tuple[int, ...]]:
     """Weight then bias: conv [O,C,k,k]+[O], FC [in,out]+[out] (tensor_core.py:81-88);
     BatchNorm gamma+beta [C]; a residual block its sub-layers' in order."""
     if isinstance(layer, Conv2d):
-        return [(layer.out_ch, layer.in_ch, layer.kernel, layer.kernel), (layer.out_ch,)]
+        return [(layer.out_ch, layer.in_ch, layer.kh, layer.kw), (layer.out_ch,)]
     if isinstance(layer, FullyConnected):
         return [(layer.in_dim, layer.out_dim), (layer.out_dim,)]
     if isinstance(layer, BatchNorm2d):
         return [(layer.channels,), (layer.channels,)]
     if isinstance(layer, Residual):
         return [s for l in layer.body + layer.shortcut for s in param_shapes(l)]
+    if isinstance(layer, Concat):
+        return [s for br in layer.branches for l in br for s in param_shapes(l)]
     return []
 
 
@@ -127,7 +172,7 @@ def param_count(layer) -> int:
 
 def fan_in(layer) -> int:
     if isinstance(layer, Conv2d):
-        return layer.in_ch * layer.kernel * layer.kernel
+        return layer.in_ch * layer.kh * layer.kw
     if isinstance(layer, FullyConnected):
         return layer.in_dim
     raise ValueError(f"{layer!r} has no parameters")
@@ -140,10 +185,10 @@ def out_shape(layer, in_shape: tuple[int, ...]) -> tuple[int, ...]:
     if isinstance(layer, Conv2d):
         if len(in_shape) != 3 or in_shape[0] != layer.in_ch:
             raise ShapeMismatch(f"Conv2d expects ({layer.in_ch}, H, W), got {in_shape}")
-        oh = (in_shape[1] + 2 * layer.padding - layer.kernel) // layer.stride + 1
-        ow = (in_shape[2] + 2 * layer.padding - layer.kernel) // layer.stride + 1
+        oh = (in_shape[1] + 2 * layer.ph - layer.kh) // layer.stride + 1
+        ow = (in_shape[2] + 2 * layer.pw - layer.kw) // layer.stride + 1
         if oh <= 0 or ow <= 0:
-            raise ShapeMismatch(f"Conv2d kernel {layer.kernel} too large for {in_shape}")
+            raise ShapeMismatch(f"Conv2d kernel {layer.kh}x{layer.kw} too large for {in_shape}")
         return (layer.out_ch, oh, ow)
     if isinstance(layer, MaxPool2d):
         if len(in_shape) != 3:
@@ -153,6 +198,29 @@ def out_shape(layer, in_shape: tuple[int, ...]) -> tuple[int, ...]:
         if oh <= 0 or ow <= 0:
             raise ShapeMismatch(f"MaxPool2d kernel {layer.kernel} too large for {in_shape}")
         return (in_shape[0], oh, ow)
+    if isinstance(layer, AvgPool2d):
+        if len(in_shape) != 3:
+            raise ShapeMismatch(f"AvgPool2d expects (C, H, W), got {in_shape}")
+        oh = (in_shape[1] + 2 * layer.padding - layer.kernel) // layer.stride + 1
+        ow = (in_shape[2] + 2 * layer.padding - layer.kernel) // layer.stride + 1
+        if oh <= 0 or ow <= 0 or layer.padding * 2 > layer.kernel:
+            raise ShapeMismatch(f"AvgPool2d kernel {layer.kernel} pad {layer.padding} does "
+                                f"not fit {in_shape}")
+        return (in_shape[0], oh, ow)
+    if isinstance(layer, Concat):
+        if not layer.branches or any(not br for br in layer.branches):
+            raise ShapeMismatch("Concat needs non-empty branches")
+        outs = []
+        for br in layer.branches:
+            shape = in_shape
+            for l in br:
+                shape = out_shape(l, shape)
+            if len(shape) != 3:
+                raise ShapeMismatch(f"Concat branch ends in {shape}, expected (C, H, W)")
+            outs.append(shape)
+        if len({o[1:] for o in outs}) != 1:
+            raise ShapeMismatch(f"Concat branches disagree on H, W: {outs}")
+        return (sum(o[0] for o in outs), outs[0][1], outs[0][2])
     if isinstance(layer, Flatten):
         return (int(np.prod(in_shape)),)
     if isinstance(layer, FullyConnected):
@@ -191,6 +259,9 @@ def out_shape(layer, in_shape: tuple[int, ...]) -> tuple[int, ...]:
 def as_tuple(layer) -> tuple:
     """Plain-tuple form of a layer (the oracle's and the tests' vocabulary)."""
     if isinstance(layer, Conv2d):
+        if not layer.square:
+            return ("conv", layer.in_ch, layer.out_ch, (layer.kh, layer.kw), layer.stride,
+                    (layer.ph, layer.pw))
         return ("conv", layer.in_ch, layer.out_ch, layer.kernel, layer.stride, layer.padding)
     if isinstance(layer, MaxPool2d):
         return ("maxpool", layer.kernel, layer.stride)
@@ -209,6 +280,10 @@ def as_tuple(layer) -> tuple:
     if isinstance(layer, Residual):
         return ("residual", tuple(as_tuple(l) for l in layer.body),
                 tuple(as_tuple(l) for l in layer.shortcut))
+    if isinstance(layer, AvgPool2d):
+        return ("avgpool", layer.kernel, layer.stride, layer.padding)
+    if isinstance(layer, Concat):
+        return ("concat", tuple(tuple(as_tuple(l) for l in br) for br in layer.branches))
     raise TypeError(f"unknown layer kind {layer!r}")
 
 
@@ -398,6 +473,8 @@ def _init_layer(gen, layer) -> list[np.ndarray]:
         return [np.ones(layer.channels, FLOAT), np.zeros(layer.channels, FLOAT)]
     if isinstance(layer, Residual):
         return [t for l in layer.body + layer.shortcut for t in _init_layer(gen, l)]
+    if isinstance(layer, Concat):
+        return [t for br in layer.branches for l in br for t in _init_layer(gen, l)]
     bound = float(np.sqrt(1.0 / fan_in(layer))) if has_params(layer) else 0.0
     return [gen.uniform(-bound, bound, size=s).astype(FLOAT) for s in param_shapes(layer)]
 

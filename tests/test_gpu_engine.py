@@ -21,17 +21,20 @@ TOL = 3e-6
 def _longest_contraction(layers, in_shape, batch):
     """Largest K over the stack's forward, input-gradient and weight-gradient
     GEMMs."""
-    from paper_1812_10624_b200.tensor_core import Conv2d, FullyConnected, Residual, out_shape
+    from paper_1812_10624_b200.tensor_core import (Concat, Conv2d, FullyConnected, Residual,
+                                                    out_shape)
     shape, kmax = tuple(in_shape), 1
     for l in layers:
         nxt = out_shape(l, shape)
         if isinstance(l, Residual):
             kmax = max(kmax, _longest_contraction(l.body, shape, batch),
                        _longest_contraction(l.shortcut, shape, batch))
+        elif isinstance(l, Concat):
+            kmax = max([kmax] + [_longest_contraction(br, shape, batch) for br in l.branches])
         elif isinstance(l, FullyConnected):
             kmax = max(kmax, l.in_dim, l.out_dim, batch)
         elif isinstance(l, Conv2d):
-            kk = l.kernel * l.kernel
+            kk = l.kh * l.kw
             kmax = max(kmax, l.in_ch * kk, l.out_ch * kk, batch * nxt[1] * nxt[2])
         shape = nxt
     return kmax
@@ -70,12 +73,17 @@ def _oracle_forward_tie_aware(tl, params, x, dev_pos):
 def _bn_fed_biases(layers):
     """(layer, tensor) positions of conv biases that feed a BatchNorm, inside
     residual rows too (tensor index within the row)."""
-    from paper_1812_10624_b200.tensor_core import BatchNorm2d, Conv2d, Residual, param_shapes
+    from paper_1812_10624_b200.tensor_core import (BatchNorm2d, Concat, Conv2d, Residual,
+                                                    param_shapes)
     out = set()
 
     def scan(seq, li, t0):
         t = t0
         for j, l in enumerate(seq):
+            if isinstance(l, Concat):
+                for br in l.branches:
+                    t = scan(br, li, t)
+                continue
             if isinstance(l, Conv2d) and j + 1 < len(seq) and isinstance(seq[j + 1], BatchNorm2d):
                 out.add((li, t + 1))
             t += len(param_shapes(l))
@@ -83,6 +91,10 @@ def _bn_fed_biases(layers):
     for li, l in enumerate(layers):
         if isinstance(l, Residual):
             scan(l.shortcut, li, scan(l.body, li, 0))
+        elif isinstance(l, Concat):
+            t = 0
+            for br in l.branches:
+                t = scan(br, li, t)
         elif isinstance(l, Conv2d) and li + 1 < len(layers) and \
                 isinstance(layers[li + 1], BatchNorm2d):
             out.add((li, 1))
@@ -91,10 +103,11 @@ def _bn_fed_biases(layers):
 
 def _run(layers, in_shape, batch, need_input_grad, seed):
     from paper_1812_10624_b200.tensor_core import Conv2d, FullyConnected
-    from paper_1812_10624_b200.tensor_core import Residual
+    from paper_1812_10624_b200.tensor_core import Concat, Residual
 
     def _depth(seq):
         return sum(_depth(l.body) + _depth(l.shortcut) if isinstance(l, Residual)
+                   else max(_depth(b) for b in l.branches) if isinstance(l, Concat)
                    else isinstance(l, (Conv2d, FullyConnected)) for l in seq)
     depth = max(1, _depth(layers))
     tol = gemm_tol(_longest_contraction(layers, in_shape, batch))

@@ -1,0 +1,116 @@
+"""Inception-V3 kinds on the B200 vs the CPU oracle.
+
+The reference has no asymmetric conv, padded average pool or concat
+(tensor_core.py:37-74; Inception-V3 is only a count profile there,
+model_partition.py:346-348), so these compare the CUDA path with the
+oracle's own definitions (oracle/stanza_oracle.py conv_forward with
+(kh, kw), avgpool_*, "concat"), themselves checked against finite
+differences in tests/test_inception_cpu.py: parity UNPINNED by any
+reference output.  Block bars as tests/test_gpu_engine.py (gemm_tol of the
+longest contraction); the average pool is bit-exact; end to end the
+reference's 1e-5 max_param_dev."""
+
+import numpy as np
+import pytest
+import torch
+
+import stanza_oracle as orc
+from test_gpu_engine import _run
+
+pytestmark = pytest.mark.gpu
+
+
+RECT = [  # Inception-V3 C / E shapes at reduced batch
+    ("1x7", lambda m: [m.Conv2d(128, 128, 1, 1, 0, 7, 3)], (128, 17, 17), 2),
+    ("7x1", lambda m: [m.Conv2d(128, 192, 7, 1, 3, 1, 0)], (128, 17, 17), 2),
+    ("1x3_e", lambda m: [m.Conv2d(384, 384, 1, 1, 0, 3, 1)], (384, 8, 8), 2),
+    ("3x1_e", lambda m: [m.Conv2d(384, 384, 3, 1, 1, 1, 0)], (384, 8, 8), 2),
+    ("1x7_relu_7x1", lambda m: [m.Conv2d(160, 160, 1, 1, 0, 7, 3), m.ReLU(),
+                                m.Conv2d(160, 192, 7, 1, 3, 1, 0)], (160, 9, 9), 2),
+]
+
+
+@pytest.mark.parametrize("case", RECT, ids=lambda c: c[0])
+def test_rect_convs(case):
+    from paper_1812_10624_b200 import tensor_core as m
+    _, make, shape, batch = case
+    _run(make(m), shape, batch, True, 11)
+
+
+@pytest.mark.parametrize("k,s,p,shape", [(3, 1, 1, (64, 17, 17)), (3, 2, 1, (32, 9, 9)),
+                                         (3, 1, 1, (2048, 8, 8))])
+def test_avgpool_bit_exact(k, s, p, shape):
+    """Forward and input gradient equal the oracle bit for bit (same float64
+    summation order, one rounding)."""
+    from paper_1812_10624_b200 import _lib
+    from paper_1812_10624_b200.engine import BlockEngine, Split, rup8
+    from paper_1812_10624_b200.tensor_core import AvgPool2d, ptr, stream_of
+    batch = 3
+    eng = BlockEngine([AvgPool2d(k, s, p)], shape, batch, "cuda:0", [[]], need_input_grad=True)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((batch, *shape)).astype(np.float32)
+    out = eng.forward(torch.from_numpy(x).cuda())
+    c, oh, ow = eng.out_shape
+    gy = rng.standard_normal((batch, c, oh, ow)).astype(np.float32)
+    g = Split.alloc("nhwc", (batch, oh, ow, rup8(c)), c, "cuda:0")
+    _lib.call("stzx_pack_nchw", ptr(torch.from_numpy(gy).cuda()), g.ptr(), g.ps, batch, c, oh, ow,
+              g.width, stream_of(torch.device("cuda:0")))
+    gin = eng.backward(g)
+    torch.cuda.synchronize()
+    y = out.to_float()[..., :c].permute(0, 3, 1, 2).cpu().numpy()
+    np.testing.assert_array_equal(y, orc.avgpool_forward(x, k, s, p))
+    gx = gin.to_float()[..., :shape[0]].permute(0, 3, 1, 2).cpu().numpy()
+    np.testing.assert_array_equal(gx, orc.avgpool_backward(x.shape, gy, k, s, p))
+
+
+def _module_a(m, cin, w):
+    bc = lambda ci, co, k, s=1, p=0: (m.Conv2d(ci, co, k, s, p), m.BatchNorm2d(co), m.ReLU())  # noqa
+    return m.Concat((bc(cin, w, 1), bc(cin, w, 1) + bc(w, w, 5, 1, 2),
+                     bc(cin, w, 1) + bc(w, w, 3, 1, 1) + bc(w, w, 3, 1, 1),
+                     (m.AvgPool2d(3, 1, 1),) + bc(cin, w, 1)))
+
+
+def test_inception_a_module():
+    from paper_1812_10624_b200 import tensor_core as m
+    _run([_module_a(m, 64, 32)], (64, 9, 9), 4, True, 12)
+
+
+def test_inception_e_module_nested_concat():
+    from paper_1812_10624_b200 import tensor_core as m
+    conv = lambda ci, co, kh, kw, ph, pw: m.Conv2d(ci, co, kh, 1, ph, kw, pw)  # noqa: E731
+    split = m.Concat(((conv(64, 32, 1, 3, 0, 1),), (conv(64, 32, 3, 1, 1, 0),)))
+    blk = m.Concat(((conv(64, 32, 1, 1, 0, 0),), (conv(64, 64, 1, 1, 0, 0), m.ReLU(), split),
+                    (m.AvgPool2d(3, 1, 1), conv(64, 32, 1, 1, 0, 0))))
+    _run([blk], (64, 4, 4), 4, True, 13)
+
+
+def test_inception_b_reduction_with_pool_branch():
+    from paper_1812_10624_b200 import tensor_core as m
+    blk = m.Concat(((m.Conv2d(64, 96, 3, 2),), (m.Conv2d(64, 32, 1), m.ReLU(),
+                                                  m.Conv2d(32, 64, 3, 2)),
+                    (m.MaxPool2d(3, 2),)))
+    _run([blk], (64, 9, 9), 2, True, 14)
+
+
+@pytest.mark.parametrize("nc,nf", [(1, 1), (2, 1)])
+def test_tiny_inception_matches_oracle(lib, nc, nf):
+    """The whole Inception-V3 module sequence at reduced width / input
+    (model_partition.tiny_inception: A x3, B, C x4 with 1x7 / 7x1, D, E x2
+    with nested concats), K = 4, trained layer-separated vs the oracle."""
+    from paper_1812_10624_b200.model_partition import tiny_inception
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+    from paper_1812_10624_b200.tensor_core import as_tuple
+    spec = tiny_inception(batch_k=4)
+    mk = orc.batch_fn(spec.input_shape, spec.batch_k, 7, classes=10)
+    res = StanzaCluster(spec, n_conv=nc, n_fc=nf, batch_fn=mk, lr=0.01, momentum=0.9, seed=3,
+                        device="cuda:0").train(2)
+    ref_p, ref_v, ref_l = orc.layer_separated_train([as_tuple(l) for l in spec.layers],
+                                                    spec.batch_k, nc, nf, 2, 3, mk, lr=0.01)
+    np.testing.assert_allclose(res.losses, ref_l, rtol=1e-5)
+    dev = orc.max_param_dev(res.state.params, ref_p)
+    a = np.concatenate([np.ravel(t) for row in res.state.velocities for t in row]).astype(np.float64)
+    b = np.concatenate([np.ravel(t) for row in ref_v for t in row]).astype(np.float64)
+    cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+    print(f"tiny_inception {nc}:{nf} max_param_dev {dev:.3e} velocity cosine {cos:.6f}")
+    assert dev <= 1e-5, dev
+    assert cos >= 0.9999, cos
