@@ -90,7 +90,7 @@ def host_info() -> dict:
             "blas_threads": blas_threads(), "numpy": np.__version__}
 
 
-_REF_K = {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32}
+_REF_K = {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32, "inception_v3_exec": 32}
 
 
 def reference_sample(model: str, n_conv: int, n_fc: int, k: int) -> dict:
@@ -112,8 +112,15 @@ def reference_sample(model: str, n_conv: int, n_fc: int, k: int) -> dict:
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
     import stanza_oracle as orc
-    layers, shape = {"alexnet_exec": orc.alexnet_layers, "vgg16_exec": orc.vgg16_layers,
-                     "resnet50_exec": orc.resnet_layers}.get(model, orc.alexnet_layers)()
+    table = {"alexnet_exec": orc.alexnet_layers, "vgg16_exec": orc.vgg16_layers,
+             "resnet50_exec": orc.resnet_layers}
+    if model in table:
+        layers, shape = table[model]()
+    else:   # the oracle runs any spec in its tuple grammar (e.g. the Inception kinds)
+        from paper_1812_10624_b200.model_partition import builtin_model
+        from paper_1812_10624_b200.tensor_core import as_tuple
+        spec = builtin_model(model)
+        layers, shape = [as_tuple(l) for l in spec.layers], tuple(spec.input_shape)
     cut = orc.split_index(layers)
     front, back = layers[:cut], layers[cut:]
     params = orc.seeded_init(layers, 3)
@@ -197,7 +204,8 @@ def _sample_text(ref, n_conv, n_fc, k):
 
 
 def workload_config(args, n_conv, n_fc, k):
-    return {"workload": f"{args.model} 224x224 synthetic, K={k} images per CONV worker, "
+    side = {"inception_v3_exec": 299}.get(args.model, 224)
+    return {"workload": f"{args.model} {side}x{side} synthetic, K={k} images per CONV worker, "
                         f"{n_conv} CONV : {n_fc} FC" + (" co-located on 1 GPU"
                                                          if args.gpus == 1 else ""),
             "model": args.model, "batch_per_conv_worker": k, "n_conv": n_conv, "n_fc": n_fc,
@@ -389,8 +397,7 @@ def main():
     dev = torch.device("cuda", local)
     lib = _lib.load()
     n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
-    k = args.batch_k or {"alexnet_exec": 128, "vgg16_exec": 64, "resnet50_exec": 32}.get(
-        args.model, 4)
+    k = args.batch_k or _REF_K.get(args.model, 4)
     spec = builtin_model(args.model, k)
 
     comm = None
@@ -559,7 +566,10 @@ def main():
     for kk, (tot, c) in sorted(calls.items(), key=lambda kv: -kv[1][0]):
         mean = tot / max(c, 1)
         gbs = kk[2] / (mean / 1e3) / 1e9 if kk[2] and tot else None
-        per_call[kk[0]] = {"ms": mean, "n": c, "total_ms": tot,
+        name = kk[0]
+        while name in per_call:          # same tag, different shape (e.g. two SGD blocks)
+            name += "'"
+        per_call[name] = {"ms": mean, "n": c, "total_ms": tot,
                            "tflops": (kk[1] / (mean / 1e3) / 1e12) if kk[1] and tot else None,
                            "GBps": gbs, "hbm_frac": gbs / hbm_peak if gbs else None}
     fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None

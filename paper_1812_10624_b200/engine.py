@@ -723,12 +723,12 @@ class BlockEngine:
                     gxs.append(kid.backward(gyb, rows=rows, accumulate=accumulate, phase=phase))
                     c0 += cb
                 out = V(self.gin[i])
-                acc = gxs[0]
+                tot = gxs[0]
                 for gx in gxs[1:]:
-                    _lib.call("stzx_add", acc.ptr(), acc.ps, gx.ptr(), gx.ps, None, out.ptr(),
+                    _lib.call("stzx_add", tot.ptr(), tot.ps, gx.ptr(), gx.ps, None, out.ptr(),
                               out.ps, b * out.row_elems, st, tag=f"{self.tag}concat{i}_add",
                               nbytes=18.0 * b * out.row_elems)
-                    acc = out
+                    tot = out
                 g_full = self.gin[i]
             elif op.kind == "residual":
                 # the block's final ReLU mask (its output z > 0) is applied by

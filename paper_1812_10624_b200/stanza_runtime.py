@@ -40,6 +40,7 @@ two persistent input buffers while the current step's graph replays.
 
 from __future__ import annotations
 
+import gc
 import random
 from collections.abc import Mapping
 
@@ -572,9 +573,14 @@ class StanzaCluster:
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(self.device)
             s.wait_stream(torch.cuda.current_stream(self.device))
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
-                    fn()
+            gc.collect()
+            gc.disable()
+            try:
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                        fn()
+            finally:
+                gc.enable()
             torch.cuda.current_stream(self.device).wait_stream(s)
             self._seg_graphs[key] = g
         g.replay()
@@ -682,11 +688,19 @@ class StanzaCluster:
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
-                if slot is not None:
-                    slot.zero_()
-                self._device_step(slot, x, labels)
+        # a garbage collection during capture could destroy another cluster's
+        # graphs / events (not permitted while a stream captures): collect
+        # now and keep the collector off until the capture ends
+        gc.collect()
+        gc.disable()
+        try:
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    if slot is not None:
+                        slot.zero_()
+                    self._device_step(slot, x, labels)
+        finally:
+            gc.enable()
         torch.cuda.current_stream(self.device).wait_stream(s)
         return g
 

@@ -131,18 +131,19 @@ def test_block_contract_vs_oracle(lib):
 
 
 def test_alexnet_reduced_batch_step(lib):
-    """AlexNet layer shapes at parity K=2, co-located (1,1), 1 iteration vs
+    """AlexNet layer shapes at parity K=2, co-located (1,1), 3 iterations vs
     the oracle (full-K oracle is ~35 min/iter)."""
     from paper_1812_10624_b200 import model_partition as mp
     spec = mp.alexnet(batch_k=2)
     mk = orc.batch_fn(spec.input_shape, 2, 7, classes=1000)
     layers = [tuple_of(l) for l in spec.layers]
-    ref_p, _, ref_l = orc.layer_separated_train(layers, 2, 1, 1, 1, 3, mk)
+    ref_p, ref_v, ref_l = orc.layer_separated_train(layers, 2, 1, 1, 3, 3, mk)
     from paper_1812_10624_b200.stanza_runtime import StanzaCluster
     cl = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=mk, lr=0.05, momentum=0.9, seed=3,
                        device="cuda:0")
-    out = cl.train(1)
+    out = cl.train(3)
     assert orc.max_param_dev(out.state.params, ref_p) <= TOL
+    assert orc.max_param_dev(out.state.velocities, ref_v) <= TOL
     np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)
 
 
@@ -246,3 +247,23 @@ def test_cluster_autotune_keeps_parity(lib, case):
     assert orc.max_param_dev(res.state.params, ref_p) <= TOL
     assert orc.max_param_dev(res.state.velocities, ref_v) <= TOL
     np.testing.assert_allclose(res.losses, g["losses"], rtol=TOL)
+
+
+def test_vgg16_parity_batch(lib):
+    """VGG-16 (BASELINE config 3's model: 13 convs, the 25088 -> 4096 -> 4096
+    -> 1000 head) at parity K = 1, co-located, 2 iterations vs the oracle
+    (the full-K oracle iteration takes hours).  The 6:2 split
+    with the FC-group exchange runs as 8 processes in tools/dist_parity.py
+    (profiles/r02/dist_parity_vgg16_6x2.log)."""
+    from paper_1812_10624_b200 import model_partition as mp
+    from paper_1812_10624_b200.stanza_runtime import StanzaCluster
+    spec = mp.vgg16(batch_k=1)
+    mk = orc.batch_fn(spec.input_shape, 1, 7, classes=1000)
+    layers = [tuple_of(l) for l in spec.layers]
+    ref_p, ref_v, ref_l = orc.layer_separated_train(layers, 1, 1, 1, 2, 3, mk)
+    cl = StanzaCluster(spec, n_conv=1, n_fc=1, batch_fn=mk, lr=0.05, momentum=0.9, seed=3,
+                       device="cuda:0")
+    out = cl.train(2)
+    assert orc.max_param_dev(out.state.params, ref_p) <= TOL
+    assert orc.max_param_dev(out.state.velocities, ref_v) <= TOL
+    np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)
