@@ -129,6 +129,7 @@ class BlockEngine:
         if self.batch % self.group:
             raise ShapeMismatch(f"batch {self.batch} is not a multiple of the group {self.group}")
         self.tag = tag
+        self.ws_key = None        # split-K scratch: see tensor_core.workspace
         self._build_plan()
         self._layout_params()
         self.children: dict = {}
@@ -251,6 +252,14 @@ class BlockEngine:
                 base += eng.total if eng.param_count else 0
                 kids.append(eng)
             self.children[i] = tuple(kids)
+
+    def set_workspace_key(self, key: str | None) -> None:
+        """Use the split-K scratch named ``key`` (this engine and its children)."""
+        self.ws_key = key
+        for kids in self.children.values():
+            for k in kids:
+                if k is not None:
+                    k.set_workspace_key(key)
 
     def has_bn(self) -> bool:
         """Whether the block normalises over its batch (BatchNorm, directly or
@@ -502,7 +511,7 @@ class BlockEngine:
             x = self.pack_input(x, rows)
         self._x = x
         st = stream_of(self.device)
-        ws = workspace(self.device)
+        ws = workspace(self.device, self.ws_key)
         b = r1 - r0
         for i, op in enumerate(self.ops):
             xin = V(self._input(i))
@@ -636,7 +645,7 @@ class BlockEngine:
             raise ValueError(f"unknown backward phase {phase!r}")
         r0, r1, V = self._rows(rows)
         st = stream_of(self.device)
-        ws = workspace(self.device)
+        ws = workspace(self.device, self.ws_key)
         b = r1 - r0
         acc = int(bool(accumulate))
         do_w, do_d = phase in ("all", "wgrad"), phase in ("all", "dgrad")

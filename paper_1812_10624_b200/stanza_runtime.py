@@ -319,6 +319,7 @@ class StanzaCluster:
                                   shared=self.fcs[0] if self.fcs else None,
                                   input_grad_buffer=self.gboundary.rows_view(lo * k, hi * k))
                 eng.rows = (lo * k, hi * k)
+                eng.set_workspace_key("fc_side")
                 self.fcs.append(eng)
         else:
             if comm.n_conv != n_conv or comm.n_fc != n_fc:
@@ -447,20 +448,23 @@ class StanzaCluster:
         acts = self.conv.forward(x_in)
         mark("activations")               # zero-copy: FC workers read row slices
         mark("fc_compute")
+        overlap = ev is None
         for eng in self.fcs:
             lo, hi = eng.rows
             eng.forward(acts.rows_view(lo, hi), lab_all[lo:hi], loss_out=loss_slot)
-            eng.backward()
-        # the FC block's exchange + update depend only on the FC gradients: they
-        # run on a side stream, concurrently with the CONV backward (the
-        # momentum kernel is HBM-bound and co-resides with the GEMMs, which
-        # are bound by the L2 -> SM feed); joined before the step ends
-        overlap = ev is None
+            eng.backward(phase="dgrad" if overlap else "all")
+        # the FC weight gradients, replica sum and update depend only on the
+        # FC block: they run on a side stream (own split-K scratch),
+        # concurrently with the CONV backward, which needs only the boundary
+        # gradient the input-gradient chain above wrote; joined before the
+        # step ends
         main = torch.cuda.current_stream(self.device)
         if overlap:
             side = self._side_stream()
             side.wait_stream(main)
             with torch.cuda.stream(side):
+                for eng in self.fcs:
+                    eng.backward(phase="wgrad")
                 for eng in self.fcs[1:]:
                     self.fcs[0].add_grads_from(eng)
                 self.fcs[0].sgd(n, self.lr, self.momentum)

@@ -295,13 +295,15 @@ _WORKSPACE: dict = {}
 WORKSPACE_BYTES = 256 << 20
 
 
-def workspace(device) -> torch.Tensor:
-    """Per-device split-K scratch (the ABI itself never allocates)."""
+def workspace(device, key: str | None = None) -> torch.Tensor:
+    """Per-device split-K scratch (the ABI itself never allocates); ``key``
+    names a separate one for work issued on another stream concurrently
+    (the single-device FC weight gradients on the side stream)."""
     dev = torch.device(device)
-    ws = _WORKSPACE.get(dev)
+    ws = _WORKSPACE.get((dev, key))
     if ws is None:
         ws = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
-        _WORKSPACE[dev] = ws
+        _WORKSPACE[(dev, key)] = ws
     return ws
 
 
