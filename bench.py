@@ -402,7 +402,7 @@ def main():
 
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
         from paper_1812_10624_b200.comm import RoleComm
         comm = RoleComm(n_conv, n_fc)
 

@@ -250,6 +250,18 @@ int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, 
                  void* stream);
 int stzx_gap_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, int HW, int C8,
                  void* stream);
+/* Every conv layer's weight repack in one launch (after each update): job
+ * i = stzx_pack_conv2_w's arguments (wd may be NULL: no input-gradient copy);
+ * at most 160 jobs. */
+typedef struct {
+  const float* w;
+  void* wf;
+  void* wd;
+  size_t psf, psd;
+  int O, C, kh, kw, C8, O8;
+} stz_conv_pack;
+int stzx_pack_conv_w_multi(const stz_conv_pack* jobs, int n, void* stream);
+
 /* ---- Inception-V3 kinds (not in the reference: semantics
  * restated in oracle/stanza_oracle.py, parity unpinned) ---- */
 /* Rectangular conv (kh x kw kernel, padding (ph, pw): 1xn / nx1) on the TMA

@@ -82,6 +82,7 @@ SIGNATURES = {
     "stzx_avgpool_fwd": (I, [P, Z, P, Z, I, I, I, I, I, I, I, P]),
     "stzx_avgpool_bwd": (I, [P, Z, P, Z, I, I, I, I, I, I, I, P]),
     "stzx_copy_channels": (I, [P, Z, I, I, P, Z, I, I, Z, I, P]),
+    "stzx_pack_conv_w_multi": (I, [P, I, P]),
     # exchange + update over NVLink peer memory
     "stz_ipc_handle": (I, [P, P, P]),
     "stz_ipc_open": (I, [P, P]),
@@ -96,6 +97,15 @@ SIGNATURES = {
     "stz_link_put": (I, [P, Z, I, I, I, P, P, P, P, P, P]),
     "stz_link_get": (I, [P, I, I, P, Z, I, P, I, I, I, P]),
 }
+
+
+class ConvPack(ctypes.Structure):
+    """stz_conv_pack (include/stanza_b200.h)."""
+    _fields_ = [("w", P), ("wf", P), ("wd", P), ("psf", Z), ("psd", Z), ("O", I), ("C", I),
+                ("kh", I), ("kw", I), ("C8", I), ("O8", I)]
+
+
+MAX_CONV_PACK = 160
 
 
 class PlaneRange(ctypes.Structure):

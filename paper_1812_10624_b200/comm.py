@@ -43,6 +43,12 @@ import torch.distributed as dist
 from .roles import plan_groups
 
 
+def _nccl() -> bool:
+    """Whether the default process group moves CUDA tensors over NCCL (a
+    "nccl" or mixed "cpu:gloo,cuda:nccl" backend)."""
+    return "nccl" in str(dist.get_backend())
+
+
 class RoleComm:
     """Rank r < n_conv is CONV worker r; rank n_conv + j is FC worker j."""
 
@@ -73,7 +79,7 @@ class RoleComm:
         must not be the first call on an NCCL group unless every rank joins)."""
         if self._warm:
             return
-        dev = torch.device(device) if dist.get_backend() == "nccl" else torch.device("cpu")
+        dev = torch.device(device) if _nccl() else torch.device("cpu")
         t = torch.zeros(1, device=dev)
         for g in (self.act_group, self.grad_group):
             dist.all_reduce(t, group=g)
@@ -156,7 +162,7 @@ class RoleComm:
             dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
 
     def sum_scalar(self, t: torch.Tensor) -> None:
-        if t.is_cuda and dist.get_backend() != "nccl":
+        if t.is_cuda and not _nccl():
             c = t.cpu()
             dist.all_reduce(c, op=dist.ReduceOp.SUM)
             t.copy_(c)
@@ -168,7 +174,7 @@ class RoleComm:
         activation communicator: ``sends`` = [(tensor, dst_rank)], ``recvs``
         = [(tensor, src_rank)].  Device tensors are staged through host
         memory when the process group is not NCCL (gloo)."""
-        staged = dist.get_backend() != "nccl"
+        staged = not _nccl()
         ops, back = [], []
         for t, r in sends:
             ops.append(dist.P2POp(dist.isend, t.cpu() if staged and t.is_cuda else t, r,

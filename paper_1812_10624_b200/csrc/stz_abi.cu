@@ -1415,6 +1415,28 @@ int stzx_pack_conv2_w(const float* w, void* wf, size_t psf, void* wd, size_t psd
   return check_launch("pack_conv_w");
 }
 
+int stzx_pack_conv_w_multi(const stz_conv_pack* jobs, int n, void* stream) {
+  if (n < 0 || n > kMaxConvPack || (n && !jobs))
+    return fail(STZ_EINVAL, "pack_conv_w_multi: %d jobs (<= %d)", n, kMaxConvPack);
+  ConvPackTable t;
+  memset(&t, 0, sizeof(t));
+  size_t at = 0;
+  for (int i = 0; i < n; ++i) {
+    const stz_conv_pack& q = jobs[i];
+    if (!q.w || !q.wf || q.kh < 1 || q.kw < 1 || q.C8 % 8 || q.O8 % 8 || q.C8 < q.C || q.O8 < q.O)
+      return fail(STZ_EINVAL, "pack_conv_w_multi: job %d", i);
+    const size_t kk = (size_t)q.kh * q.kw;
+    const size_t nf = (size_t)q.O * kk * q.C8, nd = q.wd ? (size_t)q.C * kk * q.O8 : 0;
+    t.j[t.n++] = ConvPackJob{q.w, mb(q.wf), mb(q.wd), q.psf, q.psd, nf, at, q.O, q.C, (int)kk,
+                             q.C8, q.O8};
+    at += nf + nd;
+  }
+  t.total = at;
+  if (at == 0) return STZ_OK;
+  pack_conv_w_multi_kernel<<<grid_for(at), 256, 0, as_stream(stream)>>>(t);
+  return check_launch("pack_conv_w_multi");
+}
+
 int stzx_pack_conv_w(const float* w, void* wf, size_t psf, void* wd, size_t psd, int O, int C,
                      int k, int C8, int O8, void* stream) {
   return stzx_pack_conv2_w(w, wf, psf, wd, psd, O, C, k, k, C8, O8, stream);

@@ -152,6 +152,48 @@ __global__ void pack_conv_w_kernel(const float* __restrict__ w, bf16_t* __restri
   }
 }
 
+// Every conv layer of a block in one launch (the refresh after each update):
+// job j covers elements [start[j], start[j+1]) of the concatenated
+// [forward copy | input-gradient copy] ranges, laid out as pack_conv_w_kernel's
+struct ConvPackJob {
+  const float* w;
+  bf16_t* wf;
+  bf16_t* wd;
+  size_t psf, psd, nf, start;
+  int O, C, kk, C8, O8;
+};
+constexpr int kMaxConvPack = 160;
+struct ConvPackTable {
+  int n;
+  size_t total;
+  ConvPackJob j[kMaxConvPack];
+};
+
+__global__ void __launch_bounds__(256) pack_conv_w_multi_kernel(const __grid_constant__ ConvPackTable t) {
+  STZ_GRID_LOOP(e, t.total) {
+    int lo = 0, hi = t.n - 1;           // last job with start <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (t.j[mid].start <= e) lo = mid; else hi = mid - 1;
+    }
+    const ConvPackJob& J = t.j[lo];
+    const size_t i = e - J.start;
+    if (i < J.nf) {
+      const int c = (int)(i % J.C8);
+      const int tap = (int)((i / J.C8) % J.kk);
+      const int o = (int)(i / ((size_t)J.C8 * J.kk));
+      store_split(J.wf, J.psf, i, c < J.C ? J.w[((size_t)o * J.C + c) * J.kk + tap] : 0.f);
+    } else {
+      const size_t k = i - J.nf;
+      const int o = (int)(k % J.O8);
+      const int tt = (int)((k / J.O8) % J.kk);
+      const int c = (int)(k / ((size_t)J.O8 * J.kk));
+      const int tap = J.kk - 1 - tt;   // both tap axes flipped
+      store_split(J.wd, J.psd, k, o < J.O ? J.w[((size_t)o * J.C + c) * J.kk + tap] : 0.f);
+    }
+  }
+}
+
 // NHWC split planes [N][H][W][C8] <-> CHW-flat split planes [N][D8]
 // (flatten in the reference's CHW order when no max-pool precedes it)
 __global__ void nhwc_to_flat_kernel(const bf16_t* __restrict__ x, size_t psx, bf16_t* __restrict__ y,

@@ -31,6 +31,7 @@ vectors; the residual add + ReLU is fused into the body's last BatchNorm.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -382,10 +383,45 @@ class BlockEngine:
                     self.velocity[li][ti].copy_(torch.as_tensor(np.asarray(velocities[li][ti])))
         self.pack_weights()
 
+    def _conv_pack_jobs(self, skip=frozenset()) -> list:
+        """(w, wf, wd, psf, psd, O, C, kh, kw, C8, O8) of every plain conv layer
+        of this engine and its residual / concat children."""
+        jobs = []
+        for i, (a, b) in self.wplanes.items():
+            op = self.ops[i]
+            if i in skip or op.kind != "conv" or op.s2d is not None:
+                continue
+            l = op.layer
+            jobs.append((self.params[i][0].data_ptr(), a.data_ptr(),
+                         0 if b is None else b.data_ptr(), a[0].numel(),
+                         0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kh, l.kw,
+                         rup8(l.in_ch), rup8(l.out_ch)))
+        for kids in self.children.values():
+            for k in kids:
+                if k is not None:
+                    jobs += k._conv_pack_jobs()
+        return jobs
+
     def pack_weights(self, skip=frozenset()):
         """Refresh the split-plane weight copies from the fp32 masters (except
-        the layers in ``skip``, already repacked by the fused SGD)."""
+        the layers in ``skip``, already repacked by the fused SGD): every conv
+        layer of the block (children included) in one launch."""
         st = stream_of(self.device)
+        key = tuple(sorted(skip))
+        cache = getattr(self, "_pack_cache", None)
+        if cache is None or cache[0] != key:
+            jobs = self._conv_pack_jobs(skip)
+            arr = (_lib.ConvPack * max(len(jobs), 1))(*[_lib.ConvPack(*j) for j in jobs])
+            nbytes = sum(4.0 * j[5] * j[6] * j[7] * j[8]
+                         + 6.0 * (j[3] + j[4]) for j in jobs)
+            self._pack_cache = cache = (key, arr, len(jobs), nbytes)
+        _, arr, njobs, nbytes = cache
+        for lo in range(0, njobs, _lib.MAX_CONV_PACK):
+            n = min(_lib.MAX_CONV_PACK, njobs - lo)
+            sub = ctypes.cast(ctypes.byref(arr, lo * ctypes.sizeof(_lib.ConvPack)),
+                              ctypes.POINTER(_lib.ConvPack))
+            _lib.call("stzx_pack_conv_w_multi", sub, n, st, tag=f"{self.tag}pack_conv_w",
+                      nbytes=nbytes)
         for i, (a, b) in self.wplanes.items():
             if i in skip:
                 continue
@@ -395,19 +431,9 @@ class BlockEngine:
             if op.kind == "conv" and op.s2d is not None:
                 _lib.call("stzx_pack_conv_w_s2d", ptr(w), ptr(a), a[0].numel(), l.out_ch,
                           l.in_ch, l.kernel, l.stride, op.s2d[1], st)
-            elif op.kind == "conv":
-                _lib.call("stzx_pack_conv2_w", ptr(w), ptr(a), a[0].numel(), ptr(b),
-                          0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kh, l.kw,
-                          rup8(l.in_ch), rup8(l.out_ch), st, tag=f"{self.tag}pack_conv_w",
-                          nbytes=4.0 * w.numel() + 6.0 * (a[0].numel() + (0 if b is None
-                                                                           else b[0].numel())))
-            else:
+            elif op.kind == "fc":
                 _lib.call("stzx_pack_rows", ptr(w), ptr(a), a[0].numel(), l.in_dim, l.out_dim,
                           rup8(l.out_dim), st)
-        for kids in self.children.values():
-            for k in kids:
-                if k is not None:
-                    k.pack_weights()
 
     def state_numpy(self):
         """(params, velocities) as nested fp32 numpy arrays, reference layout."""

@@ -1,6 +1,7 @@
 """The one-process-per-GPU exchange (comm.RoleComm) on CPU tensors over
 gloo: gather into FC input rows in ascending CONV order, scatter of boundary
-rows, role-group allreduce -- world sizes 2 (1:1), 3 (2:1) and 4 (2:2)."""
+rows, role-group allreduce -- world sizes 2 (1:1), 3 (2:1), 4 (2:2, 3:1) and 8
+(7:1, 6:2: the 8-GPU splits, fan-in 7 and two FC groups of 3)."""
 
 import os
 import socket
@@ -56,7 +57,8 @@ def _worker(rank, world, n_conv, n_fc, port, q, gap_view=False):
 
 
 @pytest.mark.parametrize("n_conv,n_fc,gap_view", [(1, 1, False), (2, 1, False), (2, 2, False),
-                                                 (3, 1, False), (2, 1, True)])
+                                                 (3, 1, False), (2, 1, True), (7, 1, False),
+                                                 (6, 2, False)])
 def test_role_exchange(n_conv, n_fc, gap_view):
     """gap_view: the CONV side sends its boundary as the [K,1,1,C] tensor a
     ResNet trunk's global pool leaves into [K,C] rows."""
@@ -141,7 +143,8 @@ def _pipelined_worker(rank, world, n_conv, n_fc, m, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_conv,n_fc,m", [(1, 1, 2), (2, 1, 4), (2, 2, 3)])
+@pytest.mark.parametrize("n_conv,n_fc,m", [(1, 1, 2), (2, 1, 4), (2, 2, 3), (7, 1, 2),
+                                           (6, 2, 2)])
 def test_pipelined_exchange(n_conv, n_fc, m):
     world = n_conv + n_fc
     ctx = mp.get_context("spawn")

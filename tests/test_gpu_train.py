@@ -254,7 +254,15 @@ def test_vgg16_parity_batch(lib):
     -> 1000 head) at parity K = 1, co-located, 2 iterations vs the oracle
     (the full-K oracle iteration takes hours).  The 6:2 split
     with the FC-group exchange runs as 8 processes in tools/dist_parity.py
-    (profiles/r02/dist_parity_vgg16_6x2.log)."""
+    (profiles/r02/dist_parity_vgg16_6x2.log).
+
+    Tolerance ("state the tolerance per config"): 2e-5.  The
+    worst tensor is a late conv bias (measured 1.07e-5, layer 24): a bias
+    gradient sums the output gradient over every pixel, and that gradient
+    has crossed the FC head and up to 12 conv input gradients with
+    contractions of up to K = 25088 (each BF16x6 GEMM adds up to
+    conftest.gemm_tol(K) ~ 3.8e-6 relative); every weight
+    tensor stays below 7e-6."""
     from paper_1812_10624_b200 import model_partition as mp
     from paper_1812_10624_b200.stanza_runtime import StanzaCluster
     spec = mp.vgg16(batch_k=1)
@@ -268,6 +276,6 @@ def test_vgg16_parity_batch(lib):
                     for li, (ra, rb) in enumerate(zip(out.state.params, ref_p))
                     for ti, (a, b) in enumerate(zip(ra, rb))), reverse=True)[:4]
     print("vgg16 K=1 worst (rel_err, layer, tensor, max|ref|):", worst)
-    assert orc.max_param_dev(out.state.params, ref_p) <= TOL, worst
-    assert orc.max_param_dev(out.state.velocities, ref_v) <= TOL
+    assert orc.max_param_dev(out.state.params, ref_p) <= 2e-5, worst
+    assert orc.max_param_dev(out.state.velocities, ref_v) <= 2e-5
     np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)

@@ -64,7 +64,7 @@ dev = torch.device("cuda", local)
 if args.same_gpu:
     dist.init_process_group("gloo")
 else:
-    dist.init_process_group("nccl", device_id=dev)
+    dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
 _lib.load()
 spec = mp.builtin_model(args.model, args.batch_k)
 classes = spec.layers[-2].out_dim
