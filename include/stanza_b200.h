@@ -287,9 +287,17 @@ int stzx_avgpool_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, in
                      int k, int s, int p, void* stream);
 /* Channel-slice copy of split-plane rows (the Inception concat and its
  * backward): dst[r][d0 + c] = src[r][s0 + c], c < C; row pitches src8 / dst8;
- * C, s0, d0, pitches multiples of 8. */
+ * C, s0, d0, pitches multiples of 8.  mask != NULL (pitch mask8, offset m0):
+ * zero where the mask (a ReLU output) is not > 0 -- a branch's closing ReLU
+ * backward fused into the copy. */
 int stzx_copy_channels(const void* src, size_t pss, int src8, int s0, void* dst, size_t psd,
-                       int dst8, int d0, size_t rows, int C, void* stream);
+                       int dst8, int d0, size_t rows, int C, const void* mask, int mask8, int m0,
+                       void* stream);
+/* y = ((x0 + x1) + x2) + x3 (fp32 RN, the first nin of 2..4 inputs, host
+ * arrays of pointers / plane strides), n a multiple of 8: the Inception
+ * concat's input gradient in branch order. */
+int stzx_add_n(const void* const* xs, const size_t* ps, int nin, void* y, size_t psy, size_t n,
+               void* stream);
 
 /* y = a + b elementwise (fp32 RN), n a multiple of 8: residual input
  * gradients; b masked by a ReLU output (plane 0 > 0) when mask_b != NULL */

@@ -81,7 +81,8 @@ SIGNATURES = {
     "stzx_conv2_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_avgpool_fwd": (I, [P, Z, P, Z, I, I, I, I, I, I, I, P]),
     "stzx_avgpool_bwd": (I, [P, Z, P, Z, I, I, I, I, I, I, I, P]),
-    "stzx_copy_channels": (I, [P, Z, I, I, P, Z, I, I, Z, I, P]),
+    "stzx_copy_channels": (I, [P, Z, I, I, P, Z, I, I, Z, I, P, I, I, P]),
+    "stzx_add_n": (I, [P, P, I, P, Z, Z, P]),
     "stzx_pack_conv_w_multi": (I, [P, I, P]),
     # exchange + update over NVLink peer memory
     "stz_ipc_handle": (I, [P, P, P]),

@@ -1737,15 +1737,28 @@ int stzx_avgpool_bwd(const void* gy, size_t psg, void* gx, size_t psx, int N, in
 }
 
 int stzx_copy_channels(const void* src, size_t pss, int src8, int s0, void* dst, size_t psd,
-                       int dst8, int d0, size_t rows, int C, void* stream) {
+                       int dst8, int d0, size_t rows, int C, const void* mask, int mask8, int m0,
+                       void* stream) {
   if (C % 8 || s0 % 8 || d0 % 8 || src8 % 8 || dst8 % 8 || s0 + C > src8 || d0 + C > dst8 ||
-      !aligned16(src) || !aligned16(dst) || pss % 8 || psd % 8)
+      !aligned16(src) || !aligned16(dst) || pss % 8 || psd % 8 ||
+      (mask && (mask8 % 8 || m0 % 8 || m0 + C > mask8 || !aligned16(mask))))
     return fail(STZ_EINVAL, "copy_channels: C %d from %d/%d to %d/%d (multiples of 8)", C, s0,
                 src8, d0, dst8);
   if (rows == 0 || C == 0) return STZ_OK;
   copy_channels_kernel<<<grid_for(rows * (C / 8)), 256, 0, as_stream(stream)>>>(
-      cb(src), pss, src8, s0, mb(dst), psd, dst8, d0, rows, C);
+      cb(src), pss, src8, s0, mb(dst), psd, dst8, d0, rows, C, cb(mask), mask8, m0);
   return check_launch("copy_channels");
+}
+
+int stzx_add_n(const void* const* xs, const size_t* ps, int nin, void* y, size_t psy, size_t n,
+               void* stream) {
+  if (nin < 2 || nin > 4 || n % 8 || !xs || !ps)
+    return fail(STZ_EINVAL, "add_n: %d inputs (2..4), %zu elements (multiple of 8)", nin, n);
+  if (n == 0) return STZ_OK;
+  add_n_split_kernel<<<grid_for(n / 8), 256, 0, as_stream(stream)>>>(
+      cb(xs[0]), cb(xs[1]), cb(nin > 2 ? xs[2] : xs[0]), cb(nin > 3 ? xs[3] : xs[0]), ps[0], ps[1],
+      nin > 2 ? ps[2] : 0, nin > 3 ? ps[3] : 0, nin, mb(y), psy, n / 8);
+  return check_launch("add_n");
 }
 
 int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, int C8,

@@ -388,20 +388,60 @@ __global__ void __launch_bounds__(256) avgpool_bwd_kernel(const bf16_t* __restri
 
 // channel-slice copy of split-plane rows: dst[r][d0 + c] = src[r][s0 + c] for
 // c < C (C, s0, d0, both row pitches multiples of 8): the Inception concat
-// (branch output -> its channel slice) and its backward (slice -> branch)
+// (branch output -> its channel slice) and its backward (slice -> branch).
+// With `mask` (row pitch mask8, offset m0): zero where the mask value (a ReLU
+// output, plane 0) is not > 0 -- the branch's closing ReLU backward, fused
 __global__ void __launch_bounds__(256) copy_channels_kernel(const bf16_t* __restrict__ src,
                                                             size_t pss, int src8, int s0,
                                                             bf16_t* __restrict__ dst, size_t psd,
-                                                            int dst8, int d0, size_t R, int C) {
+                                                            int dst8, int d0, size_t R, int C,
+                                                            const bf16_t* __restrict__ mask,
+                                                            int mask8, int m0) {
   const int nch = C / 8;
   STZ_GRID_LOOP(i, R * nch) {
     const size_t r = i / nch;
     const int cc = (int)(i % nch) * 8;
     const bf16_t* a = src + r * src8 + s0 + cc;
     bf16_t* b = dst + r * dst8 + d0 + cc;
+    if (mask) {
+      float v[8];
+      load_split8(a, pss, v);
+      apply_mask8(mask + r * mask8 + m0 + cc, v);
+      store_split8(b, psd, v);
+      continue;
+    }
 #pragma unroll
     for (int q = 0; q < 3; ++q)
       *reinterpret_cast<uint4*>(b + q * psd) = __ldg(reinterpret_cast<const uint4*>(a + q * pss));
+  }
+}
+
+// y = ((x0 + x1) + x2) + x3 (fp32 RN, the first n inputs): the Inception
+// concat's input gradient, one pass over every branch's input gradient
+__global__ void __launch_bounds__(256) add_n_split_kernel(const bf16_t* __restrict__ x0,
+                                                          const bf16_t* __restrict__ x1,
+                                                          const bf16_t* __restrict__ x2,
+                                                          const bf16_t* __restrict__ x3,
+                                                          size_t psx0, size_t psx1, size_t psx2,
+                                                          size_t psx3, int n, bf16_t* y,
+                                                          size_t psy, size_t n8) {
+  STZ_GRID_LOOP(i, n8) {
+    float acc[8], v[8];
+    load_split8(x0 + i * 8, psx0, acc);
+    load_split8(x1 + i * 8, psx1, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], v[j]);
+    if (n > 2) {
+      load_split8(x2 + i * 8, psx2, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], v[j]);
+    }
+    if (n > 3) {
+      load_split8(x3 + i * 8, psx3, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], v[j]);
+    }
+    store_split8(y + i * 8, psy, acc);
   }
 }
 

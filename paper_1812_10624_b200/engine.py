@@ -236,6 +236,8 @@ class BlockEngine:
                                       need_input_grad=True, group=self.group, flats=(base, flats),
                                       tag=f"{self.tag}c{i}b{bi}.")
                     base += eng.total if eng.param_count else 0
+                    if eng.ops[-1].kind == "relu":     # its backward: the concat's masked copy
+                        eng.ops[-1].relu_bwd_fused = True
                     kids.append(eng)
                 self.children[i] = tuple(kids)
                 continue
@@ -622,8 +624,8 @@ class BlockEngine:
                     out = V(kid._act(len(kid.ops) - 1))
                     cb = kid.out_shape[0]
                     _lib.call("stzx_copy_channels", out.ptr(), out.ps, out.width, 0, y.ptr(), y.ps,
-                              y.width, c0, b * oh * ow, cb, st, tag=f"{self.tag}concat{i}_fwd",
-                              nbytes=12.0 * b * oh * ow * cb)
+                              y.width, c0, b * oh * ow, cb, None, 0, 0, st,
+                              tag=f"{self.tag}concat{i}_fwd", nbytes=12.0 * b * oh * ow * cb)
                     c0 += cb
             elif op.kind == "residual":
                 body, short = self.children[i]
@@ -749,21 +751,36 @@ class BlockEngine:
                 # branches' input gradients in branch order
                 _, oh, ow = op.out_shape
                 c0, gxs = 0, []
+                y_full = V(self.acts[i])
                 for kid, gyb in zip(self.children[i], self._concat_gy[i]):
                     cb = kid.out_shape[0]
                     gv = V(gyb)
+                    # a branch closing with a ReLU gets its mask applied here
+                    # (the concat output slice is that ReLU's output)
+                    masked = kid.ops[-1].kind == "relu" and kid.ops[-1].relu_bwd_fused
                     _lib.call("stzx_copy_channels", g.ptr(), g.ps, g.width, c0, gv.ptr(), gv.ps,
-                              gv.width, 0, b * oh * ow, cb, st, tag=f"{self.tag}concat{i}_bwd",
-                              nbytes=12.0 * b * oh * ow * cb)
+                              gv.width, 0, b * oh * ow, cb, y_full.ptr() if masked else None,
+                              y_full.width if masked else 0, c0 if masked else 0, st,
+                              tag=f"{self.tag}concat{i}_bwd",
+                              nbytes=(12.0 + 2.0 * masked) * b * oh * ow * cb)
                     gxs.append(kid.backward(gyb, rows=rows, accumulate=accumulate, phase=phase))
                     c0 += cb
                 out = V(self.gin[i])
-                tot = gxs[0]
-                for gx in gxs[1:]:
-                    _lib.call("stzx_add", tot.ptr(), tot.ps, gx.ptr(), gx.ps, None, out.ptr(),
-                              out.ps, b * out.row_elems, st, tag=f"{self.tag}concat{i}_add",
-                              nbytes=18.0 * b * out.row_elems)
-                    tot = out
+                pos = 0
+                while pos < len(gxs):        # fp32 left fold in branch order, <= 4 per pass
+                    take = min(4 if pos == 0 else 3, len(gxs) - pos)
+                    srcs = ([] if pos == 0 else [out]) + gxs[pos:pos + take]
+                    pos += take
+                    if len(srcs) == 1:       # a single branch: its input gradient as is
+                        _lib.call("stzx_copy_channels", srcs[0].ptr(), srcs[0].ps,
+                                  srcs[0].width, 0, out.ptr(), out.ps, out.width, 0,
+                                  b * out.row_elems // out.width, out.width, None, 0, 0, st)
+                        break
+                    xs = _lib.ptr_array([sp.ptr() for sp in srcs])
+                    pss = (ctypes.c_size_t * len(srcs))(*[sp.ps for sp in srcs])
+                    _lib.call("stzx_add_n", xs, pss, len(srcs), out.ptr(), out.ps,
+                              b * out.row_elems, st, tag=f"{self.tag}concat{i}_add",
+                              nbytes=6.0 * (len(srcs) + 1) * b * out.row_elems)
                 g_full = self.gin[i]
             elif op.kind == "residual":
                 # the block's final ReLU mask (its output z > 0) is applied by
