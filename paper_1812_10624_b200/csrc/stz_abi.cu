@@ -468,10 +468,10 @@ bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8,
   return true;
 }
 
-// NHWC [N][H][W][C8] planes as a 4D tiled map with box {8, bw, bh, 1}, no
-// swizzle: the shifted-window conv's band (out-of-range boxes zero-fill)
+// NHWC [N][H][W][C8] planes as a 4D tiled map with box {32, bw, bh, 1} and the
+// 64-byte swizzle: the shifted-window conv's band (out-of-range boxes zero-fill)
 bool enc_band4d(CUtensorMap* out, const void* base, int N, int H, int W, int C8, int bw, int bh) {
-  const std::string key = cache_key(2, (uintptr_t)base, N, H, W, C8, bw, bh);
+  const std::string key = cache_key(3, (uintptr_t)base, N, H, W, C8, bw, bh);
   auto it = g_map_cache.find(key);
   if (it != g_map_cache.end()) {
     *out = it->second;
@@ -479,11 +479,11 @@ bool enc_band4d(CUtensorMap* out, const void* base, int N, int H, int W, int C8,
   }
   cuuint64_t dims[4] = {(cuuint64_t)C8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
   cuuint64_t strides[3] = {(cuuint64_t)C8 * 2, (cuuint64_t)W * C8 * 2, (cuuint64_t)H * W * C8 * 2};
-  cuuint32_t box[4] = {8, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)bh, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   g_map_cache.emplace(key, *out);

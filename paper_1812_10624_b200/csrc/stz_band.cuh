@@ -10,13 +10,17 @@
 // serves all k^2 taps of a 32-channel block: each tap is the same band
 // addressed at a row offset.
 //
-// The band sits in shared memory non-swizzled and K-major, with the rows of
-// each 8-channel chunk contiguous (16 B per row): core matrices of 8 rows x
-// 16 B, SBO = 128 B, LBO = rows * 16 B.  A descriptor may then start at any
-// 16-byte row offset (tools/band_check.cu verifies tcgen05.mma against a CPU
-// reference at shifts 0..127).  TMA fills it with 16-byte-wide boxes of up to
-// 256 rows per (plane, chunk).
-//
+// The band sits in shared memory K-major with the 64-byte SWIZZLE_64B
+// pattern TMA writes for a {32 channels, Wp, Hb} box: one 64-byte row per
+// virtual input row, 8-row atoms of 512 B.  The swizzle is a function of
+// the absolute shared-memory address (descriptor base offset 0), so a
+// descriptor may start at ANY 64-byte row: tap (th, tw) is the band at row
+// offset th*Wi + tw, and every core matrix stays one aligned 16-byte chunk
+// per row (tools/swz_check.cu checks tcgen05.mma on shifted SW64 / SW128
+// views against a CPU reference; round 1's non-swizzled band paid a second
+// shared-memory wavefront for every shift that was not a multiple of 8).
+// TMA fills it with one 4D box per plane.
+
 // Padding needs no padded copy: the band is loaded with a 4D TMA tiled box
 // {8 channels, Wp = W + 2*pad columns, Hb rows, 1 image} at (-pad, y0 - pad);
 // out-of-range coordinates are zero-filled, so shared memory holds exactly
@@ -27,13 +31,11 @@
 // are the im2col GEMM's B operand ([N][k*k][C8] K-major, TILED_K boxes).
 // Split-K runs over channel blocks (fp32 partials + the fixed-order reduce).
 //
-// Measured limit: a tap shift that is not a multiple of 8 rows makes every
-// core matrix straddle a 128-byte line, doubling the A read per MMA (~100
-// cycles per 128x64x16 MMA instead of ~66).  The band therefore pays only
-// where the im2col GEMM is badly feed-bound and the junk rows are few: the
-// unpadded space-to-depth conv1 (images stacked into one raster, ~7% junk).
-// Padded convs (per-image tiling, 23%+ junk) measured slower than im2col, so
-// the host enables the band for pad == 0 only.
+// The band pays where the im2col GEMM is feed-bound and the junk rows are
+// few: the unpadded space-to-depth conv1 (images stacked into one raster,
+// ~7% junk).  Padded convs (per-image tiling, 23%+ junk) measured slower
+// than im2col with the old non-swizzled band, so the host enables the band
+// for pad == 0 unless stz_set_band(2).
 #pragma once
 
 #include "stz_tma.cuh"
@@ -42,7 +44,7 @@ namespace stz {
 
 template <class EP>
 struct alignas(64) BandParams {
-  CUtensorMap band[3];   // per plane: 4D [N][H][W][C8], box {8, Wp, Hb, 1}, no swizzle
+  CUtensorMap band[3];   // per plane: 4D [N][H][W][C8], box {32, Wp, Hb, 1}, SWIZZLE_64B
   TgOperand b;           // weights, TILED_K
   EP ep;
   float* partial;        // split-K partials [splits][M_out][npad] (nullptr: no split)
@@ -73,9 +75,9 @@ struct BandCfg {
   static_assert(B_PLANE % 512 == 0, "B planes must stay 512-byte aligned");
 };
 
-// band geometry: each (plane, 8-channel chunk) holds Hb * Wp rows of 16 B,
-// padded to a multiple of 8 rows (TMA destinations stay 128-byte aligned);
-// the two bands are followed by the 1024-byte aligned weight stages
+// band geometry: each plane holds Hb * Wp rows of 64 B (32 channels), padded
+// to a multiple of 8 rows (planes stay 512-byte aligned: whole swizzle
+// atoms); the two bands are followed by the 1024-byte aligned weight stages
 __host__ __device__ inline int band_rows_alloc(int Hb, int Wp) { return (Hb * Wp + 7) / 8 * 8; }
 __host__ __device__ inline int band_bytes(int rows_alloc) { return 3 * 4 * rows_alloc * 16; }
 __host__ __device__ inline int band_region(int rows_alloc) {
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
   uint8_t* smem = smem_raw + (smem_base - raw);
   const int rows_alloc = band_rows_alloc(p.Hb, p.Wp);
   const int BAND = band_bytes(rows_alloc);
-  const int PLANE = 4 * rows_alloc * 16, CHUNK = rows_alloc * 16;
+  const int PLANE = rows_alloc * 64;
   const int REGION = band_region(rows_alloc);
   const uint32_t band0 = smem_base;                          // [2] bands
   const uint32_t bst0 = band0 + REGION;                      // [STAGES] B tiles
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer --------------------------------------------
-    const uint32_t band_tx = (uint32_t)(12 * p.Hb * p.Wp * 16);   // bytes the 12 boxes land
+    const uint32_t band_tx = (uint32_t)(3 * p.Hb * p.Wp * 64);   // bytes the 3 boxes land
     int gb = 0, gs = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
       int z, n, t, n0;
@@ -178,14 +180,14 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
           mbar_arrive_tx(&band_full[bb], band_tx);
         }
         __syncwarp();
-        if (lane < 12 && !(p.debug & 4)) {   // one 4D box per (plane, 8-channel chunk): padded rows y0 .. y0+Hb-1
-          const int pl = lane / 4, c = lane % 4;
-          const uint32_t dst = band0 + bb * BAND + pl * PLANE + c * CHUNK;
+        if (lane < 3 && !(p.debug & 4)) {   // one 4D box per plane: padded rows y0 .. y0+Hb-1
+          const int pl = lane;
+          const uint32_t dst = band0 + bb * BAND + pl * PLANE;
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
               "l"(reinterpret_cast<uint64_t>(&p.band[pl])), "r"(smem_u32(&band_full[bb])),
-              "r"(cb * 32 + c * 8), "r"(-p.pad), "r"(y0 - p.pad), "r"(n)
+              "r"(cb * 32), "r"(-p.pad), "r"(y0 - p.pad), "r"(n)
               : "memory");
         }
         for (int tp = 0; tp < taps; ++tp, ++gs) {
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
     const uint32_t idesc = sg_idesc(TG_BM, BN, false, false);
     constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
     constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
-    const uint64_t da0 = umma_desc_none(band0, (uint32_t)CHUNK, 128);
+    const uint64_t da0 = umma_desc_sw64(band0, 16, 512);
     const uint64_t db0 = tg_desc(TG_TILED_K, bst0, 0);
     int gb = 0, gs = 0, it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
@@ -238,7 +240,8 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
             if (p.debug & 2) break;
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              const uint32_t arow = (uint32_t)(bb * BAND + 2 * j * CHUNK) / 16 + mt * TG_BM + shift;
+              // 16-byte units: 64-byte rows, the j-th 16-deep k step 32 B in
+              const uint32_t arow = (uint32_t)(bb * BAND) / 16 + (mt * TG_BM + shift) * 4 + j * 2;
               const uint32_t tbig = tset + mt * Cfg::ACC_COLS, tsmall = tbig + BN;
 #pragma unroll
               for (int i = 0; i < 6; ++i) {

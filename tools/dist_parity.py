@@ -164,6 +164,11 @@ for MICRO in MICROS:
         rp, rv, rl = reference
         dev_p = orc.max_param_dev(res.state.params, rp)
         dev_v = orc.max_param_dev(res.state.velocities, rv)
+        vmax = max(float(np.abs(t).max()) for row in rv for t in row)
+        worst_v = sorted(((orc.rel_err(a, b), li, ti, float(np.abs(b).max()),
+                           float(np.abs(np.asarray(a, np.float64) - b).max()))
+                          for li, (ra, rb) in enumerate(zip(res.state.velocities, rv))
+                          for ti, (a, b) in enumerate(zip(ra, rb))), reverse=True)[:3]
         dl = max(abs(a - b) / abs(b) for a, b in zip(losses, rl))
         want = ["conv_compute", "activations", "fc_compute", "boundary", "exchange", "update"]
         if args.checkpoint:
@@ -180,6 +185,8 @@ for MICRO in MICROS:
                 f"{dist.get_backend()} ({world} GPUs)",
                 "max_param_dev": dev_p, "max_velocity_dev": dev_v, "loss_rel": dl,
                 "replicas_identical": rep_ok, "ledger_phases_ok": labels == want_labels,
+                "worst_velocity_tensors": [[round(w[0], 9), w[1], w[2], w[3], w[4]]
+                                           for w in worst_v], "max_velocity": vmax,
                 "seconds": round(time.time() - t0, 1)}
         if args.checkpoint:
             line["replica_blob_ok"] = any(b for b in blobs if b is not None)
