@@ -22,6 +22,7 @@
 #include "stz_norm.cuh"
 #include "stz_tma.cuh"
 #include "stz_band.cuh"
+#include "stz_bandw.cuh"
 #include "stz_peer.cuh"
 
 #include <cuda.h>
@@ -733,6 +734,13 @@ int launch_band(BandParams<EP>& prm, int items, size_t smem, cudaStream_t st) {
   return STZ_OK;
 }
 
+// The band weight gradient (stz_bandw.cuh): 64 input / output channels,
+// stride 1, no padding (the space-to-depth conv1).  Returns -1 when the shape
+// or the switches do not allow it (the caller runs the im2col GEMM).
+int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
+                   const EpConvWgradS2D& ep, int N, int Hs, int Ws, int OH, int OW, int C8, int O,
+                   int O8, int ks, void* ws, size_t ws_bytes, cudaStream_t st);
+
 struct BandShape {
   int BN, MT, tiles, Hb;
   double junk;   // computed rows / output rows
@@ -839,6 +847,74 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   if (rc || splits == 1) return rc;
   launch_reduce(prm.partial, splits, M_out, O, ep, st);
   return check_launch("band_reduce");
+}
+
+bool enc_sw128_rows(CUtensorMap* out, const void* base, int N, int H, int W, int bw) {
+  const std::string key = cache_key(4, (uintptr_t)base, N, H, W, bw);
+  auto it = g_map_cache.find(key);
+  if (it != g_map_cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
+  cuuint32_t box[4] = {64, (cuuint32_t)bw, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  g_map_cache.emplace(key, *out);
+  return true;
+}
+
+int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
+                   const EpConvWgradS2D& ep, int N, int Hs, int Ws, int OH, int OW, int C8, int O,
+                   int O8, int ks, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!g_use_band || !g_use_tma || !tma_ready() || C8 != 64 || O8 != 64 || O > 64 || ks < 1 ||
+      ks > 4)
+    return -1;
+  const int Wv = (OW + 15) / 16 * 16;
+  const int XW = Wv + 2 * ((ks + 1) / 2);
+  if (Wv > 256 || XW > 256) return -1;
+  const int rows_total = N * OH;
+  int splits = 2 * num_sms() / ks;
+  if (splits > rows_total) splits = rows_total;
+  if (splits < 1) splits = 1;
+  const int M = ks * ks * 64;
+  if (!ws || (size_t)splits * M * 64 * sizeof(float) > ws_bytes) return -1;
+  const size_t smem = bw_smem(XW, Wv);
+  if (smem > 227 * 1024) return -1;
+  BandWParams prm;
+  for (int pl = 0; pl < 3; ++pl) {
+    if (!enc_sw128_rows(&prm.x[pl], x + pl * psx, N, Hs, Ws, XW)) return -1;
+    if (!enc_sw128_rows(&prm.g[pl], g + pl * psg, N, OH, OW, Wv)) return -1;
+  }
+  prm.partial = static_cast<float*>(ws);
+  prm.N = N;
+  prm.OH = OH;
+  prm.ks = ks;
+  prm.Wv = Wv;
+  prm.XW = XW;
+  prm.splits = splits;
+  prm.rows_total = rows_total;
+  prm.d_oh = FastDiv((uint32_t)OH);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(bandwgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const int items = ks * splits;
+  const int grid = items < num_sms() ? items : num_sms();
+  if (g_trace)
+    fprintf(stderr, "[stz] conv_wgrad[bandw] N=%d OHxOW=%dx%d ks=%d Wv=%d XW=%d splits=%d items=%d "
+            "smem=%zu\n", N, OH, OW, ks, Wv, XW, splits, items, smem);
+  bandwgrad_kernel<<<grid, BW_THREADS, smem, st>>>(prm);
+  int rc = check_launch("conv_wgrad[bandw]");
+  if (rc) return rc;
+  launch_reduce(prm.partial, splits, M, O, ep, st);
+  return check_launch("bandw_reduce");
 }
 
 // C[M,N] = A . B with TMA operands built for tile width BN
@@ -1842,8 +1918,11 @@ int stzx_conv_wgrad_s2d(const void* x, size_t psx, const void* g, size_t psg, fl
   cudaStream_t st = as_stream(stream);
   EpConvWgradS2D e{gw, ks * ks * Cs8, O, C, k, s, ks, C * s * s, FastDiv(Cs8),
                    accumulate ? 1 : 0};
-  int rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, Cs8, Hs, Ws, O, O8, ks, ks, 1, 0, 0, OH, OW, ws,
-                           ws_bytes, st);
+  int rc = run_band_wgrad(cb(x), psx, cb(g), psg, e, N, Hs, Ws, OH, OW, Cs8, O, O8, ks, ws,
+                          ws_bytes, st);
+  if (rc < 0)
+    rc = gemm_conv_wgrad(cb(x), psx, cb(g), psg, e, N, Cs8, Hs, Ws, O, O8, ks, ks, 1, 0, 0, OH, OW,
+                         ws, ws_bytes, st);
   if (rc || !gb) return rc;
   return colsum_split(cb(g), psg, N * OH * OW, O, O8, gb, ws, ws_bytes, st, accumulate);
 }

@@ -1,0 +1,223 @@
+// Shifted-window ("band") weight gradient of a stride-1 conv with 64
+// channels in and out: AlexNet conv1 as space-to-depth (3x3 taps over 4x4
+// blocks, 48 -> 64 channels, 64 outputs, reference
+// tensor_core.py:242-261).
+//
+//   dW[o][t][c] = sum_q dY[q][o] * X[q + off(t)][c]
+//
+// The im2col GEMM (stz_tma.cuh, IM2COL_MN) fetches the input once per tap:
+// 9 boxes of the same pixels per k-block, which made this the least
+// efficient GEMM of the step (profiles/r01/op/conv0_wgrad_*: 2.2 GB of TMA
+// reads for 176 MB of operands).  Here every output raster row y of image n
+// is one stage: dY row (n, y) -- Wv = rup16(OW) virtual pixels, TMA zero-fills
+// the columns past OW -- and, for the stage's tap row dh, input row
+// (n, y + dh) with Wv + ks - 1 (+ 1) pixels.  Both are SWIZZLE_128B rows of
+// 64 channels (128 B).  In the MN-major view (M = channels, K = pixels) the
+// taps (dh, dw) of one tap row are the input row shifted by dw rows, and two
+// taps form one 128-row A operand: start = row dw, LBO = 128 B (the second
+// 64-channel group starts one pixel later).  SWIZZLE_128B descriptors may
+// start at any 128-byte row with base offset 0 (tools/swz_check.cu).
+//
+// Work item = (tap row dh, split z): split z covers the output raster rows
+// [j0, j1) of the N*OH rows; all tap rows of one split run in the same wave
+// (dY shared in L2).  Per item the CTA accumulates ceil(ks/2) tap-pair tiles
+// (BF16x6: big + small fp32 accumulators, 2 x 64 columns each) over its rows,
+// then the epilogue writes its tap rows of the split's partial [576][64];
+// the fixed-order split reduce applies EpConvWgradS2D (deterministic).
+// TMEM: 2 sets x 2 tiles x 128 columns -- item i's epilogue overlaps item
+// i+1's mainloop.
+#pragma once
+
+#include "stz_band.cuh"
+
+namespace stz {
+
+struct alignas(64) BandWParams {
+  CUtensorMap x[3];   // per plane: 4D [N][Hs][Ws][64], box {64, XW, 1, 1}, SWIZZLE_128B
+  CUtensorMap g[3];   // per plane: 4D [N][OH][OW][64], box {64, Wv, 1, 1}, SWIZZLE_128B
+  float* partial;     // [splits][ks*ks*64][64]
+  int N, OH, ks, Wv, XW;
+  int splits, rows_total;   // N * OH output raster rows
+  FastDiv d_oh;
+};
+
+constexpr int BW_THREADS = 256;
+constexpr int BW_STAGES = 4;
+
+__host__ __device__ inline int bw_xplane(int XW) { return (XW * 128 + 1023) / 1024 * 1024; }
+__host__ __device__ inline int bw_gplane(int Wv) { return Wv * 128; }
+__host__ __device__ inline int bw_stage(int XW, int Wv) {
+  return 3 * (bw_xplane(XW) + bw_gplane(Wv));
+}
+__host__ inline size_t bw_smem(int XW, int Wv) {
+  return 1024 + (size_t)BW_STAGES * bw_stage(XW, Wv) + 256;
+}
+
+__global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_constant__ BandWParams p) {
+  constexpr int ACC = 128;                 // big + small, 64 columns each
+  constexpr int TILES = 2;                 // ceil(ks / 2) for ks <= 4
+  constexpr int SET = TILES * ACC;         // 256 columns
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw);
+  const int XP = bw_xplane(p.XW), GP = bw_gplane(p.Wv), STG = bw_stage(p.XW, p.Wv);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BW_STAGES * STG);
+  uint64_t* empty = full + BW_STAGES;
+  uint64_t* tfull = empty + BW_STAGES;    // [2]
+  uint64_t* tempty = tfull + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ks = p.ks;
+  const int items = ks * p.splits;
+  auto rows_of = [&](int z, int& j0, int& j1) {
+    j0 = (int)((long long)p.rows_total * z / p.splits);
+    j1 = (int)((long long)p.rows_total * (z + 1) / p.splits);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < BW_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 0 && lane < 3) {
+    prefetch_tmap(&p.x[lane]);
+    prefetch_tmap(&p.g[lane]);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * SET);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: one stage per output raster row ------------------
+    const uint32_t tx = (uint32_t)(3 * 128 * (p.XW + p.Wv));
+    int gs = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      const int z = w / ks, dh = w - z * ks;
+      int j0, j1;
+      rows_of(z, j0, j1);
+      for (int j = j0; j < j1; ++j, ++gs) {
+        const int s = gs % BW_STAGES;
+        mbar_wait(&empty[s], ((gs / BW_STAGES) & 1) ^ 1);
+        if (lane == 0) mbar_arrive_tx(&full[s], tx);
+        __syncwarp();
+        uint32_t n, y;
+        p.d_oh.divmod((uint32_t)j, n, y);
+        const uint32_t st = base + s * STG;
+        if (lane < 6) {
+          const bool isx = lane < 3;
+          const int pl = isx ? lane : lane - 3;
+          const uint32_t dst = st + (isx ? pl * XP : 3 * XP + pl * GP);
+          const CUtensorMap* map = isx ? &p.x[pl] : &p.g[pl];
+          const int row = isx ? (int)y + dh : (int)y;
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+              "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(&full[s])), "r"(0), "r"(0),
+              "r"(row), "r"((int)n)
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ---------------------------------------------------
+    const uint32_t idesc = sg_idesc(TG_BM, 64, true, true);   // A, B MN-major
+    constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
+    constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
+    const int ksteps = p.Wv / 16;
+    int gs = 0, it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int z = w / ks;
+      int j0, j1;
+      rows_of(z, j0, j1);
+      const int set = it & 1, use = it >> 1;
+      mbar_wait(&tempty[set], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tset = tmem_base + set * SET;
+      for (int j = j0; j < j1; ++j, ++gs) {
+        const int s = gs % BW_STAGES;
+        mbar_wait(&full[s], (gs / BW_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t st = base + s * STG;
+        for (int kq = 0; kq < ksteps; ++kq) {
+#pragma unroll
+          for (int tile = 0; tile < TILES; ++tile) {
+            if (2 * tile >= ks) break;
+            const uint32_t tbig = tset + tile * ACC, tsmall = tbig + 64;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+              // A: input plane AP[i], rows (2 tile) + 16 kq ..; second tap one row on
+              const uint32_t aaddr = st + AP[i] * XP + (uint32_t)(2 * tile + 16 * kq) * 128;
+              const uint32_t baddr = st + 3 * XP + BP[i] * GP + (uint32_t)(16 * kq) * 128;
+              const uint64_t da = umma_desc_sw128(aaddr, 128, 1024);
+              const uint64_t db = umma_desc_sw128(baddr, 128, 1024);
+              const bool big = i == 5;
+              const bool first = j == j0 && kq == 0 && (big || i == 0);
+              umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
+            }
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&tfull[set]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: tap rows of the split's partial ---------------------
+    const int q = warp & 3;
+    const int r = q * 32 + lane;                 // accumulator row = (tap half, channel)
+    const int mrows = ks * ks * 64;
+    int it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int z = w / ks, dh = w - z * ks;
+      const int set = it & 1, use = it >> 1;
+      mbar_wait_backoff(&tfull[set], use & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int tile = 0; tile < TILES; ++tile) {
+        if (2 * tile >= ks) break;
+        const int dw = 2 * tile + (r >= 64 ? 1 : 0);
+        const bool valid = dw < ks;
+        const int m = (dh * ks + dw) * 64 + (r & 63);
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + set * SET + tile * ACC;
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t a[32], b[32];
+          tmem_ld16(tb + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&a[0]));
+          tmem_ld16(tb + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&a[16]));
+          tmem_ld16(tb + 64 + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&b[0]));
+          tmem_ld16(tb + 64 + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&b[16]));
+          tmem_ld_wait();
+          if (!valid || m >= mrows) continue;
+          float4* dst = reinterpret_cast<float4*>(p.partial + ((size_t)z * mrows + m) * 64 + c);
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            dst[h] = make_float4(__fadd_rn(__uint_as_float(a[4 * h]), __uint_as_float(b[4 * h])),
+                                 __fadd_rn(__uint_as_float(a[4 * h + 1]), __uint_as_float(b[4 * h + 1])),
+                                 __fadd_rn(__uint_as_float(a[4 * h + 2]), __uint_as_float(b[4 * h + 2])),
+                                 __fadd_rn(__uint_as_float(a[4 * h + 3]), __uint_as_float(b[4 * h + 3])));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[set]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * SET);
+  }
+}
+
+}  // namespace stz
