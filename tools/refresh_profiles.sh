@@ -12,7 +12,7 @@ ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --clock-contr
 for tag in "$@"; do
   python tools/profile_op.py "$tag" > "$OUT/${tag}_plain.log" 2>&1 || continue
   ncu --nvtx --nvtx-include "replay/" --set full --import-source on --clock-control none \
-      -k regex:tgemm -c 1 -o "$OUT/$tag" python tools/profile_op.py "$tag" > "$OUT/${tag}_ncu.log" 2>&1
+      -k regex:"tgemm|band" -c 1 -o "$OUT/$tag" python tools/profile_op.py "$tag" > "$OUT/${tag}_ncu.log" 2>&1
   ncu -i "$OUT/$tag.ncu-rep" --page raw --csv > "$OUT/${tag}_raw.csv" 2>/dev/null
   ncu -i "$OUT/$tag.ncu-rep" --page details --csv > "$OUT/${tag}_details.csv" 2>/dev/null
   ncu -i "$OUT/$tag.ncu-rep" --page source --csv --print-source sass > "$OUT/${tag}_source.csv" 2>/dev/null
