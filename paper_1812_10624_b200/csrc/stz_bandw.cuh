@@ -21,11 +21,15 @@
 // Work item = (tap row dh, split z): split z covers the output raster rows
 // [j0, j1) of the N*OH rows; all tap rows of one split run in the same wave
 // (dY shared in L2).  Per item the CTA accumulates ceil(ks/2) tap-pair tiles
-// (BF16x6: big + small fp32 accumulators, 2 x 64 columns each) over its rows,
-// then the epilogue writes its tap rows of the split's partial [576][64];
-// the fixed-order split reduce applies EpConvWgradS2D (deterministic).
-// TMEM: 2 sets x 2 tiles x 128 columns -- item i's epilogue overlaps item
-// i+1's mainloop.
+// over its rows, then the epilogue writes its tap rows of the split's
+// partial [576][64]; the fixed-order split reduce applies EpConvWgradS2D
+// (deterministic).  BF16x6 with the thin-tile schedule of stz_tma.cuh: the
+// dY planes b0 | b1 are one 128-wide MN-major operand (LBO = plane stride),
+// so each 16-deep step is 4 MMAs -- a0.b2 -> S2, a0.[b0|b1] -> [big|S1],
+// a1.[b0|b1] -> [S1|S2], a2.b0 -> S1 (every accumulator's first write an
+// overwrite) -- instead of 6, and the epilogue adds big + (S1 + S2).  The
+// N = 64 MMAs are bound by their shared-memory operand reads, which this
+// cuts by a fifth.  TMEM: 2 tiles x 192 columns.
 #pragma once
 
 #include "stz_band.cuh"
@@ -54,9 +58,9 @@ __host__ inline size_t bw_smem(int XW, int Wv) {
 }
 
 __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_constant__ BandWParams p) {
-  constexpr int ACC = 128;                 // big + small, 64 columns each
+  constexpr int ACC = 192;                 // big | S1 | S2, 64 columns each
   constexpr int TILES = 2;                 // ceil(ks / 2) for ks <= 4
-  constexpr int SET = TILES * ACC;         // 256 columns
+  constexpr int SET = TILES * ACC;         // 384 columns, one set
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -81,17 +85,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
-    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 4);
     mbar_fence_init();
   }
   if (warp == 0 && lane < 3) {
     prefetch_tmap(&p.x[lane]);
     prefetch_tmap(&p.g[lane]);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * SET);
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -130,45 +132,44 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ---------------------------------------------------
-    const uint32_t idesc = sg_idesc(TG_BM, 64, true, true);   // A, B MN-major
-    constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
-    constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
+    const uint32_t idesc64 = sg_idesc(TG_BM, 64, true, true);    // A, B MN-major
+    const uint32_t idesc128 = sg_idesc(TG_BM, 128, true, true);  // B = [b0 | b1]
     const int ksteps = p.Wv / 16;
     int gs = 0, it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int z = w / ks;
       int j0, j1;
       rows_of(z, j0, j1);
-      const int set = it & 1, use = it >> 1;
-      mbar_wait(&tempty[set], (use & 1) ^ 1);
+      mbar_wait(&tempty[0], (it & 1) ^ 1);
       tc_fence_after();
-      const uint32_t tset = tmem_base + set * SET;
       for (int j = j0; j < j1; ++j, ++gs) {
         const int s = gs % BW_STAGES;
         mbar_wait(&full[s], (gs / BW_STAGES) & 1);
         tc_fence_after();
         const uint32_t st = base + s * STG;
+        const uint32_t b0 = st + 3 * XP;
         for (int kq = 0; kq < ksteps; ++kq) {
+          const uint32_t acc = (j == j0 && kq == 0) ? 0u : 1u;
+          const uint64_t db0 = umma_desc_sw128(b0 + kq * 2048, GP, 1024);          // [b0|b1]
+          const uint64_t db2 = umma_desc_sw128(b0 + 2 * GP + kq * 2048, GP, 1024);  // b2
 #pragma unroll
           for (int tile = 0; tile < TILES; ++tile) {
             if (2 * tile >= ks) break;
-            const uint32_t tbig = tset + tile * ACC, tsmall = tbig + 64;
-#pragma unroll
-            for (int i = 0; i < 6; ++i) {
-              // A: input plane AP[i], rows (2 tile) + 16 kq ..; second tap one row on
-              const uint32_t aaddr = st + AP[i] * XP + (uint32_t)(2 * tile + 16 * kq) * 128;
-              const uint32_t baddr = st + 3 * XP + BP[i] * GP + (uint32_t)(16 * kq) * 128;
-              const uint64_t da = umma_desc_sw128(aaddr, 128, 1024);
-              const uint64_t db = umma_desc_sw128(baddr, 128, 1024);
-              const bool big = i == 5;
-              const bool first = j == j0 && kq == 0 && (big || i == 0);
-              umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
-            }
+            // A plane a: input rows (2 tile) + 16 kq ..; the second tap one row on
+            const uint32_t arow = st + (uint32_t)(2 * tile + 16 * kq) * 128;
+            const uint64_t da0 = umma_desc_sw128(arow, 128, 1024);
+            const uint64_t da1 = umma_desc_sw128(arow + XP, 128, 1024);
+            const uint64_t da2 = umma_desc_sw128(arow + 2 * XP, 128, 1024);
+            const uint32_t tbig = tmem_base + tile * ACC, ts1 = tbig + 64, ts2 = tbig + 128;
+            umma_f16(ts2, da0, db2, idesc64, acc);     // a0.b2 -> S2
+            umma_f16(tbig, da0, db0, idesc128, acc);   // a0.[b0|b1] -> big, S1
+            umma_f16(ts1, da1, db0, idesc128, 1u);     // a1.[b0|b1] -> S1, S2
+            umma_f16(ts1, da2, db0, idesc64, 1u);      // a2.b0 -> S1
           }
         }
         umma_commit(&empty[s]);
       }
-      umma_commit(&tfull[set]);
+      umma_commit(&tfull[0]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: tap rows of the split's partial ---------------------
@@ -178,8 +179,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
     int it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int z = w / ks, dh = w - z * ks;
-      const int set = it & 1, use = it >> 1;
-      mbar_wait_backoff(&tfull[set], use & 1);
+      mbar_wait_backoff(&tfull[0], it & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int tile = 0; tile < TILES; ++tile) {
@@ -187,28 +187,30 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
         const int dw = 2 * tile + (r >= 64 ? 1 : 0);
         const bool valid = dw < ks;
         const int m = (dh * ks + dw) * 64 + (r & 63);
-        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + set * SET + tile * ACC;
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + tile * ACC;
 #pragma unroll 1
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t a[32], b[32];
-          tmem_ld16(tb + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&a[0]));
-          tmem_ld16(tb + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&a[16]));
-          tmem_ld16(tb + 64 + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&b[0]));
-          tmem_ld16(tb + 64 + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&b[16]));
+        for (int c = 0; c < 64; c += 16) {
+          uint32_t a[16], b[16], d[16];
+          tmem_ld16(tb + (uint32_t)c, a);
+          tmem_ld16(tb + 64 + (uint32_t)c, b);
+          tmem_ld16(tb + 128 + (uint32_t)c, d);
           tmem_ld_wait();
           if (!valid || m >= mrows) continue;
           float4* dst = reinterpret_cast<float4*>(p.partial + ((size_t)z * mrows + m) * 64 + c);
 #pragma unroll
-          for (int h = 0; h < 8; ++h)
-            dst[h] = make_float4(__fadd_rn(__uint_as_float(a[4 * h]), __uint_as_float(b[4 * h])),
-                                 __fadd_rn(__uint_as_float(a[4 * h + 1]), __uint_as_float(b[4 * h + 1])),
-                                 __fadd_rn(__uint_as_float(a[4 * h + 2]), __uint_as_float(b[4 * h + 2])),
-                                 __fadd_rn(__uint_as_float(a[4 * h + 3]), __uint_as_float(b[4 * h + 3])));
+          for (int h = 0; h < 4; ++h) {
+            float v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              v[e] = __fadd_rn(__uint_as_float(a[4 * h + e]),
+                               __fadd_rn(__uint_as_float(b[4 * h + e]), __uint_as_float(d[4 * h + e])));
+            dst[h] = make_float4(v[0], v[1], v[2], v[3]);
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[set]);
+      if (lane == 0) mbar_arrive(&tempty[0]);
     }
   }
 
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * SET);
+    tmem_dealloc(tmem_base, 512);
   }
 }
 
