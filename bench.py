@@ -54,6 +54,9 @@ def parse():
                     help="micro-batches per iteration for N>1 (default: 4 when K allows)")
     ap.add_argument("--no-autotune", action="store_true",
                     help="keep the cost model's GEMM tile shapes (no measured override)")
+    ap.add_argument("--band", type=int, default=None, choices=[0, 1, 2],
+                    help="shifted-window conv kernels: 0 off, 1 unpadded convs (default), "
+                         "2 padded convs too")
     ap.add_argument("--no-nvlink-probe", action="store_true",
                     help="N>1: skip the untimed CONV<->FC transfer probe after the step")
     return ap.parse_args()
@@ -396,6 +399,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _lib.load()
+    if args.band is not None:
+        lib.stz_set_band(args.band)
     n_conv, n_fc = gpu_roles(args.gpus, args.fc_workers)
     k = args.batch_k or _REF_K.get(args.model, 4)
     spec = builtin_model(args.model, k)
