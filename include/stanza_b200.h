@@ -213,6 +213,12 @@ int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, s
 int stzx_relu_fwd(const void* x, size_t psx, void* y, size_t psy, size_t n, void* stream);
 int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t psx, size_t n,
                   void* stream);
+/* Forward of a strided conv as its space-to-depth stride-1 form (ks x ks
+ * taps over Cs8-channel blocks; channels >= Creal are zero padding, so the
+ * shifted-window kernel skips their 16-deep k steps). */
+int stzx_conv_fwd_s2d(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
+                      void* y, size_t psy, int N, int Creal, int Cs8, int Hs, int Ws, int O, int O8,
+                      int ks, int relu, void* ws, size_t ws_bytes, void* stream);
 /* Space-to-depth form of a strided first conv (AlexNet conv1, 11x11/4 on 3
  * channels): the padded input is regrouped into s x s blocks, giving a
  * stride-1 ceil(k/s) x ceil(k/s) conv over C*s*s (padded to Cs8) channels

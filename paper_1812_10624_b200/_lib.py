@@ -68,6 +68,7 @@ SIGNATURES = {
     "stzx_softmax_ce": (I, [P, P, P, P, Z, I, I, I, P]),
     "stzx_pack_s2d": (I, [P, P, Z, I, I, I, I, I, I, I, I, I, P]),
     "stzx_pack_conv_w_s2d": (I, [P, P, Z, I, I, I, I, I, P]),
+    "stzx_conv_fwd_s2d": (I, [P, Z, P, Z, P, P, Z, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_bn_fwd": (I, [P, Z, P, P, P, Z, P, Z, P, I, I, I, I, I, F, I, P, Z, P]),
     "stzx_bn_bwd": (I, [P, Z, P, P, Z, P, P, P, P, I, P, Z, I, I, I, I, I, P, Z, P]),

@@ -766,7 +766,7 @@ BandShape band_shape(int BN, int MT, int Nimg, int OH, int OW, int Wp, int k) {
 template <class EP>
 int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w, size_t psw,
                   const EP& ep, int Nimg, int C8, int H, int W, int O, int k, int pad, void* ws,
-                  size_t ws_bytes, cudaStream_t st) {
+                  size_t ws_bytes, cudaStream_t st, int creal = 0) {
   if (!g_use_band || !g_use_tma || !tma_ready() || C8 % 32 != 0 || k < 1 || pad < 0) return -1;
   // padded convs measured slower than the im2col GEMM (per-image tiling adds
   // junk rows and unaligned tap shifts double the A reads): pad 0 only, with
@@ -818,6 +818,7 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   prm.partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
   prm.N = O;
   prm.C8 = C8;
+  prm.creal = creal > 0 && creal <= C8 ? creal : C8;
   prm.Nimg = vimg;
   prm.Nreal = Nimg;
   prm.Hs = stacked ? H : (1 << 24);
@@ -1023,7 +1024,7 @@ inline bool square_kp(int kh, int kw, int ph, int pw) { return kh == kw && ph ==
 template <class EP>
 int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, const EP& ep, int N,
                   int C8, int H, int W, int O, int kh, int kw, int s, int ph, int pw, int OH,
-                  int OW, void* ws, size_t ws_bytes, cudaStream_t st) {
+                  int OW, void* ws, size_t ws_bytes, cudaStream_t st, int creal = 0) {
   const int M = N * OH * OW, K = kh * kw * C8;
   const bool sq = square_kp(kh, kw, ph, pw);
   if (kh == 1 && kw == 1 && s == 1 && ph == 0 && pw == 0 && tma_on() && C8 % 32 == 0) {
@@ -1037,7 +1038,7 @@ int gemm_conv_fwd(const bf16_t* x, size_t psx, const bf16_t* wf, size_t psw, con
   }
   if (s == 1 && sq) {
     const int rc = run_band_conv("conv_fwd[band]", x, psx, wf, psw, ep, N, C8, H, W, O, kh, ph, ws,
-                                 ws_bytes, st);
+                                 ws_bytes, st, creal);
     if (rc >= 0) return rc;
   }
   if (tma_on() && C8 % 32 == 0 && ph - (kh - 1) >= -128 && pw - (kw - 1) >= -128 && ph <= 128 &&
@@ -1533,6 +1534,17 @@ int stzx_conv_fwd(const void* x, size_t psx, const void* wf, size_t psw, const f
                   int p, int relu, void* ws, size_t ws_bytes, void* stream) {
   return stzx_conv2_fwd(x, psx, wf, psw, bias, y, psy, N, C8, H, W, O, O8, k, k, s, p, p, relu, ws,
                         ws_bytes, stream);
+}
+
+int stzx_conv_fwd_s2d(const void* x, size_t psx, const void* wf, size_t psw, const float* bias,
+                      void* y, size_t psy, int N, int Creal, int Cs8, int Hs, int Ws, int O, int O8,
+                      int ks, int relu, void* ws, size_t ws_bytes, void* stream) {
+  const int OH = Hs - ks + 1, OW = Ws - ks + 1;
+  if (OH <= 0 || OW <= 0 || Cs8 % 8 || O8 % 8 || O8 < O || Creal < 1 || Creal > Cs8)
+    return fail(STZ_EINVAL, "conv_fwd_s2d: bad shape");
+  EpSplit e{mb(y), psy, N * OH * OW, O, O8, bias, nullptr, relu};
+  return gemm_conv_fwd(cb(x), psx, cb(wf), psw, e, N, Cs8, Hs, Ws, O, ks, ks, 1, 0, 0, OH, OW, ws,
+                       ws_bytes, as_stream(stream), Creal);
 }
 
 int stzx_conv2_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,

@@ -50,6 +50,7 @@ struct alignas(64) BandParams {
   float* partial;        // split-K partials [splits][M_out][npad] (nullptr: no split)
   int N;                 // GEMM N (output channels)
   int C8;                // input channels (multiple of 32)
+  int creal;             // channels < creal are real: 16-deep k steps past it are skipped
   int Nimg, pad, Wp, ksz, OH, OW;
   int Nreal, Hs;         // stacked mode (pad 0): Nimg = 1 image of Nreal * Hs rows
   FastDiv d_hs;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
           const uint32_t sb = (uint32_t)(s * Cfg::B_STAGE) >> 4;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            if (p.debug & 2) break;
+            if ((p.debug & 2) || cb * 32 + j * 16 >= p.creal) break;   // padded channels: zeros
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               // 16-byte units: 64-byte rows, the j-th 16-deep k step 32 B in

@@ -548,14 +548,19 @@ class BlockEngine:
                 c, h, w = op.in_shape
                 y = V(self.acts[i])
                 wf, _ = self.wplanes[i]
-                kh, kw, cs, ph, pw = l.kh, l.kw, l.stride, l.ph, l.pw
                 if op.s2d is not None:             # stride-1 conv over s2d blocks
-                    kh, _, h, w = op.s2d
-                    kw, cs, ph, pw = kh, 1, 0, 0
-                _lib.call("stzx_conv2_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
-                          ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w, l.out_ch,
-                          y.width, kh, kw, cs, ph, pw, int(op.fused_relu), ptr(ws),
-                          ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_fwd")
+                    ks, cs8, hs, ws_ = op.s2d
+                    _lib.call("stzx_conv_fwd_s2d", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
+                              ptr(self.params[i][1]), y.ptr(), y.ps, b,
+                              l.in_ch * l.stride * l.stride, cs8, hs, ws_, l.out_ch, y.width, ks,
+                              int(op.fused_relu), ptr(ws), ws.numel(), st,
+                              flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_fwd")
+                else:
+                    _lib.call("stzx_conv2_fwd", xin.ptr(), xin.ps, ptr(wf), wf[0].numel(),
+                              ptr(self.params[i][1]), y.ptr(), y.ps, b, xin.width, h, w,
+                              l.out_ch, y.width, l.kh, l.kw, l.stride, l.ph, l.pw,
+                              int(op.fused_relu), ptr(ws), ws.numel(), st,
+                              flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_fwd")
             elif op.kind == "fc":
                 wp, _ = self.wplanes[i]
                 if self.acts[i] is not None:
