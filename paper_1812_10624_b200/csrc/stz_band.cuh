@@ -68,7 +68,10 @@ struct BandCfg {
   static constexpr int B_PLANE = BN * TG_BK * 2;          // one plane of a B tile
   static constexpr int B_STAGE = 3 * B_PLANE;
   static constexpr int STAGES = BN <= 64 ? 4 : 3;
-  static constexpr int ACC_COLS = 2 * BN;                // big + small per M tile
+  // thin tiles (BN = 64): the 4-MMA schedule of stz_tma.cuh -- weight planes
+  // b0 | b1 (contiguous) as one 128-wide operand; accumulators big | S1 | S2
+  static constexpr bool THIN = BN == 64;
+  static constexpr int ACC_COLS = THIN ? 3 * BN : 2 * BN;
   static constexpr int SET_COLS = MT * ACC_COLS;
   static constexpr int NSETS = 2 * SET_COLS <= 512 ? 2 : 1;
   static constexpr int TMEM_COLS = NSETS * SET_COLS <= 256 ? 256 : 512;
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer --------------------------------------------------
     const uint32_t idesc = sg_idesc(TG_BM, BN, false, false);
+    const uint32_t idesc2 = sg_idesc(TG_BM, 2 * BN, false, false);   // thin: B = [b0|b1]
     constexpr int AP[6] = {0, 2, 1, 0, 1, 0};
     constexpr int BP[6] = {2, 0, 1, 1, 0, 0};
     const uint64_t da0 = umma_desc_sw64(band0, 16, 512);
@@ -244,13 +248,26 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
               // 16-byte units: 64-byte rows, the j-th 16-deep k step 32 B in
               const uint32_t arow = (uint32_t)(bb * BAND) / 16 + (mt * TG_BM + shift) * 4 + j * 2;
               const uint32_t tbig = tset + mt * Cfg::ACC_COLS, tsmall = tbig + BN;
+              if constexpr (Cfg::THIN) {
+                const uint32_t acc = (cb == cb0 && (tp | j) == 0) ? 0u : 1u;
+                const uint64_t da_0 = da0 + arow;
+                const uint64_t da_1 = da0 + (arow + (uint32_t)PLANE / 16);
+                const uint64_t da_2 = da0 + (arow + (uint32_t)(2 * PLANE) / 16);
+                const uint64_t db01 = db0 + (sb + j * 2);                             // [b0|b1]
+                const uint64_t db_2 = db0 + (sb + 2 * (Cfg::B_PLANE >> 4) + j * 2);   // b2
+                umma_f16(tsmall + BN, da_0, db_2, idesc, acc);   // a0.b2 -> S2
+                umma_f16(tbig, da_0, db01, idesc2, acc);         // a0.[b0|b1] -> big, S1
+                umma_f16(tsmall, da_1, db01, idesc2, 1u);        // a1.[b0|b1] -> S1, S2
+                umma_f16(tsmall, da_2, db0 + (sb + j * 2), idesc, 1u);   // a2.b0 -> S1
+              } else {
 #pragma unroll
-              for (int i = 0; i < 6; ++i) {
-                const uint64_t da = da0 + (arow + (uint32_t)(AP[i] * PLANE) / 16);
-                const uint64_t db = db0 + (sb + BP[i] * (Cfg::B_PLANE >> 4) + j * 2);
-                const bool big = i == 5;
-                const bool first = cb == cb0 && (tp | j) == 0 && (big || i == 0);
-                umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
+                for (int i = 0; i < 6; ++i) {
+                  const uint64_t da = da0 + (arow + (uint32_t)(AP[i] * PLANE) / 16);
+                  const uint64_t db = db0 + (sb + BP[i] * (Cfg::B_PLANE >> 4) + j * 2);
+                  const bool big = i == 5;
+                  const bool first = cb == cb0 && (tp | j) == 0 && (big || i == 0);
+                  umma_f16(big ? tbig : tsmall, da, db, idesc, first ? 0u : 1u);
+                }
               }
             }
           }
@@ -297,6 +314,15 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
           tmem_ld16(tbase + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
           tmem_ld16(tbase + BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&rs[0]));
           tmem_ld16(tbase + BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs[16]));
+          if constexpr (Cfg::THIN) {     // small = S1 + S2
+            uint32_t r2[32];
+            tmem_ld16(tbase + 2 * BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&r2[0]));
+            tmem_ld16(tbase + 2 * BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&r2[16]));
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              rs[e] = __float_as_uint(__fadd_rn(__uint_as_float(rs[e]), __uint_as_float(r2[e])));
+          }
           tmem_ld_wait();
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
