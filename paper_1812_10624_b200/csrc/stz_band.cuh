@@ -68,9 +68,12 @@ struct BandCfg {
   static constexpr int B_PLANE = BN * TG_BK * 2;          // one plane of a B tile
   static constexpr int B_STAGE = 3 * B_PLANE;
   static constexpr int STAGES = BN <= 64 ? 4 : 3;
-  // thin tiles (BN = 64): the 4-MMA schedule of stz_tma.cuh -- weight planes
-  // b0 | b1 (contiguous) as one 128-wide operand; accumulators big | S1 | S2
-  static constexpr bool THIN = BN == 64;
+  // thin tiles: the 4-MMA schedule of stz_tma.cuh -- weight planes b0 | b1
+  // (contiguous) as one 128-wide operand; accumulators big | S1 | S2.  Off:
+  // with MT = 2 its 384 columns leave one TMEM set, and the serialised
+  // epilogue cost more than the saved MMAs (conv1 forward 0.232 -> 0.287 ms,
+  // measured); with MT = 1 the weight tile per 128 rows makes it feed-bound.
+  static constexpr bool THIN = false;
   static constexpr int ACC_COLS = THIN ? 3 * BN : 2 * BN;
   static constexpr int SET_COLS = MT * ACC_COLS;
   static constexpr int NSETS = 2 * SET_COLS <= 512 ? 2 : 1;
