@@ -578,6 +578,37 @@ def main():
                            "tflops": (kk[1] / (mean / 1e3) / 1e12) if kk[1] and tot else None,
                            "GBps": gbs, "hbm_frac": gbs / hbm_peak if gbs else None}
     fc_tflops = fc_fl / (fc_ms / 1e3) / 1e12 if fc_ms > 0 else None
+    # FC GEMMs against their own roofline: max(BF16x6 tensor time, HBM time
+    # of the weight planes + activations); at M = 128-896 rows the weight
+    # read dominates ("per-FC-GEMM bound = max(flops/peak,
+    # bytes/HBM)")
+    fc_roof = None
+    if cl.fcs:
+        eng = cl.fcs[0]
+        rows_b, tot_ms, tot_bound = {}, 0.0, 0.0
+        for kk, (tot, cnt) in calls.items():
+            tag, fl = kk[0], kk[1]
+            if not tag.startswith("fc") or fl <= 0 or "_" not in tag:
+                continue
+            li = int(tag[2:].split("_")[0])
+            lay = eng.ops[li].layer
+            m_rows = fl / (2.0 * lay.in_dim * lay.out_dim)
+            w = lay.in_dim * lay.out_dim
+            act = 6.0 * m_rows * (lay.in_dim + lay.out_dim)
+            nbytes = act + (4.0 * w if tag.endswith("wgrad") else 6.0 * w)
+            t_tc = fl / (bf16_peak / 6 * 1e12) * 1e3
+            t_hbm = nbytes / (hbm_peak * 1e9) * 1e3
+            mean = tot / max(cnt, 1)
+            bound = max(t_tc, t_hbm)
+            rows_b[tag] = {"ms": mean, "bound_ms": bound, "bound": "hbm" if t_hbm > t_tc else "tensor",
+                           "frac": bound / mean if mean else None, "rows": m_rows,
+                           "GBps": nbytes / (mean / 1e3) / 1e9 if mean else None}
+            tot_ms += mean * cnt
+            tot_bound += bound * cnt
+        fc_roof = {"frac": tot_bound / tot_ms if tot_ms else None, "calls": rows_b,
+                   "note": "bound = max(algorithmic FLOPs / (bf16 peak / 6), bytes / HBM peak); "
+                           "bytes = weight planes (6 B/param; fp32 gradient write 4 B/param for "
+                           "wgrad) + split-plane activations"}
     roofline = {
         "bound": "hbm", "kernel": kernel_key, "achieved": achieved_gbs, "peak": hbm_peak,
         "unit": "GB/s", "frac": achieved_gbs / hbm_peak if hbm_peak else None,
@@ -606,7 +637,8 @@ def main():
 
     clocks.stop()
     extras = {"rank": rank, "role": "conv" if is_conv_rank else "fc", "phase_ms": phase_ms,
-              "roofline": roofline, "fc_tflops": fc_tflops, "launches": launches}
+              "roofline": roofline, "fc_tflops": fc_tflops, "launches": launches,
+              "fc_roofline": fc_roof}
     if world > 1:
         objs = [None] * world
         dist.all_gather_object(objs, extras)
@@ -647,6 +679,7 @@ def main():
             "fc_tensor_pipe_frac": (6 * fc_ex["fc_tflops"] / bf16_peak)
             if fc_ex["fc_tflops"] else None,
             "fc_tflops_algorithmic": fc_ex["fc_tflops"],
+            "fc_roofline": fc_ex.get("fc_roofline"),
             "nvlink": probe,
             "phase_ms": {o["role"] + str(o["rank"]): o["phase_ms"] for o in objs},
             "gemm": "tcgen05 BF16x6 (3-way bf16 split, 6 MMAs, split fp32 TMEM accumulators)",
