@@ -1962,8 +1962,10 @@ int fill_peers(PeerTable& t, const float* const* grads, float* const* red,
     if (grads) t.g[j] = grads[j];
     if (red) t.red[j] = red[j];
     if (flags) t.flags[j] = flags[j];
-    if ((grads && !aligned16(t.g[j])) || (red && !aligned16(t.red[j])))
-      return fail(STZ_EINVAL, "peer group: member %d buffers must be 16-byte aligned", j);
+    if ((grads && !aligned16(t.g[j])) ||
+        (red && (reinterpret_cast<uintptr_t>(t.red[j]) & 31)))
+      return fail(STZ_EINVAL, "peer group: member %d gradient must be 16-byte aligned, reduced "
+                  "buffer 32-byte aligned (256-bit stores)", j);
   }
   return STZ_OK;
 }
@@ -1998,7 +2000,7 @@ int launch_reduce_push(const PeerTable& t, size_t n, cudaStream_t st) {
   // chunk r of member r: 256-byte aligned, the last one ragged
   const size_t per = ((n + t.R - 1) / t.R + 63) / 64 * 64;
   const size_t c0 = std::min(n, per * t.me), c1 = std::min(n, c0 + per);
-  const int grid = grid_for((c1 - c0) / 8 + 1);
+  const int grid = grid_for((c1 - c0) / 16 + 1);
   switch (t.R) {
 #define STZ_RP(R) \
   case R: peer_reduce_push_kernel<R><<<grid, 256, 0, st>>>(t, c0, c1); break;
@@ -2125,7 +2127,7 @@ int stz_link_put(const void* src, size_t ps, int rows, int D, int D8, float* dst
                  const int* labels, int* labels_dst, unsigned* my_flags, unsigned* remote_slot,
                  void* stream) {
   if (!src || !dst || !my_flags || !remote_slot || rows < 0 || D < 1 || D8 < D || D8 % 8 ||
-      ps % 8 || !aligned16(src) || (D % 4 == 0 && !aligned16(dst)) ||
+      ps % 8 || !aligned16(src) || (D % 8 == 0 && (reinterpret_cast<uintptr_t>(dst) & 31)) ||
       (labels != nullptr) != (labels_dst != nullptr))
     return fail(STZ_EINVAL, "link_put: rows %d D %d D8 %d (D8 %% 8 == 0, 16-byte aligned "
                 "planes, labels and their destination together)", rows, D, D8);

@@ -129,38 +129,58 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
                      __fadd_rn(a.w, b.w));
 }
 
-// chunk [c0, c1) of the vector (c0 % 4 == 0): sum over members in rank order,
-// store into every member's reduced buffer.  Two float4 per thread per trip
-// keep 2R remote loads in flight.
+// chunk [c0, c1) of the vector (c0 % 8 == 0): sum over members in rank order,
+// store into every member's reduced buffer.  8 floats per item, two items
+// per thread per trip keep 4R remote 16-byte loads in flight; each sum
+// leaves as one 256-bit store per member (two 16-byte stores to the same
+// sector halve the NVLink store rate, tools/p2p_bench.cu).
+__device__ __forceinline__ void add8(float (&s)[8], float4 a, float4 b) {
+  s[0] = __fadd_rn(s[0], a.x); s[1] = __fadd_rn(s[1], a.y);
+  s[2] = __fadd_rn(s[2], a.z); s[3] = __fadd_rn(s[3], a.w);
+  s[4] = __fadd_rn(s[4], b.x); s[5] = __fadd_rn(s[5], b.y);
+  s[6] = __fadd_rn(s[6], b.z); s[7] = __fadd_rn(s[7], b.w);
+}
+
 template <int R>
 __global__ void __launch_bounds__(256) peer_reduce_push_kernel(PeerTable t, size_t c0, size_t c1) {
   if (ld_volatile(t.flags[t.me] + kFlagStatus)) return;   // a peer is missing: touch nothing
-  const size_t q0 = c0 / 4, q1 = c1 / 4;
+  const size_t e0 = c0 / 8, e1 = c1 / 8;                  // 8-float items
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t q = q0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < q1; q += 2 * stride) {
+  for (size_t q = e0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < e1; q += 2 * stride) {
     const size_t q2 = q + stride;
-    const bool two = q2 < q1;
-    float4 a[R], b[R];
+    const bool two = q2 < e1;
+    float4 a[R][2], b[R][2];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      a[j] = __ldcv(reinterpret_cast<const float4*>(t.g[j]) + q);
-      if (two) b[j] = __ldcv(reinterpret_cast<const float4*>(t.g[j]) + q2);
+      const float4* g4 = reinterpret_cast<const float4*>(t.g[j]);
+      a[j][0] = __ldcv(g4 + 2 * q);
+      a[j][1] = __ldcv(g4 + 2 * q + 1);
+      if (two) {
+        b[j][0] = __ldcv(g4 + 2 * q2);
+        b[j][1] = __ldcv(g4 + 2 * q2 + 1);
+      }
     }
-    float4 s = a[0], u = b[0];
+    float s[8] = {a[0][0].x, a[0][0].y, a[0][0].z, a[0][0].w,
+                  a[0][1].x, a[0][1].y, a[0][1].z, a[0][1].w};
+    float u[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (two) {
+      u[0] = b[0][0].x; u[1] = b[0][0].y; u[2] = b[0][0].z; u[3] = b[0][0].w;
+      u[4] = b[0][1].x; u[5] = b[0][1].y; u[6] = b[0][1].z; u[7] = b[0][1].w;
+    }
 #pragma unroll
     for (int j = 1; j < R; ++j) {
-      s = add4(s, a[j]);
-      if (two) u = add4(u, b[j]);
+      add8(s, a[j][0], a[j][1]);
+      if (two) add8(u, b[j][0], b[j][1]);
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      reinterpret_cast<float4*>(t.red[j])[q] = s;
-      if (two) reinterpret_cast<float4*>(t.red[j])[q2] = u;
+      stg256(t.red[j] + 8 * q, s);
+      if (two) stg256(t.red[j] + 8 * q2, u);
     }
   }
   // scalar tail of the last chunk
-  if (blockIdx.x == 0 && threadIdx.x < (c1 - q1 * 4) && q1 * 4 >= c0) {
-    const size_t i = q1 * 4 + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x < (c1 - e1 * 8) && e1 * 8 >= c0) {
+    const size_t i = e1 * 8 + threadIdx.x;
     float s = __ldcv(t.g[0] + i);
 #pragma unroll
     for (int j = 1; j < R; ++j) s = __fadd_rn(s, __ldcv(t.g[j] + i));
@@ -300,8 +320,10 @@ __global__ void __launch_bounds__(256) link_put_kernel(const bf16_t* __restrict_
     }
     float* out = dst + r * D + c;
     if (vec) {
-      reinterpret_cast<float4*>(out)[0] = make_float4(v[0], v[1], v[2], v[3]);
-      reinterpret_cast<float4*>(out)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      // one 256-bit store per 8 elements: over NVLink two 16-byte stores to
+      // the same 32-byte sector run at half the rate (tools/p2p_bench.cu:
+      // 320 vs 680 GB/s GPU -> GPU)
+      stg256(out, v);
     } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e)
