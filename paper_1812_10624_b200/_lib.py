@@ -167,6 +167,8 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if os.environ.get("STZ_BAND"):          # experiments: shifted-window kernel selection
+        lib.stz_set_band(int(os.environ["STZ_BAND"]))
     _lib = lib
     return lib
 
