@@ -1732,10 +1732,16 @@ int stzx_relu_bwd(const void* gy, size_t psg, const void* src, void* gx, size_t 
 /* ---- ResNet-trunk kinds (semantics: oracle bn_* / gap_* / residual) ---- */
 
 namespace {
-// slices per group for the BatchNorm passes: ~4 blocks per SM in total, at
-// least `min_rows` rows per slice (small late-stage layers still fill the GPU)
-int bn_slices(size_t grows, int G, int tiles, int min_rows = 64) {
-  const long want = std::max(1L, (long)(4 * num_sms()) / std::max(1, G * tiles));
+// slices per group for the BatchNorm passes: one wave of resident blocks in
+// total (`per_sm` from the kernel's occupancy), at least `min_rows` rows per
+// slice (small late-stage layers still fill the GPU)
+int resident_per_sm(const void* kernel) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, 256, 0) != cudaSuccess || n < 1) n = 1;
+  return n;
+}
+int bn_slices(size_t grows, int G, int tiles, int per_sm, int min_rows = 64) {
+  const long want = std::max(1L, (long)(per_sm * num_sms()) / std::max(1, G * tiles));
   const long cap = std::max(1L, (long)((grows + min_rows - 1) / min_rows));
   return (int)std::min(want, cap);
 }
@@ -1749,7 +1755,8 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   cudaStream_t st = as_stream(stream);
   const int G = N / group, tiles = cdiv(C8 / 8, 32);
   const size_t grows = (size_t)group * HW;
-  const int slices = bn_slices(grows, G, tiles);
+  static const int occ_r = resident_per_sm((const void*)bn_reduce_kernel<false>), occ_a = resident_per_sm((const void*)bn_apply_kernel);
+  const int slices = bn_slices(grows, G, tiles, occ_r);
   const int rps = (int)((grows + slices - 1) / slices);
   const size_t total = (size_t)N * HW * (C8 / 8);
   if (total >= (1ull << 31)) return fail(STZ_EINVAL, "bn_fwd: %zu chunks exceed 2^31", total);
@@ -1758,12 +1765,12 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   double2* coef = cv.take<double2>((size_t)G * C8);
   if (!part || !coef) return fail(STZ_EWORKSPACE, "bn_fwd: workspace too small");
   bn_reduce_kernel<false><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, nullptr, 0, nullptr,
-                                                                 nullptr, part, HW, C8, group, rps);
+                                                                 part, HW, C8, group, rps);
   bn_stats_final_kernel<<<cdiv(G * C8 * 32, 256), 256, 0, st>>>(part, stats, coef, gamma, beta, G,
                                                           slices, C, C8, (double)grows,
                                                           (double)eps);
   const uint32_t rows = (uint32_t)N * HW;
-  const int aslices = bn_slices(rows, 1, tiles, 16);
+  const int aslices = std::max(G, bn_slices(rows, 1, tiles, occ_a, 16));   // slice <= group
   const uint32_t arps = (rows + aslices - 1) / aslices;
   bn_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(cb(x), psx, coef, cb(res), psr, mb(y), psy,
                                                         rows, arps, FastDiv((uint32_t)grows), C8,
@@ -1781,7 +1788,8 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
   cudaStream_t st = as_stream(stream);
   const int G = N / group, tiles = cdiv(C8 / 8, 32);
   const size_t grows = (size_t)group * HW;
-  const int slices = bn_slices(grows, G, tiles);
+  static const int occ_r = resident_per_sm((const void*)bn_reduce_kernel<true>), occ_a = resident_per_sm((const void*)bn_bwd_apply_kernel);
+  const int slices = bn_slices(grows, G, tiles, occ_r);
   const int rps = (int)((grows + slices - 1) / slices);
   const size_t total = (size_t)N * HW * (C8 / 8);
   if (total >= (1ull << 31)) return fail(STZ_EINVAL, "bn_bwd: %zu chunks exceed 2^31", total);
@@ -1790,12 +1798,12 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
   double4* coef = cv.take<double4>((size_t)G * C8);
   if (!part || !coef) return fail(STZ_EWORKSPACE, "bn_bwd: workspace too small");
   bn_reduce_kernel<true><<<dim3(slices, G, tiles), 256, 0, st>>>(cb(x), psx, cb(g), psg, cb(mask),
-                                                                stats, part, HW, C8, group, rps);
+                                                                part, HW, C8, group, rps);
   bn_bwd_final_kernel<<<cdiv(C8 * 32, 256), 256, 0, st>>>(part, stats, gamma, coef, ggamma, gbeta, G,
                                                     slices, C, C8, (double)grows, accumulate);
   if (gx) {
     const uint32_t rows = (uint32_t)N * HW;
-    const int aslices = bn_slices(rows, 1, tiles, 16);
+    const int aslices = std::max(G, bn_slices(rows, 1, tiles, occ_a, 16));   // slice <= group
     const uint32_t arps = (rows + aslices - 1) / aslices;
     bn_bwd_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(
         cb(g), psg, cb(mask), cb(x), psx, coef, mb(gx), psgx, rows, arps,

@@ -31,14 +31,17 @@ __device__ __forceinline__ void apply_mask8(const bf16_t* m, float (&v)[8]) {
 
 // Per (group, row slice, channel) float64 partial sums.
 //   forward : (sum x, sum x^2)
-//   backward: (sum g, sum g * xhat), xhat = (x - mean) * rstd
+//   backward: (sum g, sum g*x); the finalize forms sum g*xhat =
+//             rstd*(sum g*x - mean*sum g) (fp32 products are exact in float64)
 // Block = 256 threads as L channel-chunk lanes x R row lanes (L = min(chunks
 // left in this 32-chunk tile, 32), R = 256 / L); grid (slices, groups, tiles).
+// Several rows' loads are in flight per thread (the loop is latency-bound with
+// one); each thread's adds stay in row order.
 template <bool BWD>
-__global__ void __launch_bounds__(256) bn_reduce_kernel(
+__global__ void __launch_bounds__(256, 2) bn_reduce_kernel(
     const bf16_t* __restrict__ x, size_t psx, const bf16_t* __restrict__ g, size_t psg,
-    const bf16_t* __restrict__ mask, const double* __restrict__ stats,
-    double* __restrict__ partial, int HW, int C8, int group, int rows_per_slice) {
+    const bf16_t* __restrict__ mask, double* __restrict__ partial, int HW, int C8, int group,
+    int rows_per_slice) {
   __shared__ double red[256][16];
   const int nch = C8 / 8, ct = blockIdx.z;
   const int L = min(nch - ct * 32, 32), R = 256 / L;
@@ -51,36 +54,36 @@ __global__ void __launch_bounds__(256) bn_reduce_kernel(
   double s[8], q[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.0;
-  if (rl < R) {
-    double mean[8], rstd[8];
-    if (BWD) {
+  auto acc_row = [&](const float (&v)[8], const float (&gv)[8]) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        mean[j] = stats[((size_t)gi * C8 + cc * 8 + j) * 2];
-        rstd[j] = stats[((size_t)gi * C8 + cc * 8 + j) * 2 + 1];
-      }
+    for (int j = 0; j < 8; ++j) {
+      const double a = BWD ? (double)gv[j] : (double)v[j];
+      s[j] += a;
+      q[j] = fma(a, (double)v[j], q[j]);
     }
-    for (size_t r = r0 + rl; r < r1; r += R) {
-      const size_t off = (grow0 + r) * C8 + (size_t)cc * 8;
-      float v[8];
-      load_split8(x + off, psx, v);
-      if (!BWD) {
+  };
+  auto load_row = [&](size_t r, float (&v)[8], float (&gv)[8]) {
+    const size_t off = (grow0 + r) * C8 + (size_t)cc * 8;
+    load_split8(x + off, psx, v);
+    if (BWD) {
+      load_split8(g + off, psg, gv);
+      if (mask) apply_mask8(mask + off, gv);
+    }
+  };
+  constexpr int U = BWD ? 2 : 4;   // rows in flight (the backward loads two operands)
+  if (rl < R) {
+    size_t r = r0 + rl;
+    for (; r + (U - 1) * (size_t)R < r1; r += U * (size_t)R) {
+      float v[U][8], gv[U][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          s[j] += (double)v[j];
-          q[j] = fma((double)v[j], (double)v[j], q[j]);
-        }
-      } else {
-        float gv[8];
-        load_split8(g + off, psg, gv);
-        if (mask) apply_mask8(mask + off, gv);
+      for (int u = 0; u < U; ++u) load_row(r + u * (size_t)R, v[u], gv[u]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const double xh = __dmul_rn(__dsub_rn((double)v[j], mean[j]), rstd[j]);
-          s[j] += (double)gv[j];
-          q[j] = fma((double)gv[j], xh, q[j]);
-        }
-      }
+      for (int u = 0; u < U; ++u) acc_row(v[u], gv[u]);
+    }
+    for (; r < r1; r += R) {
+      float v[8], gv[8];
+      load_row(r, v, gv);
+      acc_row(v, gv);
     }
   }
 #pragma unroll
@@ -156,6 +159,7 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial,
     }
     const size_t i = (size_t)gi * C8 + c;
     const double mean = stats[i * 2], rstd = stats[i * 2 + 1];
+    q = rstd * (q - mean * s);   // sum g*x -> sum g*xhat
     const double cf = c < C ? (double)gamma[c] * rstd / m : 0.0;
     if (lane == 0)
       coef[i] = make_double4(cf * m, -cf * q * rstd, cf * (q * rstd * mean - s), 0.0);
@@ -169,85 +173,123 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial,
 }
 
 // The apply passes use the reduce kernels' block shape: L channel-chunk lanes
-// x R row lanes over a slice of rows, so each thread keeps its 8 channels'
-// coefficients in registers (reloaded only when its rows cross into the next
-// sample group) instead of re-reading them per element.
+// x R row lanes over a slice of rows.  The float64 coefficients of the (at
+// most two) sample groups a slice touches are staged in shared memory as
+// [group][quantity][j][lane] (consecutive lanes -> consecutive words); the
+// host makes slices no longer than a group, so a slice spans at most two.
+// Four rows' loads are in flight per thread.
+constexpr int BN_APPLY_U = 4;
+
+template <int NQ, typename CT>
+__device__ __forceinline__ void bn_stage_coef(double* sc, const CT* __restrict__ coef, int g_lo,
+                                              int ng, int C8, int ct, int L) {
+  for (int i = threadIdx.x; i < ng * NQ * 8 * L; i += blockDim.x) {
+    const int lane = i % L, j = (i / L) % 8, qd = (i / (8 * L)) % NQ, gg = i / (8 * L * NQ);
+    const double* src = reinterpret_cast<const double*>(&coef[(size_t)(g_lo + gg) * C8 + (ct * 32 + lane) * 8 + j]);
+    sc[((gg * NQ + qd) * 8 + j) * 32 + lane] = src[qd];
+  }
+}
 
 // y = x*A + B (float64, one rounding), then optionally + residual (fp32
 // add) and ReLU.  grid (slices, channel tiles).
-__global__ void __launch_bounds__(256) bn_apply_kernel(
+__global__ void __launch_bounds__(256, 2) bn_apply_kernel(
     const bf16_t* __restrict__ x, size_t psx, const double2* __restrict__ coef,
     const bf16_t* __restrict__ res, size_t psr, bf16_t* __restrict__ y, size_t psy,
     uint32_t rows, uint32_t rows_per_slice, FastDiv d_grows, int C8, int relu) {
+  __shared__ double sc[2 * 2 * 8 * 32];
   const int nch = C8 / 8, ct = blockIdx.y;
   const int L = min(nch - ct * 32, 32), R = 256 / L;
   const int t = threadIdx.x, cl = t % L, rl = t / L;
-  if (rl >= R) return;
   const int cc = ct * 32 + cl;
   const uint32_t r0 = blockIdx.x * rows_per_slice, r1 = min(rows, r0 + rows_per_slice);
-  double A[8], B[8];
-  uint32_t cur = 0xFFFFFFFFu;
-  for (uint32_t r = r0 + rl; r < r1; r += R) {
-    const uint32_t gi = d_grows.div(r);
-    if (gi != cur) {
-      cur = gi;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double2 ab = coef[(size_t)gi * C8 + cc * 8 + j];
-        A[j] = ab.x;
-        B[j] = ab.y;
-      }
-    }
-    const size_t off = (size_t)r * C8 + cc * 8;
-    float v[8], rr[8];
-    load_split8(x + off, psx, v);
-    if (res) load_split8(res + off, psr, rr);
+  if (r0 >= r1) return;
+  const uint32_t g_lo = d_grows.div(r0), ng = d_grows.div(r1 - 1) - g_lo + 1;   // <= 2
+  bn_stage_coef<2>(sc, coef, (int)g_lo, (int)ng, C8, ct, L);
+  __syncthreads();
+  if (rl >= R) return;
+  auto row = [&](uint32_t r, float (&v)[8], const float (&rr)[8]) {
+    const uint32_t gg = d_grows.div(r) - g_lo;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float o = (float)fma((double)v[j], A[j], B[j]);
+      const double A = sc[((gg * 2 + 0) * 8 + j) * 32 + cl];
+      const double B = sc[((gg * 2 + 1) * 8 + j) * 32 + cl];
+      float o = (float)fma((double)v[j], A, B);
       if (res) o = __fadd_rn(o, rr[j]);
       if (relu) o = o > 0.f ? o : 0.f;
       v[j] = o;
     }
-    store_split8(y + off, psy, v);
+    store_split8(y + (size_t)r * C8 + cc * 8, psy, v);
+  };
+  uint32_t r = r0 + rl;
+  for (; r + (BN_APPLY_U - 1) * (uint32_t)R < r1; r += BN_APPLY_U * (uint32_t)R) {
+    float v[BN_APPLY_U][8], rr[BN_APPLY_U][8];
+#pragma unroll
+    for (int u = 0; u < BN_APPLY_U; ++u) {
+      const size_t off = (size_t)(r + u * R) * C8 + cc * 8;
+      load_split8(x + off, psx, v[u]);
+      if (res) load_split8(res + off, psr, rr[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < BN_APPLY_U; ++u) row(r + u * R, v[u], rr[u]);
+  }
+  for (; r < r1; r += R) {
+    const size_t off = (size_t)r * C8 + cc * 8;
+    float v[8], rr[8];
+    load_split8(x + off, psx, v);
+    if (res) load_split8(res + off, psr, rr);
+    row(r, v, rr);
   }
 }
 
 // gx = P*g + Q*x + R (float64, one rounding); g masked by a ReLU output
 // when `mask` is given
-__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(
+__global__ void __launch_bounds__(256, 2) bn_bwd_apply_kernel(
     const bf16_t* __restrict__ g, size_t psg, const bf16_t* __restrict__ mask,
     const bf16_t* __restrict__ x, size_t psx, const double4* __restrict__ coef,
     bf16_t* __restrict__ gx, size_t psgx, uint32_t rows, uint32_t rows_per_slice,
     FastDiv d_grows, int C8) {
+  __shared__ double sc[2 * 3 * 8 * 32];
   const int nch = C8 / 8, ct = blockIdx.y;
   const int L = min(nch - ct * 32, 32), R = 256 / L;
   const int t = threadIdx.x, cl = t % L, rl = t / L;
-  if (rl >= R) return;
   const int cc = ct * 32 + cl;
   const uint32_t r0 = blockIdx.x * rows_per_slice, r1 = min(rows, r0 + rows_per_slice);
-  double P[8], Q[8], Rc[8];
-  uint32_t cur = 0xFFFFFFFFu;
-  for (uint32_t r = r0 + rl; r < r1; r += R) {
-    const uint32_t gi = d_grows.div(r);
-    if (gi != cur) {
-      cur = gi;
+  if (r0 >= r1) return;
+  const uint32_t g_lo = d_grows.div(r0), ng = d_grows.div(r1 - 1) - g_lo + 1;   // <= 2
+  bn_stage_coef<3>(sc, coef, (int)g_lo, (int)ng, C8, ct, L);
+  __syncthreads();
+  if (rl >= R) return;
+  auto row = [&](uint32_t r, float (&v)[8], const float (&gv)[8]) {
+    const uint32_t gg = d_grows.div(r) - g_lo;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double4 pqr = coef[(size_t)gi * C8 + cc * 8 + j];
-        P[j] = pqr.x;
-        Q[j] = pqr.y;
-        Rc[j] = pqr.z;
-      }
+    for (int j = 0; j < 8; ++j) {
+      const double P = sc[((gg * 3 + 0) * 8 + j) * 32 + cl];
+      const double Q = sc[((gg * 3 + 1) * 8 + j) * 32 + cl];
+      const double Rc = sc[((gg * 3 + 2) * 8 + j) * 32 + cl];
+      v[j] = (float)fma(P, (double)gv[j], fma(Q, (double)v[j], Rc));
     }
+    store_split8(gx + (size_t)r * C8 + cc * 8, psgx, v);
+  };
+  uint32_t r = r0 + rl;
+  for (; r + (BN_APPLY_U - 1) * (uint32_t)R < r1; r += BN_APPLY_U * (uint32_t)R) {
+    float v[BN_APPLY_U][8], gv[BN_APPLY_U][8];
+#pragma unroll
+    for (int u = 0; u < BN_APPLY_U; ++u) {
+      const size_t off = (size_t)(r + u * R) * C8 + cc * 8;
+      load_split8(x + off, psx, v[u]);
+      load_split8(g + off, psg, gv[u]);
+      if (mask) apply_mask8(mask + off, gv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < BN_APPLY_U; ++u) row(r + u * R, v[u], gv[u]);
+  }
+  for (; r < r1; r += R) {
     const size_t off = (size_t)r * C8 + cc * 8;
     float v[8], gv[8];
     load_split8(x + off, psx, v);
     load_split8(g + off, psg, gv);
     if (mask) apply_mask8(mask + off, gv);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (float)fma(P[j], (double)gv[j], fma(Q[j], (double)v[j], Rc[j]));
-    store_split8(gx + off, psgx, v);
+    row(r, v, gv);
   }
 }
 
