@@ -223,6 +223,7 @@ struct EpSplit {
   int rs = 0, rH = 0, rW = 0;
   FastDiv rd_ow, rd_oh;
   static constexpr bool HAS_BIAS = true;
+  static constexpr bool STAGED = true;
   __device__ __forceinline__ void bias8(int n0, float (&b)[8]) const {
     if (bias) {
       ldg8_f32(bias, n0, N, b);
@@ -230,6 +231,50 @@ struct EpSplit {
 #pragma unroll
       for (int j = 0; j < 8; ++j) b[j] = 0.f;
     }
+  }
+  __device__ __forceinline__ size_t row_of(int m) const {
+    if (!rs) return (size_t)m;
+    uint32_t q, ow, n, oh;
+    rd_ow.divmod((uint32_t)m, q, ow);
+    rd_oh.divmod(q, n, oh);
+    return ((size_t)n * rH + (size_t)rs * oh) * rW + (size_t)rs * ow;
+  }
+  // staged path, before the split: ReLU, zeros at n >= N (the ReLU mask is
+  // applied to the planes by store_planes)
+  __device__ __forceinline__ void prep8(int n0, float (&v)[8]) const {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float x = v[j];
+      if (relu && x < 0.f) x = 0.f;
+      v[j] = n0 + j < N ? x : 0.f;
+    }
+  }
+  // staged path: the three planes' 16 bytes of row m, columns n0..n0+7
+  __device__ __forceinline__ void store_planes(int m, int n0, uint4 (&pl)[3]) const {
+    if (n0 >= ld) return;
+    const size_t base = row_of(m) * ld + n0;
+    if (mask) {
+      // a masked element is 0 in every plane (split of +0)
+      const uint4 mk = __ldg(reinterpret_cast<const uint4*>(mask + base));
+      const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+      uint32_t keep[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t lo = mw[j] & 0xFFFFu, hi = mw[j] >> 16;
+        keep[j] = ((lo != 0u && lo < 0x8000u) ? 0x0000FFFFu : 0u) |
+                  ((hi != 0u && hi < 0x8000u) ? 0xFFFF0000u : 0u);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        pl[k].x &= keep[0];
+        pl[k].y &= keep[1];
+        pl[k].z &= keep[2];
+        pl[k].w &= keep[3];
+      }
+    }
+    *reinterpret_cast<uint4*>(out + base) = pl[0];
+    *reinterpret_cast<uint4*>(out + base + ps) = pl[1];
+    *reinterpret_cast<uint4*>(out + base + 2 * ps) = pl[2];
   }
   // v already includes the bias
   __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const {
@@ -283,6 +328,7 @@ struct EpF32 {
   int relu;
   int accumulate;     // 1: out += value (micro-batch gradient sums)
   static constexpr bool HAS_BIAS = true;
+  static constexpr bool STAGED = false;
   __device__ __forceinline__ void bias8(int n0, float (&b)[8]) const {
     if (bias) {
       ldg8_f32(bias, n0, N, b);
@@ -351,6 +397,7 @@ struct EpConvWgrad {
   FastDiv d_c8;
   int accumulate;   // 1: gw += value (micro-batch gradient sums)
   static constexpr bool HAS_BIAS = false;
+  static constexpr bool STAGED = false;
   __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
   __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const { store8(m, n0, v); }
   __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {
@@ -377,6 +424,7 @@ struct EpConvWgradS2D {
   FastDiv d_cs8;
   int accumulate;   // 1: gw += value
   static constexpr bool HAS_BIAS = false;
+  static constexpr bool STAGED = false;
   __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
   __device__ __forceinline__ void store8_nb(int m, int n0, float (&v)[8]) const { store8(m, n0, v); }
   __device__ __forceinline__ void store8(int m, int n0, float (&v)[8]) const {

@@ -74,7 +74,11 @@ struct TgCfg {
   static constexpr int B_BYTES = B_ROWS * TG_BK * 2;
   static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;  // + alignment slack + barriers
+  // epilogue staging (STAGED epilogues): per epilogue warp, 32 rows x 32
+  // columns of the three bf16 planes, so global stores go out row-contiguous
+  static constexpr int EPI_WARP_BYTES = 3 * 32 * 64;
+  static constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;  // + slack + barriers
   // NSETS accumulator sets (2 = double-buffered across tiles), each = big + small.
   // PAIRB (thin unpaired tiles): the B planes b0 | b1 are contiguous, so they
   // act as one 128-wide operand -- 4 MMAs per 16-k (2 at N=128, 2 at N=64)
@@ -302,7 +306,8 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t smem_base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (smem_base - raw);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  const uint32_t epi_smem = smem_base + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;   // [2] accumulator set ready for the epilogue
   uint64_t* tempty_bar = tfull_bar + 2;       // [2] accumulator set drained
@@ -482,6 +487,57 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
           tmem_ld16(tbase + 2 * BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs2[16]));
         }
         tmem_ld_wait();
+        if constexpr (EP::STAGED) {
+          if (!p.partial && !(p.debug & 1)) {
+            // split planes of 32 rows x 32 columns through shared memory: each
+            // lane writes its row's four 16-byte chunks (chunk slot XOR-swizzled
+            // by row pair, conflict-free), then four lanes store one row's 64
+            // contiguous bytes per plane (8 rows per instruction)
+            const uint32_t sb = epi_smem + (uint32_t)q * Cfg::EPI_WARP_BYTES;
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+              float v[8];
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                float sm = __uint_as_float(rs[8 * hh + jj]);
+                if constexpr (Cfg::PAIRB) sm = __fadd_rn(sm, __uint_as_float(rs2[8 * hh + jj]));
+                v[jj] = __fadd_rn(__uint_as_float(r[8 * hh + jj]), sm);
+                if (EP::HAS_BIAS) v[jj] = __fadd_rn(v[jj], bb[hh][jj]);
+              }
+              p.ep.prep8(n0 + c + 8 * hh, v);
+              uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                bf16_t a0, a1, a2, c0, c1, c2;
+                split_bf16x3(v[2 * j], a0, a1, a2);
+                split_bf16x3(v[2 * j + 1], c0, c1, c2);
+                w0[j] = (uint32_t)a0 | ((uint32_t)c0 << 16);
+                w1[j] = (uint32_t)a1 | ((uint32_t)c1 << 16);
+                w2[j] = (uint32_t)a2 | ((uint32_t)c2 << 16);
+              }
+              const uint32_t o = (uint32_t)lane * 64 + (uint32_t)((hh ^ (lane >> 1)) & 3) * 16;
+              sts128u(sb + o, w0[0], w0[1], w0[2], w0[3]);
+              sts128u(sb + 2048 + o, w1[0], w1[1], w1[2], w1[3]);
+              sts128u(sb + 4096 + o, w2[0], w2[1], w2[2], w2[3]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int rr = 8 * i + (lane >> 2), ch = lane & 3;
+              const uint32_t o = (uint32_t)rr * 64 + (uint32_t)((ch ^ (rr >> 1)) & 3) * 16;
+              const int mrow = m0 + h * TG_BM + q * 32 + rr, nb = n0 + c + 8 * ch;
+              if (mrow < p.M && nb < npad) {
+                uint4 pl[3];
+                pl[0] = lds128(sb + o);
+                pl[1] = lds128(sb + 2048 + o);
+                pl[2] = lds128(sb + 4096 + o);
+                p.ep.store_planes(mrow, nb, pl);
+              }
+            }
+            __syncwarp();
+            continue;
+          }
+        }
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const int nb = n0 + c + 8 * h;
