@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "stz_fmt.cuh"
 #include "stz_norm.cuh"
@@ -1497,20 +1498,23 @@ int stzx_pack_conv_w_multi(const stz_conv_pack* jobs, int n, void* stream) {
     return fail(STZ_EINVAL, "pack_conv_w_multi: %d jobs (<= %d)", n, kMaxConvPack);
   ConvPackTable t;
   memset(&t, 0, sizeof(t));
-  size_t at = 0;
+  long tiles = 0;
   for (int i = 0; i < n; ++i) {
     const stz_conv_pack& q = jobs[i];
-    if (!q.w || !q.wf || q.kh < 1 || q.kw < 1 || q.C8 % 8 || q.O8 % 8 || q.C8 < q.C || q.O8 < q.O)
+    const int kk = q.kh * q.kw;
+    if (!q.w || !q.wf || q.kh < 1 || q.kw < 1 || kk > 288 || q.C8 % 8 || q.O8 % 8 || q.C8 < q.C ||
+        q.O8 < q.O)
       return fail(STZ_EINVAL, "pack_conv_w_multi: job %d", i);
-    const size_t kk = (size_t)q.kh * q.kw;
-    const size_t nf = (size_t)q.O * kk * q.C8, nd = q.wd ? (size_t)q.C * kk * q.O8 : 0;
-    t.j[t.n++] = ConvPackJob{q.w, mb(q.wf), mb(q.wd), q.psf, q.psd, nf, at, q.O, q.C, (int)kk,
-                             q.C8, q.O8};
-    at += nf + nd;
+    const int cb = std::max(1, std::min(32, 288 / kk));
+    const long jt = (long)cdiv(q.O8, 32) * cdiv(q.C8, cb);
+    t.j[t.n++] = ConvPackJob{q.w, mb(q.wf), mb(q.wd), q.psf, q.psd, q.O, q.C, kk, q.C8, q.O8, cb,
+                             (int)tiles};
+    tiles += jt;
   }
-  t.total = at;
-  if (at == 0) return STZ_OK;
-  pack_conv_w_multi_kernel<<<grid_for(at), 256, 0, as_stream(stream)>>>(t);
+  if (tiles >= (1L << 31)) return fail(STZ_EINVAL, "pack_conv_w_multi: %ld tiles", tiles);
+  t.tiles = (int)tiles;
+  if (tiles == 0) return STZ_OK;
+  pack_conv_w_multi_kernel<<<(unsigned)tiles, 256, 0, as_stream(stream)>>>(t);
   return check_launch("pack_conv_w_multi");
 }
 
@@ -1547,6 +1551,78 @@ int stzx_conv_fwd_s2d(const void* x, size_t psx, const void* wf, size_t psw, con
                        ws_bytes, as_stream(stream), Creal);
 }
 
+namespace {
+// Input gradient of a stride-s conv as s*s phase sub-convolutions: input
+// pixel (s i + a, s j + b) only receives the taps kh = kh0(a) + s t,
+// kw = kw0(b) + s u, from output pixel (i + d_a - t, j + d_b - u).  Each
+// phase is a stride-1 conv of dY with an nth x ntw sub-kernel over an
+// Ha x Wa grid -- the TMA im2col GEMM, whose B operand reads the phase's
+// taps out of the packed (flipped) weights by a tap remap and whose
+// epilogue scatters row (n, i, j) to pixel (n, s i + a, s j + b).  Every
+// pixel belongs to one phase; phases without taps are zeroed.  Returns -1
+// when the geometry does not fit the TMA corners (caller falls back).
+int conv_dgrad_phases(const bf16_t* g, size_t psg, const bf16_t* wd, size_t psw, bf16_t* gx,
+                      size_t psgx, const bf16_t* mask, int N, int C, int C8, int H, int W, int O8,
+                      int kh, int kw, int s, int ph, int pw, int OH, int OW, void* ws,
+                      size_t ws_bytes, cudaStream_t st) {
+  struct Phase { int a, b, Ha, Wa, nth, ntw, lo_h, lo_w, hi_h, hi_w, base; };
+  std::vector<Phase> ph_list;
+  bool empty_phase = false;
+  for (int a = 0; a < s && a < H; ++a)
+    for (int b = 0; b < s && b < W; ++b) {
+      Phase q{a, b, (H - a + s - 1) / s, (W - b + s - 1) / s};
+      const int kh0 = (a + ph) % s, kw0 = (b + pw) % s;
+      q.nth = kh0 < kh ? (kh - kh0 + s - 1) / s : 0;
+      q.ntw = kw0 < kw ? (kw - kw0 + s - 1) / s : 0;
+      if (!q.nth || !q.ntw) {
+        empty_phase = true;
+        continue;
+      }
+      q.lo_h = (a + ph - kh0) / s - (q.nth - 1);
+      q.lo_w = (b + pw - kw0) / s - (q.ntw - 1);
+      q.hi_h = q.lo_h + q.Ha - OH;
+      q.hi_w = q.lo_w + q.Wa - OW;
+      for (int v : {q.lo_h, q.lo_w, q.hi_h, q.hi_w})
+        if (v < -128 || v > 127) return -1;
+      const int fh = (kh - 1) - kh0 - s * (q.nth - 1), fw = (kw - 1) - kw0 - s * (q.ntw - 1);
+      q.base = fh * kw + fw;
+      ph_list.push_back(q);
+    }
+  if (empty_phase) {
+    const size_t plane = (size_t)N * H * W * C8 * sizeof(bf16_t);
+    for (int q = 0; q < 3; ++q)
+      if (cudaMemsetAsync(gx + q * psgx, 0, plane, st) != cudaSuccess)
+        return fail(STZ_ECUDA, "conv_dgrad: memset");
+  }
+  for (const Phase& q : ph_list) {
+    EpSplit e{gx, psgx, N * q.Ha * q.Wa, C, C8, nullptr, mask, 0};
+    e.rs = s;
+    e.rH = H;
+    e.rW = W;
+    e.ro_h = q.a;
+    e.ro_w = q.b;
+    e.rd_ow = FastDiv(q.Wa);
+    e.rd_oh = FastDiv(q.Ha);
+    const int M = N * q.Ha * q.Wa, K = q.nth * q.ntw * O8;
+    const TgShape sh = tg_shape(M, C, K, ws_bytes);
+    TgOperand A, B;
+    if (!op_im2col(A, false, g, psg, N, OH, OW, O8, q.ntw, 1, q.lo_w, q.hi_w, q.Ha, q.Wa,
+                   TG_BM * sh.MH, q.lo_h, q.hi_h) ||
+        !op_tiled_k(B, wd, psw, C, kh * kw * O8, kh * kw * O8, sh.BN / sh.CL))
+      return -1;
+    B.remap = 1;
+    B.r_base = q.base;
+    B.r_sh = s * kw;
+    B.r_sw = s;
+    B.d_ro8 = FastDiv(O8);
+    B.d_rtw = FastDiv(q.ntw);
+    const int rc = run_tgemm("conv_dgrad[phase]", sh, A, B, e, M, C, K, ws, ws_bytes, st);
+    if (rc != STZ_OK) return rc;
+  }
+  return STZ_OK;
+}
+}  // namespace
+
 int stzx_conv2_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void* gx, size_t psgx,
                      const void* mask, int N, int C, int C8, int H, int W, int O8, int kh, int kw,
                      int s, int ph, int pw, void* ws, size_t ws_bytes, void* stream) {
@@ -1575,6 +1651,12 @@ int stzx_conv2_dgrad(const void* g, size_t psg, const void* wd, size_t psw, void
     if (op_tiled_k(a, cb(g), psg, M, O8, O8, TG_BM * sh.MH) &&
         op_tiled_k(b, cb(wd), psw, C, O8, O8, sh.BN / sh.CL))
       return run_tgemm("conv_dgrad[1x1s]", sh, a, b, e, M, C, O8, ws, ws_bytes, st);
+  }
+  if (s > 1 && (kh > 1 || kw > 1) && tma_on() && O8 % 32 == 0) {
+    const int rc = conv_dgrad_phases(cb(g), psg, cb(wd), psw, mb(gx), psgx, cb(mask), N, C, C8, H,
+                                     W, O8, kh, kw, s, ph, pw, OH, OW, ws, ws_bytes,
+                                     as_stream(stream));
+    if (rc >= 0) return rc;
   }
   EpSplit e{mb(gx), psgx, N * H * W, C, C8, nullptr, cb(mask), 0};
   return gemm_conv_dgrad(cb(g), psg, cb(wd), psw, e, N, C, H, W, O8, kh, kw, s, ph, pw, OH, OW,

@@ -159,38 +159,58 @@ struct ConvPackJob {
   const float* w;
   bf16_t* wf;
   bf16_t* wd;
-  size_t psf, psd, nf, start;
+  size_t psf, psd;
   int O, C, kk, C8, O8;
+  int cb;          // input channels per tile (32 o x cb c x kk taps staged in shared memory)
+  int tile0;       // first tile of this job
 };
 constexpr int kMaxConvPack = 160;
+constexpr int kPackTileWords = 32 * 32 * 9;   // smem budget: 32 o x (cb * kk) <= 288 words per o
 struct ConvPackTable {
-  int n;
-  size_t total;
+  int n, tiles;
   ConvPackJob j[kMaxConvPack];
 };
 
+// One tile = 32 output channels x cb input channels x all kk taps of one
+// job: read w[o][c0 .. c0+cb)[*] as contiguous runs (coalesced), stage it in
+// shared memory, then write the forward operand wf [O][kk][C8] (c-runs) and
+// the flipped input-gradient operand wd [C][kk][O8] (o-runs) from it.
+// Padded channels are zeros.
 __global__ void __launch_bounds__(256) pack_conv_w_multi_kernel(const __grid_constant__ ConvPackTable t) {
-  STZ_GRID_LOOP(e, t.total) {
-    int lo = 0, hi = t.n - 1;           // last job with start <= e
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (t.j[mid].start <= e) lo = mid; else hi = mid - 1;
-    }
-    const ConvPackJob& J = t.j[lo];
-    const size_t i = e - J.start;
-    if (i < J.nf) {
-      const int c = (int)(i % J.C8);
-      const int tap = (int)((i / J.C8) % J.kk);
-      const int o = (int)(i / ((size_t)J.C8 * J.kk));
-      store_split(J.wf, J.psf, i, c < J.C ? J.w[((size_t)o * J.C + c) * J.kk + tap] : 0.f);
-    } else {
-      const size_t k = i - J.nf;
-      const int o = (int)(k % J.O8);
-      const int tt = (int)((k / J.O8) % J.kk);
-      const int c = (int)(k / ((size_t)J.O8 * J.kk));
-      const int tap = J.kk - 1 - tt;   // both tap axes flipped
-      store_split(J.wd, J.psd, k, o < J.O ? J.w[((size_t)o * J.C + c) * J.kk + tap] : 0.f);
-    }
+  __shared__ float tile[32 * (288 + 1)];
+  int lo = 0, hi = t.n - 1;           // last job with tile0 <= blockIdx.x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.j[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const ConvPackJob& J = t.j[lo];
+  const int kk = J.kk, cb = J.cb, span = cb * kk, ld = span + 1;
+  const int ncb = (J.C8 + cb - 1) / cb;
+  const int tl = (int)blockIdx.x - J.tile0;
+  const int o0 = (tl / ncb) * 32, c0 = (tl % ncb) * cb;
+  for (int idx = threadIdx.x; idx < 32 * span; idx += blockDim.x) {
+    const int ol = idx / span, rem = idx - ol * span;
+    const int o = o0 + ol, c = c0 + rem / kk;
+    tile[ol * ld + rem] = (o < J.O && c < J.C) ? __ldg(J.w + ((size_t)o * J.C + c0) * kk + rem) : 0.f;
+  }
+  __syncthreads();
+  // wf[o][tap][c], c fastest
+  for (int idx = threadIdx.x; idx < 32 * span; idx += blockDim.x) {
+    const int ol = idx / span, rem = idx - ol * span;
+    const int tap = rem / cb, cl = rem - tap * cb;
+    const int o = o0 + ol, c = c0 + cl;
+    if (o < J.O && c < J.C8)
+      store_split(J.wf, J.psf, ((size_t)o * kk + tap) * J.C8 + c, tile[ol * ld + cl * kk + tap]);
+  }
+  if (!J.wd) return;
+  // wd[c][tt][o], o fastest, tap = kk - 1 - tt (both tap axes flipped)
+  for (int idx = threadIdx.x; idx < 32 * span; idx += blockDim.x) {
+    const int cl = idx / (32 * kk), rem = idx - cl * 32 * kk;
+    const int tt = rem >> 5, ol = rem & 31;
+    const int o = o0 + ol, c = c0 + cl;
+    if (c < J.C && o < J.O8)
+      store_split(J.wd, J.psd, ((size_t)c * kk + tt) * J.O8 + o,
+                  tile[ol * ld + cl * kk + (kk - 1 - tt)]);
   }
 }
 

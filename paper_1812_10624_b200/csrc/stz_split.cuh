@@ -220,7 +220,8 @@ struct EpSplit {
   // strided row scatter (a 1x1 stride-rs conv's input gradient): GEMM row
   // m = (n, oh, ow) of the output grid lands on input pixel (n, rs*oh, rs*ow)
   // of the rH x rW input; rs = 0 keeps rows in place
-  int rs = 0, rH = 0, rW = 0;
+  // (+ offsets ro_h, ro_w: one phase of a strided conv's input gradient)
+  int rs = 0, rH = 0, rW = 0, ro_h = 0, ro_w = 0;
   FastDiv rd_ow, rd_oh;
   static constexpr bool HAS_BIAS = true;
   static constexpr bool STAGED = true;
@@ -237,7 +238,7 @@ struct EpSplit {
     uint32_t q, ow, n, oh;
     rd_ow.divmod((uint32_t)m, q, ow);
     rd_oh.divmod(q, n, oh);
-    return ((size_t)n * rH + (size_t)rs * oh) * rW + (size_t)rs * ow;
+    return ((size_t)n * rH + (size_t)rs * oh + ro_h) * rW + (size_t)rs * ow + ro_w;
   }
   // staged path, before the split: ReLU, zeros at n >= N (the ReLU mask is
   // applied to the planes by store_planes)
@@ -284,7 +285,7 @@ struct EpSplit {
       uint32_t q, ow, n, oh;
       rd_ow.divmod((uint32_t)m, q, ow);
       rd_oh.divmod(q, n, oh);
-      row = ((size_t)n * rH + (size_t)rs * oh) * rW + (size_t)rs * ow;
+      row = ((size_t)n * rH + (size_t)rs * oh + ro_h) * rW + (size_t)rs * ow + ro_w;
     }
     const size_t base = row * ld + n0;
     uint4 mk = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);

@@ -43,6 +43,11 @@ struct alignas(64) TgOperand {
   // taps (th, tw) = divmod(tap, ksz) with ksz = the kernel width
   int lo, s, C8, ksz, flip, lo_h;
   FastDiv d_ohw, d_ow, d_c8, d_k;
+  // TILED_K tap remap (the weights of one phase of a strided conv's input
+  // gradient): K index (tap', o) with tap' = (th', tw') over a sub-kernel of
+  // width r_tw reads column (r_base + th' r_sh + tw' r_sw) * r_o8 + o
+  int remap, r_base, r_sh, r_sw;
+  FastDiv d_ro8, d_rtw;
 };
 
 template <class EP>
@@ -55,7 +60,8 @@ struct alignas(64) TgParams {
 };
 
 constexpr int TG_BM = 128, TG_BK = 32;
-constexpr int TG_THREADS = 256;  // w0 TMA (32 lanes), w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
+constexpr int TG_THREADS = 384;  // w0 TMA (32 lanes), w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue
+constexpr int TG_EC = 16;        // epilogue columns per TMEM load round
 
 // CL = 1: one CTA per 128 x BN tile.  CL = 2: a CTA pair computes a 256 x BN
 // tile with cta_group::2 UMMA -- each CTA stages its own 128 A rows and HALF
@@ -74,10 +80,10 @@ struct TgCfg {
   static constexpr int B_BYTES = B_ROWS * TG_BK * 2;
   static constexpr int STAGE_BYTES = 3 * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  // epilogue staging (STAGED epilogues): per epilogue warp, 32 rows x 32
+  // epilogue staging (STAGED epilogues): per epilogue warp, 32 rows x 16
   // columns of the three bf16 planes, so global stores go out row-contiguous
-  static constexpr int EPI_WARP_BYTES = 3 * 32 * 64;
-  static constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
+  static constexpr int EPI_WARP_BYTES = 3 * 32 * 32;
+  static constexpr int EPI_BYTES = 8 * EPI_WARP_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;  // + slack + barriers
   // NSETS accumulator sets (2 = double-buffered across tiles), each = big + small.
   // PAIRB (thin unpaired tiles): the B planes b0 | b1 are contiguous, so they
@@ -241,6 +247,12 @@ __device__ __forceinline__ void tg_load_box(const TgOperand& op, int bi, uint32_
   const uint32_t dst = tile_base + plane * plane_bytes + box * op.box_bytes;
   switch (op.mode) {
     case TG_TILED_K:
+      if (op.remap) {
+        uint32_t tap, o0, th, tw;
+        op.d_ro8.divmod((uint32_t)k0, tap, o0);
+        op.d_rtw.divmod(tap, th, tw);
+        k0 = (op.r_base + (int)th * op.r_sh + (int)tw * op.r_sw) * (int)op.d_ro8.d + (int)o0;
+      }
       tma_2d<CL>(map, dst, bar, k0, r0 + box * op.box_rows);
       break;
     case TG_TILED_MN:
@@ -327,7 +339,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4 * CL);   // one arrival per epilogue warp of the pair
+      mbar_init(&tempty_bar[a], 8 * CL);   // one arrival per epilogue warp of the pair
     }
     mbar_fence_init();
   }
@@ -454,7 +466,10 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM (big + small) -> registers -> ep ---------
-    const int q = warp & 3;
+    // 8 warps: warp w reads TMEM lanes 32 (w % 4) .. (its row quadrant) and
+    // takes every other 16-column chunk (two warps per SM sub-partition, so
+    // one's TMEM / memory latency hides behind the other's arithmetic)
+    const int q = warp & 3, half = (warp - 4) >> 2;
     const int npad = cdiv(p.N, 8) * 8;
     int it = 0;
     for (int w = cid; w < items; w += ncl, ++it) {
@@ -469,104 +484,96 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
       const int m = m0 + h * TG_BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (acc + h) * Cfg::ACC_COLS;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * TG_EC; c < BN; c += 2 * TG_EC) {
         if (n0 + c >= npad) break;
-        // bias first (independent of TMEM), then 32 columns of big + small, one wait
-        float bb[4][8];
+        // bias first (independent of TMEM), then 16 columns of big + small, one wait
+        float bb[2][8];
         if (EP::HAS_BIAS && !p.partial) {
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) p.ep.bias8(n0 + c + 8 * q4, bb[q4]);
+          p.ep.bias8(n0 + c, bb[0]);
+          p.ep.bias8(n0 + c + 8, bb[1]);
         }
-        uint32_t r[32], rs[32], rs2[Cfg::PAIRB ? 32 : 1];
-        tmem_ld16(tbase + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-        tmem_ld16(tbase + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
-        tmem_ld16(tbase + BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&rs[0]));
-        tmem_ld16(tbase + BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs[16]));
-        if constexpr (Cfg::PAIRB) {
-          tmem_ld16(tbase + 2 * BN + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&rs2[0]));
-          tmem_ld16(tbase + 2 * BN + (uint32_t)c + 16, *reinterpret_cast<uint32_t(*)[16]>(&rs2[16]));
-        }
+        uint32_t r[16], rs[16], rs2[16];
+        tmem_ld16(tbase + (uint32_t)c, r);
+        tmem_ld16(tbase + BN + (uint32_t)c, rs);
+        if constexpr (Cfg::PAIRB) tmem_ld16(tbase + 2 * BN + (uint32_t)c, rs2);
         tmem_ld_wait();
-        if constexpr (EP::STAGED) {
-          if (!p.partial && !(p.debug & 1)) {
-            // split planes of 32 rows x 32 columns through shared memory: each
-            // lane writes its row's four 16-byte chunks (chunk slot XOR-swizzled
-            // by row pair, conflict-free), then four lanes store one row's 64
-            // contiguous bytes per plane (8 rows per instruction)
-            const uint32_t sb = epi_smem + (uint32_t)q * Cfg::EPI_WARP_BYTES;
+        float v[2][8];
 #pragma unroll
-            for (int hh = 0; hh < 4; ++hh) {
-              float v[8];
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                float sm = __uint_as_float(rs[8 * hh + jj]);
-                if constexpr (Cfg::PAIRB) sm = __fadd_rn(sm, __uint_as_float(rs2[8 * hh + jj]));
-                v[jj] = __fadd_rn(__uint_as_float(r[8 * hh + jj]), sm);
-                if (EP::HAS_BIAS) v[jj] = __fadd_rn(v[jj], bb[hh][jj]);
-              }
-              p.ep.prep8(n0 + c + 8 * hh, v);
-              uint32_t w0[4], w1[4], w2[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                bf16_t a0, a1, a2, c0, c1, c2;
-                split_bf16x3(v[2 * j], a0, a1, a2);
-                split_bf16x3(v[2 * j + 1], c0, c1, c2);
-                w0[j] = (uint32_t)a0 | ((uint32_t)c0 << 16);
-                w1[j] = (uint32_t)a1 | ((uint32_t)c1 << 16);
-                w2[j] = (uint32_t)a2 | ((uint32_t)c2 << 16);
-              }
-              const uint32_t o = (uint32_t)lane * 64 + (uint32_t)((hh ^ (lane >> 1)) & 3) * 16;
-              sts128u(sb + o, w0[0], w0[1], w0[2], w0[3]);
-              sts128u(sb + 2048 + o, w1[0], w1[1], w1[2], w1[3]);
-              sts128u(sb + 4096 + o, w2[0], w2[1], w2[2], w2[3]);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int rr = 8 * i + (lane >> 2), ch = lane & 3;
-              const uint32_t o = (uint32_t)rr * 64 + (uint32_t)((ch ^ (rr >> 1)) & 3) * 16;
-              const int mrow = m0 + h * TG_BM + q * 32 + rr, nb = n0 + c + 8 * ch;
-              if (mrow < p.M && nb < npad) {
-                uint4 pl[3];
-                pl[0] = lds128(sb + o);
-                pl[1] = lds128(sb + 2048 + o);
-                pl[2] = lds128(sb + 4096 + o);
-                p.ep.store_planes(mrow, nb, pl);
-              }
-            }
-            __syncwarp();
-            continue;
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int nb = n0 + c + 8 * h;
-          if (nb >= npad) break;
-          float v[8];
+        for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
-            float sm = __uint_as_float(rs[8 * h + jj]);
-            if constexpr (Cfg::PAIRB) sm = __fadd_rn(sm, __uint_as_float(rs2[8 * h + jj]));
-            v[jj] = __fadd_rn(__uint_as_float(r[8 * h + jj]), sm);
+            float sm = __uint_as_float(rs[8 * hh + jj]);
+            if constexpr (Cfg::PAIRB) sm = __fadd_rn(sm, __uint_as_float(rs2[8 * hh + jj]));
+            v[hh][jj] = __fadd_rn(__uint_as_float(r[8 * hh + jj]), sm);
           }
-          if (p.debug & 1) {
-            continue;
-          } else if (p.partial) {
-            if (m < p.M) {
+        if (p.debug & 1) continue;
+        if (p.partial) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int nb = n0 + c + 8 * hh;
+            if (m < p.M && nb < npad) {
               float* dst = p.partial + ((size_t)z * p.M + m) * npad + nb;
               if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
-                stg256(dst, v);
+                stg256(dst, v[hh]);
               } else {
-                reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-                reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+                reinterpret_cast<float4*>(dst)[0] = make_float4(v[hh][0], v[hh][1], v[hh][2], v[hh][3]);
+                reinterpret_cast<float4*>(dst)[1] = make_float4(v[hh][4], v[hh][5], v[hh][6], v[hh][7]);
               }
             }
-          } else {
-            if (EP::HAS_BIAS) {
+          }
+          continue;
+        }
+        if (EP::HAS_BIAS) {
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj) v[jj] = __fadd_rn(v[jj], bb[h][jj]);
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) v[hh][jj] = __fadd_rn(v[hh][jj], bb[hh][jj]);
+        }
+        if constexpr (EP::STAGED) {
+          // split planes of 32 rows x 16 columns through shared memory: each
+          // lane writes its row's two 16-byte chunks per plane (slot XOR row
+          // bit 2: conflict-free), then two lanes store one row's 32
+          // contiguous bytes (one full sector) per plane, 16 rows per
+          // instruction
+          const uint32_t sb = epi_smem + (uint32_t)(warp - 4) * Cfg::EPI_WARP_BYTES;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            p.ep.prep8(n0 + c + 8 * hh, v[hh]);
+            uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              bf16_t a0, a1, a2, c0, c1, c2;
+              split_bf16x3(v[hh][2 * j], a0, a1, a2);
+              split_bf16x3(v[hh][2 * j + 1], c0, c1, c2);
+              w0[j] = (uint32_t)a0 | ((uint32_t)c0 << 16);
+              w1[j] = (uint32_t)a1 | ((uint32_t)c1 << 16);
+              w2[j] = (uint32_t)a2 | ((uint32_t)c2 << 16);
             }
-            p.ep.store8_nb(m, nb, v);
+            const uint32_t o = (uint32_t)lane * 32 + (uint32_t)((hh ^ (lane >> 2)) & 1) * 16;
+            sts128u(sb + o, w0[0], w0[1], w0[2], w0[3]);
+            sts128u(sb + 1024 + o, w1[0], w1[1], w1[2], w1[3]);
+            sts128u(sb + 2048 + o, w2[0], w2[1], w2[2], w2[3]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int rr = 16 * i + (lane >> 1), ch = lane & 1;
+            const uint32_t o = (uint32_t)rr * 32 + (uint32_t)((ch ^ (rr >> 2)) & 1) * 16;
+            const int mrow = m0 + h * TG_BM + q * 32 + rr, nb = n0 + c + 8 * ch;
+            if (mrow < p.M && nb < npad) {
+              uint4 pl[3];
+              pl[0] = lds128(sb + o);
+              pl[1] = lds128(sb + 1024 + o);
+              pl[2] = lds128(sb + 2048 + o);
+              p.ep.store_planes(mrow, nb, pl);
+            }
+          }
+          __syncwarp();
+        } else {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int nb = n0 + c + 8 * hh;
+            if (nb < npad) p.ep.store8_nb(m, nb, v[hh]);
           }
         }
       }

@@ -147,6 +147,17 @@ def test_conv_vs_oracle(tc, producer, clusters, shape):
     _conv_case(tc, shape)
 
 
+STRIDED_CONV_SHAPES = [  # input gradient as s*s phase sub-convolutions (O8 % 32 == 0)
+    (2, 64, 56, 56, 128, 3, 2, 1), (2, 32, 15, 15, 64, 3, 2, 1), (1, 32, 14, 13, 96, 5, 2, 2),
+    (2, 64, 17, 17, 32, 3, 2, 0), (1, 48, 20, 20, 64, 7, 3, 3), (2, 32, 11, 11, 64, 2, 2, 0),
+    (1, 32, 10, 10, 64, 2, 3, 0), (1, 40, 23, 23, 64, 7, 2, 3)]
+
+
+@pytest.mark.parametrize("shape", STRIDED_CONV_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_strided_conv_phases_vs_oracle(tc, shape):
+    _conv_case(tc, shape)
+
+
 def _conv_case(tc, shape):
     n, c, h, w, o, k, s, p = shape
     rng = np.random.Generator(np.random.PCG64(hash(shape) & 0xFFFF))
@@ -275,3 +286,32 @@ def test_conv_two_halves(tc, producer, halves, shape):
                          ids=lambda s: "x".join(map(str, s)))
 def test_fc_two_halves(tc, producer, halves, shape):
     _fc_case(tc, shape)
+
+
+@pytest.mark.parametrize("shapes", [
+    [(64, 3, 7, 7, 8, 64), (256, 64, 1, 1, 64, 256), (128, 128, 3, 3, 128, 128)],
+    [(33, 5, 3, 3, 8, 40), (40, 70, 1, 7, 72, 40), (1000, 48, 5, 5, 48, 1000)],
+    [(16, 3, 11, 11, 8, 32), (64, 17, 7, 1, 24, 64)]], ids=["resnet", "ragged", "wide-taps"])
+def test_pack_conv_w_multi_matches_single(lib, shapes):
+    """The tiled multi-job weight pack writes exactly what the per-layer pack
+    writes (forward and flipped input-gradient operands, padded channels 0)."""
+    from paper_1812_10624_b200 import _lib
+    rng = np.random.Generator(np.random.PCG64(len(shapes)))
+    jobs, outs = [], []
+    for o, c, kh, kw, c8, o8 in shapes:
+        w = torch.tensor(rng.standard_normal((o, c, kh, kw)).astype(np.float32), device="cuda")
+        kk = kh * kw
+        wf = torch.full((3, o * kk * c8), 7, dtype=torch.int16, device="cuda")
+        wd = torch.full((3, c * kk * o8), 7, dtype=torch.int16, device="cuda")
+        rf, rd = wf.clone(), wd.clone()
+        _lib.call("stzx_pack_conv2_w", w.data_ptr(), rf.data_ptr(), rf.shape[1], rd.data_ptr(),
+                  rd.shape[1], o, c, kh, kw, c8, o8, None)
+        jobs.append(_lib.ConvPack(w.data_ptr(), wf.data_ptr(), wd.data_ptr(), wf.shape[1],
+                                  wd.shape[1], o, c, kh, kw, c8, o8))
+        outs.append((w, wf, wd, rf, rd))
+    arr = (_lib.ConvPack * len(jobs))(*jobs)
+    _lib.call("stzx_pack_conv_w_multi", arr, len(jobs), None)
+    torch.cuda.synchronize()
+    for w, wf, wd, rf, rd in outs:
+        assert torch.equal(wf, rf)
+        assert torch.equal(wd, rd)
