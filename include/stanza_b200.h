@@ -245,12 +245,15 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
                 int group, float eps, int relu, void* ws, size_t ws_bytes, void* stream);
 /* dgamma / dbeta batch sums (added with `accumulate`), gx nullable; `mask`
  * (nullable): g is the gradient of a ReLU output, masked where plane 0 of
- * `mask` (that output) is not > 0 (a residual block's final ReLU). */
+ * `mask` (that output) is not > 0 (a residual block's final ReLU).
+ * `gbias_in` (nullable, needs gx): the batch sum of gx per channel -- the
+ * gradient of a bias added to x (the producing conv's) -- from the same pass
+ * that writes gx (float64 sums of the fp32 gx values, fixed order). */
 int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size_t psx,
                 const double* stats,
-                const float* gamma, float* ggamma, float* gbeta, int accumulate, void* gx,
-                size_t psgx, int N, int HW, int C, int C8, int group, void* ws, size_t ws_bytes,
-                void* stream);
+                const float* gamma, float* ggamma, float* gbeta, float* gbias_in, int accumulate,
+                void* gx, size_t psgx, int N, int HW, int C, int C8, int group, void* ws,
+                size_t ws_bytes, void* stream);
 /* global average pool NHWC [N][HW][C8] <-> rows [N][C8] (float64 sums / HW) */
 int stzx_gap_fwd(const void* x, size_t psx, void* y, size_t psy, int N, int HW, int C8,
                  void* stream);

@@ -71,7 +71,7 @@ SIGNATURES = {
     "stzx_conv_fwd_s2d": (I, [P, Z, P, Z, P, P, Z, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_conv_wgrad_s2d": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, I, I, I, I, P, Z, P]),
     "stzx_bn_fwd": (I, [P, Z, P, P, P, Z, P, Z, P, I, I, I, I, I, F, I, P, Z, P]),
-    "stzx_bn_bwd": (I, [P, Z, P, P, Z, P, P, P, P, I, P, Z, I, I, I, I, I, P, Z, P]),
+    "stzx_bn_bwd": (I, [P, Z, P, P, Z, P, P, P, P, P, I, P, Z, I, I, I, I, I, P, Z, P]),
     "stzx_gap_fwd": (I, [P, Z, P, Z, I, I, I, P]),
     "stzx_gap_bwd": (I, [P, Z, P, Z, I, I, I, P]),
     "stzx_add": (I, [P, Z, P, Z, P, P, Z, Z, P]),

@@ -1502,10 +1502,11 @@ int stzx_pack_conv_w_multi(const stz_conv_pack* jobs, int n, void* stream) {
   for (int i = 0; i < n; ++i) {
     const stz_conv_pack& q = jobs[i];
     const int kk = q.kh * q.kw;
-    if (!q.w || !q.wf || q.kh < 1 || q.kw < 1 || kk > 288 || q.C8 % 8 || q.O8 % 8 || q.C8 < q.C ||
-        q.O8 < q.O)
+    if (!q.w || !q.wf || q.kh < 1 || q.kw < 1 || kk > kPackSpan / 2 || q.C8 % 8 || q.O8 % 8 ||
+        q.C8 < q.C || q.O8 < q.O || q.psf % 2 || (q.wd && q.psd % 2) ||
+        (reinterpret_cast<uintptr_t>(q.wf) & 3) || (reinterpret_cast<uintptr_t>(q.wd) & 3))
       return fail(STZ_EINVAL, "pack_conv_w_multi: job %d", i);
-    const int cb = std::max(1, std::min(32, 288 / kk));
+    const int cb = std::min(rup8(q.C8), (kPackSpan / kk) & ~1);   // even, >= 2
     const long jt = (long)cdiv(q.O8, 32) * cdiv(q.C8, cb);
     t.j[t.n++] = ConvPackJob{q.w, mb(q.wf), mb(q.wd), q.psf, q.psd, q.O, q.C, kk, q.C8, q.O8, cb,
                              (int)tiles};
@@ -1862,11 +1863,12 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
 
 int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size_t psx,
                 const double* stats,
-                const float* gamma, float* ggamma, float* gbeta, int accumulate, void* gx,
-                size_t psgx, int N, int HW, int C, int C8, int group, void* ws, size_t ws_bytes,
-                void* stream) {
+                const float* gamma, float* ggamma, float* gbeta, float* gbias_in, int accumulate,
+                void* gx, size_t psgx, int N, int HW, int C, int C8, int group, void* ws,
+                size_t ws_bytes, void* stream) {
   if (N <= 0 || HW <= 0 || C <= 0 || C8 < C || C8 % 8 || group <= 0 || N % group)
     return fail(STZ_EINVAL, "bn_bwd: bad shape N=%d HW=%d C=%d C8=%d group=%d", N, HW, C, C8, group);
+  if (gbias_in && !gx) return fail(STZ_EINVAL, "bn_bwd: gbias_in needs gx");
   cudaStream_t st = as_stream(stream);
   const int G = N / group, tiles = cdiv(C8 / 8, 32);
   const size_t grows = (size_t)group * HW;
@@ -1887,9 +1889,15 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
     const uint32_t rows = (uint32_t)N * HW;
     const int aslices = std::max(G, bn_slices(rows, 1, tiles, occ_a, 16));   // slice <= group
     const uint32_t arps = (rows + aslices - 1) / aslices;
+    double* bpart = nullptr;
+    if (gbias_in && !(bpart = cv.take<double>((size_t)aslices * C8)))
+      return fail(STZ_EWORKSPACE, "bn_bwd: workspace too small");
     bn_bwd_apply_kernel<<<dim3(aslices, tiles), 256, 0, st>>>(
-        cb(g), psg, cb(mask), cb(x), psx, coef, mb(gx), psgx, rows, arps,
+        cb(g), psg, cb(mask), cb(x), psx, coef, mb(gx), psgx, bpart, rows, arps,
         FastDiv((uint32_t)grows), C8);
+    if (bpart)
+      colsum_final_kernel<<<cdiv(C, 8), 256, 0, st>>>(bpart, aslices, C, C8, gbias_in,
+                                                      accumulate);
   }
   return check_launch("bn_bwd");
 }

@@ -161,11 +161,11 @@ struct ConvPackJob {
   bf16_t* wd;
   size_t psf, psd;
   int O, C, kk, C8, O8;
-  int cb;          // input channels per tile (32 o x cb c x kk taps staged in shared memory)
+  int cb;          // input channels per tile (even; 32 o x cb c x kk taps staged in shared memory)
   int tile0;       // first tile of this job
 };
 constexpr int kMaxConvPack = 160;
-constexpr int kPackTileWords = 32 * 32 * 9;   // smem budget: 32 o x (cb * kk) <= 288 words per o
+constexpr int kPackSpan = 288;   // cb * kk words per output channel in a tile
 struct ConvPackTable {
   int n, tiles;
   ConvPackJob j[kMaxConvPack];
@@ -174,10 +174,10 @@ struct ConvPackTable {
 // One tile = 32 output channels x cb input channels x all kk taps of one
 // job: read w[o][c0 .. c0+cb)[*] as contiguous runs (coalesced), stage it in
 // shared memory, then write the forward operand wf [O][kk][C8] (c-runs) and
-// the flipped input-gradient operand wd [C][kk][O8] (o-runs) from it.
-// Padded channels are zeros.
+// the flipped input-gradient operand wd [C][kk][O8] (o-runs) from it, two
+// elements per 4-byte store.  Padded channels are zeros.
 __global__ void __launch_bounds__(256) pack_conv_w_multi_kernel(const __grid_constant__ ConvPackTable t) {
-  __shared__ float tile[32 * (288 + 1)];
+  __shared__ float tile[32 * (kPackSpan + 1)];
   int lo = 0, hi = t.n - 1;           // last job with tile0 <= blockIdx.x
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -194,23 +194,26 @@ __global__ void __launch_bounds__(256) pack_conv_w_multi_kernel(const __grid_con
     tile[ol * ld + rem] = (o < J.O && c < J.C) ? __ldg(J.w + ((size_t)o * J.C + c0) * kk + rem) : 0.f;
   }
   __syncthreads();
-  // wf[o][tap][c], c fastest
-  for (int idx = threadIdx.x; idx < 32 * span; idx += blockDim.x) {
-    const int ol = idx / span, rem = idx - ol * span;
-    const int tap = rem / cb, cl = rem - tap * cb;
+  // wf[o][tap][c], c fastest, pairs (c, c+1): C8, c0 and cb are even
+  const int hb = cb >> 1;
+  for (int idx = threadIdx.x; idx < 32 * kk * hb; idx += blockDim.x) {
+    const int ol = idx / (kk * hb), rem = idx - ol * kk * hb;
+    const int tap = rem / hb, cl = 2 * (rem - tap * hb);
     const int o = o0 + ol, c = c0 + cl;
     if (o < J.O && c < J.C8)
-      store_split(J.wf, J.psf, ((size_t)o * kk + tap) * J.C8 + c, tile[ol * ld + cl * kk + tap]);
+      store_split2(J.wf, J.psf, ((size_t)o * kk + tap) * J.C8 + c, tile[ol * ld + cl * kk + tap],
+                   tile[ol * ld + (cl + 1) * kk + tap]);
   }
   if (!J.wd) return;
-  // wd[c][tt][o], o fastest, tap = kk - 1 - tt (both tap axes flipped)
-  for (int idx = threadIdx.x; idx < 32 * span; idx += blockDim.x) {
-    const int cl = idx / (32 * kk), rem = idx - cl * 32 * kk;
-    const int tt = rem >> 5, ol = rem & 31;
+  // wd[c][tt][o], o fastest, pairs (o, o+1), tap = kk - 1 - tt (both tap axes flipped)
+  for (int idx = threadIdx.x; idx < 16 * span; idx += blockDim.x) {
+    const int cl = idx / (16 * kk), rem = idx - cl * 16 * kk;
+    const int tt = rem >> 4, ol = 2 * (rem & 15);
     const int o = o0 + ol, c = c0 + cl;
+    const int src = cl * kk + (kk - 1 - tt);
     if (c < J.C && o < J.O8)
-      store_split(J.wd, J.psd, ((size_t)c * kk + tt) * J.O8 + o,
-                  tile[ol * ld + cl * kk + (kk - 1 - tt)]);
+      store_split2(J.wd, J.psd, ((size_t)c * kk + tt) * J.O8 + o, tile[ol * ld + src],
+                   tile[(ol + 1) * ld + src]);
   }
 }
 
@@ -761,7 +764,15 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const double* __restr
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= N) return;
   double s = 0.0;
-  for (int b = lane; b < blocks; b += 32) s += part[(size_t)b * N8 + c];
+  int b = lane;
+  for (; b + 96 < blocks; b += 128) {   // four blocks' loads in flight per step
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = part[(size_t)(b + 32 * u) * N8 + c];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += v[u];
+  }
+  for (; b < blocks; b += 32) s += part[(size_t)b * N8 + c];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[c] = accumulate ? __fadd_rn(out[c], (float)s) : (float)s;
 }

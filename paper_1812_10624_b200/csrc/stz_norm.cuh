@@ -101,6 +101,28 @@ __global__ void __launch_bounds__(256, 2) bn_reduce_kernel(
   }
 }
 
+// lane's share of a (sum, sum2) pair column: slices lane, lane + 32, ... in
+// order, four slices' loads in flight per step
+__device__ __forceinline__ void bn_sum_slices(const double* __restrict__ p, size_t stride,
+                                              int nslices, int lane, double& s, double& q) {
+  int k = lane;
+  for (; k + 96 < nslices; k += 128) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double2*>(p + (size_t)(k + 32 * u) * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s += v[u].x;
+      q += v[u].y;
+    }
+  }
+  for (; k < nslices; k += 32) {
+    const double2 v = *reinterpret_cast<const double2*>(p + (size_t)k * stride);
+    s += v.x;
+    q += v.y;
+  }
+}
+
 // forward finalize: per (group, channel) mean and rstd = 1/sqrt(var + eps),
 // var = E[x^2] - mean^2 (float64; clamped at 0), kept in `stats` for the
 // backward; and the apply pass's affine form y = x*A + B, A = rstd*gamma,
@@ -115,10 +137,7 @@ __global__ void bn_stats_final_kernel(const double* __restrict__ partial, double
   if (i >= G * C8) return;
   const int gi = i / C8, c = i % C8;
   double s = 0.0, q = 0.0;
-  for (int k = lane; k < nslices; k += 32) {
-    s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
-    q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
-  }
+  bn_sum_slices(partial + ((size_t)gi * nslices * C8 + c) * 2, (size_t)C8 * 2, nslices, lane, s, q);
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, o);
     q += __shfl_xor_sync(0xffffffffu, q, o);
@@ -149,10 +168,8 @@ __global__ void bn_bwd_final_kernel(const double* __restrict__ partial,
   double tg = 0.0, tgx = 0.0;
   for (int gi = 0; gi < G; ++gi) {
     double s = 0.0, q = 0.0;
-    for (int k = lane; k < nslices; k += 32) {
-      s += partial[(((size_t)gi * nslices + k) * C8 + c) * 2];
-      q += partial[(((size_t)gi * nslices + k) * C8 + c) * 2 + 1];
-    }
+    bn_sum_slices(partial + ((size_t)gi * nslices * C8 + c) * 2, (size_t)C8 * 2, nslices, lane, s,
+                  q);
     for (int o = 16; o > 0; o >>= 1) {
       s += __shfl_xor_sync(0xffffffffu, s, o);
       q += __shfl_xor_sync(0xffffffffu, q, o);
@@ -246,19 +263,26 @@ __global__ void __launch_bounds__(256, 2) bn_apply_kernel(
 __global__ void __launch_bounds__(256, 2) bn_bwd_apply_kernel(
     const bf16_t* __restrict__ g, size_t psg, const bf16_t* __restrict__ mask,
     const bf16_t* __restrict__ x, size_t psx, const double4* __restrict__ coef,
-    bf16_t* __restrict__ gx, size_t psgx, uint32_t rows, uint32_t rows_per_slice,
-    FastDiv d_grows, int C8) {
+    bf16_t* __restrict__ gx, size_t psgx, double* __restrict__ bpart, uint32_t rows,
+    uint32_t rows_per_slice, FastDiv d_grows, int C8) {
   __shared__ double sc[2 * 3 * 8 * 32];
+  __shared__ double red[256 * 8];
   const int nch = C8 / 8, ct = blockIdx.y;
   const int L = min(nch - ct * 32, 32), R = 256 / L;
   const int t = threadIdx.x, cl = t % L, rl = t / L;
   const int cc = ct * 32 + cl;
   const uint32_t r0 = blockIdx.x * rows_per_slice, r1 = min(rows, r0 + rows_per_slice);
-  if (r0 >= r1) return;
+  if (r0 >= r1) {   // an empty trailing slice still owns its partials
+    if (bpart)
+      for (int e = t; e < L * 8; e += 256) bpart[(size_t)blockIdx.x * C8 + ct * 256 + e] = 0.0;
+    return;
+  }
   const uint32_t g_lo = d_grows.div(r0), ng = d_grows.div(r1 - 1) - g_lo + 1;   // <= 2
   bn_stage_coef<3>(sc, coef, (int)g_lo, (int)ng, C8, ct, L);
   __syncthreads();
-  if (rl >= R) return;
+  double bs[8];   // batch sums of this thread's gx values (the input bias gradient)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bs[j] = 0.0;
   auto row = [&](uint32_t r, float (&v)[8], const float (&gv)[8]) {
     const uint32_t gg = d_grows.div(r) - g_lo;
 #pragma unroll
@@ -267,10 +291,11 @@ __global__ void __launch_bounds__(256, 2) bn_bwd_apply_kernel(
       const double Q = sc[((gg * 3 + 1) * 8 + j) * 32 + cl];
       const double Rc = sc[((gg * 3 + 2) * 8 + j) * 32 + cl];
       v[j] = (float)fma(P, (double)gv[j], fma(Q, (double)v[j], Rc));
+      bs[j] += (double)v[j];
     }
     store_split8(gx + (size_t)r * C8 + cc * 8, psgx, v);
   };
-  uint32_t r = r0 + rl;
+  uint32_t r = rl < R ? r0 + rl : r1;
   for (; r + (BN_APPLY_U - 1) * (uint32_t)R < r1; r += BN_APPLY_U * (uint32_t)R) {
     float v[BN_APPLY_U][8], gv[BN_APPLY_U][8];
 #pragma unroll
@@ -290,6 +315,17 @@ __global__ void __launch_bounds__(256, 2) bn_bwd_apply_kernel(
     load_split8(g + off, psg, gv);
     if (mask) apply_mask8(mask + off, gv);
     row(r, v, gv);
+  }
+  if (!bpart) return;
+  // fixed-order sum over the row lanes -> bpart[slice][c]
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[t * 8 + j] = bs[j];
+  __syncthreads();
+  for (int e = t; e < L * 8; e += 256) {
+    const int lane = e >> 3, j = e & 7;
+    double acc = 0.0;
+    for (int q = 0; q < R; ++q) acc += red[(q * L + lane) * 8 + j];
+    bpart[(size_t)blockIdx.x * C8 + (ct * 32 + lane) * 8 + j] = acc;
   }
 }
 

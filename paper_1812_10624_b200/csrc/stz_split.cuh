@@ -47,6 +47,16 @@ __device__ __forceinline__ void store_split(bf16_t* p, size_t ps, size_t i, floa
   p[i + 2 * ps] = c;
 }
 
+// 2 consecutive values -> one 4-byte store per plane (p + i 4-byte aligned, ps even)
+__device__ __forceinline__ void store_split2(bf16_t* p, size_t ps, size_t i, float x, float y) {
+  bf16_t a0, a1, a2, b0, b1, b2;
+  split_bf16x3(x, a0, a1, a2);
+  split_bf16x3(y, b0, b1, b2);
+  *reinterpret_cast<uint32_t*>(p + i) = (uint32_t)a0 | ((uint32_t)b0 << 16);
+  *reinterpret_cast<uint32_t*>(p + i + ps) = (uint32_t)a1 | ((uint32_t)b1 << 16);
+  *reinterpret_cast<uint32_t*>(p + i + 2 * ps) = (uint32_t)a2 | ((uint32_t)b2 << 16);
+}
+
 // 8 consecutive values -> one 16-byte store per plane (dst 16-byte aligned)
 __device__ __forceinline__ void store_split8(bf16_t* p, size_t ps, const float (&v)[8]) {
   uint32_t w0[4], w1[4], w2[4];

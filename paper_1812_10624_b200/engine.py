@@ -112,6 +112,7 @@ class _Op:
     skip_dgrad: bool = False
     flat_out: bool = False    # maxpool: writes the CHW-flat tensor for a following Flatten
     s2d: tuple | None = None  # first strided conv as space-to-depth: (ks, Cs8, Hs, Ws)
+    bias_by_bn: bool = False  # conv: the following BatchNorm's backward sums its bias gradient
 
 
 class BlockEngine:
@@ -179,6 +180,9 @@ class BlockEngine:
                 ops[i - 1].fused_relu = True
             if op.kind == "flatten" and i > 0 and ops[i - 1].kind in ("maxpool", "gap"):
                 ops[i - 1].flat_out = True      # gap: (C,1,1) NHWC is the flat row already
+        for i, op in enumerate(ops):
+            if op.kind == "bn" and i > 0 and ops[i - 1].kind == "conv":
+                ops[i - 1].bias_by_bn = True     # gx of that BatchNorm is the conv's output grad
         for i, op in enumerate(ops):
             if op.kind != "relu":
                 continue
@@ -727,10 +731,12 @@ class BlockEngine:
                 c, h, w = op.in_shape
                 out = None if op.skip_dgrad else V(self.gin[i])
                 m = V(gy_mask) if (gy_mask is not None and i == len(self.ops) - 1) else None
+                gbias = ptr(self.grads[i - 1][1]) if (
+                    out is not None and i > 0 and self.ops[i - 1].bias_by_bn) else None
                 _lib.call("stzx_bn_bwd", g.ptr(), g.ps, None if m is None else m.ptr(),
                           xin.ptr(), xin.ps,
                           ptr(self.bnstats[i][r0 // self.group:]), ptr(self.params[i][0]),
-                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc,
+                          ptr(self.grads[i][0]), ptr(self.grads[i][1]), gbias, acc,
                           None if out is None else out.ptr(), 0 if out is None else out.ps,
                           b, h * w, c, xin.width, self.group, ptr(ws), ws.numel(), st,
                           tag=f"{self.tag}bn{i}_bwd",
@@ -859,13 +865,15 @@ class BlockEngine:
         if op.kind == "conv" and op.s2d is not None:
             ks, cs8, hs, ws_ = op.s2d
             _lib.call("stzx_conv_wgrad_s2d", xin.ptr(), xin.ps, g.ptr(), g.ps,
-                      ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_ch, cs8,
+                      ptr(self.grads[i][0]), None if op.bias_by_bn else ptr(self.grads[i][1]),
+                      acc, b, l.in_ch, cs8,
                       hs, ws_, l.out_ch, g.width, l.kernel, l.stride, ptr(ws), ws.numel(), st,
                       flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         elif op.kind == "conv":
             c, h, w = op.in_shape
+            gb = None if op.bias_by_bn else ptr(self.grads[i][1])   # summed by the BN backward
             _lib.call("stzx_conv2_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
-                      ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, c, xin.width, h,
+                      ptr(self.grads[i][0]), gb, acc, b, c, xin.width, h,
                       w, l.out_ch, g.width, l.kh, l.kw, l.stride, l.ph, l.pw, ptr(ws),
                       ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         else:
