@@ -31,6 +31,7 @@ SIGNATURES = {
     "stz_set_debug": (I, [I]),
     "stz_set_tile": (I, [I, I, I]),
     "stz_set_band": (I, [I]),
+    "stz_set_fixup": (I, [I]),
     "stz_set_mh": (I, [I]),
     "stz_launch_count": (ctypes.c_ulonglong, []),
     "stz_conv2d_fwd": (I, [P, P, P, P, I, I, I, I, I, I, I, I, I, P, Z, P]),
@@ -169,6 +170,8 @@ def load(path: str | None = None):
         fn.argtypes = args
     if os.environ.get("STZ_BAND"):          # experiments: shifted-window kernel selection
         lib.stz_set_band(int(os.environ["STZ_BAND"]))
+    if os.environ.get("STZ_FIXUP"):         # experiments: split-K in-kernel fixup on / off
+        lib.stz_set_fixup(int(os.environ["STZ_FIXUP"]))
     _lib = lib
     return lib
 

@@ -919,6 +919,38 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   return check_launch("bandw_reduce");
 }
 
+// Split-K fixup counters: one zeroed region per workspace (split GEMMs that
+// may run concurrently never share a workspace -- their partials live in it),
+// allocated on the workspace's first split GEMM outside stream capture and
+// kept zero by the kernels between launches.  nullptr (-> separate reduce
+// pass) when the region would be too small, the workspace is first seen
+// while capturing, or stz_set_fixup(0).
+int g_fixup = 1;
+constexpr int kSemInts = 1 << 15;
+int* split_sems(const void* ws, cudaStream_t st, int n) {
+  if (n > kSemInts || !ws) return nullptr;
+  static std::vector<std::pair<std::pair<int, const void*>, int*>> regions;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  for (auto& r : regions)
+    if (r.first.first == dev && r.first.second == ws) return r.second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return nullptr;
+  int* p = nullptr;
+  if (cudaMalloc(&p, kSemInts * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaMemsetAsync(p, 0, kSemInts * sizeof(int), st) != cudaSuccess) {
+    cudaFree(p);
+    cudaGetLastError();
+    return nullptr;
+  }
+  regions.push_back({{dev, ws}, p});
+  return p;
+}
+
 // C[M,N] = A . B with TMA operands built for tile width BN
 template <class EP>
 int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand& b, const EP& ep,
@@ -942,6 +974,11 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   prm.b = b;
   prm.ep = ep;
   prm.partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
+  // in-kernel fixup only when the sums spread over the GPU: the last split of
+  // each tile reads all its partials, so few tiles x many splits (weight
+  // gradients: 7 tiles x 31 splits) would serialise on a few SMs
+  const bool fix = splits > 1 && splits <= 4 && tiles * CL >= num_sms() && g_fixup;
+  prm.sem = fix ? split_sems(ws, st, tiles * CL) : nullptr;
   prm.M = M;
   prm.N = N;
   prm.K = K;
@@ -968,7 +1005,7 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   else return fail(STZ_EINVAL, "%s: no kernel for tile %d x %d", what, BN, CL);
   int rc = check_launch(what);
   if (rc) return rc;
-  if (splits > 1) {
+  if (splits > 1 && !prm.sem) {
     launch_reduce(prm.partial, splits, M, N, ep, st);
     rc = check_launch("tgemm_reduce");
   }
@@ -1163,7 +1200,7 @@ int colsum_split(const bf16_t* g, size_t ps, int R, int N, int ld, float* out, v
   const int N8 = rup8(N);
   const int chunks = N8 / 8;
   const int lanes = chunks < 256 ? 256 / chunks : 1;
-  int rpb = cdiv(R, 4 * num_sms());
+  int rpb = cdiv(R, 2 * num_sms());   // ~2 partial rows per SM: a short final
   rpb = cdiv(rpb < 4 * lanes ? 4 * lanes : rpb, lanes) * lanes;
   const int blocks = cdiv(R, rpb);
   Carve cv(ws, ws_bytes);
@@ -1203,6 +1240,11 @@ int stz_set_mh(int mode) {
 
 int stz_set_cluster(int on) {
   g_use_cluster = on ? 1 : 0;
+  return STZ_OK;
+}
+
+int stz_set_fixup(int on) {
+  g_fixup = on ? 1 : 0;
   return STZ_OK;
 }
 

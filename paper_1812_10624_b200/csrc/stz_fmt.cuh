@@ -765,12 +765,12 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const double* __restr
   if (c >= N) return;
   double s = 0.0;
   int b = lane;
-  for (; b + 96 < blocks; b += 128) {   // four blocks' loads in flight per step
-    double v[4];
+  for (; b + 224 < blocks; b += 256) {   // eight blocks' loads in flight per step
+    double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = part[(size_t)(b + 32 * u) * N8 + c];
+    for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(b + 32 * u) * N8 + c];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s += v[u];
+    for (int u = 0; u < 8; ++u) s += v[u];
   }
   for (; b < blocks; b += 32) s += part[(size_t)b * N8 + c];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

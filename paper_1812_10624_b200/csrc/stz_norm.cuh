@@ -102,16 +102,16 @@ __global__ void __launch_bounds__(256, 2) bn_reduce_kernel(
 }
 
 // lane's share of a (sum, sum2) pair column: slices lane, lane + 32, ... in
-// order, four slices' loads in flight per step
+// order, eight slices' loads in flight per step (the finals are latency-bound)
 __device__ __forceinline__ void bn_sum_slices(const double* __restrict__ p, size_t stride,
                                               int nslices, int lane, double& s, double& q) {
   int k = lane;
-  for (; k + 96 < nslices; k += 128) {
-    double2 v[4];
+  for (; k + 224 < nslices; k += 256) {
+    double2 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double2*>(p + (size_t)(k + 32 * u) * stride);
+    for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const double2*>(p + (size_t)(k + 32 * u) * stride);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       s += v[u].x;
       q += v[u].y;
     }
@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(256) avgpool_bwd_kernel(const bf16_t* __restri
                                                           int OW, int k, int s, int p) {
   const int nch = C8 / 8;
   const double kk = (double)(k * k);
+  const double rk = 1.0 / kk;   // RN(1/kk)
   STZ_GRID_LOOP(i, (size_t)N * H * W * nch) {
     const int cc = (int)(i % nch);
     const size_t pix = i / nch;
@@ -454,7 +455,14 @@ __global__ void __launch_bounds__(256) avgpool_bwd_kernel(const bf16_t* __restri
         float v[8];
         load_split8(gy + ((n * OH + oh) * OW + ow) * C8 + (size_t)cc * 8, psg, v);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += __ddiv_rn((double)v[j], kk);
+        for (int j = 0; j < 8; ++j) {
+          // v / kk correctly rounded without a division: q0 = RN(v * RN(1/kk)) is
+          // faithful, the remainder v - q0*kk is exact (fma), and one
+          // correction step RN(q0 + r * RN(1/kk)) is the correctly rounded
+          // quotient (Markstein) -- the same double as __ddiv_rn
+          const double x = (double)v[j], q0 = x * rk, r = fma(-q0, kk, x);
+          acc[j] += fma(r, rk, q0);
+        }
       }
     }
     float o[8];

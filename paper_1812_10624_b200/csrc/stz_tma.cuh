@@ -55,6 +55,10 @@ struct alignas(64) TgParams {
   TgOperand a, b;
   EP ep;
   float* partial;
+  // split-K fixup counters (one per 128-row half tile, zero between launches):
+  // the last split of a tile to finish sums every split's partial in split
+  // order and applies the epilogue, so no separate reduce pass runs
+  int* sem;
   int M, N, K, k_per_split;
   int debug;  // bench/diagnostics only: 1 skip epilogue stores, 2 skip MMAs, 4 skip TMA loads
 };
@@ -583,6 +587,64 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
       if (lane == 0) {
         if (CL == 2) mbar_arrive_leader(&tempty_bar[acc]);
         else mbar_arrive(&tempty_bar[acc]);
+      }
+      if (p.partial && p.sem && !(p.debug & 1)) {
+        // split-K fixup: publish this split's partial, count it; the tile's
+        // last split reads all partials back (L2) and runs the epilogue
+        __shared__ int s_last;
+        const int splits = cdiv(p.K, p.k_per_split);
+        int* cnt = p.sem + rem * CL + rank;
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 4 && lane == 0) s_last = atomicAdd(cnt, 1) == splits - 1;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          const size_t zs = (size_t)p.M * npad;
+#pragma unroll 1
+          for (int h = 0; h < MH; ++h) {
+            const int m = m0 + h * TG_BM + q * 32 + lane;
+#pragma unroll 1
+            for (int c = half * TG_EC; c < BN; c += 2 * TG_EC) {
+              if (n0 + c >= npad) break;
+              // 16 columns x 4 splits of loads in flight per step, adds in split order
+              const int nb = n0 + c;
+              if (m >= p.M) continue;
+              const bool two = nb + 8 < npad;
+              const float* src = p.partial + (size_t)m * npad + nb;
+              float v[2][8];
+              for (int z0 = 0; z0 < splits; z0 += 4) {
+                float4 ld[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if (z0 + u < splits) {
+                    const float4* q4 = reinterpret_cast<const float4*>(src + (size_t)(z0 + u) * zs);
+                    ld[u][0] = __ldcg(q4);
+                    ld[u][1] = __ldcg(q4 + 1);
+                    ld[u][2] = two ? __ldcg(q4 + 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    ld[u][3] = two ? __ldcg(q4 + 3) : make_float4(0.f, 0.f, 0.f, 0.f);
+                  }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if (z0 + u >= splits) break;
+                  const float w[2][8] = {{ld[u][0].x, ld[u][0].y, ld[u][0].z, ld[u][0].w,
+                                          ld[u][1].x, ld[u][1].y, ld[u][1].z, ld[u][1].w},
+                                         {ld[u][2].x, ld[u][2].y, ld[u][2].z, ld[u][2].w,
+                                          ld[u][3].x, ld[u][3].y, ld[u][3].z, ld[u][3].w}};
+#pragma unroll
+                  for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      v[hh][j] = (z0 + u == 0) ? w[hh][j] : __fadd_rn(v[hh][j], w[hh][j]);
+                }
+              }
+              p.ep.store8(m, nb, v[0]);
+              if (two) p.ep.store8(m, nb + 8, v[1]);
+            }
+          }
+          if (warp == 4 && lane == 0) *cnt = 0;   // re-armed for the next launch
+        }
       }
     }
   }

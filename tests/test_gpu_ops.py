@@ -230,16 +230,24 @@ def tile(request, lib):
     lib.stz_set_tile(0, 0, 0)
 
 
+@pytest.fixture(params=[1, 0], ids=["fixup", "reduce-pass"])
+def fixup(request, lib):
+    """Split-K sums in the GEMM (last split of each tile) or in a separate pass."""
+    lib.stz_set_fixup(request.param)
+    yield request.param
+    lib.stz_set_fixup(1)
+
+
 @pytest.mark.parametrize("shape", [(300, 640, 1000), (896, 1024, 384), (257, 200, 96)],
                          ids=lambda s: "x".join(map(str, s)))
-def test_fc_every_tile_config(tc, tile, shape):
+def test_fc_every_tile_config(tc, tile, fixup, shape):
     _fc_case(tc, shape)
 
 
 @pytest.mark.parametrize("shape", [(2, 64, 13, 13, 384, 3, 1, 1), (3, 96, 9, 9, 256, 3, 1, 1),
                                    (2, 32, 15, 15, 192, 5, 1, 2)],
                          ids=lambda s: "x".join(map(str, s)))
-def test_conv_every_tile_config(tc, tile, shape):
+def test_conv_every_tile_config(tc, tile, fixup, shape):
     _conv_case(tc, shape)
 
 
