@@ -61,8 +61,9 @@ int stz_set_cluster(int on);
  * (measured slower, kept for coverage); 0: the im2col TMA GEMM.  The GPU
  * tests run all three. */
 int stz_set_band(int on);
-/* split-K GEMMs: 1 (default) the last split of each tile reduces in-kernel,
- * 0 a separate reduce pass (tests compare both) */
+/* split-K GEMMs: 1 the last split of each tile reduces in-kernel (when the
+ * tiles cover the GPU and splits <= 4), 0 (default) a separate reduce pass;
+ * tests compare both */
 int stz_set_fixup(int on);
 
 /* Force the TMA GEMM tile (tests / tuning): width bn in {64, 96, 128, 192,

@@ -924,8 +924,11 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
 // allocated on the workspace's first split GEMM outside stream capture and
 // kept zero by the kernels between launches.  nullptr (-> separate reduce
 // pass) when the region would be too small, the workspace is first seen
-// while capturing, or stz_set_fixup(0).
-int g_fixup = 1;
+// while capturing, or stz_set_fixup(0).  Off by default: measured slower than
+// the separate reduce pass on the model steps (AlexNet 3.67 vs 3.50 ms,
+// ResNet-50 equal): the sums land on each tile's last CTA instead of the
+// whole GPU.
+int g_fixup = 0;
 constexpr int kSemInts = 1 << 15;
 int* split_sems(const void* ws, cudaStream_t st, int n) {
   if (n > kSemInts || !ws) return nullptr;

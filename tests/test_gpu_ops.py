@@ -235,7 +235,7 @@ def fixup(request, lib):
     """Split-K sums in the GEMM (last split of each tile) or in a separate pass."""
     lib.stz_set_fixup(request.param)
     yield request.param
-    lib.stz_set_fixup(1)
+    lib.stz_set_fixup(0)
 
 
 @pytest.mark.parametrize("shape", [(300, 640, 1000), (896, 1024, 384), (257, 200, 96)],
