@@ -206,6 +206,21 @@ int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx
 int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
                   int accumulate, int M, int in_dim, int in8, int out_dim, int out8, void* ws,
                   size_t ws_bytes, void* stream);
+
+/* stzx_fc_wgrad fused with the momentum step when one FC worker owns the
+ * layer: the weight gradient of W [in][out] is consumed in the
+ * GEMM epilogue -- w / v (fp32 [in][out], 16-byte aligned) get
+ * tensor_core.py:366-388's update (v = mu*v + g*inv_n; w -= lr*v) and the
+ * split-plane GEMM copy `planes` ([in][out8], psw elements apart) is
+ * rewritten; gW is never stored.  accumulate = 1 adds the earlier
+ * micro-batches' sum held in gw first.  With wb != NULL the bias gradient
+ * (column sums of g, written to gb) updates (wb, vb) the same way.  The
+ * flat-block update then skips these ranges (stz_plane_range with
+ * planes == NULL and D == 0). */
+int stzx_fc_wgrad_sgd(const void* x, size_t psx, const void* g, size_t psg, float* w, float* v,
+                      void* planes, size_t psw, float* wb, float* vb, float* gw, float* gb,
+                      int accumulate, int M, int in_dim, int in8, int out_dim, int out8, float lr,
+                      float mu, float inv_n, void* ws, size_t ws_bytes, void* stream);
 /* MaxPool2d (tensor_core.py:183-198 / :263-276); flat_ld > 0 selects the
  * CHW-flat [N][flat_ld] layout for y / gy (the FC-block boundary). */
 int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
@@ -364,7 +379,8 @@ int stz_peer_reduce_push(const float* const* grads, float* const* red, int nrank
 
 /* A slice [off, off+len) of the flat parameter vector whose split-plane GEMM
  * copy is a row-major [len/D][D8] matrix (FC W [in][out8], planes ps
- * elements apart); off % 4 == 0. */
+ * elements apart); off % 4 == 0.  planes == NULL with D == 0 marks a slice
+ * that the update skips (already updated by stzx_fc_wgrad_sgd). */
 typedef struct {
   size_t off, len;
   void* planes;

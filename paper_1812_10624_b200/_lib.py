@@ -62,6 +62,8 @@ SIGNATURES = {
     "stzx_fc_fwd": (I, [P, Z, P, Z, P, P, Z, P, I, I, I, I, I, I, P, Z, P]),
     "stzx_fc_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, P, Z, P]),
     "stzx_fc_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, P, Z, P]),
+    "stzx_fc_wgrad_sgd": (I, [P, Z, P, Z, P, P, P, Z, P, P, P, P, I, I, I, I, I, I, F, F, F,
+                              P, Z, P]),
     "stzx_maxpool_fwd": (I, [P, Z, P, Z, P, I, I, I, I, I, I, I, I, P]),
     "stzx_maxpool_bwd": (I, [P, Z, P, P, Z, P, I, I, I, I, I, I, I, I, P]),
     "stzx_relu_fwd": (I, [P, Z, P, Z, Z, P]),

@@ -1216,6 +1216,78 @@ int colsum_split(const bf16_t* g, size_t ps, int R, int N, int ld, float* out, v
   return check_launch("colsum_final");
 }
 
+
+// One-launch BatchNorm (stz_norm.cuh bn_fused_kernel): on unless STZ_BN_FUSED=0.
+// Returns 1 when the grid cannot be co-resident (caller uses the three-launch
+// path), else a status.
+int g_bn_fused = -1;
+bool bn_fused_on() {
+  if (g_bn_fused < 0) {
+    const char* e = getenv("STZ_BN_FUSED");
+    g_bn_fused = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_bn_fused == 1;
+}
+
+template <bool BWD>
+int bn_fused_launch(BnFusedParams& p, int nch, Carve& cv, bool want_bpart, cudaStream_t st,
+                    const char* what) {
+  constexpr int kMaxDyn = 200 * 1024;
+  const int nops = BWD ? 2 : 1;
+  const size_t per_k = (size_t)BNF_THREADS * 32 * nops;   // cache bytes per row step
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(bn_fused_kernel<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxDyn) != cudaSuccess)
+      return fail(STZ_ECUDA, "%s: smem attribute", what);
+    attr = true;
+  }
+  const int tiles = p.tiles, G = p.G;
+  const int r_min = BNF_THREADS / std::min(32, nch);   // row lanes of the widest tile
+  int nb = 0, dyn = 0;
+  for (int per_sm = 2; per_sm >= 1 && !nb; --per_sm) {
+    const long cap = (long)per_sm * num_sms();
+    if ((long)G * tiles > cap) continue;
+    const long spg = std::max(1L, std::min(cap / ((long)G * tiles), (long)((p.grows + 15) / 16)));
+    const int rps = (int)((p.grows + spg - 1) / spg);
+    const int kneed = cdiv(rps, r_min);
+    const int kcap = (int)std::min<size_t>((size_t)kneed, kMaxDyn / per_k);
+    const int d = (int)(kcap * per_k);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bn_fused_kernel<BWD>, BNF_THREADS, d) !=
+        cudaSuccess)
+      return fail(STZ_ECUDA, "%s: occupancy", what);
+    if (occ < per_sm) continue;
+    // the largest tensors (ResNet-50's stem and first stage at K = 32), mostly
+    // beyond the cache, stream better through the three-launch path (its
+    // passes run at higher occupancy; measured, profiles/r02/bn_fused)
+    const double bytes = (double)p.grows * G * p.C8 * 6.0 * nops;
+    if (kcap * 2 < kneed && bytes > 128e6) return 1;
+    p.spg = (int)spg;
+    p.rps = rps;
+    p.kcap = kcap;
+    nb = G * tiles * (int)spg;
+    dyn = d;
+  }
+  if (!nb) return 1;
+  if (!(p.partial = cv.take<double>((size_t)G * p.spg * p.C8 * 2)))
+    return fail(STZ_EWORKSPACE, "%s: workspace too small", what);
+  if (want_bpart && !(p.bpart = cv.take<double>((size_t)G * p.spg * p.C8)))
+    return fail(STZ_EWORKSPACE, "%s: workspace too small", what);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(BNF_THREADS);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, bn_fused_kernel<BWD>, p);
+  if (e != cudaSuccess) return fail(STZ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return check_launch(what);
+}
 }  // namespace
 
 // ===========================================================================
@@ -1759,6 +1831,36 @@ int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx
                        as_stream(stream));
 }
 
+int stzx_fc_wgrad_sgd(const void* x, size_t psx, const void* g, size_t psg, float* w, float* v,
+                      void* planes, size_t psw, float* wb, float* vb, float* gw, float* gb,
+                      int accumulate, int M, int in_dim, int in8, int out_dim, int out8, float lr,
+                      float mu, float inv_n, void* ws, size_t ws_bytes, void* stream) {
+  if (in8 % 8 || out8 % 8 || !w || !v || !planes || (accumulate && !gw) || (wb && (!vb || !gb)))
+    return fail(STZ_EINVAL, "fc_wgrad_sgd: bad arguments");
+  if (!aligned16(w) || !aligned16(v) || !aligned16(planes) || psw % 8)
+    return fail(STZ_EINVAL, "fc_wgrad_sgd: w, v, planes must be 16-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  EpSgd e{w, v, accumulate ? gw : nullptr, mb(planes), psw, in_dim, out_dim, out8, lr, mu, inv_n};
+  int rc = gemm_fc_wgrad(cb(x), psx, cb(g), psg, e, M, in_dim, in8, out_dim, out8, ws, ws_bytes,
+                         st);
+  if (rc || !wb) return rc;
+  // bias: fixed-order column sums of g, then the momentum step on (wb, vb)
+  const int N8 = rup8(out_dim), chunks = N8 / 8;
+  const int lanes = chunks < 256 ? 256 / chunks : 1;
+  int rpb = cdiv(M, 2 * num_sms());
+  rpb = cdiv(rpb < 4 * lanes ? 4 * lanes : rpb, lanes) * lanes;
+  const int blocks = cdiv(M, rpb);
+  Carve cv(ws, ws_bytes);
+  double* part = cv.take<double>((size_t)blocks * N8);
+  if (!part) return fail(STZ_EWORKSPACE, "fc_wgrad_sgd: workspace too small");
+  colsum_partial_kernel<<<blocks, 256, 0, st>>>(cb(g), psg, M, N8, out8, rpb, part);
+  if ((rc = check_launch("colsum_partial"))) return rc;
+  colsum_sgd_final_kernel<<<cdiv(out_dim, 8), 256, 0, st>>>(part, blocks, out_dim, N8, gb,
+                                                            accumulate ? gb : nullptr, wb, vb, lr,
+                                                            mu, inv_n);
+  return check_launch("colsum_sgd_final");
+}
+
 int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* gw, float* gb,
                   int accumulate, int M, int in_dim, int in8, int out_dim, int out8, void* ws,
                   size_t ws_bytes, void* stream) {
@@ -1873,6 +1975,7 @@ int bn_slices(size_t grows, int G, int tiles, int per_sm, int min_rows = 64) {
   const long cap = std::max(1L, (long)((grows + min_rows - 1) / min_rows));
   return (int)std::min(want, cap);
 }
+
 }  // namespace
 
 int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta, const void* res,
@@ -1888,6 +1991,16 @@ int stzx_bn_fwd(const void* x, size_t psx, const float* gamma, const float* beta
   const int rps = (int)((grows + slices - 1) / slices);
   const size_t total = (size_t)N * HW * (C8 / 8);
   if (total >= (1ull << 31)) return fail(STZ_EINVAL, "bn_fwd: %zu chunks exceed 2^31", total);
+  if (bn_fused_on()) {
+    Carve fcv(ws, ws_bytes);
+    BnFusedParams fp{};
+    fp.x = cb(x); fp.psx = psx; fp.res = cb(res); fp.psr = psr; fp.y = mb(y); fp.psy = psy;
+    fp.stats = stats; fp.gamma = gamma; fp.beta = beta;
+    fp.m = (double)grows; fp.eps = (double)eps; fp.grows = grows;
+    fp.C = C; fp.C8 = C8; fp.G = G; fp.tiles = tiles; fp.relu = relu;
+    const int rc = bn_fused_launch<false>(fp, C8 / 8, fcv, false, st, "bn_fwd_fused");
+    if (rc != 1) return rc;
+  }
   Carve cv(ws, ws_bytes);
   double* part = cv.take<double>((size_t)G * slices * C8 * 2);
   double2* coef = cv.take<double2>((size_t)G * C8);
@@ -1922,6 +2035,18 @@ int stzx_bn_bwd(const void* g, size_t psg, const void* mask, const void* x, size
   const int rps = (int)((grows + slices - 1) / slices);
   const size_t total = (size_t)N * HW * (C8 / 8);
   if (total >= (1ull << 31)) return fail(STZ_EINVAL, "bn_bwd: %zu chunks exceed 2^31", total);
+  if (bn_fused_on()) {
+    Carve fcv(ws, ws_bytes);
+    BnFusedParams fp{};
+    fp.x = cb(x); fp.psx = psx; fp.g = cb(g); fp.psg = psg; fp.mask = cb(mask);
+    fp.y = mb(gx); fp.psy = psgx;
+    fp.stats = const_cast<double*>(stats); fp.gamma = gamma;
+    fp.ggamma = ggamma; fp.gbeta = gbeta; fp.gbias = gbias_in;
+    fp.m = (double)grows; fp.grows = grows;
+    fp.C = C; fp.C8 = C8; fp.G = G; fp.tiles = tiles; fp.accumulate = accumulate;
+    const int rc = bn_fused_launch<true>(fp, C8 / 8, fcv, gbias_in != nullptr, st, "bn_bwd_fused");
+    if (rc != 1) return rc;
+  }
   Carve cv(ws, ws_bytes);
   double* part = cv.take<double>((size_t)G * slices * C8 * 2);
   double4* coef = cv.take<double4>((size_t)G * C8);
@@ -2126,6 +2251,13 @@ int fill_ranges(PackTable& tab, size_t n, const stz_plane_range* ranges, int nra
   };
   for (int i = 0; i < nranges; ++i) {
     const stz_plane_range& r = ranges[i];
+    if (!r.planes && r.D == 0) {   // skip: updated in its weight-gradient epilogue
+      if (r.off < at || r.off + r.len > n || !add_plain(r.off) || tab.n == kMaxPackRanges)
+        return fail(STZ_EINVAL, "sgd pack skip range %d: off %zu len %zu", i, r.off, r.len);
+      tab.r[tab.n++] = PackRange{r.off, r.len, nullptr, 0, 0, 0};
+      at = r.off + r.len;
+      continue;
+    }
     if (r.off < at || r.off + r.len > n || r.off % 4 || !r.planes || r.D < 1 || r.D8 < r.D ||
         r.len % (size_t)r.D || r.ps % 4 || !aligned16(r.planes))
       return fail(STZ_EINVAL, "sgd pack range %d: off %zu len %zu D %d D8 %d (sorted, "

@@ -13,6 +13,8 @@
 // batches as one N = n_c*K pass, normalises exactly as each worker would.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "stz_fmt.cuh"
 
 namespace stz {
@@ -528,6 +530,289 @@ __global__ void __launch_bounds__(256) add_n_split_kernel(const bf16_t* __restri
       for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], v[j]);
     }
     store_split8(y + i * 8, psy, acc);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// One-launch BatchNorm (forward and backward) for the step's graphs
+// ---------------------------------------------------------------------------
+//
+// The three-launch form above (reduce, finalize, apply) costs two kernel
+// boundaries per BatchNorm and reads the input twice; at ResNet-50's later
+// stages (1568-6272 rows at K = 32) a BatchNorm is a few MB and the launches,
+// not the bytes, set its time (profiles/r02: 25-35 us for 2-15 MB).  Here one
+// cooperative grid (every CTA resident: cudaLaunchAttributeCooperative) runs
+// the phases with grid-wide barriers between them:
+//
+//   1  each CTA = (group, row slice, 256-channel tile) loads its rows once --
+//      x (and g, ReLU-masked) as fp32 kept in shared memory up to `kcap` rows
+//      per thread -- and writes its float64 partial sums (as bn_reduce_kernel)
+//   2  the grid's warps finalize every (group, channel) -- the same float64
+//      formulas as bn_stats_final_kernel / bn_bwd_final_kernel
+//   3  each CTA applies the affine form to its rows from shared memory
+//      (re-reading only rows beyond the cache) and stores y / gx
+//   4  (backward with a producing-conv bias) per-slice sums of gx, then the
+//      grid's warps sum them per channel in slice order (colsum_final_kernel)
+//
+// Every sum runs in a fixed order (deterministic); the float64 arithmetic per
+// element is the three-launch path's.
+constexpr int BNF_THREADS = 512;
+constexpr int BNF_RED_Q = 4;   // quantities per block-reduction round
+
+struct BnFusedParams {
+  const bf16_t* x; size_t psx;
+  const bf16_t* g; size_t psg;         // backward: output gradient
+  const bf16_t* mask;                  // backward: ReLU output masking g (or null)
+  const bf16_t* res; size_t psr;       // forward: residual added after the affine (or null)
+  bf16_t* y; size_t psy;               // forward: y; backward: gx (null: no input gradient)
+  double* partial;                     // [G][spg][C8][2]
+  double* stats;                       // [G][C8][2] (mean, rstd): forward writes, backward reads
+  const float* gamma; const float* beta;
+  float* ggamma; float* gbeta;         // backward: parameter gradients
+  float* gbias;                        // backward: the producing conv's bias gradient (or null)
+  double* bpart;                       // [G * spg][C8] per-slice gx sums (gbias)
+  double m, eps;
+  size_t grows;                        // rows per group (group * HW)
+  int C, C8, G, spg, tiles, rps, kcap, relu, accumulate;
+};
+
+__device__ __forceinline__ void bnf_put(float4* c, const float (&v)[8]) {
+  c[0] = make_float4(v[0], v[1], v[2], v[3]);
+  c[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void bnf_get(const float4* c, float (&v)[8]) {
+  const float4 a = c[0], b = c[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// fixed-order sum over the R row lanes of NQ per-thread quantities ->
+// out(lane, quantity, value) for lane < L (rounds of BNF_RED_Q quantities)
+template <int NQ, class F>
+__device__ __forceinline__ void bnf_block_reduce(double* red, const double (&val)[NQ], int L, int R,
+                                                 F&& out) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int q0 = 0; q0 < NQ; q0 += BNF_RED_Q) {
+#pragma unroll
+    for (int j = 0; j < BNF_RED_Q; ++j) red[j * BNF_THREADS + t] = val[q0 + j];
+    __syncthreads();
+    if (t < L * BNF_RED_Q) {
+      const int lane = t % L, j = t / L;
+      double acc = 0.0;
+      for (int r = 0; r < R; ++r) acc += red[j * BNF_THREADS + r * L + lane];
+      out(lane, q0 + j, acc);
+    }
+    __syncthreads();
+  }
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(BNF_THREADS, 1) bn_fused_kernel(const __grid_constant__ BnFusedParams p) {
+  extern __shared__ float4 bnf_cache[];
+  __shared__ double red[BNF_RED_Q * BNF_THREADS];
+  __shared__ double sc[3 * 8 * 32];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int nch = p.C8 / 8;
+  const int b = blockIdx.x, ct = b % p.tiles, rest = b / p.tiles;
+  const int slice = rest % p.spg, gi = rest / p.spg;
+  const int L = min(nch - ct * 32, 32), R = BNF_THREADS / L;
+  const int t = threadIdx.x, cl = t % L, rl = t / L;
+  const bool act = rl < R;
+  const int cc = ct * 32 + cl;
+  const size_t grow0 = (size_t)gi * p.grows;
+  const size_t r0 = min(p.grows, (size_t)slice * p.rps), r1 = min(p.grows, r0 + (size_t)p.rps);
+  const int nslot = R * L, slot = rl * L + cl;
+  float4* cx = bnf_cache;                                    // [kcap][nslot][2]
+  float4* cgr = bnf_cache + (size_t)p.kcap * nslot * 2;      // backward: g
+  const int warp = t >> 5, lane = t & 31;
+  const int gw = b * (BNF_THREADS / 32) + warp, nw = gridDim.x * (BNF_THREADS / 32);
+
+  // ---- phase 1: load (cache) + float64 partial sums ------------------------
+  {
+    double s[8], q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.0;
+    auto load_row = [&](size_t r, int k, float (&v)[8], float (&gv)[8]) {
+      const size_t off = (grow0 + r) * p.C8 + (size_t)cc * 8;
+      load_split8(p.x + off, p.psx, v);
+      if (BWD) {
+        load_split8(p.g + off, p.psg, gv);
+        if (p.mask) apply_mask8(p.mask + off, gv);
+      }
+      if (k < p.kcap) {
+        bnf_put(cx + ((size_t)k * nslot + slot) * 2, v);
+        if (BWD) bnf_put(cgr + ((size_t)k * nslot + slot) * 2, gv);
+      }
+    };
+    auto acc_row = [&](const float (&v)[8], const float (&gv)[8]) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double a = BWD ? (double)gv[j] : (double)v[j];
+        s[j] += a;
+        q[j] = fma(a, (double)v[j], q[j]);
+      }
+    };
+    constexpr int U = BWD ? 2 : 4;
+    if (act) {
+      size_t r = r0 + rl;
+      int k = 0;
+      for (; r + (U - 1) * (size_t)R < r1; r += U * (size_t)R, k += U) {
+        float v[U][8], gv[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) load_row(r + u * (size_t)R, k + u, v[u], gv[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc_row(v[u], gv[u]);
+      }
+      for (; r < r1; r += R, ++k) {
+        float v[8], gv[8];
+        load_row(r, k, v, gv);
+        acc_row(v, gv);
+      }
+    }
+    double val[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      val[j] = act ? s[j] : 0.0;
+      val[8 + j] = act ? q[j] : 0.0;
+    }
+    double* part = p.partial + ((size_t)gi * p.spg + slice) * p.C8 * 2;
+    bnf_block_reduce<16>(red, val, L, R, [&](int ln, int jj, double a) {
+      part[((size_t)(ct * 32 + ln) * 8 + (jj & 7)) * 2 + (jj >> 3)] = a;
+    });
+  }
+  grid.sync();
+
+  // ---- phase 2: finalize per (group, channel) ------------------------------
+  if (!BWD) {
+    for (int i = gw; i < p.G * p.C8; i += nw) {
+      const int g2 = i / p.C8, c = i % p.C8;
+      double s = 0.0, q = 0.0;
+      bn_sum_slices(p.partial + ((size_t)g2 * p.spg * p.C8 + c) * 2, (size_t)p.C8 * 2, p.spg,
+                    lane, s, q);
+      for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        q += __shfl_xor_sync(0xffffffffu, q, o);
+      }
+      if (lane == 0) {
+        const double mean = s / p.m;
+        const double var = fmax(q / p.m - mean * mean, 0.0);
+        const double rstd = 1.0 / sqrt(var + p.eps);
+        p.stats[(size_t)i * 2] = mean;
+        p.stats[(size_t)i * 2 + 1] = rstd;
+      }
+    }
+  } else {
+    for (int c = gw; c < p.C8; c += nw) {
+      double tg = 0.0, tgx = 0.0;
+      for (int g2 = 0; g2 < p.G; ++g2) {
+        double s = 0.0, q = 0.0;
+        bn_sum_slices(p.partial + ((size_t)g2 * p.spg * p.C8 + c) * 2, (size_t)p.C8 * 2, p.spg,
+                      lane, s, q);
+        for (int o = 16; o > 0; o >>= 1) {
+          s += __shfl_xor_sync(0xffffffffu, s, o);
+          q += __shfl_xor_sync(0xffffffffu, q, o);
+        }
+        const size_t i = (size_t)g2 * p.C8 + c;
+        const double mean = p.stats[i * 2], rstd = p.stats[i * 2 + 1];
+        q = rstd * (q - mean * s);   // sum g*x -> sum g*xhat
+        // the partials are no longer needed: keep (sum g, sum g*xhat) in slot 0
+        if (lane == 0) {
+          p.partial[((size_t)g2 * p.spg * p.C8 + c) * 2] = s;
+          p.partial[((size_t)g2 * p.spg * p.C8 + c) * 2 + 1] = q;
+        }
+        tg += s;
+        tgx += q;
+      }
+      if (c < p.C && lane == 0) {
+        p.ggamma[c] = p.accumulate ? __fadd_rn(p.ggamma[c], (float)tgx) : (float)tgx;
+        p.gbeta[c] = p.accumulate ? __fadd_rn(p.gbeta[c], (float)tg) : (float)tg;
+      }
+    }
+  }
+  if (BWD && !p.y) return;   // uniform over the grid: no input gradient
+  grid.sync();
+
+  // ---- phase 3: apply --------------------------------------------------------
+  // this CTA's coefficients: forward (A, B), backward (P, Q, R) as float64
+  constexpr int NQ = BWD ? 3 : 2;
+  for (int i = t; i < 8 * L; i += BNF_THREADS) {
+    const int ln = i % L, j = i / L, c = (ct * 32 + ln) * 8 + j;
+    const size_t gc = (size_t)gi * p.C8 + c;
+    const double mean = p.stats[gc * 2], rstd = p.stats[gc * 2 + 1];
+    if (!BWD) {
+      const double A = c < p.C ? rstd * (double)p.gamma[c] : 0.0;
+      sc[(0 * 8 + j) * 32 + ln] = A;
+      sc[(1 * 8 + j) * 32 + ln] = c < p.C ? (double)p.beta[c] - mean * A : 0.0;
+    } else {
+      const double* f = p.partial + ((size_t)gi * p.spg * p.C8 + c) * 2;
+      const double s = f[0], q = f[1];
+      const double cf = c < p.C ? (double)p.gamma[c] * rstd / p.m : 0.0;
+      sc[(0 * 8 + j) * 32 + ln] = cf * p.m;
+      sc[(1 * 8 + j) * 32 + ln] = -cf * q * rstd;
+      sc[(2 * 8 + j) * 32 + ln] = cf * (q * rstd * mean - s);
+    }
+  }
+  __syncthreads();
+  double bs[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bs[j] = 0.0;
+  if (act) {
+    // one row per step: the rows beyond the cache are few once the largest
+    // tensors take the three-launch path (U rows in flight here measured
+    // slower: the cached rows' shared loads serialise behind them)
+    size_t r = r0 + rl;
+    int k = 0;
+    for (; r < r1; r += R, ++k) {
+      const size_t off = (grow0 + r) * p.C8 + (size_t)cc * 8;
+      float v[8], gv[8], rr[8];
+      if (k < p.kcap) {
+        bnf_get(cx + ((size_t)k * nslot + slot) * 2, v);
+        if (BWD) bnf_get(cgr + ((size_t)k * nslot + slot) * 2, gv);
+      } else {
+        load_split8(p.x + off, p.psx, v);
+        if (BWD) {
+          load_split8(p.g + off, p.psg, gv);
+          if (p.mask) apply_mask8(p.mask + off, gv);
+        }
+      }
+      if (!BWD && p.res) load_split8(p.res + off, p.psr, rr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!BWD) {
+          float o = (float)fma((double)v[j], sc[j * 32 + cl], sc[(8 + j) * 32 + cl]);
+          if (p.res) o = __fadd_rn(o, rr[j]);
+          if (p.relu) o = o > 0.f ? o : 0.f;
+          v[j] = o;
+        } else {
+          v[j] = (float)fma(sc[j * 32 + cl], (double)gv[j],
+                            fma(sc[(8 + j) * 32 + cl], (double)v[j], sc[(16 + j) * 32 + cl]));
+          bs[j] += (double)v[j];
+        }
+      }
+      store_split8(p.y + off, p.psy, v);
+    }
+  }
+  if (!BWD || !p.gbias) return;   // uniform
+
+  // ---- phase 4: the producing conv's bias gradient = column sums of gx -----
+  {
+    double val[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) val[j] = act ? bs[j] : 0.0;
+    double* bp = p.bpart + ((size_t)gi * p.spg + slice) * p.C8;
+    bnf_block_reduce<8>(red, val, L, R, [&](int ln, int jj, double a) {
+      bp[(ct * 32 + ln) * 8 + jj] = a;
+    });
+  }
+  grid.sync();
+  const int ns = p.G * p.spg;
+  for (int c = gw; c < p.C; c += nw) {
+    double s = 0.0;
+    for (int k = lane; k < ns; k += 32) s += p.bpart[(size_t)k * p.C8 + c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) p.gbias[c] = p.accumulate ? __fadd_rn(p.gbias[c], (float)s) : (float)s;
   }
 }
 

@@ -199,6 +199,102 @@ __device__ __forceinline__ uint2 pack4(bf16_t a, bf16_t b, bf16_t c, bf16_t d) {
   return make_uint2((uint32_t)a | ((uint32_t)b << 16), (uint32_t)c | ((uint32_t)d << 16));
 }
 
+// FC weight gradient fused with the momentum step (one FC worker):
+// GEMM element (m, n) = the batch sum gW[m][n] of W [in][out] is never
+// stored -- the epilogue applies sgd_1 (the reference's op order,
+// tensor_core.py:366-388) to w / v at m*N + n and rewrites the split-plane
+// GEMM copy at m*N8 + n, so the gradient makes no round trip through HBM.
+// `accumulate`: the value is added to gw[m*N + n] first (micro-batch sums).
+struct EpSgd {
+  float* w;
+  float* v;
+  const float* gw;     // accumulate: earlier micro-batches' gradient sum (or null)
+  bf16_t* planes;
+  size_t ps;
+  int M, N, N8;
+  float lr, mu, inv_n;
+  static constexpr bool HAS_BIAS = false;
+  static constexpr bool STAGED = false;
+  __device__ __forceinline__ void bias8(int, float (&)[8]) const {}
+  __device__ __forceinline__ void store8_nb(int m, int n0, float (&g)[8]) const { store8(m, n0, g); }
+  __device__ __forceinline__ void store8(int m, int n0, float (&g)[8]) const {
+    if (m >= M || n0 >= N) return;
+    const size_t row = (size_t)m * N;
+    // the epilogue walks a row 32 columns per step: start this row's next two
+    // steps of w / v towards L2 now (the loads below are latency-bound)
+#pragma unroll
+    for (int a = 32; a <= 64; a += 32)
+      if (n0 + a < N) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(w + row + n0 + a));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(v + row + n0 + a));
+      }
+    if (n0 + 8 <= N && ((row + n0) & 3) == 0) {
+      float4* w4 = reinterpret_cast<float4*>(w + row + n0);
+      float4* v4 = reinterpret_cast<float4*>(v + row + n0);
+      const float4 a0 = w4[0], a1 = w4[1], b0 = v4[0], b1 = v4[1];
+      float ww[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float vv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      if (gw) {
+        const float4* g4 = reinterpret_cast<const float4*>(gw + row + n0);
+        const float4 c0 = g4[0], c1 = g4[1];
+        const float gg[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = __fadd_rn(gg[j], g[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sgd_1(ww[j], vv[j], g[j], lr, mu, inv_n);
+      w4[0] = make_float4(ww[0], ww[1], ww[2], ww[3]);
+      w4[1] = make_float4(ww[4], ww[5], ww[6], ww[7]);
+      v4[0] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+      v4[1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
+      store_split8(planes + (size_t)m * N8 + n0, ps, ww);
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + j;
+      if (n >= N) break;
+      float a = w[row + n], b = v[row + n];
+      const float gj = gw ? __fadd_rn(gw[row + n], g[j]) : g[j];
+      sgd_1(a, b, gj, lr, mu, inv_n);
+      w[row + n] = a;
+      v[row + n] = b;
+      store_split(planes, ps, (size_t)m * N8 + n, a);
+    }
+  }
+};
+
+// FC bias gradient (fixed-order column sums, as colsum_final_kernel) fused
+// with its momentum step; the summed gradient is also stored in gb
+__global__ void __launch_bounds__(256) colsum_sgd_final_kernel(const double* __restrict__ part,
+                                                               int blocks, int N, int N8,
+                                                               float* __restrict__ gb,
+                                                               const float* __restrict__ gb_acc,
+                                                               float* __restrict__ wb,
+                                                               float* __restrict__ vb, float lr,
+                                                               float mu, float inv_n) {
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (c >= N) return;
+  double s = 0.0;
+  int b = lane;
+  for (; b + 224 < blocks; b += 256) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(b + 32 * u) * N8 + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; b < blocks; b += 32) s += part[(size_t)b * N8 + c];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane) return;
+  const float g = gb_acc ? __fadd_rn(gb_acc[c], (float)s) : (float)s;
+  if (gb) gb[c] = g;
+  float a = wb[c], q = vb[c];
+  sgd_1(a, q, g, lr, mu, inv_n);
+  wb[c] = a;
+  vb[c] = q;
+}
+
 // Momentum SGD over every range of the table (which partitions [0, n)); a
 // range with planes also stores the new weights as split planes.  Range
 // offsets are multiples of 4 (16-byte aligned tensor views).
@@ -211,6 +307,7 @@ __global__ void __launch_bounds__(256) sgd_pack_kernel(float* __restrict__ w, fl
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (int r = 0; r < tab.n; ++r) {
     const PackRange rg = tab.r[r];
+    if (rg.D == 0) continue;   // updated in its weight-gradient epilogue (EpSgd)
     const size_t n4 = rg.len / 4;
     float4* w4 = reinterpret_cast<float4*>(w + rg.off);
     float4* v4 = reinterpret_cast<float4*>(v + rg.off);

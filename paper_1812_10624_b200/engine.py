@@ -132,6 +132,10 @@ class BlockEngine:
             raise ShapeMismatch(f"batch {self.batch} is not a multiple of the group {self.group}")
         self.tag = tag
         self.ws_key = None        # split-K scratch: see tensor_core.workspace
+        # (n, lr, mu) while the runtime lets the FC weight gradients apply the
+        # momentum step in their epilogue (one FC worker); layers so updated
+        self.sgd_in_wgrad = None
+        self._sgd_done: set = set()
         self._build_plan()
         self._layout_params()
         self.children: dict = {}
@@ -876,6 +880,20 @@ class BlockEngine:
                       ptr(self.grads[i][0]), gb, acc, b, c, xin.width, h,
                       w, l.out_ch, g.width, l.kh, l.kw, l.stride, l.ph, l.pw, ptr(ws),
                       ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
+        elif self.sgd_in_wgrad is not None and i in self.fused_pack_ranges()[2]:
+            # one FC worker owns this layer: the momentum step runs in the
+            # weight-gradient epilogue (gW never stored)
+            n, lr, mu = self.sgd_in_wgrad
+            wf = self.wplanes[i][0]
+            _lib.call("stzx_fc_wgrad_sgd", xin.ptr(), xin.ps, g.ptr(), g.ps,
+                      ptr(self.params[i][0]), ptr(self.velocity[i][0]), wf.data_ptr(),
+                      wf[0].numel(), ptr(self.params[i][1]), ptr(self.velocity[i][1]),
+                      ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_dim,
+                      xin.width, l.out_dim, g.width, float(lr), float(mu), inv_batch(n),
+                      ptr(ws), ws.numel(), st, flops=self.op_flops(i, b),
+                      tag=f"{self.tag}fc{i}_wgrad",
+                      nbytes=22.0 * l.in_dim * l.out_dim)
+            self._sgd_done.add(i)
         else:
             _lib.call("stzx_fc_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
                       ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_dim,
@@ -900,6 +918,24 @@ class BlockEngine:
             self._pack_ranges = (_lib.range_array(rs), len(rs), frozenset(idx))
         return self._pack_ranges
 
+    def _skip_ranges(self, done):
+        """Pack ranges for an update after the layers in ``done`` were
+        updated in their weight-gradient epilogues: each such layer's W and b
+        (one slice, its alignment gap included) is skipped (planes NULL,
+        D = 0); the other FC layers keep their fused repack."""
+        rs = []
+        for i, (a, _) in sorted(self.wplanes.items()):
+            op = self.ops[i]
+            if op.kind != "fc":
+                continue
+            (off, _, cnt), (boff, _, bcnt) = self.slots[i]
+            if i in done:
+                rs.append((off, boff + bcnt - off, None, 0, 0, 0))
+            elif i in self.fused_pack_ranges()[2]:
+                l = op.layer
+                rs.append((off, cnt, a.data_ptr(), a[0].numel(), l.out_dim, rup8(l.out_dim)))
+        return _lib.range_array(rs), len(rs)
+
     def fused_param_count(self) -> int:
         """Parameters whose split-plane copy the fused SGD rewrites (FC W)."""
         _, _, idx = self.fused_pack_ranges()
@@ -911,6 +947,11 @@ class BlockEngine:
         copies are repacked after it."""
         g = self.grad_flat if grad is None else grad
         ranges, nr, fused = self.fused_pack_ranges()
+        if self._sgd_done:
+            done, self._sgd_done = self._sgd_done, set()
+            if all(i in done for i, row in enumerate(self.slots) if row):
+                return                      # every parameter was updated in its epilogue
+            ranges, nr = self._skip_ranges(done)
         _lib.call("stz_sgd_momentum_pack", ptr(self.params_flat), ptr(self.vel_flat), ptr(g),
                   self.total, float(lr), float(mu), inv_batch(n), ranges, nr,
                   stream_of(self.device), tag=f"{self.tag}sgd_pack",

@@ -41,6 +41,7 @@ two persistent input buffers while the current step's graph replays.
 from __future__ import annotations
 
 import gc
+import os
 import random
 from collections.abc import Mapping
 
@@ -224,6 +225,11 @@ class StanzaCluster:
         self.comm = comm
         self.time_phases = time_phases
         self.graphs = bool(graphs)
+        # one FC worker on the co-located device: momentum step inside the FC
+        # weight-gradient epilogue (stzx_fc_wgrad_sgd).  Off by
+        # default: the epilogue's dependent w / v loads made the AlexNet step
+        # slower (3.51 -> 3.73 ms, profiles/r02/SUMMARY.md); STZ_FC_SGD_FUSED=1
+        self.fuse_fc_sgd = os.environ.get("STZ_FC_SGD_FUSED", "0") == "1"
         self.k = spec.batch_k
         self.net = net or NetConfig()
         # micro-batch pipelining of CONV fwd -> gather -> FC -> scatter -> CONV bwd
@@ -463,8 +469,13 @@ class StanzaCluster:
             side = self._side_stream()
             side.wait_stream(main)
             with torch.cuda.stream(side):
-                for eng in self.fcs:
-                    eng.backward(phase="wgrad")
+                if len(self.fcs) == 1 and self.fuse_fc_sgd:   # momentum step in the wgrad epilogue
+                    self.fcs[0].sgd_in_wgrad = (n, self.lr, self.momentum)
+                try:
+                    for eng in self.fcs:
+                        eng.backward(phase="wgrad")
+                finally:
+                    self.fcs[0].sgd_in_wgrad = None
                 for eng in self.fcs[1:]:
                     self.fcs[0].add_grads_from(eng)
                 self.fcs[0].sgd(n, self.lr, self.momentum)

@@ -323,3 +323,55 @@ def test_pack_conv_w_multi_matches_single(lib, shapes):
     for w, wf, wd, rf, rd in outs:
         assert torch.equal(wf, rf)
         assert torch.equal(wd, rd)
+
+
+@pytest.mark.parametrize("accumulate", [0, 1], ids=["batch", "accumulate"])
+@pytest.mark.parametrize("shape", [(128, 1024, 1000), (37, 200, 96), (256, 640, 4096),
+                                   (128, 9216, 512)], ids=lambda s: "x".join(map(str, s)))
+def test_fc_wgrad_sgd_matches_unfused(lib, shape, accumulate):
+    """The momentum step in the FC weight-gradient epilogue (one FC worker)
+    leaves w, v, the split-plane copy and the bias exactly as the unfused
+    weight gradient followed by the flat-block update."""
+    from paper_1812_10624_b200 import _lib
+    m, i, o = shape
+    i8, o8 = -(-i // 8) * 8, -(-o // 8) * 8
+    rng = np.random.Generator(np.random.PCG64(m + i + o + accumulate))
+    t = lambda *s: torch.tensor(rng.standard_normal(s).astype(np.float32), device=DEV)
+    x, g = t(m, i), t(m, o)
+    xp = torch.zeros((3, m, i8), dtype=torch.bfloat16, device=DEV)
+    gp = torch.zeros((3, m, o8), dtype=torch.bfloat16, device=DEV)
+    _lib.call("stzx_pack_rows", x.data_ptr(), xp.data_ptr(), xp[0].numel(), m, i, i8, None)
+    _lib.call("stzx_pack_rows", g.data_ptr(), gp.data_ptr(), gp[0].numel(), m, o, o8, None)
+    w, v, wb, vb = t(i, o), t(i, o), t(o), t(o)
+    gw0, gb0 = t(i, o), t(o)
+    lr, mu, n = 0.05, 0.9, m
+    from paper_1812_10624_b200.tensor_core import inv_batch
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device=DEV)
+
+    # unfused: gradient, then the update with the fused plane repack
+    gw, gb = (gw0.clone(), gb0.clone()) if accumulate else (torch.zeros_like(gw0),
+                                                           torch.zeros_like(gb0))
+    w1, v1, wb1, vb1 = w.clone(), v.clone(), wb.clone(), vb.clone()
+    p1 = torch.zeros((3, i, o8), dtype=torch.bfloat16, device=DEV)
+    _lib.call("stzx_fc_wgrad", xp.data_ptr(), xp[0].numel(), gp.data_ptr(), gp[0].numel(),
+              gw.data_ptr(), gb.data_ptr(), accumulate, m, i, i8, o, o8, ws.data_ptr(),
+              ws.numel(), None)
+    rs = _lib.range_array([(0, i * o, p1.data_ptr(), p1[0].numel(), o, o8)])
+    _lib.call("stz_sgd_momentum_pack", w1.data_ptr(), v1.data_ptr(), gw.data_ptr(), i * o, lr,
+              mu, inv_batch(n), rs, 1, None)
+    _lib.call("stz_sgd_momentum_pack", wb1.data_ptr(), vb1.data_ptr(), gb.data_ptr(), o, lr, mu,
+              inv_batch(n), _lib.range_array([]), 0, None)
+
+    # fused
+    w2, v2, wb2, vb2 = w.clone(), v.clone(), wb.clone(), vb.clone()
+    gw2, gb2 = gw0.clone(), gb0.clone()
+    p2 = torch.zeros_like(p1)
+    _lib.call("stzx_fc_wgrad_sgd", xp.data_ptr(), xp[0].numel(), gp.data_ptr(), gp[0].numel(),
+              w2.data_ptr(), v2.data_ptr(), p2.data_ptr(), p2[0].numel(), wb2.data_ptr(),
+              vb2.data_ptr(), gw2.data_ptr(), gb2.data_ptr(), accumulate, m, i, i8, o, o8, lr,
+              mu, inv_batch(n), ws.data_ptr(), ws.numel(), None)
+    torch.cuda.synchronize()
+    for a, b in [(w1, w2), (v1, v2), (wb1, wb2), (vb1, vb2), (gb, gb2)]:
+        assert torch.equal(a, b)
+    assert torch.equal(p1.view(torch.int16), p2.view(torch.int16))
+    assert torch.equal(gw2, gw0)          # the weight gradient itself is never stored

@@ -284,3 +284,21 @@ def test_vgg16_parity_batch(lib):
                for ra, rb in zip(out.state.velocities, ref_v) for a, b in zip(ra, rb))
     assert vdev <= 1e-5 * vmax, (vdev, vmax)
     np.testing.assert_allclose(out.losses, ref_l, rtol=1e-5)
+
+
+@pytest.mark.parametrize("case", ["tiny_1x1", "tiny32_2x1", "mlp_2x1"])
+def test_fused_fc_sgd_matches_reference_golden(lib, case):
+    """The momentum step inside the FC weight-gradient epilogue (one FC
+    worker, stzx_fc_wgrad_sgd) keeps the reference's parameters, velocities
+    and losses (same bar as test_train_matches_reference_golden)."""
+    g = golden_io.train()[f"train_{case}"]
+    spec = _spec(case.split("_")[0])
+    boundary = 4 if case.startswith("mlp") else None
+    cl = _cluster(spec, int(g["n_conv"]), int(g["n_fc"]), int(g["seed"]), int(g["data_seed"]),
+                  boundary)
+    cl.fuse_fc_sgd = True
+    res = cl.train(int(g["iters"]))
+    ref_p, ref_v = golden_io.nested_state(g)
+    assert orc.max_param_dev(res.state.params, ref_p) <= TOL
+    assert orc.max_param_dev(res.state.velocities, ref_v) <= TOL
+    np.testing.assert_allclose(res.losses, g["losses"], rtol=TOL)
