@@ -207,6 +207,13 @@ int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* g
                   int accumulate, int M, int in_dim, int in8, int out_dim, int out8, void* ws,
                   size_t ws_bytes, void* stream);
 
+/* Bias gradient on its own: out[n] (+)= sum over the R rows of split-plane
+ * g [R][ld] of column n < N, float64 sums in a fixed order rounded once
+ * (tensor_core.py:259 / :288) -- the colsum the weight-gradient entries run
+ * when given gb, issued separately so it can run on another stream. */
+int stzx_colsum(const void* g, size_t psg, int R, int N, int ld, float* out, int accumulate,
+                void* ws, size_t ws_bytes, void* stream);
+
 /* stzx_fc_wgrad fused with the momentum step when one FC worker owns the
  * layer: the weight gradient of W [in][out] is consumed in the
  * GEMM epilogue -- w / v (fp32 [in][out], 16-byte aligned) get

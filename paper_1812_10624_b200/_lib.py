@@ -62,6 +62,7 @@ SIGNATURES = {
     "stzx_fc_fwd": (I, [P, Z, P, Z, P, P, Z, P, I, I, I, I, I, I, P, Z, P]),
     "stzx_fc_dgrad": (I, [P, Z, P, Z, P, Z, P, I, I, I, I, P, Z, P]),
     "stzx_fc_wgrad": (I, [P, Z, P, Z, P, P, I, I, I, I, I, I, P, Z, P]),
+    "stzx_colsum": (I, [P, Z, I, I, I, P, I, P, Z, P]),
     "stzx_fc_wgrad_sgd": (I, [P, Z, P, Z, P, P, P, Z, P, P, P, P, I, I, I, I, I, I, F, F, F,
                               P, Z, P]),
     "stzx_maxpool_fwd": (I, [P, Z, P, Z, P, I, I, I, I, I, I, I, I, P]),

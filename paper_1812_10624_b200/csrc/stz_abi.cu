@@ -1831,6 +1831,13 @@ int stzx_fc_dgrad(const void* g, size_t psg, const void* w, size_t psw, void* gx
                        as_stream(stream));
 }
 
+int stzx_colsum(const void* g, size_t psg, int R, int N, int ld, float* out, int accumulate,
+                void* ws, size_t ws_bytes, void* stream) {
+  if (R < 0 || N <= 0 || ld < N || ld % 8 || !out) return fail(STZ_EINVAL, "colsum: bad shape");
+  if (R == 0) return STZ_OK;
+  return colsum_split(cb(g), psg, R, N, ld, out, ws, ws_bytes, as_stream(stream), accumulate);
+}
+
 int stzx_fc_wgrad_sgd(const void* x, size_t psx, const void* g, size_t psg, float* w, float* v,
                       void* planes, size_t psw, float* wb, float* vb, float* gw, float* gb,
                       int accumulate, int M, int in_dim, int in8, int out_dim, int out8, float lr,

@@ -136,6 +136,9 @@ class BlockEngine:
         # momentum step in their epilogue (one FC worker); layers so updated
         self.sgd_in_wgrad = None
         self._sgd_done: set = set()
+        # set by the runtime: conv bias column sums run on this stream,
+        # concurrently with the rest of the backward (joined before the update)
+        self.bias_stream = None
         self._build_plan()
         self._layout_params()
         self.children: dict = {}
@@ -866,16 +869,21 @@ class BlockEngine:
         ``xin`` and output-gradient rows ``g`` (``acc``: add into grad_flat)."""
         op = self.ops[i]
         l = op.layer
+        side_bias = (op.kind == "conv" and not op.bias_by_bn and self.bias_stream is not None)
+        if side_bias:
+            self._colsum_side(i, g, b, acc)
         if op.kind == "conv" and op.s2d is not None:
             ks, cs8, hs, ws_ = op.s2d
             _lib.call("stzx_conv_wgrad_s2d", xin.ptr(), xin.ps, g.ptr(), g.ps,
-                      ptr(self.grads[i][0]), None if op.bias_by_bn else ptr(self.grads[i][1]),
+                      ptr(self.grads[i][0]),
+                      None if (op.bias_by_bn or side_bias) else ptr(self.grads[i][1]),
                       acc, b, l.in_ch, cs8,
                       hs, ws_, l.out_ch, g.width, l.kernel, l.stride, ptr(ws), ws.numel(), st,
                       flops=self.op_flops(i, b), tag=f"{self.tag}conv{i}_wgrad")
         elif op.kind == "conv":
             c, h, w = op.in_shape
-            gb = None if op.bias_by_bn else ptr(self.grads[i][1])   # summed by the BN backward
+            # summed by the BN backward, or on the bias stream
+            gb = None if (op.bias_by_bn or side_bias) else ptr(self.grads[i][1])
             _lib.call("stzx_conv2_wgrad", xin.ptr(), xin.ps, g.ptr(), g.ps,
                       ptr(self.grads[i][0]), gb, acc, b, c, xin.width, h,
                       w, l.out_ch, g.width, l.kh, l.kw, l.stride, l.ph, l.pw, ptr(ws),
@@ -899,6 +907,22 @@ class BlockEngine:
                       ptr(self.grads[i][0]), ptr(self.grads[i][1]), acc, b, l.in_dim,
                       xin.width, l.out_dim, g.width, ptr(ws), ws.numel(), st,
                       flops=self.op_flops(i, b), tag=f"{self.tag}fc{i}_wgrad")
+
+    def _colsum_side(self, i, g, b, acc):
+        """Conv op i's bias gradient (column sums of its output gradient
+        ``g``, b samples) on ``self.bias_stream``, ordered after the work
+        that produced g; its own split-K scratch."""
+        main = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.bias_stream.wait_event(ev)
+        _, oh, ow = self.ops[i].out_shape
+        with torch.cuda.stream(self.bias_stream):
+            ws = workspace(self.device, "bias_side")
+            _lib.call("stzx_colsum", g.ptr(), g.ps, b * oh * ow, self.ops[i].layer.out_ch,
+                      g.width, ptr(self.grads[i][1]), acc, ptr(ws), ws.numel(),
+                      stream_of(self.device), tag=f"{self.tag}conv{i}_bias",
+                      nbytes=6.0 * b * oh * ow * g.width)
 
     def fused_pack_ranges(self):
         """(ctypes stz_plane_range array, count, layer indices): the FC weights,

@@ -146,6 +146,8 @@ class _Feed:
         self.consumed = [torch.cuda.Event(), torch.cuda.Event()]
         self.used = [False, False]
         self.h2d_bytes = 0
+        self.staged = [None, None]   # iteration whose batch each buffer holds / receives
+        self.cur = 0                 # buffer of the next iteration to run
 
     def stage(self, it: int, b: int) -> None:
         cl, k = self.cl, self.cl.k
@@ -165,6 +167,7 @@ class _Feed:
                 self._put(self.x[b][rows], self.hx[b][rows], x, torch.float32)
                 self._put(self.y[b][rows], self.hy[b][rows], y, torch.int32)
             self.copied[b].record(self.stream)
+        self.staged[b] = it
         self.h2d_bytes = self.x[b].numel() * 4 + self.y[b].numel() * 4
 
     @staticmethod
@@ -481,7 +484,16 @@ class StanzaCluster:
                 self.fcs[0].sgd(n, self.lr, self.momentum)
         mark("boundary")                  # zero-copy: FC dgrad wrote the trunk's rows
         mark("conv_backward")
-        self.conv.backward(self.gboundary)
+        if overlap:                       # conv bias column sums off the critical path
+            bias = self._bias_stream()
+            bias.wait_stream(main)
+            self.conv.bias_stream = bias
+        try:
+            self.conv.backward(self.gboundary)
+        finally:
+            self.conv.bias_stream = None
+        if overlap:
+            main.wait_stream(bias)
         mark("exchange")
         if not overlap:
             for eng in self.fcs[1:]:
@@ -512,6 +524,11 @@ class StanzaCluster:
                 e.record(torch.cuda.current_stream(self.device))
                 ev.append((label, e))
         return mark
+
+    def _bias_stream(self) -> "torch.cuda.Stream":
+        if getattr(self, "_bias", None) is None:
+            self._bias = torch.cuda.Stream(self.device)
+        return self._bias
 
     def _side_stream(self) -> "torch.cuda.Stream":
         if getattr(self, "_side", None) is None:
@@ -780,16 +797,24 @@ class StanzaCluster:
             if self._feed is None:
                 self._feed = _Feed(self)
             feed = self._feed
-            if n_it:
-                feed.stage(self.iteration, 0)
+            if n_it and feed.staged[feed.cur] != self.iteration:
+                feed.stage(self.iteration, feed.cur)
         use_graphs = self.graphs and not self.time_phases and self.graph_capable()
         for s in range(n_it):
-            b = s & 1
+            b = feed.cur if feed is not None else s & 1
             recs = self._record()
             if feed is not None:
                 feed.ready(b, main)
+                # the next iteration's batch, also past this call's last one:
+                # a later train() call then starts on a resident batch
+                # (batch_fn is a pure function of (iteration, worker))
                 if s + 1 < n_it:
                     feed.stage(self.iteration + 1, b ^ 1)
+                else:
+                    try:
+                        feed.stage(self.iteration + 1, b ^ 1)
+                    except Exception:           # a finite batch_fn: nothing to prefetch
+                        feed.staged[b ^ 1] = None
             x = feed.x[b] if feed is not None else None
             y = feed.y[b] if feed is not None else None
             if use_graphs and self._steps_done > 0:
@@ -803,6 +828,7 @@ class StanzaCluster:
                     self._pending_events.append((ev, recs))
             if feed is not None:
                 feed.done(b, main)
+                feed.cur = b ^ 1
             host_losses[s:s + 1].copy_(slots[s:s + 1], non_blocking=True)
             self.iteration += 1
         torch.cuda.synchronize(dev)

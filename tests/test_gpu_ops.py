@@ -375,3 +375,35 @@ def test_fc_wgrad_sgd_matches_unfused(lib, shape, accumulate):
         assert torch.equal(a, b)
     assert torch.equal(p1.view(torch.int16), p2.view(torch.int16))
     assert torch.equal(gw2, gw0)          # the weight gradient itself is never stored
+
+
+@pytest.mark.parametrize("shape", [(387200, 64), (128, 4096), (37, 1000), (1000, 13)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_colsum_matches_wgrad_bias(lib, shape):
+    """stzx_colsum (the bias gradient issued on its own stream) writes exactly
+    the column sums the weight-gradient entry writes (float64, fixed order),
+    and accumulates like it."""
+    from paper_1812_10624_b200 import _lib
+    r, n = shape
+    n8 = -(-n // 8) * 8
+    rng = np.random.Generator(np.random.PCG64(r + n))
+    g = torch.tensor(rng.standard_normal((r, n)).astype(np.float32), device=DEV)
+    gp = torch.zeros((3, r, n8), dtype=torch.bfloat16, device=DEV)
+    _lib.call("stzx_pack_rows", g.data_ptr(), gp.data_ptr(), gp[0].numel(), r, n, n8, None)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=DEV)
+    ref = np.asarray(g.cpu().numpy(), np.float64).sum(axis=0).astype(np.float32)
+    out = torch.full((n,), 0.5, device=DEV)
+    _lib.call("stzx_colsum", gp.data_ptr(), gp[0].numel(), r, n, n8, out.data_ptr(), 0,
+              ws.data_ptr(), ws.numel(), None)
+    assert orc.rel_err(host(out), ref) <= 1e-7
+    x = torch.zeros((r, 8), device=DEV)
+    xp = torch.zeros((3, r, 8), dtype=torch.bfloat16, device=DEV)
+    gw = torch.zeros((8, n), device=DEV)
+    gb = torch.zeros((n,), device=DEV)
+    _lib.call("stzx_fc_wgrad", xp.data_ptr(), xp[0].numel(), gp.data_ptr(), gp[0].numel(),
+              gw.data_ptr(), gb.data_ptr(), 0, r, 8, 8, n, n8, ws.data_ptr(), ws.numel(), None)
+    assert torch.equal(out, gb)
+    _lib.call("stzx_colsum", gp.data_ptr(), gp[0].numel(), r, n, n8, out.data_ptr(), 1,
+              ws.data_ptr(), ws.numel(), None)
+    torch.cuda.synchronize()
+    assert torch.equal(out, gb + gb)

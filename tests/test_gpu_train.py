@@ -92,6 +92,26 @@ def test_resume_replays_bit_exact(lib):
     assert holder.role is Role.CONV_WORKER
 
 
+def test_split_train_calls_match_one_call(lib):
+    """train(3) + train(4) (the second call starts on the batch the first one
+    prefetched) == train(7); a restored iteration counter restages."""
+    spec = _spec("tiny")
+    whole = _cluster(spec, 2, 1, 4, 21).train(7)
+    cl = _cluster(spec, 2, 1, 4, 21)
+    l1 = cl.train(3).losses
+    res = cl.train(4)
+    np.testing.assert_array_equal(l1 + res.losses, whole.losses)
+    for la, lb in zip(res.state.params, whole.state.params):
+        for x, y in zip(la, lb):
+            np.testing.assert_array_equal(x, y)
+    cl2 = _cluster(spec, 2, 1, 4, 21)
+    cl2.train(2)
+    cl2.iteration = 5                # batches are a function of the iteration
+    assert cl2._feed.staged[cl2._feed.cur] == 2
+    cl2.train(1)
+    assert cl2._feed.staged[cl2._feed.cur] == 6
+
+
 def test_phase_sequence_and_traffic(lib):
     """Reference ledger pins (test_stanza_runtime.py:158-179) on the
     cluster's own transport.ledger."""

@@ -14,9 +14,9 @@ done
 timeout 600 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/r2/prof/resnet50_step_launches.csv python tools/profile_step.py resnet50_exec 32 > gpurun_out/r2/prof/step_ncu.log 2>&1
 python tools/launch_summary.py gpurun_out/r2/prof/resnet50_step_launches.csv | head -12
-for d in false true; do
+for d in 0 1; do
   timeout 600 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none \
-    -k "regex:bn_fused_kernel<$d>" -c 1 -o gpurun_out/r2/prof/bn_fused_$d \
+    --kernel-name-base demangled -k "regex:bn_fused_kernel<.bool.$d>" -c 1 -o gpurun_out/r2/prof/bn_fused_$d \
     python tools/profile_step.py resnet50_exec 32 > gpurun_out/r2/prof/bn_$d.log 2>&1
   ncu -i gpurun_out/r2/prof/bn_fused_$d.ncu-rep --page raw --csv > gpurun_out/r2/prof/bn_fused_${d}_raw.csv 2>/dev/null
   ncu -i gpurun_out/r2/prof/bn_fused_$d.ncu-rep --page details --csv > gpurun_out/r2/prof/bn_fused_${d}_details.csv 2>/dev/null
