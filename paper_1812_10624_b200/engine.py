@@ -139,6 +139,11 @@ class BlockEngine:
         # set by the runtime: conv bias column sums run on this stream,
         # concurrently with the rest of the backward (joined before the update)
         self.bias_stream = None
+        self._bias_events: dict = {}
+        # set by the runtime: (stream, n, lr, mu) -- each conv layer's momentum
+        # step + weight repack runs on that stream as soon as its input and
+        # weight gradients are issued (joined before the next forward)
+        self.update_side = None
         self._build_plan()
         self._layout_params()
         self.children: dict = {}
@@ -852,6 +857,9 @@ class BlockEngine:
                     _lib.call("stzx_fc_dgrad", g.ptr(), g.ps, ptr(wp), wp[0].numel(), out.ptr(),
                               out.ps, mptr, b, l.in_dim, out.width, g.width, ptr(ws),
                               ws.numel(), st, flops=self.op_flops(i, b), tag=f"{self.tag}fc{i}_dgrad")
+                if (self.update_side is not None and do_w and op.kind == "conv"
+                        and not self.children and not accumulate):
+                    self._update_layer_side(i)
                 g_full = self.gin[i]
         self._gout = gout
         return V(g_full)
@@ -923,6 +931,35 @@ class BlockEngine:
                       g.width, ptr(self.grads[i][1]), acc, ptr(ws), ws.numel(),
                       stream_of(self.device), tag=f"{self.tag}conv{i}_bias",
                       nbytes=6.0 * b * oh * ow * g.width)
+            done = torch.cuda.Event()
+            done.record(self.bias_stream)
+            self._bias_events[i] = done
+
+    def _update_layer_side(self, i):
+        """Conv op i's momentum step (its W and b slice of the flat block) and
+        split-plane repack on the update stream, after the input- and
+        weight-gradient work issued so far (and its bias sums)."""
+        stream, n, lr, mu = self.update_side
+        main = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        stream.wait_event(ev)
+        if i in self._bias_events:
+            stream.wait_event(self._bias_events.pop(i))
+        (off, _, _), (boff, _, bcnt) = self.slots[i]
+        cnt = boff + bcnt - off
+        l = self.ops[i].layer
+        wf, wd = self.wplanes[i]
+        with torch.cuda.stream(stream):
+            st = stream_of(self.device)
+            _lib.call("stz_sgd_momentum_pack", ptr(self.params_flat[off:]),
+                      ptr(self.vel_flat[off:]), ptr(self.grad_flat[off:]), cnt, float(lr),
+                      float(mu), inv_batch(n), _lib.range_array([]), 0, st,
+                      tag=f"{self.tag}conv{i}_sgd", nbytes=20.0 * cnt)
+            _lib.call("stzx_pack_conv2_w", ptr(self.params[i][0]), ptr(wf), wf[0].numel(),
+                      ptr(wd), 0 if wd is None else wd[0].numel(), l.out_ch, l.in_ch, l.kh,
+                      l.kw, rup8(l.in_ch), rup8(l.out_ch), st)
+        self._sgd_done.add(i)
 
     def fused_pack_ranges(self):
         """(ctypes stz_plane_range array, count, layer indices): the FC weights,
@@ -944,20 +981,26 @@ class BlockEngine:
 
     def _skip_ranges(self, done):
         """Pack ranges for an update after the layers in ``done`` were
-        updated in their weight-gradient epilogues: each such layer's W and b
-        (one slice, its alignment gap included) is skipped (planes NULL,
-        D = 0); the other FC layers keep their fused repack."""
-        rs = []
-        for i, (a, _) in sorted(self.wplanes.items()):
-            op = self.ops[i]
-            if op.kind != "fc":
+        updated already (in their weight-gradient epilogue, or on the update
+        stream): each such layer's parameter slice is skipped (planes NULL,
+        D = 0; consecutive skipped layers merge, alignment gaps included); the
+        other FC layers keep their fused repack."""
+        fused = self.fused_pack_ranges()[2]
+        rs, prev_done = [], False
+        for i, row in enumerate(self.slots):
+            if not row:
                 continue
-            (off, _, cnt), (boff, _, bcnt) = self.slots[i]
             if i in done:
-                rs.append((off, boff + bcnt - off, None, 0, 0, 0))
-            elif i in self.fused_pack_ranges()[2]:
-                l = op.layer
+                lo, hi = row[0][0], row[-1][0] + row[-1][2]
+                if prev_done:
+                    lo = rs.pop()[0]
+                rs.append((lo, hi - lo, None, 0, 0, 0))
+            elif i in fused:
+                l = self.ops[i].layer
+                a = self.wplanes[i][0]
+                off, _, cnt = row[0]
                 rs.append((off, cnt, a.data_ptr(), a[0].numel(), l.out_dim, rup8(l.out_dim)))
+            prev_done = i in done
         return _lib.range_array(rs), len(rs)
 
     def fused_param_count(self) -> int:
@@ -974,8 +1017,9 @@ class BlockEngine:
         if self._sgd_done:
             done, self._sgd_done = self._sgd_done, set()
             if all(i in done for i, row in enumerate(self.slots) if row):
-                return                      # every parameter was updated in its epilogue
+                return                      # every parameter was already updated
             ranges, nr = self._skip_ranges(done)
+            fused = frozenset(fused | done)
         _lib.call("stz_sgd_momentum_pack", ptr(self.params_flat), ptr(self.vel_flat), ptr(g),
                   self.total, float(lr), float(mu), inv_batch(n), ranges, nr,
                   stream_of(self.device), tag=f"{self.tag}sgd_pack",

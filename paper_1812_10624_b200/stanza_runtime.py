@@ -484,14 +484,18 @@ class StanzaCluster:
                 self.fcs[0].sgd(n, self.lr, self.momentum)
         mark("boundary")                  # zero-copy: FC dgrad wrote the trunk's rows
         mark("conv_backward")
-        if overlap:                       # conv bias column sums off the critical path
-            bias = self._bias_stream()
+        if overlap:                       # conv bias sums and per-layer updates off the
+            bias = self._bias_stream()    # critical path (joined before the step ends)
+            upd = self._update_stream()
             bias.wait_stream(main)
+            upd.wait_stream(main)
             self.conv.bias_stream = bias
+            self.conv.update_side = (upd, n, self.lr, self.momentum)
         try:
             self.conv.backward(self.gboundary)
         finally:
             self.conv.bias_stream = None
+            self.conv.update_side = None
         if overlap:
             main.wait_stream(bias)
         mark("exchange")
@@ -501,6 +505,7 @@ class StanzaCluster:
         mark("update")
         self.conv.sgd(n, self.lr, self.momentum)
         if overlap:
+            main.wait_stream(upd)
             main.wait_stream(side)
         else:
             self.fcs[0].sgd(n, self.lr, self.momentum)
@@ -524,6 +529,11 @@ class StanzaCluster:
                 e.record(torch.cuda.current_stream(self.device))
                 ev.append((label, e))
         return mark
+
+    def _update_stream(self) -> "torch.cuda.Stream":
+        if getattr(self, "_upd", None) is None:
+            self._upd = torch.cuda.Stream(self.device)
+        return self._upd
 
     def _bias_stream(self) -> "torch.cuda.Stream":
         if getattr(self, "_bias", None) is None:
