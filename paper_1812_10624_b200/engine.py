@@ -144,6 +144,10 @@ class BlockEngine:
         # step + weight repack runs on that stream as soon as its input and
         # weight gradients are issued (joined before the next forward)
         self.update_side = None
+        # set by the runtime: conv weight gradients run on this stream, beside
+        # the input-gradient chain on the current stream
+        self.wgrad_stream = None
+        self._wgrad_events: dict = {}
         self._build_plan()
         self._layout_params()
         self.children: dict = {}
@@ -839,7 +843,10 @@ class BlockEngine:
                           + (6.0 + 2.0 * (mptr is not None)) * b * out.row_elems)
                 g_full = self.gin[i]
             elif op.kind in ("conv", "fc"):
-                if do_w:
+                if do_w and self.wgrad_stream is not None and op.kind == "conv" \
+                        and not self.children:
+                    self._wgrad_side(i, xin, g, b, acc)
+                elif do_w:
                     self._wgrad(i, xin, g, b, acc, ws, st)
                 if op.skip_dgrad or (op.kind == "conv" and op.s2d is not None):
                     g_full = None
@@ -935,6 +942,21 @@ class BlockEngine:
             done.record(self.bias_stream)
             self._bias_events[i] = done
 
+    def _wgrad_side(self, i, xin, g, b, acc):
+        """Conv op i's weight (and bias) gradient on ``self.wgrad_stream``,
+        ordered after the work that produced its output gradient; its own
+        split-K scratch."""
+        main = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.wgrad_stream.wait_event(ev)
+        with torch.cuda.stream(self.wgrad_stream):
+            ws = workspace(self.device, "wgrad_side")
+            self._wgrad(i, xin, g, b, acc, ws, stream_of(self.device))
+            done = torch.cuda.Event()
+            done.record(self.wgrad_stream)
+            self._wgrad_events[i] = done
+
     def _update_layer_side(self, i):
         """Conv op i's momentum step (its W and b slice of the flat block) and
         split-plane repack on the update stream, after the input- and
@@ -946,6 +968,8 @@ class BlockEngine:
         stream.wait_event(ev)
         if i in self._bias_events:
             stream.wait_event(self._bias_events.pop(i))
+        if i in self._wgrad_events:
+            stream.wait_event(self._wgrad_events.pop(i))
         (off, _, _), (boff, _, bcnt) = self.slots[i]
         cnt = boff + bcnt - off
         l = self.ops[i].layer

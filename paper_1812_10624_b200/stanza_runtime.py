@@ -233,6 +233,9 @@ class StanzaCluster:
         # default: the epilogue's dependent w / v loads made the AlexNet step
         # slower (3.51 -> 3.73 ms, profiles/r02/SUMMARY.md); STZ_FC_SGD_FUSED=1
         self.fuse_fc_sgd = os.environ.get("STZ_FC_SGD_FUSED", "0") == "1"
+        # co-located step: conv weight gradients on their own stream beside
+        # the input-gradient chain (STZ_WGRAD_STREAM=1)
+        self.wgrad_side = os.environ.get("STZ_WGRAD_STREAM", "0") == "1"
         self.k = spec.batch_k
         self.net = net or NetConfig()
         # micro-batch pipelining of CONV fwd -> gather -> FC -> scatter -> CONV bwd
@@ -491,13 +494,22 @@ class StanzaCluster:
             upd.wait_stream(main)
             self.conv.bias_stream = bias
             self.conv.update_side = (upd, n, self.lr, self.momentum)
+            if self.wgrad_side:
+                wst = self._wgrad_stream()
+                wst.wait_stream(main)
+                self.conv.wgrad_stream = wst
         try:
             self.conv.backward(self.gboundary)
         finally:
             self.conv.bias_stream = None
             self.conv.update_side = None
+            self.conv.wgrad_stream = None
+            self.conv._wgrad_events.clear()
+            self.conv._bias_events.clear()
         if overlap:
             main.wait_stream(bias)
+            if self.wgrad_side:
+                main.wait_stream(wst)
         mark("exchange")
         if not overlap:
             for eng in self.fcs[1:]:
@@ -529,6 +541,11 @@ class StanzaCluster:
                 e.record(torch.cuda.current_stream(self.device))
                 ev.append((label, e))
         return mark
+
+    def _wgrad_stream(self) -> "torch.cuda.Stream":
+        if getattr(self, "_wst", None) is None:
+            self._wst = torch.cuda.Stream(self.device)
+        return self._wst
 
     def _update_stream(self) -> "torch.cuda.Stream":
         if getattr(self, "_upd", None) is None:
