@@ -1623,10 +1623,14 @@ int stzx_pack_conv_w_multi(const stz_conv_pack* jobs, int n, void* stream) {
         q.C8 < q.C || q.O8 < q.O || q.psf % 2 || (q.wd && q.psd % 2) ||
         (reinterpret_cast<uintptr_t>(q.wf) & 3) || (reinterpret_cast<uintptr_t>(q.wd) & 3))
       return fail(STZ_EINVAL, "pack_conv_w_multi: job %d", i);
-    const int cb = std::min(rup8(q.C8), (kPackSpan / kk) & ~1);   // even, >= 2
+    // a multiple of 8 where the span allows (8-element stores), else even
+    int cb = std::min(rup8(q.C8), (kPackSpan / kk) & ~7);
+    if (cb == 0) cb = std::min(rup8(q.C8), (kPackSpan / kk) & ~1);   // even, >= 2
+    const int vec = cb % 8 == 0 && aligned16(q.wf) && (!q.wd || aligned16(q.wd)) &&
+                    q.psf % 8 == 0 && (!q.wd || q.psd % 8 == 0);
     const long jt = (long)cdiv(q.O8, 32) * cdiv(q.C8, cb);
     t.j[t.n++] = ConvPackJob{q.w, mb(q.wf), mb(q.wd), q.psf, q.psd, q.O, q.C, kk, q.C8, q.O8, cb,
-                             (int)tiles};
+                             (int)tiles, vec};
     tiles += jt;
   }
   if (tiles >= (1L << 31)) return fail(STZ_EINVAL, "pack_conv_w_multi: %ld tiles", tiles);

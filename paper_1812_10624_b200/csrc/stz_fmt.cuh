@@ -163,6 +163,7 @@ struct ConvPackJob {
   int O, C, kk, C8, O8;
   int cb;          // input channels per tile (even; 32 o x cb c x kk taps staged in shared memory)
   int tile0;       // first tile of this job
+  int vec;         // cb % 8 == 0 and 16-byte aligned planes: 8-element stores
 };
 constexpr int kMaxConvPack = 160;
 constexpr int kPackSpan = 288;   // cb * kk words per output channel in a tile
@@ -194,6 +195,34 @@ __global__ void __launch_bounds__(256) pack_conv_w_multi_kernel(const __grid_con
     tile[ol * ld + rem] = (o < J.O && c < J.C) ? __ldg(J.w + ((size_t)o * J.C + c0) * kk + rem) : 0.f;
   }
   __syncthreads();
+  if (J.vec) {
+    // wf[o][tap][c], c fastest: 8 channels per thread, one 16-byte store per plane
+    const int cg8 = cb >> 3;
+    for (int idx = threadIdx.x; idx < 32 * kk * cg8; idx += blockDim.x) {
+      const int ol = idx / (kk * cg8), rem = idx - ol * kk * cg8;
+      const int tap = rem / cg8, cl = 8 * (rem - tap * cg8);
+      const int o = o0 + ol, c = c0 + cl;
+      if (o >= J.O || c >= J.C8) continue;
+      float v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = tile[ol * ld + (cl + t) * kk + tap];
+      store_split8(J.wf + ((size_t)o * kk + tap) * J.C8 + c, J.psf, v);
+    }
+    if (!J.wd) return;
+    // wd[c][tt][o], o fastest, tap = kk - 1 - tt: 8 output channels per thread
+    for (int idx = threadIdx.x; idx < 4 * span; idx += blockDim.x) {
+      const int cl = idx / (4 * kk), rem = idx - cl * 4 * kk;
+      const int tt = rem >> 2, ol = 8 * (rem & 3);
+      const int o = o0 + ol, c = c0 + cl;
+      if (c >= J.C || o >= J.O8) continue;
+      const int src = cl * kk + (kk - 1 - tt);
+      float v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = tile[(ol + t) * ld + src];
+      store_split8(J.wd + ((size_t)c * kk + tt) * J.O8 + o, J.psd, v);
+    }
+    return;
+  }
   // wf[o][tap][c], c fastest, pairs (c, c+1): C8, c0 and cb are even
   const int hb = cb >> 1;
   for (int idx = threadIdx.x; idx < 32 * kk * hb; idx += blockDim.x) {

@@ -595,7 +595,16 @@ class StanzaCluster:
                 link.get_grads(j)
                 self.conv.backward(self.gboundary, rows=(j * kb, (j + 1) * kb), phase="dgrad")
             mark("conv_backward")
-            self.conv.backward(phase="wgrad")
+            main = torch.cuda.current_stream(self.device)
+            bias = self._bias_stream()    # conv bias column sums beside the weight gradients
+            bias.wait_stream(main)
+            self.conv.bias_stream = bias
+            try:
+                self.conv.backward(phase="wgrad")
+            finally:
+                self.conv.bias_stream = None
+                self.conv._bias_events.clear()
+            main.wait_stream(bias)
         else:
             eng = self.fcs[0]
             g = link.g
