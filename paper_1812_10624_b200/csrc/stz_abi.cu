@@ -801,8 +801,11 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   else if (sh.BN == 192) smem = band_smem<192, 1>(rows_alloc);
   else smem = band_smem<128, 1>(rows_alloc);
   if (smem > 227 * 1024) return -1;
-  // split-K over channel blocks to keep K per work item <= TG_MAX_KB k-blocks
-  const int cblocks = C8 / 32;
+  // split-K over channel blocks to keep K per work item <= TG_MAX_KB k-blocks;
+  // blocks wholly past the real channels (a space-to-depth input padded to
+  // 64) are neither loaded nor multiplied
+  const int creal_eff = creal > 0 && creal <= C8 ? creal : C8;
+  const int cblocks = cdiv(creal_eff, 32);
   const int kb_per_cb = k * k;
   int cb_per_split = TG_MAX_KB / kb_per_cb;
   if (cb_per_split < 1) cb_per_split = 1;
@@ -819,7 +822,8 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   prm.partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
   prm.N = O;
   prm.C8 = C8;
-  prm.creal = creal > 0 && creal <= C8 ? creal : C8;
+  prm.creal = creal_eff;
+  prm.cblocks = cblocks;
   prm.Nimg = vimg;
   prm.Nreal = Nimg;
   prm.Hs = stacked ? H : (1 << 24);
@@ -886,9 +890,13 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   if (splits < 1) splits = 1;
   const int M = ks * ks * 64;
   if (!ws || (size_t)splits * M * 64 * sizeof(float) > ws_bytes) return -1;
-  const size_t smem = bw_smem(XW, Wv);
+  // as many stages as fit (ResNet-50's 112-wide stem rows fit two)
+  int nst = BW_STAGES;
+  while (nst > 2 && bw_smem(XW, Wv, nst) > 227 * 1024) --nst;
+  const size_t smem = bw_smem(XW, Wv, nst);
   if (smem > 227 * 1024) return -1;
   BandWParams prm;
+  prm.nst = nst;
   for (int pl = 0; pl < 3; ++pl) {
     if (!enc_sw128_rows(&prm.x[pl], x + pl * psx, N, Hs, Ws, XW)) return -1;
     if (!enc_sw128_rows(&prm.g[pl], g + pl * psg, N, OH, OW, Wv)) return -1;
@@ -911,7 +919,7 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   const int grid = items < num_sms() ? items : num_sms();
   if (g_trace)
     fprintf(stderr, "[stz] conv_wgrad[bandw] N=%d OHxOW=%dx%d ks=%d Wv=%d XW=%d splits=%d items=%d "
-            "smem=%zu\n", N, OH, OW, ks, Wv, XW, splits, items, smem);
+            "stages=%d smem=%zu\n", N, OH, OW, ks, Wv, XW, splits, items, nst, smem);
   bandwgrad_kernel<<<grid, BW_THREADS, smem, st>>>(prm);
   int rc = check_launch("conv_wgrad[bandw]");
   if (rc) return rc;

@@ -51,6 +51,7 @@ struct alignas(64) BandParams {
   int N;                 // GEMM N (output channels)
   int C8;                // input channels (multiple of 32)
   int creal;             // channels < creal are real: 16-deep k steps past it are skipped
+  int cblocks;           // 32-channel blocks holding real channels (cdiv(creal, 32))
   int Nimg, pad, Wp, ksz, OH, OW;
   int Nreal, Hs;         // stacked mode (pad 0): Nimg = 1 image of Nreal * Hs rows
   FastDiv d_hs;
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
   const int nt = cdiv(p.N, BN);
   const int per_split = p.Nimg * p.tiles_per_img * nt;
   const int items = per_split * p.splits;
-  const int cblocks = p.C8 / 32, taps = p.ksz * p.ksz;
+  const int cblocks = p.cblocks, taps = p.ksz * p.ksz;
   // item w -> (split z, image n, tile t, n tile); n fastest so tiles share the band in L2
   auto decode = [&](int w, int& z, int& n, int& t, int& n0) {
     z = w / per_split;

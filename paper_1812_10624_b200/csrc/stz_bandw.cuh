@@ -42,6 +42,7 @@ struct alignas(64) BandWParams {
   float* partial;     // [splits][ks*ks*64][64]
   int N, OH, ks, Wv, XW;
   int splits, rows_total;   // N * OH output raster rows
+  int nst;                  // pipeline stages (2..BW_STAGES: wide rows fit fewer)
   FastDiv d_oh;
 };
 
@@ -53,8 +54,8 @@ __host__ __device__ inline int bw_gplane(int Wv) { return Wv * 128; }
 __host__ __device__ inline int bw_stage(int XW, int Wv) {
   return 3 * (bw_xplane(XW) + bw_gplane(Wv));
 }
-__host__ inline size_t bw_smem(int XW, int Wv) {
-  return 1024 + (size_t)BW_STAGES * bw_stage(XW, Wv) + 256;
+__host__ inline size_t bw_smem(int XW, int Wv, int nst = BW_STAGES) {
+  return 1024 + (size_t)nst * bw_stage(XW, Wv) + 256;
 }
 
 __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_constant__ BandWParams p) {
@@ -66,9 +67,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw);
   const int XP = bw_xplane(p.XW), GP = bw_gplane(p.Wv), STG = bw_stage(p.XW, p.Wv);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BW_STAGES * STG);
-  uint64_t* empty = full + BW_STAGES;
-  uint64_t* tfull = empty + BW_STAGES;    // [2]
+  const int NST = p.nst;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STG);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;    // [2]
   uint64_t* tempty = tfull + 2;           // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < BW_STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -108,8 +110,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
       int j0, j1;
       rows_of(z, j0, j1);
       for (int j = j0; j < j1; ++j, ++gs) {
-        const int s = gs % BW_STAGES;
-        mbar_wait(&empty[s], ((gs / BW_STAGES) & 1) ^ 1);
+        const int s = gs % NST;
+        mbar_wait(&empty[s], ((gs / NST) & 1) ^ 1);
         if (lane == 0) mbar_arrive_tx(&full[s], tx);
         __syncwarp();
         uint32_t n, y;
@@ -143,8 +145,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
       mbar_wait(&tempty[0], (it & 1) ^ 1);
       tc_fence_after();
       for (int j = j0; j < j1; ++j, ++gs) {
-        const int s = gs % BW_STAGES;
-        mbar_wait(&full[s], (gs / BW_STAGES) & 1);
+        const int s = gs % NST;
+        mbar_wait(&full[s], (gs / NST) & 1);
         tc_fence_after();
         const uint32_t st = base + s * STG;
         const uint32_t b0 = st + 3 * XP;

@@ -169,6 +169,15 @@ def test_alexnet_conv1_space_to_depth(clusters):
     assert eng.ops[0].s2d == (3, 64, 57, 57)
 
 
+@pytest.mark.parametrize("side", [64, 224], ids=["64px", "224px"])
+def test_resnet_stem_space_to_depth(clusters, side):
+    """ResNet-50's 7x7/2 stem as a stride-1 4x4 conv over 2x2 space-to-depth
+    blocks (12 real of 32 channels)."""
+    from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
+    eng = _run([Conv2d(3, 64, 7, 2, 3), ReLU(), MaxPool2d(3, 2)], (3, side, side), 2, False, 1)
+    assert eng.ops[0].s2d == (4, 32, side // 2 + 3, side // 2 + 3)
+
+
 def test_alexnet_conv2_to_pool_tma(clusters):
     from paper_1812_10624_b200.tensor_core import Conv2d, MaxPool2d, ReLU
     _run([Conv2d(64, 192, 5, 1, 2), ReLU(), MaxPool2d(3, 2)], (64, 27, 27), 2, True, 2)
