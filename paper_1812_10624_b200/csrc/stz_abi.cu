@@ -855,21 +855,25 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   return check_launch("band_reduce");
 }
 
-bool enc_sw128_rows(CUtensorMap* out, const void* base, int N, int H, int W, int bw) {
-  const std::string key = cache_key(4, (uintptr_t)base, N, H, W, bw);
+// pixel rows of `ch` channels (64: SWIZZLE_128B, 32: SWIZZLE_64B), one box =
+// bw pixels of one raster row
+bool enc_sw128_rows(CUtensorMap* out, const void* base, int N, int H, int W, int bw,
+                    int ch = 64) {
+  const std::string key = cache_key(4, (uintptr_t)base, N, H, W, bw * 1000 + ch);
   auto it = g_map_cache.find(key);
   if (it != g_map_cache.end()) {
     *out = it->second;
     return true;
   }
-  cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
-  cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
-  cuuint32_t box[4] = {64, (cuuint32_t)bw, 1, 1};
+  const cuuint64_t rb = (cuuint64_t)ch * 2;
+  cuuint64_t dims[4] = {(cuuint64_t)ch, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {rb, (cuuint64_t)W * rb, (cuuint64_t)H * W * rb};
+  cuuint32_t box[4] = {(cuuint32_t)ch, (cuuint32_t)bw, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   g_map_cache.emplace(key, *out);
   return true;
@@ -878,8 +882,8 @@ bool enc_sw128_rows(CUtensorMap* out, const void* base, int N, int H, int W, int
 int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
                    const EpConvWgradS2D& ep, int N, int Hs, int Ws, int OH, int OW, int C8, int O,
                    int O8, int ks, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (!g_use_band || !g_use_tma || !tma_ready() || C8 != 64 || O8 != 64 || O > 64 || ks < 1 ||
-      ks > 4)
+  if (!g_use_band || !g_use_tma || !tma_ready() || (C8 != 64 && C8 != 32) || O8 != 64 ||
+      O > 64 || ks < 1 || ks > 4)
     return -1;
   const int Wv = (OW + 15) / 16 * 16;
   const int XW = Wv + 2 * ((ks + 1) / 2);
@@ -888,17 +892,17 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   int splits = 2 * num_sms() / ks;
   if (splits > rows_total) splits = rows_total;
   if (splits < 1) splits = 1;
-  const int M = ks * ks * 64;
+  const int M = ks * ks * C8;
   if (!ws || (size_t)splits * M * 64 * sizeof(float) > ws_bytes) return -1;
-  // as many stages as fit (ResNet-50's 112-wide stem rows fit two)
+  // as many stages as fit (wide rows fit fewer)
   int nst = BW_STAGES;
-  while (nst > 2 && bw_smem(XW, Wv, nst) > 227 * 1024) --nst;
-  const size_t smem = bw_smem(XW, Wv, nst);
+  while (nst > 2 && bw_smem(XW, Wv, nst, C8) > 227 * 1024) --nst;
+  const size_t smem = bw_smem(XW, Wv, nst, C8);
   if (smem > 227 * 1024) return -1;
   BandWParams prm;
   prm.nst = nst;
   for (int pl = 0; pl < 3; ++pl) {
-    if (!enc_sw128_rows(&prm.x[pl], x + pl * psx, N, Hs, Ws, XW)) return -1;
+    if (!enc_sw128_rows(&prm.x[pl], x + pl * psx, N, Hs, Ws, XW, C8)) return -1;
     if (!enc_sw128_rows(&prm.g[pl], g + pl * psg, N, OH, OW, Wv)) return -1;
   }
   prm.partial = static_cast<float*>(ws);
@@ -912,7 +916,10 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   prm.d_oh = FastDiv((uint32_t)OH);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(bandwgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bandwgrad_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(bandwgrad_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
     attr = true;
   }
   const int items = ks * splits;
@@ -920,7 +927,8 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   if (g_trace)
     fprintf(stderr, "[stz] conv_wgrad[bandw] N=%d OHxOW=%dx%d ks=%d Wv=%d XW=%d splits=%d items=%d "
             "stages=%d smem=%zu\n", N, OH, OW, ks, Wv, XW, splits, items, nst, smem);
-  bandwgrad_kernel<<<grid, BW_THREADS, smem, st>>>(prm);
+  if (C8 == 64) bandwgrad_kernel<64><<<grid, BW_THREADS, smem, st>>>(prm);
+  else bandwgrad_kernel<32><<<grid, BW_THREADS, smem, st>>>(prm);
   int rc = check_launch("conv_wgrad[bandw]");
   if (rc) return rc;
   launch_reduce(prm.partial, splits, M, O, ep, st);

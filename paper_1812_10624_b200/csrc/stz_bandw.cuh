@@ -1,7 +1,9 @@
-// Shifted-window ("band") weight gradient of a stride-1 conv with 64
-// channels in and out: AlexNet conv1 as space-to-depth (3x3 taps over 4x4
-// blocks, 48 -> 64 channels, 64 outputs, reference
-// tensor_core.py:242-261).
+// Shifted-window ("band") weight gradient of a stride-1 conv with 64 or 32
+// input channels and 64 outputs: AlexNet conv1 as space-to-depth (3x3 taps
+// over 4x4 blocks, 48 -> 64 channels) and ResNet-50's stem (4x4 taps over
+// 2x2 blocks, 12 -> 32 channels; CW = 32 puts four taps in one 128-row
+// operand on SWIZZLE_64B rows), reference
+// tensor_core.py:242-261.  The description below is the CW = 64 case.
 //
 //   dW[o][t][c] = sum_q dY[q][o] * X[q + off(t)][c]
 //
@@ -37,9 +39,9 @@
 namespace stz {
 
 struct alignas(64) BandWParams {
-  CUtensorMap x[3];   // per plane: 4D [N][Hs][Ws][64], box {64, XW, 1, 1}, SWIZZLE_128B
+  CUtensorMap x[3];   // per plane: 4D [N][Hs][Ws][CW], box {CW, XW, 1, 1}, SWIZZLE_(2 CW)B
   CUtensorMap g[3];   // per plane: 4D [N][OH][OW][64], box {64, Wv, 1, 1}, SWIZZLE_128B
-  float* partial;     // [splits][ks*ks*64][64]
+  float* partial;     // [splits][ks*ks*CW][64]
   int N, OH, ks, Wv, XW;
   int splits, rows_total;   // N * OH output raster rows
   int nst;                  // pipeline stages (2..BW_STAGES: wide rows fit fewer)
@@ -49,24 +51,31 @@ struct alignas(64) BandWParams {
 constexpr int BW_THREADS = 256;
 constexpr int BW_STAGES = 4;
 
-__host__ __device__ inline int bw_xplane(int XW) { return (XW * 128 + 1023) / 1024 * 1024; }
-__host__ __device__ inline int bw_gplane(int Wv) { return Wv * 128; }
-__host__ __device__ inline int bw_stage(int XW, int Wv) {
-  return 3 * (bw_xplane(XW) + bw_gplane(Wv));
+// CW = input channels per pixel row: 64 (SWIZZLE_128B rows, two taps per
+// 128-row A operand: AlexNet conv1) or 32 (SWIZZLE_64B rows, four taps per
+// operand: ResNet-50's 7x7/2 stem as 4x4 taps over 12 of 32 channels)
+__host__ __device__ inline int bw_xplane(int XW, int CW = 64) {
+  return (XW * 2 * CW + 1023) / 1024 * 1024;
 }
-__host__ inline size_t bw_smem(int XW, int Wv, int nst = BW_STAGES) {
-  return 1024 + (size_t)nst * bw_stage(XW, Wv) + 256;
+__host__ __device__ inline int bw_gplane(int Wv) { return Wv * 128; }
+__host__ __device__ inline int bw_stage(int XW, int Wv, int CW = 64) {
+  return 3 * (bw_xplane(XW, CW) + bw_gplane(Wv));
+}
+__host__ inline size_t bw_smem(int XW, int Wv, int nst = BW_STAGES, int CW = 64) {
+  return 1024 + (size_t)nst * bw_stage(XW, Wv, CW) + 256;
 }
 
+template <int CW>
 __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_constant__ BandWParams p) {
   constexpr int ACC = 192;                 // big | S1 | S2, 64 columns each
-  constexpr int TILES = 2;                 // ceil(ks / 2) for ks <= 4
-  constexpr int SET = TILES * ACC;         // 384 columns, one set
+  constexpr int TPT = 128 / CW;            // taps per 128-row A operand
+  constexpr int TILES = (4 + TPT - 1) / TPT;   // ceil(ks / TPT) for ks <= 4
+  constexpr int SET = TILES * ACC;         // columns of one set
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw);
-  const int XP = bw_xplane(p.XW), GP = bw_gplane(p.Wv), STG = bw_stage(p.XW, p.Wv);
+  const int XP = bw_xplane(p.XW, CW), GP = bw_gplane(p.Wv), STG = bw_stage(p.XW, p.Wv, CW);
   const int NST = p.nst;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STG);
   uint64_t* empty = full + NST;
@@ -103,7 +112,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
 
   if (warp == 0) {
     // ---------------- TMA producer: one stage per output raster row ------------------
-    const uint32_t tx = (uint32_t)(3 * 128 * (p.XW + p.Wv));
+    const uint32_t tx = (uint32_t)(3 * (2 * CW * p.XW + 128 * p.Wv));
     int gs = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
       const int z = w / ks, dh = w - z * ks;
@@ -156,12 +165,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
           const uint64_t db2 = umma_desc_sw128(b0 + 2 * GP + kq * 2048, GP, 1024);  // b2
 #pragma unroll
           for (int tile = 0; tile < TILES; ++tile) {
-            if (2 * tile >= ks) break;
-            // A plane a: input rows (2 tile) + 16 kq ..; the second tap one row on
-            const uint32_t arow = st + (uint32_t)(2 * tile + 16 * kq) * 128;
-            const uint64_t da0 = umma_desc_sw128(arow, 128, 1024);
-            const uint64_t da1 = umma_desc_sw128(arow + XP, 128, 1024);
-            const uint64_t da2 = umma_desc_sw128(arow + 2 * XP, 128, 1024);
+            if (TPT * tile >= ks) break;
+            // A plane a: input rows (TPT tile) + 16 kq ..; each further tap one row on
+            const uint32_t arow = st + (uint32_t)(TPT * tile + 16 * kq) * (2 * CW);
+            const uint64_t da0 = CW == 64 ? umma_desc_sw128(arow, 128, 1024)
+                                          : umma_desc_sw64(arow, 64, 512);
+            const uint64_t da1 = CW == 64 ? umma_desc_sw128(arow + XP, 128, 1024)
+                                          : umma_desc_sw64(arow + XP, 64, 512);
+            const uint64_t da2 = CW == 64 ? umma_desc_sw128(arow + 2 * XP, 128, 1024)
+                                          : umma_desc_sw64(arow + 2 * XP, 64, 512);
             const uint32_t tbig = tmem_base + tile * ACC, ts1 = tbig + 64, ts2 = tbig + 128;
             umma_f16(ts2, da0, db2, idesc64, acc);     // a0.b2 -> S2
             umma_f16(tbig, da0, db0, idesc128, acc);   // a0.[b0|b1] -> big, S1
@@ -176,8 +188,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
   } else if (warp >= 4) {
     // ---------------- epilogue: tap rows of the split's partial ---------------------
     const int q = warp & 3;
-    const int r = q * 32 + lane;                 // accumulator row = (tap half, channel)
-    const int mrows = ks * ks * 64;
+    const int r = q * 32 + lane;                 // accumulator row = (tap in tile, channel)
+    const int mrows = ks * ks * CW;
     int it = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int z = w / ks, dh = w - z * ks;
@@ -185,10 +197,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
       tc_fence_after();
 #pragma unroll 1
       for (int tile = 0; tile < TILES; ++tile) {
-        if (2 * tile >= ks) break;
-        const int dw = 2 * tile + (r >= 64 ? 1 : 0);
+        if (TPT * tile >= ks) break;
+        const int dw = TPT * tile + r / CW;
         const bool valid = dw < ks;
-        const int m = (dh * ks + dw) * 64 + (r & 63);
+        const int m = (dh * ks + dw) * CW + (r % CW);
         const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + tile * ACC;
 #pragma unroll 1
         for (int c = 0; c < 64; c += 16) {
