@@ -445,6 +445,31 @@ bool enc_tiled(CUtensorMap* out, const void* base, uint64_t inner, uint64_t oute
   return true;
 }
 
+// the three split planes of a [rows][K] operand (plane stride ps elements) as
+// one 3D map {K, rows, plane}: a box {32, R, 3} lands the planes R*64 bytes
+// apart, exactly the layout of three {32, R} boxes
+bool enc_planes3(CUtensorMap* out, const void* base, uint64_t K, uint64_t rows, uint64_t ld,
+                 uint64_t ps, uint32_t R) {
+  if ((ps * 2) % 16 || (ld * 2) % 16) return false;
+  const std::string key = cache_key(5, (uintptr_t)base, K, rows, ld, ps, R);
+  auto it = g_map_cache.find(key);
+  if (it != g_map_cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  cuuint64_t dims[3] = {K, rows, 3};
+  cuuint64_t strides[2] = {ld * 2, ps * 2};
+  cuuint32_t box[3] = {32, R, 3};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc_tiled(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  g_map_cache.emplace(key, *out);
+  return true;
+}
+
 bool enc_im2col(CUtensorMap* out, const void* base, int N, int H, int W, int C8, int s, int lo,
                 int hi, int pixels, int chans = 32, int lo_h = INT_MIN, int hi_h = INT_MIN) {
   if (lo_h == INT_MIN) lo_h = lo;
@@ -721,6 +746,17 @@ void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
 // ---- shifted-window (band) conv: stride-1 "valid" conv over an NHWC input ----------
 int g_use_band = 1;     // stz_set_band
 int g_band_padded = 0;  // 1: also padded convs (measured slower; tests keep the path covered)
+// band weights: a stage's three planes as one TMA box (STZ_BAND_B3=0: three)
+const int g_band_b3 = [] {
+  const char* e = getenv("STZ_BAND_B3");
+  return e && *e == '0' ? 0 : 1;
+}();
+// stacked band as exactly the raster rows a tile reads: 1 always, 0 only when
+// whole padded rows do not fit (STZ_BAND_EXACT)
+const int g_band_exact = [] {
+  const char* e = getenv("STZ_BAND_EXACT");
+  return e && *e == '1' ? 1 : 0;
+}();
 
 template <int BN, int MT, class EP>
 int launch_band(BandParams<EP>& prm, int items, size_t smem, cudaStream_t st) {
@@ -794,13 +830,38 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
     if (stacked) sh.junk *= (double)vrows / (Nimg * OH);
     if (sh.junk > 1.12) return -1;   // wide tiles are near MMA-bound: junk costs directly
   }
-  if (sh.Hb > 256) return -1;
-  const int rows_alloc = band_rows_alloc(sh.Hb, Wp);
-  size_t smem = 0;
-  if (sh.BN == 64) smem = sh.MT == 2 ? band_smem<64, 2>(rows_alloc) : band_smem<64, 1>(rows_alloc);
-  else if (sh.BN == 192) smem = band_smem<192, 1>(rows_alloc);
-  else smem = band_smem<128, 1>(rows_alloc);
-  if (smem > 227 * 1024) return -1;
+  auto smem_of = [&](const BandShape& b, int rows) -> size_t {
+    if (b.BN == 64) return b.MT == 2 ? band_smem<64, 2>(rows) : band_smem<64, 1>(rows);
+    if (b.BN == 192) return band_smem<192, 1>(rows);
+    return band_smem<128, 1>(rows);
+  };
+  int rows_alloc = sh.Hb <= 256 ? band_rows_alloc(sh.Hb, Wp) : 1 << 20;
+  size_t smem = sh.Hb <= 256 ? smem_of(sh, rows_alloc) : (size_t)1 << 30;
+  int exact = 0, brows = 0, nbx = 0;
+  if (stacked && (g_band_exact || smem > 227 * 1024)) {
+    // the band as exactly the TM + (k-1)(Wp+1) raster rows a tile reads (2D
+    // boxes over the stacked pixels): ResNet-50's 115-wide stem rows do not
+    // fit as whole rows; fall back to one-tile (MT = 1) bands if needed
+    for (int mt = sh.MT; mt >= 1 && !exact; --mt) {
+      BandShape b = sh;
+      if (mt != sh.MT) {
+        b = band_shape(sh.BN, mt, Nimg, vrows, OW, Wp, k);
+        b.junk *= (double)vrows / (Nimg * OH);
+      }
+      const int R = mt * TG_BM + (k - 1) * (Wp + 1);
+      const int nb = cdiv(R, 256), br = (cdiv(R, nb) + 7) / 8 * 8;
+      const size_t sm = smem_of(b, nb * br);
+      if (sm <= 227 * 1024) {
+        sh = b;
+        exact = 1;
+        nbx = nb;
+        brows = br;
+        rows_alloc = nb * br;
+        smem = sm;
+      }
+    }
+  }
+  if (!exact && (sh.Hb > 256 || smem > 227 * 1024)) return -1;
   // split-K over channel blocks to keep K per work item <= TG_MAX_KB k-blocks;
   // blocks wholly past the real channels (a space-to-depth input padded to
   // 64) are neither loaded nor multiplied
@@ -814,10 +875,19 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   const int M_out = Nimg * OH * OW, npad = rup8(O);
   if (splits > 1 && (!ws || (size_t)splits * M_out * npad * sizeof(float) > ws_bytes)) return -1;
   BandParams<EP> prm;
-  for (int pl = 0; pl < 3; ++pl)
-    if (!enc_band4d(&prm.band[pl], x + pl * psx, vimg, stacked ? Nimg * H : H, W, C8, Wp, sh.Hb))
-      return -1;
+  for (int pl = 0; pl < 3; ++pl) {
+    const bool ok = exact
+        ? enc_band4d(&prm.band[pl], x + pl * psx, 1, 1, Nimg * H * W, C8, brows, 1)
+        : enc_band4d(&prm.band[pl], x + pl * psx, vimg, stacked ? Nimg * H : H, W, C8, Wp, sh.Hb);
+    if (!ok) return -1;
+  }
+  prm.exact = exact;
+  prm.brows = brows;
+  prm.nbx = nbx;
   if (!op_tiled_k(prm.b, w, psw, O, k * k * C8, k * k * C8, sh.BN)) return -1;
+  prm.use_b3 = g_band_b3 && prm.b.nbox == 1 &&
+               enc_planes3(&prm.b3, w, (uint64_t)k * k * C8, (uint64_t)O, (uint64_t)k * k * C8,
+                           (uint64_t)psw, (uint32_t)sh.BN);
   prm.ep = ep;
   prm.partial = splits > 1 ? static_cast<float*>(ws) : nullptr;
   prm.N = O;
@@ -842,9 +912,9 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
   const int items = vimg * sh.tiles * cdiv(O, sh.BN) * splits;
   if (g_trace)
     fprintf(stderr, "[stz] %-16s band N=%d OHxOW=%dx%d Wp=%d k=%d pad=%d C8=%d O=%d BN=%d MT=%d "
-            "tiles/img=%d Hb=%d junk=%.2f splits=%d items=%d smem=%zu\n",
-            what, Nimg, OH, OW, Wp, k, pad, C8, O, sh.BN, sh.MT, sh.tiles, sh.Hb, sh.junk, splits,
-            items, smem);
+            "tiles/img=%d Hb=%d exact=%d(%dx%d) junk=%.2f splits=%d items=%d smem=%zu\n",
+            what, Nimg, OH, OW, Wp, k, pad, C8, O, sh.BN, sh.MT, sh.tiles, sh.Hb, exact, nbx,
+            brows, sh.junk, splits, items, smem);
   if (sh.BN == 64 && sh.MT == 2) launch_band<64, 2>(prm, items, smem, st);
   else if (sh.BN == 64) launch_band<64, 1>(prm, items, smem, st);
   else if (sh.BN == 192) launch_band<192, 1>(prm, items, smem, st);

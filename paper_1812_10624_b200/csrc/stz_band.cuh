@@ -46,10 +46,14 @@ template <class EP>
 struct alignas(64) BandParams {
   CUtensorMap band[3];   // per plane: 4D [N][H][W][C8], box {32, Wp, Hb, 1}, SWIZZLE_64B
   TgOperand b;           // weights, TILED_K
+  CUtensorMap b3;        // weights as one 3D map {K, O, plane}: a stage's three planes in one box
+  int use_b3;
   EP ep;
   float* partial;        // split-K partials [splits][M_out][npad] (nullptr: no split)
   int N;                 // GEMM N (output channels)
   int C8;                // input channels (multiple of 32)
+  int exact;             // stacked raster only: the band is exactly the rows a tile reads,
+  int brows, nbx;        //   nbx 2D boxes of brows pixels each (else whole padded rows)
   int creal;             // channels < creal are real: 16-deep k steps past it are skipped
   int cblocks;           // 32-channel blocks holding real channels (cdiv(creal, 32))
   int Nimg, pad, Wp, ksz, OH, OW;
@@ -68,7 +72,7 @@ template <int BN, int MT>
 struct BandCfg {
   static constexpr int B_PLANE = BN * TG_BK * 2;          // one plane of a B tile
   static constexpr int B_STAGE = 3 * B_PLANE;
-  static constexpr int STAGES = BN <= 64 ? 4 : 3;
+  static constexpr int STAGES = (BN <= 64 && MT == 2) ? 4 : 3;
   // thin tiles: the 4-MMA schedule of stz_tma.cuh -- weight planes b0 | b1
   // (contiguous) as one 128-wide operand; accumulators big | S1 | S2.  Off:
   // with MT = 2 its 384 columns leave one TMEM set, and the serialised
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t smem_base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (smem_base - raw);
-  const int rows_alloc = band_rows_alloc(p.Hb, p.Wp);
+  const int rows_alloc = p.exact ? p.nbx * p.brows : band_rows_alloc(p.Hb, p.Wp);
   const int BAND = band_bytes(rows_alloc);
   const int PLANE = rows_alloc * 64;
   const int REGION = band_region(rows_alloc);
@@ -172,7 +176,8 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer --------------------------------------------
-    const uint32_t band_tx = (uint32_t)(3 * p.Hb * p.Wp * 64);   // bytes the 3 boxes land
+    const uint32_t band_tx = (uint32_t)(p.exact ? 3 * p.nbx * p.brows * 64   // bytes the boxes land
+                                                : 3 * p.Hb * p.Wp * 64);
     int gb = 0, gs = 0;
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
       int z, n, t, n0;
@@ -188,7 +193,18 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
           mbar_arrive_tx(&band_full[bb], band_tx);
         }
         __syncwarp();
-        if (lane < 3 && !(p.debug & 4)) {   // one 4D box per plane: padded rows y0 .. y0+Hb-1
+        if (p.exact) {   // raster rows t*TM .. as nbx boxes per plane
+          if (lane < 3 * p.nbx && !(p.debug & 4)) {
+            const int pl = lane % 3, bi = lane / 3;
+            const uint32_t dst = band0 + bb * BAND + pl * PLANE + bi * p.brows * 64;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+                "l"(reinterpret_cast<uint64_t>(&p.band[pl])), "r"(smem_u32(&band_full[bb])),
+                "r"(cb * 32), "r"(t * TM + bi * p.brows), "r"(0), "r"(0)
+                : "memory");
+          }
+        } else if (lane < 3 && !(p.debug & 4)) {   // one 4D box per plane: padded rows y0 .. y0+Hb-1
           const int pl = lane;
           const uint32_t dst = band0 + bb * BAND + pl * PLANE;
           asm volatile(
@@ -209,8 +225,12 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
           if (lane == 0) mbar_arrive_tx(&b_full[s], Cfg::B_STAGE);
           __syncwarp();
           const uint32_t st = bst0 + s * Cfg::B_STAGE;
-          for (int bi = lane; bi < 3 * p.b.nbox; bi += 32)
-            tg_load_box<1>(p.b, bi, st, Cfg::B_PLANE, &b_full[s], n0, tp * p.C8 + cb * 32);
+          if (p.use_b3) {   // TMA cost is per box: the three planes as one {32, BN, 3} box
+            if (lane == 0) tma_3d<1>(&p.b3, st, &b_full[s], tp * p.C8 + cb * 32, n0, 0);
+          } else {
+            for (int bi = lane; bi < 3 * p.b.nbox; bi += 32)
+              tg_load_box<1>(p.b, bi, st, Cfg::B_PLANE, &b_full[s], n0, tp * p.C8 + cb * 32);
+          }
         }
       }
     }
@@ -226,7 +246,8 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       int z, n, t, n0;
       decode(w, z, n, t, n0);
-      const uint32_t x0 = (uint32_t)((t * TM) % p.Wp);   // band row of the tile's first output
+      // band row of the tile's first output
+      const uint32_t x0 = p.exact ? 0u : (uint32_t)((t * TM) % p.Wp);
       const int cb0 = z * p.cb_per_split, cb1 = min(cblocks, cb0 + p.cb_per_split);
       const int set = NSETS == 2 ? (it & 1) : 0;
       const int use = NSETS == 2 ? (it >> 1) : it;
@@ -328,6 +349,27 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
               rs[e] = __float_as_uint(__fadd_rn(__uint_as_float(rs[e]), __uint_as_float(r2[e])));
           }
           tmem_ld_wait();
+          if constexpr (EP::STAGED) {
+            // split-plane output: 16 columns per lane and plane as one 256-bit
+            // store (whole sectors; the row-per-lane stores of 16 bytes kept
+            // the LSU busy at half-sector granularity)
+            if (!p.partial && !(p.debug & 1)) {
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const int nb = n0 + c + 16 * h2;
+                if (nb >= npad) break;
+                float v[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  v[jj] = __fadd_rn(__uint_as_float(r[16 * h2 + jj]),
+                                    __uint_as_float(rs[16 * h2 + jj]));
+                  if (EP::HAS_BIAS) v[jj] = __fadd_rn(v[jj], bb[2 * h2 + jj / 8][jj % 8]);
+                }
+                if (valid) p.ep.store16_nb(m, nb, v);
+              }
+              continue;
+            }
+          }
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
             const int nb = n0 + c + 8 * h;

@@ -325,6 +325,64 @@ struct EpSplit {
     }
     store8_nb(m, n0, v);
   }
+  // 16 columns of row m (v includes the bias): one 256-bit store per plane,
+  // i.e. whole 32-byte sectors, where the row segment is 32-byte aligned and
+  // in range; else two store8_nb
+  __device__ __forceinline__ void store16_nb(int m, int n0, float (&v)[16]) const {
+    if (m >= M || n0 >= ld) return;
+    const size_t base = (size_t)m * ld + n0;
+    if (rs || n0 + 16 > ld || ((reinterpret_cast<uintptr_t>(out + base) |
+                                 reinterpret_cast<uintptr_t>(out + base + ps)) & 31)) {
+      float a[8], b[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a[j] = v[j];
+        b[j] = v[8 + j];
+      }
+      store8_nb(m, n0, a);
+      store8_nb(m, n0 + 8, b);
+      return;
+    }
+    uint32_t mw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mw[j] = 0xFFFFFFFFu;
+    if (mask) {
+      const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(mask + base));
+      const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(mask + base + 8));
+      mw[0] = m0.x; mw[1] = m0.y; mw[2] = m0.z; mw[3] = m0.w;
+      mw[4] = m1.x; mw[5] = m1.y; mw[6] = m1.z; mw[7] = m1.w;
+    }
+    uint32_t w[3][8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float x2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = 2 * j + e;
+        float x = v[jj];
+        if (n0 + jj < N) {
+          if (relu && x < 0.f) x = 0.f;
+          const uint32_t h = (mw[j] >> (16 * e)) & 0xFFFFu;
+          if (mask && !(h != 0u && h < 0x8000u)) x = 0.f;
+        } else {
+          x = 0.f;
+        }
+        x2[e] = x;
+      }
+      bf16_t a0, a1, a2, c0, c1, c2;
+      split_bf16x3(x2[0], a0, a1, a2);
+      split_bf16x3(x2[1], c0, c1, c2);
+      w[0][j] = (uint32_t)a0 | ((uint32_t)c0 << 16);
+      w[1][j] = (uint32_t)a1 | ((uint32_t)c1 << 16);
+      w[2][j] = (uint32_t)a2 | ((uint32_t)c2 << 16);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + base + k * ps),
+                   "r"(w[k][0]), "r"(w[k][1]), "r"(w[k][2]), "r"(w[k][3]), "r"(w[k][4]),
+                   "r"(w[k][5]), "r"(w[k][6]), "r"(w[k][7])
+                   : "memory");
+  }
 };
 
 // fp32 output with the general index (m/mdiv)*ld_hi + (m%mdiv)*ld_lo + n*ld_n
