@@ -746,6 +746,12 @@ void launch_tg(const TgParams<EP>& prm, int splits, cudaStream_t st) {
 // ---- shifted-window (band) conv: stride-1 "valid" conv over an NHWC input ----------
 int g_use_band = 1;     // stz_set_band
 int g_band_padded = 0;  // 1: also padded convs (measured slower; tests keep the path covered)
+// split-plane GEMM epilogue as 256-bit per-row stores (STZ_EPI_DIRECT=1)
+// instead of the shared-memory staged row-contiguous stores
+const int g_epi_direct = [] {
+  const char* e = getenv("STZ_EPI_DIRECT");
+  return e && *e == '1' ? 1 : 0;
+}();
 // band weights: a stage's three planes as one TMA box (STZ_BAND_B3=0: three)
 const int g_band_b3 = [] {
   const char* e = getenv("STZ_BAND_B3");
@@ -1059,6 +1065,7 @@ int run_tgemm(const char* what, TgShape sh, const TgOperand& a, const TgOperand&
   const int kps = cdiv(nkb, splits) * TG_BK;
   splits = cdiv(K, kps);
   TgParams<EP> prm;
+  prm.epi_direct = g_epi_direct;
   prm.a = a;
   prm.b = b;
   prm.ep = ep;

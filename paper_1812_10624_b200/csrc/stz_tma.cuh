@@ -61,6 +61,7 @@ struct alignas(64) TgParams {
   int* sem;
   int M, N, K, k_per_split;
   int debug;  // bench/diagnostics only: 1 skip epilogue stores, 2 skip MMAs, 4 skip TMA loads
+  int epi_direct;   // split-plane epilogue: 256-bit per-row stores instead of smem staging
 };
 
 constexpr int TG_BM = 128, TG_BK = 32;
@@ -534,6 +535,16 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
             for (int jj = 0; jj < 8; ++jj) v[hh][jj] = __fadd_rn(v[hh][jj], bb[hh][jj]);
         }
         if constexpr (EP::STAGED) {
+          if (p.epi_direct) {   // each lane: its row's 16 columns, one 256-bit store per plane
+            float v16[16];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              v16[jj] = v[0][jj];
+              v16[8 + jj] = v[1][jj];
+            }
+            p.ep.store16_nb(m, n0 + c, v16);
+            continue;
+          }
           // split planes of 32 rows x 16 columns through shared memory: each
           // lane writes its row's two 16-byte chunks per plane (slot XOR row
           // bit 2: conflict-free), then two lanes store one row's 32
