@@ -757,6 +757,14 @@ const int g_band_b3 = [] {
   const char* e = getenv("STZ_BAND_B3");
   return e && *e == '0' ? 0 : 1;
 }();
+// thin outputs (O <= 64): one 128-row tile per work item with the 4-MMA thin
+// schedule (weight planes b0 | b1 as one 128-wide operand, three
+// accumulators, two TMEM sets) instead of two tiles on the 6-MMA schedule
+// (STZ_BAND_THIN=1)
+const int g_band_thin = [] {
+  const char* e = getenv("STZ_BAND_THIN");
+  return e && *e == '1' ? 1 : 0;
+}();
 // stacked band as exactly the raster rows a tile reads: 1 always, 0 only when
 // whole padded rows do not fit (STZ_BAND_EXACT)
 const int g_band_exact = [] {
@@ -764,16 +772,16 @@ const int g_band_exact = [] {
   return e && *e == '1' ? 1 : 0;
 }();
 
-template <int BN, int MT, class EP>
+template <int BN, int MT, bool THIN = false, class EP>
 int launch_band(BandParams<EP>& prm, int items, size_t smem, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(bandconv_kernel<BN, MT, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
+    cudaFuncSetAttribute(bandconv_kernel<BN, MT, EP, THIN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   const int grid = items < num_sms() ? items : num_sms();
-  bandconv_kernel<BN, MT, EP><<<grid, BD_THREADS, smem, st>>>(prm);
+  bandconv_kernel<BN, MT, EP, THIN><<<grid, BD_THREADS, smem, st>>>(prm);
   return STZ_OK;
 }
 
@@ -829,7 +837,7 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
       s2.junk *= (double)vrows / (Nimg * OH);
       s1.junk *= (double)vrows / (Nimg * OH);
     }
-    sh = s2.junk <= s1.junk * 1.05 ? s2 : s1;
+    sh = s2.junk <= s1.junk * 1.05 && !g_band_thin ? s2 : s1;
     if (sh.junk > 1.35) return -1;
   } else {
     sh = band_shape(O % 192 == 0 ? 192 : 128, 1, Nimg, vrows, OW, Wp, k);
@@ -837,6 +845,7 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
     if (sh.junk > 1.12) return -1;   // wide tiles are near MMA-bound: junk costs directly
   }
   auto smem_of = [&](const BandShape& b, int rows) -> size_t {
+    if (b.BN == 64 && b.MT == 1 && g_band_thin) return band_smem<64, 1, true>(rows);
     if (b.BN == 64) return b.MT == 2 ? band_smem<64, 2>(rows) : band_smem<64, 1>(rows);
     if (b.BN == 192) return band_smem<192, 1>(rows);
     return band_smem<128, 1>(rows);
@@ -922,6 +931,7 @@ int run_band_conv(const char* what, const bf16_t* x, size_t psx, const bf16_t* w
             what, Nimg, OH, OW, Wp, k, pad, C8, O, sh.BN, sh.MT, sh.tiles, sh.Hb, exact, nbx,
             brows, sh.junk, splits, items, smem);
   if (sh.BN == 64 && sh.MT == 2) launch_band<64, 2>(prm, items, smem, st);
+  else if (sh.BN == 64 && g_band_thin) launch_band<64, 1, true>(prm, items, smem, st);
   else if (sh.BN == 64) launch_band<64, 1>(prm, items, smem, st);
   else if (sh.BN == 192) launch_band<192, 1>(prm, items, smem, st);
   else launch_band<128, 1>(prm, items, smem, st);
@@ -990,6 +1000,7 @@ int run_band_wgrad(const bf16_t* x, size_t psx, const bf16_t* g, size_t psg,
   prm.splits = splits;
   prm.rows_total = rows_total;
   prm.d_oh = FastDiv((uint32_t)OH);
+  prm.debug = g_debug;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bandwgrad_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,

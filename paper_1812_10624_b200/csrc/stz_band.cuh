@@ -68,17 +68,18 @@ struct alignas(64) BandParams {
 
 constexpr int BD_THREADS = 256;
 
-template <int BN, int MT>
+template <int BN, int MT, bool THIN_ = false>
 struct BandCfg {
   static constexpr int B_PLANE = BN * TG_BK * 2;          // one plane of a B tile
   static constexpr int B_STAGE = 3 * B_PLANE;
-  static constexpr int STAGES = (BN <= 64 && MT == 2) ? 4 : 3;
+  static constexpr int STAGES = (BN <= 64 && (MT == 2 || THIN_)) ? 4 : 3;
   // thin tiles: the 4-MMA schedule of stz_tma.cuh -- weight planes b0 | b1
   // (contiguous) as one 128-wide operand; accumulators big | S1 | S2.  Off:
   // with MT = 2 its 384 columns leave one TMEM set, and the serialised
   // epilogue cost more than the saved MMAs (conv1 forward 0.232 -> 0.287 ms,
-  // measured); with MT = 1 the weight tile per 128 rows makes it feed-bound.
-  static constexpr bool THIN = false;
+  // measured); with MT = 1 the weight tile per 128 rows doubles the weight
+  // feed (STZ_BAND_THIN=1 selects MT = 1 with the thin schedule).
+  static constexpr bool THIN = THIN_;
   static constexpr int ACC_COLS = THIN ? 3 * BN : 2 * BN;
   static constexpr int SET_COLS = MT * ACC_COLS;
   static constexpr int NSETS = 2 * SET_COLS <= 512 ? 2 : 1;
@@ -96,9 +97,9 @@ __host__ __device__ inline int band_region(int rows_alloc) {
   return (2 * band_bytes(rows_alloc) + 1023) / 1024 * 1024;
 }
 
-template <int BN, int MT>
+template <int BN, int MT, bool THIN = false>
 __host__ inline int band_smem(int rows_alloc) {
-  using Cfg = BandCfg<BN, MT>;
+  using Cfg = BandCfg<BN, MT, THIN>;
   return 1024 + band_region(rows_alloc) + Cfg::STAGES * Cfg::B_STAGE + 512;
 }
 
@@ -112,10 +113,10 @@ __device__ __forceinline__ uint64_t umma_desc_none(uint32_t saddr, uint32_t lbo,
   return d;
 }
 
-template <int BN, int MT, class EP>
+template <int BN, int MT, class EP, bool THIN = false>
 __global__ void __launch_bounds__(BD_THREADS, 1)
     bandconv_kernel(const __grid_constant__ BandParams<EP> p) {
-  using Cfg = BandCfg<BN, MT>;
+  using Cfg = BandCfg<BN, MT, THIN>;
   constexpr int STAGES = Cfg::STAGES, NSETS = Cfg::NSETS;
   constexpr int TM = MT * TG_BM;   // virtual rows per work item
   extern __shared__ uint8_t smem_raw[];

@@ -46,6 +46,7 @@ struct alignas(64) BandWParams {
   int splits, rows_total;   // N * OH output raster rows
   int nst;                  // pipeline stages (2..BW_STAGES: wide rows fit fewer)
   FastDiv d_oh;
+  int debug;  // diagnostics only (stz_set_debug): 1 skip partial stores, 2 skip MMAs, 4 skip TMA
 };
 
 constexpr int BW_THREADS = 256;
@@ -121,6 +122,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
       for (int j = j0; j < j1; ++j, ++gs) {
         const int s = gs % NST;
         mbar_wait(&empty[s], ((gs / NST) & 1) ^ 1);
+        if (p.debug & 4) {
+          if (lane == 0) mbar_arrive(&full[s]);
+          __syncwarp();
+          continue;
+        }
         if (lane == 0) mbar_arrive_tx(&full[s], tx);
         __syncwarp();
         uint32_t n, y;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
         tc_fence_after();
         const uint32_t st = base + s * STG;
         const uint32_t b0 = st + 3 * XP;
-        for (int kq = 0; kq < ksteps; ++kq) {
+        for (int kq = 0; kq < ksteps && !(p.debug & 2); ++kq) {
           const uint32_t acc = (j == j0 && kq == 0) ? 0u : 1u;
           const uint64_t db0 = umma_desc_sw128(b0 + kq * 2048, GP, 1024);          // [b0|b1]
           const uint64_t db2 = umma_desc_sw128(b0 + 2 * GP + kq * 2048, GP, 1024);  // b2
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) bandwgrad_kernel(const __grid_c
           tmem_ld16(tb + 64 + (uint32_t)c, b);
           tmem_ld16(tb + 128 + (uint32_t)c, d);
           tmem_ld_wait();
-          if (!valid || m >= mrows) continue;
+          if (!valid || m >= mrows || (p.debug & 1)) continue;
           float4* dst = reinterpret_cast<float4*>(p.partial + ((size_t)z * mrows + m) * 64 + c);
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
