@@ -2022,6 +2022,12 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
   return check_launch("maxpool_fwd");
 }
 
+// row-tiled max-pool backward (maxpool_bwd_tiled_kernel); STZ_POOL_TILED=0: untiled
+const int g_pool_tiled = [] {
+  const char* e = getenv("STZ_POOL_TILED");
+  return e && *e == '0' ? 0 : 1;
+}();
+
 int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, size_t psx,
                      const void* mask, int N, int C, int C8, int H, int W, int k, int s,
                      int flat_ld, void* stream) {
@@ -2041,6 +2047,25 @@ int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, s
     maxpool_bwd_flat_kernel<<<N, 512, flat_smem, st>>>(cb(gy), psg, arg, mb(gx), psx, cb(mask), C,
                                                         C8, H, W, k, s, OH, OW, flat_ld);
     return check_launch("maxpool_bwd_flat");
+  }
+  // row-tiled form: each tile's gradient windows joined once into shared
+  // memory; TOH output rows per tile, their windows (+ the row above when
+  // windows overlap) within 48 KB
+  const size_t row_smem = (size_t)OW * C8 * (sizeof(float) + 1);
+  const int halo = k > s ? 1 : 0;
+  const int toh = std::min(OH, (int)(48 * 1024 / row_smem) - halo);
+  if (flat_ld == 0 && g_pool_tiled && s == 2 && (k == 3 || k == 2) && toh >= 1) {
+    const int tiles = cdiv(OH, toh);
+    const size_t sm = (size_t)(toh + halo) * row_smem;
+    if (k == 3)
+      maxpool_bwd_tiled_kernel<3, 2><<<N * tiles, 256, sm, st>>>(
+          cb(gy), psg, arg, mb(gx), psx, cb(mask), C, C8, H, W, OH, OW, toh, FastDiv(C8 / 8),
+          FastDiv(OW), FastDiv(W));
+    else
+      maxpool_bwd_tiled_kernel<2, 2><<<N * tiles, 256, sm, st>>>(
+          cb(gy), psg, arg, mb(gx), psx, cb(mask), C, C8, H, W, OH, OW, toh, FastDiv(C8 / 8),
+          FastDiv(OW), FastDiv(W));
+    return check_launch("maxpool_bwd_tiled");
   }
   if (flat_ld == 0 && k == 3 && s == 2) {
     maxpool_bwd_nhwc_kernel<3, 2><<<grid_for(total), 256, 0, st>>>(

@@ -491,6 +491,94 @@ __global__ void maxpool_bwd_nhwc_kernel(const bf16_t* __restrict__ gy, size_t ps
   }
 }
 
+// Row-tiled form of maxpool_bwd_nhwc_kernel (same values, same summation
+// order, so bit-identical): one block per (image, TOH output rows).  The
+// gradient windows the tile's input rows read -- output rows [oh_lo, oh_hi]
+// -- are joined from their three bf16 planes into fp32 ONCE, into shared
+// memory with their argmax bytes; the per-input-pixel gather then reads
+// shared memory.  The untiled kernel re-joined every window for each of the
+// up to R*R input pixels that read it (K = 3, S = 2: 4 candidate windows per
+// pixel), which made it instruction-bound (profiles/r02/op/pool2_bwd_*:
+// 68% issue slots busy at 0.25 of HBM).  Input rows [S*oh0, S*(oh0+TOH)) of
+// the tile, the last tile through H (rows past every window get zero).
+template <int K, int S>
+__global__ void __launch_bounds__(256) maxpool_bwd_tiled_kernel(
+    const bf16_t* __restrict__ gy, size_t psg, const uint8_t* __restrict__ arg,
+    bf16_t* __restrict__ gx, size_t psx, const bf16_t* __restrict__ mask, int C, int C8, int H,
+    int W, int OH, int OW, int TOH, FastDiv d_ch, FastDiv d_ow, FastDiv d_w) {
+  constexpr int R = (K + S - 1) / S;
+  extern __shared__ float4 pool_smem4[];
+  const int tiles = (OH + TOH - 1) / TOH;
+  const int n = blockIdx.x / tiles, tt = blockIdx.x - n * tiles;
+  const int oh0 = tt * TOH;
+  const int h_lo = S * oh0, h_hi = tt == tiles - 1 ? H : min(H, S * (oh0 + TOH));
+  // windows covering rows [h_lo, h_hi): oh*S <= h <= oh*S + K - 1
+  const int w_lo = max(0, (h_lo - K + S) / S), w_hi = min(OH - 1, (h_hi - 1) / S);
+  const int nrows = w_hi - w_lo + 1;
+  const int rowc = OW * C8;                       // values per window row
+  float* gs = reinterpret_cast<float*>(pool_smem4);
+  uint8_t* as = reinterpret_cast<uint8_t*>(gs + (size_t)nrows * rowc);
+  const int groups = nrows * OW * (C8 / 8);
+  for (int i = threadIdx.x; i < groups; i += blockDim.x) {
+    uint32_t rw, cc, r, ow;
+    d_ch.divmod((uint32_t)i, rw, cc);
+    d_ow.divmod(rw, r, ow);
+    const size_t o = (((size_t)n * OH + w_lo + r) * OW + ow) * C8 + cc * 8;
+    float g[8];
+    load_split8(gy + o, psg, g);
+    const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o));
+    float4* d = reinterpret_cast<float4*>(gs + (size_t)i * 8);
+    d[0] = make_float4(g[0], g[1], g[2], g[3]);
+    d[1] = make_float4(g[4], g[5], g[6], g[7]);
+    *reinterpret_cast<uint2*>(as + (size_t)i * 8) = a;
+  }
+  __syncthreads();
+  const int pix_groups = (h_hi - h_lo) * W * (C8 / 8);
+  for (int i = threadIdx.x; i < pix_groups; i += blockDim.x) {
+    uint32_t pr, cc, hr, w;
+    d_ch.divmod((uint32_t)i, pr, cc);
+    d_w.divmod(pr, hr, w);
+    const int h = h_lo + (int)hr;
+    const size_t xi = (((size_t)n * H + h) * W + w) * C8 + cc * 8;
+    uint4 mk = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (mask) mk = __ldg(reinterpret_cast<const uint4*>(mask + xi));
+    const int oh_hi = min(OH - 1, h / S), ow_hi = min(OW - 1, (int)w / S);
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        const int oh = oh_hi - a, ow = ow_hi - b;
+        if (oh < 0 || ow < 0 || h - oh * S >= K || (int)w - ow * S >= K) continue;
+        const size_t si = ((size_t)(oh - w_lo) * OW + ow) * C8 + cc * 8;
+        const uint2 ar = *reinterpret_cast<const uint2*>(as + si);
+        const uint32_t want = (uint32_t)((h - oh * S) * K + ((int)w - ow * S));
+        const uint32_t rep = want * 0x01010101u;
+        const uint32_t m0 = __vcmpeq4(ar.x, rep), m1 = __vcmpeq4(ar.y, rep);
+        if ((m0 | m1) == 0u) continue;
+        const float4 g0 = *reinterpret_cast<const float4*>(gs + si);
+        const float4 g1 = *reinterpret_cast<const float4*>(gs + si + 4);
+        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t mj = ((j < 4 ? m0 : m1) >> (8 * (j & 3))) & 1u;
+          if (mj) acc[j] += (double)gv[j];
+        }
+      }
+    const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t hb = (mw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;   // bf16 > 0
+      const bool keep = !mask || (hb != 0u && hb < 0x8000u);
+      v[j] = ((int)(cc * 8 + j) < C && keep) ? (float)acc[j] : 0.f;
+    }
+    store_split8(gx + xi, psx, v);
+  }
+}
+
 // forward into the CHW-flat FC boundary, one block per image: windows are
 // scanned NHWC (coalesced, 8 channels per thread), the maxima land in shared
 // memory in flat (c, oh, ow) order and leave as coalesced 8-element rows; the

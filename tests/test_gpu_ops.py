@@ -205,7 +205,8 @@ def _fc_case(tc, shape):
 
 
 @pytest.mark.parametrize("k,s,shape", [(3, 2, (4, 64, 55, 55)), (2, 2, (2, 8, 16, 16)),
-                                       (3, 2, (2, 256, 13, 13))])
+                                       (3, 2, (2, 256, 13, 13)), (3, 2, (2, 16, 56, 57)),
+                                       (2, 2, (3, 8, 17, 15)), (3, 2, (2, 192, 27, 27))])
 def test_maxpool_vs_oracle_bit_exact(tc, k, s, shape):
     rng = np.random.Generator(np.random.PCG64(k * 100 + shape[1]))
     x = rng.standard_normal(shape).astype(np.float32)
