@@ -1989,6 +1989,12 @@ int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* g
   return colsum_split(cb(g), psg, M, out_dim, out8, gb, ws, ws_bytes, st, accumulate);
 }
 
+// row-tiled max-pool forward / backward (maxpool_*_tiled_kernel); STZ_POOL_TILED=0: untiled
+const int g_pool_tiled = [] {
+  const char* e = getenv("STZ_POOL_TILED");
+  return e && *e == '0' ? 0 : 1;
+}();
+
 int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
                      int C8, int H, int W, int k, int s, int flat_ld, void* stream) {
   const int OH = (H - k) / s + 1, OW = (W - k) / s + 1;
@@ -2009,6 +2015,25 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
                                                         k, s, OH, OW, flat_ld);
     return check_launch("maxpool_fwd_flat");
   }
+  // row-tiled NHWC form: the input rows of TOH output rows (+ k - s halo)
+  // joined once into <= 96 KB of shared memory
+  const long in_row = (long)W * C8 * (long)sizeof(float);
+  const long tohf = k >= s ? (96L * 1024 / in_row - (k - s)) / s : 0;
+  if (flat_ld == 0 && g_pool_tiled && k >= s && tohf >= 1) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(maxpool_fwd_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024);
+      attr = true;
+    }
+    const int toh = (int)std::min((long)OH, tohf);
+    const int tiles = cdiv(OH, toh);
+    const size_t sm = (size_t)((toh - 1) * s + k) * (size_t)in_row;
+    maxpool_fwd_tiled_kernel<<<N * tiles, 256, sm, st>>>(
+        cb(x), psx, mb(y), psy, arg, C, C8, H, W, k, s, OH, OW, toh, FastDiv(C8 / 8),
+        FastDiv(W), FastDiv(OW));
+    return check_launch("maxpool_fwd_tiled");
+  }
   if (flat_ld > C * OH * OW) {
     zero_flat_tail_kernel<<<grid_for((size_t)N * (flat_ld - C * OH * OW)), 256, 0, st>>>(
         mb(y), psy, N, C * OH * OW, flat_ld);
@@ -2021,12 +2046,6 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
                                                              FastDiv(OH));
   return check_launch("maxpool_fwd");
 }
-
-// row-tiled max-pool backward (maxpool_bwd_tiled_kernel); STZ_POOL_TILED=0: untiled
-const int g_pool_tiled = [] {
-  const char* e = getenv("STZ_POOL_TILED");
-  return e && *e == '0' ? 0 : 1;
-}();
 
 int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, size_t psx,
                      const void* mask, int N, int C, int C8, int H, int W, int k, int s,

@@ -353,6 +353,79 @@ __global__ void maxpool_fwd_split_kernel(const bf16_t* __restrict__ x, size_t ps
   }
 }
 
+// Row-tiled form of maxpool_fwd_split_kernel for NHWC outputs (same
+// comparisons in the same order, so bit-identical): one block per (image,
+// TOH output rows).  The input rows the tile's windows read are joined from
+// their three bf16 planes into fp32 shared memory once -- the untiled kernel
+// joined each input pixel once per window reading it (9 joins per output at
+// 3x3/2 against (2 TOH + 1) W / (TOH OW) here).
+__global__ void __launch_bounds__(256) maxpool_fwd_tiled_kernel(
+    const bf16_t* __restrict__ x, size_t psx, bf16_t* __restrict__ y, size_t psy,
+    uint8_t* __restrict__ arg, int C, int C8, int H, int W, int k, int s, int OH, int OW,
+    int TOH, FastDiv d_ch, FastDiv d_w, FastDiv d_ow) {
+  extern __shared__ float4 poolf_smem4[];
+  float* xs = reinterpret_cast<float*>(poolf_smem4);
+  const int tiles = (OH + TOH - 1) / TOH;
+  const int n = blockIdx.x / tiles, tt = blockIdx.x - n * tiles;
+  const int oh0 = tt * TOH, oh1 = min(OH, oh0 + TOH);
+  const int h0 = oh0 * s, h1 = min(H, (oh1 - 1) * s + k);
+  const int groups = (h1 - h0) * W * (C8 / 8);
+  for (int i = threadIdx.x; i < groups; i += blockDim.x) {
+    uint32_t pr, cc, r, w;
+    d_ch.divmod((uint32_t)i, pr, cc);
+    d_w.divmod(pr, r, w);
+    float v[8];
+    load_split8(x + (((size_t)n * H + h0 + r) * W + w) * C8 + cc * 8, psx, v);
+    float4* d = reinterpret_cast<float4*>(xs + (size_t)i * 8);
+    d[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+  __syncthreads();
+  const int outs = (oh1 - oh0) * OW * (C8 / 8);
+  for (int i = threadIdx.x; i < outs; i += blockDim.x) {
+    uint32_t pr, cc, r, ow;
+    d_ch.divmod((uint32_t)i, pr, cc);
+    d_ow.divmod(pr, r, ow);
+    const int oh = oh0 + (int)r;
+    const float* b0 = xs + (((size_t)(oh * s - h0) * W + ow * s) * C8 + cc * 8);
+    float best[8];
+    int bi[8];
+    {
+      const float4 p0 = *reinterpret_cast<const float4*>(b0);
+      const float4 p1 = *reinterpret_cast<const float4*>(b0 + 4);
+      best[0] = p0.x; best[1] = p0.y; best[2] = p0.z; best[3] = p0.w;
+      best[4] = p1.x; best[5] = p1.y; best[6] = p1.z; best[7] = p1.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bi[j] = 0;
+    for (int kh = 0; kh < k; ++kh)
+      for (int kw = 0; kw < k; ++kw) {
+        if ((kh | kw) == 0) continue;
+        const float* q = b0 + ((size_t)kh * W + kw) * C8;
+        const float4 p0 = *reinterpret_cast<const float4*>(q);
+        const float4 p1 = *reinterpret_cast<const float4*>(q + 4);
+        const float v[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v[j] > best[j]) {
+            best[j] = v[j];
+            bi[j] = kh * k + kw;
+          }
+      }
+    const size_t o = (((size_t)n * OH + oh) * OW + ow) * C8 + cc * 8;
+    uint2 packed;
+    packed.x = (uint32_t)bi[0] | ((uint32_t)bi[1] << 8) | ((uint32_t)bi[2] << 16) |
+               ((uint32_t)bi[3] << 24);
+    packed.y = (uint32_t)bi[4] | ((uint32_t)bi[5] << 8) | ((uint32_t)bi[6] << 16) |
+               ((uint32_t)bi[7] << 24);
+    *reinterpret_cast<uint2*>(arg + o) = packed;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if ((int)(cc * 8 + j) >= C) best[j] = 0.f;
+    store_split8(y + o, psy, best);
+  }
+}
+
 // zero the CHW-flat tail columns [C*OH*OW, flat_ld) once per buffer
 __global__ void zero_flat_tail_kernel(bf16_t* __restrict__ y, size_t psy, int N, int D, int ld) {
   const int tail = ld - D;
