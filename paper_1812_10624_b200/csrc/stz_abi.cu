@@ -1989,10 +1989,17 @@ int stzx_fc_wgrad(const void* x, size_t psx, const void* g, size_t psg, float* g
   return colsum_split(cb(g), psg, M, out_dim, out8, gb, ws, ws_bytes, st, accumulate);
 }
 
-// row-tiled max-pool forward / backward (maxpool_*_tiled_kernel); STZ_POOL_TILED=0: untiled
+// row-tiled max-pool backward (maxpool_bwd_tiled_kernel; STZ_POOL_TILED=0:
+// untiled) and forward (maxpool_fwd_tiled_kernel, STZ_POOL_FWD_TILED=1:
+// measured slower than the untiled forward -- pool2 0.0556 vs 0.0439 ms --
+// whose 9 loads per output hit L1, so it stays off)
 const int g_pool_tiled = [] {
   const char* e = getenv("STZ_POOL_TILED");
   return e && *e == '0' ? 0 : 1;
+}();
+const int g_pool_fwd_tiled = [] {
+  const char* e = getenv("STZ_POOL_FWD_TILED");
+  return e && *e == '1' ? 1 : 0;
 }();
 
 int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* arg, int N, int C,
@@ -2019,7 +2026,7 @@ int stzx_maxpool_fwd(const void* x, size_t psx, void* y, size_t psy, uint8_t* ar
   // joined once into <= 96 KB of shared memory
   const long in_row = (long)W * C8 * (long)sizeof(float);
   const long tohf = k >= s ? (96L * 1024 / in_row - (k - s)) / s : 0;
-  if (flat_ld == 0 && g_pool_tiled && k >= s && tohf >= 1) {
+  if (flat_ld == 0 && g_pool_fwd_tiled && k >= s && tohf >= 1) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(maxpool_fwd_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
