@@ -204,11 +204,19 @@ def _sync_check(name: str) -> int:
 TILE_TABLE: dict = {}
 
 _TILE_CANDIDATES = ((64, 1), (96, 1), (128, 1), (192, 1), (128, 2), (192, 2), (256, 2))
+# split-K counts tried per tile with STZ_AUTOTUNE_SPLITS=1 (0: the cost
+# model's count for that tile; counts under the accumulation cap are raised
+# to it by the library).  Off by default: the isolated-call wins did not
+# carry into the step (AlexNet 36,953 vs 37,084, ResNet-50 2,495 vs 2,483
+# images/s, profiles/r02/autotune_splits/)
+_SPLIT_CANDIDATES = (0, 2, 4, 8, 16, 32, 64, 148) \
+    if os.environ.get("STZ_AUTOTUNE_SPLITS", "0") == "1" else (0,)
 
 
 def autotune_tiles(run_step, reps: int = 5, gain: float = 0.97) -> dict:
-    """Time every GEMM call of one step under each tile shape and keep the
-    measured winner where it beats the cost model's pick by > 3%.
+    """Time every GEMM call of one step under each tile shape and split-K
+    count and keep the measured winner (BN, CL, splits) where it beats the
+    cost model's pick by > 3%.
 
     ``run_step()`` runs one EAGER step (no graph replay: replays bypass this
     module and record nothing); its GEMM calls (every call carrying
@@ -216,8 +224,10 @@ def autotune_tiles(run_step, reps: int = 5, gain: float = 0.97) -> dict:
     CUDA events on the stream each call was launched on -- like a
     convolution autotuner, the replays overwrite that step's outputs, so run
     it before real training steps (or before the warm-up).  A forced tile
-    keeps the accumulation cap per work item but the library
-    re-derives the split count for the new width.  Returns and installs the
+    keeps the accumulation cap per work item; splits = 0
+    lets the library derive the split count for the forced width (the fp32
+    summation order of the split-K partials follows the split count, within
+    the GEMM tolerance of DESIGN.md 3.2).  Returns and installs the
     table; when the step recorded no GEMM the installed table is left
     unchanged."""
     global PROFILE_HOOK
@@ -266,11 +276,15 @@ def autotune_tiles(run_step, reps: int = 5, gain: float = 0.97) -> dict:
             continue
         best, best_ms = None, base * gain
         for bn, cl in _TILE_CANDIDATES:
-            if lib.stz_set_tile(bn, cl, 0) != 0:
-                continue
-            ms = timed(name, args)
-            if ms is not None and ms < best_ms:
-                best, best_ms = (bn, cl), ms
+            for sp in _SPLIT_CANDIDATES:
+                if lib.stz_set_tile(bn, cl, sp) != 0:
+                    break
+                try:
+                    ms = timed(name, args)
+                except Exception:   # e.g. the call's workspace is too small for sp
+                    ms = None
+                if ms is not None and ms < best_ms:
+                    best, best_ms = (bn, cl, sp), ms
         lib.stz_set_tile(0, 0, 0)
         if best is not None:
             table[key] = best
@@ -287,7 +301,7 @@ def call(name: str, *args, flops: float = 0.0, tag: str | None = None,
     lib = load()
     tile = TILE_TABLE.get((name, tag, flops)) if TILE_TABLE else None
     if tile is not None:
-        lib.stz_set_tile(tile[0], tile[1], 0)
+        lib.stz_set_tile(tile[0], tile[1], tile[2] if len(tile) > 2 else 0)
     try:
         if PROFILE_HOOK is not None:
             with PROFILE_HOOK(name, args, flops, tag, nbytes=nbytes):

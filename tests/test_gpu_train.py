@@ -242,8 +242,9 @@ def test_autotune_tiles_installs_valid_table(lib):
     try:
         table = _lib.autotune_tiles(lambda: cl.train(1), reps=2)
         assert table is not _lib.TILE_TABLE and table == _lib.TILE_TABLE
-        for (name, tag, flops), (bn, c) in table.items():
-            assert flops > 0 and (bn, c) in _lib._TILE_CANDIDATES
+        for (name, tag, flops), t in table.items():
+            assert flops > 0 and (t[0], t[1]) in _lib._TILE_CANDIDATES
+            assert len(t) == 2 or t[2] in _lib._SPLIT_CANDIDATES
         cl.train(1)   # runs under the installed overrides
     finally:
         _lib.TILE_TABLE.clear()
