@@ -219,6 +219,24 @@ def test_maxpool_vs_oracle_bit_exact(tc, k, s, shape):
     np.testing.assert_array_equal(host(gx), rgx)
 
 
+@pytest.mark.parametrize("shape", [(2, 64, 55, 55), (2, 24, 27, 27)])
+def test_maxpool_backward_shared_maxima_bit_exact(tc, shape):
+    """3x3/2 pooling with a spike on every (even, even) pixel: each spike is
+    the argmax of up to four overlapping windows, so most gradient cells sum
+    three or four contributions (the float64 re-sum of the tiled kernel)."""
+    rng = np.random.Generator(np.random.PCG64(shape[1] * 7 + shape[2]))
+    x = rng.standard_normal(shape).astype(np.float32)
+    x[:, :, ::2, ::2] += 8.0
+    ry, arg = orc.maxpool_forward(x, 3, 2)
+    gy = (rng.standard_normal(ry.shape) * np.exp2(rng.integers(-30, 30, ry.shape))).astype(
+        np.float32)
+    rgx = orc.maxpool_backward(arg, x.shape, gy, 3, 2)
+    y, cache = tc.forward(tc.MaxPool2d(3, 2), [], dev(x))
+    np.testing.assert_array_equal(host(y), ry)
+    gx, _ = tc.backward(tc.MaxPool2d(3, 2), [], cache, dev(gy))
+    np.testing.assert_array_equal(host(gx), rgx)
+
+
 TILE_CONFIGS = [(64, 1, 1), (96, 1, 1), (128, 1, 1), (192, 1, 1), (128, 2, 1), (192, 2, 1),
                 (256, 2, 1), (64, 1, 3), (128, 2, 4), (192, 1, 2), (256, 2, 5)]
 
