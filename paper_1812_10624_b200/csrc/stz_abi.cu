@@ -2077,18 +2077,38 @@ int stzx_maxpool_bwd(const void* gy, size_t psg, const uint8_t* arg, void* gx, s
   // row-tiled form: each tile's gradient windows joined once into shared
   // memory; TOH output rows per tile, their windows (+ the row above when
   // windows overlap) within 48 KB
+  // shared-memory budget per block / block size (STZ_POOL_KB,
+  // STZ_POOL_THREADS): 48 KB x 512 threads measured best over 24-160 KB x
+  // 128-512 on AlexNet's pool2 + pool5 (0.121 ms against 0.124 at 256
+  // threads; profiles/r02/pool_tiled/pool_sweep.log)
+  static const int pool_kb = [] {
+    const char* e = getenv("STZ_POOL_KB");
+    return e ? atoi(e) : 48;
+  }();
+  static const int pool_thr = [] {
+    const char* e = getenv("STZ_POOL_THREADS");
+    return e ? atoi(e) : 512;
+  }();
   const size_t row_smem = (size_t)OW * C8 * (sizeof(float) + 1);
   const int halo = k > s ? 1 : 0;
-  const int toh = std::min(OH, (int)(48 * 1024 / row_smem) - halo);
+  const int toh = std::min(OH, (int)((size_t)pool_kb * 1024 / row_smem) - halo);
   if (flat_ld == 0 && g_pool_tiled && s == 2 && (k == 3 || k == 2) && toh >= 1) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(maxpool_bwd_tiled_kernel<3, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(maxpool_bwd_tiled_kernel<2, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
     const int tiles = cdiv(OH, toh);
     const size_t sm = (size_t)(toh + halo) * row_smem;
     if (k == 3)
-      maxpool_bwd_tiled_kernel<3, 2><<<N * tiles, 256, sm, st>>>(
+      maxpool_bwd_tiled_kernel<3, 2><<<N * tiles, pool_thr, sm, st>>>(
           cb(gy), psg, arg, mb(gx), psx, cb(mask), C, C8, H, W, OH, OW, toh, FastDiv(C8 / 8),
           FastDiv(OW), FastDiv(W));
     else
-      maxpool_bwd_tiled_kernel<2, 2><<<N * tiles, 256, sm, st>>>(
+      maxpool_bwd_tiled_kernel<2, 2><<<N * tiles, pool_thr, sm, st>>>(
           cb(gy), psg, arg, mb(gx), psx, cb(mask), C, C8, H, W, OH, OW, toh, FastDiv(C8 / 8),
           FastDiv(OW), FastDiv(W));
     return check_launch("maxpool_bwd_tiled");

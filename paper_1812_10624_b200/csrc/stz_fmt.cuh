@@ -575,7 +575,7 @@ __global__ void maxpool_bwd_nhwc_kernel(const bf16_t* __restrict__ gy, size_t ps
 // 68% issue slots busy at 0.25 of HBM).  Input rows [S*oh0, S*(oh0+TOH)) of
 // the tile, the last tile through H (rows past every window get zero).
 template <int K, int S>
-__global__ void __launch_bounds__(256) maxpool_bwd_tiled_kernel(
+__global__ void __launch_bounds__(512) maxpool_bwd_tiled_kernel(
     const bf16_t* __restrict__ gy, size_t psg, const uint8_t* __restrict__ arg,
     bf16_t* __restrict__ gx, size_t psx, const bf16_t* __restrict__ mask, int C, int C8, int H,
     int W, int OH, int OW, int TOH, FastDiv d_ch, FastDiv d_ow, FastDiv d_w) {
