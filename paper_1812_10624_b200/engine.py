@@ -32,6 +32,7 @@ vectors; the residual add + ReLU is fused into the body's last BatchNorm.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -113,6 +114,7 @@ class _Op:
     flat_out: bool = False    # maxpool: writes the CHW-flat tensor for a following Flatten
     s2d: tuple | None = None  # first strided conv as space-to-depth: (ks, Cs8, Hs, Ws)
     bias_by_bn: bool = False  # conv: the following BatchNorm's backward sums its bias gradient
+    c8_in: int = 0            # conv: input channel stride when not rup8(in_ch) (first layer)
 
 
 class BlockEngine:
@@ -222,6 +224,13 @@ class BlockEngine:
                 # shifted-window weight gradient, 0.39 -> 0.28 ms, but its
                 # im2col forward then multiplies the padding: 0.23 -> 0.34 ms)
                 ops[0].s2d = (ks, cs8, oh - 1 + ks, ow - 1 + ks)
+            elif ops[0].kind == "conv" and l0.stride == 1 and rup8(l0.in_ch) < 32 \
+                    and os.environ.get("STZ_FIRST_C32", "1") != "0":
+                # a stride-1 first conv on few channels (VGG-16 conv1_1): its
+                # input is packed 32 channels wide (zeros past in_ch), so the
+                # forward and the weight gradient run on the TMA GEMM instead
+                # of the cp.async fallback that needs no 32-channel k-blocks
+                ops[0].c8_in = 32
         self.ops = ops
 
     def _layout_params(self):
@@ -307,7 +316,7 @@ class BlockEngine:
         for i, op in enumerate(self.ops):
             l = op.layer
             if op.kind == "conv":
-                kk, c8, o8 = l.kh * l.kw, rup8(l.in_ch), rup8(l.out_ch)
+                kk, c8, o8 = l.kh * l.kw, op.c8_in or rup8(l.in_ch), rup8(l.out_ch)
                 if op.s2d is not None:
                     ks, cs8, _, _ = op.s2d
                     kk, c8 = ks * ks, cs8
@@ -341,6 +350,7 @@ class BlockEngine:
         self.losses = None
         self.dlogits = None
         self.xin = None   # packed block input, allocated on first pack_input()
+        self.xin32 = None  # its 32-channel-wide copy for a first conv with c8_in
         self._gout = None  # per-op output-gradient buffers of the last backward
         self.bnstats: dict = {}   # bn op -> float64 [groups][C8][2] (mean, rstd)
         for i, op in enumerate(self.ops):
@@ -420,7 +430,7 @@ class BlockEngine:
             jobs.append((self.params[i][0].data_ptr(), a.data_ptr(),
                          0 if b is None else b.data_ptr(), a[0].numel(),
                          0 if b is None else b[0].numel(), l.out_ch, l.in_ch, l.kh, l.kw,
-                         rup8(l.in_ch), rup8(l.out_ch)))
+                         op.c8_in or rup8(l.in_ch), rup8(l.out_ch)))
         for kids in self.children.values():
             for k in kids:
                 if k is not None:
@@ -529,6 +539,9 @@ class BlockEngine:
                                        l0.in_ch * l0.stride ** 2, self.device)
             else:
                 self.xin = self._split_for(self.in_shape, self.batch)
+            if op0.c8_in:   # the forward's copy, 32 channels wide (the wgrad reads xin)
+                c, h, w = self.in_shape
+                self.xin32 = Split.alloc("nhwc", (self.batch, h, w, op0.c8_in), c, self.device)
         s = view(self.xin)
         xs = x[r0:r1]
         if op0.s2d is not None:
@@ -541,6 +554,11 @@ class BlockEngine:
             c, h, w = self.in_shape
             _lib.call("stzx_pack_nchw", ptr(xs), s.ptr(), s.ps, b, c, h, w, s.width, st,
                       tag=f"{self.tag}pack_nchw", nbytes=4.0 * b * c * h * w + 6.0 * b * s.row_elems)
+            if op0.c8_in:
+                s32 = view(self.xin32)
+                _lib.call("stzx_pack_nchw", ptr(xs), s32.ptr(), s32.ps, b, c, h, w, s32.width,
+                          st, tag=f"{self.tag}pack_nchw32",
+                          nbytes=4.0 * b * c * h * w + 6.0 * b * s32.row_elems)
         else:
             _lib.call("stzx_pack_rows", ptr(xs), s.ptr(), s.ps, b, self.in_shape[0],
                       s.width, st)
@@ -566,6 +584,11 @@ class BlockEngine:
         b = r1 - r0
         for i, op in enumerate(self.ops):
             xin = V(self._input(i))
+            if i == 0 and op.c8_in:
+                if self._x is not self.xin:
+                    raise ShapeMismatch("a block whose first conv reads a 32-wide input copy "
+                                        "takes fp32 batches (pack_input)")
+                xin = V(self.xin32)
             l = op.layer
             if op.kind == "conv":
                 c, h, w = op.in_shape
@@ -985,7 +1008,7 @@ class BlockEngine:
                       tag=f"{self.tag}conv{i}_sgd", nbytes=20.0 * cnt)
             _lib.call("stzx_pack_conv2_w", ptr(self.params[i][0]), ptr(wf), wf[0].numel(),
                       ptr(wd), 0 if wd is None else wd[0].numel(), l.out_ch, l.in_ch, l.kh,
-                      l.kw, rup8(l.in_ch), rup8(l.out_ch), st)
+                      l.kw, self.ops[i].c8_in or rup8(l.in_ch), rup8(l.out_ch), st)
         self._sgd_done.add(i)
 
     def fused_pack_ranges(self):
